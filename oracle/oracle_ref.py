@@ -1,0 +1,347 @@
+"""Float64 reference ("oracle") for the OpenTinker policy-gradient hot path — TEST INFRASTRUCTURE.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline / --impl reference) may use this
+module. It shares no code with the CUDA path (paper_2601_07376_b200/) and imports nothing from it.
+
+What it computes (PAPER.md = /root/reference/PAPER.md, SPEC.md = /root/reference/SPEC.md; the
+paper names no RL algorithm, so steps O2-O4 follow the readings listed in DESIGN.md §3):
+
+  O1 build_masks           PAPER.md:167-174 (§2.2 PENDING / GENERATING / INTERACTING token masking),
+                           PAPER.md:192 (§2.3 independent per-agent policies).
+  O2 episode_returns,      SPEC.md:95 (return = sum of per-turn scores, undiscounted)
+     group_advantages      (A_i = (R_i - mean)/(std if std > 1e-8 else 1)), BASELINE.json north_star (2).
+  O3 row_forward           north_star (3): log-softmax + gather + entropy over the vocabulary.
+  O4 row_loss_terms,       north_star (4): PPO-clipped surrogate + KL penalty, token-mean reduction,
+     policy_loss_fwd_bwd   dlogits = coef * (softmax - onehot); gradient pattern SPEC.md:323.
+  O5 shard_partials,       vocab-sharded forward (north_star "all-reduced row max/sum-exp"): per-shard
+     combine_partials      partials combined exactly (DESIGN.md §3 R25).
+
+Every step is the plain definition in float64: numpy vector ops per row (exp/log/max) and
+math.fsum (exactly rounded) for every sum; no blocking, fusion or reordering.
+
+Pins (tests/test_oracle_pins.py, -m "not gpu"): SPEC.md's ARITH worked example for O1, brute-force
+segment enumeration, closed-form binary-group advantages, constant-group zero, zero-sum
+antisymmetry, uniform / two-level / V=2 rows for O3, torch float64 log_softmax
+(library routine), old=new and clip closed forms, k3 values, central finite differences of the
+loss for the gradient, and the SFT case against torch float64 cross_entropy autograd.
+Parity unpinned: none of the functions; the CHOICE among readings R2, R14-R16 (std estimator,
+clip epsilon, ratio clamp, KL estimator) cannot be pinned to anything the paper prints.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+# Segment sources (§2.2 states; SPEC.md:31 SegmentSource + PAD, R12)
+CONTEXT, ACTION, OBSERVATION, PAD = 0, 1, 2, 3
+ANY_AGENT = -1
+
+KL_K1, KL_K2, KL_K3 = 1, 2, 3
+
+
+class OracleError(Exception):
+    code = "ERROR"
+
+
+class EmptyGroup(OracleError):        # SPEC.md:324 errors: EmptyGroup
+    code = "EMPTY_GROUP"
+
+
+class Unterminated(OracleError):      # SPEC.md:324 errors: UnterminatedTrajectory
+    code = "UNTERMINATED"
+
+
+class BadTrajectory(OracleError):     # SPEC.md:79-87 validate_trajectory; SPEC.md:91 partition
+    code = "BAD_TRAJECTORY"
+
+
+class TargetRange(OracleError):
+    code = "TARGET_RANGE"
+
+
+class GroupRange(OracleError):
+    code = "GROUP_RANGE"
+
+
+# --------------------------------------------------------------------------------------------
+# O1: loss / response masks
+# --------------------------------------------------------------------------------------------
+def build_masks(tok_offsets, seg_offsets, seg_source, seg_agent, seg_len, terminated=None,
+                train_agent: int = ANY_AGENT, traj_agent=None):
+    """Expand per-trajectory segment lists into per-row labels.
+
+    PENDING (CONTEXT) tokens are "excluded from loss computation"; only GENERATING
+    (ACTION) tokens are "trainable"; INTERACTING (OBSERVATION) tokens "are masked
+    from the loss". Agents do not share gradients, so an ACTION row
+    is trainable only for the agent that emitted it (train_agent, or traj_agent[b] per view).
+    response_mask: every non-PAD row after the turn-0 CONTEXT (prompt) segment (R13).
+    """
+    tok_offsets = np.asarray(tok_offsets, np.int64)
+    B = tok_offsets.shape[0] - 1
+    if B < 1:
+        raise EmptyGroup("no trajectories")
+    N = int(tok_offsets[B])
+    loss_mask = np.zeros(N, np.uint8)
+    response_mask = np.zeros(N, np.uint8)
+    row_traj = np.full(N, -1, np.int32)
+    traj_loss_tokens = np.zeros(B, np.int64)
+    traj_source_counts = np.zeros((B, 4), np.int64)
+    for b in range(B):
+        if terminated is not None and not terminated[b]:
+            raise Unterminated(f"trajectory {b} not terminated")
+        ta = int(traj_agent[b]) if traj_agent is not None else int(train_agent)
+        row = int(tok_offsets[b])
+        s0, s1 = int(seg_offsets[b]), int(seg_offsets[b + 1])
+        if s1 < s0:
+            raise BadTrajectory(f"trajectory {b}: segment offsets decrease")
+        for k in range(s0, s1):
+            src, L, ag = int(seg_source[k]), int(seg_len[k]), int(seg_agent[k])
+            if L <= 0 or src > PAD:
+                raise BadTrajectory(f"trajectory {b}: bad segment {k}")
+            trainable = src == ACTION and (ta == ANY_AGENT or ag == ta)
+            is_prompt = (k == s0) and src == CONTEXT
+            responding = (not is_prompt) and src != PAD
+            if row + L > int(tok_offsets[b + 1]):
+                raise BadTrajectory(f"trajectory {b}: segments exceed its rows")
+            loss_mask[row:row + L] = 1 if trainable else 0
+            response_mask[row:row + L] = 1 if responding else 0
+            row_traj[row:row + L] = b
+            traj_source_counts[b, src] += L
+            if trainable:
+                traj_loss_tokens[b] += L
+            row += L
+        if row != int(tok_offsets[b + 1]):
+            raise BadTrajectory(f"trajectory {b}: segment lengths != row count")
+    return dict(loss_mask=loss_mask, response_mask=response_mask, row_traj=row_traj,
+                traj_loss_tokens=traj_loss_tokens, traj_source_counts=traj_source_counts,
+                n_loss=int(traj_loss_tokens.sum()))
+
+
+# --------------------------------------------------------------------------------------------
+# O2: returns and group-relative advantages  (north_star (2))
+# --------------------------------------------------------------------------------------------
+def episode_returns(turn_offsets, turn_rewards):
+    """R_b = sum of the per-turn scores of trajectory b, undiscounted."""
+    B = len(turn_offsets) - 1
+    return np.array([math.fsum(turn_rewards[turn_offsets[b]:turn_offsets[b + 1]]) for b in range(B)],
+                    np.float64)
+
+
+def group_advantages(group_id, returns, num_groups: int, std_norm: bool = True, unbiased: bool = False,
+                     std_floor: float = 1e-8):
+    """A_b = (R_b - mean_g) / (std_g if std_g > std_floor else 1)   (R2-R4).
+
+    mean_g and std_g over the trajectories of b's group g; std is the population std unless
+    `unbiased` (then / (n_g - 1), and std_g = 0 when n_g <= 1). std_norm=False gives R_b - mean_g.
+    """
+    group_id = np.asarray(group_id)
+    returns = np.asarray(returns, np.float64)
+    B = returns.shape[0]
+    if B < 1:
+        raise EmptyGroup("no trajectories")
+    if np.any(group_id < 0) or np.any(group_id >= num_groups):
+        raise GroupRange("group id out of range")
+    mean = np.zeros(num_groups)
+    std = np.zeros(num_groups)
+    size = np.zeros(num_groups, np.int32)
+    for g in range(num_groups):
+        Rg = [float(returns[b]) for b in range(B) if group_id[b] == g]
+        n = len(Rg)
+        size[g] = n
+        if n == 0:
+            continue
+        mean[g] = math.fsum(Rg) / n
+        denom = (n - 1) if unbiased else n
+        if denom > 0:
+            std[g] = math.sqrt(math.fsum((r - mean[g]) ** 2 for r in Rg) / denom)
+    adv = np.zeros(B)
+    for b in range(B):
+        g = int(group_id[b])
+        centred = float(returns[b]) - mean[g]
+        if std_norm:
+            adv[b] = centred / (std[g] if std[g] > std_floor else 1.0)
+        else:
+            adv[b] = centred
+    return dict(adv=adv, group_mean=mean, group_std=std, group_size=size)
+
+
+# --------------------------------------------------------------------------------------------
+# O3: per-row log-softmax + gather + entropy  (north_star (3))
+# --------------------------------------------------------------------------------------------
+def row_forward(x, y: int, logit_scale: float = 1.0):
+    """z = s*x;  M = max z;  S = sum exp(z-M);  lse = M + ln S;  logp = z_y - lse;
+    H = ln S - sum exp(z-M)(z-M) / S   (terms with exp(z-M) == 0 contribute 0).
+    Returns (logp, H, lse, p) with p = exp(z - lse)."""
+    z = float(logit_scale) * np.asarray(x, np.float64)
+    V = z.shape[0]
+    if not (0 <= y < V):
+        raise TargetRange(f"target {y} outside [0, {V})")
+    M = float(np.max(z))
+    e = np.exp(z - M)
+    S = math.fsum(e)
+    lse = M + math.log(S)
+    logp = float(z[y]) - lse
+    nz = e > 0
+    H = math.log(S) - math.fsum(e[nz] * (z[nz] - M)) / S
+    p = np.exp(z - lse)
+    return logp, H, lse, p
+
+
+def logprob_entropy_fwd(logits, targets, row_mask=None, logit_scale: float = 1.0):
+    """Rows with row_mask == 0 are skipped and reported as 0 (R26)."""
+    logits = np.asarray(logits, np.float64)
+    N = logits.shape[0]
+    logp, H, lse = np.zeros(N), np.zeros(N), np.zeros(N)
+    for j in range(N):
+        if row_mask is not None and not row_mask[j]:
+            continue
+        logp[j], H[j], lse[j], _ = row_forward(logits[j], int(targets[j]), logit_scale)
+    return dict(logp=logp, entropy=H, lse=lse)
+
+
+# --------------------------------------------------------------------------------------------
+# O4: PPO-clip + KL surrogate, token-mean, fused backward  (north_star (4))
+# --------------------------------------------------------------------------------------------
+@dataclass
+class LossCfg:
+    clip_low: float = 0.2          # epsilon_low  (R14)
+    clip_high: float = 0.2         # epsilon_high
+    kl_beta: float = 0.04          # beta (R16); 0 => no KL term, ref unused
+    kl_type: int = KL_K3
+    log_ratio_clamp: float = 20.0  # C (R15)
+    logit_scale: float = 1.0       # s = 1/temperature (R19)
+
+
+def row_loss_terms(logp: float, old: float, ref: Optional[float], A: float, cfg: LossCfg):
+    """Per-token surrogate L = pg + beta*KL and its derivative G = dL/dlogp.
+
+    delta = clamp(logp - old, -C, C); r = exp(delta); rbar = min(max(r, 1-eps_lo), 1+eps_hi)
+    pg = max(-A*r, -A*rbar); clipped <=> (A>0 and r>1+eps_hi) or (A<0 and r<1-eps_lo)
+    dpg/dlogp = 0 if clipped or |logp-old| > C else -A*r
+    k3: d = clamp(ref - logp, -C, C); KL = exp(d) - d - 1; dKL/dlogp = 0 if |ref-logp| > C else 1 - exp(d)
+    k1: KL = logp - ref, dKL/dlogp = 1;   k2: KL = (logp-ref)^2/2, dKL/dlogp = logp - ref
+    Returns (L, G, clipped, KL).
+    """
+    C = cfg.log_ratio_clamp
+    draw = logp - old
+    delta = min(max(draw, -C), C)
+    r = math.exp(delta)
+    rbar = min(max(r, 1.0 - cfg.clip_low), 1.0 + cfg.clip_high)
+    pg = max(-A * r, -A * rbar)
+    clipped = (A > 0 and r > 1.0 + cfg.clip_high) or (A < 0 and r < 1.0 - cfg.clip_low)
+    G = 0.0 if (clipped or abs(draw) > C) else -A * r
+    kl = 0.0
+    if cfg.kl_beta != 0.0:
+        if cfg.kl_type == KL_K3:
+            dr = ref - logp
+            d = min(max(dr, -C), C)
+            kl = math.exp(d) - d - 1.0
+            Gk = 0.0 if abs(dr) > C else 1.0 - math.exp(d)
+        elif cfg.kl_type == KL_K1:
+            kl = logp - ref
+            Gk = 1.0
+        elif cfg.kl_type == KL_K2:
+            kl = 0.5 * (logp - ref) ** 2
+            Gk = logp - ref
+        else:
+            raise ValueError("kl_type")
+        G += cfg.kl_beta * Gk
+    L = pg + cfg.kl_beta * kl
+    return L, G, bool(clipped), kl
+
+
+def policy_loss_fwd_bwd(logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss: int,
+                        cfg: LossCfg = LossCfg(), zero_masked_rows: bool = True,
+                        rows: Optional[Sequence[int]] = None):
+    """loss = sum_j m_j L_j / N   (N = n_loss, the global loss-token count; 0 => loss 0, grads 0)
+    dlogits[j, v] = coef_j * (p_jv - [v == y_j]),  coef_j = -s * (m_j / N) * G_j.
+
+    `rows` restricts the per-row outputs to a subset (sampled parity at full size); the loss and
+    stats are then sums over that subset only. Rows with m_j == 0 get dlogits 0, logp 0, entropy 0.
+    """
+    logits_is_array = not callable(logits)
+    N_rows = len(targets)
+    rows = range(N_rows) if rows is None else rows
+    s = cfg.logit_scale
+    invN = (1.0 / n_loss) if n_loss > 0 else 0.0
+    out_dl, out_logp, out_H = {}, {}, {}
+    terms, klterms, Hterms = [], [], []
+    n_clipped = 0
+    n_tok = 0
+    for j in rows:
+        x = logits[j] if logits_is_array else logits(j)
+        m = int(loss_mask[j])
+        if not m:
+            out_dl[j] = np.zeros(len(x)) if zero_masked_rows else None
+            out_logp[j], out_H[j] = 0.0, 0.0
+            continue
+        y = int(targets[j])
+        logp, H, lse, p = row_forward(x, y, s)
+        A = float(adv[int(row_traj[j])])
+        ref = float(ref_logp[j]) if ref_logp is not None else None
+        L, G, clipped, kl = row_loss_terms(logp, float(old_logp[j]), ref, A, cfg)
+        coef = -s * invN * G
+        dl = coef * p
+        dl[y] = coef * (p[y] - 1.0)
+        out_dl[j], out_logp[j], out_H[j] = dl, logp, H
+        terms.append(L); klterms.append(kl); Hterms.append(H)
+        n_clipped += int(clipped)
+        n_tok += 1
+    loss = math.fsum(terms) * invN if n_loss > 0 else 0.0
+    stats = dict(loss=loss, n_clipped=n_clipped, kl_sum=math.fsum(klterms),
+                 entropy_sum=math.fsum(Hterms), n_tokens=n_tok)
+    if logits_is_array and rows == range(N_rows):
+        dl = np.stack([out_dl[j] for j in range(N_rows)]) if zero_masked_rows else None
+        return dict(loss=loss, dlogits=dl, logp=np.array([out_logp[j] for j in range(N_rows)]),
+                    entropy=np.array([out_H[j] for j in range(N_rows)]), stats=stats)
+    return dict(loss=loss, dlogits=out_dl, logp=out_logp, entropy=out_H, stats=stats)
+
+
+def loss_only(logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss, cfg=LossCfg()):
+    """The scalar loss alone (used by the finite-difference pin)."""
+    s = cfg.logit_scale
+    terms = []
+    for j in range(len(targets)):
+        if not loss_mask[j]:
+            continue
+        logp, _, _, _ = row_forward(logits[j], int(targets[j]), s)
+        ref = float(ref_logp[j]) if ref_logp is not None else None
+        L, _, _, _ = row_loss_terms(logp, float(old_logp[j]), ref, float(adv[int(row_traj[j])]), cfg)
+        terms.append(L)
+    return math.fsum(terms) / n_loss if n_loss > 0 else 0.0
+
+
+# --------------------------------------------------------------------------------------------
+# O5: vocab-sharded forward (north_star: vocab-sharding with all-reduced row max / sum-exp)
+# --------------------------------------------------------------------------------------------
+def shard_partials(x_shard, y: int, vocab_start: int, logit_scale: float = 1.0):
+    """Partials of one vocab shard [vocab_start, vocab_start + len): (m, s, t, zy) with
+    m = max z, s = sum exp(z-m), t = sum exp(z-m)(z-m), zy = z_y if y in the shard else 0."""
+    z = float(logit_scale) * np.asarray(x_shard, np.float64)
+    if z.shape[0] == 0:
+        return (-math.inf, 0.0, 0.0, 0.0)
+    m = float(np.max(z))
+    if m == -math.inf:                      # every entry -inf: the shard holds no probability mass
+        return (-math.inf, 0.0, 0.0, 0.0)
+    e = np.exp(z - m)
+    nz = e > 0
+    s = math.fsum(e)
+    t = math.fsum(e[nz] * (z[nz] - m))
+    zy = float(z[y - vocab_start]) if vocab_start <= y < vocab_start + z.shape[0] else 0.0
+    return (m, s, t, zy)
+
+
+def combine_partials(parts):
+    """M = max m_p; S = sum s_p e^{m_p-M}; T = sum e^{m_p-M}(t_p + (m_p-M) s_p);
+    lse = M + ln S; H = ln S - T/S; logp = sum zy_p - lse.   Returns (logp, H, lse)."""
+    M = max(p[0] for p in parts)
+    w = [math.exp(p[0] - M) if p[0] != -math.inf else 0.0 for p in parts]
+    S = math.fsum(wi * p[1] for wi, p in zip(w, parts))
+    T = math.fsum(wi * (p[2] + (p[0] - M) * p[1]) for wi, p in zip(w, parts) if wi > 0)
+    lse = M + math.log(S)
+    H = math.log(S) - T / S
+    logp = math.fsum(p[3] for p in parts) - lse
+    return logp, H, lse

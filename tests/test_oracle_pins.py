@@ -1,0 +1,415 @@
+"""Pins of the float64 oracle to things other than itself (-m "not gpu").
+
+Each test names what fixes the expected value: a SPEC.md/PAPER.md worked example (tests/golden/),
+a closed form derived independently of the oracle's algorithm, brute force on tiny inputs, an
+invariant, or a library routine (torch float64).
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle_ref as O
+from synth.trajectories import _pack, random_small_batch, make_batch, CONTEXT, ACTION, OBSERVATION, PAD
+from tests.conftest import load_golden
+
+CF = {k: float(v) for k, v in load_golden("closed_forms.txt").items()}
+
+
+# ----------------------------------------------------------------------------- O1 masks
+def _masks(tb, **kw):
+    return O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len,
+                         tb.terminated, traj_agent=tb.traj_agent, **kw)
+
+
+def test_arith_worked_example():
+    """SPEC.md:215/389-391/414: [CONTEXT "3+4=", ACTION "7\\n", OBSERVATION "done"]."""
+    g = load_golden("arith_mask.txt")
+    names = {"CONTEXT": CONTEXT, "ACTION": ACTION, "OBSERVATION": OBSERVATION}
+    segs = []
+    for part in g["segments"].split("|"):
+        src, text = part.strip().split(":", 1)
+        text = text.replace("\\n", "\n")
+        segs.append((names[src], 0 if src == "ACTION" else -1, len(text)))
+    tb = _pack([segs], [[float(g["turn_rewards"])]], [0], 1)
+    m = _masks(tb)
+    assert tb.num_rows == int(g["n_tokens"])
+    assert "".join(map(str, m["loss_mask"])) == g["loss_mask"]
+    assert "".join(map(str, m["response_mask"])) == g["response_mask"]
+    c = m["traj_source_counts"][0]
+    assert (c[CONTEXT], c[ACTION], c[OBSERVATION]) == (
+        int(g["context_tokens"]), int(g["action_tokens"]), int(g["observation_tokens"]))
+    assert m["n_loss"] == int(g["action_tokens"])
+
+
+def _brute_tokens(segs):
+    """Literal expansion: one (source, agent, segment-position) record per token."""
+    toks = []
+    for k, (s, a, L) in enumerate(segs):
+        toks.extend([(s, a, k)] * L)
+    return toks
+
+
+@pytest.mark.parametrize("train_agent", [-1, 0, 1])
+def test_masks_bruteforce_enumeration(train_agent):
+    """Every sequence of <= 3 segments over {CTX, ACT(a0), ACT(a1), OBS, PAD} x len {1, 2}."""
+    kinds = [(CONTEXT, -1), (ACTION, 0), (ACTION, 1), (OBSERVATION, -1), (PAD, -1)]
+    cases = []
+    for n in (1, 2, 3):
+        for combo in itertools.product(kinds, repeat=n):
+            for lens in itertools.product((1, 2), repeat=n):
+                cases.append([(s, a, L) for (s, a), L in zip(combo, lens)])
+    # pack many trajectories into one batch (exercises the CSR offsets too)
+    tb = _pack(cases, [[0.0]] * len(cases), [0] * len(cases), 1)
+    m = _masks(tb, train_agent=train_agent)
+    row = 0
+    for b, segs in enumerate(cases):
+        for (s, a, k) in _brute_tokens(segs):
+            want_loss = int(s == ACTION and (train_agent == -1 or a == train_agent))
+            want_resp = int(not (k == 0 and s == CONTEXT) and s != PAD)
+            assert m["loss_mask"][row] == want_loss
+            assert m["response_mask"][row] == want_resp
+            assert m["row_traj"][row] == b
+            row += 1
+        total = sum(L for _, _, L in segs)
+        assert m["traj_source_counts"][b].sum() == total          # SPEC.md:91 partition
+        assert m["traj_loss_tokens"][b] == sum(L for s, a, L in segs
+                                                if s == ACTION and (train_agent == -1 or a == train_agent))
+    assert row == tb.num_rows
+    assert m["n_loss"] == int(m["loss_mask"].sum())
+
+
+def test_masks_agent_views_partition_actions():
+    """two agents' loss masks over a shared transcript are disjoint and cover ACTION."""
+    tb = make_batch("marl")
+    both = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len,
+                         train_agent=-1)
+    m0 = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, train_agent=0)
+    m1 = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, train_agent=1)
+    assert not np.any(m0["loss_mask"] & m1["loss_mask"])
+    assert np.array_equal(m0["loss_mask"] | m1["loss_mask"], both["loss_mask"])
+    view = _masks(tb)  # per-view agent: each view trains only its own agent's actions
+    for b in range(tb.num_traj):
+        r0, r1 = tb.tok_offsets[b], tb.tok_offsets[b + 1]
+        src = m0 if tb.traj_agent[b] == 0 else m1
+        assert np.array_equal(view["loss_mask"][r0:r1], src["loss_mask"][r0:r1])
+
+
+def test_masks_errors():
+    tb = _pack([[(CONTEXT, -1, 2), (ACTION, 0, 2)]], [[1.0]], [0], 1, terminated=[0])
+    with pytest.raises(O.Unterminated):
+        _masks(tb)
+    tb = _pack([[(CONTEXT, -1, 2), (ACTION, 0, 2)]], [[1.0]], [0], 1)
+    tb.tok_offsets[1] = 5   # rows != sum of segment lengths
+    with pytest.raises(O.BadTrajectory):
+        _masks(tb)
+    with pytest.raises(O.EmptyGroup):
+        O.build_masks(np.zeros(1, np.int64), np.zeros(1, np.int32), [], [], [])
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_masks_random_properties(seed):
+    rng = np.random.default_rng(seed)
+    tb = random_small_batch(rng, 20)
+    m = _masks(tb)
+    assert int(m["traj_source_counts"].sum()) == tb.num_rows
+    for b in range(tb.num_traj):
+        r0, r1 = tb.tok_offsets[b], tb.tok_offsets[b + 1]
+        assert np.all(m["row_traj"][r0:r1] == b)
+        assert m["loss_mask"][r0:r1].sum() == m["traj_source_counts"][b, ACTION]
+
+
+# ----------------------------------------------------------------------------- O2 advantages
+def test_constant_group_zero_advantage():
+    """all returns equal -> A = 0 (exact for dyadic values)."""
+    for v in (0.0, 1.0, -1.0, 0.5):
+        a = O.group_advantages([0] * 8, [v] * 8, 1)["adv"]
+        assert np.all(a == 0.0)
+    a = O.group_advantages([0] * 3, [0.1] * 3, 1)["adv"]
+    assert np.all(np.abs(a) <= 1e-15)
+
+
+@pytest.mark.parametrize("k", range(1, 8))
+def test_binary_group_closed_form(k):
+    G = 8
+    R = [1.0] * k + [0.0] * (G - k)
+    pop = O.group_advantages([0] * G, R, 1)["adv"]
+    smp = O.group_advantages([0] * G, R, 1, unbiased=True)["adv"]
+    ap, an = math.sqrt((G - k) / k), -math.sqrt(k / (G - k))
+    assert np.allclose(pop[:k], ap, rtol=0, atol=1e-14) and np.allclose(pop[k:], an, rtol=0, atol=1e-14)
+    f = math.sqrt((G - 1) / G)
+    assert np.allclose(smp[:k], ap * f, atol=1e-14) and np.allclose(smp[k:], an * f, atol=1e-14)
+    if k == 2:
+        assert abs(pop[0] - CF["binary_G8_k2_pop_pos"]) < 1e-14
+        assert abs(pop[-1] - CF["binary_G8_k2_pop_neg"]) < 1e-14
+        assert abs(smp[0] - CF["binary_G8_k2_sample_pos"]) < 1e-14
+        assert abs(smp[-1] - CF["binary_G8_k2_sample_neg"]) < 1e-14
+
+
+def test_two_member_group():
+    a = O.group_advantages([0, 0], [0.0, 1.0], 1)["adv"]
+    assert a.tolist() == [-1.0, 1.0]
+    a = O.group_advantages([0, 0], [0.0, 1.0], 1, unbiased=True)["adv"]
+    assert np.allclose(a, [-1 / math.sqrt(2), 1 / math.sqrt(2)], atol=1e-15)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_advantage_invariants(seed):
+    rng = np.random.default_rng(seed)
+    G, B = 5, 60
+    gid = rng.integers(0, G, B)
+    R = rng.normal(size=B)
+    out = O.group_advantages(gid, R, G)
+    for g in range(G):
+        a = out["adv"][gid == g]
+        if len(a) >= 2:
+            assert abs(a.sum()) < 1e-12                      # sum of centred values
+            assert abs((a ** 2).sum() - len(a)) < 1e-10      # population: sum A^2 = n
+        assert out["group_size"][g] == int((gid == g).sum())
+    nostd = O.group_advantages(gid, R, G, std_norm=False)["adv"]
+    for b in range(B):
+        assert abs(nostd[b] - (R[b] - R[gid == gid[b]].mean())) < 1e-12
+
+
+def test_degenerate_and_singleton_groups():
+    a = O.group_advantages([0, 1, 1], [3.0, 2.0, 2.0 + 1e-9], 2)
+    assert a["adv"][0] == 0.0                      # singleton group: R - mean = 0
+    assert a["group_std"][1] < 1e-8               # std below the floor: divide by 1
+    assert abs(a["adv"][2] - 0.5e-9) < 1e-15
+    with pytest.raises(O.GroupRange):
+        O.group_advantages([0, 2], [1.0, 2.0], 2)
+    with pytest.raises(O.EmptyGroup):
+        O.group_advantages([], [], 1)
+
+
+def test_zero_sum_antisymmetry():
+    """PAPER.md:263 / SPEC.md:230: zero-sum two-agent episodes => A(agent1) = -A(agent0) exactly."""
+    tb = make_batch("marl")
+    R = O.episode_returns(tb.turn_offsets, tb.turn_rewards)
+    assert np.all(R[0::2] == -R[1::2])
+    a = O.group_advantages(tb.group_id, R, tb.num_groups)["adv"]
+    assert np.all(a[0::2] == -a[1::2])
+
+
+def test_episode_returns_undiscounted():
+    """return = sum over turns of the per-turn scores, undiscounted."""
+    R = O.episode_returns(np.array([0, 3, 3, 5]), np.array([0.5, 0.0, -1.0, 0.25, 0.25]))
+    assert R.tolist() == [-0.5, 0.0, 0.5]
+
+
+# ----------------------------------------------------------------------------- O3 forward
+@pytest.mark.parametrize("V", [151936, 1024])
+def test_uniform_row(V):
+    """north_star: uniform logits give log-prob = -ln V (and entropy ln V)."""
+    logp, H, lse, p = O.row_forward(np.zeros(V), 7)
+    want = CF[f"uniform_logp_V{V}"]
+    assert abs(logp - want) < 1e-12 and abs(H + want) < 1e-12
+    assert abs(math.fsum(p) - 1) < 1e-12
+
+
+@pytest.mark.parametrize("V,L", [(151936, 10), (1024, 5)])
+def test_two_level_row(V, L):
+    x = np.zeros(V)
+    x[3] = L
+    logp, H, _, _ = O.row_forward(x, 3)
+    assert abs(logp - CF[f"twolevel_V{V}_L{L}_logp"]) < 1e-11
+    assert abs(H - CF[f"twolevel_V{V}_L{L}_H"]) < 1e-11
+
+
+def test_two_token_softplus():
+    """V = 2: logp_y = -softplus(z_other - z_y)  (SPEC.md:327 two-token case)."""
+    for a, b in [(0.3, -1.2), (5.0, 5.0), (-30.0, 12.0)]:
+        logp, _, _, _ = O.row_forward(np.array([a, b]), 0)
+        d = b - a
+        want = -(max(d, 0.0) + math.log1p(math.exp(-abs(d))))
+        assert abs(logp - want) < 1e-14
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_forward_vs_torch_float64(seed):
+    """Library pin: torch.log_softmax / Categorical.entropy in float64 on CPU."""
+    rng = np.random.default_rng(seed)
+    x = rng.normal(scale=3.0, size=(6, 4099))
+    t = torch.from_numpy(x)
+    lsm = torch.log_softmax(t, dim=-1).numpy()
+    ent = torch.distributions.Categorical(logits=t).entropy().numpy()
+    for j in range(6):
+        y = int(rng.integers(0, 4099))
+        logp, H, lse, p = O.row_forward(x[j], y)
+        assert abs(logp - lsm[j, y]) < 1e-12
+        assert abs(H - ent[j]) < 1e-11
+        assert np.allclose(np.log(p), lsm[j], atol=1e-12)
+
+
+def test_forward_invariants():
+    rng = np.random.default_rng(9)
+    x = rng.normal(size=777) * 2
+    base = O.row_forward(x, 5)
+    shifted = O.row_forward(x + 123.25, 5)
+    assert abs(base[0] - shifted[0]) < 1e-12 and abs(base[1] - shifted[1]) < 1e-12
+    scaled = O.row_forward(x, 5, logit_scale=1 / 0.7)
+    direct = O.row_forward(x / 0.7, 5)
+    assert abs(scaled[0] - direct[0]) < 1e-13
+    # sum_v exp(logp_v) = 1 over all targets (SPEC.md:308 normalisation)
+    assert abs(math.fsum(math.exp(O.row_forward(x, v)[0]) for v in range(777)) - 1) < 1e-12
+    # -inf entries contribute nothing: equal to the row with them removed
+    xi = x.copy()
+    xi[[1, 50, 600]] = -np.inf
+    keep = np.setdiff1d(np.arange(777), [1, 50, 600])
+    a = O.row_forward(xi, 5)
+    b = O.row_forward(x[keep], int(np.searchsorted(keep, 5)))
+    assert abs(a[0] - b[0]) < 1e-13 and abs(a[1] - b[1]) < 1e-13
+    with pytest.raises(O.TargetRange):
+        O.row_forward(x, 777)
+
+
+# ----------------------------------------------------------------------------- O4 loss + grad
+def _tiny_problem(rng, N=12, V=8, B=3, beta=0.04, kl_type=3, scale=1.0, delta_sd=0.05):
+    x = rng.normal(scale=2.0, size=(N, V))
+    y = rng.integers(0, V, N)
+    mask = (rng.random(N) < 0.7).astype(np.uint8)
+    row_traj = np.sort(rng.integers(0, B, N)).astype(np.int32)
+    adv = rng.normal(size=B)
+    cfg = O.LossCfg(kl_beta=beta, kl_type=kl_type, logit_scale=scale)
+    logp = np.array([O.row_forward(x[j], int(y[j]), scale)[0] for j in range(N)])
+    old = logp + rng.normal(scale=delta_sd, size=N)
+    ref = logp + rng.normal(scale=0.1, size=N)
+    return x, y, mask, row_traj, adv, old, ref, cfg
+
+
+def test_on_policy_loss_is_minus_mean_advantage():
+    """north_star: old = new makes the ratio 1, so (with ref = new, KL 0) loss = -sum m A / N."""
+    rng = np.random.default_rng(1)
+    x, y, mask, rt, adv, _, _, cfg = _tiny_problem(rng)
+    logp = np.array([O.row_forward(x[j], int(y[j]))[0] for j in range(len(y))])
+    N = int(mask.sum())
+    out = O.policy_loss_fwd_bwd(x, y, mask, rt, adv, logp, logp, N, cfg)
+    want = -math.fsum(adv[rt[j]] for j in range(len(y)) if mask[j]) / N
+    assert abs(out["loss"] - want) < 1e-14
+    assert out["stats"]["kl_sum"] == 0.0 and out["stats"]["n_clipped"] == 0
+
+
+def test_balanced_groups_zero_loss():
+    """Equal trainable length per trajectory of a full group + on-policy => loss = 0 (sum A = 0)."""
+    rng = np.random.default_rng(2)
+    B, T, V = 8, 5, 6
+    R = rng.normal(size=B)
+    adv = O.group_advantages([0] * B, R, 1)["adv"]
+    x = rng.normal(size=(B * T, V))
+    y = rng.integers(0, V, B * T)
+    rt = np.repeat(np.arange(B), T).astype(np.int32)
+    mask = np.tile([0, 1, 1, 1, 0], B).astype(np.uint8)
+    logp = np.array([O.row_forward(x[j], int(y[j]))[0] for j in range(B * T)])
+    out = O.policy_loss_fwd_bwd(x, y, mask, rt, adv, logp, None, int(mask.sum()), O.LossCfg(kl_beta=0.0))
+    assert abs(out["loss"]) < 1e-15
+
+
+def test_clip_closed_forms():
+    cfg = O.LossCfg(kl_beta=0.0)
+    for A in (0.7, 2.0):
+        L, G, clipped, _ = O.row_loss_terms(math.log(1.5), 0.0, None, A, cfg)
+        assert abs(L - CF["clip_pos_factor"] * A) < 1e-15 and G == 0.0 and clipped
+    for A in (-0.7, -2.0):
+        L, G, clipped, _ = O.row_loss_terms(math.log(0.5), 0.0, None, A, cfg)
+        assert abs(L - CF["clip_neg_factor"] * A) < 1e-15 and G == 0.0 and clipped
+    # inside the trust region: pg = -A r, gradient -A r
+    L, G, clipped, _ = O.row_loss_terms(math.log(1.1), 0.0, None, 1.5, cfg)
+    assert abs(L + 1.5 * 1.1) < 1e-14 and abs(G + 1.5 * 1.1) < 1e-14 and not clipped
+    # A > 0 with r < 1 - eps is NOT clipped (min picks the unclipped term)
+    L, G, clipped, _ = O.row_loss_terms(math.log(0.5), 0.0, None, 1.0, cfg)
+    assert abs(L + 0.5) < 1e-15 and abs(G + 0.5) < 1e-15 and not clipped
+    # ratio clamp: |logp - old| > C => r = e^C and zero gradient
+    L, G, _, _ = O.row_loss_terms(30.0, 0.0, None, -1.0, O.LossCfg(kl_beta=0.0, clip_low=10.0))
+    assert G == 0.0 and abs(L - math.exp(20.0)) < 1e-6
+
+
+def test_kl_estimators():
+    cfg = O.LossCfg(kl_beta=1.0, clip_low=0.2)
+    L, G, _, kl = O.row_loss_terms(-1.0, -1.0, -0.9, 0.0, cfg)      # d = ref - logp = 0.1
+    assert abs(kl - CF["k3_d0p1_value"]) < 1e-15 and abs(G - CF["k3_d0p1_grad"]) < 1e-15
+    L, G, _, kl = O.row_loss_terms(-1.0, -1.0, -1.5, 0.0, O.LossCfg(kl_beta=1.0, kl_type=1))
+    assert abs(kl - 0.5) < 1e-15 and G == 1.0
+    L, G, _, kl = O.row_loss_terms(-1.0, -1.0, -1.5, 0.0, O.LossCfg(kl_beta=1.0, kl_type=2))
+    assert abs(kl - 0.125) < 1e-15 and abs(G - 0.5) < 1e-15
+
+
+@pytest.mark.parametrize("V,kl_type,scale,seed", [
+    (2, 3, 1.0, 0), (3, 3, 1.0, 1), (8, 1, 1.0, 2), (8, 2, 1 / 0.7, 3), (32, 3, 1.0, 4), (32, 3, 1 / 0.7, 5)])
+def test_gradient_finite_differences(V, kl_type, scale, seed):
+    """analytic dlogits vs central finite differences of the loss (h = 1e-6)."""
+    rng = np.random.default_rng(seed)
+    x, y, mask, rt, adv, old, ref, cfg = _tiny_problem(rng, N=10, V=V, kl_type=kl_type, scale=scale)
+    # force one clipped row and keep every row >= 1e-3 away from the clip / clamp kinks
+    j0 = int(np.flatnonzero(mask)[0])
+    logp0 = O.row_forward(x[j0], int(y[j0]), scale)[0]
+    adv[rt[j0]] = abs(adv[rt[j0]]) + 0.1
+    old[j0] = logp0 - math.log(1.5)
+    N = int(mask.sum())
+    out = O.policy_loss_fwd_bwd(x, y, mask, rt, adv, old, ref, N, cfg)
+    for j in range(len(y)):
+        if mask[j]:
+            r = math.exp(out["logp"][j] - old[j])
+            assert min(abs(r - 0.8), abs(r - 1.2)) > 1e-3
+    h = 1e-6
+    fd = np.zeros_like(x)
+    for j in range(x.shape[0]):
+        for v in range(V):
+            xp, xm = x.copy(), x.copy()
+            xp[j, v] += h
+            xm[j, v] -= h
+            fd[j, v] = (O.loss_only(xp, y, mask, rt, adv, old, ref, N, cfg)
+                        - O.loss_only(xm, y, mask, rt, adv, old, ref, N, cfg)) / (2 * h)
+    an = out["dlogits"]
+    scale_ = np.max(np.abs(an))
+    assert np.max(np.abs(an - fd)) <= 1e-6 * scale_ + 1e-12
+    assert np.all(an[mask == 0] == 0.0)                        # mask soundness
+    assert np.all(np.abs(an.sum(axis=1)) < 1e-15 + 1e-13 * scale_)   # rows sum to 0
+    assert np.all(an[j0] == 0.0) or cfg.kl_beta != 0.0         # clipped row: only KL gradient
+
+
+def test_sft_case_matches_torch_cross_entropy():
+    """SPEC.md:503 SFT = update with A = 1: with old = logp, beta = 0, every row trainable,
+    dlogits = d mean-CE / dz (torch float64 autograd, a library routine)."""
+    rng = np.random.default_rng(7)
+    N, V = 9, 17
+    x = rng.normal(size=(N, V))
+    y = rng.integers(0, V, N)
+    logp = np.array([O.row_forward(x[j], int(y[j]))[0] for j in range(N)])
+    out = O.policy_loss_fwd_bwd(x, y, np.ones(N, np.uint8), np.zeros(N, np.int32), np.ones(1),
+                                logp, None, N, O.LossCfg(kl_beta=0.0))
+    t = torch.from_numpy(x).requires_grad_(True)
+    ce = torch.nn.functional.cross_entropy(t, torch.from_numpy(y))
+    ce.backward()
+    assert np.max(np.abs(out["dlogits"] - t.grad.numpy())) < 1e-16 + 1e-14
+    assert abs(out["loss"] + 1.0) < 1e-15      # pg = -A r = -1 on every row
+
+
+def test_zero_loss_tokens():
+    rng = np.random.default_rng(3)
+    x, y, mask, rt, adv, old, ref, cfg = _tiny_problem(rng)
+    mask[:] = 0
+    out = O.policy_loss_fwd_bwd(x, y, mask, rt, adv, old, ref, 0, cfg)
+    assert out["loss"] == 0.0 and np.all(out["dlogits"] == 0.0)
+
+
+# ----------------------------------------------------------------------------- O5 vocab shards
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_vocab_shard_combine_equals_unsharded(P):
+    rng = np.random.default_rng(P)
+    V = 1000
+    x = rng.normal(scale=3, size=V)
+    x[[5, 400]] = -np.inf
+    for y in (0, 333, 999):
+        bounds = np.linspace(0, V, P + 1).astype(int)
+        parts = [O.shard_partials(x[a:b], y, a) for a, b in zip(bounds[:-1], bounds[1:])]
+        logp, H, lse = O.combine_partials(parts)
+        ref = O.row_forward(x, y)
+        assert abs(logp - ref[0]) < 1e-12 and abs(H - ref[1]) < 1e-12 and abs(lse - ref[2]) < 1e-12
+    # an empty shard and an all -inf shard contribute nothing
+    empty = O.shard_partials(x[:0], 3, 0)
+    dead = O.shard_partials(np.full(4, -np.inf), 3, 0)
+    assert empty == dead == (-math.inf, 0.0, 0.0, 0.0)
+    got = O.combine_partials([empty, O.shard_partials(x, 3, 0), dead])
+    assert abs(got[0] - O.row_forward(x, 3)[0]) < 1e-12
