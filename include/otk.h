@@ -1,0 +1,240 @@
+/*
+ * otk.h — C ABI of the OpenTinker (arxiv 2601.07376) policy-gradient hot path on B200 (sm_100a).
+ *
+ * The paper's Task Server runs every RL job's update in "forward inference (fwd)" and "parameter
+ * updates" resource pools (caption of Fig. mas-framework). BASELINE.json's north_star
+ * names the computation those pools run; each step is one entry point here:
+ *
+ *   (1) otk_build_masks          loss/response masks from FSM-labelled segments
+ *   (2) otk_group_advantages     GRPO group-relative advantages
+ *   (3) otk_logprob_entropy_fwd  fused vocab-wide log-softmax + gather + entropy  north_star (3)
+ *   (4) otk_policy_loss_fwd_bwd  PPO-clip + KL surrogate, token-mean, fused       north_star (4)
+ *                                backward dlogits = coef * (softmax - onehot)
+ *   vocab sharding (north_star "vocab-sharding logits with an all-reduce of row max and sum-exp"):
+ *       otk_row_partials → (caller all-gathers partials) → otk_logprob_entropy_combine /
+ *       otk_policy_loss_fwd_bwd_partials.
+ *
+ * Conventions (all entry points):
+ *  - Pointers are DEVICE pointers unless stated otherwise. All buffers are caller-owned; the library
+ *    never allocates on the hot path (the ctx owns a small scratch area, the sticky error word and the
+ *    staging buffers of the host-buffer entry point).
+ *  - Every call is asynchronous on `stream` (a cudaStream_t), performs no host synchronisation, and is
+ *    CUDA-graph capturable (except otk_ctx_check and otk_policy_loss_fwd_bwd_host).
+ *  - Host-checkable errors (NULL pointers, sizes, alignment, dtype, empty batch) return immediately and
+ *    launch nothing. Data-dependent errors (segment lengths, unterminated trajectory, group id or target
+ *    out of range) set the ctx's sticky device error word; the offending rows / trajectories are then
+ *    treated as loss-masked so kernels stay memory-safe; otk_ctx_check reports the first such error.
+ *  - Outputs never alias inputs. A ctx may be used from one stream at a time (its scratch is shared).
+ *  - Layout: logits / dlogits are row-major [num_rows, ld] with ld >= vocab and ld * sizeof(dtype) a
+ *    multiple of 16 bytes, base pointer 16-byte aligned. Row j's logits score target j (the caller
+ *    shifts; R7). Only columns [0, vocab) are read or written.
+ */
+#ifndef OTK_H_
+#define OTK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OTK_VERSION 100 /* 0.1.0 */
+
+typedef struct CUstream_st* otk_stream_t; /* identical to cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  OTK_OK = 0,
+  OTK_ERR_INVALID_ARG = 1,   /* NULL pointer, bad flag, bad config value                   */
+  OTK_ERR_SHAPE = 2,         /* negative / inconsistent sizes, vocab larger than supported  */
+  OTK_ERR_ALIGNMENT = 3,     /* logits/dlogits base or row stride not 16-byte aligned       */
+  OTK_ERR_DTYPE = 4,         /* unknown otk_dtype                                           */
+  OTK_ERR_EMPTY_GROUP = 5,   /* num_traj < 1 (SPEC.md:324 EmptyGroup)                      */
+  OTK_ERR_UNTERMINATED = 6,  /* terminated[b] == 0 (SPEC.md:324 UnterminatedTrajectory)     */
+  OTK_ERR_BAD_TRAJECTORY = 7,/* segment lengths/sources inconsistent with the row count     */
+  OTK_ERR_TARGET_RANGE = 8,  /* target outside [0, vocab_total)                             */
+  OTK_ERR_CUDA = 9,          /* a CUDA runtime call failed (see otk_last_error)             */
+  OTK_ERR_GROUP_RANGE = 10   /* group_id outside [0, num_groups)                            */
+} otk_status;
+
+typedef enum { OTK_SRC_CONTEXT = 0, OTK_SRC_ACTION = 1, OTK_SRC_OBSERVATION = 2, OTK_SRC_PAD = 3 } otk_source;
+typedef enum { OTK_F32 = 0, OTK_BF16 = 1 } otk_dtype;
+typedef enum { OTK_KL_K1 = 1, OTK_KL_K2 = 2, OTK_KL_K3 = 3 } otk_kl_type;
+
+#define OTK_ANY_AGENT (-1)
+#define OTK_ADV_STD_NORM 0x1u /* divide by the group std (default on)        */
+#define OTK_ADV_UNBIASED 0x2u /* std with n-1 instead of n (R2; default off)    */
+
+/* ---------------------------------------------------------------------------------------------
+ * Context. Owns: the device index, SM count, a sticky device error word, O(#SM) scratch for the
+ * deterministic reductions, and (lazily, on first use of the host entry point) staging buffers.
+ * ------------------------------------------------------------------------------------------- */
+typedef struct otk_ctx otk_ctx;
+
+otk_status otk_ctx_create(int cuda_device, otk_ctx** out);
+otk_status otk_ctx_destroy(otk_ctx* ctx);
+/* Synchronises `stream`, returns (and clears) the first device-side data error since the last check. */
+otk_status otk_ctx_check(otk_ctx* ctx, otk_stream_t stream);
+const char* otk_status_string(otk_status s);
+const char* otk_last_error(void); /* thread-local detail of the last host-side error */
+int otk_version(void);
+
+/* ---------------------------------------------------------------------------------------------
+ * (1) Masks — PAPER.md §2.2 (lines 167-174): PENDING (context) tokens "are excluded from loss
+ * computation"; only GENERATING (action) tokens "are marked as trainable"; INTERACTING (observation)
+ * tokens "are masked from the loss". PAPER.md:192: "Model parameters and gradients are not shared
+ * across agents", so an ACTION row is trainable only for the agent that emitted it.
+ *
+ * One trajectory = a list of segments (SPEC.md:37-50 Segment{source, tokens}) packed into rows
+ * [tok_offsets[b], tok_offsets[b+1]) of the batch, in order.
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t num_traj;             /* B >= 1, else OTK_ERR_EMPTY_GROUP                                */
+  int64_t num_rows;             /* N = tok_offsets[B] (host copy; checked on device)               */
+  const int64_t* tok_offsets;   /* [B+1] row offsets, tok_offsets[0] = 0, non-decreasing           */
+  const int32_t* seg_offsets;   /* [B+1] offsets into the segment arrays                          */
+  const uint8_t* seg_source;    /* [S] otk_source                                                  */
+  const int16_t* seg_agent;     /* [S] emitting agent of an ACTION segment (ignored otherwise)     */
+  const int32_t* seg_len;       /* [S] > 0; a trajectory's lengths sum to its row count            */
+  const uint8_t* terminated;    /* [B] or NULL (= all terminated); 0 => OTK_ERR_UNTERMINATED        */
+  const int16_t* traj_agent;    /* [B] or NULL: agent trained on trajectory b (overrides train_agent) */
+} otk_traj_batch;
+
+/*
+ * Outputs (device): loss_mask[N] u8 = (src == ACTION) && (agent matches); response_mask[N] u8 (NULL ok)
+ * = every non-PAD row outside the trajectory's leading CONTEXT segment (R13);
+ * row_traj[N] i32 = b; traj_loss_tokens[B] i64; traj_source_counts[B*4] i64 (NULL ok; SPEC.md:408-416
+ * mask_report, order CONTEXT, ACTION, OBSERVATION, PAD); n_loss[1] i64 = sum of loss_mask (this batch;
+ * a batch-sharded caller all-reduces it to the global token count before step (4)).
+ * Rows of an invalid trajectory get loss_mask 0 and the error word is set. Bit-exact.
+ */
+otk_status otk_build_masks(otk_ctx* ctx, const otk_traj_batch* batch /* host struct, device arrays */,
+                           int16_t train_agent, uint8_t* loss_mask, uint8_t* response_mask, int32_t* row_traj,
+                           int64_t* traj_loss_tokens, int64_t* traj_source_counts, int64_t* n_loss,
+                           otk_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * (2) Group-relative advantages — PAPER.md:177 ("rewards are associated with the corresponding action
+ * tokens"), SPEC.md:95 (return = undiscounted sum of per-turn scores), SPEC.md:323:
+ *   A_b = (R_b - mean_g) / (std_g if std_g > std_floor else 1)   (flags & OTK_ADV_STD_NORM)
+ *   A_b =  R_b - mean_g                                         (otherwise)
+ * over the trajectories b' with group_id[b'] == group_id[b]; std is the population std unless
+ * OTK_ADV_UNBIASED (std = 0 for groups of size <= 1). Sums run in trajectory order, float64.
+ * Returns come either from returns[B] or from per-turn scores (turn_offsets[B+1], turn_rewards[...]):
+ * exactly one of `returns` and `turn_offsets` must be non-NULL. A batch-sharded caller passes the
+ * all-gathered (group_id, return) arrays of all ranks, so every rank computes identical statistics.
+ * Outputs: adv[B] f64; returns_out[B], group_mean[G], group_std[G] f64, group_size[G] i32 (NULL ok).
+ * Tolerance vs the float64 oracle: 1e-6 abs (north_star). Out-of-range group ids set
+ * OTK_ERR_GROUP_RANGE and give A = 0 for that trajectory.
+ * ------------------------------------------------------------------------------------------- */
+otk_status otk_group_advantages(otk_ctx* ctx, int32_t num_traj, const int32_t* group_id, int32_t num_groups,
+                                const double* returns, const int32_t* turn_offsets, const double* turn_rewards,
+                                uint32_t flags, double std_floor, double* adv, double* returns_out,
+                                double* group_mean, double* group_std, int32_t* group_size, otk_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * (3) Forward: per row j with row_mask[j] != 0 (row_mask NULL = all rows), z = logit_scale * x:
+ *   M = max_v z_v, S = sum_v e^{z_v - M}, lse = M + ln S, logp_j = z_{y_j} - lse,
+ *   entropy_j = ln S - sum_v e^{z_v - M}(z_v - M) / S.
+ * logits: [num_rows, ld] of dtype (bf16 or fp32); targets[num_rows] i32 in [0, vocab).
+ * Outputs logp / entropy / lse [num_rows] f32 (entropy, lse may be NULL); masked rows get 0.
+ * fp32 accumulation, one HBM read of each logit. Tolerance vs oracle: 2e-3 abs (bf16), 1e-5 (fp32).
+ * logit_scale > 0 (= 1/temperature, R19).
+ * ------------------------------------------------------------------------------------------- */
+otk_status otk_logprob_entropy_fwd(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld, otk_dtype dtype,
+                                   const void* logits, const int32_t* targets, const uint8_t* row_mask,
+                                   float logit_scale, float* logp, float* entropy, float* lse,
+                                   otk_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * (4) Loss forward + fused backward. Per row j (A = adv[row_traj[j]], m = loss_mask[j], N = *n_loss):
+ *   delta = clamp(logp - old, -C, C), r = e^delta, rbar = clamp(r, 1 - clip_low, 1 + clip_high)
+ *   pg = max(-A r, -A rbar); clipped <=> (A > 0 && r > 1 + clip_high) || (A < 0 && r < 1 - clip_low)
+ *   KL: k3 = e^d - d - 1, d = clamp(ref - logp, -C, C); k1 = logp - ref; k2 = (logp - ref)^2 / 2
+ *   L_j = pg + kl_beta * KL;   loss = sum_j m_j L_j / N   (token mean over the GLOBAL batch, R17)
+ *   dlogits[j, v] = coef_j * (softmax_jv - [v == y_j]),  coef_j = -s * (m_j / N) * dL_j/dlogp_j
+ * with dL/dlogp = (clipped or |logp - old| > C ? 0 : -A r) + beta * (k3: |ref-logp| > C ? 0 : 1 - e^d;
+ * k1: 1; k2: logp - ref). old/ref are detached constants; ref_logp may be NULL iff kl_beta == 0.
+ * n_loss is a DEVICE pointer (never read on the host). Rows with m == 0: dlogits row = 0 if
+ * cfg->zero_masked_rows (else untouched), logp = entropy = 0; they are not read (write-only rows).
+ * stats (device): accumulated (+=) when cfg->accumulate_stats, else overwritten; reduced in a fixed
+ * order (deterministic, no float atomics). A step over several micro-batches sets accumulate_stats = 0
+ * on the first call. dlogits has the logits' dtype and layout and must not alias them.
+ * Tolerances vs oracle: loss 1e-4 relative (R22), dlogits |d| <= 2^-7 |ref| + 1e-5 |coef_j| (bf16).
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+  double clip_low;          /* epsilon_low, default 0.2  (R14) */
+  double clip_high;         /* epsilon_high, default 0.2                  */
+  double kl_beta;           /* beta, default 0.04; 0 disables KL and ref  */
+  double log_ratio_clamp;   /* C, default 20 (R15)                         */
+  double logit_scale;       /* s = 1/temperature > 0, default 1 (R19)      */
+  int32_t kl_type;          /* otk_kl_type, default OTK_KL_K3 (R16)        */
+  int32_t zero_masked_rows; /* default 1                                   */
+  int32_t accumulate_stats; /* default 0                                   */
+  int32_t reserved;         /* must be 0                                   */
+} otk_loss_cfg;
+
+typedef struct {
+  double loss;        /* sum_j m_j L_j / N                     */
+  double n_clipped;   /* number of trainable rows with clipping */
+  double kl_sum;      /* sum_j m_j KL_j                         */
+  double entropy_sum; /* sum_j m_j H_j                          */
+  double n_tokens;    /* number of trainable rows seen          */
+} otk_loss_stats;
+
+otk_status otk_policy_loss_fwd_bwd(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld, otk_dtype dtype,
+                                   const void* logits, const int32_t* targets, const uint8_t* loss_mask,
+                                   const int32_t* row_traj, const double* adv, const float* old_logp,
+                                   const float* ref_logp, const int64_t* n_loss, const otk_loss_cfg* cfg,
+                                   void* dlogits, float* logp, float* entropy, otk_loss_stats* stats,
+                                   otk_stream_t stream);
+
+/* Same computation as otk_policy_loss_fwd_bwd but every array argument is a HOST pointer (pinned
+ * memory recommended): rows are streamed through ctx-owned device staging buffers in chunks, with the
+ * host->device copies of chunk k+1 overlapping the kernel on chunk k. dlogits_host may be NULL (the
+ * gradient is then computed on the device and discarded); stats_host receives the result. Blocking:
+ * returns after the stats have been copied back. Used to measure the end-to-end (e2e) metric. */
+otk_status otk_policy_loss_fwd_bwd_host(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld,
+                                        otk_dtype dtype, const void* logits_host, const int32_t* targets_host,
+                                        const uint8_t* loss_mask_host, const int32_t* row_traj_host,
+                                        int32_t num_traj, const double* adv_host, const float* old_logp_host,
+                                        const float* ref_logp_host, int64_t n_loss, const otk_loss_cfg* cfg,
+                                        void* dlogits_host, otk_loss_stats* stats_host, int64_t rows_per_chunk);
+
+/* ---------------------------------------------------------------------------------------------
+ * Vocab sharding. A rank holds columns [vocab_start, vocab_start + vocab_local) of every row, with
+ * global targets. otk_row_partials writes per row (m2, s, t2, zy) as 4 floats: m2 = log2(e) * max z,
+ * s = sum 2^{log2(e) z - m2}, t2 = sum 2^{..}(log2(e) z - m2), zy = z_y if y is in the shard else 0
+ * (rows with row_mask 0: (-inf, 0, 0, 0)). The caller all-gathers them into [nshards][num_rows][4]
+ * (rank order); the combine (R25) is exact rescaling in rank order, identical on all ranks.
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+  int64_t vocab_start; /* first global column held by this rank */
+  int64_t vocab_total; /* global vocabulary (targets are checked against it) */
+} otk_vocab_shard;
+
+otk_status otk_row_partials(otk_ctx* ctx, int64_t num_rows, int64_t vocab_local, int64_t ld, otk_dtype dtype,
+                            const void* logits, const int32_t* targets, const uint8_t* row_mask,
+                            const otk_vocab_shard* shard, float logit_scale, float* partials, otk_stream_t stream);
+
+otk_status otk_logprob_entropy_combine(otk_ctx* ctx, int64_t num_rows, int32_t nshards, const float* partials,
+                                       const uint8_t* row_mask, float* logp, float* entropy, float* lse,
+                                       otk_stream_t stream);
+
+/* (4) on a vocab shard: the row statistics come from the all-gathered partials; this rank writes the
+ * dlogits of its columns. loss/stats are the global values on every rank. */
+otk_status otk_policy_loss_fwd_bwd_partials(otk_ctx* ctx, int64_t num_rows, int64_t vocab_local, int64_t ld,
+                                            otk_dtype dtype, const void* logits, const int32_t* targets,
+                                            const uint8_t* loss_mask, const int32_t* row_traj, const double* adv,
+                                            const float* old_logp, const float* ref_logp, const int64_t* n_loss,
+                                            const otk_loss_cfg* cfg, const otk_vocab_shard* shard,
+                                            int32_t nshards, const float* partials, void* dlogits, float* logp,
+                                            float* entropy, otk_loss_stats* stats, otk_stream_t stream);
+
+/* Harness helper (not on the path): number of kernel launches the library issued since ctx creation. */
+int64_t otk_ctx_launch_count(const otk_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OTK_H_ */

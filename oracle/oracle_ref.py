@@ -267,7 +267,7 @@ def policy_loss_fwd_bwd(logits, targets, loss_mask, row_traj, adv, old_logp, ref
     rows = range(N_rows) if rows is None else rows
     s = cfg.logit_scale
     invN = (1.0 / n_loss) if n_loss > 0 else 0.0
-    out_dl, out_logp, out_H = {}, {}, {}
+    out_dl, out_logp, out_H, out_coef = {}, {}, {}, {}
     terms, klterms, Hterms = [], [], []
     n_clipped = 0
     n_tok = 0
@@ -276,7 +276,7 @@ def policy_loss_fwd_bwd(logits, targets, loss_mask, row_traj, adv, old_logp, ref
         m = int(loss_mask[j])
         if not m:
             out_dl[j] = np.zeros(len(x)) if zero_masked_rows else None
-            out_logp[j], out_H[j] = 0.0, 0.0
+            out_logp[j], out_H[j], out_coef[j] = 0.0, 0.0, 0.0
             continue
         y = int(targets[j])
         logp, H, lse, p = row_forward(x, y, s)
@@ -286,7 +286,7 @@ def policy_loss_fwd_bwd(logits, targets, loss_mask, row_traj, adv, old_logp, ref
         coef = -s * invN * G
         dl = coef * p
         dl[y] = coef * (p[y] - 1.0)
-        out_dl[j], out_logp[j], out_H[j] = dl, logp, H
+        out_dl[j], out_logp[j], out_H[j], out_coef[j] = dl, logp, H, coef
         terms.append(L); klterms.append(kl); Hterms.append(H)
         n_clipped += int(clipped)
         n_tok += 1
@@ -296,8 +296,9 @@ def policy_loss_fwd_bwd(logits, targets, loss_mask, row_traj, adv, old_logp, ref
     if logits_is_array and rows == range(N_rows):
         dl = np.stack([out_dl[j] for j in range(N_rows)]) if zero_masked_rows else None
         return dict(loss=loss, dlogits=dl, logp=np.array([out_logp[j] for j in range(N_rows)]),
-                    entropy=np.array([out_H[j] for j in range(N_rows)]), stats=stats)
-    return dict(loss=loss, dlogits=out_dl, logp=out_logp, entropy=out_H, stats=stats)
+                    entropy=np.array([out_H[j] for j in range(N_rows)]),
+                    coef=np.array([out_coef[j] for j in range(N_rows)]), stats=stats)
+    return dict(loss=loss, dlogits=out_dl, logp=out_logp, entropy=out_H, coef=out_coef, stats=stats)
 
 
 def loss_only(logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss, cfg=LossCfg()):

@@ -1,0 +1,392 @@
+"""otk — B200-native hot path of OpenTinker's (arxiv 2601.07376) RL policy-gradient update.
+
+Thin ctypes binding over ``libotk.so`` (C ABI, ``include/otk.h``). Functions carry the C names and
+only marshal arguments: every step of the path runs in the library's sm_100a kernels. torch supplies
+device memory and streams. There is no CPU fallback: importing this package without the built
+library raises ImportError (build it with ``python -m paper_2601_07376_b200.build``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libotk.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2601_07376_b200.build` "
+                      "(the otk hot path has no CPU fallback)")
+_lib = C.CDLL(LIB_PATH)
+
+OTK_F32, OTK_BF16 = 0, 1
+OTK_KL_K1, OTK_KL_K2, OTK_KL_K3 = 1, 2, 3
+OTK_ANY_AGENT = -1
+OTK_ADV_STD_NORM, OTK_ADV_UNBIASED = 0x1, 0x2
+CONTEXT, ACTION, OBSERVATION, PAD = 0, 1, 2, 3
+
+STATUS = {0: "OTK_OK", 1: "OTK_ERR_INVALID_ARG", 2: "OTK_ERR_SHAPE", 3: "OTK_ERR_ALIGNMENT", 4: "OTK_ERR_DTYPE",
+          5: "OTK_ERR_EMPTY_GROUP", 6: "OTK_ERR_UNTERMINATED", 7: "OTK_ERR_BAD_TRAJECTORY",
+          8: "OTK_ERR_TARGET_RANGE", 9: "OTK_ERR_CUDA", 10: "OTK_ERR_GROUP_RANGE"}
+
+
+class OtkError(RuntimeError):
+    def __init__(self, status: int, detail: str = ""):
+        self.status = int(status)
+        self.name = STATUS.get(self.status, "OTK_ERR_UNKNOWN")
+        super().__init__(f"{self.name}: {detail}")
+
+
+class otk_traj_batch(C.Structure):
+    _fields_ = [("num_traj", C.c_int32), ("num_rows", C.c_int64), ("tok_offsets", C.c_void_p),
+                ("seg_offsets", C.c_void_p), ("seg_source", C.c_void_p), ("seg_agent", C.c_void_p),
+                ("seg_len", C.c_void_p), ("terminated", C.c_void_p), ("traj_agent", C.c_void_p)]
+
+
+class otk_loss_cfg(C.Structure):
+    _fields_ = [("clip_low", C.c_double), ("clip_high", C.c_double), ("kl_beta", C.c_double),
+                ("log_ratio_clamp", C.c_double), ("logit_scale", C.c_double), ("kl_type", C.c_int32),
+                ("zero_masked_rows", C.c_int32), ("accumulate_stats", C.c_int32), ("reserved", C.c_int32)]
+
+
+class otk_vocab_shard(C.Structure):
+    _fields_ = [("vocab_start", C.c_int64), ("vocab_total", C.c_int64)]
+
+
+STATS_FIELDS = ("loss", "n_clipped", "kl_sum", "entropy_sum", "n_tokens")   # otk_loss_stats (5 doubles)
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_sig = {
+    "otk_version": (C.c_int, []),
+    "otk_last_error": (C.c_char_p, []),
+    "otk_status_string": (C.c_char_p, [C.c_int]),
+    "otk_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "otk_ctx_destroy": (C.c_int, [_P]),
+    "otk_ctx_check": (C.c_int, [_P, _P]),
+    "otk_ctx_launch_count": (_I64, [_P]),
+    "otk_build_masks": (C.c_int, [_P, C.POINTER(otk_traj_batch), C.c_int16, _P, _P, _P, _P, _P, _P, _P]),
+    "otk_group_advantages": (C.c_int, [_P, C.c_int32, _P, C.c_int32, _P, _P, _P, C.c_uint32, C.c_double,
+                                       _P, _P, _P, _P, _P, _P]),
+    "otk_logprob_entropy_fwd": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, C.c_float, _P, _P, _P, _P]),
+    "otk_policy_loss_fwd_bwd": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, _P, _P, _P, _P, _P,
+                                          C.POINTER(otk_loss_cfg), _P, _P, _P, _P, _P]),
+    "otk_policy_loss_fwd_bwd_host": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, _P, C.c_int32, _P, _P,
+                                               _P, _I64, C.POINTER(otk_loss_cfg), _P, _P, _I64]),
+    "otk_row_partials": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, C.POINTER(otk_vocab_shard),
+                                   C.c_float, _P, _P]),
+    "otk_logprob_entropy_combine": (C.c_int, [_P, _I64, C.c_int32, _P, _P, _P, _P, _P, _P]),
+    "otk_policy_loss_fwd_bwd_partials": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, _P, _P, _P, _P,
+                                                   _P, C.POINTER(otk_loss_cfg), C.POINTER(otk_vocab_shard),
+                                                   C.c_int32, _P, _P, _P, _P, _P, _P]),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_sig)
+
+
+def _check(st: int):
+    if st != 0:
+        raise OtkError(st, _lib.otk_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _dev(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return OTK_BF16
+    if t.dtype == torch.float32:
+        return OTK_F32
+    raise ValueError("logits must be bfloat16 or float32")
+
+
+@dataclass
+class LossCfg:
+    clip_low: float = 0.2
+    clip_high: float = 0.2
+    kl_beta: float = 0.04
+    kl_type: int = OTK_KL_K3
+    log_ratio_clamp: float = 20.0
+    logit_scale: float = 1.0
+    zero_masked_rows: bool = True
+    accumulate_stats: bool = False
+
+    def c(self, accumulate: Optional[bool] = None) -> otk_loss_cfg:
+        acc = self.accumulate_stats if accumulate is None else accumulate
+        return otk_loss_cfg(self.clip_low, self.clip_high, self.kl_beta, self.log_ratio_clamp, self.logit_scale,
+                            int(self.kl_type), int(bool(self.zero_masked_rows)), int(bool(acc)), 0)
+
+
+class Context:
+    """Owns an otk_ctx (sticky error word, reduction scratch, staging) on one CUDA device."""
+
+    def __init__(self, device: Optional[int] = None):
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = int(device)
+        h = C.c_void_p()
+        _check(_lib.otk_ctx_create(self.device, C.byref(h)))
+        self.handle = h
+
+    def check(self, stream=None):
+        """Synchronise `stream` and raise OtkError for a device-side data error since the last check."""
+        _check(_lib.otk_ctx_check(self.handle, _stream(stream)))
+
+    @property
+    def launches(self) -> int:
+        return int(_lib.otk_ctx_launch_count(self.handle))
+
+    def close(self):
+        if self.handle:
+            _lib.otk_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------------------------------------
+# trajectories on the device
+# ------------------------------------------------------------------------------------------------
+@dataclass
+class DeviceTrajBatch:
+    tok_offsets: torch.Tensor
+    seg_offsets: torch.Tensor
+    seg_source: torch.Tensor
+    seg_agent: torch.Tensor
+    seg_len: torch.Tensor
+    terminated: Optional[torch.Tensor]
+    traj_agent: Optional[torch.Tensor]
+    num_traj: int
+    num_rows: int
+
+    def c(self) -> otk_traj_batch:
+        return otk_traj_batch(self.num_traj, self.num_rows, _ptr(self.tok_offsets), _ptr(self.seg_offsets),
+                              _ptr(self.seg_source), _ptr(self.seg_agent), _ptr(self.seg_len),
+                              _ptr(self.terminated), _ptr(self.traj_agent))
+
+
+def traj_batch_to_device(tb, device="cuda", non_blocking=False) -> DeviceTrajBatch:
+    """Copy a host segment CSR (any object with the otk_traj_batch fields as numpy arrays) to `device`."""
+    def t(a, dt):
+        if a is None:
+            return None
+        x = torch.as_tensor(a).to(dt)
+        return x.to(device, non_blocking=non_blocking)
+    return DeviceTrajBatch(
+        tok_offsets=t(tb.tok_offsets, torch.int64), seg_offsets=t(tb.seg_offsets, torch.int32),
+        seg_source=t(tb.seg_source, torch.uint8), seg_agent=t(tb.seg_agent, torch.int16),
+        seg_len=t(tb.seg_len, torch.int32), terminated=t(tb.terminated, torch.uint8),
+        traj_agent=t(getattr(tb, "traj_agent", None), torch.int16),
+        num_traj=int(len(tb.tok_offsets) - 1), num_rows=int(tb.tok_offsets[-1]))
+
+
+# ------------------------------------------------------------------------------------------------
+# (1) masks
+# ------------------------------------------------------------------------------------------------
+def otk_build_masks(ctx: Context, batch: DeviceTrajBatch, train_agent: int = OTK_ANY_AGENT, *,
+                    response_mask: bool = True, source_counts: bool = True, out: Optional[dict] = None,
+                    stream=None) -> dict:
+    dev = batch.tok_offsets.device
+    N, B = batch.num_rows, batch.num_traj
+    o = out if out is not None else {}
+    o.setdefault("loss_mask", torch.empty(N, dtype=torch.uint8, device=dev))
+    if response_mask:
+        o.setdefault("response_mask", torch.empty(N, dtype=torch.uint8, device=dev))
+    o.setdefault("row_traj", torch.empty(N, dtype=torch.int32, device=dev))
+    o.setdefault("traj_loss_tokens", torch.empty(B, dtype=torch.int64, device=dev))
+    if source_counts:
+        o.setdefault("traj_source_counts", torch.empty((B, 4), dtype=torch.int64, device=dev))
+    o.setdefault("n_loss", torch.empty(1, dtype=torch.int64, device=dev))
+    cb = batch.c()
+    _check(_lib.otk_build_masks(ctx.handle, C.byref(cb), train_agent, _ptr(o["loss_mask"]),
+                                _ptr(o.get("response_mask")), _ptr(o["row_traj"]), _ptr(o["traj_loss_tokens"]),
+                                _ptr(o.get("traj_source_counts")), _ptr(o["n_loss"]), _stream(stream)))
+    return o
+
+
+# ------------------------------------------------------------------------------------------------
+# (2) advantages
+# ------------------------------------------------------------------------------------------------
+def otk_group_advantages(ctx: Context, group_id: torch.Tensor, num_groups: int, *,
+                         returns: Optional[torch.Tensor] = None, turn_offsets: Optional[torch.Tensor] = None,
+                         turn_rewards: Optional[torch.Tensor] = None, std_norm: bool = True,
+                         unbiased: bool = False, std_floor: float = 1e-8, out: Optional[dict] = None,
+                         stream=None) -> dict:
+    _dev(group_id, "group_id")
+    B = int(group_id.numel())
+    dev = group_id.device
+    o = out if out is not None else {}
+    o.setdefault("adv", torch.empty(B, dtype=torch.float64, device=dev))
+    o.setdefault("returns", torch.empty(B, dtype=torch.float64, device=dev))
+    o.setdefault("group_mean", torch.empty(num_groups, dtype=torch.float64, device=dev))
+    o.setdefault("group_std", torch.empty(num_groups, dtype=torch.float64, device=dev))
+    o.setdefault("group_size", torch.empty(num_groups, dtype=torch.int32, device=dev))
+    flags = (OTK_ADV_STD_NORM if std_norm else 0) | (OTK_ADV_UNBIASED if unbiased else 0)
+    _check(_lib.otk_group_advantages(ctx.handle, B, _ptr(group_id), int(num_groups), _ptr(returns),
+                                     _ptr(turn_offsets), _ptr(turn_rewards), flags, float(std_floor),
+                                     _ptr(o["adv"]), _ptr(o["returns"]), _ptr(o["group_mean"]),
+                                     _ptr(o["group_std"]), _ptr(o["group_size"]), _stream(stream)))
+    return o
+
+
+# ------------------------------------------------------------------------------------------------
+# (3) forward
+# ------------------------------------------------------------------------------------------------
+def otk_logprob_entropy_fwd(ctx: Context, logits: torch.Tensor, targets: torch.Tensor, *,
+                            vocab: Optional[int] = None, row_mask: Optional[torch.Tensor] = None,
+                            logit_scale: float = 1.0, want_lse: bool = False, out: Optional[dict] = None,
+                            stream=None) -> dict:
+    _dev(logits, "logits")
+    N, ld = logits.shape
+    V = ld if vocab is None else int(vocab)
+    dev = logits.device
+    o = out if out is not None else {}
+    o.setdefault("logp", torch.empty(N, dtype=torch.float32, device=dev))
+    o.setdefault("entropy", torch.empty(N, dtype=torch.float32, device=dev))
+    if want_lse:
+        o.setdefault("lse", torch.empty(N, dtype=torch.float32, device=dev))
+    _check(_lib.otk_logprob_entropy_fwd(ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits), _ptr(targets),
+                                        _ptr(row_mask), float(logit_scale), _ptr(o["logp"]), _ptr(o.get("entropy")),
+                                        _ptr(o.get("lse")), _stream(stream)))
+    return o
+
+
+# ------------------------------------------------------------------------------------------------
+# (4) loss forward + fused backward
+# ------------------------------------------------------------------------------------------------
+def otk_policy_loss_fwd_bwd(ctx: Context, logits: torch.Tensor, targets: torch.Tensor, loss_mask: torch.Tensor,
+                            row_traj: torch.Tensor, adv: torch.Tensor, old_logp: torch.Tensor,
+                            ref_logp: Optional[torch.Tensor], n_loss: torch.Tensor, cfg: LossCfg = LossCfg(), *,
+                            vocab: Optional[int] = None, dlogits: Optional[torch.Tensor] = None,
+                            logp: Optional[torch.Tensor] = None, entropy: Optional[torch.Tensor] = None,
+                            stats: Optional[torch.Tensor] = None, accumulate: Optional[bool] = None,
+                            want_logp: bool = True, stream=None) -> dict:
+    _dev(logits, "logits")
+    N, ld = logits.shape
+    V = ld if vocab is None else int(vocab)
+    dev = logits.device
+    if dlogits is None:
+        dlogits = torch.empty_like(logits)
+    if want_logp and logp is None:
+        logp = torch.empty(N, dtype=torch.float32, device=dev)
+    if want_logp and entropy is None:
+        entropy = torch.empty(N, dtype=torch.float32, device=dev)
+    if stats is None:
+        stats = torch.zeros(len(STATS_FIELDS), dtype=torch.float64, device=dev)
+    c = cfg.c(accumulate)
+    _check(_lib.otk_policy_loss_fwd_bwd(ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits), _ptr(targets),
+                                        _ptr(loss_mask), _ptr(row_traj), _ptr(adv), _ptr(old_logp),
+                                        _ptr(ref_logp), _ptr(n_loss), C.byref(c), _ptr(dlogits), _ptr(logp),
+                                        _ptr(entropy), _ptr(stats), _stream(stream)))
+    return dict(dlogits=dlogits, logp=logp, entropy=entropy, stats=stats)
+
+
+def otk_policy_loss_fwd_bwd_host(ctx: Context, logits: torch.Tensor, targets, loss_mask, row_traj, adv, old_logp,
+                                 ref_logp, n_loss: int, cfg: LossCfg = LossCfg(), *, vocab: Optional[int] = None,
+                                 dlogits: Optional[torch.Tensor] = None, rows_per_chunk: int = 4096):
+    """Host-buffer entry point: every tensor is a CPU (ideally pinned) tensor; returns the stats dict."""
+    for t in (logits, targets, loss_mask, row_traj, adv, old_logp):
+        if t.is_cuda:
+            raise ValueError("host entry point takes CPU tensors")
+    N, ld = logits.shape
+    V = ld if vocab is None else int(vocab)
+    stats = (C.c_double * len(STATS_FIELDS))()
+    c = cfg.c(False)
+    _check(_lib.otk_policy_loss_fwd_bwd_host(ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits), _ptr(targets),
+                                             _ptr(loss_mask), _ptr(row_traj), int(adv.numel()), _ptr(adv),
+                                             _ptr(old_logp), _ptr(ref_logp), int(n_loss), C.byref(c),
+                                             _ptr(dlogits), C.cast(stats, C.c_void_p), int(rows_per_chunk)))
+    return dict(zip(STATS_FIELDS, list(stats)))
+
+
+def stats_dict(stats: torch.Tensor) -> dict:
+    return dict(zip(STATS_FIELDS, stats.detach().cpu().tolist()))
+
+
+# ------------------------------------------------------------------------------------------------
+# vocab sharding
+# ------------------------------------------------------------------------------------------------
+def otk_row_partials(ctx: Context, logits: torch.Tensor, targets: torch.Tensor, vocab_start: int, vocab_total: int,
+                     *, vocab_local: Optional[int] = None, row_mask: Optional[torch.Tensor] = None,
+                     logit_scale: float = 1.0, partials: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    _dev(logits, "logits")
+    N, ld = logits.shape
+    V = ld if vocab_local is None else int(vocab_local)
+    if partials is None:
+        partials = torch.empty((N, 4), dtype=torch.float32, device=logits.device)
+    sh = otk_vocab_shard(int(vocab_start), int(vocab_total))
+    _check(_lib.otk_row_partials(ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits), _ptr(targets),
+                                 _ptr(row_mask), C.byref(sh), float(logit_scale), _ptr(partials), _stream(stream)))
+    return partials
+
+
+def otk_logprob_entropy_combine(ctx: Context, partials: torch.Tensor, *, row_mask: Optional[torch.Tensor] = None,
+                                want_lse: bool = False, stream=None) -> dict:
+    """partials: [nshards, N, 4] float32 (rank order)."""
+    _dev(partials, "partials")
+    P, N, _ = partials.shape
+    dev = partials.device
+    o = dict(logp=torch.empty(N, dtype=torch.float32, device=dev),
+             entropy=torch.empty(N, dtype=torch.float32, device=dev))
+    if want_lse:
+        o["lse"] = torch.empty(N, dtype=torch.float32, device=dev)
+    _check(_lib.otk_logprob_entropy_combine(ctx.handle, N, P, _ptr(partials), _ptr(row_mask), _ptr(o["logp"]),
+                                            _ptr(o["entropy"]), _ptr(o.get("lse")), _stream(stream)))
+    return o
+
+
+def otk_policy_loss_fwd_bwd_partials(ctx: Context, logits: torch.Tensor, targets, loss_mask, row_traj, adv,
+                                     old_logp, ref_logp, n_loss, cfg: LossCfg, vocab_start: int, vocab_total: int,
+                                     partials: torch.Tensor, *, vocab_local: Optional[int] = None,
+                                     dlogits: Optional[torch.Tensor] = None, logp=None, entropy=None, stats=None,
+                                     accumulate: Optional[bool] = None, stream=None) -> dict:
+    _dev(logits, "logits")
+    N, ld = logits.shape
+    V = ld if vocab_local is None else int(vocab_local)
+    dev = logits.device
+    if dlogits is None:
+        dlogits = torch.empty_like(logits)
+    if logp is None:
+        logp = torch.empty(N, dtype=torch.float32, device=dev)
+    if entropy is None:
+        entropy = torch.empty(N, dtype=torch.float32, device=dev)
+    if stats is None:
+        stats = torch.zeros(len(STATS_FIELDS), dtype=torch.float64, device=dev)
+    sh = otk_vocab_shard(int(vocab_start), int(vocab_total))
+    c = cfg.c(accumulate)
+    _check(_lib.otk_policy_loss_fwd_bwd_partials(
+        ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits), _ptr(targets), _ptr(loss_mask), _ptr(row_traj),
+        _ptr(adv), _ptr(old_logp), _ptr(ref_logp), _ptr(n_loss), C.byref(c), C.byref(sh), int(partials.shape[0]),
+        _ptr(partials), _ptr(dlogits), _ptr(logp), _ptr(entropy), _ptr(stats), _stream(stream)))
+    return dict(dlogits=dlogits, logp=logp, entropy=entropy, stats=stats)
+
+
+__all__ = [n for n in list(globals()) if n.startswith("otk_") or n in (
+    "Context", "LossCfg", "OtkError", "DeviceTrajBatch", "traj_batch_to_device", "stats_dict", "EXPORTED")]

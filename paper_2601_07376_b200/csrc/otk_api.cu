@@ -1,0 +1,475 @@
+// otk_api.cu — the C ABI (include/otk.h): argument validation, ctx ownership, launches, and the
+// host-buffer streaming executor used for the end-to-end measurement.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "otk_internal.h"
+
+namespace {
+
+thread_local std::string tl_err;
+
+otk_status fail(otk_status s, const std::string& msg) {
+  tl_err = msg;
+  return s;
+}
+
+otk_status cuda_fail(cudaError_t e, const char* where) {
+  tl_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return OTK_ERR_CUDA;
+}
+
+#define OTK_REQUIRE(cond, code, msg) \
+  do {                               \
+    if (!(cond)) return fail(code, msg); \
+  } while (0)
+
+#define OTK_CUDA(call, where)                      \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+size_t dtype_size(otk_dtype d) { return d == OTK_BF16 ? 2 : 4; }
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Cluster size for the row kernels: the smallest power of two whose per-CTA column segment fits
+// the resident ring budget. Every mode uses the same rule so that the forward
+// (3) and the fused loss (4) reduce in the same order (bitwise-equal logp: on-policy ratio = 1).
+int choose_csize(int64_t vocab, size_t es, int* seg_elems) {
+  const int64_t budget = int64_t(otk::kSlots - otk::kMinLookahead) * otk::kChunkBytes;
+  for (int c = 1; c <= 8; c *= 2) {
+    int64_t seg = (vocab + c - 1) / c;
+    seg = (seg + 7) / 8 * 8;
+    if (seg * int64_t(es) <= budget && int64_t(c - 1) * seg < vocab) {
+      *seg_elems = int(seg);
+      return c;
+    }
+  }
+  return 0;
+}
+
+otk_status check_rows(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld, otk_dtype dtype, const void* logits,
+                      const int32_t* targets, int* csize, int* seg_elems) {
+  OTK_REQUIRE(ctx, OTK_ERR_INVALID_ARG, "ctx is NULL");
+  OTK_REQUIRE(dtype == OTK_BF16 || dtype == OTK_F32, OTK_ERR_DTYPE, "unknown dtype");
+  OTK_REQUIRE(num_rows >= 0 && vocab >= 1 && ld >= vocab, OTK_ERR_SHAPE, "need num_rows >= 0, vocab >= 1, ld >= vocab");
+  OTK_REQUIRE(logits && targets, OTK_ERR_INVALID_ARG, "logits / targets is NULL");
+  OTK_REQUIRE(aligned16(logits) && (ld * int64_t(dtype_size(dtype))) % 16 == 0, OTK_ERR_ALIGNMENT,
+              "logits base and row stride must be 16-byte aligned");
+  *csize = choose_csize(vocab, dtype_size(dtype), seg_elems);
+  OTK_REQUIRE(*csize > 0, OTK_ERR_SHAPE, "vocab too large for the row kernel (> 8 x 188 KB per row)");
+  return OTK_OK;
+}
+
+otk_status check_cfg(const otk_loss_cfg* cfg, const float* ref_logp) {
+  OTK_REQUIRE(cfg, OTK_ERR_INVALID_ARG, "cfg is NULL");
+  OTK_REQUIRE(cfg->clip_low >= 0 && cfg->clip_low < 1 && cfg->clip_high >= 0, OTK_ERR_INVALID_ARG,
+              "clip_low must be in [0,1), clip_high >= 0");
+  OTK_REQUIRE(cfg->log_ratio_clamp > 0 && std::isfinite(cfg->log_ratio_clamp), OTK_ERR_INVALID_ARG,
+              "log_ratio_clamp must be > 0");
+  OTK_REQUIRE(cfg->logit_scale > 0 && std::isfinite(cfg->logit_scale), OTK_ERR_INVALID_ARG, "logit_scale must be > 0");
+  OTK_REQUIRE(cfg->kl_beta >= 0 && std::isfinite(cfg->kl_beta), OTK_ERR_INVALID_ARG, "kl_beta must be >= 0");
+  OTK_REQUIRE(cfg->kl_type >= 1 && cfg->kl_type <= 3, OTK_ERR_INVALID_ARG, "kl_type must be 1, 2 or 3");
+  OTK_REQUIRE(cfg->kl_beta == 0 || ref_logp, OTK_ERR_INVALID_ARG, "ref_logp is required when kl_beta != 0");
+  return OTK_OK;
+}
+
+otk::RowParams base_params(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld, const void* logits,
+                           const int32_t* targets, const uint8_t* mask, float scale, int csize, int seg_elems) {
+  otk::RowParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.num_rows = num_rows;
+  p.vocab = vocab;
+  p.ld = ld;
+  p.logits = logits;
+  p.targets = targets;
+  p.mask = mask;
+  p.scale = scale;
+  p.vocab_start = 0;
+  p.vocab_total = vocab;
+  p.csize = csize;
+  p.seg_elems = seg_elems;
+  p.cta_partials = ctx->d_partials;
+  p.ticket = ctx->d_tickets + otk::kTicketRows;
+  p.err = ctx->d_err;
+  p.nshards = 0;
+  return p;
+}
+
+void set_loss(otk::RowParams& p, const int32_t* row_traj, const double* adv, const float* old_logp,
+              const float* ref_logp, const int64_t* n_loss, const otk_loss_cfg* cfg, void* dlogits, float* logp,
+              float* entropy, otk_loss_stats* stats) {
+  p.row_traj = row_traj;
+  p.adv = adv;
+  p.old_logp = old_logp;
+  p.ref_logp = cfg->kl_beta != 0 ? ref_logp : nullptr;
+  p.n_loss = n_loss;
+  p.clip_low = cfg->clip_low;
+  p.clip_high = cfg->clip_high;
+  p.kl_beta = cfg->kl_beta;
+  p.clamp = cfg->log_ratio_clamp;
+  p.kl_type = cfg->kl_type;
+  p.zero_masked = cfg->zero_masked_rows;
+  p.accumulate = cfg->accumulate_stats;
+  p.dlogits = dlogits;
+  p.logp = logp;
+  p.entropy = entropy;
+  p.stats = stats;
+}
+
+}  // namespace
+
+extern "C" {
+
+int otk_version(void) { return OTK_VERSION; }
+
+const char* otk_last_error(void) { return tl_err.c_str(); }
+
+const char* otk_status_string(otk_status s) {
+  switch (s) {
+    case OTK_OK: return "OTK_OK";
+    case OTK_ERR_INVALID_ARG: return "OTK_ERR_INVALID_ARG";
+    case OTK_ERR_SHAPE: return "OTK_ERR_SHAPE";
+    case OTK_ERR_ALIGNMENT: return "OTK_ERR_ALIGNMENT";
+    case OTK_ERR_DTYPE: return "OTK_ERR_DTYPE";
+    case OTK_ERR_EMPTY_GROUP: return "OTK_ERR_EMPTY_GROUP";
+    case OTK_ERR_UNTERMINATED: return "OTK_ERR_UNTERMINATED";
+    case OTK_ERR_BAD_TRAJECTORY: return "OTK_ERR_BAD_TRAJECTORY";
+    case OTK_ERR_TARGET_RANGE: return "OTK_ERR_TARGET_RANGE";
+    case OTK_ERR_CUDA: return "OTK_ERR_CUDA";
+    case OTK_ERR_GROUP_RANGE: return "OTK_ERR_GROUP_RANGE";
+  }
+  return "OTK_ERR_UNKNOWN";
+}
+
+otk_status otk_ctx_create(int cuda_device, otk_ctx** out) {
+  OTK_REQUIRE(out, OTK_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  int ndev = 0;
+  OTK_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  OTK_REQUIRE(cuda_device >= 0 && cuda_device < ndev, OTK_ERR_INVALID_ARG, "bad device index");
+  OTK_CUDA(cudaSetDevice(cuda_device), "cudaSetDevice");
+  otk_ctx* c = new otk_ctx();
+  c->device = cuda_device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  cudaDeviceGetAttribute(&c->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, cuda_device);
+  c->cap_returns = int64_t(1) << 20;
+  cudaError_t e = cudaMalloc(&c->d_err, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_tickets, 8 * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_partials, size_t(otk::kMaxCtas) * otk::kStatSlots * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_scratch_i64, size_t(otk::kMaxCtas) * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_returns, size_t(c->cap_returns) * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemset(c->d_err, 0, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->d_tickets, 0, 8 * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    otk_ctx_destroy(c);
+    return cuda_fail(e, "otk_ctx_create");
+  }
+  if (c->max_smem_optin < int(otk::kSlots * otk::kChunkBytes + 1024)) {
+    otk_ctx_destroy(c);
+    return fail(OTK_ERR_CUDA, "device lacks the shared memory the row kernel needs (sm_100a required)");
+  }
+  *out = c;
+  return OTK_OK;
+}
+
+otk_status otk_ctx_destroy(otk_ctx* c) {
+  if (!c) return OTK_OK;
+  cudaFree(c->d_err);
+  cudaFree(c->d_tickets);
+  cudaFree(c->d_partials);
+  cudaFree(c->d_scratch_i64);
+  cudaFree(c->d_returns);
+  for (int i = 0; i < 2; ++i) cudaFree(c->stage[i]);
+  for (int i = 0; i < 4; ++i)
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->exec_stream) cudaStreamDestroy(c->exec_stream);
+  delete c;
+  return OTK_OK;
+}
+
+otk_status otk_ctx_check(otk_ctx* ctx, otk_stream_t stream) {
+  OTK_REQUIRE(ctx, OTK_ERR_INVALID_ARG, "ctx is NULL");
+  OTK_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)), "cudaStreamSynchronize");
+  int err = 0;
+  OTK_CUDA(cudaMemcpy(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost), "read error word");
+  if (err) {
+    OTK_CUDA(cudaMemset(ctx->d_err, 0, sizeof(int)), "clear error word");
+    return fail(otk_status(err), std::string("device-side data error: ") + otk_status_string(otk_status(err)));
+  }
+  return OTK_OK;
+}
+
+int64_t otk_ctx_launch_count(const otk_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+otk_status otk_build_masks(otk_ctx* ctx, const otk_traj_batch* batch, int16_t train_agent, uint8_t* loss_mask,
+                           uint8_t* response_mask, int32_t* row_traj, int64_t* traj_loss_tokens,
+                           int64_t* traj_source_counts, int64_t* n_loss, otk_stream_t stream) {
+  OTK_REQUIRE(ctx && batch, OTK_ERR_INVALID_ARG, "ctx / batch is NULL");
+  OTK_REQUIRE(batch->num_traj >= 1, OTK_ERR_EMPTY_GROUP, "num_traj < 1 (EmptyGroup)");
+  OTK_REQUIRE(batch->num_rows >= 0, OTK_ERR_SHAPE, "num_rows < 0");
+  OTK_REQUIRE(batch->tok_offsets && batch->seg_offsets && batch->seg_source && batch->seg_agent && batch->seg_len,
+              OTK_ERR_INVALID_ARG, "segment arrays must not be NULL");
+  OTK_REQUIRE(batch->num_rows == 0 || (loss_mask && row_traj), OTK_ERR_INVALID_ARG, "loss_mask / row_traj is NULL");
+  OTK_REQUIRE(traj_loss_tokens && n_loss, OTK_ERR_INVALID_ARG, "traj_loss_tokens / n_loss is NULL");
+  OTK_REQUIRE(train_agent >= -1, OTK_ERR_INVALID_ARG, "train_agent must be >= -1");
+  otk::MaskParams p;
+  p.b = *batch;
+  p.train_agent = train_agent;
+  p.loss_mask = loss_mask;
+  p.response_mask = response_mask;
+  p.row_traj = row_traj;
+  p.traj_loss_tokens = traj_loss_tokens;
+  p.traj_source_counts = traj_source_counts;
+  p.n_loss = n_loss;
+  p.ticket = ctx->d_tickets + otk::kTicketMasks;
+  p.err = ctx->d_err;
+  OTK_CUDA(otk::launch_masks(p, reinterpret_cast<cudaStream_t>(stream)), "k_build_masks launch");
+  ctx->launches += 1;
+  return OTK_OK;
+}
+
+otk_status otk_group_advantages(otk_ctx* ctx, int32_t num_traj, const int32_t* group_id, int32_t num_groups,
+                                const double* returns, const int32_t* turn_offsets, const double* turn_rewards,
+                                uint32_t flags, double std_floor, double* adv, double* returns_out,
+                                double* group_mean, double* group_std, int32_t* group_size, otk_stream_t stream) {
+  OTK_REQUIRE(ctx, OTK_ERR_INVALID_ARG, "ctx is NULL");
+  OTK_REQUIRE(num_traj >= 1, OTK_ERR_EMPTY_GROUP, "num_traj < 1 (EmptyGroup)");
+  OTK_REQUIRE(num_groups >= 1 && num_groups <= 12000, OTK_ERR_SHAPE, "num_groups must be in [1, 12000]");
+  OTK_REQUIRE(group_id && adv, OTK_ERR_INVALID_ARG, "group_id / adv is NULL");
+  OTK_REQUIRE((returns != nullptr) != (turn_offsets != nullptr), OTK_ERR_INVALID_ARG,
+              "exactly one of returns and turn_offsets must be given");
+  OTK_REQUIRE(!turn_offsets || turn_rewards, OTK_ERR_INVALID_ARG, "turn_rewards is NULL");
+  OTK_REQUIRE((flags & ~(OTK_ADV_STD_NORM | OTK_ADV_UNBIASED)) == 0, OTK_ERR_INVALID_ARG, "unknown flag bits");
+  OTK_REQUIRE(std_floor >= 0 && std::isfinite(std_floor), OTK_ERR_INVALID_ARG, "std_floor must be >= 0");
+  OTK_REQUIRE(returns_out || num_traj <= ctx->cap_returns, OTK_ERR_SHAPE, "num_traj exceeds ctx scratch");
+  otk::AdvParams p;
+  p.num_traj = num_traj;
+  p.group_id = group_id;
+  p.num_groups = num_groups;
+  p.returns = returns;
+  p.turn_offsets = turn_offsets;
+  p.turn_rewards = turn_rewards;
+  p.flags = flags;
+  p.std_floor = std_floor;
+  p.adv = adv;
+  p.returns_out = returns_out ? returns_out : ctx->d_returns;
+  p.group_mean = group_mean;
+  p.group_std = group_std;
+  p.group_size = group_size;
+  p.err = ctx->d_err;
+  OTK_CUDA(otk::launch_advantages(p, reinterpret_cast<cudaStream_t>(stream)), "k_group_advantages launch");
+  ctx->launches += 1;
+  return OTK_OK;
+}
+
+otk_status otk_logprob_entropy_fwd(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld, otk_dtype dtype,
+                                   const void* logits, const int32_t* targets, const uint8_t* row_mask,
+                                   float logit_scale, float* logp, float* entropy, float* lse, otk_stream_t stream) {
+  int csize = 0, seg = 0;
+  otk_status st = check_rows(ctx, num_rows, vocab, ld, dtype, logits, targets, &csize, &seg);
+  if (st != OTK_OK) return st;
+  OTK_REQUIRE(logp, OTK_ERR_INVALID_ARG, "logp is NULL");
+  OTK_REQUIRE(logit_scale > 0 && std::isfinite(logit_scale), OTK_ERR_INVALID_ARG, "logit_scale must be > 0");
+  if (num_rows == 0) return OTK_OK;
+  otk::RowParams p = base_params(ctx, num_rows, vocab, ld, logits, targets, row_mask, logit_scale, csize, seg);
+  p.logp = logp;
+  p.entropy = entropy;
+  p.lse = lse;
+  OTK_CUDA(otk::launch_rows(ctx, otk::kModeFwd, dtype, p, reinterpret_cast<cudaStream_t>(stream), nullptr),
+           "k_rows<fwd> launch");
+  ctx->launches += 1;
+  return OTK_OK;
+}
+
+otk_status otk_policy_loss_fwd_bwd(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld, otk_dtype dtype,
+                                   const void* logits, const int32_t* targets, const uint8_t* loss_mask,
+                                   const int32_t* row_traj, const double* adv, const float* old_logp,
+                                   const float* ref_logp, const int64_t* n_loss, const otk_loss_cfg* cfg,
+                                   void* dlogits, float* logp, float* entropy, otk_loss_stats* stats,
+                                   otk_stream_t stream) {
+  int csize = 0, seg = 0;
+  otk_status st = check_rows(ctx, num_rows, vocab, ld, dtype, logits, targets, &csize, &seg);
+  if (st != OTK_OK) return st;
+  st = check_cfg(cfg, ref_logp);
+  if (st != OTK_OK) return st;
+  OTK_REQUIRE(loss_mask && row_traj && adv && old_logp && n_loss && dlogits && stats, OTK_ERR_INVALID_ARG,
+              "loss_mask, row_traj, adv, old_logp, n_loss, dlogits and stats are required");
+  OTK_REQUIRE(dlogits != logits, OTK_ERR_INVALID_ARG, "dlogits must not alias logits");
+  OTK_REQUIRE(aligned16(dlogits), OTK_ERR_ALIGNMENT, "dlogits must be 16-byte aligned");
+  otk::RowParams p = base_params(ctx, num_rows, vocab, ld, logits, targets, loss_mask, float(cfg->logit_scale),
+                                 csize, seg);
+  set_loss(p, row_traj, adv, old_logp, ref_logp, n_loss, cfg, dlogits, logp, entropy, stats);
+  OTK_CUDA(otk::launch_rows(ctx, otk::kModeBwd, dtype, p, reinterpret_cast<cudaStream_t>(stream), nullptr),
+           "k_rows<bwd> launch");
+  ctx->launches += 1;
+  return OTK_OK;
+}
+
+otk_status otk_row_partials(otk_ctx* ctx, int64_t num_rows, int64_t vocab_local, int64_t ld, otk_dtype dtype,
+                            const void* logits, const int32_t* targets, const uint8_t* row_mask,
+                            const otk_vocab_shard* shard, float logit_scale, float* partials, otk_stream_t stream) {
+  int csize = 0, seg = 0;
+  otk_status st = check_rows(ctx, num_rows, vocab_local, ld, dtype, logits, targets, &csize, &seg);
+  if (st != OTK_OK) return st;
+  OTK_REQUIRE(shard && partials, OTK_ERR_INVALID_ARG, "shard / partials is NULL");
+  OTK_REQUIRE(shard->vocab_start >= 0 && shard->vocab_start + vocab_local <= shard->vocab_total, OTK_ERR_SHAPE,
+              "shard outside [0, vocab_total)");
+  OTK_REQUIRE(aligned16(partials), OTK_ERR_ALIGNMENT, "partials must be 16-byte aligned");
+  OTK_REQUIRE(logit_scale > 0 && std::isfinite(logit_scale), OTK_ERR_INVALID_ARG, "logit_scale must be > 0");
+  if (num_rows == 0) return OTK_OK;
+  otk::RowParams p = base_params(ctx, num_rows, vocab_local, ld, logits, targets, row_mask, logit_scale, csize, seg);
+  p.vocab_start = shard->vocab_start;
+  p.vocab_total = shard->vocab_total;
+  p.partials_out = reinterpret_cast<float4*>(partials);
+  OTK_CUDA(otk::launch_rows(ctx, otk::kModePartial, dtype, p, reinterpret_cast<cudaStream_t>(stream), nullptr),
+           "k_rows<partial> launch");
+  ctx->launches += 1;
+  return OTK_OK;
+}
+
+otk_status otk_logprob_entropy_combine(otk_ctx* ctx, int64_t num_rows, int32_t nshards, const float* partials,
+                                       const uint8_t* row_mask, float* logp, float* entropy, float* lse,
+                                       otk_stream_t stream) {
+  OTK_REQUIRE(ctx && partials && logp, OTK_ERR_INVALID_ARG, "ctx / partials / logp is NULL");
+  OTK_REQUIRE(num_rows >= 0 && nshards >= 1, OTK_ERR_SHAPE, "num_rows >= 0 and nshards >= 1 required");
+  OTK_REQUIRE(aligned16(partials), OTK_ERR_ALIGNMENT, "partials must be 16-byte aligned");
+  if (num_rows == 0) return OTK_OK;
+  OTK_CUDA(otk::launch_combine(ctx, num_rows, nshards, reinterpret_cast<const float4*>(partials), row_mask, logp,
+                               entropy, lse, reinterpret_cast<cudaStream_t>(stream)),
+           "k_combine launch");
+  ctx->launches += 1;
+  return OTK_OK;
+}
+
+otk_status otk_policy_loss_fwd_bwd_partials(otk_ctx* ctx, int64_t num_rows, int64_t vocab_local, int64_t ld,
+                                            otk_dtype dtype, const void* logits, const int32_t* targets,
+                                            const uint8_t* loss_mask, const int32_t* row_traj, const double* adv,
+                                            const float* old_logp, const float* ref_logp, const int64_t* n_loss,
+                                            const otk_loss_cfg* cfg, const otk_vocab_shard* shard, int32_t nshards,
+                                            const float* partials, void* dlogits, float* logp, float* entropy,
+                                            otk_loss_stats* stats, otk_stream_t stream) {
+  int csize = 0, seg = 0;
+  otk_status st = check_rows(ctx, num_rows, vocab_local, ld, dtype, logits, targets, &csize, &seg);
+  if (st != OTK_OK) return st;
+  st = check_cfg(cfg, ref_logp);
+  if (st != OTK_OK) return st;
+  OTK_REQUIRE(loss_mask && row_traj && adv && old_logp && n_loss && dlogits && stats && shard && partials,
+              OTK_ERR_INVALID_ARG, "a required pointer is NULL");
+  OTK_REQUIRE(nshards >= 1, OTK_ERR_SHAPE, "nshards >= 1 required");
+  OTK_REQUIRE(shard->vocab_start >= 0 && shard->vocab_start + vocab_local <= shard->vocab_total, OTK_ERR_SHAPE,
+              "shard outside [0, vocab_total)");
+  OTK_REQUIRE(dlogits != logits, OTK_ERR_INVALID_ARG, "dlogits must not alias logits");
+  OTK_REQUIRE(aligned16(dlogits) && aligned16(partials), OTK_ERR_ALIGNMENT, "dlogits / partials alignment");
+  otk::RowParams p = base_params(ctx, num_rows, vocab_local, ld, logits, targets, loss_mask,
+                                 float(cfg->logit_scale), csize, seg);
+  p.vocab_start = shard->vocab_start;
+  p.vocab_total = shard->vocab_total;
+  p.partials_in = reinterpret_cast<const float4*>(partials);
+  p.nshards = nshards;
+  set_loss(p, row_traj, adv, old_logp, ref_logp, n_loss, cfg, dlogits, logp, entropy, stats);
+  OTK_CUDA(otk::launch_rows(ctx, otk::kModeBwdPartials, dtype, p, reinterpret_cast<cudaStream_t>(stream), nullptr),
+           "k_rows<bwd_partials> launch");
+  ctx->launches += 1;
+  return OTK_OK;
+}
+
+// ---- host-buffer streaming executor (e2e measurement) -------------------------------------------------
+otk_status otk_policy_loss_fwd_bwd_host(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld, otk_dtype dtype,
+                                        const void* logits_host, const int32_t* targets_host,
+                                        const uint8_t* loss_mask_host, const int32_t* row_traj_host, int32_t num_traj,
+                                        const double* adv_host, const float* old_logp_host,
+                                        const float* ref_logp_host, int64_t n_loss, const otk_loss_cfg* cfg,
+                                        void* dlogits_host, otk_loss_stats* stats_host, int64_t rows_per_chunk) {
+  int csize = 0, seg = 0;
+  otk_status st = check_rows(ctx, num_rows, vocab, ld, dtype, logits_host, targets_host, &csize, &seg);
+  if (st != OTK_OK) return st;
+  st = check_cfg(cfg, ref_logp_host);
+  if (st != OTK_OK) return st;
+  OTK_REQUIRE(loss_mask_host && row_traj_host && adv_host && old_logp_host && stats_host && num_traj >= 1,
+              OTK_ERR_INVALID_ARG, "a required host pointer is NULL");
+  OTK_REQUIRE(rows_per_chunk >= 1, OTK_ERR_SHAPE, "rows_per_chunk >= 1 required");
+  const size_t es = dtype_size(dtype);
+  const size_t row_bytes = size_t(ld) * es;
+  const bool has_ref = cfg->kl_beta != 0;
+  // staging layout per buffer: logits | dlogits | targets | mask | row_traj | old | ref
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t R = size_t(rows_per_chunk);
+  const size_t off_dl = al(R * row_bytes);
+  const size_t off_tg = off_dl + al(R * row_bytes);
+  const size_t off_m = off_tg + al(R * 4);
+  const size_t off_rt = off_m + al(R);
+  const size_t off_old = off_rt + al(R * 4);
+  const size_t off_ref = off_old + al(R * 4);
+  const size_t off_end = off_ref + al(R * 4);
+  const size_t shared_bytes = al(size_t(num_traj) * 8) + al(8) + al(sizeof(otk_loss_stats));
+  const size_t need = off_end + shared_bytes;
+  if (ctx->stage_bytes < need) {
+    for (int i = 0; i < 2; ++i) {
+      cudaFree(ctx->stage[i]);
+      ctx->stage[i] = nullptr;
+    }
+    ctx->stage_bytes = 0;
+    for (int i = 0; i < 2; ++i) OTK_CUDA(cudaMalloc(&ctx->stage[i], need), "staging cudaMalloc");
+    ctx->stage_bytes = need;
+  }
+  if (!ctx->copy_stream) OTK_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "stream");
+  if (!ctx->exec_stream) OTK_CUDA(cudaStreamCreateWithFlags(&ctx->exec_stream, cudaStreamNonBlocking), "stream");
+  for (int i = 0; i < 4; ++i)
+    if (!ctx->ev[i]) OTK_CUDA(cudaEventCreateWithFlags(&ctx->ev[i], cudaEventDisableTiming), "event");
+  cudaStream_t cs = ctx->copy_stream, xs = ctx->exec_stream;
+  char* shared = reinterpret_cast<char*>(ctx->stage[0]) + off_end;  // adv | n_loss | stats live in buffer 0
+  double* d_adv = reinterpret_cast<double*>(shared);
+  int64_t* d_nl = reinterpret_cast<int64_t*>(shared + al(size_t(num_traj) * 8));
+  otk_loss_stats* d_stats = reinterpret_cast<otk_loss_stats*>(shared + al(size_t(num_traj) * 8) + al(8));
+  OTK_CUDA(cudaMemcpyAsync(d_adv, adv_host, size_t(num_traj) * 8, cudaMemcpyHostToDevice, xs), "H2D adv");
+  OTK_CUDA(cudaMemcpyAsync(d_nl, &n_loss, 8, cudaMemcpyHostToDevice, xs), "H2D n_loss");
+  OTK_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(otk_loss_stats), xs), "zero stats");
+  OTK_CUDA(cudaStreamSynchronize(xs), "sync");  // n_loss lives on the host stack
+  int64_t k = 0;
+  for (int64_t r0 = 0; r0 < num_rows || (num_rows == 0 && k == 0); r0 += rows_per_chunk, ++k) {
+    const int b = int(k & 1);
+    const int64_t n = std::min<int64_t>(rows_per_chunk, num_rows - r0);
+    char* sb = reinterpret_cast<char*>(ctx->stage[b]);
+    if (k >= 2) OTK_CUDA(cudaStreamWaitEvent(cs, ctx->ev[2 + b], 0), "wait free");
+    if (n > 0) {
+      OTK_CUDA(cudaMemcpyAsync(sb, reinterpret_cast<const char*>(logits_host) + size_t(r0) * row_bytes,
+                               size_t(n) * row_bytes, cudaMemcpyHostToDevice, cs), "H2D logits");
+      OTK_CUDA(cudaMemcpyAsync(sb + off_tg, targets_host + r0, size_t(n) * 4, cudaMemcpyHostToDevice, cs), "H2D");
+      OTK_CUDA(cudaMemcpyAsync(sb + off_m, loss_mask_host + r0, size_t(n), cudaMemcpyHostToDevice, cs), "H2D");
+      OTK_CUDA(cudaMemcpyAsync(sb + off_rt, row_traj_host + r0, size_t(n) * 4, cudaMemcpyHostToDevice, cs), "H2D");
+      OTK_CUDA(cudaMemcpyAsync(sb + off_old, old_logp_host + r0, size_t(n) * 4, cudaMemcpyHostToDevice, cs), "H2D");
+      if (has_ref)
+        OTK_CUDA(cudaMemcpyAsync(sb + off_ref, ref_logp_host + r0, size_t(n) * 4, cudaMemcpyHostToDevice, cs), "H2D");
+    }
+    OTK_CUDA(cudaEventRecord(ctx->ev[b], cs), "record ready");
+    OTK_CUDA(cudaStreamWaitEvent(xs, ctx->ev[b], 0), "wait ready");
+    otk_loss_cfg c2 = *cfg;
+    c2.accumulate_stats = 1;
+    st = otk_policy_loss_fwd_bwd(ctx, std::max<int64_t>(n, 0), vocab, ld, dtype, sb,
+                                 reinterpret_cast<const int32_t*>(sb + off_tg),
+                                 reinterpret_cast<const uint8_t*>(sb + off_m),
+                                 reinterpret_cast<const int32_t*>(sb + off_rt), d_adv,
+                                 reinterpret_cast<const float*>(sb + off_old),
+                                 has_ref ? reinterpret_cast<const float*>(sb + off_ref) : nullptr, d_nl, &c2,
+                                 sb + off_dl, nullptr, nullptr, d_stats, reinterpret_cast<otk_stream_t>(xs));
+    if (st != OTK_OK) return st;
+    if (dlogits_host && n > 0)
+      OTK_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(dlogits_host) + size_t(r0) * row_bytes, sb + off_dl,
+                               size_t(n) * row_bytes, cudaMemcpyDeviceToHost, xs), "D2H dlogits");
+    OTK_CUDA(cudaEventRecord(ctx->ev[2 + b], xs), "record free");
+    if (num_rows == 0) break;
+  }
+  OTK_CUDA(cudaMemcpyAsync(stats_host, d_stats, sizeof(otk_loss_stats), cudaMemcpyDeviceToHost, xs), "D2H stats");
+  OTK_CUDA(cudaStreamSynchronize(xs), "sync exec");
+  return OTK_OK;
+}
+
+}  // extern "C"

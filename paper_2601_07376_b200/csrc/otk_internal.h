@@ -1,0 +1,126 @@
+// otk_internal.h — the ctx object and the kernel parameter blocks shared by the .cu files.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/otk.h"
+
+struct otk_ctx {
+  int device = 0;
+  int num_sms = 0;
+  int max_smem_optin = 0;
+  int* d_err = nullptr;            // sticky device error word (first otk_status != OK wins)
+  unsigned int* d_tickets = nullptr;  // [8] last-CTA tickets (one per kernel family)
+  double* d_partials = nullptr;    // [kMaxCtas * kStatSlots] per-CTA deterministic partials
+  int64_t* d_scratch_i64 = nullptr;  // [kMaxCtas] per-CTA integer partials
+  double* d_returns = nullptr;     // [cap_returns] scratch for otk_group_advantages
+  int64_t cap_returns = 0;
+  // staging for the host entry point (allocated lazily, reused)
+  void* stage[2] = {nullptr, nullptr};
+  size_t stage_bytes = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaStream_t exec_stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t launches = 0;
+};
+
+namespace otk {
+
+constexpr int kMaxCtas = 1024;
+constexpr int kStatSlots = 8;
+enum Ticket { kTicketMasks = 0, kTicketRows = 1 };
+
+// Fused row kernel configuration.
+constexpr int kChunkBytes = 8192;        // one bulk-TMA transfer / ring slot
+constexpr int kSlots = 27;               // ring depth: 216 KB of shared memory per CTA
+constexpr int kConsumerWarps = 8;        // 256 compute threads
+constexpr int kThreads = 32 * (1 + kConsumerWarps);  // + 1 producer warp
+constexpr int kMinLookahead = 4;         // slots kept free for the next row in resident (BWD) mode
+
+enum RowMode : int {
+  kModeFwd = 0,       // (3): logp / entropy / lse
+  kModePartial = 1,   // vocab shard pass 1: per-row (m2, s, t2, zy)
+  kModeBwd = 2,       // (4): pass 1 + loss + pass 2 from the SMEM-resident row segment
+  kModeBwdPartials = 3  // (4) on a vocab shard: stats from gathered partials, streaming pass 2
+};
+
+struct RowParams {
+  int64_t num_rows;
+  int64_t vocab;         // columns of this call (local vocab under sharding)
+  int64_t ld;            // row stride in elements
+  const void* logits;
+  const int32_t* targets;
+  const uint8_t* mask;   // row_mask (FWD/PARTIAL) or loss_mask (BWD); may be NULL in FWD/PARTIAL
+  float scale;           // logit scale s
+  int64_t vocab_start;   // global column of local column 0
+  int64_t vocab_total;   // global vocabulary (target range check)
+  int seg_elems;         // per-CTA column segment (multiple of 8) when the cluster splits a row
+  int csize;             // CTAs per row (cluster size)
+  // forward outputs
+  float* logp;
+  float* entropy;
+  float* lse;
+  float4* partials_out;
+  // partial-combine input
+  const float4* partials_in;  // [nshards][num_rows]
+  int nshards;
+  // loss
+  const int32_t* row_traj;
+  const double* adv;
+  const float* old_logp;
+  const float* ref_logp;
+  const int64_t* n_loss;
+  double clip_low, clip_high, kl_beta, clamp;
+  int kl_type;
+  int zero_masked;
+  int accumulate;
+  void* dlogits;
+  otk_loss_stats* stats;
+  // ctx scratch
+  double* cta_partials;
+  unsigned int* ticket;
+  int* err;
+};
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const RowParams& p, cudaStream_t s,
+                        int* grid_out);
+cudaError_t launch_combine(const otk_ctx* ctx, int64_t num_rows, int nshards, const float4* partials,
+                           const uint8_t* row_mask, float* logp, float* entropy, float* lse, cudaStream_t s);
+
+struct MaskParams {
+  otk_traj_batch b;
+  int16_t train_agent;
+  uint8_t* loss_mask;
+  uint8_t* response_mask;
+  int32_t* row_traj;
+  int64_t* traj_loss_tokens;
+  int64_t* traj_source_counts;
+  int64_t* n_loss;
+  unsigned int* ticket;
+  int* err;
+};
+cudaError_t launch_masks(const MaskParams& p, cudaStream_t s);
+
+struct AdvParams {
+  int32_t num_traj;
+  const int32_t* group_id;
+  int32_t num_groups;
+  const double* returns;
+  const int32_t* turn_offsets;
+  const double* turn_rewards;
+  uint32_t flags;
+  double std_floor;
+  double* adv;
+  double* returns_out;   // never NULL here (ctx scratch when the caller passed NULL)
+  double* group_mean;
+  double* group_std;
+  int32_t* group_size;
+  int* err;
+};
+cudaError_t launch_advantages(const AdvParams& p, cudaStream_t s);
+
+__device__ __forceinline__ void set_error(int* err, int code) { atomicCAS(err, 0, code); }
+
+}  // namespace otk
