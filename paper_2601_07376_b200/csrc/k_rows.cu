@@ -32,21 +32,25 @@ struct Stat {
   float m, s, t;
 };
 
+// combine / finalize use explicitly rounded ops (__fmul_rn / __fadd_rn are never contracted into
+// FMAs), so every template instantiation and every CTA produces bitwise-identical row statistics:
+// the fwd pool's logp (3) equals the logp recomputed inside the loss (4), making the on-policy ratio
+// exactly 1, and all ranks of a vocab shard agree.
 __device__ __forceinline__ Stat combine(const Stat a, const Stat b) {
   const float M = fmaxf(a.m, b.m);
   if (M == -INFINITY) return a;
   float sa = 0.f, ta = 0.f, sb = 0.f, tb = 0.f;
   if (a.m != -INFINITY) {
-    const float d = a.m - M, f = ex2(d);
-    sa = a.s * f;
-    ta = f * fmaf(d, a.s, a.t);
+    const float d = __fsub_rn(a.m, M), f = ex2(d);
+    sa = __fmul_rn(a.s, f);
+    ta = __fmul_rn(f, __fmaf_rn(d, a.s, a.t));
   }
   if (b.m != -INFINITY) {
-    const float d = b.m - M, f = ex2(d);
-    sb = b.s * f;
-    tb = f * fmaf(d, b.s, b.t);
+    const float d = __fsub_rn(b.m, M), f = ex2(d);
+    sb = __fmul_rn(b.s, f);
+    tb = __fmul_rn(f, __fmaf_rn(d, b.s, b.t));
   }
-  return Stat{M, sa + sb, ta + tb};
+  return Stat{M, __fadd_rn(sa, sb), __fadd_rn(ta, tb)};
 }
 
 struct RowStats {
@@ -59,10 +63,10 @@ struct RowStats {
 __device__ __forceinline__ RowStats finalize(const Stat t, const float zy) {
   RowStats r;
   const float lg2S = lg2(t.s);
-  r.L2 = t.m + lg2S;
-  r.lse = r.L2 * kLn2;
-  r.logp = zy - r.lse;
-  r.H = kLn2 * (lg2S - t.t / t.s);
+  r.L2 = __fadd_rn(t.m, lg2S);
+  r.lse = __fmul_rn(r.L2, kLn2);
+  r.logp = __fsub_rn(zy, r.lse);
+  r.H = __fmul_rn(kLn2, __fsub_rn(lg2S, __fdiv_rn(t.t, t.s)));
   return r;
 }
 
@@ -285,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows(const RowParams p) {
               for (int i = 0; i < EV; ++i)
                 if (vcol + i < c1) mx = fmaxf(mx, x[i]);
             }
-            if (uint64_t(yl - vcol) < uint64_t(EV) && yl < c1) S.zy = p.scale * VT::load1(buf, yl - cbase);
+            if (uint64_t(yl - vcol) < uint64_t(EV) && yl < c1) S.zy = __fmul_rn(p.scale, VT::load1(buf, yl - cbase));
           }
           if (mx > -INFINITY) {
             const float mn = fmaxf(st.m, mx * s2);
@@ -297,6 +301,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows(const RowParams p) {
               }
               st.m = mn;
             }
+            // chunk-local partial sums (short fp32 accumulation chains), then one add per chunk
+            float cs = 0.f, ctt = 0.f;
 #pragma unroll
             for (int k = 0; k < VPT; ++k) {
               const int64_t vcol = cbase + int64_t(ct + k * NCT) * EV;
@@ -307,8 +313,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows(const RowParams p) {
                 for (int i = 0; i < EV; ++i) {
                   const float d = fmaxf(fmaf(x[i], s2, -st.m), -FLT_MAX);
                   const float e = ex2(d);
-                  st.s += e;
-                  st.t = fmaf(e, d, st.t);
+                  cs += e;
+                  ctt = fmaf(e, d, ctt);
                 }
               } else if (vcol < c1) {
 #pragma unroll
@@ -316,12 +322,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows(const RowParams p) {
                   if (vcol + i < c1) {
                     const float d = fmaxf(fmaf(x[i], s2, -st.m), -FLT_MAX);
                     const float e = ex2(d);
-                    st.s += e;
-                    st.t = fmaf(e, d, st.t);
+                    cs += e;
+                    ctt = fmaf(e, d, ctt);
                   }
                 }
               }
             }
+            st.s += cs;
+            st.t += ctt;
           }
           if (!kResident) {
             __syncwarp();

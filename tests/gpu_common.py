@@ -52,14 +52,37 @@ def near_kink(logp, old, ref, A, cfg, eps=1e-4):
             or (ref is not None and abs(abs(ref - logp) - cfg.log_ratio_clamp) < eps))
 
 
-def check_dlogits_rows(got, want, coef, rows, dtype, V):
-    """|d| <= rel*|ref| + 1e-5*|coef_j| per element (DESIGN.md §6 tolerance)."""
+def coef_sensitivity(logp, old, ref, A, N, cfg):
+    """|d coef_j / d logp_j| from oracle quantities: coef = -s (m/N) G(logp) with dG/dlogp = -A r
+    (unclipped) + beta * (k3: e^d, k1: 0, k2: 1). The kernel's fp32 logp carries ~1e-6 absolute error,
+    so coef inherits |dcoef/dlogp| * dlogp of ABSOLUTE error even when coef itself is tiny (G can cancel)."""
+    C = cfg.log_ratio_clamp
+    r = math.exp(max(min(logp - old, C), -C))
+    s = cfg.logit_scale
+    dg = abs(A) * r
+    if cfg.kl_beta:
+        if cfg.kl_type == 3:
+            dg += cfg.kl_beta * math.exp(max(min(ref - logp, C), -C))
+        elif cfg.kl_type == 2:
+            dg += cfg.kl_beta
+    return s * dg / max(N, 1)
+
+
+def check_dlogits_rows(got, want, coef, rows, dtype, V, dcoef=None, logp_err=1e-5):
+    """|d| <= rel*|ref| + 1e-5*|coef_j| + logp_err*|dcoef_j/dlogp_j| per element."""
     rel = BF16_REL if dtype == "bf16" else F32_REL
     worst = 0.0
     for j in rows:
         g = got[j, :V].double().cpu().numpy() if isinstance(got, torch.Tensor) else got[j]
         w = want[j]
-        tol = rel * np.abs(w) + COEF_ABS * abs(coef[j]) + 1e-30
+        floor = COEF_ABS * abs(coef[j]) + (logp_err * dcoef[j] if dcoef is not None else 0.0)
+        tol = rel * np.abs(w) + floor + 1e-30
         ratio = float(np.max(np.abs(g - w) / tol))
         worst = max(worst, ratio)
     return worst
+
+
+def dcoef_rows(h, want_logp, cfg, N, beta):
+    return {j: coef_sensitivity(want_logp[j], h["old"][j], h["ref"][j] if beta else 0.0,
+                                h["adv"][h["row_traj"][j]], N, cfg)
+            for j in range(len(h["mask"])) if h["mask"][j]}

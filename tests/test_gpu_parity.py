@@ -2,7 +2,8 @@
 
 Tolerances (north_star, DESIGN.md §3/§6): masks / row_traj / counts / group sizes bit-exact;
 advantages 1e-6 abs; logp / entropy 2e-3 abs for bf16 logits (1e-5 for fp32); loss 1e-4 relative to
-max(|loss|, sum m|L|/N); dlogits |d| <= 2^-7 |ref| + 1e-5 |coef_j| (bf16), 1e-5 |ref| + 1e-5 |coef_j| (fp32).
+max(|loss|, sum m|L|/N); dlogits |d| <= rho |ref| + 1e-5 (|coef_j| + |dcoef_j/dlogp_j|) with rho = 2^-7 (bf16
+output) or 1e-5 (fp32): the second term is the absolute error coef inherits from fp32 logp.
 """
 import math
 
@@ -12,7 +13,7 @@ import torch
 
 from oracle import oracle_ref as O
 from synth import CONFIGS, make_batch
-from tests.gpu_common import LOGP_TOL, check_dlogits_rows, near_kink, oracle_cfg, row_problem
+from tests.gpu_common import LOGP_TOL, check_dlogits_rows, dcoef_rows, near_kink, oracle_cfg, row_problem
 
 pytestmark = pytest.mark.gpu
 
@@ -180,7 +181,8 @@ def test_policy_loss_fwd_bwd(otk, ctx, V, ld, dtype, n, beta, kl_type, scale, ze
                                                                h["ref"][j] if beta else None,
                                                                h["adv"][h["row_traj"][j]], ocfg)}
     rows = [j for j in range(n) if h["mask"][j] and j not in kinks]
-    assert check_dlogits_rows(got["dlogits"], want["dlogits"], want["coef"], rows, dtype, V) <= 1.0
+    dc = dcoef_rows(h, want["logp"], ocfg, N, beta)
+    assert check_dlogits_rows(got["dlogits"], want["dlogits"], want["coef"], rows, dtype, V, dc) <= 1.0
     masked = [j for j in range(n) if not h["mask"][j]]
     gd = got["dlogits"].float().cpu()
     if zero_masked:
@@ -323,7 +325,8 @@ def test_vocab_sharded_equals_oracle(otk, ctx, P, V, dtype):
     ctx.check()
     assert len(set(losses)) == 1                       # identical on every shard
     rows = [j for j in range(n) if h["mask"][j]]
-    assert check_dlogits_rows(dl, wl["dlogits"], wl["coef"], rows, dtype, V) <= 1.0
+    dc = dcoef_rows(h, wl["logp"], oracle_cfg(cfg), N, True)
+    assert check_dlogits_rows(dl, wl["dlogits"], wl["coef"], rows, dtype, V, dc) <= 1.0
     assert abs(losses[0] - wl["loss"]) <= 1e-4 * max(abs(wl["loss"]), 1e-3)
 
 
