@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""bench.py — one training step of the otk hot path (north_star (1)-(4)) on synthetic trajectories.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl otk|reference] [--config math]
+
+A step = otk_build_masks + otk_group_advantages + otk_policy_loss_fwd_bwd over every micro-batch of
+the batch (A3 runs fused inside A4), on BASELINE.json configs[1] ("math": 512 trajectories x T=2048,
+V=151936 bf16 logits, N = 2^20 rows) per GPU. Under torchrun (N > 1) each rank holds its own 512
+trajectories (weak scaling) and the step adds the batch-sharding exchanges (all-reduce of the token
+count, all-gather of group returns, all-reduce of the loss statistics).
+Prints ONE JSON line on rank 0 (schema: the driver's bench contract).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "logit-tokens/s for fused logprob+GRPO loss fwd+bwd (V=151936), % HBM peak, 1/2/4/8 GPU"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="otk", choices=["otk", "reference"])
+    ap.add_argument("--config", default="math")
+    ap.add_argument("--micro-rows", type=int, default=65536)
+    ap.add_argument("--logit-buffers", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------------------
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist.group.WORLD
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local, pg
+
+
+class ClockSampler:
+    """Samples SM clock and clock-event reasons with NVML during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clocks"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.stop = [], set(), threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml-unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------------------------------------
+def build_workload(args, rank, world, device):
+    """Synthetic inputs (untimed): this rank's trajectories, cycled logits buffers, per-row old/ref."""
+    import paper_2601_07376_b200 as otk
+    from synth import CONFIGS, make_batch, make_logits, make_noise
+    cfgw = CONFIGS[args.config]
+    tb = make_batch(args.config, seed=cfgw.seed + 1000 * rank)
+    tb.group_id = tb.group_id + np.int32(rank * cfgw.num_groups)   # this rank's groups (global ids)
+    N, V = tb.num_rows, cfgw.V
+    M = min(args.micro_rows, N)
+    ctx = otk.Context(torch.cuda.current_device())
+    dbatch = otk.traj_batch_to_device(tb, device)
+    gid = torch.from_numpy(tb.group_id).to(device)
+    toff = torch.from_numpy(tb.turn_offsets).to(device)
+    trew = torch.from_numpy(tb.turn_rewards).to(device)
+    nbuf = max(1, min(args.logit_buffers, (N + M - 1) // M))
+    bufs, tgts = [], []
+    for k in range(nbuf):
+        lg, tg = make_logits(M, V, dtype=cfgw.dtype, seed=cfgw.seed * 100 + 10 * rank + k, device=device,
+                             rows_per_chunk=4096)
+        bufs.append(lg)
+        tgts.append(tg)
+    dlogits = torch.empty_like(bufs[0])
+    # old/ref = the fwd pool's log-probs (otk_logprob_entropy_fwd) + synth noise, per micro-batch
+    base_logp = [otk.otk_logprob_entropy_fwd(ctx, b, t)["logp"] for b, t in zip(bufs, tgts)]
+    from paper_2601_07376_b200.step import MicroBatch
+    mbs = []
+    for i, r0 in enumerate(range(0, N, M)):
+        r1 = min(N, r0 + M)
+        n = r1 - r0
+        k = i % nbuf
+        old = base_logp[k][:n] + make_noise(n, 0.05, 7000 + i, device=device)
+        ref = base_logp[k][:n] + make_noise(n, 0.1, 9000 + i, device=device) if cfgw.kl_beta else None
+        mbs.append(MicroBatch(r0, r1, bufs[k][:n], tgts[k][:n], old.contiguous(),
+                              None if ref is None else ref.contiguous(), dlogits[:n]))
+    ctx.check()
+    return dict(otk=otk, cfgw=cfgw, tb=tb, ctx=ctx, dbatch=dbatch, gid=gid, toff=toff, trew=trew, bufs=bufs,
+                tgts=tgts, mbs=mbs, N=N, V=V, M=M, dlogits=dlogits)
+
+
+def algorithmic_bytes(V, n_train, n_masked, beta):
+    """a trainable row reads + writes the V-wide bf16 row plus its side data
+    (target 4, mask 1, row_traj 4, old 4, ref 4 if beta > 0); a masked row is only zero-filled (+ mask 1)."""
+    side = 4 + 1 + 4 + 4 + (4 if beta else 0)
+    return n_train * (4 * V + side) + n_masked * (2 * V + 1)
+
+
+def run_otk(args):
+    world, rank, local, pg = dist_setup(args)
+    device = torch.device("cuda", torch.cuda.current_device())
+    W = build_workload(args, rank, world, device)
+    otk, ctx = W["otk"], W["ctx"]
+    from paper_2601_07376_b200.step import PolicyLossStep
+    cfgw = W["cfgw"]
+    cfg = otk.LossCfg(kl_beta=cfgw.kl_beta)
+    step = PolicyLossStep(ctx, W["dbatch"], W["gid"], cfgw.num_groups * world if pg else cfgw.num_groups,
+                          W["toff"], W["trew"], W["V"], cfg, process_group=pg,
+                          global_num_traj=[W["tb"].num_traj] * world if pg else None,
+                          global_num_groups=cfgw.num_groups * world if pg else None)
+    if pg is None:
+        step.num_groups = cfgw.num_groups
+    stream = torch.cuda.current_stream()
+    nmb = len(W["mbs"])
+    # CUDA events around every loss launch of every timed step, on the launching stream
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nmb)]
+          for _ in range(args.steps)]
+    cur = {"s": 0}
+
+    def on_launch(k, what):
+        ev[cur["s"]][k][0 if what == "begin" else 1].record(stream)
+
+    def barrier():
+        if pg is not None:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step.run(W["mbs"])
+    ctx.check()
+    barrier()
+    launches0 = ctx.launches
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for s in range(args.steps):
+            cur["s"] = s
+            step.run(W["mbs"], on_launch=on_launch)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    k4_ms_all = [[a.elapsed_time(b) for a, b in row] for row in ev]
+    k4_ms = [sum(r[k] for r in k4_ms_all) / args.steps for k in range(nmb)]
+    barrier()
+    launches = ctx.launches - launches0
+    elapsed = t0.elapsed_time(t1)
+    if pg is not None:
+        import torch.distributed as dist
+        t = torch.tensor([elapsed], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    ms_per_step = elapsed / args.steps
+    stats = otk.stats_dict(step.stats)
+    ctx.check()
+
+    # masks / token counts for the roofline bytes (from the device outputs; one D2H after timing)
+    lm = step.masks["loss_mask"]
+    n_train = [int(lm[mb.r0:mb.r1].sum()) for mb in W["mbs"]]
+    n_rows = [mb.r1 - mb.r0 for mb in W["mbs"]]
+    bytes_k4 = [algorithmic_bytes(W["V"], t, r - t, cfgw.kl_beta) for t, r in zip(n_train, n_rows)]
+    avg_bytes = sum(bytes_k4) / nmb
+    avg_ms = sum(k4_ms) / nmb
+    achieved = avg_bytes / (avg_ms * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    total_rows = W["N"] * world
+    value = total_rows / (ms_per_step * 1e-3)
+    step_bytes = sum(bytes_k4)
+    res = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": cfgw.dtype, "data": "synthetic (seeded; SURVEY.md §8(d) recipe)",
+        "config": {"workload": f"{args.config}: {cfgw.note}", "global_batch_traj": W["tb"].num_traj * world,
+                   "rows_per_gpu": W["N"], "vocab": W["V"], "micro_batch_rows": W["M"],
+                   "micro_batches": nmb, "parallelism": f"batch-shard dp{world}" if world > 1 else "single GPU",
+                   "l2": f"inputs >> L2: {len(W['bufs'])} logits buffers of "
+                         f"{W['bufs'][0].numel() * W['bufs'][0].element_size() / 1e9:.1f} GB cycled",
+                   "kl_beta": cfgw.kl_beta, "clip": [0.2, 0.2], "kl": "k3"},
+        "trainable_rows_per_s": sum(n_train) * world / (ms_per_step * 1e-3),
+        "step_algorithmic_GBps": step_bytes / (ms_per_step * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm", "kernel": "k_rows<bf16,BWD> (otk_policy_loss_fwd_bwd)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_source": peak_src,
+                     "bytes_per_launch": avg_bytes, "avg_launch_ms": avg_ms,
+                     "share_of_step": sum(k4_ms) / ms_per_step},
+        "gpu_launches": launches,
+        "gpu_launches_per_step": launches / args.steps,
+        "loss": stats["loss"], "n_loss": stats["n_tokens"],
+    }
+    res["clocks"] = clk.summary()
+    traffic = os.path.join(ROOT, "profiles", "k4_traffic.json")
+    if os.path.exists(traffic):
+        try:
+            tj = json.load(open(traffic))
+            res["roofline"]["traffic"] = tj.get("traffic_bytes_per_launch")
+            res["roofline"]["traffic_source"] = tj.get("source")
+        except Exception:
+            pass
+    if not args.no_e2e:
+        res["e2e"] = e2e(args, W, world, step, cfg)
+    if rank == 0 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(args, W, cfg)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if pg is not None:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------------------------
+def e2e(args, W, world, step, cfg):
+    """Same metric through the C-ABI host-buffer entry point (otk_policy_loss_fwd_bwd_host): every
+    micro-batch's logits + side arrays are copied H2D from pinned host memory inside the timed region
+    (pipelined in 4096-row chunks on a copy stream), and the loss statistics come back D2H. The step's
+    masks / advantages (device outputs of (1)-(2)) are inputs of this call and are staged once."""
+    otk, ctx = W["otk"], W["ctx"]
+    mbs = W["mbs"]
+    N = W["N"]
+    host_bufs = [b.cpu().pin_memory() for b in W["bufs"]]
+    adv = step.masks_and_advantages()
+    torch.cuda.synchronize()
+    n_loss = int(step.masks["n_loss"].item())
+    lm_h = step.masks["loss_mask"].cpu().pin_memory()
+    rt_h = step.masks["row_traj"].cpu().pin_memory()
+    adv_h = adv.cpu().pin_memory()
+    side = [(mb.targets.cpu().pin_memory(), mb.old_logp.cpu().pin_memory(),
+             None if mb.ref_logp is None else mb.ref_logp.cpu().pin_memory()) for mb in mbs]
+    nb = len(host_bufs)
+
+    def one_step():
+        tot = 0.0
+        for i, mb in enumerate(mbs):
+            tg, old, ref = side[i]
+            s = otk.otk_policy_loss_fwd_bwd_host(ctx, host_bufs[i % nb][:mb.r1 - mb.r0], tg, lm_h[mb.r0:mb.r1],
+                                                 rt_h[mb.r0:mb.r1], adv_h, old, ref, n_loss, cfg,
+                                                 rows_per_chunk=4096)
+            tot += s["loss"]
+        return tot
+
+    one_step()  # warm-up (allocates the staging buffers once)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        one_step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / args.e2e_steps
+    row_bytes = W["bufs"][0].shape[1] * W["bufs"][0].element_size()
+    side_b = 4 + 1 + 4 + 4 + (4 if mbs[0].ref_logp is not None else 0)
+    h2d = N * (row_bytes + side_b) + len(mbs) * (adv_h.numel() * 8 + 8)
+    return {"value": N * world / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": len(mbs) * 40, "steps": args.e2e_steps,
+            "h2d_GBps": h2d / dt / 1e9,
+            "path": "otk_policy_loss_fwd_bwd_host (C ABI, pinned host buffers, 4096-row chunks double-buffered)",
+            "clock": "host wall clock around the blocking C-ABI calls" + ("; rank 0" if world > 1 else "")}
+
+
+def cpu_baseline(args, W, cfg, seconds=None):
+    """The C float64 oracle (as it stands) on a bounded sample of the same workload, all host cores.
+    Its inputs are the seeded generator's (logits, targets) plus masks / advantages / old / ref computed
+    by the oracle itself — nothing from the CUDA path."""
+    from oracle import oracle_cpu as OC
+    from oracle import oracle_ref as O
+    from synth import make_noise
+    seconds = args.cpu_seconds if seconds is None else seconds
+    tb, cfgw = W["tb"], W["cfgw"]
+    mb = W["mbs"][0]
+    m = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated)
+    adv = O.group_advantages(tb.group_id - tb.group_id.min(), O.episode_returns(tb.turn_offsets, tb.turn_rewards),
+                             cfgw.num_groups)["adv"]
+    ocfg = O.LossCfg(kl_beta=cfg.kl_beta)
+    threads = os.cpu_count()
+    done, ntrain, t_used, r0, block = 0, 0, 0.0, 0, 64
+    while t_used < seconds and r0 + block <= mb.r1 - mb.r0:
+        lg = OC.bf16_bits(mb.logits[r0:r0 + block]) if cfgw.dtype == "bf16" else mb.logits[r0:r0 + block].cpu().numpy()
+        tg = mb.targets[r0:r0 + block].cpu().numpy()
+        base = OC.logprob_entropy(lg, tg)["logp"]
+        old = (base + make_noise(block, 0.05, 7000 + r0).double().numpy()).astype(np.float32)
+        ref = (base + make_noise(block, 0.1, 9000 + r0).double().numpy()).astype(np.float32) if cfg.kl_beta else None
+        lm = m["loss_mask"][r0:r0 + block]
+        t = time.perf_counter()
+        OC.policy_loss(lg, tg, lm, m["row_traj"][r0:r0 + block], adv, old, ref, m["n_loss"], ocfg)
+        t_used += time.perf_counter() - t
+        done += block
+        ntrain += int(lm.sum())
+        r0 += block
+        block = min(block * 2, 1024)
+    return {"value": done / t_used, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"first {done} rows of micro-batch 0 of the {args.config} workload ({ntrain} trainable): "
+                      f"fused loss fwd+bwd with dlogits materialised, C float64 oracle (oracle/oracle_cpu.c, "
+                      f"OpenMP {threads} threads), {t_used:.1f} s"}
+
+
+# ------------------------------------------------------------------------------------------------
+def run_reference(args):
+    """--impl reference: the float64 oracle as it stands on the host cores (the base contract's
+    reference arm for this tier). Rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle import oracle_cpu as OC
+    from oracle import oracle_ref as O
+    from synth import CONFIGS, make_batch, make_logits, make_noise
+    cfgw = CONFIGS[args.config]
+    tb = make_batch(args.config)
+    V = cfgw.V
+    rows = 256   # bounded per-step sample: the whole --steps/--warmup run stays within minutes
+    m = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated)
+    R = O.episode_returns(tb.turn_offsets, tb.turn_rewards)
+    adv = O.group_advantages(tb.group_id, R, cfgw.num_groups)["adv"]
+    lg, tg = make_logits(rows, V, dtype=cfgw.dtype, seed=cfgw.seed * 100, device="cpu")
+    bits = OC.bf16_bits(lg) if cfgw.dtype == "bf16" else lg.numpy()
+    base = OC.logprob_entropy(bits, tg.numpy())["logp"]
+    old = (base + make_noise(rows, 0.05, 7000).double().numpy()).astype(np.float32)
+    ref = (base + make_noise(rows, 0.1, 9000).double().numpy()).astype(np.float32)
+    ocfg = O.LossCfg(kl_beta=cfgw.kl_beta)
+
+    def step():
+        mm = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated)
+        aa = O.group_advantages(tb.group_id, O.episode_returns(tb.turn_offsets, tb.turn_rewards), cfgw.num_groups)
+        OC.policy_loss(bits, tg.numpy(), mm["loss_mask"][:rows], mm["row_traj"][:rows], aa["adv"], old,
+                       ref if cfgw.kl_beta else None, mm["n_loss"], ocfg)
+
+    for _ in range(args.warmup):
+        step()
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t) / args.steps
+    threads = os.cpu_count()
+    sample = (f"per step: masks + advantages of the full {args.config} batch ({tb.num_traj} trajectories, "
+              f"pure-Python oracle) + fused loss fwd+bwd of its first {rows} rows "
+              f"({int(m['loss_mask'][:rows].sum())} trainable; C float64 oracle, OpenMP {threads} threads)")
+    value = rows / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfgw.note}", "rows_per_step_sample": rows},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_otk(args)
+
+
+if __name__ == "__main__":
+    main()

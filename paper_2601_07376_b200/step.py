@@ -1,0 +1,131 @@
+"""One training step of the hot path (north_star (1)-(4)) over one batch of trajectories.
+
+Sequences the C-ABI calls and, when a torch.distributed process group is given (batch sharding,
+DESIGN.md §7), the exchanges between them:
+
+  otk_build_masks            -> all_reduce(n_loss, SUM)            global token count (R17)
+  otk_group_advantages       -> all_gather(group_id, return)       cross-shard group statistics;
+     (local returns)            otk_group_advantages (global)      every rank computes identical stats
+  otk_policy_loss_fwd_bwd x M micro-batches (stats accumulated on the device)
+                             -> all_reduce(stats, SUM)             global loss on every rank
+
+No host synchronisation inside a step (n_loss and the stats never leave the device), so a step can be
+captured in a CUDA graph. Everything arithmetic happens in libotk's kernels; this module only moves
+pointers and calls collectives.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, List, Optional, Sequence, Tuple
+
+import torch
+
+from . import (Context, DeviceTrajBatch, LossCfg, STATS_FIELDS, otk_build_masks, otk_group_advantages,
+               otk_policy_loss_fwd_bwd)
+
+
+@dataclass
+class MicroBatch:
+    """Row range [r0, r1) of the step and the tensors the loss call reads for it."""
+    r0: int
+    r1: int
+    logits: torch.Tensor            # [r1 - r0, ld]
+    targets: torch.Tensor           # [r1 - r0] int32
+    old_logp: torch.Tensor          # [r1 - r0] f32
+    ref_logp: Optional[torch.Tensor]
+    dlogits: torch.Tensor           # [r1 - r0, ld] output
+
+
+class PolicyLossStep:
+    def __init__(self, ctx: Context, batch: DeviceTrajBatch, group_id: torch.Tensor, num_groups: int,
+                 turn_offsets: torch.Tensor, turn_rewards: torch.Tensor, vocab: int, cfg: LossCfg = LossCfg(), *,
+                 train_agent: int = -1, std_norm: bool = True, unbiased: bool = False,
+                 process_group=None, global_num_traj: Optional[Sequence[int]] = None,
+                 global_num_groups: Optional[int] = None):
+        self.ctx, self.batch, self.cfg, self.vocab = ctx, batch, cfg, vocab
+        self.group_id, self.num_groups = group_id, num_groups
+        self.turn_offsets, self.turn_rewards = turn_offsets, turn_rewards
+        self.train_agent, self.std_norm, self.unbiased = train_agent, std_norm, unbiased
+        self.pg = process_group
+        dev = batch.tok_offsets.device
+        N, B = batch.num_rows, batch.num_traj
+        self.masks = dict(loss_mask=torch.empty(N, dtype=torch.uint8, device=dev),
+                          row_traj=torch.empty(N, dtype=torch.int32, device=dev),
+                          traj_loss_tokens=torch.empty(B, dtype=torch.int64, device=dev),
+                          n_loss=torch.empty(1, dtype=torch.int64, device=dev))
+        self.adv_out = dict(adv=torch.empty(B, dtype=torch.float64, device=dev),
+                            returns=torch.empty(B, dtype=torch.float64, device=dev),
+                            group_mean=torch.empty(num_groups, dtype=torch.float64, device=dev),
+                            group_std=torch.empty(num_groups, dtype=torch.float64, device=dev),
+                            group_size=torch.empty(num_groups, dtype=torch.int32, device=dev))
+        self.stats = torch.zeros(len(STATS_FIELDS), dtype=torch.float64, device=dev)
+        if self.pg is not None:
+            import torch.distributed as dist
+            self.world = dist.get_world_size(self.pg)
+            self.rank = dist.get_rank(self.pg)
+            counts = list(global_num_traj) if global_num_traj is not None else [B] * self.world
+            self.counts = counts
+            self.b0 = sum(counts[:self.rank])
+            self.Bmax = max(counts)
+            self.G_global = global_num_groups if global_num_groups is not None else num_groups
+            Bg = sum(counts)
+            self.gather_gid = torch.empty(self.world * self.Bmax, dtype=torch.int32, device=dev)
+            self.gather_ret = torch.empty(self.world * self.Bmax, dtype=torch.float64, device=dev)
+            self.pad_gid = torch.zeros(self.Bmax, dtype=torch.int32, device=dev)
+            self.pad_ret = torch.zeros(self.Bmax, dtype=torch.float64, device=dev)
+            self.gid_g = torch.empty(Bg, dtype=torch.int32, device=dev)
+            self.ret_g = torch.empty(Bg, dtype=torch.float64, device=dev)
+            self.adv_g = dict(adv=torch.empty(Bg, dtype=torch.float64, device=dev),
+                              returns=torch.empty(Bg, dtype=torch.float64, device=dev),
+                              group_mean=torch.empty(self.G_global, dtype=torch.float64, device=dev),
+                              group_std=torch.empty(self.G_global, dtype=torch.float64, device=dev),
+                              group_size=torch.empty(self.G_global, dtype=torch.int32, device=dev))
+
+    # -- (1) + (2) --------------------------------------------------------------------------------
+    def masks_and_advantages(self):
+        otk_build_masks(self.ctx, self.batch, self.train_agent, response_mask=False, source_counts=False,
+                        out=self.masks)
+        if self.pg is None:
+            otk_group_advantages(self.ctx, self.group_id, self.num_groups, turn_offsets=self.turn_offsets,
+                                 turn_rewards=self.turn_rewards, std_norm=self.std_norm, unbiased=self.unbiased,
+                                 out=self.adv_out)
+            return self.adv_out["adv"]
+        import torch.distributed as dist
+        dist.all_reduce(self.masks["n_loss"], op=dist.ReduceOp.SUM, group=self.pg)
+        # local returns (group statistics of this call are discarded), then the global exchange
+        otk_group_advantages(self.ctx, self.group_id, self.num_groups, turn_offsets=self.turn_offsets,
+                             turn_rewards=self.turn_rewards, out=self.adv_out)
+        B = self.batch.num_traj
+        self.pad_gid[:B].copy_(self.group_id)
+        self.pad_ret[:B].copy_(self.adv_out["returns"])
+        dist.all_gather_into_tensor(self.gather_gid, self.pad_gid, group=self.pg)
+        dist.all_gather_into_tensor(self.gather_ret, self.pad_ret, group=self.pg)
+        o = 0
+        for r, c in enumerate(self.counts):    # unpad in rank order (host-known counts: no sync)
+            self.gid_g[o:o + c].copy_(self.gather_gid[r * self.Bmax:r * self.Bmax + c])
+            self.ret_g[o:o + c].copy_(self.gather_ret[r * self.Bmax:r * self.Bmax + c])
+            o += c
+        otk_group_advantages(self.ctx, self.gid_g, self.G_global, returns=self.ret_g, std_norm=self.std_norm,
+                             unbiased=self.unbiased, out=self.adv_g)
+        return self.adv_g["adv"][self.b0:self.b0 + B]
+
+    # -- (3) + (4) --------------------------------------------------------------------------------
+    def loss(self, adv: torch.Tensor, micro_batches: Sequence[MicroBatch],
+             on_launch: Optional[Callable[[int, str], None]] = None):
+        for k, mb in enumerate(micro_batches):
+            if on_launch:
+                on_launch(k, "begin")
+            otk_policy_loss_fwd_bwd(self.ctx, mb.logits, mb.targets, self.masks["loss_mask"][mb.r0:mb.r1],
+                                    self.masks["row_traj"][mb.r0:mb.r1], adv, mb.old_logp, mb.ref_logp,
+                                    self.masks["n_loss"], self.cfg, vocab=self.vocab, dlogits=mb.dlogits,
+                                    stats=self.stats, accumulate=k > 0, want_logp=False)
+            if on_launch:
+                on_launch(k, "end")
+        if self.pg is not None:
+            import torch.distributed as dist
+            dist.all_reduce(self.stats, op=dist.ReduceOp.SUM, group=self.pg)
+        return self.stats
+
+    def run(self, micro_batches: Sequence[MicroBatch], on_launch=None):
+        adv = self.masks_and_advantages()
+        return self.loss(adv, micro_batches, on_launch)
