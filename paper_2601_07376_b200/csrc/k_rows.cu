@@ -1,20 +1,26 @@
-// k_rows.cu — the fused vocab-row kernel behind otk_logprob_entropy_fwd (north_star (3)),
+// k_rows.cu — the fused vocab-row kernels behind otk_logprob_entropy_fwd (north_star (3)),
 // otk_policy_loss_fwd_bwd (north_star (4)) and the vocab-sharded variants.
 //
-// One persistent CTA per SM (216 KB ring of 8 KB slots). A row is split across a thread-block
-// cluster of `csize` CTAs (csize = 2 for bf16 V = 151936) so each CTA's column segment (148 KB)
-// stays resident in shared memory between pass 1 (max / sum-exp / entropy) and pass 2
-// (softmax - onehot, scaled): every logit is read from HBM once and every dlogit written once.
-//   warp 0, lane 0  : producer — 1-D bulk TMA (cp.async.bulk) of 8 KB chunks into the ring,
-//                     L2 evict_first (logits are read once), paced by per-slot empty mbarriers.
-//   warps 1..8      : consumers — LDS.128, online max / sum 2^x / sum 2^x*x in fp32 (MUFU ex2),
-//                     warp shuffle + CTA combine, cluster exchange of 16-byte row partials via DSMEM
-//                     (st.async + mbarrier), loss terms in fp64 by one thread, pass 2 from SMEM with
-//                     streaming 16-byte stores.
+// k_rows_tm (modes FWD / PARTIAL / BWD): one persistent CTA per SM; a row is split over a
+// thread-block cluster of `csize` CTAs (csize = 2 for bf16 V = 151936: 148 KB per CTA).
+//   warp 0, lane 0 : producer — 1-D bulk TMA (cp.async.bulk) of 8 KB chunks into a 27-slot (216 KB)
+//                    shared-memory ring, L2 evict_first, paced by per-slot empty mbarriers.
+//   warps 1..8     : consumers — read each chunk from the ring once and release the slot at once, so
+//                    the ring streams the next row while this one is computed. Pass 1: online max
+//                    (packed bf16 max) and 2^(y - m) once per element (MUFU), sums in 4 independent
+//                    fp32 chains; for the loss (BWD) e = 2^(y - m_c) is parked in TENSOR MEMORY (f16 for
+//                    bf16 input; 152 of a warp's 256 TMEM columns), with the chunk's reference max m_c.
+//                    Warp shuffle + CTA combine + cluster exchange of 16-byte partials through DSMEM
+//                    (st.async + mbarrier). Loss terms in fp64 by one thread. Pass 2: softmax =
+//                    e * 2^(m_c - lse): one FMUL per element (no second read of the logits, no second
+//                    exponential), dlogits = coef * (softmax - onehot), 16-byte streaming stores.
+// k_rows_stream (mode BWD_PARTIALS, vocab shard): stats come from the all-gathered partials, so the
+//   row is streamed once through the ring and written (one exponential per element).
 // Rows with loss mask 0 are never read: their dlogits are zero-filled (write-only).
-// Reductions are in a fixed order, so results are deterministic and identical across the CTAs
-// of a cluster (and across ranks under vocab sharding).
+// All reductions run in a fixed order with explicitly rounded combine steps, so results are
+// deterministic and bitwise identical between (3) and (4) and across the CTAs of a cluster.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <cfloat>
 
@@ -26,6 +32,9 @@ using namespace ptx;
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
+constexpr int kNCT = 32 * kConsumerWarps;
+constexpr int kVPT = kChunkBytes / 16 / kNCT;  // 16-byte vectors per consumer thread per chunk (2)
+static_assert(kVPT * kNCT * 16 == kChunkBytes, "chunk must split evenly over consumers");
 
 // Running (max, sum 2^(y-m), sum 2^(y-m)(y-m)) in log2 units: y = log2(e) * s * x.
 struct Stat {
@@ -33,9 +42,7 @@ struct Stat {
 };
 
 // combine / finalize use explicitly rounded ops (__fmul_rn / __fadd_rn are never contracted into
-// FMAs), so every template instantiation and every CTA produces bitwise-identical row statistics:
-// the fwd pool's logp (3) equals the logp recomputed inside the loss (4), making the on-policy ratio
-// exactly 1, and all ranks of a vocab shard agree.
+// FMAs), so every template instantiation and every CTA produces bitwise-identical row statistics.
 __device__ __forceinline__ Stat combine(const Stat a, const Stat b) {
   const float M = fmaxf(a.m, b.m);
   if (M == -INFINITY) return a;
@@ -82,12 +89,24 @@ struct Vec<float> {
     x[2] = __uint_as_float(v.z);
     x[3] = __uint_as_float(v.w);
   }
-  __device__ static __forceinline__ float vmax(const uint4 v) {
-    return fmaxf(fmaxf(__uint_as_float(v.x), __uint_as_float(v.y)), fmaxf(__uint_as_float(v.z), __uint_as_float(v.w)));
-  }
   __device__ static __forceinline__ uint4 pack(const float (&g)[4]) {
     return make_uint4(__float_as_uint(g[0]), __float_as_uint(g[1]), __float_as_uint(g[2]), __float_as_uint(g[3]));
   }
+  // e values are kept at full precision for fp32 inputs
+  __device__ static __forceinline__ uint4 pack_e(const float (&e)[4]) { return pack(e); }
+  __device__ static __forceinline__ void unpack_e(const uint4 v, float (&e)[4]) { unpack(v, e); }
+  __device__ static __forceinline__ uint4 mask_tail(uint4 v, int nvalid) {
+    return make_uint4(nvalid > 0 ? v.x : 0xff800000u, nvalid > 1 ? v.y : 0xff800000u, nvalid > 2 ? v.z : 0xff800000u,
+                      nvalid > 3 ? v.w : 0xff800000u);
+  }
+  __device__ static __forceinline__ float vmax_acc(float acc, const uint4 v) {
+    return fmaxf(acc, fmaxf(fmaxf(__uint_as_float(v.x), __uint_as_float(v.y)),
+                            fmaxf(__uint_as_float(v.z), __uint_as_float(v.w))));
+  }
+  using MaxAcc = float;
+  __device__ static __forceinline__ float max_init() { return -INFINITY; }
+  __device__ static __forceinline__ float max_acc(float acc, const uint4 v) { return vmax_acc(acc, v); }
+  __device__ static __forceinline__ float max_final(float acc) { return acc; }
   __device__ static __forceinline__ float load1(const void* base, int64_t i) {
     return reinterpret_cast<const float*>(base)[i];
   }
@@ -102,14 +121,46 @@ struct Vec<__nv_bfloat16> {
     x[0] = bf_lo(v.x), x[1] = bf_hi(v.x), x[2] = bf_lo(v.y), x[3] = bf_hi(v.y);
     x[4] = bf_lo(v.z), x[5] = bf_hi(v.z), x[6] = bf_lo(v.w), x[7] = bf_hi(v.w);
   }
-  __device__ static __forceinline__ float vmax(const uint4 v) {
-    const uint32_t m = bmax2(bmax2(v.x, v.y), bmax2(v.z, v.w));
-    return fmaxf(bf_lo(m), bf_hi(m));
-  }
   __device__ static __forceinline__ uint4 pack(const float (&g)[8]) {
     return make_uint4(pack_bf16x2(g[0], g[1]), pack_bf16x2(g[2], g[3]), pack_bf16x2(g[4], g[5]),
                       pack_bf16x2(g[6], g[7]));
   }
+  // e = 2^(y - m) in [0, 1] is kept as f16 (11-bit significand; DESIGN.md §6 error budget)
+  __device__ static __forceinline__ uint32_t h2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+  }
+  __device__ static __forceinline__ void h2f(uint32_t w, float& lo, float& hi) {
+    asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+        : "=f"(lo), "=f"(hi)
+        : "r"(w));
+  }
+  __device__ static __forceinline__ uint4 pack_e(const float (&e)[8]) {
+    return make_uint4(h2(e[0], e[1]), h2(e[2], e[3]), h2(e[4], e[5]), h2(e[6], e[7]));
+  }
+  __device__ static __forceinline__ void unpack_e(const uint4 v, float (&e)[8]) {
+    h2f(v.x, e[0], e[1]);
+    h2f(v.y, e[2], e[3]);
+    h2f(v.z, e[4], e[5]);
+    h2f(v.w, e[6], e[7]);
+  }
+  // lanes >= nvalid become -inf (bf16 0xff80)
+  __device__ static __forceinline__ uint32_t mask_word(uint32_t w, int lane0, int nvalid) {
+    if (lane0 >= nvalid) return 0xff80ff80u;
+    if (lane0 + 1 >= nvalid) return (w & 0x0000ffffu) | 0xff800000u;
+    return w;
+  }
+  __device__ static __forceinline__ uint4 mask_tail(uint4 v, int nvalid) {
+    return make_uint4(mask_word(v.x, 0, nvalid), mask_word(v.y, 2, nvalid), mask_word(v.z, 4, nvalid),
+                      mask_word(v.w, 6, nvalid));
+  }
+  using MaxAcc = uint32_t;  // packed bf16x2 running max
+  __device__ static __forceinline__ uint32_t max_init() { return 0xff80ff80u; }
+  __device__ static __forceinline__ uint32_t max_acc(uint32_t acc, const uint4 v) {
+    return bmax2(acc, bmax2(bmax2(v.x, v.y), bmax2(v.z, v.w)));
+  }
+  __device__ static __forceinline__ float max_final(uint32_t acc) { return fmaxf(bf_lo(acc), bf_hi(acc)); }
   __device__ static __forceinline__ float load1(const void* base, int64_t i) {
     return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[i]);
   }
@@ -130,21 +181,221 @@ struct Smem {
 constexpr size_t kRingBytes = size_t(kSlots) * kChunkBytes;
 constexpr size_t kSmemBytes = kRingBytes + sizeof(Smem);
 
+__device__ __forceinline__ bool row_active(const RowParams& p, int32_t y, uint8_t m) {
+  return m && y >= 0 && int64_t(y) < p.vocab_total;
+}
+
+// ---- producer: bulk-TMA every active row's column segment, chunk by chunk, into the ring ------------
+template <typename T>
+__device__ __forceinline__ void produce(const RowParams& p, uint8_t* ring, Smem& S, int64_t group,
+                                        int64_t ngroups, int64_t c0, uint32_t seg_bytes, int nch) {
+  const uint64_t pol = policy_evict_first();
+  const char* base = reinterpret_cast<const char*>(p.logits) + c0 * int64_t(sizeof(T));
+  const int64_t row_bytes = p.ld * int64_t(sizeof(T));
+  uint32_t slot = 0, phase = 0;
+  int64_t row = group;
+  int32_t y_n = row < p.num_rows ? p.targets[row] : 0;
+  uint8_t m_n = (row < p.num_rows && p.mask) ? p.mask[row] : 1;
+  for (; row < p.num_rows; row += ngroups) {
+    const int32_t y = y_n;
+    const uint8_t m = m_n;
+    const int64_t nrow = row + ngroups;
+    if (nrow < p.num_rows) {
+      y_n = p.targets[nrow];
+      m_n = p.mask ? p.mask[nrow] : 1;
+    }
+    if (!row_active(p, y, m)) continue;
+    const char* src = base + row * row_bytes;
+    uint32_t off = 0;
+    for (int c = 0; c < nch; ++c) {
+      mbar_wait(&S.empty[slot], phase ^ 1u);
+      const uint32_t bytes = min(uint32_t(kChunkBytes), seg_bytes - off);
+      mbar_arrive_expect_tx(&S.full[slot], bytes);
+      bulk_g2s(ring + size_t(slot) * kChunkBytes, src + off, bytes, &S.full[slot], pol);
+      off += kChunkBytes;
+      if (++slot == kSlots) {
+        slot = 0;
+        phase ^= 1u;
+      }
+    }
+  }
+}
+
+// ---- rows that are never read: zero-filled dlogits / zero outputs (R26) ----------------
 template <typename T, int MODE>
-__global__ void __launch_bounds__(kThreads, 1) k_rows(const RowParams p) {
+__device__ __forceinline__ void inactive_row(const RowParams& p, int64_t row, int ct, uint32_t crank, int64_t c0,
+                                             int segn, bool bad_target) {
+  constexpr int EV = Vec<T>::EV;
+  if (bad_target && ct == 0 && crank == 0) set_error(p.err, OTK_ERR_TARGET_RANGE);
+  if (MODE == kModeBwd || MODE == kModeBwdPartials) {
+    if (p.zero_masked) {
+      char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
+      for (int lc = ct * EV; lc < segn; lc += kNCT * EV) {
+        if (lc + EV <= segn) {
+          stg_cs_v4(drow + size_t(lc) * sizeof(T), make_uint4(0, 0, 0, 0));
+        } else {
+          for (int k = lc; k < segn; ++k) Vec<T>::store1(drow, k, 0.f);
+        }
+      }
+    }
+    if (ct == 0 && crank == 0) {
+      if (p.logp) p.logp[row] = 0.f;
+      if (p.entropy) p.entropy[row] = 0.f;
+    }
+  } else if (ct == 0 && crank == 0) {
+    if (MODE == kModeFwd) {
+      p.logp[row] = 0.f;
+      if (p.entropy) p.entropy[row] = 0.f;
+      if (p.lse) p.lse[row] = 0.f;
+    } else {
+      p.partials_out[row] = make_float4(-INFINITY, 0.f, 0.f, 0.f);
+    }
+  }
+}
+
+// ---- per-token loss (north_star (4); same definition as oracle_ref.row_loss_terms) ----------------
+struct LossOut {
+  double L, kl;
+  float coef;
+  bool clipped;
+};
+__device__ __forceinline__ LossOut loss_terms(const RowParams& p, float logp, int32_t rt, float old_lp,
+                                              float ref_lp, int64_t nl) {
+  const double lp = double(logp);
+  const double A = p.adv[rt];
+  const double C = p.clamp;
+  const double draw = lp - double(old_lp);
+  const double delta = fmin(fmax(draw, -C), C);
+  const double r = exp(delta);
+  const double lo = 1.0 - p.clip_low, hi = 1.0 + p.clip_high;
+  const double rbar = fmin(fmax(r, lo), hi);
+  const double pg = fmax(-A * r, -A * rbar);
+  const bool clipped = (A > 0.0 && r > hi) || (A < 0.0 && r < lo);
+  double G = (clipped || fabs(draw) > C) ? 0.0 : -A * r;
+  double kl = 0.0;
+  const double beta = p.kl_beta;
+  if (beta != 0.0) {
+    const double ref = double(ref_lp);
+    double gk;
+    if (p.kl_type == OTK_KL_K3) {
+      const double dr = ref - lp;
+      const double d = fmin(fmax(dr, -C), C);
+      const double ed = exp(d);
+      kl = ed - d - 1.0;
+      gk = fabs(dr) > C ? 0.0 : 1.0 - ed;
+    } else if (p.kl_type == OTK_KL_K1) {
+      kl = lp - ref;
+      gk = 1.0;
+    } else {
+      kl = 0.5 * (lp - ref) * (lp - ref);
+      gk = lp - ref;
+    }
+    G += beta * gk;
+  }
+  LossOut o;
+  o.L = pg + beta * kl;
+  o.kl = kl;
+  o.clipped = clipped;
+  const double invN = nl > 0 ? 1.0 / double(nl) : 0.0;
+  o.coef = float(-double(p.scale) * invN * G);
+  return o;
+}
+
+// warp + CTA reduction of the per-thread Stat into S.wred (caller syncs)
+__device__ __forceinline__ void reduce_warp_to_smem(Stat st, Smem& S, int lane, int cw) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    Stat o;
+    o.m = __shfl_xor_sync(0xffffffffu, st.m, off);
+    o.s = __shfl_xor_sync(0xffffffffu, st.s, off);
+    o.t = __shfl_xor_sync(0xffffffffu, st.t, off);
+    st = (lane & off) ? combine(o, st) : combine(st, o);
+  }
+  if (lane == 0) S.wred[cw] = make_float4(st.m, st.s, st.t, 0.f);
+}
+
+// thread 0: CTA total -> cluster exchange (rank order) -> row total
+__device__ __forceinline__ void cta_and_cluster_total(Smem& S, int csize, uint32_t crank, uint32_t q, Stat& tot,
+                                                      float& zyt) {
+  Stat r{S.wred[0].x, S.wred[0].y, S.wred[0].z};
+#pragma unroll
+  for (int w = 1; w < kConsumerWarps; ++w) r = combine(r, Stat{S.wred[w].x, S.wred[w].y, S.wred[w].z});
+  const float zy = S.zy;
+  S.zy = 0.f;
+  if (csize > 1) {
+    const uint32_t par = q & 1u;
+    for (int dst = 0; dst < csize; ++dst) {
+      if (dst == int(crank)) continue;
+      st_async_f4(mapa(smem_u32(&S.xrecv[par][crank]), dst), r.m, r.s, r.t, zy, mapa(smem_u32(&S.xbar[par]), dst));
+    }
+    mbar_arrive_expect_tx(&S.xbar[par], 16u * uint32_t(csize - 1));
+    mbar_wait_cluster(&S.xbar[par], (q >> 1) & 1u);
+    tot = Stat{-INFINITY, 0.f, 0.f};
+    zyt = 0.f;
+    for (int k = 0; k < csize; ++k) {
+      const float4 P = (k == int(crank)) ? make_float4(r.m, r.s, r.t, zy) : S.xrecv[par][k];
+      tot = combine(tot, Stat{P.x, P.y, P.z});
+      zyt += P.w;
+    }
+  } else {
+    tot = r;
+    zyt = zy;
+  }
+}
+
+__device__ __forceinline__ void stats_epilogue(const RowParams& p, double acc_L, double acc_clip, double acc_kl,
+                                               double acc_H, double acc_n, int64_t nl) {
+  double* part = p.cta_partials + size_t(blockIdx.x) * kStatSlots;
+  part[0] = acc_L;
+  part[1] = acc_clip;
+  part[2] = acc_kl;
+  part[3] = acc_H;
+  part[4] = acc_n;
+  __threadfence();
+  const unsigned int t = atomicAdd(p.ticket, 1u);
+  if (t == gridDim.x - 1) {
+    __threadfence();
+    double tot[5] = {0, 0, 0, 0, 0};
+    for (unsigned int b = 0; b < gridDim.x; ++b) {
+      const volatile double* q2 = p.cta_partials + size_t(b) * kStatSlots;
+      for (int k = 0; k < 5; ++k) tot[k] += q2[k];
+    }
+    const double invN = nl > 0 ? 1.0 / double(nl) : 0.0;
+    otk_loss_stats* o = p.stats;
+    if (p.accumulate) {
+      o->loss += tot[0] * invN;
+      o->n_clipped += tot[1];
+      o->kl_sum += tot[2];
+      o->entropy_sum += tot[3];
+      o->n_tokens += tot[4];
+    } else {
+      o->loss = tot[0] * invN;
+      o->n_clipped = tot[1];
+      o->kl_sum = tot[2];
+      o->entropy_sum = tot[3];
+      o->n_tokens = tot[4];
+    }
+    *p.ticket = 0u;
+  }
+}
+
+// =====================================================================================================
+// k_rows_tm: FWD / PARTIAL / BWD. Pass 1 streams each chunk from the ring exactly once (slot released
+// right away); for BWD the exponentials e = 2^(y - m_c) (f16 for bf16 input, with m_c the thread's
+// running max after chunk c) and m_c are parked in TENSOR MEMORY, so pass 2 needs no second read of the
+// logits and no second exponential: softmax = e * 2^(m_c - lse).
+// =====================================================================================================
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
   Smem& S = *reinterpret_cast<Smem*>(smem + kRingBytes);
-
+  __shared__ uint32_t s_tmem_base;
   using VT = Vec<T>;
   constexpr int EV = VT::EV;
-  constexpr int CE = kChunkBytes / int(sizeof(T));                    // elements per chunk
-  constexpr int NCT = 32 * kConsumerWarps;                             // consumer threads
-  constexpr int VPT = kChunkBytes / 16 / NCT;                          // 16-B vectors per thread per chunk
-  static_assert(VPT * NCT * 16 == kChunkBytes, "chunk must split evenly over consumers");
-  constexpr bool kBwd = (MODE == kModeBwd || MODE == kModeBwdPartials);
-  constexpr bool kPass1 = (MODE != kModeBwdPartials);
-  constexpr bool kResident = (MODE == kModeBwd);
+  constexpr int CE = kChunkBytes / int(sizeof(T));
+  constexpr bool kBwd = (MODE == kModeBwd);
+  constexpr int kColM = 8 * kMaxChunks;  // per-thread TMEM columns: [0, 8*kMaxChunks) e, then m_c
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int csize = p.csize;
@@ -153,9 +404,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows(const RowParams p) {
   const int64_t ngroups = gridDim.x / csize;
   const int64_t c0 = int64_t(crank) * p.seg_elems;
   const int64_t c1 = min(p.vocab, c0 + int64_t(p.seg_elems));
-  const int64_t segn = c1 > c0 ? c1 - c0 : 0;
-  const uint32_t seg_bytes = uint32_t((segn * int64_t(sizeof(T)) + 15) & ~int64_t(15));
-  const int nch = int((seg_bytes + kChunkBytes - 1) / kChunkBytes);
+  const int segn = c1 > c0 ? int(c1 - c0) : 0;
+  const uint32_t seg_bytes = (uint32_t(segn) * uint32_t(sizeof(T)) + 15u) & ~15u;
+  const int nch = int((seg_bytes + kChunkBytes - 1) / kChunkBytes);  // <= kMaxChunks (host-checked)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSlots; ++i) {
@@ -167,50 +418,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows(const RowParams p) {
     S.zy = 0.f;
     fence_mbar_init();
   }
+  if (kBwd && warp == 1) {  // one warp owns the TMEM allocation (all 512 columns; 1 CTA per SM)
+    tmem_alloc(&s_tmem_base, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
   if (csize > 1)
     cluster_sync_all();
   else
     __syncthreads();
+  tc_fence_after();
 
   if (warp == 0) {
-    // ============================== producer ==============================
-    if (lane == 0 && nch > 0) {
-      const uint64_t pol = policy_evict_first();
-      const char* base = reinterpret_cast<const char*>(p.logits) + c0 * int64_t(sizeof(T));
-      const int64_t row_bytes = p.ld * int64_t(sizeof(T));
-      uint32_t seq = 0;
-      int64_t row = group;
-      int32_t y_n = row < p.num_rows ? p.targets[row] : 0;
-      uint8_t m_n = (row < p.num_rows && p.mask) ? p.mask[row] : 1;
-      for (; row < p.num_rows; row += ngroups) {
-        const int32_t y = y_n;
-        const uint8_t m = m_n;
-        const int64_t nrow = row + ngroups;
-        if (nrow < p.num_rows) {
-          y_n = p.targets[nrow];
-          m_n = p.mask ? p.mask[nrow] : 1;
-        }
-        if (!(m && y >= 0 && int64_t(y) < p.vocab_total)) continue;
-        const char* src = base + row * row_bytes;
-        for (int c = 0; c < nch; ++c, ++seq) {
-          const uint32_t slot = seq % kSlots, ph = (seq / kSlots) & 1u;
-          mbar_wait(&S.empty[slot], ph ^ 1u);
-          const uint32_t bytes = min(uint32_t(kChunkBytes), seg_bytes - uint32_t(c) * kChunkBytes);
-          mbar_arrive_expect_tx(&S.full[slot], bytes);
-          bulk_g2s(ring + size_t(slot) * kChunkBytes, src + size_t(c) * kChunkBytes, bytes, &S.full[slot], pol);
-        }
-      }
-    }
+    if (lane == 0 && nch > 0) produce<T>(p, ring, S, group, ngroups, c0, seg_bytes, nch);
     __syncwarp();
   } else {
-    // ============================== consumers =============================
     const int ct = threadIdx.x - 32;
     const int cw = warp - 1;
-    const float s2 = p.scale * kLog2e;
+    // this warp's TMEM window: its lane quadrant (warp % 4) and one half of the 512 columns
+    const uint32_t tm = kBwd ? s_tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(256 * (cw >> 2)) : 0u;
+    const float s2 = __fmul_rn(p.scale, kLog2e);
     double acc_L = 0.0, acc_clip = 0.0, acc_kl = 0.0, acc_H = 0.0, acc_n = 0.0;
     int64_t nl = 0;
     if (kBwd && ct == 0) nl = *p.n_loss;
-    uint32_t seq = 0, q = 0;
+    uint32_t slot = 0, phase = 0, q = 0;
 
     int64_t row = group;
     int32_t y_n = row < p.num_rows ? p.targets[row] : 0;
@@ -223,166 +454,87 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows(const RowParams p) {
         y_n = p.targets[nrow];
         m_n = p.mask ? p.mask[nrow] : 1;
       }
-      const bool in_range = y >= 0 && int64_t(y) < p.vocab_total;
-      if (!(m && in_range)) {
-        // ---------------- inactive row: never read ----------------
-        if (m && ct == 0 && crank == 0) set_error(p.err, OTK_ERR_TARGET_RANGE);
-        if (kBwd) {
-          if (p.zero_masked) {
-            char* drow = reinterpret_cast<char*>(p.dlogits) + row * p.ld * int64_t(sizeof(T));
-            for (int64_t col = c0 + int64_t(ct) * EV; col < c1; col += int64_t(NCT) * EV) {
-              if (col + EV <= c1) {
-                stg_cs_v4(drow + col * int64_t(sizeof(T)), make_uint4(0, 0, 0, 0));
-              } else {
-                for (int64_t k = col; k < c1; ++k) VT::store1(drow, k, 0.f);
-              }
-            }
-          }
-          if (ct == 0 && crank == 0) {
-            if (p.logp) p.logp[row] = 0.f;
-            if (p.entropy) p.entropy[row] = 0.f;
-          }
-        } else if (ct == 0 && crank == 0) {
-          if (MODE == kModeFwd) {
-            p.logp[row] = 0.f;
-            if (p.entropy) p.entropy[row] = 0.f;
-            if (p.lse) p.lse[row] = 0.f;
-          } else {
-            p.partials_out[row] = make_float4(-INFINITY, 0.f, 0.f, 0.f);
-          }
-        }
+      if (!row_active(p, y, m)) {
+        inactive_row<T, MODE>(p, row, ct, crank, c0, segn, m != 0);
         continue;
       }
-      const int64_t yl = int64_t(y) - p.vocab_start;  // local target column (may lie outside this shard)
-
-      // thread 0: side data for the loss, issued early (consumed after pass 1)
+      const int64_t ylc64 = int64_t(y) - p.vocab_start - c0;  // target column local to this CTA's segment
+      const int ylc = (ylc64 >= 0 && ylc64 < segn) ? int(ylc64) : -1;
       int32_t rt = 0;
       float old_lp = 0.f, ref_lp = 0.f;
-      if (kBwd && ct == 0) {
+      if (kBwd && ct == 0) {  // issued early, consumed after pass 1
         rt = p.row_traj[row];
         old_lp = p.old_logp[row];
         if (p.ref_logp) ref_lp = p.ref_logp[row];
       }
 
-      // ---------------- pass 1: online max / sum-exp / entropy numerator ----------------
+      // ---------------- pass 1: online max / sum 2^(y-m) / sum 2^(y-m)(y-m), one exponential per element
       Stat st{-INFINITY, 0.f, 0.f};
-      if (kPass1) {
-        for (int c = 0; c < nch; ++c) {
-          const uint32_t sq = seq + uint32_t(c);
-          const uint32_t slot = sq % kSlots;
-          mbar_wait(&S.full[slot], (sq / kSlots) & 1u);
-          const uint8_t* buf = ring + size_t(slot) * kChunkBytes;
-          const int64_t cbase = c0 + int64_t(c) * CE;
-          uint4 v[VPT];
-          float mx = -INFINITY;
+      for (int c = 0; c < nch; ++c) {
+        mbar_wait(&S.full[slot], phase);
+        const uint8_t* buf = ring + size_t(slot) * kChunkBytes;
+        uint4 v[kVPT];
+        typename VT::MaxAcc macc = VT::max_init();
 #pragma unroll
-          for (int k = 0; k < VPT; ++k) {
-            const int vi = ct + k * NCT;
-            const int64_t vcol = cbase + int64_t(vi) * EV;
-            v[k] = *reinterpret_cast<const uint4*>(buf + size_t(vi) * 16);
-            if (vcol + EV <= c1) {
-              mx = fmaxf(mx, VT::vmax(v[k]));
-            } else if (vcol < c1) {
-              float x[EV];
-              VT::unpack(v[k], x);
-#pragma unroll
-              for (int i = 0; i < EV; ++i)
-                if (vcol + i < c1) mx = fmaxf(mx, x[i]);
+        for (int k = 0; k < kVPT; ++k) {
+          const int vi = ct + k * kNCT;
+          const int lc = c * CE + vi * EV;
+          uint4 w = *reinterpret_cast<const uint4*>(buf + vi * 16);
+          if (lc + EV > segn) w = VT::mask_tail(w, segn - lc);
+          v[k] = w;
+          if (unsigned(ylc - lc) < unsigned(EV)) S.zy = __fmul_rn(p.scale, VT::load1(buf, ylc - c * CE));
+          macc = VT::max_acc(macc, w);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[slot]);
+        if (++slot == kSlots) {
+          slot = 0;
+          phase ^= 1u;
+        }
+        // running max update (rescale the sums when it grows; exact no-op otherwise)
+        const float mx = VT::max_final(macc);
+        if (mx != -INFINITY) {
+          const float mn = fmaxf(st.m, __fmul_rn(mx, s2));
+          if (mn > st.m) {
+            if (st.m != -INFINITY) {
+              const float d = __fsub_rn(st.m, mn), f = ex2(d);
+              st.t = __fmul_rn(f, __fmaf_rn(d, st.s, st.t));
+              st.s = __fmul_rn(st.s, f);
             }
-            if (uint64_t(yl - vcol) < uint64_t(EV) && yl < c1) S.zy = __fmul_rn(p.scale, VT::load1(buf, yl - cbase));
-          }
-          if (mx > -INFINITY) {
-            const float mn = fmaxf(st.m, mx * s2);
-            if (mn > st.m) {
-              if (st.m != -INFINITY) {
-                const float d = st.m - mn, f = ex2(d);
-                st.t = f * fmaf(d, st.s, st.t);
-                st.s *= f;
-              }
-              st.m = mn;
-            }
-            // chunk-local partial sums (short fp32 accumulation chains), then one add per chunk
-            float cs = 0.f, ctt = 0.f;
-#pragma unroll
-            for (int k = 0; k < VPT; ++k) {
-              const int64_t vcol = cbase + int64_t(ct + k * NCT) * EV;
-              float x[EV];
-              VT::unpack(v[k], x);
-              if (vcol + EV <= c1) {
-#pragma unroll
-                for (int i = 0; i < EV; ++i) {
-                  const float d = fmaxf(fmaf(x[i], s2, -st.m), -FLT_MAX);
-                  const float e = ex2(d);
-                  cs += e;
-                  ctt = fmaf(e, d, ctt);
-                }
-              } else if (vcol < c1) {
-#pragma unroll
-                for (int i = 0; i < EV; ++i) {
-                  if (vcol + i < c1) {
-                    const float d = fmaxf(fmaf(x[i], s2, -st.m), -FLT_MAX);
-                    const float e = ex2(d);
-                    cs += e;
-                    ctt = fmaf(e, d, ctt);
-                  }
-                }
-              }
-            }
-            st.s += cs;
-            st.t += ctt;
-          }
-          if (!kResident) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&S.empty[slot]);
+            st.m = mn;
           }
         }
+        const float mref = (st.m == -INFINITY) ? 0.f : st.m;
+        float sa[4] = {0.f, 0.f, 0.f, 0.f}, ta[4] = {0.f, 0.f, 0.f, 0.f};
+        uint4 ev[kVPT];
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) {
-          Stat o;
-          o.m = __shfl_xor_sync(0xffffffffu, st.m, off);
-          o.s = __shfl_xor_sync(0xffffffffu, st.s, off);
-          o.t = __shfl_xor_sync(0xffffffffu, st.t, off);
-          st = (lane & off) ? combine(o, st) : combine(st, o);
+        for (int k = 0; k < kVPT; ++k) {
+          float x[EV], e[EV];
+          VT::unpack(v[k], x);
+#pragma unroll
+          for (int i = 0; i < EV; ++i) {
+            const float d = fmaxf(__fmaf_rn(x[i], s2, -mref), -256.f);  // -inf logits -> e = 0, e*d = 0
+            e[i] = ex2(d);
+            sa[i & 3] = __fadd_rn(sa[i & 3], e[i]);
+            ta[i & 3] = __fmaf_rn(e[i], d, ta[i & 3]);
+          }
+          if (kBwd) ev[k] = VT::pack_e(e);
         }
-        if (lane == 0) S.wred[cw] = make_float4(st.m, st.s, st.t, 0.f);
-        named_bar_sync(1, NCT);
+        st.s = __fadd_rn(st.s, __fadd_rn(__fadd_rn(sa[0], sa[1]), __fadd_rn(sa[2], sa[3])));
+        st.t = __fadd_rn(st.t, __fadd_rn(__fadd_rn(ta[0], ta[1]), __fadd_rn(ta[2], ta[3])));
+        if (kBwd) {
+          tmem_st8(tm + uint32_t(8 * c), ev[0], ev[1]);
+          tmem_st1(tm + uint32_t(kColM + c), __float_as_uint(mref));
+        }
       }
+      if (kBwd) tmem_wait_st();
+      reduce_warp_to_smem(st, S, lane, cw);
+      named_bar_sync(1, kNCT);
 
       if (ct == 0) {
-        Stat tot{-INFINITY, 0.f, 0.f};
-        float zyt = 0.f;
-        if (kPass1) {
-          Stat r{S.wred[0].x, S.wred[0].y, S.wred[0].z};
-#pragma unroll
-          for (int w = 1; w < kConsumerWarps; ++w) r = combine(r, Stat{S.wred[w].x, S.wred[w].y, S.wred[w].z});
-          const float zy = S.zy;
-          S.zy = 0.f;
-          if (csize > 1) {
-            const uint32_t par = q & 1u;
-            for (int dst = 0; dst < csize; ++dst) {
-              if (dst == int(crank)) continue;
-              st_async_f4(mapa(smem_u32(&S.xrecv[par][crank]), dst), r.m, r.s, r.t, zy,
-                          mapa(smem_u32(&S.xbar[par]), dst));
-            }
-            mbar_arrive_expect_tx(&S.xbar[par], 16u * uint32_t(csize - 1));
-            mbar_wait_cluster(&S.xbar[par], (q >> 1) & 1u);
-            for (int k = 0; k < csize; ++k) {
-              const float4 P = (k == int(crank)) ? make_float4(r.m, r.s, r.t, zy) : S.xrecv[par][k];
-              tot = combine(tot, Stat{P.x, P.y, P.z});
-              zyt += P.w;
-            }
-          } else {
-            tot = r;
-            zyt = zy;
-          }
-        } else {
-          for (int k = 0; k < p.nshards; ++k) {
-            const float4 P = p.partials_in[int64_t(k) * p.num_rows + row];
-            tot = combine(tot, Stat{P.x, P.y, P.z});
-            zyt += P.w;
-          }
-        }
-
+        Stat tot;
+        float zyt;
+        cta_and_cluster_total(S, csize, crank, q, tot, zyt);
         if (MODE == kModePartial) {
           if (crank == 0) p.partials_out[row] = make_float4(tot.m, tot.s, tot.t, zyt);
         } else {
@@ -394,140 +546,201 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows(const RowParams p) {
               if (p.lse) p.lse[row] = rs.lse;
             }
           } else {
-            // ---------------- loss terms (fp64, one thread) ----------------
-            const double lp = double(rs.logp);
-            const double A = p.adv[rt];
-            const double C = double(p.clamp);
-            const double draw = lp - double(old_lp);
-            const double delta = fmin(fmax(draw, -C), C);
-            const double r = exp(delta);
-            const double lo = 1.0 - double(p.clip_low), hi = 1.0 + double(p.clip_high);
-            const double rbar = fmin(fmax(r, lo), hi);
-            const double pg = fmax(-A * r, -A * rbar);
-            const bool clipped = (A > 0.0 && r > hi) || (A < 0.0 && r < lo);
-            double G = (clipped || fabs(draw) > C) ? 0.0 : -A * r;
-            double kl = 0.0;
-            const double beta = double(p.kl_beta);
-            if (beta != 0.0) {
-              const double ref = double(ref_lp);
-              double gk;
-              if (p.kl_type == OTK_KL_K3) {
-                const double dr = ref - lp;
-                const double d = fmin(fmax(dr, -C), C);
-                const double ed = exp(d);
-                kl = ed - d - 1.0;
-                gk = fabs(dr) > C ? 0.0 : 1.0 - ed;
-              } else if (p.kl_type == OTK_KL_K1) {
-                kl = lp - ref;
-                gk = 1.0;
-              } else {
-                kl = 0.5 * (lp - ref) * (lp - ref);
-                gk = lp - ref;
-              }
-              G += beta * gk;
-            }
-            const double L = pg + beta * kl;
-            const double invN = nl > 0 ? 1.0 / double(nl) : 0.0;
-            const float coef = float(-double(p.scale) * invN * G);
+            const LossOut lo = loss_terms(p, rs.logp, rt, old_lp, ref_lp, nl);
             if (crank == 0) {
-              acc_L += L;
-              acc_clip += clipped ? 1.0 : 0.0;
-              acc_kl += kl;
+              acc_L += lo.L;
+              acc_clip += lo.clipped ? 1.0 : 0.0;
+              acc_kl += lo.kl;
               acc_H += double(rs.H);
               acc_n += 1.0;
               if (p.logp) p.logp[row] = rs.logp;
               if (p.entropy) p.entropy[row] = rs.H;
             }
-            S.rowbc[q & 1u] = make_float4(rs.L2, coef, 0.f, 0.f);
+            S.rowbc[q & 1u] = make_float4(rs.L2, lo.coef, 0.f, 0.f);
           }
         }
       }
+      named_bar_sync(1, kNCT);
 
       if (kBwd) {
-        // ---------------- pass 2: dlogits = coef * (p - onehot) ----------------
-        named_bar_sync(1, NCT);
+        // ---------------- pass 2: dlogits = coef * (e * 2^(m_c - lse) - onehot), e from TMEM -----------
         const float4 bc = S.rowbc[q & 1u];
-        const float L2 = bc.x, coef = bc.y;
-        char* drow = reinterpret_cast<char*>(p.dlogits) + row * p.ld * int64_t(sizeof(T));
+        const float coef = bc.y;
+        char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
         for (int c = 0; c < nch; ++c) {
-          const uint32_t sq = seq + uint32_t(c);
-          const uint32_t slot = sq % kSlots;
-          if (!kResident) mbar_wait(&S.full[slot], (sq / kSlots) & 1u);
-          const uint8_t* buf = ring + size_t(slot) * kChunkBytes;
-          const int64_t cbase = c0 + int64_t(c) * CE;
+          uint4 ev[kVPT];
+          uint32_t mw;
+          tmem_ld8_1(tm + uint32_t(8 * c), tm + uint32_t(kColM + c), ev[0], ev[1], mw);
+          const float kt = __fmul_rn(coef, ex2(__fsub_rn(__uint_as_float(mw), bc.x)));
 #pragma unroll
-          for (int k = 0; k < VPT; ++k) {
-            const int vi = ct + k * NCT;
-            const int64_t vcol = cbase + int64_t(vi) * EV;
-            if (vcol >= c1) continue;
-            const uint4 v = *reinterpret_cast<const uint4*>(buf + size_t(vi) * 16);
-            float x[EV], g[EV];
-            VT::unpack(v, x);
+          for (int k = 0; k < kVPT; ++k) {
+            const int lc = c * CE + (ct + k * kNCT) * EV;
+            if (lc < segn) {
+              float e[EV], g[EV];
+              VT::unpack_e(ev[k], e);
 #pragma unroll
-            for (int i = 0; i < EV; ++i) g[i] = coef * ex2(fmaf(x[i], s2, -L2));
-            if (uint64_t(yl - vcol) < uint64_t(EV)) {
+              for (int i = 0; i < EV; ++i) g[i] = __fmul_rn(e[i], kt);
+              if (unsigned(ylc - lc) < unsigned(EV)) {
 #pragma unroll
-              for (int i = 0; i < EV; ++i)
-                if (vcol + i == yl) g[i] -= coef;
-            }
-            if (vcol + EV <= c1) {
-              stg_cs_v4(drow + vcol * int64_t(sizeof(T)), VT::pack(g));
-            } else {
+                for (int i = 0; i < EV; ++i)
+                  if (lc + i == ylc) g[i] = __fsub_rn(g[i], coef);
+              }
+              if (lc + EV <= segn) {
+                stg_cs_v4(drow + size_t(lc) * sizeof(T), VT::pack(g));
+              } else {
 #pragma unroll
-              for (int i = 0; i < EV; ++i)
-                if (vcol + i < c1) VT::store1(drow, vcol + i, g[i]);
+                for (int i = 0; i < EV; ++i)
+                  if (lc + i < segn) VT::store1(drow, lc + i, g[i]);
+              }
             }
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&S.empty[slot]);
         }
       }
-      seq += uint32_t(nch);
       ++q;
-      if (!kBwd) named_bar_sync(1, NCT);  // S.wred / S.zy reuse guard for the next row
     }
-
-    // ---------------- deterministic stats reduction (last CTA) ----------------
-    if (kBwd && ct == 0) {
-      double* part = p.cta_partials + size_t(blockIdx.x) * kStatSlots;
-      part[0] = acc_L;
-      part[1] = acc_clip;
-      part[2] = acc_kl;
-      part[3] = acc_H;
-      part[4] = acc_n;
-      __threadfence();
-      const unsigned int t = atomicAdd(p.ticket, 1u);
-      if (t == gridDim.x - 1) {
-        __threadfence();
-        double tot[5] = {0, 0, 0, 0, 0};
-        for (unsigned int b = 0; b < gridDim.x; ++b) {
-          const volatile double* q2 = p.cta_partials + size_t(b) * kStatSlots;
-          for (int k = 0; k < 5; ++k) tot[k] += q2[k];
-        }
-        const double invN = nl > 0 ? 1.0 / double(nl) : 0.0;
-        otk_loss_stats* o = p.stats;
-        if (p.accumulate) {
-          o->loss += tot[0] * invN;
-          o->n_clipped += tot[1];
-          o->kl_sum += tot[2];
-          o->entropy_sum += tot[3];
-          o->n_tokens += tot[4];
-        } else {
-          o->loss = tot[0] * invN;
-          o->n_clipped = tot[1];
-          o->kl_sum = tot[2];
-          o->entropy_sum = tot[3];
-          o->n_tokens = tot[4];
-        }
-        *p.ticket = 0u;
-      }
-    }
+    if (kBwd && ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl);
   }
+  tc_fence_before();
+  if (csize > 1)
+    cluster_sync_all();
+  else
+    __syncthreads();
+  if (kBwd && warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(s_tmem_base, 512);
+  }
+}
 
+// =====================================================================================================
+// k_rows_stream: BWD on a vocab shard from all-gathered partials (no pass 1): stream, write, release
+// =====================================================================================================
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* ring = smem;
+  Smem& S = *reinterpret_cast<Smem*>(smem + kRingBytes);
+  using VT = Vec<T>;
+  constexpr int EV = VT::EV;
+  constexpr int CE = kChunkBytes / int(sizeof(T));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int csize = p.csize;
+  const uint32_t crank = csize > 1 ? cluster_ctarank() : 0u;
+  const int64_t group = blockIdx.x / csize;
+  const int64_t ngroups = gridDim.x / csize;
+  const int64_t c0 = int64_t(crank) * p.seg_elems;
+  const int64_t c1 = min(p.vocab, c0 + int64_t(p.seg_elems));
+  const int segn = c1 > c0 ? int(c1 - c0) : 0;
+  const uint32_t seg_bytes = (uint32_t(segn) * uint32_t(sizeof(T)) + 15u) & ~15u;
+  const int nch = int((seg_bytes + kChunkBytes - 1) / kChunkBytes);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  if (csize > 1)
+    cluster_sync_all();
+  else
+    __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0 && nch > 0) produce<T>(p, ring, S, group, ngroups, c0, seg_bytes, nch);
+    __syncwarp();
+  } else {
+    const int ct = threadIdx.x - 32;
+    const float s2 = __fmul_rn(p.scale, kLog2e);
+    double acc_L = 0.0, acc_clip = 0.0, acc_kl = 0.0, acc_H = 0.0, acc_n = 0.0;
+    int64_t nl = 0;
+    if (ct == 0) nl = *p.n_loss;
+    uint32_t slot = 0, phase = 0, q = 0;
+    int64_t row = group;
+    int32_t y_n = row < p.num_rows ? p.targets[row] : 0;
+    uint8_t m_n = (row < p.num_rows && p.mask) ? p.mask[row] : 1;
+    for (; row < p.num_rows; row += ngroups) {
+      const int32_t y = y_n;
+      const uint8_t m = m_n;
+      const int64_t nrow = row + ngroups;
+      if (nrow < p.num_rows) {
+        y_n = p.targets[nrow];
+        m_n = p.mask ? p.mask[nrow] : 1;
+      }
+      if (!row_active(p, y, m)) {
+        inactive_row<T, kModeBwdPartials>(p, row, ct, crank, c0, segn, m != 0);
+        continue;
+      }
+      const int64_t ylc64 = int64_t(y) - p.vocab_start - c0;
+      const int ylc = (ylc64 >= 0 && ylc64 < segn) ? int(ylc64) : -1;
+      if (ct == 0) {
+        Stat tot{-INFINITY, 0.f, 0.f};
+        float zyt = 0.f;
+        for (int k = 0; k < p.nshards; ++k) {
+          const float4 P = p.partials_in[int64_t(k) * p.num_rows + row];
+          tot = combine(tot, Stat{P.x, P.y, P.z});
+          zyt += P.w;
+        }
+        const RowStats rs = finalize(tot, zyt);
+        const float old_lp = p.old_logp[row];
+        const float ref_lp = p.ref_logp ? p.ref_logp[row] : 0.f;
+        const LossOut lo = loss_terms(p, rs.logp, p.row_traj[row], old_lp, ref_lp, nl);
+        if (crank == 0) {
+          acc_L += lo.L;
+          acc_clip += lo.clipped ? 1.0 : 0.0;
+          acc_kl += lo.kl;
+          acc_H += double(rs.H);
+          acc_n += 1.0;
+          if (p.logp) p.logp[row] = rs.logp;
+          if (p.entropy) p.entropy[row] = rs.H;
+        }
+        S.rowbc[q & 1u] = make_float4(rs.L2, lo.coef, 0.f, 0.f);
+      }
+      named_bar_sync(1, kNCT);
+      const float4 bc = S.rowbc[q & 1u];
+      const float L2 = bc.x, coef = bc.y;
+      char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
+      for (int c = 0; c < nch; ++c) {
+        mbar_wait(&S.full[slot], phase);
+        const uint8_t* buf = ring + size_t(slot) * kChunkBytes;
+#pragma unroll
+        for (int k = 0; k < kVPT; ++k) {
+          const int vi = ct + k * kNCT;
+          const int lc = c * CE + vi * EV;
+          if (lc >= segn) continue;
+          const uint4 w = *reinterpret_cast<const uint4*>(buf + vi * 16);
+          float x[EV], g[EV];
+          VT::unpack(w, x);
+#pragma unroll
+          for (int i = 0; i < EV; ++i) g[i] = __fmul_rn(coef, ex2(__fmaf_rn(x[i], s2, -L2)));
+          if (unsigned(ylc - lc) < unsigned(EV)) {
+#pragma unroll
+            for (int i = 0; i < EV; ++i)
+              if (lc + i == ylc) g[i] = __fsub_rn(g[i], coef);
+          }
+          if (lc + EV <= segn) {
+            stg_cs_v4(drow + size_t(lc) * sizeof(T), VT::pack(g));
+          } else {
+#pragma unroll
+            for (int i = 0; i < EV; ++i)
+              if (lc + i < segn) VT::store1(drow, lc + i, g[i]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[slot]);
+        if (++slot == kSlots) {
+          slot = 0;
+          phase ^= 1u;
+        }
+      }
+      ++q;
+    }
+    if (ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl);
+  }
   if (csize > 1) cluster_sync_all();
 }
 
-// ---- vocab-shard combine (otk_logprob_entropy_combine): same combine / finalize as k_rows ----------
+// ---- vocab-shard combine (otk_logprob_entropy_combine): same combine / finalize as the row kernels -----
 __global__ void k_combine(int64_t num_rows, int nshards, const float4* __restrict__ partials,
                           const uint8_t* __restrict__ row_mask, float* logp, float* entropy, float* lse) {
   for (int64_t row = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; row < num_rows;
@@ -552,10 +765,10 @@ __global__ void k_combine(int64_t num_rows, int nshards, const float4* __restric
   }
 }
 
-// ---- launchers -------------------------------------------------------------------------------------
-template <typename T, int MODE>
-static cudaError_t launch_rows_t(const otk_ctx* ctx, const RowParams& p, cudaStream_t s, int* grid_out) {
-  auto kern = k_rows<T, MODE>;
+// ---- launchers ---------------------------------------------------------------------------------------
+template <typename KernelT>
+static cudaError_t launch_row_kernel(KernelT kern, const otk_ctx* ctx, const RowParams& p, cudaStream_t s,
+                                     int* grid_out) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes));
   if (e != cudaSuccess) return e;
   int64_t groups = ctx->num_sms / p.csize;
@@ -582,18 +795,19 @@ static cudaError_t launch_rows_t(const otk_ctx* ctx, const RowParams& p, cudaStr
 cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const RowParams& p, cudaStream_t s,
                         int* grid_out) {
   if (dtype == OTK_BF16) {
+    using B = __nv_bfloat16;
     switch (mode) {
-      case kModeFwd: return launch_rows_t<__nv_bfloat16, kModeFwd>(ctx, p, s, grid_out);
-      case kModePartial: return launch_rows_t<__nv_bfloat16, kModePartial>(ctx, p, s, grid_out);
-      case kModeBwd: return launch_rows_t<__nv_bfloat16, kModeBwd>(ctx, p, s, grid_out);
-      case kModeBwdPartials: return launch_rows_t<__nv_bfloat16, kModeBwdPartials>(ctx, p, s, grid_out);
+      case kModeFwd: return launch_row_kernel(k_rows_tm<B, kModeFwd>, ctx, p, s, grid_out);
+      case kModePartial: return launch_row_kernel(k_rows_tm<B, kModePartial>, ctx, p, s, grid_out);
+      case kModeBwd: return launch_row_kernel(k_rows_tm<B, kModeBwd>, ctx, p, s, grid_out);
+      case kModeBwdPartials: return launch_row_kernel(k_rows_stream<B>, ctx, p, s, grid_out);
     }
   } else {
     switch (mode) {
-      case kModeFwd: return launch_rows_t<float, kModeFwd>(ctx, p, s, grid_out);
-      case kModePartial: return launch_rows_t<float, kModePartial>(ctx, p, s, grid_out);
-      case kModeBwd: return launch_rows_t<float, kModeBwd>(ctx, p, s, grid_out);
-      case kModeBwdPartials: return launch_rows_t<float, kModeBwdPartials>(ctx, p, s, grid_out);
+      case kModeFwd: return launch_row_kernel(k_rows_tm<float, kModeFwd>, ctx, p, s, grid_out);
+      case kModePartial: return launch_row_kernel(k_rows_tm<float, kModePartial>, ctx, p, s, grid_out);
+      case kModeBwd: return launch_row_kernel(k_rows_tm<float, kModeBwd>, ctx, p, s, grid_out);
+      case kModeBwdPartials: return launch_row_kernel(k_rows_stream<float>, ctx, p, s, grid_out);
     }
   }
   return cudaErrorInvalidValue;

@@ -37,11 +37,11 @@ otk_status cuda_fail(cudaError_t e, const char* where) {
 size_t dtype_size(otk_dtype d) { return d == OTK_BF16 ? 2 : 4; }
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// Cluster size for the row kernels: the smallest power of two whose per-CTA column segment fits
-// the resident ring budget. Every mode uses the same rule so that the forward
-// (3) and the fused loss (4) reduce in the same order (bitwise-equal logp: on-policy ratio = 1).
+// Cluster size for the row kernels: the smallest power of two whose per-CTA column segment fits the
+// tensor-memory-resident budget (kMaxChunks chunks). Every mode uses the same rule so that the
+// forward (3) and the fused loss (4) reduce in the same order (bitwise-equal logp: on-policy ratio = 1).
 int choose_csize(int64_t vocab, size_t es, int* seg_elems) {
-  const int64_t budget = int64_t(otk::kSlots - otk::kMinLookahead) * otk::kChunkBytes;
+  const int64_t budget = int64_t(otk::kMaxChunks) * otk::kChunkBytes;
   for (int c = 1; c <= 8; c *= 2) {
     int64_t seg = (vocab + c - 1) / c;
     seg = (seg + 7) / 8 * 8;
@@ -62,7 +62,7 @@ otk_status check_rows(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld,
   OTK_REQUIRE(aligned16(logits) && (ld * int64_t(dtype_size(dtype))) % 16 == 0, OTK_ERR_ALIGNMENT,
               "logits base and row stride must be 16-byte aligned");
   *csize = choose_csize(vocab, dtype_size(dtype), seg_elems);
-  OTK_REQUIRE(*csize > 0, OTK_ERR_SHAPE, "vocab too large for the row kernel (> 8 x 188 KB per row)");
+  OTK_REQUIRE(*csize > 0, OTK_ERR_SHAPE, "vocab too large for the row kernel (> 8 x 152 KB per row)");
   return OTK_OK;
 }
 

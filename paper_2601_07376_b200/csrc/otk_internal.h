@@ -32,11 +32,13 @@ constexpr int kStatSlots = 8;
 enum Ticket { kTicketMasks = 0, kTicketRows = 1 };
 
 // Fused row kernel configuration.
+// 1 producer warp + 8 consumer warps (2 per TMEM lane quadrant); an 8 KB chunk is exactly
+// 2 x 16-byte vectors per consumer thread.
 constexpr int kChunkBytes = 8192;        // one bulk-TMA transfer / ring slot
 constexpr int kSlots = 27;               // ring depth: 216 KB of shared memory per CTA
 constexpr int kConsumerWarps = 8;        // 256 compute threads
-constexpr int kThreads = 32 * (1 + kConsumerWarps);  // + 1 producer warp
-constexpr int kMinLookahead = 4;         // slots kept free for the next row in resident (BWD) mode
+constexpr int kThreads = 32 * (1 + kConsumerWarps);
+constexpr int kMaxChunks = 19;           // a CTA's row segment (<= 19 chunks, 152 KB) is kept in TMEM
 
 enum RowMode : int {
   kModeFwd = 0,       // (3): logp / entropy / lse
