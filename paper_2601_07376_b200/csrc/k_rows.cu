@@ -77,6 +77,49 @@ __device__ __forceinline__ RowStats finalize(const Stat t, const float zy) {
   return r;
 }
 
+// ---- packed fp32 pairs (sm_100 FFMA2 / FADD2 / FMUL2: two lanes per instruction) -----------------
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_split(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float f2_sum(uint64_t v) {
+  float lo, hi;
+  f2_split(v, lo, hi);
+  return __fadd_rn(lo, hi);
+}
+
+// One element pair of pass 1: d = s2*x - m; e = 2^d; S += e; T += e*d (per-lane fp32 chains).
+__device__ __forceinline__ void pass1_pair(float xlo, float xhi, uint64_t s2x2, uint64_t negm2, uint64_t& accS,
+                                           uint64_t& accT, float& e0, float& e1) {
+  const uint64_t d2 = ffma2(f2(xlo, xhi), s2x2, negm2);
+  float d0, d1;
+  f2_split(d2, d0, d1);
+  e0 = ex2(d0);
+  e1 = ex2(d1);
+  const uint64_t e2 = f2(e0, e1);
+  accS = fadd2(accS, e2);
+  accT = ffma2(e2, d2, accT);
+}
+
 // ---- element-type traits ------------------------------------------------------------------------
 template <typename T>
 struct Vec;
@@ -109,6 +152,23 @@ struct Vec<float> {
   __device__ static __forceinline__ float max_final(float acc) { return acc; }
   __device__ static __forceinline__ float load1(const void* base, int64_t i) {
     return reinterpret_cast<const float*>(base)[i];
+  }
+  // pass 1 on one 16-byte vector (4 fp32 logits): e kept at full precision
+  template <bool kKeepE>
+  __device__ static __forceinline__ uint4 pass1(const uint4 v, uint64_t s2x2, uint64_t negm2, uint64_t (&aS)[2],
+                                                uint64_t (&aT)[2]) {
+    float e[4];
+    pass1_pair(fmaxf(__uint_as_float(v.x), -1e30f), fmaxf(__uint_as_float(v.y), -1e30f), s2x2, negm2, aS[0], aT[0],
+               e[0], e[1]);
+    pass1_pair(fmaxf(__uint_as_float(v.z), -1e30f), fmaxf(__uint_as_float(v.w), -1e30f), s2x2, negm2, aS[1], aT[1],
+               e[2], e[3]);
+    return kKeepE ? pack(e) : make_uint4(0, 0, 0, 0);
+  }
+  __device__ static __forceinline__ uint4 pass2(const uint4 e, uint64_t kt2) {
+    float g[4];
+    f2_split(fmul2(f2(__uint_as_float(e.x), __uint_as_float(e.y)), kt2), g[0], g[1]);
+    f2_split(fmul2(f2(__uint_as_float(e.z), __uint_as_float(e.w)), kt2), g[2], g[3]);
+    return pack(g);
   }
   __device__ static __forceinline__ void store1(void* base, int64_t i, float v) {
     reinterpret_cast<float*>(base)[i] = v;
@@ -163,6 +223,34 @@ struct Vec<__nv_bfloat16> {
   __device__ static __forceinline__ float max_final(uint32_t acc) { return fmaxf(bf_lo(acc), bf_hi(acc)); }
   __device__ static __forceinline__ float load1(const void* base, int64_t i) {
     return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[i]);
+  }
+  // pass 1 on one 16-byte vector (8 bf16 logits). -inf (anything below -1e30) is clamped to -1e30 with
+  // one packed max per pair, so e = 0 and e*d = 0 without a per-element guard. e = 2^(y - m) in (0, 1]
+  // is kept as bf16 (relative error 2^-9; DESIGN.md §6 error budget).
+  __device__ static __forceinline__ uint32_t pass1_word(uint32_t w, uint64_t s2x2, uint64_t negm2, uint64_t& aS,
+                                                        uint64_t& aT) {
+    w = bmax2(w, 0xf14af14au);  // bf16x2(-1.0e30)
+    float e0, e1;
+    pass1_pair(bf_lo(w), bf_hi(w), s2x2, negm2, aS, aT, e0, e1);
+    return pack_bf16x2(e0, e1);
+  }
+  template <bool kKeepE>
+  __device__ static __forceinline__ uint4 pass1(const uint4 v, uint64_t s2x2, uint64_t negm2, uint64_t (&aS)[2],
+                                                uint64_t (&aT)[2]) {
+    uint4 r;
+    r.x = pass1_word(v.x, s2x2, negm2, aS[0], aT[0]);
+    r.y = pass1_word(v.y, s2x2, negm2, aS[1], aT[1]);
+    r.z = pass1_word(v.z, s2x2, negm2, aS[0], aT[0]);
+    r.w = pass1_word(v.w, s2x2, negm2, aS[1], aT[1]);
+    return r;
+  }
+  __device__ static __forceinline__ uint32_t pass2_word(uint32_t w, uint64_t kt2) {
+    float g0, g1;
+    f2_split(fmul2(f2(bf_lo(w), bf_hi(w)), kt2), g0, g1);
+    return pack_bf16x2(g0, g1);
+  }
+  __device__ static __forceinline__ uint4 pass2(const uint4 e, uint64_t kt2) {
+    return make_uint4(pass2_word(e.x, kt2), pass2_word(e.y, kt2), pass2_word(e.z, kt2), pass2_word(e.w, kt2));
   }
   __device__ static __forceinline__ void store1(void* base, int64_t i, float v) {
     reinterpret_cast<__nv_bfloat16*>(base)[i] = __float2bfloat16_rn(v);
@@ -229,14 +317,11 @@ __device__ __forceinline__ void inactive_row(const RowParams& p, int64_t row, in
   if (bad_target && ct == 0 && crank == 0) set_error(p.err, OTK_ERR_TARGET_RANGE);
   if (MODE == kModeBwd || MODE == kModeBwdPartials) {
     if (p.zero_masked) {
-      char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
-      for (int lc = ct * EV; lc < segn; lc += kNCT * EV) {
-        if (lc + EV <= segn) {
-          stg_cs_v4(drow + size_t(lc) * sizeof(T), make_uint4(0, 0, 0, 0));
-        } else {
-          for (int k = lc; k < segn; ++k) Vec<T>::store1(drow, k, 0.f);
-        }
-      }
+      char* base = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
+      const int nv = segn / EV;  // full 16-byte vectors
+      for (int v = ct; v < nv; v += kNCT) stg_cs_v4(base + size_t(v) * 16, make_uint4(0, 0, 0, 0));
+      if (ct == 0)
+        for (int k = nv * EV; k < segn; ++k) Vec<T>::store1(base, k, 0.f);
     }
     if (ct == 0 && crank == 0) {
       if (p.logp) p.logp[row] = 0.f;
@@ -256,7 +341,8 @@ __device__ __forceinline__ void inactive_row(const RowParams& p, int64_t row, in
 // ---- per-token loss (north_star (4); same definition as oracle_ref.row_loss_terms) ----------------
 struct LossOut {
   double L, kl;
-  float coef;
+  float coef;  // -s * (m/N) * dL/dlogp
+  float gy;    // coef * (p_y - 1): the target column's dlogit
   bool clipped;
 };
 __device__ __forceinline__ LossOut loss_terms(const RowParams& p, float logp, int32_t rt, float old_lp,
@@ -297,7 +383,9 @@ __device__ __forceinline__ LossOut loss_terms(const RowParams& p, float logp, in
   o.kl = kl;
   o.clipped = clipped;
   const double invN = nl > 0 ? 1.0 / double(nl) : 0.0;
-  o.coef = float(-double(p.scale) * invN * G);
+  const double cf = -double(p.scale) * invN * G;
+  o.coef = float(cf);
+  o.gy = float(cf * (exp(lp) - 1.0));
   return o;
 }
 
@@ -469,22 +557,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       }
 
       // ---------------- pass 1: online max / sum 2^(y-m) / sum 2^(y-m)(y-m), one exponential per element
+      // owner of the target column (one thread of one CTA of the cluster): chunk cy, thread owner_ct
+      const int cy = ylc >= 0 ? ylc / CE : -1;
+      const int owner_ct = ylc >= 0 ? ((ylc - cy * CE) / EV) % kNCT : -1;
+      const uint64_t s2x2 = f2(s2, s2);
       Stat st{-INFINITY, 0.f, 0.f};
       for (int c = 0; c < nch; ++c) {
         mbar_wait(&S.full[slot], phase);
         const uint8_t* buf = ring + size_t(slot) * kChunkBytes;
-        uint4 v[kVPT];
-        typename VT::MaxAcc macc = VT::max_init();
-#pragma unroll
-        for (int k = 0; k < kVPT; ++k) {
-          const int vi = ct + k * kNCT;
-          const int lc = c * CE + vi * EV;
-          uint4 w = *reinterpret_cast<const uint4*>(buf + vi * 16);
-          if (lc + EV > segn) w = VT::mask_tail(w, segn - lc);
-          v[k] = w;
-          if (unsigned(ylc - lc) < unsigned(EV)) S.zy = __fmul_rn(p.scale, VT::load1(buf, ylc - c * CE));
-          macc = VT::max_acc(macc, w);
+        uint4 v0 = *reinterpret_cast<const uint4*>(buf + ct * 16);
+        uint4 v1 = *reinterpret_cast<const uint4*>(buf + (ct + kNCT) * 16);
+        if (c == nch - 1) {  // the segment's last chunk may be partial: lanes past segn become -inf
+          const int lc0 = c * CE + ct * EV, lc1 = lc0 + kNCT * EV;
+          if (lc0 + EV > segn) v0 = VT::mask_tail(v0, segn - lc0);
+          if (lc1 + EV > segn) v1 = VT::mask_tail(v1, segn - lc1);
         }
+        if (c == cy && ct == owner_ct) S.zy = __fmul_rn(p.scale, VT::load1(buf, ylc - c * CE));
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty[slot]);
         if (++slot == kSlots) {
@@ -492,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
           phase ^= 1u;
         }
         // running max update (rescale the sums when it grows; exact no-op otherwise)
-        const float mx = VT::max_final(macc);
+        const float mx = VT::max_final(VT::max_acc(VT::max_acc(VT::max_init(), v0), v1));
         if (mx != -INFINITY) {
           const float mn = fmaxf(st.m, __fmul_rn(mx, s2));
           if (mn > st.m) {
@@ -505,25 +593,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
           }
         }
         const float mref = (st.m == -INFINITY) ? 0.f : st.m;
-        float sa[4] = {0.f, 0.f, 0.f, 0.f}, ta[4] = {0.f, 0.f, 0.f, 0.f};
-        uint4 ev[kVPT];
-#pragma unroll
-        for (int k = 0; k < kVPT; ++k) {
-          float x[EV], e[EV];
-          VT::unpack(v[k], x);
-#pragma unroll
-          for (int i = 0; i < EV; ++i) {
-            const float d = fmaxf(__fmaf_rn(x[i], s2, -mref), -256.f);  // -inf logits -> e = 0, e*d = 0
-            e[i] = ex2(d);
-            sa[i & 3] = __fadd_rn(sa[i & 3], e[i]);
-            ta[i & 3] = __fmaf_rn(e[i], d, ta[i & 3]);
-          }
-          if (kBwd) ev[k] = VT::pack_e(e);
-        }
-        st.s = __fadd_rn(st.s, __fadd_rn(__fadd_rn(sa[0], sa[1]), __fadd_rn(sa[2], sa[3])));
-        st.t = __fadd_rn(st.t, __fadd_rn(__fadd_rn(ta[0], ta[1]), __fadd_rn(ta[2], ta[3])));
+        const uint64_t negm2 = f2(-mref, -mref);
+        uint64_t aS[2] = {0ull, 0ull}, aT[2] = {0ull, 0ull};
+        const uint4 e0 = VT::template pass1<kBwd>(v0, s2x2, negm2, aS, aT);
+        const uint4 e1 = VT::template pass1<kBwd>(v1, s2x2, negm2, aS, aT);
+        st.s = __fadd_rn(st.s, __fadd_rn(f2_sum(aS[0]), f2_sum(aS[1])));
+        st.t = __fadd_rn(st.t, __fadd_rn(f2_sum(aT[0]), f2_sum(aT[1])));
         if (kBwd) {
-          tmem_st8(tm + uint32_t(8 * c), ev[0], ev[1]);
+          tmem_st8(tm + uint32_t(8 * c), e0, e1);
           tmem_st1(tm + uint32_t(kColM + c), __float_as_uint(mref));
         }
       }
@@ -556,45 +633,45 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
               if (p.logp) p.logp[row] = rs.logp;
               if (p.entropy) p.entropy[row] = rs.H;
             }
-            S.rowbc[q & 1u] = make_float4(rs.L2, lo.coef, 0.f, 0.f);
+            S.rowbc[q & 1u] = make_float4(rs.L2, lo.coef, lo.gy, 0.f);
           }
         }
       }
       named_bar_sync(1, kNCT);
 
       if (kBwd) {
-        // ---------------- pass 2: dlogits = coef * (e * 2^(m_c - lse) - onehot), e from TMEM -----------
+        // ---------------- pass 2: dlogits = coef * e * 2^(m_c - lse) from TMEM; target column fixed below
         const float4 bc = S.rowbc[q & 1u];
         const float coef = bc.y;
         char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
         for (int c = 0; c < nch; ++c) {
-          uint4 ev[kVPT];
+          uint4 e0, e1;
           uint32_t mw;
-          tmem_ld8_1(tm + uint32_t(8 * c), tm + uint32_t(kColM + c), ev[0], ev[1], mw);
+          tmem_ld8_1(tm + uint32_t(8 * c), tm + uint32_t(kColM + c), e0, e1, mw);
           const float kt = __fmul_rn(coef, ex2(__fsub_rn(__uint_as_float(mw), bc.x)));
+          const uint64_t kt2 = f2(kt, kt);
+          const uint4 g0 = VT::pass2(e0, kt2), g1 = VT::pass2(e1, kt2);
+          const int lc0 = c * CE + ct * EV, lc1 = lc0 + kNCT * EV;
+          if (c < nch - 1) {
+            stg_cs_v4(drow + size_t(lc0) * sizeof(T), g0);
+            stg_cs_v4(drow + size_t(lc1) * sizeof(T), g1);
+          } else {  // last (possibly partial) chunk
+            const uint4 gg[2] = {g0, g1};
+            const int lcs[2] = {lc0, lc1};
 #pragma unroll
-          for (int k = 0; k < kVPT; ++k) {
-            const int lc = c * CE + (ct + k * kNCT) * EV;
-            if (lc < segn) {
-              float e[EV], g[EV];
-              VT::unpack_e(ev[k], e);
-#pragma unroll
-              for (int i = 0; i < EV; ++i) g[i] = __fmul_rn(e[i], kt);
-              if (unsigned(ylc - lc) < unsigned(EV)) {
-#pragma unroll
-                for (int i = 0; i < EV; ++i)
-                  if (lc + i == ylc) g[i] = __fsub_rn(g[i], coef);
-              }
-              if (lc + EV <= segn) {
-                stg_cs_v4(drow + size_t(lc) * sizeof(T), VT::pack(g));
-              } else {
-#pragma unroll
-                for (int i = 0; i < EV; ++i)
-                  if (lc + i < segn) VT::store1(drow, lc + i, g[i]);
+            for (int k = 0; k < 2; ++k) {
+              if (lcs[k] + EV <= segn) {
+                stg_cs_v4(drow + size_t(lcs[k]) * sizeof(T), gg[k]);
+              } else if (lcs[k] < segn) {
+                float g[EV];
+                VT::unpack(gg[k], g);
+                for (int i = 0; i < EV && lcs[k] + i < segn; ++i) VT::store1(drow, lcs[k] + i, g[i]);
               }
             }
           }
         }
+        // target column: coef * (p_y - 1), overwriting this thread's own vector store (program order)
+        if (ct == owner_ct) VT::store1(drow, ylc, bc.z);
       }
       ++q;
     }
