@@ -261,29 +261,36 @@ struct Smem {
   uint64_t full[kSlots];
   uint64_t empty[kSlots];
   uint64_t xbar[2];
-  float4 xrecv[2][8];
-  float4 wred[kConsumerWarps];
-  float4 rowbc[2];
-  float zy;
+  float4 xrecv[2][8];                 // peer partials, double-buffered by active-row parity
+  float4 wred[2][kConsumerWarps];     // warp partials, double-buffered by active-row parity
+  float4 rowbc[2];                    // (stream kernel) row broadcast
+  unsigned long long zy[2];           // (row tag << 32 | bits of s * x_target), by parity
+  uint32_t tmem_base;
 };
+constexpr int kZeroBytes = 4096;  // zero block: source of the bulk stores that zero-fill masked rows
 constexpr size_t kRingBytes = size_t(kSlots) * kChunkBytes;
-constexpr size_t kSmemBytes = kRingBytes + sizeof(Smem);
+constexpr size_t kSmemBytes = kRingBytes + kZeroBytes + sizeof(Smem);
 
 __device__ __forceinline__ bool row_active(const RowParams& p, int32_t y, uint8_t m) {
   return m && y >= 0 && int64_t(y) < p.vocab_total;
 }
 
-// ---- producer: bulk-TMA every active row's column segment, chunk by chunk, into the ring ------------
-template <typename T>
-__device__ __forceinline__ void produce(const RowParams& p, uint8_t* ring, Smem& S, int64_t group,
-                                        int64_t ngroups, int64_t c0, uint32_t seg_bytes, int nch) {
+// ---- producer: bulk-TMA every active row's column segment, chunk by chunk, into the ring; zero-fill
+// the segment of every inactive row with bulk async stores from a zeroed shared-memory block --------------
+template <typename T, bool kZeroFill>
+__device__ __forceinline__ void produce(const RowParams& p, uint8_t* ring, const uint8_t* zero, Smem& S,
+                                        int64_t group, int64_t ngroups, int64_t c0, int segn, uint32_t seg_bytes,
+                                        int nch) {
   const uint64_t pol = policy_evict_first();
   const char* base = reinterpret_cast<const char*>(p.logits) + c0 * int64_t(sizeof(T));
+  char* dbase = reinterpret_cast<char*>(p.dlogits) + c0 * int64_t(sizeof(T));
   const int64_t row_bytes = p.ld * int64_t(sizeof(T));
+  const uint32_t zero_bytes = (uint32_t(segn) * uint32_t(sizeof(T))) & ~15u;  // 16-byte multiple part
   uint32_t slot = 0, phase = 0;
   int64_t row = group;
   int32_t y_n = row < p.num_rows ? p.targets[row] : 0;
   uint8_t m_n = (row < p.num_rows && p.mask) ? p.mask[row] : 1;
+  bool pending = false;
   for (; row < p.num_rows; row += ngroups) {
     const int32_t y = y_n;
     const uint8_t m = m_n;
@@ -292,7 +299,17 @@ __device__ __forceinline__ void produce(const RowParams& p, uint8_t* ring, Smem&
       y_n = p.targets[nrow];
       m_n = p.mask ? p.mask[nrow] : 1;
     }
-    if (!row_active(p, y, m)) continue;
+    if (!row_active(p, y, m)) {
+      if (kZeroFill && p.zero_masked && zero_bytes) {
+        char* dst = dbase + row * row_bytes;
+        for (uint32_t off = 0; off < zero_bytes; off += kZeroBytes)
+          bulk_s2g(dst + off, zero, min(uint32_t(kZeroBytes), zero_bytes - off), pol);
+        bulk_commit();
+        bulk_wait_read_8();
+        pending = true;
+      }
+      continue;
+    }
     const char* src = base + row * row_bytes;
     uint32_t off = 0;
     for (int c = 0; c < nch; ++c) {
@@ -307,27 +324,27 @@ __device__ __forceinline__ void produce(const RowParams& p, uint8_t* ring, Smem&
       }
     }
   }
+  if (pending) bulk_wait_all();
 }
 
-// ---- rows that are never read: zero-filled dlogits / zero outputs (R26) ----------------
+// ---- rows that are never read (R26): outputs 0; the dlogits zero-fill is the producer's bulk
+// stores, except a sub-16-byte tail at the end of the vocabulary, written here ---------------------------
 template <typename T, int MODE>
 __device__ __forceinline__ void inactive_row(const RowParams& p, int64_t row, int ct, uint32_t crank, int64_t c0,
                                              int segn, bool bad_target) {
-  constexpr int EV = Vec<T>::EV;
   if (bad_target && ct == 0 && crank == 0) set_error(p.err, OTK_ERR_TARGET_RANGE);
+  if (ct != 0) return;
   if (MODE == kModeBwd || MODE == kModeBwdPartials) {
     if (p.zero_masked) {
       char* base = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
-      const int nv = segn / EV;  // full 16-byte vectors
-      for (int v = ct; v < nv; v += kNCT) stg_cs_v4(base + size_t(v) * 16, make_uint4(0, 0, 0, 0));
-      if (ct == 0)
-        for (int k = nv * EV; k < segn; ++k) Vec<T>::store1(base, k, 0.f);
+      const int done = int(((uint32_t(segn) * uint32_t(sizeof(T))) & ~15u) / sizeof(T));
+      for (int k = done; k < segn; ++k) Vec<T>::store1(base, k, 0.f);
     }
-    if (ct == 0 && crank == 0) {
+    if (crank == 0) {
       if (p.logp) p.logp[row] = 0.f;
       if (p.entropy) p.entropy[row] = 0.f;
     }
-  } else if (ct == 0 && crank == 0) {
+  } else if (crank == 0) {
     if (MODE == kModeFwd) {
       p.logp[row] = 0.f;
       if (p.entropy) p.entropy[row] = 0.f;
@@ -338,97 +355,54 @@ __device__ __forceinline__ void inactive_row(const RowParams& p, int64_t row, in
   }
 }
 
-// ---- per-token loss (north_star (4); same definition as oracle_ref.row_loss_terms) ----------------
+// ---- per-token loss (north_star (4); same definition as oracle_ref.row_loss_terms), fp32 ---------------
 struct LossOut {
-  double L, kl;
+  float L, kl;
   float coef;  // -s * (m/N) * dL/dlogp
   float gy;    // coef * (p_y - 1): the target column's dlogit
   bool clipped;
 };
-__device__ __forceinline__ LossOut loss_terms(const RowParams& p, float logp, int32_t rt, float old_lp,
-                                              float ref_lp, int64_t nl) {
-  const double lp = double(logp);
-  const double A = p.adv[rt];
-  const double C = p.clamp;
-  const double draw = lp - double(old_lp);
-  const double delta = fmin(fmax(draw, -C), C);
-  const double r = exp(delta);
-  const double lo = 1.0 - p.clip_low, hi = 1.0 + p.clip_high;
-  const double rbar = fmin(fmax(r, lo), hi);
-  const double pg = fmax(-A * r, -A * rbar);
-  const bool clipped = (A > 0.0 && r > hi) || (A < 0.0 && r < lo);
-  double G = (clipped || fabs(draw) > C) ? 0.0 : -A * r;
-  double kl = 0.0;
-  const double beta = p.kl_beta;
-  if (beta != 0.0) {
-    const double ref = double(ref_lp);
-    double gk;
+struct RowSide {
+  double A;
+  float old_lp, ref_lp;
+};
+__device__ __forceinline__ LossOut loss_terms(const RowParams& p, float lp, const RowSide& sd, float invN) {
+  const float A = float(sd.A);
+  const float C = float(p.clamp);
+  const float draw = lp - sd.old_lp;
+  const float delta = fminf(fmaxf(draw, -C), C);
+  const float r = expf(delta);
+  const float lo = float(1.0 - p.clip_low), hi = float(1.0 + p.clip_high);
+  const float rbar = fminf(fmaxf(r, lo), hi);
+  const float pg = fmaxf(-A * r, -A * rbar);
+  const bool clipped = (A > 0.f && r > hi) || (A < 0.f && r < lo);
+  float G = (clipped || fabsf(draw) > C) ? 0.f : -A * r;
+  float kl = 0.f;
+  const float beta = float(p.kl_beta);
+  if (beta != 0.f) {
+    float gk;
     if (p.kl_type == OTK_KL_K3) {
-      const double dr = ref - lp;
-      const double d = fmin(fmax(dr, -C), C);
-      const double ed = exp(d);
-      kl = ed - d - 1.0;
-      gk = fabs(dr) > C ? 0.0 : 1.0 - ed;
+      const float dr = sd.ref_lp - lp;
+      const float d = fminf(fmaxf(dr, -C), C);
+      const float em1 = expm1f(d);
+      kl = em1 - d;           // e^d - d - 1 without cancellation
+      gk = fabsf(dr) > C ? 0.f : -em1;
     } else if (p.kl_type == OTK_KL_K1) {
-      kl = lp - ref;
-      gk = 1.0;
+      kl = lp - sd.ref_lp;
+      gk = 1.f;
     } else {
-      kl = 0.5 * (lp - ref) * (lp - ref);
-      gk = lp - ref;
+      kl = 0.5f * (lp - sd.ref_lp) * (lp - sd.ref_lp);
+      gk = lp - sd.ref_lp;
     }
-    G += beta * gk;
+    G = fmaf(beta, gk, G);
   }
   LossOut o;
-  o.L = pg + beta * kl;
+  o.L = fmaf(beta, kl, pg);
   o.kl = kl;
   o.clipped = clipped;
-  const double invN = nl > 0 ? 1.0 / double(nl) : 0.0;
-  const double cf = -double(p.scale) * invN * G;
-  o.coef = float(cf);
-  o.gy = float(cf * (exp(lp) - 1.0));
+  o.coef = -p.scale * invN * G;
+  o.gy = o.coef * expm1f(lp);  // coef * (p_y - 1), no cancellation when p_y -> 1
   return o;
-}
-
-// warp + CTA reduction of the per-thread Stat into S.wred (caller syncs)
-__device__ __forceinline__ void reduce_warp_to_smem(Stat st, Smem& S, int lane, int cw) {
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    Stat o;
-    o.m = __shfl_xor_sync(0xffffffffu, st.m, off);
-    o.s = __shfl_xor_sync(0xffffffffu, st.s, off);
-    o.t = __shfl_xor_sync(0xffffffffu, st.t, off);
-    st = (lane & off) ? combine(o, st) : combine(st, o);
-  }
-  if (lane == 0) S.wred[cw] = make_float4(st.m, st.s, st.t, 0.f);
-}
-
-// thread 0: CTA total -> cluster exchange (rank order) -> row total
-__device__ __forceinline__ void cta_and_cluster_total(Smem& S, int csize, uint32_t crank, uint32_t q, Stat& tot,
-                                                      float& zyt) {
-  Stat r{S.wred[0].x, S.wred[0].y, S.wred[0].z};
-#pragma unroll
-  for (int w = 1; w < kConsumerWarps; ++w) r = combine(r, Stat{S.wred[w].x, S.wred[w].y, S.wred[w].z});
-  const float zy = S.zy;
-  S.zy = 0.f;
-  if (csize > 1) {
-    const uint32_t par = q & 1u;
-    for (int dst = 0; dst < csize; ++dst) {
-      if (dst == int(crank)) continue;
-      st_async_f4(mapa(smem_u32(&S.xrecv[par][crank]), dst), r.m, r.s, r.t, zy, mapa(smem_u32(&S.xbar[par]), dst));
-    }
-    mbar_arrive_expect_tx(&S.xbar[par], 16u * uint32_t(csize - 1));
-    mbar_wait_cluster(&S.xbar[par], (q >> 1) & 1u);
-    tot = Stat{-INFINITY, 0.f, 0.f};
-    zyt = 0.f;
-    for (int k = 0; k < csize; ++k) {
-      const float4 P = (k == int(crank)) ? make_float4(r.m, r.s, r.t, zy) : S.xrecv[par][k];
-      tot = combine(tot, Stat{P.x, P.y, P.z});
-      zyt += P.w;
-    }
-  } else {
-    tot = r;
-    zyt = zy;
-  }
 }
 
 __device__ __forceinline__ void stats_epilogue(const RowParams& p, double acc_L, double acc_clip, double acc_kl,
@@ -467,9 +441,79 @@ __device__ __forceinline__ void stats_epilogue(const RowParams& p, double acc_L,
   }
 }
 
+// Shared setup of both row kernels: barriers, zero block, optional TMEM allocation (warp 1).
+template <bool kTmem>
+__device__ __forceinline__ void row_kernel_setup(Smem& S, uint8_t* zero, int warp, int csize) {
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], kConsumerWarps);
+    }
+    mbar_init(&S.xbar[0], 1);
+    mbar_init(&S.xbar[1], 1);
+    S.zy[0] = S.zy[1] = ~0ull;
+    fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < kZeroBytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(zero)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();  // the bulk-store engine (async proxy) must see the zeros
+  if (kTmem && warp == 1) {  // one warp owns the TMEM allocation (all 512 columns; 1 CTA per SM)
+    tmem_alloc(&S.tmem_base, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  if (csize > 1)
+    cluster_sync_all();
+  else
+    __syncthreads();
+  tc_fence_after();
+}
+
+// Row statistics after pass 1, computed redundantly by every consumer thread (no second barrier):
+// CTA total in warp order, then the cluster exchange of 16-byte partials (rank order).
+__device__ __forceinline__ void row_total(Smem& S, Stat st, int lane, int cw, int ct, int csize, uint32_t crank,
+                                          uint32_t q, int64_t row, Stat& tot, float& zyt) {
+  const uint32_t par = q & 1u;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    Stat o;
+    o.m = __shfl_xor_sync(0xffffffffu, st.m, off);
+    o.s = __shfl_xor_sync(0xffffffffu, st.s, off);
+    o.t = __shfl_xor_sync(0xffffffffu, st.t, off);
+    st = (lane & off) ? combine(o, st) : combine(st, o);
+  }
+  if (lane == 0) S.wred[par][cw] = make_float4(st.m, st.s, st.t, 0.f);
+  named_bar_sync(1, kNCT);
+  Stat r{S.wred[par][0].x, S.wred[par][0].y, S.wred[par][0].z};
+#pragma unroll
+  for (int w = 1; w < kConsumerWarps; ++w) r = combine(r, Stat{S.wred[par][w].x, S.wred[par][w].y, S.wred[par][w].z});
+  const unsigned long long zt = S.zy[par];
+  const float zy = (uint32_t(zt >> 32) == uint32_t(row)) ? __uint_as_float(uint32_t(zt)) : 0.f;
+  if (csize > 1) {
+    if (ct == 0) {
+      for (int dst = 0; dst < csize; ++dst) {
+        if (dst == int(crank)) continue;
+        st_async_f4(mapa(smem_u32(&S.xrecv[par][crank]), dst), r.m, r.s, r.t, zy, mapa(smem_u32(&S.xbar[par]), dst));
+      }
+      mbar_arrive_expect_tx(&S.xbar[par], 16u * uint32_t(csize - 1));
+    }
+    mbar_wait_cluster(&S.xbar[par], (q >> 1) & 1u);
+    tot = Stat{-INFINITY, 0.f, 0.f};
+    zyt = 0.f;
+    for (int k = 0; k < csize; ++k) {
+      const float4 P = (k == int(crank)) ? make_float4(r.m, r.s, r.t, zy) : S.xrecv[par][k];
+      tot = combine(tot, Stat{P.x, P.y, P.z});
+      zyt += P.w;
+    }
+  } else {
+    tot = r;
+    zyt = zy;
+  }
+}
+
 // =====================================================================================================
 // k_rows_tm: FWD / PARTIAL / BWD. Pass 1 streams each chunk from the ring exactly once (slot released
-// right away); for BWD the exponentials e = 2^(y - m_c) (f16 for bf16 input, with m_c the thread's
+// right away); for BWD the exponentials e = 2^(y - m_c) (bf16 for bf16 input, with m_c the thread's
 // running max after chunk c) and m_c are parked in TENSOR MEMORY, so pass 2 needs no second read of the
 // logits and no second exponential: softmax = e * 2^(m_c - lse).
 // =====================================================================================================
@@ -477,8 +521,8 @@ template <typename T, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
-  Smem& S = *reinterpret_cast<Smem*>(smem + kRingBytes);
-  __shared__ uint32_t s_tmem_base;
+  uint8_t* zero = smem + kRingBytes;
+  Smem& S = *reinterpret_cast<Smem*>(smem + kRingBytes + kZeroBytes);
   using VT = Vec<T>;
   constexpr int EV = VT::EV;
   constexpr int CE = kChunkBytes / int(sizeof(T));
@@ -496,39 +540,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
   const uint32_t seg_bytes = (uint32_t(segn) * uint32_t(sizeof(T)) + 15u) & ~15u;
   const int nch = int((seg_bytes + kChunkBytes - 1) / kChunkBytes);  // <= kMaxChunks (host-checked)
 
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kSlots; ++i) {
-      mbar_init(&S.full[i], 1);
-      mbar_init(&S.empty[i], kConsumerWarps);
-    }
-    mbar_init(&S.xbar[0], 1);
-    mbar_init(&S.xbar[1], 1);
-    S.zy = 0.f;
-    fence_mbar_init();
-  }
-  if (kBwd && warp == 1) {  // one warp owns the TMEM allocation (all 512 columns; 1 CTA per SM)
-    tmem_alloc(&s_tmem_base, 512);
-    tmem_relinquish();
-  }
-  tc_fence_before();
-  if (csize > 1)
-    cluster_sync_all();
-  else
-    __syncthreads();
-  tc_fence_after();
+  row_kernel_setup<kBwd>(S, zero, warp, csize);
 
   if (warp == 0) {
-    if (lane == 0 && nch > 0) produce<T>(p, ring, S, group, ngroups, c0, seg_bytes, nch);
+    if (lane == 0 && nch > 0) produce<T, kBwd>(p, ring, zero, S, group, ngroups, c0, segn, seg_bytes, nch);
     __syncwarp();
   } else {
     const int ct = threadIdx.x - 32;
     const int cw = warp - 1;
     // this warp's TMEM window: its lane quadrant (warp % 4) and one half of the 512 columns
-    const uint32_t tm = kBwd ? s_tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(256 * (cw >> 2)) : 0u;
+    const uint32_t tm = kBwd ? S.tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(256 * (cw >> 2)) : 0u;
     const float s2 = __fmul_rn(p.scale, kLog2e);
+    const uint64_t s2x2 = f2(s2, s2);
     double acc_L = 0.0, acc_clip = 0.0, acc_kl = 0.0, acc_H = 0.0, acc_n = 0.0;
     int64_t nl = 0;
-    if (kBwd && ct == 0) nl = *p.n_loss;
+    float invN = 0.f;
+    if (kBwd) {
+      nl = *p.n_loss;
+      invN = nl > 0 ? float(1.0 / double(nl)) : 0.f;
+    }
     uint32_t slot = 0, phase = 0, q = 0;
 
     int64_t row = group;
@@ -548,19 +578,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       }
       const int64_t ylc64 = int64_t(y) - p.vocab_start - c0;  // target column local to this CTA's segment
       const int ylc = (ylc64 >= 0 && ylc64 < segn) ? int(ylc64) : -1;
-      int32_t rt = 0;
-      float old_lp = 0.f, ref_lp = 0.f;
-      if (kBwd && ct == 0) {  // issued early, consumed after pass 1
-        rt = p.row_traj[row];
-        old_lp = p.old_logp[row];
-        if (p.ref_logp) ref_lp = p.ref_logp[row];
+      RowSide sd{0.0, 0.f, 0.f};
+      if (kBwd) {  // broadcast loads, issued early and consumed after pass 1
+        sd.A = p.adv[p.row_traj[row]];
+        sd.old_lp = p.old_logp[row];
+        if (p.ref_logp) sd.ref_lp = p.ref_logp[row];
       }
 
       // ---------------- pass 1: online max / sum 2^(y-m) / sum 2^(y-m)(y-m), one exponential per element
-      // owner of the target column (one thread of one CTA of the cluster): chunk cy, thread owner_ct
-      const int cy = ylc >= 0 ? ylc / CE : -1;
+      const int cy = ylc >= 0 ? ylc / CE : -1;  // the target column's chunk and owning thread
       const int owner_ct = ylc >= 0 ? ((ylc - cy * CE) / EV) % kNCT : -1;
-      const uint64_t s2x2 = f2(s2, s2);
       Stat st{-INFINITY, 0.f, 0.f};
       for (int c = 0; c < nch; ++c) {
         mbar_wait(&S.full[slot], phase);
@@ -572,7 +599,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
           if (lc0 + EV > segn) v0 = VT::mask_tail(v0, segn - lc0);
           if (lc1 + EV > segn) v1 = VT::mask_tail(v1, segn - lc1);
         }
-        if (c == cy && ct == owner_ct) S.zy = __fmul_rn(p.scale, VT::load1(buf, ylc - c * CE));
+        if (c == cy && ct == owner_ct)
+          S.zy[q & 1u] = (static_cast<unsigned long long>(uint32_t(row)) << 32) |
+                         __float_as_uint(__fmul_rn(p.scale, VT::load1(buf, ylc - c * CE)));
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty[slot]);
         if (++slot == kSlots) {
@@ -605,73 +634,72 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
         }
       }
       if (kBwd) tmem_wait_st();
-      reduce_warp_to_smem(st, S, lane, cw);
-      named_bar_sync(1, kNCT);
 
-      if (ct == 0) {
-        Stat tot;
-        float zyt;
-        cta_and_cluster_total(S, csize, crank, q, tot, zyt);
-        if (MODE == kModePartial) {
-          if (crank == 0) p.partials_out[row] = make_float4(tot.m, tot.s, tot.t, zyt);
-        } else {
-          const RowStats rs = finalize(tot, zyt);
-          if (MODE == kModeFwd) {
-            if (crank == 0) {
-              p.logp[row] = rs.logp;
-              if (p.entropy) p.entropy[row] = rs.H;
-              if (p.lse) p.lse[row] = rs.lse;
-            }
-          } else {
-            const LossOut lo = loss_terms(p, rs.logp, rt, old_lp, ref_lp, nl);
-            if (crank == 0) {
-              acc_L += lo.L;
-              acc_clip += lo.clipped ? 1.0 : 0.0;
-              acc_kl += lo.kl;
-              acc_H += double(rs.H);
-              acc_n += 1.0;
-              if (p.logp) p.logp[row] = rs.logp;
-              if (p.entropy) p.entropy[row] = rs.H;
-            }
-            S.rowbc[q & 1u] = make_float4(rs.L2, lo.coef, lo.gy, 0.f);
+      Stat tot;
+      float zyt;
+      row_total(S, st, lane, cw, ct, csize, crank, q, row, tot, zyt);
+      if (MODE == kModePartial) {
+        if (ct == 0 && crank == 0) p.partials_out[row] = make_float4(tot.m, tot.s, tot.t, zyt);
+      } else {
+        const RowStats rs = finalize(tot, zyt);
+        if (MODE == kModeFwd) {
+          if (ct == 0 && crank == 0) {
+            p.logp[row] = rs.logp;
+            if (p.entropy) p.entropy[row] = rs.H;
+            if (p.lse) p.lse[row] = rs.lse;
           }
-        }
-      }
-      named_bar_sync(1, kNCT);
-
-      if (kBwd) {
-        // ---------------- pass 2: dlogits = coef * e * 2^(m_c - lse) from TMEM; target column fixed below
-        const float4 bc = S.rowbc[q & 1u];
-        const float coef = bc.y;
-        char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
-        for (int c = 0; c < nch; ++c) {
-          uint4 e0, e1;
-          uint32_t mw;
-          tmem_ld8_1(tm + uint32_t(8 * c), tm + uint32_t(kColM + c), e0, e1, mw);
-          const float kt = __fmul_rn(coef, ex2(__fsub_rn(__uint_as_float(mw), bc.x)));
-          const uint64_t kt2 = f2(kt, kt);
-          const uint4 g0 = VT::pass2(e0, kt2), g1 = VT::pass2(e1, kt2);
-          const int lc0 = c * CE + ct * EV, lc1 = lc0 + kNCT * EV;
-          if (c < nch - 1) {
-            stg_cs_v4(drow + size_t(lc0) * sizeof(T), g0);
-            stg_cs_v4(drow + size_t(lc1) * sizeof(T), g1);
-          } else {  // last (possibly partial) chunk
-            const uint4 gg[2] = {g0, g1};
-            const int lcs[2] = {lc0, lc1};
+        } else {
+          const LossOut lo = loss_terms(p, rs.logp, sd, invN);
+          if (ct == 0 && crank == 0) {
+            acc_L += double(lo.L);
+            acc_clip += lo.clipped ? 1.0 : 0.0;
+            acc_kl += double(lo.kl);
+            acc_H += double(rs.H);
+            acc_n += 1.0;
+            if (p.logp) p.logp[row] = rs.logp;
+            if (p.entropy) p.entropy[row] = rs.H;
+          }
+          // ---------------- pass 2: dlogits = coef * e * 2^(m_c - lse) from TMEM (2-deep load pipeline)
+          char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
+          uint4 ea, eb;
+          uint32_t ma;
+          tmem_ld8_1_issue(tm, tm + uint32_t(kColM), ea, eb, ma);
+          tmem_wait_ld_dep(ea, eb, ma);
+          for (int c = 0; c < nch; ++c) {
+            uint4 na = ea, nb = eb;
+            uint32_t nm = ma;
+            if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), na, nb, nm);
+            const float kt = __fmul_rn(lo.coef, ex2(__fsub_rn(__uint_as_float(ma), rs.L2)));
+            const uint64_t kt2 = f2(kt, kt);
+            const uint4 g0 = VT::pass2(ea, kt2), g1 = VT::pass2(eb, kt2);
+            const int lc0 = c * CE + ct * EV, lc1 = lc0 + kNCT * EV;
+            if (c < nch - 1) {
+              stg_cs_v4(drow + size_t(lc0) * sizeof(T), g0);
+              stg_cs_v4(drow + size_t(lc1) * sizeof(T), g1);
+            } else {  // last (possibly partial) chunk
+              const uint4 gg[2] = {g0, g1};
+              const int lcs[2] = {lc0, lc1};
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              if (lcs[k] + EV <= segn) {
-                stg_cs_v4(drow + size_t(lcs[k]) * sizeof(T), gg[k]);
-              } else if (lcs[k] < segn) {
-                float g[EV];
-                VT::unpack(gg[k], g);
-                for (int i = 0; i < EV && lcs[k] + i < segn; ++i) VT::store1(drow, lcs[k] + i, g[i]);
+              for (int k = 0; k < 2; ++k) {
+                if (lcs[k] + EV <= segn) {
+                  stg_cs_v4(drow + size_t(lcs[k]) * sizeof(T), gg[k]);
+                } else if (lcs[k] < segn) {
+                  float g[EV];
+                  VT::unpack(gg[k], g);
+                  for (int i = 0; i < EV && lcs[k] + i < segn; ++i) VT::store1(drow, lcs[k] + i, g[i]);
+                }
               }
             }
+            if (c + 1 < nch) {
+              tmem_wait_ld_dep(na, nb, nm);
+              ea = na;
+              eb = nb;
+              ma = nm;
+            }
           }
+          // target column: coef * (p_y - 1), overwriting this thread's own vector store (program order)
+          if (ct == owner_ct) VT::store1(drow, ylc, lo.gy);
         }
-        // target column: coef * (p_y - 1), overwriting this thread's own vector store (program order)
-        if (ct == owner_ct) VT::store1(drow, ylc, bc.z);
       }
       ++q;
     }
@@ -684,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
     __syncthreads();
   if (kBwd && warp == 1) {
     tc_fence_after();
-    tmem_dealloc(s_tmem_base, 512);
+    tmem_dealloc(S.tmem_base, 512);
   }
 }
 
@@ -695,7 +723,8 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
-  Smem& S = *reinterpret_cast<Smem*>(smem + kRingBytes);
+  uint8_t* zero = smem + kRingBytes;
+  Smem& S = *reinterpret_cast<Smem*>(smem + kRingBytes + kZeroBytes);
   using VT = Vec<T>;
   constexpr int EV = VT::EV;
   constexpr int CE = kChunkBytes / int(sizeof(T));
@@ -711,27 +740,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) 
   const uint32_t seg_bytes = (uint32_t(segn) * uint32_t(sizeof(T)) + 15u) & ~15u;
   const int nch = int((seg_bytes + kChunkBytes - 1) / kChunkBytes);
 
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kSlots; ++i) {
-      mbar_init(&S.full[i], 1);
-      mbar_init(&S.empty[i], kConsumerWarps);
-    }
-    fence_mbar_init();
-  }
-  if (csize > 1)
-    cluster_sync_all();
-  else
-    __syncthreads();
+  row_kernel_setup<false>(S, zero, warp, csize);
 
   if (warp == 0) {
-    if (lane == 0 && nch > 0) produce<T>(p, ring, S, group, ngroups, c0, seg_bytes, nch);
+    if (lane == 0 && nch > 0) produce<T, true>(p, ring, zero, S, group, ngroups, c0, segn, seg_bytes, nch);
     __syncwarp();
   } else {
     const int ct = threadIdx.x - 32;
     const float s2 = __fmul_rn(p.scale, kLog2e);
     double acc_L = 0.0, acc_clip = 0.0, acc_kl = 0.0, acc_H = 0.0, acc_n = 0.0;
-    int64_t nl = 0;
-    if (ct == 0) nl = *p.n_loss;
+    const int64_t nl = *p.n_loss;
+    const float invN = nl > 0 ? float(1.0 / double(nl)) : 0.f;
     uint32_t slot = 0, phase = 0, q = 0;
     int64_t row = group;
     int32_t y_n = row < p.num_rows ? p.targets[row] : 0;
@@ -750,32 +769,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) 
       }
       const int64_t ylc64 = int64_t(y) - p.vocab_start - c0;
       const int ylc = (ylc64 >= 0 && ylc64 < segn) ? int(ylc64) : -1;
-      if (ct == 0) {
-        Stat tot{-INFINITY, 0.f, 0.f};
-        float zyt = 0.f;
-        for (int k = 0; k < p.nshards; ++k) {
-          const float4 P = p.partials_in[int64_t(k) * p.num_rows + row];
-          tot = combine(tot, Stat{P.x, P.y, P.z});
-          zyt += P.w;
-        }
-        const RowStats rs = finalize(tot, zyt);
-        const float old_lp = p.old_logp[row];
-        const float ref_lp = p.ref_logp ? p.ref_logp[row] : 0.f;
-        const LossOut lo = loss_terms(p, rs.logp, p.row_traj[row], old_lp, ref_lp, nl);
-        if (crank == 0) {
-          acc_L += lo.L;
-          acc_clip += lo.clipped ? 1.0 : 0.0;
-          acc_kl += lo.kl;
-          acc_H += double(rs.H);
-          acc_n += 1.0;
-          if (p.logp) p.logp[row] = rs.logp;
-          if (p.entropy) p.entropy[row] = rs.H;
-        }
-        S.rowbc[q & 1u] = make_float4(rs.L2, lo.coef, 0.f, 0.f);
+      // every thread combines the gathered partials (rank order) and evaluates the loss terms
+      Stat tot{-INFINITY, 0.f, 0.f};
+      float zyt = 0.f;
+      for (int k = 0; k < p.nshards; ++k) {
+        const float4 P = p.partials_in[int64_t(k) * p.num_rows + row];
+        tot = combine(tot, Stat{P.x, P.y, P.z});
+        zyt += P.w;
       }
-      named_bar_sync(1, kNCT);
-      const float4 bc = S.rowbc[q & 1u];
-      const float L2 = bc.x, coef = bc.y;
+      const RowStats rs = finalize(tot, zyt);
+      RowSide sd{p.adv[p.row_traj[row]], p.old_logp[row], p.ref_logp ? p.ref_logp[row] : 0.f};
+      const LossOut lo = loss_terms(p, rs.logp, sd, invN);
+      if (ct == 0 && crank == 0) {
+        acc_L += double(lo.L);
+        acc_clip += lo.clipped ? 1.0 : 0.0;
+        acc_kl += double(lo.kl);
+        acc_H += double(rs.H);
+        acc_n += 1.0;
+        if (p.logp) p.logp[row] = rs.logp;
+        if (p.entropy) p.entropy[row] = rs.H;
+      }
+      const float L2 = rs.L2, coef = lo.coef;
       char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
       for (int c = 0; c < nch; ++c) {
         mbar_wait(&S.full[slot], phase);
@@ -793,7 +807,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) 
           if (unsigned(ylc - lc) < unsigned(EV)) {
 #pragma unroll
             for (int i = 0; i < EV; ++i)
-              if (lc + i == ylc) g[i] = __fsub_rn(g[i], coef);
+              if (lc + i == ylc) g[i] = lo.gy;
           }
           if (lc + EV <= segn) {
             stg_cs_v4(drow + size_t(lc) * sizeof(T), VT::pack(g));

@@ -139,6 +139,34 @@ __device__ __forceinline__ void tmem_ld8_1(uint32_t taddr8, uint32_t taddr1, uin
       : "memory");
 }
 
+// split issue / wait: the wait takes the loaded registers as in-out operands so no use of them can be
+// scheduled before it (software pipelining of TMEM loads)
+__device__ __forceinline__ void tmem_ld8_1_issue(uint32_t taddr8, uint32_t taddr1, uint4& a, uint4& b, uint32_t& m) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%9];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%8}, [%10];"
+      : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w), "=r"(m)
+      : "r"(taddr8), "r"(taddr1)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld_dep(uint4& a, uint4& b, uint32_t& m) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(a.x), "+r"(a.y), "+r"(a.z), "+r"(a.w), "+r"(b.x), "+r"(b.y), "+r"(b.z), "+r"(b.w), "+r"(m)
+               :
+               : "memory");
+}
+
+// ---- bulk async stores (shared -> global) --------------------------------------------------------
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_s2g(void* dst_gmem, const void* src_smem, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst_gmem),
+               "r"(smem_u32(src_smem)), "r"(bytes), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_8() { asm volatile("cp.async.bulk.wait_group.read 8;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // ---- named barriers ----------------------------------------------------------------------------
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -222,7 +222,8 @@ def test_on_policy_bitwise_and_minus_mean_adv(otk, ctx):
     assert torch.equal(got["logp"][m], lp[m])            # same reduction order: bitwise equal
     st = otk.stats_dict(got["stats"])
     want = -sum(h["adv"][h["row_traj"][j]] for j in range(n) if h["mask"][j]) / N
-    assert abs(st["loss"] - want) <= 1e-12 * max(1.0, abs(want))
+    # per-token terms are fp32 on the device (A rounded to fp32: 6e-8 relative), summed in fp64
+    assert abs(st["loss"] - want) <= 1e-6 * max(1.0, abs(want))
     assert st["kl_sum"] == 0.0 and st["n_clipped"] == 0
 
 
