@@ -528,6 +528,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
   constexpr int CE = kChunkBytes / int(sizeof(T));
   constexpr bool kBwd = (MODE == kModeBwd);
   constexpr int kColM = 8 * kMaxChunks;  // per-thread TMEM columns: [0, 8*kMaxChunks) e, then m_c
+  static_assert(kColM + kMaxChunks <= kTmemWindow, "TMEM window too small");
+  static_assert(kConsumerWarps / 4 * kTmemWindow <= 512, "TMEM has 512 columns");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int csize = p.csize;
@@ -548,8 +550,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
   } else {
     const int ct = threadIdx.x - 32;
     const int cw = warp - 1;
-    // this warp's TMEM window: its lane quadrant (warp % 4) and one half of the 512 columns
-    const uint32_t tm = kBwd ? S.tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(256 * (cw >> 2)) : 0u;
+    // this warp's TMEM window: its lane quadrant (warp % 4) and one of three 128-column windows
+    const uint32_t tm = kBwd ? S.tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(kTmemWindow * (cw >> 2)) : 0u;
     const float s2 = __fmul_rn(p.scale, kLog2e);
     const uint64_t s2x2 = f2(s2, s2);
     double acc_L = 0.0, acc_clip = 0.0, acc_kl = 0.0, acc_H = 0.0, acc_n = 0.0;

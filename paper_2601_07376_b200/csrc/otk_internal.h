@@ -32,13 +32,14 @@ constexpr int kStatSlots = 8;
 enum Ticket { kTicketMasks = 0, kTicketRows = 1 };
 
 // Fused row kernel configuration.
-// 1 producer warp + 8 consumer warps (2 per TMEM lane quadrant); an 8 KB chunk is exactly
-// 2 x 16-byte vectors per consumer thread.
-constexpr int kChunkBytes = 8192;        // one bulk-TMA transfer / ring slot
-constexpr int kSlots = 27;               // ring depth: 216 KB of shared memory per CTA
-constexpr int kConsumerWarps = 8;        // 256 compute threads
+// 1 producer warp + 12 consumer warps (3 per SM sub-partition / TMEM lane quadrant; <= 128 registers
+// per thread); a 12 KB chunk is exactly 2 x 16-byte vectors per consumer thread.
+constexpr int kChunkBytes = 12288;       // one bulk-TMA transfer / ring slot
+constexpr int kSlots = 18;               // ring depth: 216 KB of shared memory per CTA
+constexpr int kConsumerWarps = 12;       // 384 compute threads
 constexpr int kThreads = 32 * (1 + kConsumerWarps);
-constexpr int kMaxChunks = 19;           // a CTA's row segment (<= 19 chunks, 152 KB) is kept in TMEM
+constexpr int kMaxChunks = 13;           // a CTA's row segment (<= 13 chunks, 156 KB) is kept in TMEM
+constexpr int kTmemWindow = 128;         // TMEM columns per consumer warp (3 windows per lane quadrant)
 
 enum RowMode : int {
   kModeFwd = 0,       // (3): logp / entropy / lse
