@@ -69,10 +69,6 @@ class PolicyLossStep:
             self.Bmax = max(counts)
             self.G_global = global_num_groups if global_num_groups is not None else num_groups
             Bg = sum(counts)
-            self.gather_gid = torch.empty(self.world * self.Bmax, dtype=torch.int32, device=dev)
-            self.gather_ret = torch.empty(self.world * self.Bmax, dtype=torch.float64, device=dev)
-            self.pad_gid = torch.zeros(self.Bmax, dtype=torch.int32, device=dev)
-            self.pad_ret = torch.zeros(self.Bmax, dtype=torch.float64, device=dev)
             self.gid_g = torch.empty(Bg, dtype=torch.int32, device=dev)
             self.ret_g = torch.empty(Bg, dtype=torch.float64, device=dev)
             self.adv_g = dict(adv=torch.empty(Bg, dtype=torch.float64, device=dev),
@@ -90,21 +86,13 @@ class PolicyLossStep:
                                  turn_rewards=self.turn_rewards, std_norm=self.std_norm, unbiased=self.unbiased,
                                  out=self.adv_out)
             return self.adv_out["adv"]
-        import torch.distributed as dist
-        dist.all_reduce(self.masks["n_loss"], op=dist.ReduceOp.SUM, group=self.pg)
+        from .dist import all_gather_group_returns, all_reduce_n_loss
+        all_reduce_n_loss(self.masks["n_loss"], self.pg)
         # local returns (group statistics of this call are discarded), then the global exchange
         otk_group_advantages(self.ctx, self.group_id, self.num_groups, turn_offsets=self.turn_offsets,
                              turn_rewards=self.turn_rewards, out=self.adv_out)
-        B = self.batch.num_traj
-        self.pad_gid[:B].copy_(self.group_id)
-        self.pad_ret[:B].copy_(self.adv_out["returns"])
-        dist.all_gather_into_tensor(self.gather_gid, self.pad_gid, group=self.pg)
-        dist.all_gather_into_tensor(self.gather_ret, self.pad_ret, group=self.pg)
-        o = 0
-        for r, c in enumerate(self.counts):    # unpad in rank order (host-known counts: no sync)
-            self.gid_g[o:o + c].copy_(self.gather_gid[r * self.Bmax:r * self.Bmax + c])
-            self.ret_g[o:o + c].copy_(self.gather_ret[r * self.Bmax:r * self.Bmax + c])
-            o += c
+        all_gather_group_returns(self.group_id, self.adv_out["returns"], self.counts, self.pg,
+                                 out=(self.gid_g, self.ret_g))
         otk_group_advantages(self.ctx, self.gid_g, self.G_global, returns=self.ret_g, std_norm=self.std_norm,
                              unbiased=self.unbiased, out=self.adv_g)
         return self.adv_g["adv"][self.b0:self.b0 + B]
@@ -122,8 +110,8 @@ class PolicyLossStep:
             if on_launch:
                 on_launch(k, "end")
         if self.pg is not None:
-            import torch.distributed as dist
-            dist.all_reduce(self.stats, op=dist.ReduceOp.SUM, group=self.pg)
+            from .dist import all_reduce_stats
+            all_reduce_stats(self.stats, self.pg)
         return self.stats
 
     def run(self, micro_batches: Sequence[MicroBatch], on_launch=None):

@@ -1,0 +1,146 @@
+"""Multi-rank host logic of the two sharding modes on CPU (gloo, world size 2) — DESIGN.md §7.
+
+The product's shard planning and collectives (paper_2601_07376_b200.dist) run under gloo; the per-rank
+compute is done by the float64 oracle standing in for the device kernels, and the sharded results must
+equal the unsharded oracle: integers bit-exact, group statistics bit-exact (same inputs, same order),
+floats to 1e-12.
+"""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2601_07376_b200.dist import (all_gather_group_returns, all_gather_vocab_partials, all_reduce_n_loss,
+                                        all_reduce_stats, plan_batch_shards, traj_costs, vocab_shard_bounds)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _sub_batch(tb, b0, b1):
+    from synth.trajectories import TrajBatch
+    s0, s1 = int(tb.seg_offsets[b0]), int(tb.seg_offsets[b1])
+    t0, t1 = int(tb.turn_offsets[b0]), int(tb.turn_offsets[b1])
+    r0 = int(tb.tok_offsets[b0])
+    return TrajBatch(tok_offsets=tb.tok_offsets[b0:b1 + 1] - r0, seg_offsets=(tb.seg_offsets[b0:b1 + 1] - s0).astype(np.int32),
+                     seg_source=tb.seg_source[s0:s1], seg_agent=tb.seg_agent[s0:s1], seg_len=tb.seg_len[s0:s1],
+                     terminated=tb.terminated[b0:b1],
+                     traj_agent=None if tb.traj_agent is None else tb.traj_agent[b0:b1],
+                     turn_offsets=(tb.turn_offsets[b0:b1 + 1] - t0).astype(np.int32),
+                     turn_rewards=tb.turn_rewards[t0:t1], group_id=tb.group_id[b0:b1], num_groups=tb.num_groups)
+
+
+def _worker(rank, world, port, config, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle_ref as O
+        from synth import make_batch
+        tb = make_batch(config)
+        V = 1000
+        # ---- batch sharding: plan, local masks/returns (oracle stands in for the kernels), exchanges
+        plan = plan_batch_shards(traj_costs(tb, 151936), world)
+        b0, b1 = plan[rank]
+        counts = [e - s for s, e in plan]
+        loc = _sub_batch(tb, b0, b1)
+        m_loc = O.build_masks(loc.tok_offsets, loc.seg_offsets, loc.seg_source, loc.seg_agent, loc.seg_len,
+                              loc.terminated, traj_agent=loc.traj_agent)
+        n_loss = torch.tensor([m_loc["n_loss"]], dtype=torch.int64)
+        all_reduce_n_loss(n_loss)
+        R_loc = torch.from_numpy(O.episode_returns(loc.turn_offsets, loc.turn_rewards))
+        gid_g, ret_g = all_gather_group_returns(torch.from_numpy(loc.group_id), R_loc, counts)
+        adv_g = O.group_advantages(gid_g.numpy(), ret_g.numpy(), tb.num_groups)["adv"]
+        # ---- loss partial sums with the GLOBAL N, then all-reduce of the stats
+        rng = np.random.default_rng(100 + rank)
+        rows = np.flatnonzero(m_loc["loss_mask"])[:6]
+        logits = rng.normal(scale=2.0, size=(len(rows), V))
+        y = rng.integers(0, V, len(rows))
+        lp = np.array([O.row_forward(logits[i], int(y[i]))[0] for i in range(len(rows))])
+        adv_loc = adv_g[b0:b1]
+        cfg = O.LossCfg(kl_beta=0.0)
+        L = [O.row_loss_terms(lp[i], lp[i], None, float(adv_loc[m_loc["row_traj"][r]]), cfg)[0]
+             for i, r in enumerate(rows)]
+        stats = torch.tensor([math.fsum(L) / int(n_loss.item()), float(len(rows)), 0.0, 0.0, float(len(rows))],
+                             dtype=torch.float64)
+        all_reduce_stats(stats)
+        # ---- vocab sharding: per-rank partials of the same rows, gathered in rank order
+        vrng = np.random.default_rng(7)
+        X = vrng.normal(scale=3.0, size=(5, 1003))
+        X[2, 17] = -np.inf
+        Y = vrng.integers(0, 1003, 5)
+        v0, v1 = vocab_shard_bounds(1003, world)[rank]
+        part = torch.tensor([O.shard_partials(X[j, v0:v1], int(Y[j]), v0) for j in range(5)], dtype=torch.float64)
+        gathered = all_gather_vocab_partials(part)
+        comb = [O.combine_partials([tuple(gathered[k, j].tolist()) for k in range(world)]) for j in range(5)]
+        q.put(dict(rank=rank, n_loss=int(n_loss.item()), gid=gid_g.numpy(), ret=ret_g.numpy(), adv=adv_g,
+                   plan=plan, stats=stats.numpy(), L=L, comb=comb, X=X, Y=Y))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("config", ["game", "marl", "math"])
+def test_batch_and_vocab_sharding_gloo(config):
+    from oracle import oracle_ref as O
+    from synth import make_batch
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, config, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda d: d["rank"])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    tb = make_batch(config)
+    full = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated,
+                         traj_agent=tb.traj_agent)
+    R = O.episode_returns(tb.turn_offsets, tb.turn_rewards)
+    adv = O.group_advantages(tb.group_id, R, tb.num_groups)["adv"]
+    for r in res:
+        assert r["n_loss"] == full["n_loss"]                       # global token count, bit-exact
+        assert np.array_equal(r["gid"], tb.group_id)               # gathered in rank order
+        assert np.array_equal(r["ret"], R)
+        assert np.array_equal(r["adv"], adv)                       # identical stats on every rank
+    assert np.array_equal(res[0]["stats"], res[1]["stats"])
+    want = (math.fsum(res[0]["L"]) + math.fsum(res[1]["L"])) / full["n_loss"]
+    assert abs(res[0]["stats"][0] - want) < 1e-14
+    for j in range(5):
+        ref = O.row_forward(res[0]["X"][j], int(res[0]["Y"][j]))
+        for r in res:
+            assert abs(r["comb"][j][0] - ref[0]) < 1e-12 and abs(r["comb"][j][1] - ref[1]) < 1e-12
+
+
+def test_plan_batch_shards_balanced():
+    from synth import make_batch
+    for name in ("math", "game", "marl"):
+        tb = make_batch(name)
+        c = traj_costs(tb, 151936)
+        for world in (2, 4, 8):
+            plan = plan_batch_shards(c, world)
+            assert plan[0][0] == 0 and plan[-1][1] == len(c)
+            assert all(a < b for a, b in plan) and all(plan[i][1] == plan[i + 1][0] for i in range(world - 1))
+            loads = [c[a:b].sum() for a, b in plan]
+            assert max(loads) <= c.sum() / world + c.max() + 1e-6   # within one trajectory of ideal
+    with pytest.raises(ValueError):
+        plan_batch_shards([1.0], 2)
+
+
+def test_vocab_shard_bounds():
+    for V, P in ((151936, 2), (151936, 4), (151936, 8), (1003, 3)):
+        b = vocab_shard_bounds(V, P)
+        assert b[0][0] == 0 and b[-1][1] == V
+        assert all(x[1] == y[0] for x, y in zip(b, b[1:]))
+        assert all(x[0] % 8 == 0 for x in b)
+    assert vocab_shard_bounds(151936, 4)[1] == (37984, 75968)
