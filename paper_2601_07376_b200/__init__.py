@@ -15,7 +15,7 @@ from typing import Optional
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libotk.so")
+LIB_PATH = os.environ.get("OTK_LIB") or os.path.join(HERE, "libotk.so")  # OTK_LIB: experiment builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2601_07376_b200.build` "

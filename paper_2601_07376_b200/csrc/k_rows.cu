@@ -27,6 +27,16 @@
 #include "otk_internal.h"
 #include "otk_ptx.cuh"
 
+#ifndef OTK_P2PAIR
+#define OTK_P2PAIR 1
+#endif
+#ifndef OTK_PREFETCH
+#define OTK_PREFETCH 1
+#endif
+#ifndef OTK_PIPE_FETCH
+#define OTK_PIPE_FETCH 0
+#endif
+
 namespace otk {
 using namespace ptx;
 
@@ -264,7 +274,6 @@ struct Smem {
   float4 xrecv[2][8];                 // peer partials, double-buffered by active-row parity
   float4 wred[2][kConsumerWarps];     // warp partials, double-buffered by active-row parity
   float4 rowbc[2];                    // (stream kernel) row broadcast
-  unsigned long long zy[2];           // (row tag << 32 | bits of s * x_target), by parity
   uint32_t tmem_base;
 };
 constexpr int kZeroBytes = 4096;  // zero block: source of the bulk stores that zero-fill masked rows
@@ -275,22 +284,17 @@ __device__ __forceinline__ bool row_active(const RowParams& p, int32_t y, uint8_
   return m && y >= 0 && int64_t(y) < p.vocab_total;
 }
 
-// ---- producer: bulk-TMA every active row's column segment, chunk by chunk, into the ring; zero-fill
-// the segment of every inactive row with bulk async stores from a zeroed shared-memory block --------------
-template <typename T, bool kZeroFill>
-__device__ __forceinline__ void produce(const RowParams& p, uint8_t* ring, const uint8_t* zero, Smem& S,
-                                        int64_t group, int64_t ngroups, int64_t c0, int segn, uint32_t seg_bytes,
-                                        int nch) {
+// ---- loader (warp 0, one thread): bulk-TMA every active row's column segment, chunk by chunk, into the ring
+template <typename T>
+__device__ __forceinline__ void load_rows(const RowParams& p, uint8_t* ring, Smem& S, int64_t group, int64_t ngroups,
+                                          int64_t c0, uint32_t seg_bytes, int nch) {
   const uint64_t pol = policy_evict_first();
   const char* base = reinterpret_cast<const char*>(p.logits) + c0 * int64_t(sizeof(T));
-  char* dbase = reinterpret_cast<char*>(p.dlogits) + c0 * int64_t(sizeof(T));
   const int64_t row_bytes = p.ld * int64_t(sizeof(T));
-  const uint32_t zero_bytes = (uint32_t(segn) * uint32_t(sizeof(T))) & ~15u;  // 16-byte multiple part
   uint32_t slot = 0, phase = 0;
   int64_t row = group;
   int32_t y_n = row < p.num_rows ? p.targets[row] : 0;
   uint8_t m_n = (row < p.num_rows && p.mask) ? p.mask[row] : 1;
-  bool pending = false;
   for (; row < p.num_rows; row += ngroups) {
     const int32_t y = y_n;
     const uint8_t m = m_n;
@@ -299,17 +303,7 @@ __device__ __forceinline__ void produce(const RowParams& p, uint8_t* ring, const
       y_n = p.targets[nrow];
       m_n = p.mask ? p.mask[nrow] : 1;
     }
-    if (!row_active(p, y, m)) {
-      if (kZeroFill && p.zero_masked && zero_bytes) {
-        char* dst = dbase + row * row_bytes;
-        for (uint32_t off = 0; off < zero_bytes; off += kZeroBytes)
-          bulk_s2g(dst + off, zero, min(uint32_t(kZeroBytes), zero_bytes - off), pol);
-        bulk_commit();
-        bulk_wait_read_8();
-        pending = true;
-      }
-      continue;
-    }
+    if (!row_active(p, y, m)) continue;
     const char* src = base + row * row_bytes;
     uint32_t off = 0;
     for (int c = 0; c < nch; ++c) {
@@ -323,6 +317,31 @@ __device__ __forceinline__ void produce(const RowParams& p, uint8_t* ring, const
         phase ^= 1u;
       }
     }
+  }
+}
+
+// ---- zero-filler (warp 13, one thread): the dlogits segment of every inactive row is written with bulk
+// async shared->global stores from a zeroed 4 KB block — never read, never touched by the consumers ----------
+template <typename T>
+__device__ __forceinline__ void zero_rows(const RowParams& p, const uint8_t* zero, int64_t group, int64_t ngroups,
+                                          int64_t c0, int segn) {
+  if (!p.zero_masked) return;
+  const uint32_t zero_bytes = (uint32_t(segn) * uint32_t(sizeof(T))) & ~15u;  // 16-byte multiple part
+  if (!zero_bytes) return;
+  const uint64_t pol = policy_evict_first();
+  char* dbase = reinterpret_cast<char*>(p.dlogits) + c0 * int64_t(sizeof(T));
+  const int64_t row_bytes = p.ld * int64_t(sizeof(T));
+  bool pending = false;
+  for (int64_t row = group; row < p.num_rows; row += ngroups) {
+    const int32_t y = p.targets[row];
+    const uint8_t m = p.mask ? p.mask[row] : 1;
+    if (row_active(p, y, m)) continue;
+    char* dst = dbase + row * row_bytes;
+    for (uint32_t off = 0; off < zero_bytes; off += kZeroBytes)
+      bulk_s2g(dst + off, zero, min(uint32_t(kZeroBytes), zero_bytes - off), pol);
+    bulk_commit();
+    bulk_wait_read_8();
+    pending = true;
   }
   if (pending) bulk_wait_all();
 }
@@ -451,7 +470,6 @@ __device__ __forceinline__ void row_kernel_setup(Smem& S, uint8_t* zero, int war
     }
     mbar_init(&S.xbar[0], 1);
     mbar_init(&S.xbar[1], 1);
-    S.zy[0] = S.zy[1] = ~0ull;
     fence_mbar_init();
   }
   for (int i = threadIdx.x; i < kZeroBytes / 16; i += blockDim.x)
@@ -469,45 +487,57 @@ __device__ __forceinline__ void row_kernel_setup(Smem& S, uint8_t* zero, int war
   tc_fence_after();
 }
 
-// Row statistics after pass 1, computed redundantly by every consumer thread (no second barrier):
-// CTA total in warp order, then the cluster exchange of 16-byte partials (rank order).
-__device__ __forceinline__ void row_total(Smem& S, Stat st, int lane, int cw, int ct, int csize, uint32_t crank,
-                                          uint32_t q, int64_t row, Stat& tot, float& zyt) {
-  const uint32_t par = q & 1u;
+// Warp-wide (max, sum-exp, sum-exp*d): max first, one rescale per lane, then two butterfly sums. Every lane
+// ends with the same bits (butterfly addition is commutative), so all warps agree without a broadcast.
+__device__ __forceinline__ Stat warp_reduce(Stat st) {
+  float M = st.m;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  float s = 0.f, t = 0.f;
+  if (st.m != -INFINITY) {
+    const float d = __fsub_rn(st.m, M), f = ex2(d);
+    s = __fmul_rn(st.s, f);
+    t = __fmul_rn(f, __fmaf_rn(d, st.s, st.t));
+  }
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
-    Stat o;
-    o.m = __shfl_xor_sync(0xffffffffu, st.m, off);
-    o.s = __shfl_xor_sync(0xffffffffu, st.s, off);
-    o.t = __shfl_xor_sync(0xffffffffu, st.t, off);
-    st = (lane & off) ? combine(o, st) : combine(st, o);
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+    t = __fadd_rn(t, __shfl_xor_sync(0xffffffffu, t, off));
   }
+  return Stat{M, s, t};
+}
+
+// Row statistics after pass 1. Warp partials go through shared memory; every warp then reduces the 12
+// partials lane-parallel (identical result in every thread, so no second barrier and no broadcast), and
+// thread 0 exchanges the CTA total with the cluster peers through DSMEM (rank-order combine).
+__device__ __forceinline__ void row_total(Smem& S, Stat st, int lane, int cw, int ct, int csize, uint32_t crank,
+                                          uint32_t q, Stat& tot) {
+  const uint32_t par = q & 1u;
+  st = warp_reduce(st);
   if (lane == 0) S.wred[par][cw] = make_float4(st.m, st.s, st.t, 0.f);
   named_bar_sync(1, kNCT);
-  Stat r{S.wred[par][0].x, S.wred[par][0].y, S.wred[par][0].z};
-#pragma unroll
-  for (int w = 1; w < kConsumerWarps; ++w) r = combine(r, Stat{S.wred[par][w].x, S.wred[par][w].y, S.wred[par][w].z});
-  const unsigned long long zt = S.zy[par];
-  const float zy = (uint32_t(zt >> 32) == uint32_t(row)) ? __uint_as_float(uint32_t(zt)) : 0.f;
+  Stat mine{-INFINITY, 0.f, 0.f};
+  if (lane < kConsumerWarps) {
+    const float4 w = S.wred[par][lane];
+    mine = Stat{w.x, w.y, w.z};
+  }
+  const Stat r = warp_reduce(mine);
   if (csize > 1) {
     if (ct == 0) {
       for (int dst = 0; dst < csize; ++dst) {
         if (dst == int(crank)) continue;
-        st_async_f4(mapa(smem_u32(&S.xrecv[par][crank]), dst), r.m, r.s, r.t, zy, mapa(smem_u32(&S.xbar[par]), dst));
+        st_async_f4(mapa(smem_u32(&S.xrecv[par][crank]), dst), r.m, r.s, r.t, 0.f, mapa(smem_u32(&S.xbar[par]), dst));
       }
       mbar_arrive_expect_tx(&S.xbar[par], 16u * uint32_t(csize - 1));
     }
-    mbar_wait_cluster(&S.xbar[par], (q >> 1) & 1u);
+    mbar_wait(&S.xbar[par], (q >> 1) & 1u);
     tot = Stat{-INFINITY, 0.f, 0.f};
-    zyt = 0.f;
     for (int k = 0; k < csize; ++k) {
-      const float4 P = (k == int(crank)) ? make_float4(r.m, r.s, r.t, zy) : S.xrecv[par][k];
+      const float4 P = (k == int(crank)) ? make_float4(r.m, r.s, r.t, 0.f) : S.xrecv[par][k];
       tot = combine(tot, Stat{P.x, P.y, P.z});
-      zyt += P.w;
     }
   } else {
     tot = r;
-    zyt = zy;
   }
 }
 
@@ -545,7 +575,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
   row_kernel_setup<kBwd>(S, zero, warp, csize);
 
   if (warp == 0) {
-    if (lane == 0 && nch > 0) produce<T, kBwd>(p, ring, zero, S, group, ngroups, c0, segn, seg_bytes, nch);
+    if (lane == 0 && nch > 0) load_rows<T>(p, ring, S, group, ngroups, c0, seg_bytes, nch);
+    __syncwarp();
+  } else if (warp == kConsumerWarps + 1) {
+    if (kBwd && lane == 0) zero_rows<T>(p, zero, group, ngroups, c0, segn);
     __syncwarp();
   } else {
     const int ct = threadIdx.x - 32;
@@ -563,6 +596,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
     }
     uint32_t slot = 0, phase = 0, q = 0;
 
+#if OTK_PREFETCH
+    int64_t row = group;
+    int32_t y_n = 0, rt_n = 0;
+    uint8_t m_n = 1;
+    float old_n = 0.f, ref_n = 0.f;
+    if (row < p.num_rows) {
+      y_n = p.targets[row];
+      m_n = p.mask ? p.mask[row] : 1;
+      if (kBwd) {
+        rt_n = p.row_traj[row];
+        old_n = p.old_logp[row];
+        if (p.ref_logp) ref_n = p.ref_logp[row];
+      }
+    }
+    for (; row < p.num_rows; row += ngroups) {
+      const int32_t y = y_n;
+      const uint8_t m = m_n;
+      RowSide sd{0.0, old_n, ref_n};
+      const int32_t rt = rt_n;
+      const int64_t nrow = row + ngroups;
+      if (nrow < p.num_rows) {  // side data of the next row: in flight while this row is computed
+        y_n = p.targets[nrow];
+        m_n = p.mask ? p.mask[nrow] : 1;
+        if (kBwd) {
+          rt_n = p.row_traj[nrow];
+          old_n = p.old_logp[nrow];
+          if (p.ref_logp) ref_n = p.ref_logp[nrow];
+        }
+      }
+#else
     int64_t row = group;
     int32_t y_n = row < p.num_rows ? p.targets[row] : 0;
     uint8_t m_n = (row < p.num_rows && p.mask) ? p.mask[row] : 1;
@@ -574,44 +637,64 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
         y_n = p.targets[nrow];
         m_n = p.mask ? p.mask[nrow] : 1;
       }
+      RowSide sd{0.0, 0.f, 0.f};
+      int32_t rt = 0;
+      if (kBwd && row_active(p, y, m)) {
+        rt = p.row_traj[row];
+        sd.old_lp = p.old_logp[row];
+        if (p.ref_logp) sd.ref_lp = p.ref_logp[row];
+      }
+#endif
       if (!row_active(p, y, m)) {
         inactive_row<T, MODE>(p, row, ct, crank, c0, segn, m != 0);
         continue;
       }
       const int64_t ylc64 = int64_t(y) - p.vocab_start - c0;  // target column local to this CTA's segment
       const int ylc = (ylc64 >= 0 && ylc64 < segn) ? int(ylc64) : -1;
-      RowSide sd{0.0, 0.f, 0.f};
-      if (kBwd) {  // broadcast loads, issued early and consumed after pass 1
-        sd.A = p.adv[p.row_traj[row]];
-        sd.old_lp = p.old_logp[row];
-        if (p.ref_logp) sd.ref_lp = p.ref_logp[row];
-      }
+      if (kBwd) sd.A = p.adv[rt];  // consumed after pass 1
+      // the target logit, read straight from HBM (one sector per row; in flight during pass 1)
+      const int64_t yg = int64_t(y) - p.vocab_start;
+      const float xy = (yg >= 0 && yg < p.vocab)
+                           ? VT::load1(p.logits, row * p.ld + yg) : 0.f;
 
       // ---------------- pass 1: online max / sum 2^(y-m) / sum 2^(y-m)(y-m), one exponential per element
-      const int cy = ylc >= 0 ? ylc / CE : -1;  // the target column's chunk and owning thread
-      const int owner_ct = ylc >= 0 ? ((ylc - cy * CE) / EV) % kNCT : -1;
+      const int owner_ct = ylc >= 0 ? ((ylc % CE) / EV) % kNCT : -1;  // thread that stores the target column
       Stat st{-INFINITY, 0.f, 0.f};
-      for (int c = 0; c < nch; ++c) {
+      // software-pipelined by one chunk: while chunk c's exponentials run, chunk c+1 is read from the ring,
+      // released, and its max reduced (independent instruction streams the scheduler interleaves)
+      uint4 v0n = make_uint4(0, 0, 0, 0), v1n = v0n;
+      float mxn = -INFINITY;
+      auto fetch = [&](int c) {
         mbar_wait(&S.full[slot], phase);
         const uint8_t* buf = ring + size_t(slot) * kChunkBytes;
-        uint4 v0 = *reinterpret_cast<const uint4*>(buf + ct * 16);
-        uint4 v1 = *reinterpret_cast<const uint4*>(buf + (ct + kNCT) * 16);
+        v0n = *reinterpret_cast<const uint4*>(buf + ct * 16);
+        v1n = *reinterpret_cast<const uint4*>(buf + (ct + kNCT) * 16);
         if (c == nch - 1) {  // the segment's last chunk may be partial: lanes past segn become -inf
           const int lc0 = c * CE + ct * EV, lc1 = lc0 + kNCT * EV;
-          if (lc0 + EV > segn) v0 = VT::mask_tail(v0, segn - lc0);
-          if (lc1 + EV > segn) v1 = VT::mask_tail(v1, segn - lc1);
+          if (lc0 + EV > segn) v0n = VT::mask_tail(v0n, segn - lc0);
+          if (lc1 + EV > segn) v1n = VT::mask_tail(v1n, segn - lc1);
         }
-        if (c == cy && ct == owner_ct)
-          S.zy[q & 1u] = (static_cast<unsigned long long>(uint32_t(row)) << 32) |
-                         __float_as_uint(__fmul_rn(p.scale, VT::load1(buf, ylc - c * CE)));
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty[slot]);
         if (++slot == kSlots) {
           slot = 0;
           phase ^= 1u;
         }
+        mxn = VT::max_final(VT::max_acc(VT::max_acc(VT::max_init(), v0n), v1n));
+      };
+#if OTK_PIPE_FETCH
+      if (nch > 0) fetch(0);
+#endif
+      for (int c = 0; c < nch; ++c) {
+#if !OTK_PIPE_FETCH
+        fetch(c);
+#endif
+        const uint4 v0 = v0n, v1 = v1n;
+        const float mx = mxn;
+#if OTK_PIPE_FETCH
+        if (c + 1 < nch) fetch(c + 1);
+#endif
         // running max update (rescale the sums when it grows; exact no-op otherwise)
-        const float mx = VT::max_final(VT::max_acc(VT::max_acc(VT::max_init(), v0), v1));
         if (mx != -INFINITY) {
           const float mn = fmaxf(st.m, __fmul_rn(mx, s2));
           if (mn > st.m) {
@@ -638,8 +721,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       if (kBwd) tmem_wait_st();
 
       Stat tot;
-      float zyt;
-      row_total(S, st, lane, cw, ct, csize, crank, q, row, tot, zyt);
+      row_total(S, st, lane, cw, ct, csize, crank, q, tot);
+      const float zyt = __fmul_rn(p.scale, xy);
       if (MODE == kModePartial) {
         if (ct == 0 && crank == 0) p.partials_out[row] = make_float4(tot.m, tot.s, tot.t, zyt);
       } else {
@@ -661,6 +744,55 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
             if (p.logp) p.logp[row] = rs.logp;
             if (p.entropy) p.entropy[row] = rs.H;
           }
+#if OTK_P2PAIR
+          // ---------------- pass 2: dlogits = coef * e * 2^(m_c - lse) from TMEM, two chunks per load,
+          // the next pair's load in flight while this pair is computed and stored
+          char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
+          uint4 ecur[4];
+          uint32_t mcur[2];
+          tmem_ld16_2_issue(tm, tm + uint32_t(kColM), ecur, mcur);
+          tmem_wait_ld_dep16(ecur, mcur);
+          for (int c = 0; c < nch; c += 2) {
+            uint4 enx[4] = {ecur[0], ecur[1], ecur[2], ecur[3]};
+            uint32_t mnx[2] = {mcur[0], mcur[1]};
+            const bool more = c + 2 < nch;
+            if (more) tmem_ld16_2_issue(tm + uint32_t(8 * (c + 2)), tm + uint32_t(kColM + c + 2), enx, mnx);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int cc = c + h;
+              if (cc < nch) {
+                const float kt = __fmul_rn(lo.coef, ex2(__fsub_rn(__uint_as_float(mcur[h]), rs.L2)));
+                const uint64_t kt2 = f2(kt, kt);
+                const uint4 g0 = VT::pass2(ecur[2 * h], kt2), g1 = VT::pass2(ecur[2 * h + 1], kt2);
+                const int lc0 = cc * CE + ct * EV, lc1 = lc0 + kNCT * EV;
+                if (cc < nch - 1) {
+                  stg_cs_v4(drow + size_t(lc0) * sizeof(T), g0);
+                  stg_cs_v4(drow + size_t(lc1) * sizeof(T), g1);
+                } else {  // last (possibly partial) chunk
+                  const uint4 gg[2] = {g0, g1};
+                  const int lcs[2] = {lc0, lc1};
+#pragma unroll
+                  for (int k = 0; k < 2; ++k) {
+                    if (lcs[k] + EV <= segn) {
+                      stg_cs_v4(drow + size_t(lcs[k]) * sizeof(T), gg[k]);
+                    } else if (lcs[k] < segn) {
+                      float g[EV];
+                      VT::unpack(gg[k], g);
+                      for (int i = 0; i < EV && lcs[k] + i < segn; ++i) VT::store1(drow, lcs[k] + i, g[i]);
+                    }
+                  }
+                }
+              }
+            }
+            if (more) {
+              tmem_wait_ld_dep16(enx, mnx);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) ecur[i] = enx[i];
+              mcur[0] = mnx[0];
+              mcur[1] = mnx[1];
+            }
+          }
+#else
           // ---------------- pass 2: dlogits = coef * e * 2^(m_c - lse) from TMEM (2-deep load pipeline)
           char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
           uint4 ea, eb;
@@ -699,6 +831,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
               ma = nm;
             }
           }
+#endif
           // target column: coef * (p_y - 1), overwriting this thread's own vector store (program order)
           if (ct == owner_ct) VT::store1(drow, ylc, lo.gy);
         }
@@ -745,7 +878,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) 
   row_kernel_setup<false>(S, zero, warp, csize);
 
   if (warp == 0) {
-    if (lane == 0 && nch > 0) produce<T, true>(p, ring, zero, S, group, ngroups, c0, segn, seg_bytes, nch);
+    if (lane == 0 && nch > 0) load_rows<T>(p, ring, S, group, ngroups, c0, seg_bytes, nch);
+    __syncwarp();
+  } else if (warp == kConsumerWarps + 1) {
+    if (lane == 0) zero_rows<T>(p, zero, group, ngroups, c0, segn);
     __syncwarp();
   } else {
     const int ct = threadIdx.x - 32;

@@ -32,12 +32,13 @@ constexpr int kStatSlots = 8;
 enum Ticket { kTicketMasks = 0, kTicketRows = 1 };
 
 // Fused row kernel configuration.
-// 1 producer warp + 12 consumer warps (3 per SM sub-partition / TMEM lane quadrant; <= 128 registers
-// per thread); a 12 KB chunk is exactly 2 x 16-byte vectors per consumer thread.
+// Warp 0 loads (bulk TMA), warps 1..12 compute (3 per SM sub-partition / TMEM lane quadrant; <= 128
+// registers per thread), warp 13 zero-fills masked rows (bulk async stores). A 12 KB chunk is exactly
+// 2 x 16-byte vectors per consumer thread.
 constexpr int kChunkBytes = 12288;       // one bulk-TMA transfer / ring slot
 constexpr int kSlots = 18;               // ring depth: 216 KB of shared memory per CTA
 constexpr int kConsumerWarps = 12;       // 384 compute threads
-constexpr int kThreads = 32 * (1 + kConsumerWarps);
+constexpr int kThreads = 32 * (2 + kConsumerWarps);  // + loader warp 0 + zero-fill warp 13
 constexpr int kMaxChunks = 13;           // a CTA's row segment (<= 13 chunks, 156 KB) is kept in TMEM
 constexpr int kTmemWindow = 128;         // TMEM columns per consumer warp (3 windows per lane quadrant)
 

@@ -156,6 +156,27 @@ __device__ __forceinline__ void tmem_wait_ld_dep(uint4& a, uint4& b, uint32_t& m
                : "memory");
 }
 
+// two chunks per load: 16 e columns + 2 reference-max columns
+__device__ __forceinline__ void tmem_ld16_2_issue(uint32_t taddr16, uint32_t taddr2, uint4 (&e)[4], uint32_t (&m)[2]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, "
+      "[%18];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x2.b32 {%16, %17}, [%19];"
+      : "=r"(e[0].x), "=r"(e[0].y), "=r"(e[0].z), "=r"(e[0].w), "=r"(e[1].x), "=r"(e[1].y), "=r"(e[1].z),
+        "=r"(e[1].w), "=r"(e[2].x), "=r"(e[2].y), "=r"(e[2].z), "=r"(e[2].w), "=r"(e[3].x), "=r"(e[3].y),
+        "=r"(e[3].z), "=r"(e[3].w), "=r"(m[0]), "=r"(m[1])
+      : "r"(taddr16), "r"(taddr2)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld_dep16(uint4 (&e)[4], uint32_t (&m)[2]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(e[0].x), "+r"(e[0].y), "+r"(e[0].z), "+r"(e[0].w), "+r"(e[1].x), "+r"(e[1].y), "+r"(e[1].z),
+                 "+r"(e[1].w), "+r"(e[2].x), "+r"(e[2].y), "+r"(e[2].z), "+r"(e[2].w), "+r"(e[3].x), "+r"(e[3].y),
+                 "+r"(e[3].z), "+r"(e[3].w), "+r"(m[0]), "+r"(m[1])
+               :
+               : "memory");
+}
+
 // ---- bulk async stores (shared -> global) --------------------------------------------------------
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_s2g(void* dst_gmem, const void* src_smem, uint32_t bytes, uint64_t policy) {
