@@ -23,18 +23,13 @@
 #include <cuda_fp16.h>
 
 #include <cfloat>
+#include <type_traits>
 
 #include "otk_internal.h"
 #include "otk_ptx.cuh"
 
-#ifndef OTK_P2PAIR
-#define OTK_P2PAIR 1
-#endif
 #ifndef OTK_PREFETCH
 #define OTK_PREFETCH 1
-#endif
-#ifndef OTK_PIPE_FETCH
-#define OTK_PIPE_FETCH 0
 #endif
 
 namespace otk {
@@ -174,7 +169,8 @@ struct Vec<float> {
                e[2], e[3]);
     return kKeepE ? pack(e) : make_uint4(0, 0, 0, 0);
   }
-  __device__ static __forceinline__ uint4 pass2(const uint4 e, uint64_t kt2) {
+  __device__ static __forceinline__ uint4 pass2(const uint4 e, float kt) {
+    const uint64_t kt2 = f2(kt, kt);
     float g[4];
     f2_split(fmul2(f2(__uint_as_float(e.x), __uint_as_float(e.y)), kt2), g[0], g[1]);
     f2_split(fmul2(f2(__uint_as_float(e.z), __uint_as_float(e.w)), kt2), g[2], g[3]);
@@ -254,13 +250,20 @@ struct Vec<__nv_bfloat16> {
     r.w = pass1_word(v.w, s2x2, negm2, aS[1], aT[1]);
     return r;
   }
-  __device__ static __forceinline__ uint32_t pass2_word(uint32_t w, uint64_t kt2) {
-    float g0, g1;
-    f2_split(fmul2(f2(bf_lo(w), bf_hi(w)), kt2), g0, g1);
-    return pack_bf16x2(g0, g1);
+  // g = e * kt directly in bf16x2: kt is split into kt_hi + kt_lo (both bf16), g = fma(e, kt_hi, e * kt_lo)
+  // rounds once to bf16 (the kt split keeps 16 significant bits): 2 instructions per pair of elements.
+  __device__ static __forceinline__ uint32_t pass2_word(uint32_t w, uint32_t hi2, uint32_t lo2) {
+    uint32_t t, r;
+    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(t) : "r"(w), "r"(lo2));
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(hi2), "r"(t));
+    return r;
   }
-  __device__ static __forceinline__ uint4 pass2(const uint4 e, uint64_t kt2) {
-    return make_uint4(pass2_word(e.x, kt2), pass2_word(e.y, kt2), pass2_word(e.z, kt2), pass2_word(e.w, kt2));
+  __device__ static __forceinline__ uint4 pass2(const uint4 e, float kt) {
+    const uint32_t hi2 = pack_bf16x2(kt, kt);
+    const float khi = bf_lo(hi2);
+    const uint32_t lo2 = pack_bf16x2(__fsub_rn(kt, khi), __fsub_rn(kt, khi));
+    return make_uint4(pass2_word(e.x, hi2, lo2), pass2_word(e.y, hi2, lo2), pass2_word(e.z, hi2, lo2),
+                      pass2_word(e.w, hi2, lo2));
   }
   __device__ static __forceinline__ void store1(void* base, int64_t i, float v) {
     reinterpret_cast<__nv_bfloat16*>(base)[i] = __float2bfloat16_rn(v);
@@ -660,19 +663,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       // ---------------- pass 1: online max / sum 2^(y-m) / sum 2^(y-m)(y-m), one exponential per element
       const int owner_ct = ylc >= 0 ? ((ylc % CE) / EV) % kNCT : -1;  // thread that stores the target column
       Stat st{-INFINITY, 0.f, 0.f};
-      // software-pipelined by one chunk: while chunk c's exponentials run, chunk c+1 is read from the ring,
-      // released, and its max reduced (independent instruction streams the scheduler interleaves)
-      uint4 v0n = make_uint4(0, 0, 0, 0), v1n = v0n;
-      float mxn = -INFINITY;
-      auto fetch = [&](int c) {
+      // one chunk of pass 1; kTail only for the segment's last chunk (lanes past segn become -inf)
+      auto chunk1 = [&](int c, auto tail) {
+        constexpr bool kTail = decltype(tail)::value;
         mbar_wait(&S.full[slot], phase);
         const uint8_t* buf = ring + size_t(slot) * kChunkBytes;
-        v0n = *reinterpret_cast<const uint4*>(buf + ct * 16);
-        v1n = *reinterpret_cast<const uint4*>(buf + (ct + kNCT) * 16);
-        if (c == nch - 1) {  // the segment's last chunk may be partial: lanes past segn become -inf
+        uint4 v0 = *reinterpret_cast<const uint4*>(buf + ct * 16);
+        uint4 v1 = *reinterpret_cast<const uint4*>(buf + (ct + kNCT) * 16);
+        if constexpr (kTail) {
           const int lc0 = c * CE + ct * EV, lc1 = lc0 + kNCT * EV;
-          if (lc0 + EV > segn) v0n = VT::mask_tail(v0n, segn - lc0);
-          if (lc1 + EV > segn) v1n = VT::mask_tail(v1n, segn - lc1);
+          if (lc0 + EV > segn) v0 = VT::mask_tail(v0, segn - lc0);
+          if (lc1 + EV > segn) v1 = VT::mask_tail(v1, segn - lc1);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty[slot]);
@@ -680,21 +681,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
           slot = 0;
           phase ^= 1u;
         }
-        mxn = VT::max_final(VT::max_acc(VT::max_acc(VT::max_init(), v0n), v1n));
-      };
-#if OTK_PIPE_FETCH
-      if (nch > 0) fetch(0);
-#endif
-      for (int c = 0; c < nch; ++c) {
-#if !OTK_PIPE_FETCH
-        fetch(c);
-#endif
-        const uint4 v0 = v0n, v1 = v1n;
-        const float mx = mxn;
-#if OTK_PIPE_FETCH
-        if (c + 1 < nch) fetch(c + 1);
-#endif
         // running max update (rescale the sums when it grows; exact no-op otherwise)
+        const float mx = VT::max_final(VT::max_acc(VT::max_acc(VT::max_init(), v0), v1));
         if (mx != -INFINITY) {
           const float mn = fmaxf(st.m, __fmul_rn(mx, s2));
           if (mn > st.m) {
@@ -717,7 +705,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
           tmem_st8(tm + uint32_t(8 * c), e0, e1);
           tmem_st1(tm + uint32_t(kColM + c), __float_as_uint(mref));
         }
-      }
+      };
+      for (int c = 0; c < nch - 1; ++c) chunk1(c, std::false_type{});
+      if (nch > 0) chunk1(nch - 1, std::true_type{});
       if (kBwd) tmem_wait_st();
 
       Stat tot;
@@ -744,94 +734,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
             if (p.logp) p.logp[row] = rs.logp;
             if (p.entropy) p.entropy[row] = rs.H;
           }
-#if OTK_P2PAIR
-          // ---------------- pass 2: dlogits = coef * e * 2^(m_c - lse) from TMEM, two chunks per load,
-          // the next pair's load in flight while this pair is computed and stored
+          // ---------------- pass 2: dlogits = e * (coef * 2^(m_c - lse)) from TMEM; the TMEM load of chunk
+          // c+1 is in flight while chunk c is scaled and stored (two register sets, ping-pong, no copies)
           char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
-          uint4 ecur[4];
-          uint32_t mcur[2];
-          tmem_ld16_2_issue(tm, tm + uint32_t(kColM), ecur, mcur);
-          tmem_wait_ld_dep16(ecur, mcur);
-          for (int c = 0; c < nch; c += 2) {
-            uint4 enx[4] = {ecur[0], ecur[1], ecur[2], ecur[3]};
-            uint32_t mnx[2] = {mcur[0], mcur[1]};
-            const bool more = c + 2 < nch;
-            if (more) tmem_ld16_2_issue(tm + uint32_t(8 * (c + 2)), tm + uint32_t(kColM + c + 2), enx, mnx);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int cc = c + h;
-              if (cc < nch) {
-                const float kt = __fmul_rn(lo.coef, ex2(__fsub_rn(__uint_as_float(mcur[h]), rs.L2)));
-                const uint64_t kt2 = f2(kt, kt);
-                const uint4 g0 = VT::pass2(ecur[2 * h], kt2), g1 = VT::pass2(ecur[2 * h + 1], kt2);
-                const int lc0 = cc * CE + ct * EV, lc1 = lc0 + kNCT * EV;
-                if (cc < nch - 1) {
-                  stg_cs_v4(drow + size_t(lc0) * sizeof(T), g0);
-                  stg_cs_v4(drow + size_t(lc1) * sizeof(T), g1);
-                } else {  // last (possibly partial) chunk
-                  const uint4 gg[2] = {g0, g1};
-                  const int lcs[2] = {lc0, lc1};
-#pragma unroll
-                  for (int k = 0; k < 2; ++k) {
-                    if (lcs[k] + EV <= segn) {
-                      stg_cs_v4(drow + size_t(lcs[k]) * sizeof(T), gg[k]);
-                    } else if (lcs[k] < segn) {
-                      float g[EV];
-                      VT::unpack(gg[k], g);
-                      for (int i = 0; i < EV && lcs[k] + i < segn; ++i) VT::store1(drow, lcs[k] + i, g[i]);
-                    }
-                  }
-                }
-              }
-            }
-            if (more) {
-              tmem_wait_ld_dep16(enx, mnx);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) ecur[i] = enx[i];
-              mcur[0] = mnx[0];
-              mcur[1] = mnx[1];
-            }
-          }
-#else
-          // ---------------- pass 2: dlogits = coef * e * 2^(m_c - lse) from TMEM (2-deep load pipeline)
-          char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
-          uint4 ea, eb;
-          uint32_t ma;
-          tmem_ld8_1_issue(tm, tm + uint32_t(kColM), ea, eb, ma);
-          tmem_wait_ld_dep(ea, eb, ma);
-          for (int c = 0; c < nch; ++c) {
-            uint4 na = ea, nb = eb;
-            uint32_t nm = ma;
-            if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), na, nb, nm);
-            const float kt = __fmul_rn(lo.coef, ex2(__fsub_rn(__uint_as_float(ma), rs.L2)));
-            const uint64_t kt2 = f2(kt, kt);
-            const uint4 g0 = VT::pass2(ea, kt2), g1 = VT::pass2(eb, kt2);
-            const int lc0 = c * CE + ct * EV, lc1 = lc0 + kNCT * EV;
-            if (c < nch - 1) {
-              stg_cs_v4(drow + size_t(lc0) * sizeof(T), g0);
-              stg_cs_v4(drow + size_t(lc1) * sizeof(T), g1);
-            } else {  // last (possibly partial) chunk
+          char* tp = drow + ct * 16;
+          auto chunk2 = [&](int c, const uint4& e0, const uint4& e1, uint32_t mw) {
+            const float kt = __fmul_rn(lo.coef, ex2(__fsub_rn(__uint_as_float(mw), rs.L2)));
+            const uint4 g0 = VT::pass2(e0, kt), g1 = VT::pass2(e1, kt);
+            char* q0 = tp + size_t(c) * kChunkBytes;
+            if (c < nch - 1 || (c + 1) * CE <= segn) {
+              stg_cs_v4(q0, g0);
+              stg_cs_v4(q0 + kNCT * 16, g1);
+            } else {  // last, partial chunk
               const uint4 gg[2] = {g0, g1};
-              const int lcs[2] = {lc0, lc1};
 #pragma unroll
               for (int k = 0; k < 2; ++k) {
-                if (lcs[k] + EV <= segn) {
-                  stg_cs_v4(drow + size_t(lcs[k]) * sizeof(T), gg[k]);
-                } else if (lcs[k] < segn) {
+                const int lc = c * CE + (ct + k * kNCT) * EV;
+                if (lc + EV <= segn) {
+                  stg_cs_v4(q0 + k * kNCT * 16, gg[k]);
+                } else if (lc < segn) {
                   float g[EV];
                   VT::unpack(gg[k], g);
-                  for (int i = 0; i < EV && lcs[k] + i < segn; ++i) VT::store1(drow, lcs[k] + i, g[i]);
+                  for (int i = 0; i < EV && lc + i < segn; ++i) VT::store1(drow, lc + i, g[i]);
                 }
               }
             }
-            if (c + 1 < nch) {
-              tmem_wait_ld_dep(na, nb, nm);
-              ea = na;
-              eb = nb;
-              ma = nm;
-            }
+          };
+          uint4 a0, a1, b0, b1;
+          uint32_t am, bm;
+          tmem_ld8_1_issue(tm, tm + uint32_t(kColM), a0, a1, am);
+          tmem_wait_ld_dep(a0, a1, am);
+          for (int c = 0;;) {
+            if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), b0, b1, bm);
+            chunk2(c, a0, a1, am);
+            if (++c >= nch) break;
+            tmem_wait_ld_dep(b0, b1, bm);
+            if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), a0, a1, am);
+            chunk2(c, b0, b1, bm);
+            if (++c >= nch) break;
+            tmem_wait_ld_dep(a0, a1, am);
           }
-#endif
           // target column: coef * (p_y - 1), overwriting this thread's own vector store (program order)
           if (ct == owner_ct) VT::store1(drow, ylc, lo.gy);
         }
