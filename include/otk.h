@@ -203,10 +203,11 @@ otk_status otk_policy_loss_fwd_bwd_host(otk_ctx* ctx, int64_t num_rows, int64_t 
 
 /* ---------------------------------------------------------------------------------------------
  * Vocab sharding. A rank holds columns [vocab_start, vocab_start + vocab_local) of every row, with
- * global targets. otk_row_partials writes per row (m2, s, t2, zy) as 4 floats: m2 = log2(e) * max z,
- * s = sum 2^{log2(e) z - m2}, t2 = sum 2^{..}(log2(e) z - m2), zy = z_y if y is in the shard else 0
- * (rows with row_mask 0: (-inf, 0, 0, 0)). The caller all-gathers them into [nshards][num_rows][4]
- * (rank order); the combine (R25) is exact rescaling in rank order, identical on all ranks.
+ * global targets. otk_row_partials writes per row (m2, s, t2, w) as 4 floats: m2 = a reference max of
+ * y = log2(e) * s * x over the shard, s = sum 2^{y - m2}, t2 = sum 2^{y - m2}(y - m2), and w = y_target - m2
+ * if the target column is in the shard, else -inf (rows with row_mask 0: (-inf, 0, 0, -inf)). The caller
+ * all-gathers them into [nshards][num_rows][4] (rank order); the combine (R25) is exact
+ * rescaling in rank order, identical on all ranks.
  * ------------------------------------------------------------------------------------------- */
 typedef struct {
   int64_t vocab_start; /* first global column held by this rank */

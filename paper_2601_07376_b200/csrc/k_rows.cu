@@ -72,14 +72,32 @@ struct RowStats {
   float lse;
 };
 
-__device__ __forceinline__ RowStats finalize(const Stat t, const float zy) {
+// dy = log2(e) * s * x_y - t.m, formed with an FMA against the row reference (no cancellation between two
+// large numbers, so logp keeps ~1e-6 absolute accuracy even for logits of magnitude 1e4).
+__device__ __forceinline__ RowStats finalize(const Stat t, const float dy) {
   RowStats r;
   const float lg2S = lg2(t.s);
   r.L2 = __fadd_rn(t.m, lg2S);
   r.lse = __fmul_rn(r.L2, kLn2);
-  r.logp = __fsub_rn(zy, r.lse);
+  r.logp = __fmul_rn(kLn2, __fsub_rn(dy, lg2S));
   r.H = __fmul_rn(kLn2, __fsub_rn(lg2S, __fdividef(t.t, t.s)));
   return r;
+}
+
+// Combine gathered vocab-shard partials (m, s, t, w) in rank order; w = s2*x_y - m of the shard holding the
+// target (-inf on the others). Returns the row total and dy relative to its reference.
+__device__ __forceinline__ Stat combine_partials(const float4* P, int64_t stride, int nshards, float& dy) {
+  Stat tot{-INFINITY, 0.f, 0.f};
+  for (int k = 0; k < nshards; ++k) {
+    const float4 q = P[int64_t(k) * stride];
+    tot = combine(tot, Stat{q.x, q.y, q.z});
+  }
+  dy = -INFINITY;
+  for (int k = 0; k < nshards; ++k) {
+    const float4 q = P[int64_t(k) * stride];
+    if (q.w != -INFINITY) dy = __fadd_rn(q.w, __fsub_rn(q.x, tot.m));  // m_k - M is exact (Sterbenz)
+  }
+  return tot;
 }
 
 // ---- packed fp32 pairs (sm_100 FFMA2 / FADD2 / FMUL2: two lanes per instruction) -----------------
@@ -112,7 +130,9 @@ __device__ __forceinline__ float f2_sum(uint64_t v) {
   return __fadd_rn(lo, hi);
 }
 
-// One element pair of pass 1: d = s2*x - m; e = 2^d; S += e; T += e*d (per-lane fp32 chains).
+// One element pair of pass 1: d = s2*x - m; e = 2^d; S += e; T += e*d (per-lane fp32 chains; kInit starts
+// the chains instead of adding to them).
+template <bool kInit>
 __device__ __forceinline__ void pass1_pair(float xlo, float xhi, uint64_t s2x2, uint64_t negm2, uint64_t& accS,
                                            uint64_t& accT, float& e0, float& e1) {
   const uint64_t d2 = ffma2(f2(xlo, xhi), s2x2, negm2);
@@ -121,8 +141,13 @@ __device__ __forceinline__ void pass1_pair(float xlo, float xhi, uint64_t s2x2, 
   e0 = ex2(d0);
   e1 = ex2(d1);
   const uint64_t e2 = f2(e0, e1);
-  accS = fadd2(accS, e2);
-  accT = ffma2(e2, d2, accT);
+  if (kInit) {
+    accS = e2;
+    accT = fmul2(e2, d2);
+  } else {
+    accS = fadd2(accS, e2);
+    accT = ffma2(e2, d2, accT);
+  }
 }
 
 // ---- element-type traits ------------------------------------------------------------------------
@@ -143,9 +168,11 @@ struct Vec<float> {
   // e values are kept at full precision for fp32 inputs
   __device__ static __forceinline__ uint4 pack_e(const float (&e)[4]) { return pack(e); }
   __device__ static __forceinline__ void unpack_e(const uint4 v, float (&e)[4]) { unpack(v, e); }
+  // lanes >= nvalid become -1e30 (finite: e = 0 and e*d = 0, no NaN in the fast path)
   __device__ static __forceinline__ uint4 mask_tail(uint4 v, int nvalid) {
-    return make_uint4(nvalid > 0 ? v.x : 0xff800000u, nvalid > 1 ? v.y : 0xff800000u, nvalid > 2 ? v.z : 0xff800000u,
-                      nvalid > 3 ? v.w : 0xff800000u);
+    constexpr uint32_t kLow = 0xf149f2cau;  // -1.0e30f
+    return make_uint4(nvalid > 0 ? v.x : kLow, nvalid > 1 ? v.y : kLow, nvalid > 2 ? v.z : kLow,
+                      nvalid > 3 ? v.w : kLow);
   }
   __device__ static __forceinline__ float vmax_acc(float acc, const uint4 v) {
     return fmaxf(acc, fmaxf(fmaxf(__uint_as_float(v.x), __uint_as_float(v.y)),
@@ -158,15 +185,17 @@ struct Vec<float> {
   __device__ static __forceinline__ float load1(const void* base, int64_t i) {
     return reinterpret_cast<const float*>(base)[i];
   }
-  // pass 1 on one 16-byte vector (4 fp32 logits): e kept at full precision
-  template <bool kKeepE>
+  // pass 1 on one 16-byte vector (4 fp32 logits): e kept at full precision. kClamp maps -inf to -1e30.
+  template <bool kKeepE, bool kClamp, bool kInit>
   __device__ static __forceinline__ uint4 pass1(const uint4 v, uint64_t s2x2, uint64_t negm2, uint64_t (&aS)[2],
                                                 uint64_t (&aT)[2]) {
-    float e[4];
-    pass1_pair(fmaxf(__uint_as_float(v.x), -1e30f), fmaxf(__uint_as_float(v.y), -1e30f), s2x2, negm2, aS[0], aT[0],
-               e[0], e[1]);
-    pass1_pair(fmaxf(__uint_as_float(v.z), -1e30f), fmaxf(__uint_as_float(v.w), -1e30f), s2x2, negm2, aS[1], aT[1],
-               e[2], e[3]);
+    float x[4], e[4];
+    unpack(v, x);
+    if (kClamp)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) x[i] = fmaxf(x[i], -1e30f);
+    pass1_pair<kInit>(x[0], x[1], s2x2, negm2, aS[0], aT[0], e[0], e[1]);
+    pass1_pair<kInit>(x[2], x[3], s2x2, negm2, aS[1], aT[1], e[2], e[3]);
     return kKeepE ? pack(e) : make_uint4(0, 0, 0, 0);
   }
   __device__ static __forceinline__ uint4 pass2(const uint4 e, float kt) {
@@ -211,10 +240,10 @@ struct Vec<__nv_bfloat16> {
     h2f(v.z, e[4], e[5]);
     h2f(v.w, e[6], e[7]);
   }
-  // lanes >= nvalid become -inf (bf16 0xff80)
+  // lanes >= nvalid become -1e30 (bf16 0xf14a: finite, so e = 0 and e*d = 0 without NaN)
   __device__ static __forceinline__ uint32_t mask_word(uint32_t w, int lane0, int nvalid) {
-    if (lane0 >= nvalid) return 0xff80ff80u;
-    if (lane0 + 1 >= nvalid) return (w & 0x0000ffffu) | 0xff800000u;
+    if (lane0 >= nvalid) return 0xf14af14au;
+    if (lane0 + 1 >= nvalid) return (w & 0x0000ffffu) | 0xf14a0000u;
     return w;
   }
   __device__ static __forceinline__ uint4 mask_tail(uint4 v, int nvalid) {
@@ -230,24 +259,24 @@ struct Vec<__nv_bfloat16> {
   __device__ static __forceinline__ float load1(const void* base, int64_t i) {
     return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[i]);
   }
-  // pass 1 on one 16-byte vector (8 bf16 logits). -inf (anything below -1e30) is clamped to -1e30 with
-  // one packed max per pair, so e = 0 and e*d = 0 without a per-element guard. e = 2^(y - m) in (0, 1]
-  // is kept as bf16 (relative error 2^-9; DESIGN.md §6 error budget).
+  // pass 1 on one 16-byte vector (8 bf16 logits). kClamp (the exact path) maps -inf to -1e30 with one packed
+  // max per pair, so e = 0 and e*d = 0. e = 2^(y - m) is kept as bf16 (relative error 2^-9).
+  template <bool kClamp, bool kInit>
   __device__ static __forceinline__ uint32_t pass1_word(uint32_t w, uint64_t s2x2, uint64_t negm2, uint64_t& aS,
                                                         uint64_t& aT) {
-    w = bmax2(w, 0xf14af14au);  // bf16x2(-1.0e30)
+    if (kClamp) w = bmax2(w, 0xf14af14au);  // bf16x2(-1.0e30)
     float e0, e1;
-    pass1_pair(bf_lo(w), bf_hi(w), s2x2, negm2, aS, aT, e0, e1);
+    pass1_pair<kInit>(bf_lo(w), bf_hi(w), s2x2, negm2, aS, aT, e0, e1);
     return pack_bf16x2(e0, e1);
   }
-  template <bool kKeepE>
+  template <bool kKeepE, bool kClamp, bool kInit>
   __device__ static __forceinline__ uint4 pass1(const uint4 v, uint64_t s2x2, uint64_t negm2, uint64_t (&aS)[2],
                                                 uint64_t (&aT)[2]) {
     uint4 r;
-    r.x = pass1_word(v.x, s2x2, negm2, aS[0], aT[0]);
-    r.y = pass1_word(v.y, s2x2, negm2, aS[1], aT[1]);
-    r.z = pass1_word(v.z, s2x2, negm2, aS[0], aT[0]);
-    r.w = pass1_word(v.w, s2x2, negm2, aS[1], aT[1]);
+    r.x = pass1_word<kClamp, kInit>(v.x, s2x2, negm2, aS[0], aT[0]);
+    r.y = pass1_word<kClamp, kInit>(v.y, s2x2, negm2, aS[1], aT[1]);
+    r.z = pass1_word<kClamp, false>(v.z, s2x2, negm2, aS[0], aT[0]);
+    r.w = pass1_word<kClamp, false>(v.w, s2x2, negm2, aS[1], aT[1]);
     return r;
   }
   // g = e * kt directly in bf16x2: kt is split into kt_hi + kt_lo (both bf16), g = fma(e, kt_hi, e * kt_lo)
@@ -372,7 +401,7 @@ __device__ __forceinline__ void inactive_row(const RowParams& p, int64_t row, in
       if (p.entropy) p.entropy[row] = 0.f;
       if (p.lse) p.lse[row] = 0.f;
     } else {
-      p.partials_out[row] = make_float4(-INFINITY, 0.f, 0.f, 0.f);
+      p.partials_out[row] = make_float4(-INFINITY, 0.f, 0.f, -INFINITY);
     }
   }
 }
@@ -676,8 +705,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
 
       // ---------------- pass 1: online max / sum 2^(y-m) / sum 2^(y-m)(y-m), one exponential per element
       const int owner_ct = ylc >= 0 ? ((ylc % CE) / EV) % kNCT : -1;  // thread that stores the target column
-      Stat st{-INFINITY, 0.f, 0.f};
-      // one chunk of pass 1; kTail only for the segment's last chunk (lanes past segn become -inf)
+      // Row-level pair accumulators of (sum e, sum e*d). The reference max mref is set by the row's first
+      // chunk (exact path) and raised only when a chunk's values overflow 2^64 or hold -inf — detected from
+      // the chunk's partial sums — so the common chunk needs neither a max reduction nor a rescale.
+      uint64_t rS = 0ull, rT = 0ull;
+      float mref = -INFINITY;
+      // one chunk of pass 1; kTail only for the segment's last chunk (lanes past segn become -1e30)
       auto chunk1 = [&](int c, auto tail) {
         constexpr bool kTail = decltype(tail)::value;
         mbar_wait(&S.full[slot], phase);
@@ -695,42 +728,63 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
           slot = 0;
           phase ^= 1u;
         }
-        // running max update (rescale the sums when it grows; exact no-op otherwise)
-        const float mx = VT::max_final(VT::max_acc(VT::max_acc(VT::max_init(), v0), v1));
-        if (mx != -INFINITY) {
-          const float mn = fmaxf(st.m, __fmul_rn(mx, s2));
-          if (mn > st.m) {
-            if (st.m != -INFINITY) {
-              const float d = __fsub_rn(st.m, mn), f = ex2(d);
-              st.t = __fmul_rn(f, __fmaf_rn(d, st.s, st.t));
-              st.s = __fmul_rn(st.s, f);
-            }
-            st.m = mn;
-          }
+        uint64_t cS[2], cT[2];
+        uint4 e0, e1;
+        bool ok = false;
+        if (mref != -INFINITY) {  // fast path: fixed reference, no clamp
+          const uint64_t negm2 = f2(-mref, -mref);
+          e0 = VT::template pass1<kBwd, false, true>(v0, s2x2, negm2, cS, cT);
+          e1 = VT::template pass1<kBwd, false, false>(v1, s2x2, negm2, cS, cT);
+          const uint64_t sS = fadd2(cS[0], cS[1]), sT = fadd2(cT[0], cT[1]);
+          float s0, s1, t0, t1;
+          f2_split(sS, s0, s1);
+          f2_split(sT, t0, t1);
+          ok = fmaxf(s0, s1) <= 0x1p64f && !isnan(t0 + t1);  // also false for inf / NaN sums
+          cS[0] = sS;
+          cT[0] = sT;
         }
-        const float mref = (st.m == -INFINITY) ? 0.f : st.m;
-        const uint64_t negm2 = f2(-mref, -mref);
-        uint64_t aS[2] = {0ull, 0ull}, aT[2] = {0ull, 0ull};
-        const uint4 e0 = VT::template pass1<kBwd>(v0, s2x2, negm2, aS, aT);
-        const uint4 e1 = VT::template pass1<kBwd>(v1, s2x2, negm2, aS, aT);
-        st.s = __fadd_rn(st.s, __fadd_rn(f2_sum(aS[0]), f2_sum(aS[1])));
-        st.t = __fadd_rn(st.t, __fadd_rn(f2_sum(aT[0]), f2_sum(aT[1])));
+        if (!ok) {  // exact path: the row's first chunk, an overflow, or -inf logits
+          // lanes at or below -1e30 (masked tails, clamped -inf) never set the reference: with a reference
+          // that large, s2*x - m would be dominated by the rounding residual of the product
+          const float mx = VT::max_final(VT::max_acc(VT::max_acc(VT::max_init(), v0), v1));
+          if (mx > -1e30f) {
+            const float mn = fmaxf(mref, __fmul_rn(mx, s2));
+            if (mn > mref) {
+              if (mref != -INFINITY) {
+                const float d = __fsub_rn(mref, mn), f = ex2(d);
+                const uint64_t f2x = f2(f, f);
+                rT = fmul2(f2x, ffma2(f2(d, d), rS, rT));
+                rS = fmul2(rS, f2x);
+              }
+              mref = mn;
+            }
+          }
+          const float mr = (mref == -INFINITY) ? 0.f : mref;
+          const uint64_t negm2 = f2(-mr, -mr);
+          e0 = VT::template pass1<kBwd, true, true>(v0, s2x2, negm2, cS, cT);
+          e1 = VT::template pass1<kBwd, true, false>(v1, s2x2, negm2, cS, cT);
+          cS[0] = fadd2(cS[0], cS[1]);
+          cT[0] = fadd2(cT[0], cT[1]);
+        }
+        rS = fadd2(rS, cS[0]);
+        rT = fadd2(rT, cT[0]);
         if (kBwd) {
           tmem_st8(tm + uint32_t(8 * c), e0, e1);
-          tmem_st1(tm + uint32_t(kColM + c), __float_as_uint(mref));
+          tmem_st1(tm + uint32_t(kColM + c), __float_as_uint(mref == -INFINITY ? 0.f : mref));
         }
       };
       for (int c = 0; c < nch - 1; ++c) chunk1(c, std::false_type{});
       if (nch > 0) chunk1(nch - 1, std::true_type{});
+      const Stat st{mref, f2_sum(rS), f2_sum(rT)};
       if (kBwd) tmem_wait_st();
 
       Stat tot;
       row_total(S, st, lane, cw, ct, csize, crank, q, tot);
-      const float zyt = __fmul_rn(p.scale, xy);
+      const float dy = (yg >= 0 && yg < p.vocab) ? __fmaf_rn(xy, s2, -tot.m) : -INFINITY;
       if (MODE == kModePartial) {
-        if (ct == 0 && crank == 0) p.partials_out[row] = make_float4(tot.m, tot.s, tot.t, zyt);
+        if (ct == 0 && crank == 0) p.partials_out[row] = make_float4(tot.m, tot.s, tot.t, dy);
       } else {
-        const RowStats rs = finalize(tot, zyt);
+        const RowStats rs = finalize(tot, dy);
         if (MODE == kModeFwd) {
           if (ct == 0 && crank == 0) {
             p.logp[row] = rs.logp;
@@ -864,14 +918,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) 
       const int64_t ylc64 = int64_t(y) - p.vocab_start - c0;
       const int ylc = (ylc64 >= 0 && ylc64 < segn) ? int(ylc64) : -1;
       // every thread combines the gathered partials (rank order) and evaluates the loss terms
-      Stat tot{-INFINITY, 0.f, 0.f};
-      float zyt = 0.f;
-      for (int k = 0; k < p.nshards; ++k) {
-        const float4 P = p.partials_in[int64_t(k) * p.num_rows + row];
-        tot = combine(tot, Stat{P.x, P.y, P.z});
-        zyt += P.w;
-      }
-      const RowStats rs = finalize(tot, zyt);
+      float dy;
+      const Stat tot = combine_partials(p.partials_in + row, p.num_rows, p.nshards, dy);
+      const RowStats rs = finalize(tot, dy);
       RowSide sd{p.adv[p.row_traj[row]], p.old_logp[row], p.ref_logp ? p.ref_logp[row] : 0.f};
       const LossOut lo = loss_terms(p, rs.logp, sd, invN);
       if (ct == 0 && crank == 0) {
@@ -936,14 +985,9 @@ __global__ void k_combine(int64_t num_rows, int nshards, const float4* __restric
       if (lse) lse[row] = 0.f;
       continue;
     }
-    Stat tot{-INFINITY, 0.f, 0.f};
-    float zyt = 0.f;
-    for (int k = 0; k < nshards; ++k) {
-      const float4 P = partials[int64_t(k) * num_rows + row];
-      tot = combine(tot, Stat{P.x, P.y, P.z});
-      zyt += P.w;
-    }
-    const RowStats rs = finalize(tot, zyt);
+    float dy;
+    const Stat tot = combine_partials(partials + row, num_rows, nshards, dy);
+    const RowStats rs = finalize(tot, dy);
     logp[row] = rs.logp;
     if (entropy) entropy[row] = rs.H;
     if (lse) lse[row] = rs.lse;

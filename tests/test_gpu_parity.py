@@ -348,3 +348,55 @@ def test_host_entry_point_matches_device(otk, ctx):
     assert torch.equal(dl_host, dev["dlogits"].cpu())
     want = otk.stats_dict(dev["stats"])
     assert abs(st["loss"] - want["loss"]) < 1e-12 and st["n_tokens"] == want["n_tokens"]
+
+
+# ------------------------------------------------------------------------------------------ numerics edge cases
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_extreme_rows(otk, ctx, dtype):
+    """-inf logits, late maxima 40-90 nats above everything seen before (the kernel's overflow re-reference
+    path), very negative rows, and the uniform row, for the forward and the fused loss."""
+    import torch as T
+    V = 151936
+    n = 12
+    rng = np.random.default_rng(77)
+    x = rng.normal(scale=2.0, size=(n, V))
+    x[0, rng.integers(0, V, 5000)] = -np.inf                 # sprinkled -inf
+    x[1, : V // 2] = -np.inf                                  # the whole first half (first CTA segment) -inf
+    x[2, V - 5] = 90.0                                        # max in the last chunk, far above the reference
+    x[3, 70000] = 60.0
+    x[3, 150000] = 120.0                                      # two late jumps
+    x[4] -= 1e4                                               # very negative, finite
+    x[5] = 0.0                                                # uniform
+    x[6, 3] = 50.0                                            # early dominant token
+    t = T.from_numpy(x).to(T.bfloat16 if dtype == "bf16" else T.float32)
+    wide = t.to(T.float64).numpy()
+    y = rng.integers(0, V, n)
+    y[1] = V - 7                                              # target in the finite half
+    y[2] = V - 5
+    y[3] = 3
+    tg = T.from_numpy(y.astype(np.int32)).cuda()
+    lg = t.cuda()
+    f = otk.otk_logprob_entropy_fwd(ctx, lg, tg)
+    want = O.logprob_entropy_fwd(wide, y)
+    # fp32 outputs of magnitude ~100 carry ~4e-6 of rounding alone: the fp32 tolerance scales as
+    # 1e-5 + 2^-22 |value| (DESIGN.md §6)
+    tol = LOGP_TOL[dtype] + (2.0 ** -22 if dtype == "f32" else 0.0) * np.abs(want["logp"])
+    assert np.all(np.abs(f["logp"].cpu().numpy() - want["logp"]) < tol)
+    assert np.all(np.abs(f["entropy"].cpu().numpy() - want["entropy"]) < LOGP_TOL[dtype])
+    mask = np.ones(n, np.uint8)
+    rt = np.zeros(n, np.int32)
+    adv = np.array([0.7])
+    old = (want["logp"] + rng.normal(scale=0.05, size=n)).astype(np.float32)
+    ref = (want["logp"] + rng.normal(scale=0.1, size=n)).astype(np.float32)
+    cfg = otk.LossCfg()
+    out = otk.otk_policy_loss_fwd_bwd(ctx, lg, tg, T.from_numpy(mask).cuda(), T.from_numpy(rt).cuda(),
+                                      T.from_numpy(adv).cuda(), T.from_numpy(old).cuda(), T.from_numpy(ref).cuda(),
+                                      T.tensor([n], dtype=T.int64, device="cuda"), cfg)
+    ctx.check()
+    assert T.equal(out["logp"], f["logp"])                   # same reduction order as the forward
+    ocfg = oracle_cfg(cfg)
+    w = O.policy_loss_fwd_bwd(wide, y, mask, rt, adv, old.astype(np.float64), ref.astype(np.float64), n, ocfg)
+    h = dict(old=old.astype(np.float64), ref=ref.astype(np.float64), adv=adv, row_traj=rt, mask=mask)
+    dc = dcoef_rows(h, w["logp"], ocfg, n, True)
+    assert check_dlogits_rows(out["dlogits"], w["dlogits"], w["coef"], list(range(n)), dtype, V, dc) <= 1.0
+    assert not bool(T.isnan(out["dlogits"].float()).any())
