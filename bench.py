@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--shard", default="batch", choices=["batch", "vocab"],
+                    help="batch: each rank owns whole trajectories (weak scaling); vocab: each rank owns V/N "
+                         "columns of every row (strong scaling, row partials all-gathered)")
     return ap.parse_args()
 
 
@@ -55,8 +58,13 @@ def dist_setup(args):
     pg = None
     if world > 1:
         import torch.distributed as dist
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("OTK_DIST_BACKEND", "nccl")   # gloo: multi-rank functional runs on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         pg = dist.group.WORLD
     else:
         torch.cuda.set_device(0)
@@ -124,13 +132,21 @@ def peaks():
 
 # ------------------------------------------------------------------------------------------------
 def build_workload(args, rank, world, device):
-    """Synthetic inputs (untimed): this rank's trajectories, cycled logits buffers, per-row old/ref."""
+    """Synthetic inputs (untimed): this rank's trajectories, cycled logits buffers, per-row old/ref.
+    batch sharding: rank-specific trajectories (seed + 1000 * rank), full-vocabulary logits.
+    vocab sharding: the same trajectories and targets on every rank, logits columns [v0, v1) of this rank."""
     import paper_2601_07376_b200 as otk
+    from paper_2601_07376_b200.dist import vocab_shard_bounds
+    from paper_2601_07376_b200.step import MicroBatch, VocabShard
     from synth import CONFIGS, make_batch, make_logits, make_noise
     cfgw = CONFIGS[args.config]
-    tb = make_batch(args.config, seed=cfgw.seed + 1000 * rank)
-    tb.group_id = tb.group_id + np.int32(rank * cfgw.num_groups)   # this rank's groups (global ids)
+    vocab_mode = args.shard == "vocab"
+    brank = 0 if vocab_mode else rank
+    tb = make_batch(args.config, seed=cfgw.seed + 1000 * brank)
+    tb.group_id = tb.group_id + np.int32(brank * cfgw.num_groups)   # this rank's groups (global ids)
     N, V = tb.num_rows, cfgw.V
+    v0, v1 = vocab_shard_bounds(V, world)[rank] if vocab_mode else (0, V)
+    Vl = v1 - v0
     M = min(args.micro_rows, N)
     ctx = otk.Context(torch.cuda.current_device())
     dbatch = otk.traj_batch_to_device(tb, device)
@@ -140,14 +156,25 @@ def build_workload(args, rank, world, device):
     nbuf = max(1, min(args.logit_buffers, (N + M - 1) // M))
     bufs, tgts = [], []
     for k in range(nbuf):
-        lg, tg = make_logits(M, V, dtype=cfgw.dtype, seed=cfgw.seed * 100 + 10 * rank + k, device=device,
+        lg, tg = make_logits(M, Vl, dtype=cfgw.dtype, seed=cfgw.seed * 100 + 10 * rank + k, device=device,
                              rows_per_chunk=4096)
+        if vocab_mode:   # global targets, identical on every rank
+            g = torch.Generator(device=device)
+            g.manual_seed(cfgw.seed * 100 + k)
+            tg = torch.randint(0, V, (M,), generator=g, device=device, dtype=torch.int32)
         bufs.append(lg)
         tgts.append(tg)
     dlogits = torch.empty_like(bufs[0])
-    # old/ref = the fwd pool's log-probs (otk_logprob_entropy_fwd) + synth noise, per micro-batch
-    base_logp = [otk.otk_logprob_entropy_fwd(ctx, b, t)["logp"] for b, t in zip(bufs, tgts)]
-    from paper_2601_07376_b200.step import MicroBatch
+    vshard = VocabShard(ctx, v0, Vl, V, None) if vocab_mode else None
+    pg = None
+    if vocab_mode and world > 1:
+        import torch.distributed as dist
+        vshard.pg = dist.group.WORLD
+    # old/ref = the fwd pool's log-probs (otk_logprob_entropy_fwd, or its vocab-sharded form) + synth noise
+    if vocab_mode:
+        base_logp = [vshard.forward(b, t)["logp"] for b, t in zip(bufs, tgts)]
+    else:
+        base_logp = [otk.otk_logprob_entropy_fwd(ctx, b, t)["logp"] for b, t in zip(bufs, tgts)]
     mbs = []
     for i, r0 in enumerate(range(0, N, M)):
         r1 = min(N, r0 + M)
@@ -159,7 +186,7 @@ def build_workload(args, rank, world, device):
                               None if ref is None else ref.contiguous(), dlogits[:n]))
     ctx.check()
     return dict(otk=otk, cfgw=cfgw, tb=tb, ctx=ctx, dbatch=dbatch, gid=gid, toff=toff, trew=trew, bufs=bufs,
-                tgts=tgts, mbs=mbs, N=N, V=V, M=M, dlogits=dlogits)
+                tgts=tgts, mbs=mbs, N=N, V=V, Vl=Vl, v0=v0, M=M, dlogits=dlogits, vshard=vshard)
 
 
 def algorithmic_bytes(V, n_train, n_masked, beta):
@@ -177,12 +204,11 @@ def run_otk(args):
     from paper_2601_07376_b200.step import PolicyLossStep
     cfgw = W["cfgw"]
     cfg = otk.LossCfg(kl_beta=cfgw.kl_beta)
-    step = PolicyLossStep(ctx, W["dbatch"], W["gid"], cfgw.num_groups * world if pg else cfgw.num_groups,
-                          W["toff"], W["trew"], W["V"], cfg, process_group=pg,
-                          global_num_traj=[W["tb"].num_traj] * world if pg else None,
-                          global_num_groups=cfgw.num_groups * world if pg else None)
-    if pg is None:
-        step.num_groups = cfgw.num_groups
+    vocab_mode = args.shard == "vocab"
+    bpg = pg if not vocab_mode else None
+    step = PolicyLossStep(ctx, W["dbatch"], W["gid"], cfgw.num_groups, W["toff"], W["trew"], W["Vl"], cfg,
+                          process_group=bpg, global_num_traj=[W["tb"].num_traj] * world if bpg else None,
+                          global_num_groups=cfgw.num_groups * world if bpg else None, vocab_shard=W["vshard"])
     stream = torch.cuda.current_stream()
     nmb = len(W["mbs"])
     # CUDA events around every loss launch of every timed step, on the launching stream
@@ -230,27 +256,40 @@ def run_otk(args):
     lm = step.masks["loss_mask"]
     n_train = [int(lm[mb.r0:mb.r1].sum()) for mb in W["mbs"]]
     n_rows = [mb.r1 - mb.r0 for mb in W["mbs"]]
-    bytes_k4 = [algorithmic_bytes(W["V"], t, r - t, cfgw.kl_beta) for t, r in zip(n_train, n_rows)]
+    if vocab_mode:   # row partials (read 2V_l) + all-gather + streaming pass 2 (read 2V_l, write 2V_l)
+        Vl = W["Vl"]
+        side = 4 + 1 + 4 + 4 + (4 if cfgw.kl_beta else 0) + 16 * world
+        bytes_k4 = [t * (6 * Vl + side) + (r - t) * (2 * Vl + 1) for t, r in zip(n_train, n_rows)]
+        kname = "k_rows_tm<bf16,PARTIAL> + all_gather + k_rows_stream<bf16> (vocab-sharded loss)"
+    else:
+        bytes_k4 = [algorithmic_bytes(W["V"], t, r - t, cfgw.kl_beta) for t, r in zip(n_train, n_rows)]
+        kname = "k_rows_tm<bf16,BWD> (otk_policy_loss_fwd_bwd)"
     avg_bytes = sum(bytes_k4) / nmb
     avg_ms = sum(k4_ms) / nmb
     achieved = avg_bytes / (avg_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
-    total_rows = W["N"] * world
+    total_rows = W["N"] * (1 if vocab_mode else world)
     value = total_rows / (ms_per_step * 1e-3)
     step_bytes = sum(bytes_k4)
+    if world == 1:
+        par = "single GPU" + (" (vocab-shard path, 1 shard)" if vocab_mode else "")
+    else:
+        par = f"vocab-shard tp{world}" if vocab_mode else f"batch-shard dp{world}"
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if vocab_mode else "weak",
         "vs_baseline": None, "dtype": cfgw.dtype, "data": "synthetic (seeded; SURVEY.md §8(d) recipe)",
-        "config": {"workload": f"{args.config}: {cfgw.note}", "global_batch_traj": W["tb"].num_traj * world,
-                   "rows_per_gpu": W["N"], "vocab": W["V"], "micro_batch_rows": W["M"],
-                   "micro_batches": nmb, "parallelism": f"batch-shard dp{world}" if world > 1 else "single GPU",
+        "config": {"workload": f"{args.config}: {cfgw.note}",
+                   "global_batch_traj": W["tb"].num_traj * (1 if vocab_mode else world),
+                   "rows_per_gpu": W["N"], "vocab": W["V"], "vocab_per_gpu": W["Vl"], "micro_batch_rows": W["M"],
+                   "micro_batches": nmb, "parallelism": par,
                    "l2": f"inputs >> L2: {len(W['bufs'])} logits buffers of "
                          f"{W['bufs'][0].numel() * W['bufs'][0].element_size() / 1e9:.1f} GB cycled",
                    "kl_beta": cfgw.kl_beta, "clip": [0.2, 0.2], "kl": "k3"},
-        "trainable_rows_per_s": sum(n_train) * world / (ms_per_step * 1e-3),
+        "trainable_rows_per_s": sum(n_train) * (1 if vocab_mode else world) / (ms_per_step * 1e-3),
         "step_algorithmic_GBps": step_bytes / (ms_per_step * 1e-3) / 1e9,
-        "roofline": {"bound": "hbm", "kernel": "k_rows<bf16,BWD> (otk_policy_loss_fwd_bwd)",
+        "roofline": {"bound": "hbm", "kernel": kname,
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "peak_source": peak_src,
                      "bytes_per_launch": avg_bytes, "avg_launch_ms": avg_ms,
@@ -261,16 +300,16 @@ def run_otk(args):
     }
     res["clocks"] = clk.summary()
     traffic = os.path.join(ROOT, "profiles", "k4_traffic.json")
-    if os.path.exists(traffic):
+    if os.path.exists(traffic) and not vocab_mode:
         try:
             tj = json.load(open(traffic))
             res["roofline"]["traffic"] = tj.get("traffic_bytes_per_launch")
             res["roofline"]["traffic_source"] = tj.get("source")
         except Exception:
             pass
-    if not args.no_e2e:
+    if not args.no_e2e and not vocab_mode:
         res["e2e"] = e2e(args, W, world, step, cfg)
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline and not vocab_mode:
         res["cpu_baseline"] = cpu_baseline(args, W, cfg)
     if rank == 0:
         print(json.dumps(res), flush=True)

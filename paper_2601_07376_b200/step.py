@@ -9,6 +9,9 @@ DESIGN.md §7), the exchanges between them:
   otk_policy_loss_fwd_bwd x M micro-batches (stats accumulated on the device)
                              -> all_reduce(stats, SUM)             global loss on every rank
 
+Vocab sharding (VocabShard): every rank holds all rows and a column range; per micro-batch
+  otk_row_partials -> all_gather(16 B / row) -> otk_policy_loss_fwd_bwd_partials (identical stats on all ranks).
+
 No host synchronisation inside a step (n_loss and the stats never leave the device), so a step can be
 captured in a CUDA graph. Everything arithmetic happens in libotk's kernels; this module only moves
 pointers and calls collectives.
@@ -21,7 +24,8 @@ from typing import Callable, List, Optional, Sequence, Tuple
 import torch
 
 from . import (Context, DeviceTrajBatch, LossCfg, STATS_FIELDS, otk_build_masks, otk_group_advantages,
-               otk_policy_loss_fwd_bwd)
+               otk_logprob_entropy_combine, otk_policy_loss_fwd_bwd, otk_policy_loss_fwd_bwd_partials,
+               otk_row_partials)
 
 
 @dataclass
@@ -36,12 +40,46 @@ class MicroBatch:
     dlogits: torch.Tensor           # [r1 - r0, ld] output
 
 
+class VocabShard:
+    """(3) and (4) on a vocab shard [vocab_start, vocab_start + vocab_local) of every row:
+    otk_row_partials (16 B per row) -> all_gather in rank order -> exact combine / streaming pass 2.
+    Every rank ends with the same logp, entropy and loss statistics."""
+
+    def __init__(self, ctx: Context, vocab_start: int, vocab_local: int, vocab_total: int, process_group=None):
+        self.ctx, self.v0, self.vl, self.vt, self.pg = ctx, vocab_start, vocab_local, vocab_total, process_group
+
+    def _gather(self, partials):
+        if self.pg is None:
+            return partials.unsqueeze(0)
+        from .dist import all_gather_vocab_partials
+        return all_gather_vocab_partials(partials, self.pg)
+
+    def forward(self, logits: torch.Tensor, targets: torch.Tensor, row_mask=None, logit_scale: float = 1.0):
+        part = otk_row_partials(self.ctx, logits, targets, self.v0, self.vt, vocab_local=self.vl, row_mask=row_mask,
+                                logit_scale=logit_scale)
+        return otk_logprob_entropy_combine(self.ctx, self._gather(part), row_mask=row_mask)
+
+    def loss(self, logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss, cfg: LossCfg, *,
+             dlogits=None, stats=None, accumulate=None):
+        part = otk_row_partials(self.ctx, logits, targets, self.v0, self.vt, vocab_local=self.vl, row_mask=loss_mask,
+                                logit_scale=cfg.logit_scale)
+        return otk_policy_loss_fwd_bwd_partials(self.ctx, logits, targets, loss_mask, row_traj, adv, old_logp,
+                                                ref_logp, n_loss, cfg, self.v0, self.vt, self._gather(part),
+                                                vocab_local=self.vl, dlogits=dlogits, stats=stats,
+                                                accumulate=accumulate)
+
+
 class PolicyLossStep:
     def __init__(self, ctx: Context, batch: DeviceTrajBatch, group_id: torch.Tensor, num_groups: int,
                  turn_offsets: torch.Tensor, turn_rewards: torch.Tensor, vocab: int, cfg: LossCfg = LossCfg(), *,
                  train_agent: int = -1, std_norm: bool = True, unbiased: bool = False,
                  process_group=None, global_num_traj: Optional[Sequence[int]] = None,
-                 global_num_groups: Optional[int] = None):
+                 global_num_groups: Optional[int] = None, vocab_shard: Optional[VocabShard] = None):
+        """process_group: batch sharding (this rank's trajectories; exchanges below). vocab_shard: vocab
+        sharding (every rank holds all rows, a column range of the logits). Exclusive."""
+        if process_group is not None and vocab_shard is not None:
+            raise ValueError("batch and vocab sharding are exclusive in this step (2-D sharding is future work)")
+        self.vshard = vocab_shard
         self.ctx, self.batch, self.cfg, self.vocab = ctx, batch, cfg, vocab
         self.group_id, self.num_groups = group_id, num_groups
         self.turn_offsets, self.turn_rewards = turn_offsets, turn_rewards
@@ -53,11 +91,12 @@ class PolicyLossStep:
                           row_traj=torch.empty(N, dtype=torch.int32, device=dev),
                           traj_loss_tokens=torch.empty(B, dtype=torch.int64, device=dev),
                           n_loss=torch.empty(1, dtype=torch.int64, device=dev))
+        G_loc = global_num_groups if (process_group is not None and global_num_groups) else num_groups
         self.adv_out = dict(adv=torch.empty(B, dtype=torch.float64, device=dev),
                             returns=torch.empty(B, dtype=torch.float64, device=dev),
-                            group_mean=torch.empty(num_groups, dtype=torch.float64, device=dev),
-                            group_std=torch.empty(num_groups, dtype=torch.float64, device=dev),
-                            group_size=torch.empty(num_groups, dtype=torch.int32, device=dev))
+                            group_mean=torch.empty(G_loc, dtype=torch.float64, device=dev),
+                            group_std=torch.empty(G_loc, dtype=torch.float64, device=dev),
+                            group_size=torch.empty(G_loc, dtype=torch.int32, device=dev))
         self.stats = torch.zeros(len(STATS_FIELDS), dtype=torch.float64, device=dev)
         if self.pg is not None:
             import torch.distributed as dist
@@ -88,14 +127,14 @@ class PolicyLossStep:
             return self.adv_out["adv"]
         from .dist import all_gather_group_returns, all_reduce_n_loss
         all_reduce_n_loss(self.masks["n_loss"], self.pg)
-        # local returns (group statistics of this call are discarded), then the global exchange
-        otk_group_advantages(self.ctx, self.group_id, self.num_groups, turn_offsets=self.turn_offsets,
+        # local returns (group statistics of this call are discarded; ids are global), then the exchange
+        otk_group_advantages(self.ctx, self.group_id, self.G_global, turn_offsets=self.turn_offsets,
                              turn_rewards=self.turn_rewards, out=self.adv_out)
         all_gather_group_returns(self.group_id, self.adv_out["returns"], self.counts, self.pg,
                                  out=(self.gid_g, self.ret_g))
         otk_group_advantages(self.ctx, self.gid_g, self.G_global, returns=self.ret_g, std_norm=self.std_norm,
                              unbiased=self.unbiased, out=self.adv_g)
-        return self.adv_g["adv"][self.b0:self.b0 + B]
+        return self.adv_g["adv"][self.b0:self.b0 + self.batch.num_traj]
 
     # -- (3) + (4) --------------------------------------------------------------------------------
     def loss(self, adv: torch.Tensor, micro_batches: Sequence[MicroBatch],
@@ -103,10 +142,16 @@ class PolicyLossStep:
         for k, mb in enumerate(micro_batches):
             if on_launch:
                 on_launch(k, "begin")
-            otk_policy_loss_fwd_bwd(self.ctx, mb.logits, mb.targets, self.masks["loss_mask"][mb.r0:mb.r1],
-                                    self.masks["row_traj"][mb.r0:mb.r1], adv, mb.old_logp, mb.ref_logp,
-                                    self.masks["n_loss"], self.cfg, vocab=self.vocab, dlogits=mb.dlogits,
-                                    stats=self.stats, accumulate=k > 0, want_logp=False)
+            if self.vshard is not None:
+                self.vshard.loss(mb.logits, mb.targets, self.masks["loss_mask"][mb.r0:mb.r1],
+                                 self.masks["row_traj"][mb.r0:mb.r1], adv, mb.old_logp, mb.ref_logp,
+                                 self.masks["n_loss"], self.cfg, dlogits=mb.dlogits, stats=self.stats,
+                                 accumulate=k > 0)
+            else:
+                otk_policy_loss_fwd_bwd(self.ctx, mb.logits, mb.targets, self.masks["loss_mask"][mb.r0:mb.r1],
+                                        self.masks["row_traj"][mb.r0:mb.r1], adv, mb.old_logp, mb.ref_logp,
+                                        self.masks["n_loss"], self.cfg, vocab=self.vocab, dlogits=mb.dlogits,
+                                        stats=self.stats, accumulate=k > 0, want_logp=False)
             if on_launch:
                 on_launch(k, "end")
         if self.pg is not None:
