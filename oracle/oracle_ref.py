@@ -205,6 +205,9 @@ def logprob_entropy_fwd(logits, targets, row_mask=None, logit_scale: float = 1.0
 # --------------------------------------------------------------------------------------------
 # O4: PPO-clip + KL surrogate, token-mean, fused backward  (north_star (4))
 # --------------------------------------------------------------------------------------------
+TOKEN_MEAN, SEQ_MEAN_TOKEN_MEAN, SEQ_MEAN_TOKEN_SUM = 0, 1, 2
+
+
 @dataclass
 class LossCfg:
     clip_low: float = 0.2          # epsilon_low  (R14)
@@ -213,6 +216,11 @@ class LossCfg:
     kl_type: int = KL_K3
     log_ratio_clamp: float = 20.0  # C (R15)
     logit_scale: float = 1.0       # s = 1/temperature (R19)
+    # A4 variants (R27-R30)
+    ent_coef: float = 0.0          # entropy bonus c_H: L -= c_H * H
+    dual_clip: float = 0.0         # c > 1 caps the loss of A < 0 tokens at -c*A (0 = off)
+    sft: bool = False              # supervised mode: L = -logp, ignores A / old / clip
+    reduction: int = TOKEN_MEAN    # TOKEN_MEAN | SEQ_MEAN_TOKEN_MEAN | SEQ_MEAN_TOKEN_SUM
 
 
 def row_loss_terms(logp: float, old: float, ref: Optional[float], A: float, cfg: LossCfg):
@@ -221,18 +229,29 @@ def row_loss_terms(logp: float, old: float, ref: Optional[float], A: float, cfg:
     delta = clamp(logp - old, -C, C); r = exp(delta); rbar = min(max(r, 1-eps_lo), 1+eps_hi)
     pg = max(-A*r, -A*rbar); clipped <=> (A>0 and r>1+eps_hi) or (A<0 and r<1-eps_lo)
     dpg/dlogp = 0 if clipped or |logp-old| > C else -A*r
+    dual clip (c > 1, A < 0): pg <- min(pg, -c*A), zero gradient where the cap is active
+    sft: pg = -logp, dpg/dlogp = -1 (A, old and the clip are not used)
     k3: d = clamp(ref - logp, -C, C); KL = exp(d) - d - 1; dKL/dlogp = 0 if |ref-logp| > C else 1 - exp(d)
     k1: KL = logp - ref, dKL/dlogp = 1;   k2: KL = (logp-ref)^2/2, dKL/dlogp = logp - ref
-    Returns (L, G, clipped, KL).
+    Returns (L, G, clipped, KL). The entropy bonus (-c_H * H) is added by the caller: it depends on the
+    whole row, not on logp alone.
     """
     C = cfg.log_ratio_clamp
-    draw = logp - old
-    delta = min(max(draw, -C), C)
-    r = math.exp(delta)
-    rbar = min(max(r, 1.0 - cfg.clip_low), 1.0 + cfg.clip_high)
-    pg = max(-A * r, -A * rbar)
-    clipped = (A > 0 and r > 1.0 + cfg.clip_high) or (A < 0 and r < 1.0 - cfg.clip_low)
-    G = 0.0 if (clipped or abs(draw) > C) else -A * r
+    clipped = False
+    if cfg.sft:
+        pg = -logp
+        G = -1.0
+    else:
+        draw = logp - old
+        delta = min(max(draw, -C), C)
+        r = math.exp(delta)
+        rbar = min(max(r, 1.0 - cfg.clip_low), 1.0 + cfg.clip_high)
+        pg = max(-A * r, -A * rbar)
+        clipped = (A > 0 and r > 1.0 + cfg.clip_high) or (A < 0 and r < 1.0 - cfg.clip_low)
+        G = 0.0 if (clipped or abs(draw) > C) else -A * r
+        if cfg.dual_clip > 0.0 and A < 0 and pg > -cfg.dual_clip * A:
+            pg = -cfg.dual_clip * A
+            G = 0.0
     kl = 0.0
     if cfg.kl_beta != 0.0:
         if cfg.kl_type == KL_K3:
@@ -253,11 +272,34 @@ def row_loss_terms(logp: float, old: float, ref: Optional[float], A: float, cfg:
     return L, G, bool(clipped), kl
 
 
+def row_weights(loss_mask, row_traj, reduction: int, n_loss: int, traj_tokens=None, n_active=None):
+    """w_j of loss = sum_j w_j L_j (R17, R29):
+    token-mean: m_j / N; seq-mean-token-mean: m_j / (n_b * B_eff); seq-mean-token-sum: m_j / B_eff, with
+    n_b the loss tokens of row j's trajectory and B_eff the trajectories with n_b > 0 (global values may be
+    passed for sharded batches). Any zero denominator gives weight 0."""
+    loss_mask = np.asarray(loss_mask)
+    row_traj = np.asarray(row_traj)
+    if reduction == TOKEN_MEAN:
+        return np.where(loss_mask != 0, (1.0 / n_loss) if n_loss > 0 else 0.0, 0.0)
+    if traj_tokens is None:
+        traj_tokens = np.bincount(row_traj[loss_mask != 0], minlength=int(row_traj.max()) + 1)
+    if n_active is None:
+        n_active = int(np.count_nonzero(traj_tokens))
+    w = np.zeros(len(loss_mask))
+    for j in range(len(loss_mask)):
+        if loss_mask[j] and n_active > 0:
+            nb = traj_tokens[row_traj[j]]
+            w[j] = 1.0 / (nb * n_active) if reduction == SEQ_MEAN_TOKEN_MEAN else 1.0 / n_active
+    return w
+
+
 def policy_loss_fwd_bwd(logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss: int,
                         cfg: LossCfg = LossCfg(), zero_masked_rows: bool = True,
-                        rows: Optional[Sequence[int]] = None):
-    """loss = sum_j m_j L_j / N   (N = n_loss, the global loss-token count; 0 => loss 0, grads 0)
-    dlogits[j, v] = coef_j * (p_jv - [v == y_j]),  coef_j = -s * (m_j / N) * G_j.
+                        rows: Optional[Sequence[int]] = None, traj_tokens=None, n_active=None):
+    """loss = sum_j w_j L_j with L_j = pg + beta*KL - c_H*H_j and w_j from row_weights (token-mean: m_j/N;
+    N = n_loss, the global loss-token count; 0 => loss 0, grads 0)
+    dlogits[j, v] = coef_j * (p_jv - [v == y_j]) + w_j c_H s p_jv (ln p_jv + H_j),  coef_j = -s * w_j * G_j
+    (dH/dz_v = -p_v (ln p_v + H); z = s x).
 
     `rows` restricts the per-row outputs to a subset (sampled parity at full size); the loss and
     stats are then sums over that subset only. Rows with m_j == 0 get dlogits 0, logp 0, entropy 0.
@@ -266,7 +308,7 @@ def policy_loss_fwd_bwd(logits, targets, loss_mask, row_traj, adv, old_logp, ref
     N_rows = len(targets)
     rows = range(N_rows) if rows is None else rows
     s = cfg.logit_scale
-    invN = (1.0 / n_loss) if n_loss > 0 else 0.0
+    W = row_weights(loss_mask, row_traj, cfg.reduction, n_loss, traj_tokens, n_active)
     out_dl, out_logp, out_H, out_coef = {}, {}, {}, {}
     terms, klterms, Hterms = [], [], []
     n_clipped = 0
@@ -283,14 +325,20 @@ def policy_loss_fwd_bwd(logits, targets, loss_mask, row_traj, adv, old_logp, ref
         A = float(adv[int(row_traj[j])])
         ref = float(ref_logp[j]) if ref_logp is not None else None
         L, G, clipped, kl = row_loss_terms(logp, float(old_logp[j]), ref, A, cfg)
-        coef = -s * invN * G
+        L -= cfg.ent_coef * H
+        w = float(W[j])
+        coef = -s * w * G
         dl = coef * p
         dl[y] = coef * (p[y] - 1.0)
+        if cfg.ent_coef != 0.0:
+            with np.errstate(divide="ignore", invalid="ignore"):
+                lnp = np.where(p > 0, np.log(np.where(p > 0, p, 1.0)), 0.0)
+            dl = dl + w * cfg.ent_coef * s * p * (lnp + H)
         out_dl[j], out_logp[j], out_H[j], out_coef[j] = dl, logp, H, coef
-        terms.append(L); klterms.append(kl); Hterms.append(H)
+        terms.append(w * L); klterms.append(kl); Hterms.append(H)
         n_clipped += int(clipped)
         n_tok += 1
-    loss = math.fsum(terms) * invN if n_loss > 0 else 0.0
+    loss = math.fsum(terms)
     stats = dict(loss=loss, n_clipped=n_clipped, kl_sum=math.fsum(klterms),
                  entropy_sum=math.fsum(Hterms), n_tokens=n_tok)
     if logits_is_array and rows == range(N_rows):
@@ -304,15 +352,16 @@ def policy_loss_fwd_bwd(logits, targets, loss_mask, row_traj, adv, old_logp, ref
 def loss_only(logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss, cfg=LossCfg()):
     """The scalar loss alone (used by the finite-difference pin)."""
     s = cfg.logit_scale
+    W = row_weights(loss_mask, row_traj, cfg.reduction, n_loss)
     terms = []
     for j in range(len(targets)):
         if not loss_mask[j]:
             continue
-        logp, _, _, _ = row_forward(logits[j], int(targets[j]), s)
+        logp, H, _, _ = row_forward(logits[j], int(targets[j]), s)
         ref = float(ref_logp[j]) if ref_logp is not None else None
         L, _, _, _ = row_loss_terms(logp, float(old_logp[j]), ref, float(adv[int(row_traj[j])]), cfg)
-        terms.append(L)
-    return math.fsum(terms) / n_loss if n_loss > 0 else 0.0
+        terms.append(W[j] * (L - cfg.ent_coef * H))
+    return math.fsum(terms)
 
 
 # --------------------------------------------------------------------------------------------

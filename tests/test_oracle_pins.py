@@ -413,3 +413,110 @@ def test_vocab_shard_combine_equals_unsharded(P):
     assert empty == dead == (-math.inf, 0.0, 0.0, 0.0)
     got = O.combine_partials([empty, O.shard_partials(x, 3, 0), dead])
     assert abs(got[0] - O.row_forward(x, 3)[0]) < 1e-12
+
+
+# ----------------------------------------------------------------------------- A4 variants (NEXT-4)
+def test_dual_clip_closed_forms():
+    """Dual-clip PPO (c = 3): for A < 0 the loss is capped at -c*A with zero gradient."""
+    cfg = O.LossCfg(kl_beta=0.0, dual_clip=3.0)
+    L, G, _, _ = O.row_loss_terms(math.log(5.0), 0.0, None, -1.0, cfg)     # pg = 5 > 3: capped
+    assert abs(L - 3.0) < 1e-15 and G == 0.0
+    L, G, _, _ = O.row_loss_terms(math.log(2.0), 0.0, None, -1.0, cfg)     # pg = 2 < 3: unchanged
+    assert abs(L - 2.0) < 1e-15 and abs(G - 2.0) < 1e-15
+    L, G, _, _ = O.row_loss_terms(math.log(5.0), 0.0, None, 1.0, cfg)      # A > 0: no dual clip
+    assert abs(L + 1.2) < 1e-15 and G == 0.0
+
+
+def _onpolicy(rng, tok_per_traj, V=6):
+    rows = sum(tok_per_traj)
+    x = rng.normal(size=(rows, V))
+    y = rng.integers(0, V, rows)
+    rt = np.repeat(np.arange(len(tok_per_traj)), tok_per_traj).astype(np.int32)
+    lp = np.array([O.row_forward(x[j], int(y[j]))[0] for j in range(rows)])
+    return x, y, rt, lp
+
+
+def test_sequence_mean_reductions_closed_form():
+    """seq-mean-token-mean: (1/B) sum_b mean_{j in b} L_j; seq-mean-token-sum: (1/B) sum_b sum_j L_j.
+    On-policy, beta = 0: L_j = -A_b, so the losses are -(A0 + A1)/2 and -(A0*1 + A1*3)/2."""
+    rng = np.random.default_rng(4)
+    x, y, rt, lp = _onpolicy(rng, [1, 3])
+    mask = np.ones(4, np.uint8)
+    A = np.array([0.75, -0.25])
+    base = dict(kl_beta=0.0)
+    r1 = O.policy_loss_fwd_bwd(x, y, mask, rt, A, lp, None, 4, O.LossCfg(reduction=O.SEQ_MEAN_TOKEN_MEAN, **base))
+    assert abs(r1["loss"] + (0.75 - 0.25) / 2) < 1e-15
+    r2 = O.policy_loss_fwd_bwd(x, y, mask, rt, A, lp, None, 4, O.LossCfg(reduction=O.SEQ_MEAN_TOKEN_SUM, **base))
+    assert abs(r2["loss"] + (0.75 * 1 - 0.25 * 3) / 2) < 1e-15
+    r0 = O.policy_loss_fwd_bwd(x, y, mask, rt, A, lp, None, 4, O.LossCfg(**base))
+    assert abs(r0["loss"] + (0.75 - 3 * 0.25) / 4) < 1e-15
+    # equal lengths: seq-mean-token-mean == token-mean
+    x, y, rt, lp = _onpolicy(rng, [2, 2, 2])
+    m = np.ones(6, np.uint8)
+    a = O.policy_loss_fwd_bwd(x, y, m, rt, np.array([1.0, -2.0, 0.5]), lp, None, 6, O.LossCfg(**base))
+    b = O.policy_loss_fwd_bwd(x, y, m, rt, np.array([1.0, -2.0, 0.5]), lp, None, 6,
+                              O.LossCfg(reduction=O.SEQ_MEAN_TOKEN_MEAN, **base))
+    assert abs(a["loss"] - b["loss"]) < 1e-15 and np.allclose(a["dlogits"], b["dlogits"], atol=1e-16)
+
+
+def test_entropy_bonus_vs_torch_autograd():
+    """L = -c_H * H (A = 0 removes the PPO term): dlogits = w c_H s p (ln p + H), pinned to torch float64
+    autograd of -c_H * w * H(softmax(s x)); a uniform row has zero entropy gradient."""
+    rng = np.random.default_rng(8)
+    N, V, c, s = 5, 9, 0.3, 1 / 0.7
+    x = rng.normal(size=(N, V))
+    x[2] = 0.0
+    y = rng.integers(0, V, N)
+    lp = np.array([O.row_forward(x[j], int(y[j]), s)[0] for j in range(N)])
+    out = O.policy_loss_fwd_bwd(x, y, np.ones(N, np.uint8), np.zeros(N, np.int32), np.zeros(1), lp, None, N,
+                                O.LossCfg(kl_beta=0.0, ent_coef=c, logit_scale=s))
+    t = torch.from_numpy(x).requires_grad_(True)
+    logp = torch.log_softmax(s * t, dim=-1)
+    H = -(logp.exp() * logp).sum(dim=-1)
+    (-c * H.sum() / N).backward()
+    assert np.max(np.abs(out["dlogits"] - t.grad.numpy())) < 1e-15
+    assert np.max(np.abs(out["dlogits"][2])) < 1e-17
+    assert abs(out["loss"] + c * float(H.sum()) / N) < 1e-14
+
+
+def test_sft_flag_matches_cross_entropy():
+    """SPEC.md:503 SFT: L = -logp per token; token-mean equals torch cross_entropy (library pin)."""
+    rng = np.random.default_rng(12)
+    N, V = 7, 11
+    x = rng.normal(size=(N, V))
+    y = rng.integers(0, V, N)
+    junk = rng.normal(size=N)                               # A / old must not matter in SFT mode
+    out = O.policy_loss_fwd_bwd(x, y, np.ones(N, np.uint8), np.zeros(N, np.int32), np.array([-3.0]), junk, None,
+                                N, O.LossCfg(kl_beta=0.0, sft=True))
+    t = torch.from_numpy(x).requires_grad_(True)
+    ce = torch.nn.functional.cross_entropy(t, torch.from_numpy(y))
+    ce.backward()
+    assert abs(out["loss"] - float(ce.detach())) < 1e-14
+    assert np.max(np.abs(out["dlogits"] - t.grad.numpy())) < 1e-16 + 1e-14
+
+
+@pytest.mark.parametrize("variant", ["dual", "ent", "seqmean", "seqsum", "sft"])
+def test_variant_gradients_finite_differences(variant):
+    rng = np.random.default_rng({"dual": 1, "ent": 2, "seqmean": 3, "seqsum": 4, "sft": 5}[variant])
+    kw = dict(dual=dict(dual_clip=3.0), ent=dict(ent_coef=0.1), seqmean=dict(reduction=O.SEQ_MEAN_TOKEN_MEAN),
+              seqsum=dict(reduction=O.SEQ_MEAN_TOKEN_SUM), sft=dict(sft=True))[variant]
+    x, y, mask, rt, adv, old, ref, _ = _tiny_problem(rng, N=10, V=7)
+    if variant == "dual":   # push some negative-advantage rows past the cap, away from the kink
+        adv[:] = -np.abs(adv) - 0.2
+        lp = np.array([O.row_forward(x[j], int(y[j]))[0] for j in range(10)])
+        old = lp - np.where(np.arange(10) % 2 == 0, math.log(5.0), math.log(1.05))
+    cfg = O.LossCfg(**kw)
+    N = int(mask.sum())
+    out = O.policy_loss_fwd_bwd(x, y, mask, rt, adv, old, ref, N, cfg)
+    h = 1e-6
+    fd = np.zeros_like(x)
+    for j in range(x.shape[0]):
+        for v in range(x.shape[1]):
+            xp, xm = x.copy(), x.copy()
+            xp[j, v] += h
+            xm[j, v] -= h
+            fd[j, v] = (O.loss_only(xp, y, mask, rt, adv, old, ref, N, cfg)
+                        - O.loss_only(xm, y, mask, rt, adv, old, ref, N, cfg)) / (2 * h)
+    sc = np.max(np.abs(out["dlogits"]))
+    assert np.max(np.abs(out["dlogits"] - fd)) <= 1e-6 * sc + 1e-12
+    assert abs(out["loss"] - O.loss_only(x, y, mask, rt, adv, old, ref, N, cfg)) < 1e-14
