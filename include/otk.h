@@ -60,6 +60,10 @@ typedef enum {
 typedef enum { OTK_SRC_CONTEXT = 0, OTK_SRC_ACTION = 1, OTK_SRC_OBSERVATION = 2, OTK_SRC_PAD = 3 } otk_source;
 typedef enum { OTK_F32 = 0, OTK_BF16 = 1 } otk_dtype;
 typedef enum { OTK_KL_K1 = 1, OTK_KL_K2 = 2, OTK_KL_K3 = 3 } otk_kl_type;
+/* loss = sum_j w_j L_j with w_j = m_j / N (token mean), m_j / (n_b B) (mean over trajectories of the
+ * per-trajectory token mean) or m_j / B (mean over trajectories of the token sum); n_b = loss tokens of
+ * row j's trajectory, B = trajectories with n_b > 0 (global). DESIGN.md R17, R29. */
+typedef enum { OTK_TOKEN_MEAN = 0, OTK_SEQ_MEAN_TOKEN_MEAN = 1, OTK_SEQ_MEAN_TOKEN_SUM = 2 } otk_reduction;
 
 #define OTK_ANY_AGENT (-1)
 #define OTK_ADV_STD_NORM 0x1u /* divide by the group std (default on)        */
@@ -111,6 +115,7 @@ typedef struct {
 otk_status otk_build_masks(otk_ctx* ctx, const otk_traj_batch* batch /* host struct, device arrays */,
                            int16_t train_agent, uint8_t* loss_mask, uint8_t* response_mask, int32_t* row_traj,
                            int64_t* traj_loss_tokens, int64_t* traj_source_counts, int64_t* n_loss,
+                           int64_t* n_active_traj /* [1] or NULL: trajectories with >= 1 loss token */,
                            otk_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------------
@@ -151,8 +156,10 @@ otk_status otk_logprob_entropy_fwd(otk_ctx* ctx, int64_t num_rows, int64_t vocab
  *   delta = clamp(logp - old, -C, C), r = e^delta, rbar = clamp(r, 1 - clip_low, 1 + clip_high)
  *   pg = max(-A r, -A rbar); clipped <=> (A > 0 && r > 1 + clip_high) || (A < 0 && r < 1 - clip_low)
  *   KL: k3 = e^d - d - 1, d = clamp(ref - logp, -C, C); k1 = logp - ref; k2 = (logp - ref)^2 / 2
- *   L_j = pg + kl_beta * KL;   loss = sum_j m_j L_j / N   (token mean over the GLOBAL batch, R17)
- *   dlogits[j, v] = coef_j * (softmax_jv - [v == y_j]),  coef_j = -s * (m_j / N) * dL_j/dlogp_j
+ *   L_j = pg + kl_beta * KL - ent_coef * H_j;   loss = sum_j w_j L_j  (w_j = m_j / N: token mean over the
+ *   GLOBAL batch, R17; or a sequence-mean reduction, see otk_reduction)
+ *   dlogits[j, v] = coef_j * (softmax_jv - [v == y_j]) + w_j ent_coef s p_jv (ln p_jv + H_j),
+ *   coef_j = -s * w_j * dL_j/dlogp_j  (dual clip / SFT variants: see otk_loss_cfg)
  * with dL/dlogp = (clipped or |logp - old| > C ? 0 : -A r) + beta * (k3: |ref-logp| > C ? 0 : 1 - e^d;
  * k1: 1; k2: logp - ref). old/ref are detached constants; ref_logp may be NULL iff kl_beta == 0.
  * n_loss is a DEVICE pointer (never read on the host). Rows with m == 0: dlogits row = 0 if
@@ -172,6 +179,13 @@ typedef struct {
   int32_t zero_masked_rows; /* default 1                                   */
   int32_t accumulate_stats; /* default 0                                   */
   int32_t reserved;         /* must be 0                                   */
+  /* A4 variants (R27-R30) */
+  double ent_coef;          /* entropy bonus c_H: L -= c_H * H, dlogits += w c_H s p (ln p + H); default 0 */
+  double dual_clip;         /* c > 1: loss of A < 0 tokens capped at -c*A (zero gradient); 0 = off     */
+  int32_t reduction;        /* otk_reduction, default OTK_TOKEN_MEAN                                   */
+  int32_t sft;              /* 1: supervised L = -logp (A, old_logp and the clip unused)   */
+  const int64_t* traj_loss_tokens; /* device [B]: loss tokens per trajectory (seq-mean reductions)     */
+  const int64_t* n_active_traj;    /* device [1]: trajectories with >= 1 loss token, global (seq-mean) */
 } otk_loss_cfg;
 
 typedef struct {

@@ -49,7 +49,12 @@ class otk_traj_batch(C.Structure):
 class otk_loss_cfg(C.Structure):
     _fields_ = [("clip_low", C.c_double), ("clip_high", C.c_double), ("kl_beta", C.c_double),
                 ("log_ratio_clamp", C.c_double), ("logit_scale", C.c_double), ("kl_type", C.c_int32),
-                ("zero_masked_rows", C.c_int32), ("accumulate_stats", C.c_int32), ("reserved", C.c_int32)]
+                ("zero_masked_rows", C.c_int32), ("accumulate_stats", C.c_int32), ("reserved", C.c_int32),
+                ("ent_coef", C.c_double), ("dual_clip", C.c_double), ("reduction", C.c_int32), ("sft", C.c_int32),
+                ("traj_loss_tokens", C.c_void_p), ("n_active_traj", C.c_void_p)]
+
+
+OTK_TOKEN_MEAN, OTK_SEQ_MEAN_TOKEN_MEAN, OTK_SEQ_MEAN_TOKEN_SUM = 0, 1, 2
 
 
 class otk_vocab_shard(C.Structure):
@@ -68,7 +73,7 @@ _sig = {
     "otk_ctx_destroy": (C.c_int, [_P]),
     "otk_ctx_check": (C.c_int, [_P, _P]),
     "otk_ctx_launch_count": (_I64, [_P]),
-    "otk_build_masks": (C.c_int, [_P, C.POINTER(otk_traj_batch), C.c_int16, _P, _P, _P, _P, _P, _P, _P]),
+    "otk_build_masks": (C.c_int, [_P, C.POINTER(otk_traj_batch), C.c_int16, _P, _P, _P, _P, _P, _P, _P, _P]),
     "otk_group_advantages": (C.c_int, [_P, C.c_int32, _P, C.c_int32, _P, _P, _P, C.c_uint32, C.c_double,
                                        _P, _P, _P, _P, _P, _P]),
     "otk_logprob_entropy_fwd": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, C.c_float, _P, _P, _P, _P]),
@@ -133,11 +138,19 @@ class LossCfg:
     logit_scale: float = 1.0
     zero_masked_rows: bool = True
     accumulate_stats: bool = False
+    ent_coef: float = 0.0                  # entropy bonus (NEXT-4)
+    dual_clip: float = 0.0                 # dual-clip c > 1 (0 = off)
+    reduction: int = 0                     # OTK_TOKEN_MEAN | OTK_SEQ_MEAN_TOKEN_MEAN | OTK_SEQ_MEAN_TOKEN_SUM
+    sft: bool = False                      # supervised mode
+    traj_loss_tokens: Optional[torch.Tensor] = None   # device i64 [B] (sequence-mean reductions)
+    n_active_traj: Optional[torch.Tensor] = None      # device i64 [1] (sequence-mean reductions, global)
 
     def c(self, accumulate: Optional[bool] = None) -> otk_loss_cfg:
         acc = self.accumulate_stats if accumulate is None else accumulate
         return otk_loss_cfg(self.clip_low, self.clip_high, self.kl_beta, self.log_ratio_clamp, self.logit_scale,
-                            int(self.kl_type), int(bool(self.zero_masked_rows)), int(bool(acc)), 0)
+                            int(self.kl_type), int(bool(self.zero_masked_rows)), int(bool(acc)), 0,
+                            float(self.ent_coef), float(self.dual_clip), int(self.reduction), int(bool(self.sft)),
+                            _ptr(self.traj_loss_tokens), _ptr(self.n_active_traj))
 
 
 class Context:
@@ -224,10 +237,12 @@ def otk_build_masks(ctx: Context, batch: DeviceTrajBatch, train_agent: int = OTK
     if source_counts:
         o.setdefault("traj_source_counts", torch.empty((B, 4), dtype=torch.int64, device=dev))
     o.setdefault("n_loss", torch.empty(1, dtype=torch.int64, device=dev))
+    o.setdefault("n_active_traj", torch.empty(1, dtype=torch.int64, device=dev))
     cb = batch.c()
     _check(_lib.otk_build_masks(ctx.handle, C.byref(cb), train_agent, _ptr(o["loss_mask"]),
                                 _ptr(o.get("response_mask")), _ptr(o["row_traj"]), _ptr(o["traj_loss_tokens"]),
-                                _ptr(o.get("traj_source_counts")), _ptr(o["n_loss"]), _stream(stream)))
+                                _ptr(o.get("traj_source_counts")), _ptr(o["n_loss"]), _ptr(o["n_active_traj"]),
+                                _stream(stream)))
     return o
 
 

@@ -131,13 +131,19 @@ __global__ void __launch_bounds__(kMaskThreads) k_build_masks(const MaskParams p
   if (s_last) {
     // last CTA: n_loss = sum of traj_loss_tokens in index order (warp-parallel, exact integers)
     __threadfence();
-    int64_t acc = 0;
-    for (int i = tid; i < tb.num_traj; i += kMaskThreads) acc += ((volatile int64_t*)p.traj_loss_tokens)[i];
-    int64_t total;
-    const int64_t ex = block_excl_scan(acc, s_warp, &total);
-    (void)ex;
+    int64_t acc = 0, act = 0;
+    for (int i = tid; i < tb.num_traj; i += kMaskThreads) {
+      const int64_t t = ((volatile int64_t*)p.traj_loss_tokens)[i];
+      acc += t;
+      act += t > 0 ? 1 : 0;
+    }
+    int64_t total, nact;
+    (void)block_excl_scan(acc, s_warp, &total);
+    __syncthreads();
+    (void)block_excl_scan(act, s_warp, &nact);
     if (tid == 0) {
       *p.n_loss = total;
+      if (p.n_active) *p.n_active = nact;
       if (tb.tok_offsets[0] != 0 || tb.tok_offsets[tb.num_traj] != N) set_error(p.err, OTK_ERR_BAD_TRAJECTORY);
       *p.ticket = 0u;
     }

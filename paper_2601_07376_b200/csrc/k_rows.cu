@@ -28,9 +28,6 @@
 #include "otk_internal.h"
 #include "otk_ptx.cuh"
 
-#ifndef OTK_PREFETCH
-#define OTK_PREFETCH 1
-#endif
 
 namespace otk {
 using namespace ptx;
@@ -198,6 +195,14 @@ struct Vec<float> {
     pass1_pair<kInit>(x[2], x[3], s2x2, negm2, aS[1], aT[1], e[2], e[3]);
     return kKeepE ? pack(e) : make_uint4(0, 0, 0, 0);
   }
+  // entropy-bonus variant: g = e (A + B log2 e)
+  __device__ static __forceinline__ uint4 pass2_ent(const uint4 e, float A, float B) {
+    float x[4], g[4];
+    unpack(e, x);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) g[i] = x[i] * fmaf(B, fmaxf(lg2(x[i]), -1e30f), A);
+    return pack(g);
+  }
   __device__ static __forceinline__ uint4 pass2(const uint4 e, float kt) {
     const uint64_t kt2 = f2(kt, kt);
     float g[4];
@@ -286,6 +291,14 @@ struct Vec<__nv_bfloat16> {
     asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(t) : "r"(w), "r"(lo2));
     asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(hi2), "r"(t));
     return r;
+  }
+  // entropy-bonus variant: g = e (A + B log2 e) in fp32, rounded once to bf16
+  __device__ static __forceinline__ uint4 pass2_ent(const uint4 e, float A, float B) {
+    float x[8], g[8];
+    unpack(e, x);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) g[i] = x[i] * fmaf(B, fmaxf(lg2(x[i]), -1e30f), A);
+    return pack(g);
   }
   __device__ static __forceinline__ uint4 pass2(const uint4 e, float kt) {
     const uint32_t hi2 = pack_bf16x2(kt, kt);
@@ -408,14 +421,17 @@ __device__ __forceinline__ void inactive_row(const RowParams& p, int64_t row, in
 
 // ---- per-token loss (north_star (4); same definition as oracle_ref.row_loss_terms), fp32 ---------------
 struct LossOut {
-  float L, kl;
-  float coef;  // -s * (m/N) * dL/dlogp
-  float gy;    // coef * (p_y - 1): the target column's dlogit
+  float L, kl;  // L = pg + beta*KL - c_H*H (unweighted)
+  float w;      // row weight of the reduction (token mean: 1/N)
+  float coef;   // -s * w * dL/dlogp
+  float wcs;    // w * c_H * s: scale of the entropy-bonus gradient p (ln p + H)
+  float gy;     // the target column's dlogit: coef (p_y - 1) + wcs p_y (logp + H)
   bool clipped;
 };
 struct RowSide {
   double A;
   float old_lp, ref_lp;
+  int64_t nb;   // loss tokens of the row's trajectory (sequence-mean reductions)
 };
 // e^x via MUFU (relative error ~2^-22) and expm1 with a degree-5 Taylor branch near 0 (|x| < 1/4: relative
 // error < 2e-6, no cancellation) — the per-row loss terms only need fp32-level accuracy.
@@ -425,17 +441,37 @@ __device__ __forceinline__ float expm1_fast(float x) {
   return fabsf(x) < 0.25f ? t : exp_fast(x) - 1.f;
 }
 
-__device__ __forceinline__ LossOut loss_terms(const RowParams& p, float lp, const RowSide& sd, float invN) {
-  const float A = float(sd.A);
+// Row weight w_j (R17, R29): token mean 1/N, seq-mean-token-mean 1/(n_b B), seq-mean-token-sum 1/B.
+__device__ __forceinline__ float row_weight(const RowParams& p, float invN, int64_t nb, int64_t nact) {
+  if (p.reduction == OTK_TOKEN_MEAN) return invN;
+  if (nact <= 0) return 0.f;
+  if (p.reduction == OTK_SEQ_MEAN_TOKEN_SUM) return float(1.0 / double(nact));
+  return nb > 0 ? float(1.0 / (double(nb) * double(nact))) : 0.f;
+}
+
+__device__ __forceinline__ LossOut loss_terms(const RowParams& p, float lp, float H, const RowSide& sd, float w) {
   const float C = float(p.clamp);
-  const float draw = lp - sd.old_lp;
-  const float delta = fminf(fmaxf(draw, -C), C);
-  const float r = exp_fast(delta);
-  const float lo = float(1.0 - p.clip_low), hi = float(1.0 + p.clip_high);
-  const float rbar = fminf(fmaxf(r, lo), hi);
-  const float pg = fmaxf(-A * r, -A * rbar);
-  const bool clipped = (A > 0.f && r > hi) || (A < 0.f && r < lo);
-  float G = (clipped || fabsf(draw) > C) ? 0.f : -A * r;
+  bool clipped = false;
+  float pg, G;
+  if (p.sft) {  // supervised cross-entropy on the trainable tokens
+    pg = -lp;
+    G = -1.f;
+  } else {
+    const float A = float(sd.A);
+    const float draw = lp - sd.old_lp;
+    const float delta = fminf(fmaxf(draw, -C), C);
+    const float r = exp_fast(delta);
+    const float lo = float(1.0 - p.clip_low), hi = float(1.0 + p.clip_high);
+    const float rbar = fminf(fmaxf(r, lo), hi);
+    pg = fmaxf(-A * r, -A * rbar);
+    clipped = (A > 0.f && r > hi) || (A < 0.f && r < lo);
+    G = (clipped || fabsf(draw) > C) ? 0.f : -A * r;
+    const float dc = float(p.dual_clip);
+    if (dc > 0.f && A < 0.f && pg > -dc * A) {  // dual clip: cap at -c*A, zero gradient
+      pg = -dc * A;
+      G = 0.f;
+    }
+  }
   float kl = 0.f;
   const float beta = float(p.kl_beta);
   if (beta != 0.f) {
@@ -455,12 +491,16 @@ __device__ __forceinline__ LossOut loss_terms(const RowParams& p, float lp, cons
     }
     G = fmaf(beta, gk, G);
   }
+  const float ce = float(p.ent_coef);
   LossOut o;
-  o.L = fmaf(beta, kl, pg);
+  o.L = fmaf(-ce, H, fmaf(beta, kl, pg));
   o.kl = kl;
   o.clipped = clipped;
-  o.coef = -p.scale * invN * G;
+  o.w = w;
+  o.coef = -p.scale * w * G;
+  o.wcs = w * ce * p.scale;
   o.gy = o.coef * expm1_fast(lp);  // coef * (p_y - 1), no cancellation when p_y -> 1
+  if (ce != 0.f) o.gy = fmaf(o.wcs * exp_fast(lp), lp + H, o.gy);
   return o;
 }
 
@@ -481,16 +521,16 @@ __device__ __forceinline__ void stats_epilogue(const RowParams& p, double acc_L,
       const volatile double* q2 = p.cta_partials + size_t(b) * kStatSlots;
       for (int k = 0; k < 5; ++k) tot[k] += q2[k];
     }
-    const double invN = nl > 0 ? 1.0 / double(nl) : 0.0;
+    (void)nl;
     otk_loss_stats* o = p.stats;
     if (p.accumulate) {
-      o->loss += tot[0] * invN;
+      o->loss += tot[0];
       o->n_clipped += tot[1];
       o->kl_sum += tot[2];
       o->entropy_sum += tot[3];
       o->n_tokens += tot[4];
     } else {
-      o->loss = tot[0] * invN;
+      o->loss = tot[0];
       o->n_clipped = tot[1];
       o->kl_sum = tot[2];
       o->entropy_sum = tot[3];
@@ -636,13 +676,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
     double acc_L = 0.0, acc_clip = 0.0, acc_kl = 0.0, acc_H = 0.0, acc_n = 0.0;
     int64_t nl = 0;
     float invN = 0.f;
+    int64_t nact = 0;
     if (kBwd) {
       nl = *p.n_loss;
       invN = nl > 0 ? float(1.0 / double(nl)) : 0.f;
+      if (p.reduction != OTK_TOKEN_MEAN) nact = *p.n_active;
     }
     uint32_t slot = 0, phase = 0, q = 0;
 
-#if OTK_PREFETCH
     int64_t row = group;
     int32_t y_n = 0, rt_n = 0;
     uint8_t m_n = 1;
@@ -659,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
     for (; row < p.num_rows; row += ngroups) {
       const int32_t y = y_n;
       const uint8_t m = m_n;
-      RowSide sd{0.0, old_n, ref_n};
+      RowSide sd{0.0, old_n, ref_n, 0};
       const int32_t rt = rt_n;
       const int64_t nrow = row + ngroups;
       if (nrow < p.num_rows) {  // side data of the next row: in flight while this row is computed
@@ -671,33 +712,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
           if (p.ref_logp) ref_n = p.ref_logp[nrow];
         }
       }
-#else
-    int64_t row = group;
-    int32_t y_n = row < p.num_rows ? p.targets[row] : 0;
-    uint8_t m_n = (row < p.num_rows && p.mask) ? p.mask[row] : 1;
-    for (; row < p.num_rows; row += ngroups) {
-      const int32_t y = y_n;
-      const uint8_t m = m_n;
-      const int64_t nrow = row + ngroups;
-      if (nrow < p.num_rows) {
-        y_n = p.targets[nrow];
-        m_n = p.mask ? p.mask[nrow] : 1;
-      }
-      RowSide sd{0.0, 0.f, 0.f};
-      int32_t rt = 0;
-      if (kBwd && row_active(p, y, m)) {
-        rt = p.row_traj[row];
-        sd.old_lp = p.old_logp[row];
-        if (p.ref_logp) sd.ref_lp = p.ref_logp[row];
-      }
-#endif
       if (!row_active(p, y, m)) {
         inactive_row<T, MODE>(p, row, ct, crank, c0, segn, m != 0);
         continue;
       }
       const int64_t ylc64 = int64_t(y) - p.vocab_start - c0;  // target column local to this CTA's segment
       const int ylc = (ylc64 >= 0 && ylc64 < segn) ? int(ylc64) : -1;
-      if (kBwd) sd.A = p.adv[rt];  // consumed after pass 1
+      if (kBwd) {  // consumed after pass 1
+        sd.A = p.adv[rt];
+        if (p.reduction != OTK_TOKEN_MEAN) sd.nb = p.traj_tokens[rt];
+      }
       // the target logit, read straight from HBM (one sector per row; in flight during pass 1)
       const int64_t yg = int64_t(y) - p.vocab_start;
       const float xy = (yg >= 0 && yg < p.vocab)
@@ -792,9 +816,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
             if (p.lse) p.lse[row] = rs.lse;
           }
         } else {
-          const LossOut lo = loss_terms(p, rs.logp, sd, invN);
+          const LossOut lo = loss_terms(p, rs.logp, rs.H, sd, row_weight(p, invN, sd.nb, nact));
           if (ct == 0 && crank == 0) {
-            acc_L += double(lo.L);
+            acc_L += double(lo.w) * double(lo.L);
             acc_clip += lo.clipped ? 1.0 : 0.0;
             acc_kl += double(lo.kl);
             acc_H += double(rs.H);
@@ -806,9 +830,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
           // c+1 is in flight while chunk c is scaled and stored (two register sets, ping-pong, no copies)
           char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
           char* tp = drow + ct * 16;
+          const bool ent = lo.wcs != 0.f;  // entropy bonus: one extra MUFU (log2 e) per element
           auto chunk2 = [&](int c, const uint4& e0, const uint4& e1, uint32_t mw) {
-            const float kt = __fmul_rn(lo.coef, ex2(__fsub_rn(__uint_as_float(mw), rs.L2)));
-            const uint4 g0 = VT::pass2(e0, kt), g1 = VT::pass2(e1, kt);
+            const float dm = __fsub_rn(__uint_as_float(mw), rs.L2);   // m_c - lse (log2 units)
+            const float qc = ex2(dm);
+            uint4 g0, g1;
+            if (!ent) {
+              const float kt = __fmul_rn(lo.coef, qc);
+              g0 = VT::pass2(e0, kt);
+              g1 = VT::pass2(e1, kt);
+            } else {  // g = e q (coef + wcs (ln2 (log2 e + m_c - lse) + H))
+              const float Ac = qc * fmaf(lo.wcs, fmaf(kLn2, dm, rs.H), lo.coef);
+              const float Bc = qc * lo.wcs * kLn2;
+              g0 = VT::pass2_ent(e0, Ac, Bc);
+              g1 = VT::pass2_ent(e1, Ac, Bc);
+            }
             char* q0 = tp + size_t(c) * kChunkBytes;
             if (c < nch - 1 || (c + 1) * CE <= segn) {
               stg_cs_v4(q0, g0);
@@ -899,6 +935,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) 
     double acc_L = 0.0, acc_clip = 0.0, acc_kl = 0.0, acc_H = 0.0, acc_n = 0.0;
     const int64_t nl = *p.n_loss;
     const float invN = nl > 0 ? float(1.0 / double(nl)) : 0.f;
+    const int64_t nact = p.reduction != OTK_TOKEN_MEAN ? *p.n_active : 0;
     uint32_t slot = 0, phase = 0, q = 0;
     int64_t row = group;
     int32_t y_n = row < p.num_rows ? p.targets[row] : 0;
@@ -921,10 +958,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) 
       float dy;
       const Stat tot = combine_partials(p.partials_in + row, p.num_rows, p.nshards, dy);
       const RowStats rs = finalize(tot, dy);
-      RowSide sd{p.adv[p.row_traj[row]], p.old_logp[row], p.ref_logp ? p.ref_logp[row] : 0.f};
-      const LossOut lo = loss_terms(p, rs.logp, sd, invN);
+      const int32_t rt = p.row_traj[row];
+      RowSide sd{p.adv[rt], p.old_logp[row], p.ref_logp ? p.ref_logp[row] : 0.f,
+                 p.reduction != OTK_TOKEN_MEAN ? p.traj_tokens[rt] : 0};
+      const LossOut lo = loss_terms(p, rs.logp, rs.H, sd, row_weight(p, invN, sd.nb, nact));
       if (ct == 0 && crank == 0) {
-        acc_L += double(lo.L);
+        acc_L += double(lo.w) * double(lo.L);
         acc_clip += lo.clipped ? 1.0 : 0.0;
         acc_kl += double(lo.kl);
         acc_H += double(rs.H);
@@ -946,7 +985,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) 
           float x[EV], g[EV];
           VT::unpack(w, x);
 #pragma unroll
-          for (int i = 0; i < EV; ++i) g[i] = __fmul_rn(coef, ex2(__fmaf_rn(x[i], s2, -L2)));
+          for (int i = 0; i < EV; ++i) {
+            const float d = __fmaf_rn(x[i], s2, -L2);   // log2 p
+            const float pv = ex2(d);
+            // coef p + wcs p (ln p + H): the entropy-bonus term costs two FMAs, no extra exponential
+            g[i] = lo.wcs == 0.f ? __fmul_rn(coef, pv) : pv * fmaf(lo.wcs, fmaf(kLn2, fmaxf(d, -1e30f), rs.H), coef);
+          }
           if (unsigned(ylc - lc) < unsigned(EV)) {
 #pragma unroll
             for (int i = 0; i < EV; ++i)

@@ -76,6 +76,14 @@ otk_status check_cfg(const otk_loss_cfg* cfg, const float* ref_logp) {
   OTK_REQUIRE(cfg->kl_beta >= 0 && std::isfinite(cfg->kl_beta), OTK_ERR_INVALID_ARG, "kl_beta must be >= 0");
   OTK_REQUIRE(cfg->kl_type >= 1 && cfg->kl_type <= 3, OTK_ERR_INVALID_ARG, "kl_type must be 1, 2 or 3");
   OTK_REQUIRE(cfg->kl_beta == 0 || ref_logp, OTK_ERR_INVALID_ARG, "ref_logp is required when kl_beta != 0");
+  OTK_REQUIRE(std::isfinite(cfg->ent_coef), OTK_ERR_INVALID_ARG, "ent_coef must be finite");
+  OTK_REQUIRE(cfg->dual_clip == 0 || (cfg->dual_clip > 1 && std::isfinite(cfg->dual_clip)), OTK_ERR_INVALID_ARG,
+              "dual_clip must be 0 (off) or > 1");
+  OTK_REQUIRE(cfg->reduction >= OTK_TOKEN_MEAN && cfg->reduction <= OTK_SEQ_MEAN_TOKEN_SUM, OTK_ERR_INVALID_ARG,
+              "unknown reduction");
+  OTK_REQUIRE(cfg->reduction == OTK_TOKEN_MEAN || (cfg->traj_loss_tokens && cfg->n_active_traj), OTK_ERR_INVALID_ARG,
+              "sequence-mean reductions need traj_loss_tokens and n_active_traj");
+  OTK_REQUIRE(cfg->sft == 0 || cfg->sft == 1, OTK_ERR_INVALID_ARG, "sft must be 0 or 1");
   return OTK_OK;
 }
 
@@ -114,6 +122,12 @@ void set_loss(otk::RowParams& p, const int32_t* row_traj, const double* adv, con
   p.kl_beta = cfg->kl_beta;
   p.clamp = cfg->log_ratio_clamp;
   p.kl_type = cfg->kl_type;
+  p.ent_coef = cfg->ent_coef;
+  p.dual_clip = cfg->dual_clip;
+  p.reduction = cfg->reduction;
+  p.sft = cfg->sft;
+  p.traj_tokens = cfg->traj_loss_tokens;
+  p.n_active = cfg->n_active_traj;
   p.zero_masked = cfg->zero_masked_rows;
   p.accumulate = cfg->accumulate_stats;
   p.dlogits = dlogits;
@@ -211,7 +225,8 @@ int64_t otk_ctx_launch_count(const otk_ctx* ctx) { return ctx ? ctx->launches : 
 
 otk_status otk_build_masks(otk_ctx* ctx, const otk_traj_batch* batch, int16_t train_agent, uint8_t* loss_mask,
                            uint8_t* response_mask, int32_t* row_traj, int64_t* traj_loss_tokens,
-                           int64_t* traj_source_counts, int64_t* n_loss, otk_stream_t stream) {
+                           int64_t* traj_source_counts, int64_t* n_loss, int64_t* n_active_traj,
+                           otk_stream_t stream) {
   OTK_REQUIRE(ctx && batch, OTK_ERR_INVALID_ARG, "ctx / batch is NULL");
   OTK_REQUIRE(batch->num_traj >= 1, OTK_ERR_EMPTY_GROUP, "num_traj < 1 (EmptyGroup)");
   OTK_REQUIRE(batch->num_rows >= 0, OTK_ERR_SHAPE, "num_rows < 0");
@@ -229,6 +244,7 @@ otk_status otk_build_masks(otk_ctx* ctx, const otk_traj_batch* batch, int16_t tr
   p.traj_loss_tokens = traj_loss_tokens;
   p.traj_source_counts = traj_source_counts;
   p.n_loss = n_loss;
+  p.n_active = n_active_traj;
   p.ticket = ctx->d_tickets + otk::kTicketMasks;
   p.err = ctx->d_err;
   OTK_CUDA(otk::launch_masks(p, reinterpret_cast<cudaStream_t>(stream)), "k_build_masks launch");
@@ -396,6 +412,7 @@ otk_status otk_policy_loss_fwd_bwd_host(otk_ctx* ctx, int64_t num_rows, int64_t 
   OTK_REQUIRE(loss_mask_host && row_traj_host && adv_host && old_logp_host && stats_host && num_traj >= 1,
               OTK_ERR_INVALID_ARG, "a required host pointer is NULL");
   OTK_REQUIRE(rows_per_chunk >= 1, OTK_ERR_SHAPE, "rows_per_chunk >= 1 required");
+  OTK_REQUIRE(cfg->reduction == OTK_TOKEN_MEAN, OTK_ERR_INVALID_ARG, "host entry point: token-mean reduction only");
   const size_t es = dtype_size(dtype);
   const size_t row_bytes = size_t(ld) * es;
   const bool has_ref = cfg->kl_beta != 0;

@@ -76,6 +76,10 @@ struct RowParams {
   const float* ref_logp;
   const int64_t* n_loss;
   double clip_low, clip_high, kl_beta, clamp;
+  double ent_coef, dual_clip;
+  int reduction, sft;
+  const int64_t* traj_tokens;
+  const int64_t* n_active;
   int kl_type;
   int zero_masked;
   int accumulate;
@@ -102,6 +106,7 @@ struct MaskParams {
   int64_t* traj_loss_tokens;
   int64_t* traj_source_counts;
   int64_t* n_loss;
+  int64_t* n_active;
   unsigned int* ticket;
   int* err;
 };

@@ -80,7 +80,7 @@ class PolicyLossStep:
         if process_group is not None and vocab_shard is not None:
             raise ValueError("batch and vocab sharding are exclusive in this step (2-D sharding is future work)")
         self.vshard = vocab_shard
-        self.ctx, self.batch, self.cfg, self.vocab = ctx, batch, cfg, vocab
+        self.ctx, self.batch, self.cfg, self.vocab = ctx, batch, cfg, vocab   # (cfg may gain count pointers)
         self.group_id, self.num_groups = group_id, num_groups
         self.turn_offsets, self.turn_rewards = turn_offsets, turn_rewards
         self.train_agent, self.std_norm, self.unbiased = train_agent, std_norm, unbiased
@@ -90,7 +90,12 @@ class PolicyLossStep:
         self.masks = dict(loss_mask=torch.empty(N, dtype=torch.uint8, device=dev),
                           row_traj=torch.empty(N, dtype=torch.int32, device=dev),
                           traj_loss_tokens=torch.empty(B, dtype=torch.int64, device=dev),
-                          n_loss=torch.empty(1, dtype=torch.int64, device=dev))
+                          n_loss=torch.empty(1, dtype=torch.int64, device=dev),
+                          n_active_traj=torch.empty(1, dtype=torch.int64, device=dev))
+        if cfg.reduction != 0:   # sequence-mean reductions read the per-trajectory token counts (R29)
+            import dataclasses
+            self.cfg = dataclasses.replace(cfg, traj_loss_tokens=self.masks["traj_loss_tokens"],
+                                           n_active_traj=self.masks["n_active_traj"])
         G_loc = global_num_groups if (process_group is not None and global_num_groups) else num_groups
         self.adv_out = dict(adv=torch.empty(B, dtype=torch.float64, device=dev),
                             returns=torch.empty(B, dtype=torch.float64, device=dev),
@@ -127,6 +132,8 @@ class PolicyLossStep:
             return self.adv_out["adv"]
         from .dist import all_gather_group_returns, all_reduce_n_loss
         all_reduce_n_loss(self.masks["n_loss"], self.pg)
+        if self.cfg.reduction != 0:
+            all_reduce_n_loss(self.masks["n_active_traj"], self.pg)
         # local returns (group statistics of this call are discarded; ids are global), then the exchange
         otk_group_advantages(self.ctx, self.group_id, self.G_global, turn_offsets=self.turn_offsets,
                              turn_rewards=self.turn_rewards, out=self.adv_out)

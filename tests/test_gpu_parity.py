@@ -13,7 +13,8 @@ import torch
 
 from oracle import oracle_ref as O
 from synth import CONFIGS, make_batch
-from tests.gpu_common import LOGP_TOL, check_dlogits_rows, dcoef_rows, near_kink, oracle_cfg, row_problem
+from tests.gpu_common import (LOGP_TOL, check_dlogits_rows, coef_sensitivity, dcoef_rows, near_kink, oracle_cfg,
+                               row_problem)
 
 pytestmark = pytest.mark.gpu
 
@@ -400,3 +401,62 @@ def test_extreme_rows(otk, ctx, dtype):
     dc = dcoef_rows(h, w["logp"], ocfg, n, True)
     assert check_dlogits_rows(out["dlogits"], w["dlogits"], w["coef"], list(range(n)), dtype, V, dc) <= 1.0
     assert not bool(T.isnan(out["dlogits"].float()).any())
+
+
+# ------------------------------------------------------------------------------------------ A4 variants
+VARIANTS = {
+    "dual": dict(dual_clip=3.0),
+    "ent": dict(ent_coef=0.05),
+    "seqmean": dict(reduction=1),
+    "seqsum": dict(reduction=2),
+    "sft": dict(sft=True),
+    "all": dict(ent_coef=0.02, dual_clip=2.5, reduction=1),
+}
+
+
+@pytest.mark.parametrize("dtype,V,n", [("bf16", 151936, 96), ("f32", 1000, 128)])
+@pytest.mark.parametrize("variant", list(VARIANTS))
+def test_policy_loss_variants(otk, ctx, variant, dtype, V, n):
+    """NEXT-4 variants of (4) vs the oracle (tests/test_oracle_pins.py pins them)."""
+    kw = VARIANTS[variant]
+    d, h = row_problem(n, V, dtype=dtype, seed=hash_seed(variant, V), force_clip=4, B=7)
+    if kw.get("dual_clip"):   # negative advantages with ratios past the cap on half of the rows
+        h["adv"][:] = -np.abs(h["adv"]) - 0.2
+        d["adv"] = torch.from_numpy(h["adv"]).cuda()
+    N = int(h["mask"].sum())
+    tt = np.bincount(h["row_traj"][h["mask"] == 1], minlength=7).astype(np.int64)
+    na = int(np.count_nonzero(tt))
+    cfg = otk.LossCfg(**kw, traj_loss_tokens=torch.from_numpy(tt).cuda(),
+                      n_active_traj=torch.tensor([na], dtype=torch.int64, device="cuda"))
+    out = otk.otk_policy_loss_fwd_bwd(ctx, d["logits"], d["targets"], d["mask"], d["row_traj"], d["adv"], d["old"],
+                                      d["ref"], torch.tensor([N], dtype=torch.int64, device="cuda"), cfg, vocab=V)
+    ctx.check()
+    ocfg = O.LossCfg(**{k: v for k, v in kw.items()})
+    want = O.policy_loss_fwd_bwd(h["wide"], h["targets"], h["mask"], h["row_traj"], h["adv"], h["old"], h["ref"], N,
+                                 ocfg, traj_tokens=tt, n_active=na)
+    W = O.row_weights(h["mask"], h["row_traj"], ocfg.reduction, N, tt, na)
+    rows = [j for j in range(n) if h["mask"][j] and not near_kink(want["logp"][j], h["old"][j], h["ref"][j],
+                                                                   h["adv"][h["row_traj"][j]], ocfg)]
+    g = out["dlogits"].double().cpu().numpy()
+    rel = 2.0 ** -7 if dtype == "bf16" else 1e-5
+    worst = 0.0
+    for j in rows:
+        lp, H, _, p = O.row_forward(h["wide"][j], int(h["targets"][j]))
+        with np.errstate(divide="ignore"):
+            lnp = np.where(p > 0, np.log(np.where(p > 0, p, 1.0)), 0.0)
+        dcj = coef_sensitivity(lp, h["old"][j], h["ref"][j], h["adv"][h["row_traj"][j]], 1, ocfg) * W[j]
+        ent = W[j] * ocfg.ent_coef * p * (np.abs(lnp) + H)       # entropy-bonus term scale (bf16 e in log2 e)
+        tol = rel * np.abs(want["dlogits"][j]) + 1e-5 * (abs(want["coef"][j]) + dcj) + 2.0 ** -7 * ent + 1e-30
+        worst = max(worst, float(np.max(np.abs(g[j, :V] - want["dlogits"][j]) / tol)))
+    assert worst <= 1.0, worst
+    st = otk.stats_dict(out["stats"])
+    scale = max(abs(want["loss"]), float(np.sum(W * np.abs([O.row_loss_terms(want["logp"][j], h["old"][j],
+                                                                             h["ref"][j], h["adv"][h["row_traj"][j]],
+                                                                             ocfg)[0] - ocfg.ent_coef *
+                                                            want["entropy"][j] if h["mask"][j] else 0.0
+                                                            for j in range(n)]))))
+    assert abs(st["loss"] - want["loss"]) <= 1e-4 * scale, (st["loss"], want["loss"])
+
+
+def hash_seed(name, V):
+    return sum(ord(c) for c in name) * 7 + V % 1000
