@@ -830,12 +830,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
           // c+1 is in flight while chunk c is scaled and stored (two register sets, ping-pong, no copies)
           char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
           char* tp = drow + ct * 16;
-          const bool ent = lo.wcs != 0.f;  // entropy bonus: one extra MUFU (log2 e) per element
-          auto chunk2 = [&](int c, const uint4& e0, const uint4& e1, uint32_t mw) {
+          // one chunk of pass 2; kEnt selects the entropy-bonus form (one extra MUFU, log2 e, per element)
+          auto chunk2 = [&](int c, const uint4& e0, const uint4& e1, uint32_t mw, auto entf) {
+            constexpr bool kEnt = decltype(entf)::value;
             const float dm = __fsub_rn(__uint_as_float(mw), rs.L2);   // m_c - lse (log2 units)
             const float qc = ex2(dm);
             uint4 g0, g1;
-            if (!ent) {
+            if constexpr (!kEnt) {
               const float kt = __fmul_rn(lo.coef, qc);
               g0 = VT::pass2(e0, kt);
               g1 = VT::pass2(e1, kt);
@@ -864,20 +865,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
               }
             }
           };
-          uint4 a0, a1, b0, b1;
-          uint32_t am, bm;
-          tmem_ld8_1_issue(tm, tm + uint32_t(kColM), a0, a1, am);
-          tmem_wait_ld_dep(a0, a1, am);
-          for (int c = 0;;) {
-            if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), b0, b1, bm);
-            chunk2(c, a0, a1, am);
-            if (++c >= nch) break;
-            tmem_wait_ld_dep(b0, b1, bm);
-            if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), a0, a1, am);
-            chunk2(c, b0, b1, bm);
-            if (++c >= nch) break;
+          // TMEM load of chunk c+1 in flight while chunk c is scaled and stored (two register sets)
+          auto pass2 = [&](auto entf) {
+            uint4 a0, a1, b0, b1;
+            uint32_t am, bm;
+            tmem_ld8_1_issue(tm, tm + uint32_t(kColM), a0, a1, am);
             tmem_wait_ld_dep(a0, a1, am);
-          }
+            for (int c = 0;;) {
+              if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), b0, b1, bm);
+              chunk2(c, a0, a1, am, entf);
+              if (++c >= nch) break;
+              tmem_wait_ld_dep(b0, b1, bm);
+              if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), a0, a1, am);
+              chunk2(c, b0, b1, bm, entf);
+              if (++c >= nch) break;
+              tmem_wait_ld_dep(a0, a1, am);
+            }
+          };
+          if (lo.wcs == 0.f)
+            pass2(std::false_type{});
+          else
+            pass2(std::true_type{});
           // target column: coef * (p_y - 1), overwriting this thread's own vector store (program order)
           if (ct == owner_ct) VT::store1(drow, ylc, lo.gy);
         }
