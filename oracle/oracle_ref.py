@@ -13,6 +13,8 @@ paper names no RL algorithm, so steps O2-O4 follow the readings listed in DESIGN
   O3 row_forward           north_star (3): log-softmax + gather + entropy over the vocabulary.
   O4 row_loss_terms,       north_star (4): PPO-clipped surrogate + KL penalty, token-mean reduction,
      policy_loss_fwd_bwd   dlogits = coef * (softmax - onehot); gradient pattern SPEC.md:323.
+  O6 turn_returns,         turn-level credit (SURVEY.md §8(f) NEXT-2; PAPER.md:177, SPEC.md:95, :364;
+     turn_level_advantages DESIGN.md R31): discounted reward-to-go per trainable ACTION turn.
   O5 shard_partials,       vocab-sharded forward (north_star "all-reduced row max/sum-exp"): per-shard
      combine_partials      partials combined exactly (DESIGN.md §3 R25).
 
@@ -87,6 +89,7 @@ def build_masks(tok_offsets, seg_offsets, seg_source, seg_agent, seg_len, termin
     loss_mask = np.zeros(N, np.uint8)
     response_mask = np.zeros(N, np.uint8)
     row_traj = np.full(N, -1, np.int32)
+    row_seg = np.full(N, -1, np.int32)
     traj_loss_tokens = np.zeros(B, np.int64)
     traj_source_counts = np.zeros((B, 4), np.int64)
     for b in range(B):
@@ -109,13 +112,14 @@ def build_masks(tok_offsets, seg_offsets, seg_source, seg_agent, seg_len, termin
             loss_mask[row:row + L] = 1 if trainable else 0
             response_mask[row:row + L] = 1 if responding else 0
             row_traj[row:row + L] = b
+            row_seg[row:row + L] = k
             traj_source_counts[b, src] += L
             if trainable:
                 traj_loss_tokens[b] += L
             row += L
         if row != int(tok_offsets[b + 1]):
             raise BadTrajectory(f"trajectory {b}: segment lengths != row count")
-    return dict(loss_mask=loss_mask, response_mask=response_mask, row_traj=row_traj,
+    return dict(loss_mask=loss_mask, response_mask=response_mask, row_traj=row_traj, row_seg=row_seg,
                 traj_loss_tokens=traj_loss_tokens, traj_source_counts=traj_source_counts,
                 n_loss=int(traj_loss_tokens.sum()))
 
@@ -131,18 +135,20 @@ def episode_returns(turn_offsets, turn_rewards):
 
 
 def group_advantages(group_id, returns, num_groups: int, std_norm: bool = True, unbiased: bool = False,
-                     std_floor: float = 1e-8):
+                     std_floor: float = 1e-8, skip_ungrouped: bool = False):
     """A_b = (R_b - mean_g) / (std_g if std_g > std_floor else 1)   (R2-R4).
 
     mean_g and std_g over the trajectories of b's group g; std is the population std unless
     `unbiased` (then / (n_g - 1), and std_g = 0 when n_g <= 1). std_norm=False gives R_b - mean_g.
+    skip_ungrouped: elements with a negative group id belong to no group and get A = 0 (turn-level
+    credit, O6: the non-unit segments).
     """
     group_id = np.asarray(group_id)
     returns = np.asarray(returns, np.float64)
     B = returns.shape[0]
     if B < 1:
         raise EmptyGroup("no trajectories")
-    if np.any(group_id < 0) or np.any(group_id >= num_groups):
+    if (not skip_ungrouped and np.any(group_id < 0)) or np.any(group_id >= num_groups):
         raise GroupRange("group id out of range")
     mean = np.zeros(num_groups)
     std = np.zeros(num_groups)
@@ -160,12 +166,54 @@ def group_advantages(group_id, returns, num_groups: int, std_norm: bool = True, 
     adv = np.zeros(B)
     for b in range(B):
         g = int(group_id[b])
+        if g < 0:
+            continue
         centred = float(returns[b]) - mean[g]
         if std_norm:
             adv[b] = centred / (std[g] if std[g] > std_floor else 1.0)
         else:
             adv[b] = centred
     return dict(adv=adv, group_mean=mean, group_std=std, group_size=size)
+
+
+# --------------------------------------------------------------------------------------------
+# O6: turn-level credit assignment  (R31)
+# --------------------------------------------------------------------------------------------
+def turn_returns(seg_offsets, seg_source, seg_agent, turn_offsets, turn_rewards, group_id, gamma: float = 1.0,
+                 train_agent: int = ANY_AGENT, traj_agent=None):
+    """Per-segment reward-to-go of the trainable ACTION turns.
+
+    "rewards are associated with the corresponding action tokens": the k-th trainable
+    ACTION segment of trajectory b (source ACTION, emitted by the agent trained on b; k = 0, 1, ...
+    in segment order) is turn k, and its return is the discounted reward-to-go over b's per-turn
+    scores r_{b,0..R_b-1} (SPEC.md:95 stores scores per turn; SPEC.md:364 lists discounting as the
+    extension):   G_{b,k} = sum_{j=k}^{R_b-1} gamma^(j-k) r_{b,j}   (0 when k >= R_b).
+    Returns seg_return[S] (0 for other segments) and seg_group[S] = group_id[b] for a turn, -1
+    otherwise — the input of group_advantages(..., skip_ungrouped=True).
+    """
+    seg_offsets = np.asarray(seg_offsets)
+    B = len(seg_offsets) - 1
+    S = int(seg_offsets[B])
+    seg_return = np.zeros(S)
+    seg_group = np.full(S, -1, np.int32)
+    for b in range(B):
+        ta = int(traj_agent[b]) if traj_agent is not None else int(train_agent)
+        r = [float(x) for x in turn_rewards[int(turn_offsets[b]):int(turn_offsets[b + 1])]]
+        k = 0
+        for s in range(int(seg_offsets[b]), int(seg_offsets[b + 1])):
+            if int(seg_source[s]) == ACTION and (ta == ANY_AGENT or int(seg_agent[s]) == ta):
+                seg_return[s] = math.fsum(gamma ** (j - k) * r[j] for j in range(k, len(r)))
+                seg_group[s] = int(group_id[b])
+                k += 1
+    return seg_return, seg_group
+
+
+def turn_level_advantages(tb_masks_row_seg, seg_return, seg_group, num_groups: int, **kw):
+    """Row advantages of turn-level credit: A of the row's segment (group-normalised over the group's
+    turns by group_advantages), i.e. the turn's advantage broadcast over its ACTION tokens."""
+    adv_seg = group_advantages(seg_group, seg_return, num_groups, skip_ungrouped=True, **kw)["adv"]
+    row_seg = np.asarray(tb_masks_row_seg)
+    return adv_seg, np.where(row_seg >= 0, adv_seg[np.maximum(row_seg, 0)], 0.0)
 
 
 # --------------------------------------------------------------------------------------------
@@ -295,7 +343,7 @@ def row_weights(loss_mask, row_traj, reduction: int, n_loss: int, traj_tokens=No
 
 def policy_loss_fwd_bwd(logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss: int,
                         cfg: LossCfg = LossCfg(), zero_masked_rows: bool = True,
-                        rows: Optional[Sequence[int]] = None, traj_tokens=None, n_active=None):
+                        rows: Optional[Sequence[int]] = None, traj_tokens=None, n_active=None, adv_index=None):
     """loss = sum_j w_j L_j with L_j = pg + beta*KL - c_H*H_j and w_j from row_weights (token-mean: m_j/N;
     N = n_loss, the global loss-token count; 0 => loss 0, grads 0)
     dlogits[j, v] = coef_j * (p_jv - [v == y_j]) + w_j c_H s p_jv (ln p_jv + H_j),  coef_j = -s * w_j * G_j
@@ -303,6 +351,7 @@ def policy_loss_fwd_bwd(logits, targets, loss_mask, row_traj, adv, old_logp, ref
 
     `rows` restricts the per-row outputs to a subset (sampled parity at full size); the loss and
     stats are then sums over that subset only. Rows with m_j == 0 get dlogits 0, logp 0, entropy 0.
+    adv_index (turn-level credit, O6): A_j = adv[adv_index[j]] (the row's segment) instead of adv[row_traj[j]].
     """
     logits_is_array = not callable(logits)
     N_rows = len(targets)
@@ -322,7 +371,7 @@ def policy_loss_fwd_bwd(logits, targets, loss_mask, row_traj, adv, old_logp, ref
             continue
         y = int(targets[j])
         logp, H, lse, p = row_forward(x, y, s)
-        A = float(adv[int(row_traj[j])])
+        A = float(adv[int(row_traj[j]) if adv_index is None else int(adv_index[j])])
         ref = float(ref_logp[j]) if ref_logp is not None else None
         L, G, clipped, kl = row_loss_terms(logp, float(old_logp[j]), ref, A, cfg)
         L -= cfg.ent_coef * H

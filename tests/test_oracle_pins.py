@@ -199,6 +199,125 @@ def test_episode_returns_undiscounted():
     assert R.tolist() == [-0.5, 0.0, 0.5]
 
 
+# ----------------------------------------------------------------------------- O6 turn-level credit
+def _one_traj(sources, agents, rewards, gid=0):
+    from synth.trajectories import _pack
+    segs = [(s, a, 3) for s, a in zip(sources, agents)]
+    return _pack([segs], [rewards], [gid], 1)
+
+
+def test_turn_returns_worked_example():
+    """DESIGN.md R31 by hand: turns = trainable ACTION segments in order; G_k = sum_{j>=k} gamma^(j-k) r_j.
+    Rewards [1, 0, 2] over 2 action turns (the third score lies past the last action and flows back)."""
+    C, A_, Ob = O.CONTEXT, O.ACTION, O.OBSERVATION
+    tb = _one_traj([C, A_, Ob, A_, Ob], [-1, 0, -1, 0, -1], [1.0, 0.0, 2.0])
+    for gamma, want in ((0.5, [1.5, 1.0]), (1.0, [3.0, 2.0]), (0.0, [1.0, 0.0])):
+        G, grp = O.turn_returns(tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.turn_offsets, tb.turn_rewards,
+                                tb.group_id, gamma)
+        assert G.tolist() == [0.0, want[0], 0.0, want[1], 0.0]
+        assert grp.tolist() == [-1, 0, -1, 0, -1]
+    # a turn with no score left (k >= R_b) has return 0
+    tb = _one_traj([C, A_, A_, A_], [-1, 0, 0, 0], [4.0])
+    G, _ = O.turn_returns(tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.turn_offsets, tb.turn_rewards,
+                          tb.group_id, 0.9)
+    assert G.tolist() == [0.0, 4.0, 0.0, 0.0]
+
+
+def test_turn_returns_agent_views():
+    """a view's turns are only its own agent's ACTION segments."""
+    C, A_, Ob = O.CONTEXT, O.ACTION, O.OBSERVATION
+    tb = _one_traj([C, A_, Ob, A_, Ob, A_], [-1, 0, -1, 1, -1, 0], [1.0, 2.0])
+    for ta, want, units in ((0, [0.0, 2.0, 0.0, 0.0, 0.0, 2.0], (1, 5)), (1, [0.0, 0.0, 0.0, 2.0, 0.0, 0.0], (3,))):
+        G, grp = O.turn_returns(tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.turn_offsets, tb.turn_rewards,
+                                tb.group_id, 0.5, train_agent=ta)
+        assert G.tolist() == want                       # agent 0: [1 + 0.5*2, 2]; agent 1: [1 + 0.5*2]
+        assert np.flatnonzero(grp >= 0).tolist() == list(units)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_turn_returns_bellman_recursion(seed):
+    """The reward-to-go satisfies G_k = r_k + gamma G_{k+1} (G_K = sum of the scores past the last turn,
+    discounted) — a different formulation than the oracle's direct sum."""
+    rng = np.random.default_rng(seed)
+    C, A_, Ob = O.CONTEXT, O.ACTION, O.OBSERVATION
+    K = int(rng.integers(1, 7))
+    R = int(rng.integers(0, K + 3))
+    r = rng.normal(size=R)
+    srcs = [C] + [A_, Ob] * K
+    tb = _one_traj(srcs, [-1] + [0, -1] * K, list(r))
+    gamma = float(rng.uniform(0.5, 1.0))
+    G, _ = O.turn_returns(tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.turn_offsets, tb.turn_rewards,
+                          tb.group_id, gamma)
+    Gt = G[1::2]
+    nxt = 0.0
+    for j in range(R - 1, K - 1, -1):          # scores past the last turn
+        nxt = r[j] + gamma * nxt
+    for k in range(K - 1, -1, -1):
+        rk = r[k] if k < R else 0.0
+        nxt = rk + gamma * nxt
+        assert abs(Gt[k] - nxt) <= 1e-12 * max(1.0, abs(nxt))
+
+
+def test_turn_level_reduces_to_trajectory_level():
+    """One trainable ACTION turn per trajectory (single-turn math) and gamma = 1: turn-level credit IS
+    trajectory-level GRPO, row by row, bit for bit (same values in the same order)."""
+    from synth import make_batch
+    tb = make_batch("math")
+    m = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated)
+    G, grp = O.turn_returns(tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.turn_offsets, tb.turn_rewards,
+                            tb.group_id, 1.0)
+    adv_seg, adv_row = O.turn_level_advantages(m["row_seg"], G, grp, tb.num_groups)
+    traj = O.group_advantages(tb.group_id, O.episode_returns(tb.turn_offsets, tb.turn_rewards), tb.num_groups)["adv"]
+    tr = m["loss_mask"] == 1
+    assert np.array_equal(adv_row[tr], traj[m["row_traj"]][tr])
+
+
+def test_turn_level_group_worked_example_and_invariants():
+    """Two trajectories of one group: turns G = [1.5, 1.0] and [0.5]; mean 1, population std sqrt(1/6), so
+    A = [sqrt(1.5), 0, -sqrt(1.5)]. On the game workload every group's turn advantages have mean 0, std 1."""
+    from synth.trajectories import _pack
+    C, A_, Ob = O.CONTEXT, O.ACTION, O.OBSERVATION
+    tb = _pack([[(C, -1, 2), (A_, 0, 2), (Ob, -1, 1), (A_, 0, 2)], [(C, -1, 2), (A_, 0, 3)]],
+               [[1.0, 0.0, 2.0], [0.5]], [0, 0], 1)
+    G, grp = O.turn_returns(tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.turn_offsets, tb.turn_rewards,
+                            tb.group_id, 0.5)
+    m = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len)
+    adv_seg, adv_row = O.turn_level_advantages(m["row_seg"], G, grp, 1)
+    s = math.sqrt(1.5)
+    assert np.allclose(adv_seg, [0.0, s, 0.0, 0.0, 0.0, -s], atol=1e-15)
+    assert np.allclose(adv_row, [0, 0, s, s, 0, 0, 0, 0, 0, -s, -s, -s], atol=1e-15)
+    from synth import make_batch
+    tb = make_batch("game")
+    G, grp = O.turn_returns(tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.turn_offsets, tb.turn_rewards,
+                            tb.group_id, 0.95)
+    a = O.group_advantages(grp, G, tb.num_groups, skip_ungrouped=True)
+    for g in range(tb.num_groups):
+        x = a["adv"][grp == g]
+        if a["group_std"][g] > 1e-8:
+            assert abs(x.mean()) < 1e-12 and abs(x.std() - 1.0) < 1e-12
+    assert np.all(a["adv"][grp < 0] == 0.0)
+
+
+def test_loss_adv_index_plumbing():
+    """adv_index selects the advantage per row: a segment-level array equal to the broadcast trajectory
+    advantage gives the trajectory-level loss and gradient exactly."""
+    from synth.trajectories import random_small_batch
+    rng = np.random.default_rng(5)
+    tb = random_small_batch(rng, 6, max_segs=5, max_len=6)
+    m = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated)
+    adv = rng.normal(size=tb.num_traj)
+    seg_traj = np.repeat(np.arange(tb.num_traj), np.diff(tb.seg_offsets))
+    adv_seg = adv[seg_traj]
+    N = tb.num_rows
+    X = rng.normal(size=(N, 50))
+    y = rng.integers(0, 50, N)
+    old = rng.normal(size=N) - 4.0
+    a = O.policy_loss_fwd_bwd(X, y, m["loss_mask"], m["row_traj"], adv, old, None, m["n_loss"], O.LossCfg(kl_beta=0))
+    b = O.policy_loss_fwd_bwd(X, y, m["loss_mask"], m["row_traj"], adv_seg, old, None, m["n_loss"],
+                              O.LossCfg(kl_beta=0), adv_index=m["row_seg"])
+    assert a["loss"] == b["loss"] and all(np.array_equal(a["dlogits"][j], b["dlogits"][j]) for j in range(N))
+
+
 # ----------------------------------------------------------------------------- O3 forward
 @pytest.mark.parametrize("V", [151936, 1024])
 def test_uniform_row(V):
