@@ -7,6 +7,7 @@
  *
  *   (1) otk_build_masks          loss/response masks from FSM-labelled segments
  *   (2) otk_group_advantages     GRPO group-relative advantages
+ *   (2') otk_turn_returns        turn-level credit: reward-to-go per ACTION turn
  *   (3) otk_logprob_entropy_fwd  fused vocab-wide log-softmax + gather + entropy  north_star (3)
  *   (4) otk_policy_loss_fwd_bwd  PPO-clip + KL surrogate, token-mean, fused       north_star (4)
  *                                backward dlogits = coef * (softmax - onehot)
@@ -68,6 +69,7 @@ typedef enum { OTK_TOKEN_MEAN = 0, OTK_SEQ_MEAN_TOKEN_MEAN = 1, OTK_SEQ_MEAN_TOK
 #define OTK_ANY_AGENT (-1)
 #define OTK_ADV_STD_NORM 0x1u /* divide by the group std (default on)        */
 #define OTK_ADV_UNBIASED 0x2u /* std with n-1 instead of n (R2; default off)    */
+#define OTK_ADV_SKIP_UNGROUPED 0x4u /* group_id < 0: no group, A = 0, no error (turn-level credit) */
 
 /* ---------------------------------------------------------------------------------------------
  * Context. Owns: the device index, SM count, a sticky device error word, O(#SM) scratch for the
@@ -109,13 +111,16 @@ typedef struct {
  * = every non-PAD row outside the trajectory's leading CONTEXT segment (R13);
  * row_traj[N] i32 = b; traj_loss_tokens[B] i64; traj_source_counts[B*4] i64 (NULL ok; SPEC.md:408-416
  * mask_report, order CONTEXT, ACTION, OBSERVATION, PAD); n_loss[1] i64 = sum of loss_mask (this batch;
- * a batch-sharded caller all-reduces it to the global token count before step (4)).
+ * a batch-sharded caller all-reduces it to the global token count before step (4)); n_active_traj[1]
+ * (NULL ok) = trajectories with >= 1 loss token; row_seg[N] i32 (NULL ok) = global index of the row's
+ * segment (-1 for rows of an invalid trajectory).
  * Rows of an invalid trajectory get loss_mask 0 and the error word is set. Bit-exact.
  */
 otk_status otk_build_masks(otk_ctx* ctx, const otk_traj_batch* batch /* host struct, device arrays */,
                            int16_t train_agent, uint8_t* loss_mask, uint8_t* response_mask, int32_t* row_traj,
                            int64_t* traj_loss_tokens, int64_t* traj_source_counts, int64_t* n_loss,
                            int64_t* n_active_traj /* [1] or NULL: trajectories with >= 1 loss token */,
+                           int32_t* row_seg /* [N] or NULL: global segment index of each row (turn-level credit) */,
                            otk_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------------
@@ -136,6 +141,24 @@ otk_status otk_group_advantages(otk_ctx* ctx, int32_t num_traj, const int32_t* g
                                 const double* returns, const int32_t* turn_offsets, const double* turn_rewards,
                                 uint32_t flags, double std_floor, double* adv, double* returns_out,
                                 double* group_mean, double* group_std, int32_t* group_size, otk_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * (2') Turn-level credit (R31). PAPER.md:177 "rewards are associated
+ * with the corresponding action tokens"; SPEC.md:95 stores one score per turn, SPEC.md:364 lists
+ * discounting as the extension. Turn k of trajectory b is its k-th trainable ACTION segment (source
+ * ACTION, agent = traj_agent[b] or train_agent, as in (1)); its return is the discounted reward-to-go
+ *   G_{b,k} = sum_{j=k}^{R_b-1} gamma^(j-k) r_{b,j}     (r_{b,.} = turn_rewards[turn_offsets[b] ..]; 0 if k >= R_b)
+ * Outputs per segment s (device, [num_segments] = seg_offsets[B]): seg_return[s] f64 = G of the turn
+ * (0 otherwise), seg_group[s] i32 = group_id[b] for a turn, -1 otherwise. The advantages then come
+ * from otk_group_advantages(num_traj = num_segments, group_id = seg_group, returns = seg_return,
+ * flags | OTK_ADV_SKIP_UNGROUPED), and step (4) reads them per row with cfg->adv_index = row_seg.
+ * gamma in [0, 1]. A negative group_id or seg_offsets[B] != num_segments sets the error word.
+ * Tolerance vs oracle: 1e-12 relative (float64, Horner order).
+ * ------------------------------------------------------------------------------------------- */
+otk_status otk_turn_returns(otk_ctx* ctx, const otk_traj_batch* batch /* host struct, device arrays */,
+                            int32_t num_segments, int16_t train_agent, const int32_t* group_id,
+                            const int32_t* turn_offsets, const double* turn_rewards, double gamma,
+                            double* seg_return, int32_t* seg_group, otk_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------------
  * (3) Forward: per row j with row_mask[j] != 0 (row_mask NULL = all rows), z = logit_scale * x:
@@ -186,6 +209,8 @@ typedef struct {
   int32_t sft;              /* 1: supervised L = -logp (A, old_logp and the clip unused)   */
   const int64_t* traj_loss_tokens; /* device [B]: loss tokens per trajectory (seq-mean reductions)     */
   const int64_t* n_active_traj;    /* device [1]: trajectories with >= 1 loss token, global (seq-mean) */
+  const int32_t* adv_index;        /* device [num_rows] or NULL: A_j = adv[adv_index[j]] instead of
+                                      adv[row_traj[j]] (turn-level credit: row_seg + segment advantages) */
 } otk_loss_cfg;
 
 typedef struct {

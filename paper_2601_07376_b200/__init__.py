@@ -25,7 +25,7 @@ _lib = C.CDLL(LIB_PATH)
 OTK_F32, OTK_BF16 = 0, 1
 OTK_KL_K1, OTK_KL_K2, OTK_KL_K3 = 1, 2, 3
 OTK_ANY_AGENT = -1
-OTK_ADV_STD_NORM, OTK_ADV_UNBIASED = 0x1, 0x2
+OTK_ADV_STD_NORM, OTK_ADV_UNBIASED, OTK_ADV_SKIP_UNGROUPED = 0x1, 0x2, 0x4
 CONTEXT, ACTION, OBSERVATION, PAD = 0, 1, 2, 3
 
 STATUS = {0: "OTK_OK", 1: "OTK_ERR_INVALID_ARG", 2: "OTK_ERR_SHAPE", 3: "OTK_ERR_ALIGNMENT", 4: "OTK_ERR_DTYPE",
@@ -51,7 +51,7 @@ class otk_loss_cfg(C.Structure):
                 ("log_ratio_clamp", C.c_double), ("logit_scale", C.c_double), ("kl_type", C.c_int32),
                 ("zero_masked_rows", C.c_int32), ("accumulate_stats", C.c_int32), ("reserved", C.c_int32),
                 ("ent_coef", C.c_double), ("dual_clip", C.c_double), ("reduction", C.c_int32), ("sft", C.c_int32),
-                ("traj_loss_tokens", C.c_void_p), ("n_active_traj", C.c_void_p)]
+                ("traj_loss_tokens", C.c_void_p), ("n_active_traj", C.c_void_p), ("adv_index", C.c_void_p)]
 
 
 OTK_TOKEN_MEAN, OTK_SEQ_MEAN_TOKEN_MEAN, OTK_SEQ_MEAN_TOKEN_SUM = 0, 1, 2
@@ -73,9 +73,11 @@ _sig = {
     "otk_ctx_destroy": (C.c_int, [_P]),
     "otk_ctx_check": (C.c_int, [_P, _P]),
     "otk_ctx_launch_count": (_I64, [_P]),
-    "otk_build_masks": (C.c_int, [_P, C.POINTER(otk_traj_batch), C.c_int16, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "otk_build_masks": (C.c_int, [_P, C.POINTER(otk_traj_batch), C.c_int16, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "otk_group_advantages": (C.c_int, [_P, C.c_int32, _P, C.c_int32, _P, _P, _P, C.c_uint32, C.c_double,
                                        _P, _P, _P, _P, _P, _P]),
+    "otk_turn_returns": (C.c_int, [_P, C.POINTER(otk_traj_batch), C.c_int32, C.c_int16, _P, _P, _P, C.c_double,
+                                   _P, _P, _P]),
     "otk_logprob_entropy_fwd": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, C.c_float, _P, _P, _P, _P]),
     "otk_policy_loss_fwd_bwd": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, _P, _P, _P, _P, _P,
                                           C.POINTER(otk_loss_cfg), _P, _P, _P, _P, _P]),
@@ -144,13 +146,14 @@ class LossCfg:
     sft: bool = False                      # supervised mode
     traj_loss_tokens: Optional[torch.Tensor] = None   # device i64 [B] (sequence-mean reductions)
     n_active_traj: Optional[torch.Tensor] = None      # device i64 [1] (sequence-mean reductions, global)
+    adv_index: Optional[torch.Tensor] = None          # device i32 [num_rows]: A_j = adv[adv_index[j]] (turn level)
 
     def c(self, accumulate: Optional[bool] = None) -> otk_loss_cfg:
         acc = self.accumulate_stats if accumulate is None else accumulate
         return otk_loss_cfg(self.clip_low, self.clip_high, self.kl_beta, self.log_ratio_clamp, self.logit_scale,
                             int(self.kl_type), int(bool(self.zero_masked_rows)), int(bool(acc)), 0,
                             float(self.ent_coef), float(self.dual_clip), int(self.reduction), int(bool(self.sft)),
-                            _ptr(self.traj_loss_tokens), _ptr(self.n_active_traj))
+                            _ptr(self.traj_loss_tokens), _ptr(self.n_active_traj), _ptr(self.adv_index))
 
 
 class Context:
@@ -224,8 +227,8 @@ def traj_batch_to_device(tb, device="cuda", non_blocking=False) -> DeviceTrajBat
 # (1) masks
 # ------------------------------------------------------------------------------------------------
 def otk_build_masks(ctx: Context, batch: DeviceTrajBatch, train_agent: int = OTK_ANY_AGENT, *,
-                    response_mask: bool = True, source_counts: bool = True, out: Optional[dict] = None,
-                    stream=None) -> dict:
+                    response_mask: bool = True, source_counts: bool = True, row_seg: bool = False,
+                    out: Optional[dict] = None, stream=None) -> dict:
     dev = batch.tok_offsets.device
     N, B = batch.num_rows, batch.num_traj
     o = out if out is not None else {}
@@ -238,11 +241,13 @@ def otk_build_masks(ctx: Context, batch: DeviceTrajBatch, train_agent: int = OTK
         o.setdefault("traj_source_counts", torch.empty((B, 4), dtype=torch.int64, device=dev))
     o.setdefault("n_loss", torch.empty(1, dtype=torch.int64, device=dev))
     o.setdefault("n_active_traj", torch.empty(1, dtype=torch.int64, device=dev))
+    if row_seg:
+        o.setdefault("row_seg", torch.empty(N, dtype=torch.int32, device=dev))
     cb = batch.c()
     _check(_lib.otk_build_masks(ctx.handle, C.byref(cb), train_agent, _ptr(o["loss_mask"]),
                                 _ptr(o.get("response_mask")), _ptr(o["row_traj"]), _ptr(o["traj_loss_tokens"]),
                                 _ptr(o.get("traj_source_counts")), _ptr(o["n_loss"]), _ptr(o["n_active_traj"]),
-                                _stream(stream)))
+                                _ptr(o.get("row_seg")), _stream(stream)))
     return o
 
 
@@ -252,8 +257,8 @@ def otk_build_masks(ctx: Context, batch: DeviceTrajBatch, train_agent: int = OTK
 def otk_group_advantages(ctx: Context, group_id: torch.Tensor, num_groups: int, *,
                          returns: Optional[torch.Tensor] = None, turn_offsets: Optional[torch.Tensor] = None,
                          turn_rewards: Optional[torch.Tensor] = None, std_norm: bool = True,
-                         unbiased: bool = False, std_floor: float = 1e-8, out: Optional[dict] = None,
-                         stream=None) -> dict:
+                         unbiased: bool = False, std_floor: float = 1e-8, skip_ungrouped: bool = False,
+                         out: Optional[dict] = None, stream=None) -> dict:
     _dev(group_id, "group_id")
     B = int(group_id.numel())
     dev = group_id.device
@@ -263,11 +268,27 @@ def otk_group_advantages(ctx: Context, group_id: torch.Tensor, num_groups: int, 
     o.setdefault("group_mean", torch.empty(num_groups, dtype=torch.float64, device=dev))
     o.setdefault("group_std", torch.empty(num_groups, dtype=torch.float64, device=dev))
     o.setdefault("group_size", torch.empty(num_groups, dtype=torch.int32, device=dev))
-    flags = (OTK_ADV_STD_NORM if std_norm else 0) | (OTK_ADV_UNBIASED if unbiased else 0)
+    flags = ((OTK_ADV_STD_NORM if std_norm else 0) | (OTK_ADV_UNBIASED if unbiased else 0)
+             | (OTK_ADV_SKIP_UNGROUPED if skip_ungrouped else 0))
     _check(_lib.otk_group_advantages(ctx.handle, B, _ptr(group_id), int(num_groups), _ptr(returns),
                                      _ptr(turn_offsets), _ptr(turn_rewards), flags, float(std_floor),
                                      _ptr(o["adv"]), _ptr(o["returns"]), _ptr(o["group_mean"]),
                                      _ptr(o["group_std"]), _ptr(o["group_size"]), _stream(stream)))
+    return o
+
+
+def otk_turn_returns(ctx: Context, batch: DeviceTrajBatch, num_segments: int, group_id: torch.Tensor,
+                     turn_offsets: torch.Tensor, turn_rewards: torch.Tensor, gamma: float = 1.0,
+                     train_agent: int = OTK_ANY_AGENT, *, out: Optional[dict] = None, stream=None) -> dict:
+    """(2') turn-level credit: per-segment reward-to-go of the trainable ACTION turns (otk.h otk_turn_returns)."""
+    dev = batch.seg_offsets.device
+    o = out if out is not None else {}
+    o.setdefault("seg_return", torch.empty(num_segments, dtype=torch.float64, device=dev))
+    o.setdefault("seg_group", torch.empty(num_segments, dtype=torch.int32, device=dev))
+    cb = batch.c()
+    _check(_lib.otk_turn_returns(ctx.handle, C.byref(cb), int(num_segments), int(train_agent), _ptr(group_id),
+                                 _ptr(turn_offsets), _ptr(turn_rewards), float(gamma), _ptr(o["seg_return"]),
+                                 _ptr(o["seg_group"]), _stream(stream)))
     return o
 
 

@@ -57,6 +57,10 @@ __global__ void __launch_bounds__(kAdvThreads) k_group_advantages(const AdvParam
   // 3) advantages
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
     const int g = p.group_id[b];
+    if (g < 0 && (p.flags & OTK_ADV_SKIP_UNGROUPED)) {  // turn-level credit: not a turn
+      p.adv[b] = 0.0;
+      continue;
+    }
     if (g < 0 || g >= G) {
       set_error(p.err, OTK_ERR_GROUP_RANGE);
       p.adv[b] = 0.0;

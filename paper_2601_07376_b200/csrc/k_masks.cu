@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(kMaskThreads) k_build_masks(const MaskParams p
           p.loss_mask[row] = f & 1u;
           if (p.response_mask) p.response_mask[row] = (f >> 1) & 1u;
           p.row_traj[row] = b;
+          if (p.row_seg) p.row_seg[row] = base + lo;
         }
       }
       running += total;
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(kMaskThreads) k_build_masks(const MaskParams p
         p.loss_mask[row] = 0;
         if (p.response_mask) p.response_mask[row] = 0;
         p.row_traj[row] = b;
+        if (p.row_seg) p.row_seg[row] = -1;
       }
     }
   }

@@ -719,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       const int64_t ylc64 = int64_t(y) - p.vocab_start - c0;  // target column local to this CTA's segment
       const int ylc = (ylc64 >= 0 && ylc64 < segn) ? int(ylc64) : -1;
       if (kBwd) {  // consumed after pass 1
-        sd.A = p.adv[rt];
+        sd.A = p.adv[p.adv_index ? p.adv_index[row] : rt];
         if (p.reduction != OTK_TOKEN_MEAN) sd.nb = p.traj_tokens[rt];
       }
       // the target logit, read straight from HBM (one sector per row; in flight during pass 1)
@@ -967,7 +967,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) 
       const Stat tot = combine_partials(p.partials_in + row, p.num_rows, p.nshards, dy);
       const RowStats rs = finalize(tot, dy);
       const int32_t rt = p.row_traj[row];
-      RowSide sd{p.adv[rt], p.old_logp[row], p.ref_logp ? p.ref_logp[row] : 0.f,
+      RowSide sd{p.adv[p.adv_index ? p.adv_index[row] : rt], p.old_logp[row], p.ref_logp ? p.ref_logp[row] : 0.f,
                  p.reduction != OTK_TOKEN_MEAN ? p.traj_tokens[rt] : 0};
       const LossOut lo = loss_terms(p, rs.logp, rs.H, sd, row_weight(p, invN, sd.nb, nact));
       if (ct == 0 && crank == 0) {

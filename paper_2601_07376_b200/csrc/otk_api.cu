@@ -128,6 +128,7 @@ void set_loss(otk::RowParams& p, const int32_t* row_traj, const double* adv, con
   p.sft = cfg->sft;
   p.traj_tokens = cfg->traj_loss_tokens;
   p.n_active = cfg->n_active_traj;
+  p.adv_index = cfg->adv_index;
   p.zero_masked = cfg->zero_masked_rows;
   p.accumulate = cfg->accumulate_stats;
   p.dlogits = dlogits;
@@ -226,7 +227,7 @@ int64_t otk_ctx_launch_count(const otk_ctx* ctx) { return ctx ? ctx->launches : 
 otk_status otk_build_masks(otk_ctx* ctx, const otk_traj_batch* batch, int16_t train_agent, uint8_t* loss_mask,
                            uint8_t* response_mask, int32_t* row_traj, int64_t* traj_loss_tokens,
                            int64_t* traj_source_counts, int64_t* n_loss, int64_t* n_active_traj,
-                           otk_stream_t stream) {
+                           int32_t* row_seg, otk_stream_t stream) {
   OTK_REQUIRE(ctx && batch, OTK_ERR_INVALID_ARG, "ctx / batch is NULL");
   OTK_REQUIRE(batch->num_traj >= 1, OTK_ERR_EMPTY_GROUP, "num_traj < 1 (EmptyGroup)");
   OTK_REQUIRE(batch->num_rows >= 0, OTK_ERR_SHAPE, "num_rows < 0");
@@ -245,6 +246,7 @@ otk_status otk_build_masks(otk_ctx* ctx, const otk_traj_batch* batch, int16_t tr
   p.traj_source_counts = traj_source_counts;
   p.n_loss = n_loss;
   p.n_active = n_active_traj;
+  p.row_seg = row_seg;
   p.ticket = ctx->d_tickets + otk::kTicketMasks;
   p.err = ctx->d_err;
   OTK_CUDA(otk::launch_masks(p, reinterpret_cast<cudaStream_t>(stream)), "k_build_masks launch");
@@ -263,7 +265,8 @@ otk_status otk_group_advantages(otk_ctx* ctx, int32_t num_traj, const int32_t* g
   OTK_REQUIRE((returns != nullptr) != (turn_offsets != nullptr), OTK_ERR_INVALID_ARG,
               "exactly one of returns and turn_offsets must be given");
   OTK_REQUIRE(!turn_offsets || turn_rewards, OTK_ERR_INVALID_ARG, "turn_rewards is NULL");
-  OTK_REQUIRE((flags & ~(OTK_ADV_STD_NORM | OTK_ADV_UNBIASED)) == 0, OTK_ERR_INVALID_ARG, "unknown flag bits");
+  OTK_REQUIRE((flags & ~(OTK_ADV_STD_NORM | OTK_ADV_UNBIASED | OTK_ADV_SKIP_UNGROUPED)) == 0, OTK_ERR_INVALID_ARG,
+              "unknown flag bits");
   OTK_REQUIRE(std_floor >= 0 && std::isfinite(std_floor), OTK_ERR_INVALID_ARG, "std_floor must be >= 0");
   OTK_REQUIRE(returns_out || num_traj <= ctx->cap_returns, OTK_ERR_SHAPE, "num_traj exceeds ctx scratch");
   otk::AdvParams p;
@@ -282,6 +285,35 @@ otk_status otk_group_advantages(otk_ctx* ctx, int32_t num_traj, const int32_t* g
   p.group_size = group_size;
   p.err = ctx->d_err;
   OTK_CUDA(otk::launch_advantages(p, reinterpret_cast<cudaStream_t>(stream)), "k_group_advantages launch");
+  ctx->launches += 1;
+  return OTK_OK;
+}
+
+otk_status otk_turn_returns(otk_ctx* ctx, const otk_traj_batch* batch, int32_t num_segments, int16_t train_agent,
+                            const int32_t* group_id, const int32_t* turn_offsets, const double* turn_rewards,
+                            double gamma, double* seg_return, int32_t* seg_group, otk_stream_t stream) {
+  OTK_REQUIRE(ctx && batch, OTK_ERR_INVALID_ARG, "ctx / batch is NULL");
+  OTK_REQUIRE(batch->num_traj >= 1, OTK_ERR_EMPTY_GROUP, "num_traj < 1 (EmptyGroup)");
+  OTK_REQUIRE(num_segments >= 0, OTK_ERR_SHAPE, "num_segments < 0");
+  OTK_REQUIRE(batch->seg_offsets && batch->seg_source && batch->seg_agent, OTK_ERR_INVALID_ARG,
+              "segment arrays must not be NULL");
+  OTK_REQUIRE(group_id && turn_offsets && turn_rewards, OTK_ERR_INVALID_ARG, "group_id / turn arrays are NULL");
+  OTK_REQUIRE(num_segments == 0 || (seg_return && seg_group), OTK_ERR_INVALID_ARG, "seg_return / seg_group is NULL");
+  OTK_REQUIRE(gamma >= 0.0 && gamma <= 1.0, OTK_ERR_INVALID_ARG, "gamma must be in [0, 1]");
+  OTK_REQUIRE(train_agent >= -1, OTK_ERR_INVALID_ARG, "train_agent must be >= -1");
+  if (num_segments == 0) return OTK_OK;
+  otk::TurnParams p;
+  p.b = *batch;
+  p.num_segments = num_segments;
+  p.train_agent = train_agent;
+  p.group_id = group_id;
+  p.turn_offsets = turn_offsets;
+  p.turn_rewards = turn_rewards;
+  p.gamma = gamma;
+  p.seg_return = seg_return;
+  p.seg_group = seg_group;
+  p.err = ctx->d_err;
+  OTK_CUDA(otk::launch_turn_returns(p, reinterpret_cast<cudaStream_t>(stream)), "k_turn_returns launch");
   ctx->launches += 1;
   return OTK_OK;
 }
@@ -413,6 +445,7 @@ otk_status otk_policy_loss_fwd_bwd_host(otk_ctx* ctx, int64_t num_rows, int64_t 
               OTK_ERR_INVALID_ARG, "a required host pointer is NULL");
   OTK_REQUIRE(rows_per_chunk >= 1, OTK_ERR_SHAPE, "rows_per_chunk >= 1 required");
   OTK_REQUIRE(cfg->reduction == OTK_TOKEN_MEAN, OTK_ERR_INVALID_ARG, "host entry point: token-mean reduction only");
+  OTK_REQUIRE(!cfg->adv_index, OTK_ERR_INVALID_ARG, "host entry point: adv_index not supported");
   const size_t es = dtype_size(dtype);
   const size_t row_bytes = size_t(ld) * es;
   const bool has_ref = cfg->kl_beta != 0;

@@ -80,6 +80,7 @@ struct RowParams {
   int reduction, sft;
   const int64_t* traj_tokens;
   const int64_t* n_active;
+  const int32_t* adv_index;  // NULL: adv[row_traj[row]]
   int kl_type;
   int zero_masked;
   int accumulate;
@@ -107,6 +108,7 @@ struct MaskParams {
   int64_t* traj_source_counts;
   int64_t* n_loss;
   int64_t* n_active;
+  int32_t* row_seg;
   unsigned int* ticket;
   int* err;
 };
@@ -129,6 +131,20 @@ struct AdvParams {
   int* err;
 };
 cudaError_t launch_advantages(const AdvParams& p, cudaStream_t s);
+
+struct TurnParams {
+  otk_traj_batch b;
+  int32_t num_segments;
+  int16_t train_agent;
+  const int32_t* group_id;
+  const int32_t* turn_offsets;
+  const double* turn_rewards;
+  double gamma;
+  double* seg_return;
+  int32_t* seg_group;
+  int* err;
+};
+cudaError_t launch_turn_returns(const TurnParams& p, cudaStream_t s);
 
 __device__ __forceinline__ void set_error(int* err, int code) { atomicCAS(err, 0, code); }
 

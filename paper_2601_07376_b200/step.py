@@ -9,6 +9,10 @@ DESIGN.md §7), the exchanges between them:
   otk_policy_loss_fwd_bwd x M micro-batches (stats accumulated on the device)
                              -> all_reduce(stats, SUM)             global loss on every rank
 
+Turn-level credit (credit="turn", NEXT-2): otk_build_masks also writes row_seg; otk_turn_returns gives
+the reward-to-go of every trainable ACTION turn (per segment), all_gather(seg_group, seg_return) when
+batch-sharded, otk_group_advantages(skip_ungrouped) over the segments; the loss reads A by row_seg.
+
 Vocab sharding (VocabShard): every rank holds all rows and a column range; per micro-batch
   otk_row_partials -> all_gather(16 B / row) -> otk_policy_loss_fwd_bwd_partials (identical stats on all ranks).
 
@@ -18,6 +22,7 @@ pointers and calls collectives.
 """
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass
 from typing import Callable, List, Optional, Sequence, Tuple
 
@@ -25,7 +30,7 @@ import torch
 
 from . import (Context, DeviceTrajBatch, LossCfg, STATS_FIELDS, otk_build_masks, otk_group_advantages,
                otk_logprob_entropy_combine, otk_policy_loss_fwd_bwd, otk_policy_loss_fwd_bwd_partials,
-               otk_row_partials)
+               otk_row_partials, otk_turn_returns)
 
 
 @dataclass
@@ -74,9 +79,15 @@ class PolicyLossStep:
                  turn_offsets: torch.Tensor, turn_rewards: torch.Tensor, vocab: int, cfg: LossCfg = LossCfg(), *,
                  train_agent: int = -1, std_norm: bool = True, unbiased: bool = False,
                  process_group=None, global_num_traj: Optional[Sequence[int]] = None,
-                 global_num_groups: Optional[int] = None, vocab_shard: Optional[VocabShard] = None):
+                 global_num_groups: Optional[int] = None, vocab_shard: Optional[VocabShard] = None,
+                 credit: str = "trajectory", gamma: float = 1.0,
+                 global_num_segments: Optional[Sequence[int]] = None):
         """process_group: batch sharding (this rank's trajectories; exchanges below). vocab_shard: vocab
-        sharding (every rank holds all rows, a column range of the logits). Exclusive."""
+        sharding (every rank holds all rows, a column range of the logits). Exclusive.
+        credit: "trajectory" (north_star (2): one A per trajectory) or "turn" (NEXT-2, R31: the
+        discounted reward-to-go of each trainable ACTION turn, group-normalised over the group's turns,
+        read per row through the row's segment). global_num_segments: per-rank segment counts (batch
+        sharding with turn credit; default: every rank has this rank's count)."""
         if process_group is not None and vocab_shard is not None:
             raise ValueError("batch and vocab sharding are exclusive in this step (2-D sharding is future work)")
         self.vshard = vocab_shard
@@ -85,20 +96,30 @@ class PolicyLossStep:
         self.turn_offsets, self.turn_rewards = turn_offsets, turn_rewards
         self.train_agent, self.std_norm, self.unbiased = train_agent, std_norm, unbiased
         self.pg = process_group
+        if credit not in ("trajectory", "turn"):
+            raise ValueError(f"credit must be 'trajectory' or 'turn', not {credit!r}")
+        self.credit, self.gamma = credit, float(gamma)
         dev = batch.tok_offsets.device
         N, B = batch.num_rows, batch.num_traj
+        S = int(batch.seg_len.numel())
+        self.S = S
         self.masks = dict(loss_mask=torch.empty(N, dtype=torch.uint8, device=dev),
                           row_traj=torch.empty(N, dtype=torch.int32, device=dev),
                           traj_loss_tokens=torch.empty(B, dtype=torch.int64, device=dev),
                           n_loss=torch.empty(1, dtype=torch.int64, device=dev),
                           n_active_traj=torch.empty(1, dtype=torch.int64, device=dev))
+        E = B
+        if credit == "turn":     # advantages live on segments; rows find theirs through row_seg
+            self.masks["row_seg"] = torch.empty(N, dtype=torch.int32, device=dev)
+            self.turn_out = dict(seg_return=torch.empty(S, dtype=torch.float64, device=dev),
+                                 seg_group=torch.empty(S, dtype=torch.int32, device=dev))
+            E = S
         if cfg.reduction != 0:   # sequence-mean reductions read the per-trajectory token counts (R29)
-            import dataclasses
             self.cfg = dataclasses.replace(cfg, traj_loss_tokens=self.masks["traj_loss_tokens"],
                                            n_active_traj=self.masks["n_active_traj"])
         G_loc = global_num_groups if (process_group is not None and global_num_groups) else num_groups
-        self.adv_out = dict(adv=torch.empty(B, dtype=torch.float64, device=dev),
-                            returns=torch.empty(B, dtype=torch.float64, device=dev),
+        self.adv_out = dict(adv=torch.empty(E, dtype=torch.float64, device=dev),
+                            returns=torch.empty(E, dtype=torch.float64, device=dev),
                             group_mean=torch.empty(G_loc, dtype=torch.float64, device=dev),
                             group_std=torch.empty(G_loc, dtype=torch.float64, device=dev),
                             group_size=torch.empty(G_loc, dtype=torch.int32, device=dev))
@@ -108,8 +129,11 @@ class PolicyLossStep:
             self.world = dist.get_world_size(self.pg)
             self.rank = dist.get_rank(self.pg)
             counts = list(global_num_traj) if global_num_traj is not None else [B] * self.world
+            if credit == "turn":
+                counts = list(global_num_segments) if global_num_segments is not None else [S] * self.world
             self.counts = counts
             self.b0 = sum(counts[:self.rank])
+            self.E = E
             self.Bmax = max(counts)
             self.G_global = global_num_groups if global_num_groups is not None else num_groups
             Bg = sum(counts)
@@ -123,8 +147,12 @@ class PolicyLossStep:
 
     # -- (1) + (2) --------------------------------------------------------------------------------
     def masks_and_advantages(self):
+        """Steps (1) + (2). Returns the advantage array the loss indexes: per trajectory (row_traj), or per
+        segment (row_seg) with credit="turn"."""
         otk_build_masks(self.ctx, self.batch, self.train_agent, response_mask=False, source_counts=False,
-                        out=self.masks)
+                        row_seg=self.credit == "turn", out=self.masks)
+        if self.credit == "turn":
+            return self._turn_advantages()
         if self.pg is None:
             otk_group_advantages(self.ctx, self.group_id, self.num_groups, turn_offsets=self.turn_offsets,
                                  turn_rewards=self.turn_rewards, std_norm=self.std_norm, unbiased=self.unbiased,
@@ -143,21 +171,41 @@ class PolicyLossStep:
                              unbiased=self.unbiased, out=self.adv_g)
         return self.adv_g["adv"][self.b0:self.b0 + self.batch.num_traj]
 
+    def _turn_advantages(self):
+        otk_turn_returns(self.ctx, self.batch, self.S, self.group_id, self.turn_offsets, self.turn_rewards,
+                         self.gamma, self.train_agent, out=self.turn_out)
+        seg_group, seg_return = self.turn_out["seg_group"], self.turn_out["seg_return"]
+        if self.pg is None:
+            otk_group_advantages(self.ctx, seg_group, self.num_groups, returns=seg_return, std_norm=self.std_norm,
+                                 unbiased=self.unbiased, skip_ungrouped=True, out=self.adv_out)
+            return self.adv_out["adv"]
+        from .dist import all_gather_group_returns, all_reduce_n_loss
+        all_reduce_n_loss(self.masks["n_loss"], self.pg)
+        if self.cfg.reduction != 0:
+            all_reduce_n_loss(self.masks["n_active_traj"], self.pg)
+        all_gather_group_returns(seg_group, seg_return, self.counts, self.pg, out=(self.gid_g, self.ret_g))
+        otk_group_advantages(self.ctx, self.gid_g, self.G_global, returns=self.ret_g, std_norm=self.std_norm,
+                             unbiased=self.unbiased, skip_ungrouped=True, out=self.adv_g)
+        return self.adv_g["adv"][self.b0:self.b0 + self.E]
+
     # -- (3) + (4) --------------------------------------------------------------------------------
     def loss(self, adv: torch.Tensor, micro_batches: Sequence[MicroBatch],
              on_launch: Optional[Callable[[int, str], None]] = None):
         for k, mb in enumerate(micro_batches):
             if on_launch:
                 on_launch(k, "begin")
+            cfg = self.cfg
+            if self.credit == "turn":
+                cfg = dataclasses.replace(cfg, adv_index=self.masks["row_seg"][mb.r0:mb.r1])
             if self.vshard is not None:
                 self.vshard.loss(mb.logits, mb.targets, self.masks["loss_mask"][mb.r0:mb.r1],
                                  self.masks["row_traj"][mb.r0:mb.r1], adv, mb.old_logp, mb.ref_logp,
-                                 self.masks["n_loss"], self.cfg, dlogits=mb.dlogits, stats=self.stats,
+                                 self.masks["n_loss"], cfg, dlogits=mb.dlogits, stats=self.stats,
                                  accumulate=k > 0)
             else:
                 otk_policy_loss_fwd_bwd(self.ctx, mb.logits, mb.targets, self.masks["loss_mask"][mb.r0:mb.r1],
                                         self.masks["row_traj"][mb.r0:mb.r1], adv, mb.old_logp, mb.ref_logp,
-                                        self.masks["n_loss"], self.cfg, vocab=self.vocab, dlogits=mb.dlogits,
+                                        self.masks["n_loss"], cfg, vocab=self.vocab, dlogits=mb.dlogits,
                                         stats=self.stats, accumulate=k > 0, want_logp=False)
             if on_launch:
                 on_launch(k, "end")

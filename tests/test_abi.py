@@ -54,7 +54,8 @@ def test_host_side_validation_without_gpu(lib):
     """Host-checkable errors return before any CUDA call (works on a GPU-less host)."""
     L, _ = lib
     assert L.otk_ctx_destroy(None) == 0
-    assert L.otk_build_masks(None, None, 0, None, None, None, None, None, None, None) == 1
+    assert L.otk_build_masks(None, None, 0, None, None, None, None, None, None, None, None, None) == 1
+    assert L.otk_turn_returns(None, None, 0, 0, None, None, None, C.c_double(1.0), None, None, None) == 1
     h = C.c_void_p()
     st = L.otk_ctx_create(0, C.byref(h))
     import torch

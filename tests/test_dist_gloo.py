@@ -60,6 +60,12 @@ def _worker(rank, world, port, config, q):
         R_loc = torch.from_numpy(O.episode_returns(loc.turn_offsets, loc.turn_rewards))
         gid_g, ret_g = all_gather_group_returns(torch.from_numpy(loc.group_id), R_loc, counts)
         adv_g = O.group_advantages(gid_g.numpy(), ret_g.numpy(), tb.num_groups)["adv"]
+        # ---- turn-level credit (R31): per-segment returns gathered with the per-rank SEGMENT counts
+        seg_counts = [int(tb.seg_offsets[e] - tb.seg_offsets[s]) for s, e in plan]
+        G_loc, grp_loc = O.turn_returns(loc.seg_offsets, loc.seg_source, loc.seg_agent, loc.turn_offsets,
+                                        loc.turn_rewards, loc.group_id, 0.9, traj_agent=loc.traj_agent)
+        sg_g, sr_g = all_gather_group_returns(torch.from_numpy(grp_loc), torch.from_numpy(G_loc), seg_counts)
+        tadv_g = O.group_advantages(sg_g.numpy(), sr_g.numpy(), tb.num_groups, skip_ungrouped=True)["adv"]
         # ---- loss partial sums with the GLOBAL N, then all-reduce of the stats
         rng = np.random.default_rng(100 + rank)
         rows = np.flatnonzero(m_loc["loss_mask"])[:6]
@@ -83,7 +89,7 @@ def _worker(rank, world, port, config, q):
         gathered = all_gather_vocab_partials(part)
         comb = [O.combine_partials([tuple(gathered[k, j].tolist()) for k in range(world)]) for j in range(5)]
         q.put(dict(rank=rank, n_loss=int(n_loss.item()), gid=gid_g.numpy(), ret=ret_g.numpy(), adv=adv_g,
-                   plan=plan, stats=stats.numpy(), L=L, comb=comb, X=X, Y=Y))
+                   plan=plan, stats=stats.numpy(), L=L, comb=comb, X=X, Y=Y, tadv=tadv_g))
     finally:
         dist.destroy_process_group()
 
@@ -113,6 +119,11 @@ def test_batch_and_vocab_sharding_gloo(config):
         assert np.array_equal(r["gid"], tb.group_id)               # gathered in rank order
         assert np.array_equal(r["ret"], R)
         assert np.array_equal(r["adv"], adv)                       # identical stats on every rank
+    G, grp = O.turn_returns(tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.turn_offsets, tb.turn_rewards,
+                            tb.group_id, 0.9, traj_agent=tb.traj_agent)
+    tadv = O.group_advantages(grp, G, tb.num_groups, skip_ungrouped=True)["adv"]
+    for r in res:
+        assert np.array_equal(r["tadv"], tadv)                     # turn-level: same segments, same order
     assert np.array_equal(res[0]["stats"], res[1]["stats"])
     want = (math.fsum(res[0]["L"]) + math.fsum(res[1]["L"])) / full["n_loss"]
     assert abs(res[0]["stats"][0] - want) < 1e-14

@@ -55,12 +55,15 @@ def _worker(rank, world, port, mode, q):
         ref = (lp + make_noise(N, 0.1, 2, device=dev)).contiguous()
         cfg = otk.LossCfg()
 
-        def step_for(b, pg=None, counts=None, vshard=None, cols=(0, V)):
+        credit = "turn" if mode == "batch_turn" else "trajectory"
+
+        def step_for(b, pg=None, counts=None, vshard=None, cols=(0, V), seg_counts=None):
             db = otk.traj_batch_to_device(b, dev)
             st = PolicyLossStep(ctx, db, torch.from_numpy(b.group_id).to(dev), 4,
                                 torch.from_numpy(b.turn_offsets).to(dev), torch.from_numpy(b.turn_rewards).to(dev),
                                 cols[1] - cols[0], cfg, process_group=pg, global_num_traj=counts,
-                                global_num_groups=4 if pg is not None else None, vocab_shard=vshard)
+                                global_num_groups=4 if pg is not None else None, vocab_shard=vshard,
+                                credit=credit, gamma=0.9, global_num_segments=seg_counts)
             return st, db
 
         # unsharded reference on every rank
@@ -68,14 +71,17 @@ def _worker(rank, world, port, mode, q):
         dl0 = torch.empty_like(logits)
         st0.run([MicroBatch(0, N, logits, targets, old, ref, dl0)])
         res = dict(rank=rank, ref_loss=otk.stats_dict(st0.stats), ref_adv=st0.adv_out["adv"].cpu().numpy())
-        if mode == "batch":
+        if mode in ("batch", "batch_turn"):
             plan = plan_batch_shards(traj_costs(tb, V), world)
             b0, b1 = plan[rank]
             loc = _sub(tb, b0, b1)
             r0, r1 = int(tb.tok_offsets[b0]), int(tb.tok_offsets[b1])
-            st, _ = step_for(loc, pg=dist.group.WORLD, counts=[e - s for s, e in plan])
+            st, _ = step_for(loc, pg=dist.group.WORLD, counts=[e - s for s, e in plan],
+                             seg_counts=[int(tb.seg_offsets[e] - tb.seg_offsets[s]) for s, e in plan])
             dl = torch.empty_like(logits[r0:r1])
             adv = st.masks_and_advantages()
+            if mode == "batch_turn":     # advantages live on segments: compare the rank's segment range
+                b0, b1 = int(tb.seg_offsets[b0]), int(tb.seg_offsets[b1])
             st.loss(adv, [MicroBatch(0, r1 - r0, logits[r0:r1].contiguous(), targets[r0:r1].contiguous(),
                                      old[r0:r1].contiguous(), ref[r0:r1].contiguous(), dl)])
             res.update(adv=adv.cpu().numpy(), b0=b0, b1=b1, loss=otk.stats_dict(st.stats),
@@ -99,7 +105,7 @@ def _worker(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["batch", "vocab"])
+@pytest.mark.parametrize("mode", ["batch", "vocab", "batch_turn"])
 def test_sharded_step_two_ranks_one_gpu(mode):
     world = 2
     ctx = mp.get_context("spawn")
@@ -117,7 +123,7 @@ def test_sharded_step_two_ranks_one_gpu(mode):
         rel = abs(r["loss"]["loss"] - ref["loss"]) / max(abs(ref["loss"]), 1e-6)
         assert rel < 1e-5, (r["loss"], ref)
         assert r["loss"]["n_tokens"] == ref["n_tokens"]
-    if mode == "batch":
+    if mode in ("batch", "batch_turn"):
         for r in res:
             assert np.array_equal(r["adv"], r["ref_adv"][r["b0"]:r["b1"]])     # global group statistics
             assert r["n_loss"] == r["n_loss_ref"]                               # global token count
