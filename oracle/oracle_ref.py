@@ -15,6 +15,8 @@ paper names no RL algorithm, so steps O2-O4 follow the readings listed in DESIGN
      policy_loss_fwd_bwd   dlogits = coef * (softmax - onehot); gradient pattern SPEC.md:323.
   O6 turn_returns,         turn-level credit (SURVEY.md §8(f) NEXT-2; PAPER.md:177, SPEC.md:95, :364;
      turn_level_advantages DESIGN.md R31): discounted reward-to-go per trainable ACTION turn.
+  O7 sample_token           rollout sampling (R32):
+                           inverse-transform softmax sampling with a given uniform, greedy argmax.
   O5 shard_partials,       vocab-sharded forward (north_star "all-reduced row max/sum-exp"): per-shard
      combine_partials      partials combined exactly (DESIGN.md §3 R25).
 
@@ -444,3 +446,35 @@ def combine_partials(parts):
     H = math.log(S) - T / S
     logp = math.fsum(p[3] for p in parts) - lse
     return logp, H, lse
+
+
+# --------------------------------------------------------------------------------------------
+# O7: rollout-side token sampling (PAPER.md:170-171 GENERATING)
+# --------------------------------------------------------------------------------------------
+def sample_token(x, u: float, logit_scale: float = 1.0, greedy: bool = False):
+    """One generated token from a row of logits (R32).
+
+    sample ("samples from softmax(logits/temperature)"): inverse transform with the
+    caller's uniform u in [0, 1): t = min{ t : sum_{v <= t} p_v > u }, p = softmax(s x), s = 1/temperature.
+    greedy (SPEC.md:309-318 greedy_token; also the temperature < 1e-6 limit of SPEC.md:305): the argmax
+    of the logits, ties to the lowest token id. Returns (t, log p_t) with p the softmax(s x) distribution.
+    """
+    z = float(logit_scale) * np.asarray(x, np.float64)
+    M = float(np.max(z))
+    e = np.exp(z - M)
+    S = math.fsum(e)
+    if greedy:
+        t = int(np.argmax(np.asarray(x, np.float64)))          # first maximal index
+    else:
+        cdf = np.cumsum(e / S)
+        t = int(np.searchsorted(cdf, u, side="right"))           # first t with cdf_t > u
+        if t >= len(z):                                           # u beyond the rounded total mass
+            t = int(np.flatnonzero(e > 0)[-1])
+    return t, float(z[t]) - (M + math.log(S))
+
+
+def sample_tokens(logits, u, logit_scale: float = 1.0, greedy: bool = False):
+    logits = np.asarray(logits, np.float64)
+    out = [sample_token(logits[j], float(u[j]) if u is not None else 0.0, logit_scale, greedy)
+           for j in range(logits.shape[0])]
+    return np.array([t for t, _ in out], np.int32), np.array([lp for _, lp in out])

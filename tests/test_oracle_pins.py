@@ -639,3 +639,73 @@ def test_variant_gradients_finite_differences(variant):
     sc = np.max(np.abs(out["dlogits"]))
     assert np.max(np.abs(out["dlogits"] - fd)) <= 1e-6 * sc + 1e-12
     assert abs(out["loss"] - O.loss_only(x, y, mask, rt, adv, old, ref, N, cfg)) < 1e-14
+
+
+# ----------------------------------------------------------------------------- O7 sampling
+def test_greedy_spec_examples():
+    """zero weights -> token 0; single positive logit on 53 -> 53; ties -> lowest id."""
+    x = np.zeros(128)
+    assert O.sample_token(x, 0.3, greedy=True)[0] == 0
+    x[53] = 2.0
+    assert O.sample_token(x, 0.3, greedy=True)[0] == 53
+    x = np.zeros(128)
+    x[7] = x[9] = 1.5
+    assert O.sample_token(x, 0.9, greedy=True)[0] == 7
+
+
+def test_sample_two_token_closed_form():
+    """V = 2: p_0 = 1 / (1 + e^{s (x_1 - x_0)}); token 0 iff u < p_0."""
+    x = np.array([0.7, -0.4])
+    for s in (1.0, 0.5, 3.0):
+        p0 = 1.0 / (1.0 + math.exp(s * (x[1] - x[0])))
+        assert O.sample_token(x, p0 - 1e-9, s)[0] == 0
+        assert O.sample_token(x, p0 + 1e-9, s)[0] == 1
+        t, lp = O.sample_token(x, p0 + 1e-9, s)
+        assert abs(lp - math.log(1.0 - p0)) < 1e-12
+
+
+def test_sample_uniform_row_is_floor():
+    """Uniform logits: the inverse transform is t = floor(u V)."""
+    V = 1000
+    rng = np.random.default_rng(0)
+    for u in rng.random(50):
+        if abs(u * V - round(u * V)) > 1e-6:
+            t, lp = O.sample_token(np.full(V, 0.25), u)
+            assert t == int(math.floor(u * V)) and abs(lp + math.log(V)) < 1e-12
+
+
+def test_sample_bruteforce_prefix_definition():
+    """t = min{t : sum_{v<=t} p_v > u} by exactly rounded partial sums on small rows (-inf columns never drawn)."""
+    rng = np.random.default_rng(1)
+    for _ in range(40):
+        V = int(rng.integers(2, 12))
+        x = rng.normal(scale=2.0, size=V)
+        x[rng.random(V) < 0.2] = -np.inf
+        if np.all(np.isinf(x)):
+            x[0] = 0.0
+        u = float(rng.random())
+        p = np.exp(x - x.max())
+        p = p / math.fsum(p)
+        want = next(t for t in range(V) if math.fsum(p[:t + 1]) > u)
+        t, _ = O.sample_token(x, u)
+        assert t == want and np.isfinite(x[t])
+
+
+def test_sample_empirical_frequencies():
+    """draws follow softmax(x / temperature): frequencies within 4 sigma over 20000 uniforms."""
+    rng = np.random.default_rng(2)
+    x = np.array([1.0, 0.0, -1.0, 2.0, 0.5])
+    s = 0.7
+    p = np.exp(s * x) / np.exp(s * x).sum()
+    n = 20000
+    t, _ = O.sample_tokens(np.tile(x, (n, 1)), rng.random(n), s)
+    f = np.bincount(t, minlength=5) / n
+    assert np.all(np.abs(f - p) < 4 * np.sqrt(p * (1 - p) / n))
+
+
+def test_sample_temperature_is_logit_scale():
+    """softmax(x / T): sampling x with scale s equals sampling s*x with scale 1."""
+    rng = np.random.default_rng(3)
+    x = rng.normal(size=300)
+    for u in rng.random(20):
+        assert O.sample_token(x, u, 2.5)[0] == O.sample_token(2.5 * x, u, 1.0)[0]
