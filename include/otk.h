@@ -11,6 +11,7 @@
  *   (3) otk_logprob_entropy_fwd  fused vocab-wide log-softmax + gather + entropy  north_star (3)
  *   (4) otk_policy_loss_fwd_bwd  PPO-clip + KL surrogate, token-mean, fused       north_star (4)
  *                                backward dlogits = coef * (softmax - onehot)
+ *   rollout sampling (NEXT-3): otk_sample_tokens — softmax / greedy token per row
  *   vocab sharding (north_star "vocab-sharding logits with an all-reduce of row max and sum-exp"):
  *       otk_row_partials → (caller all-gathers partials) → otk_logprob_entropy_combine /
  *       otk_policy_loss_fwd_bwd_partials.
@@ -270,6 +271,23 @@ otk_status otk_policy_loss_fwd_bwd_partials(otk_ctx* ctx, int64_t num_rows, int6
                                             const otk_loss_cfg* cfg, const otk_vocab_shard* shard,
                                             int32_t nshards, const float* partials, void* dlogits, float* logp,
                                             float* entropy, otk_loss_stats* stats, otk_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Rollout-side token sampling (R32). PAPER.md:170-171 GENERATING
+ * ("generates tokens autoregressively"); SPEC.md:300-306 sample_token: a draw from softmax(s x),
+ * s = logit_scale = 1/temperature, returned with its probability; SPEC.md:309-318 greedy_token.
+ *   greedy == 0: tokens[j] = min{ t : sum_{v <= t} p_jv > u_j },  p_j = softmax(s x_j),  u_j = uniforms[j]
+ *                (inverse transform; the caller draws u_j in [0, 1) — out-of-range u sets
+ *                OTK_ERR_INVALID_ARG in the error word and is clamped);
+ *   greedy == 1: tokens[j] = argmax_v x_jv, ties to the lowest id (uniforms may be NULL).
+ * logp[j] (NULL ok) = log p_j(tokens[j]). A row whose logits are all -inf gives token 0, logp -inf.
+ * logits: [num_rows, ld] bf16 / fp32, 16-byte aligned rows; tokens[num_rows] i32 (device).
+ * One HBM read of each logit (the re-reads of pass 2/3 hit L2). Parity: greedy bit-exact; a sampled
+ * token is exact unless u_j lies within 2e-5 of a cdf boundary, where either neighbour is accepted.
+ * ------------------------------------------------------------------------------------------- */
+otk_status otk_sample_tokens(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld, otk_dtype dtype,
+                             const void* logits, const float* uniforms, float logit_scale, int32_t greedy,
+                             int32_t* tokens, float* logp, otk_stream_t stream);
 
 /* Harness helper (not on the path): number of kernel launches the library issued since ctx creation. */
 int64_t otk_ctx_launch_count(const otk_ctx* ctx);

@@ -83,6 +83,7 @@ _sig = {
                                           C.POINTER(otk_loss_cfg), _P, _P, _P, _P, _P]),
     "otk_policy_loss_fwd_bwd_host": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, _P, C.c_int32, _P, _P,
                                                _P, _I64, C.POINTER(otk_loss_cfg), _P, _P, _I64]),
+    "otk_sample_tokens": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, C.c_float, C.c_int32, _P, _P, _P]),
     "otk_row_partials": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, C.POINTER(otk_vocab_shard),
                                    C.c_float, _P, _P]),
     "otk_logprob_entropy_combine": (C.c_int, [_P, _I64, C.c_int32, _P, _P, _P, _P, _P, _P]),
@@ -289,6 +290,33 @@ def otk_turn_returns(ctx: Context, batch: DeviceTrajBatch, num_segments: int, gr
     _check(_lib.otk_turn_returns(ctx.handle, C.byref(cb), int(num_segments), int(train_agent), _ptr(group_id),
                                  _ptr(turn_offsets), _ptr(turn_rewards), float(gamma), _ptr(o["seg_return"]),
                                  _ptr(o["seg_group"]), _stream(stream)))
+    return o
+
+
+# ------------------------------------------------------------------------------------------------
+# rollout sampling (NEXT-3)
+# ------------------------------------------------------------------------------------------------
+def otk_sample_tokens(ctx: Context, logits: torch.Tensor, uniforms: Optional[torch.Tensor] = None, *,
+                      logit_scale: float = 1.0, greedy: bool = False, vocab: Optional[int] = None,
+                      want_logp: bool = True, out: Optional[dict] = None, stream=None) -> dict:
+    """One token per row: inverse-transform draw from softmax(logit_scale * x) with the caller's uniforms,
+    or the greedy argmax (otk.h otk_sample_tokens)."""
+    _dev(logits, "logits")
+    N, ld = logits.shape
+    V = ld if vocab is None else int(vocab)
+    if not greedy:
+        if uniforms is None:
+            raise ValueError("uniforms are required unless greedy")
+        _dev(uniforms, "uniforms")
+        if uniforms.dtype != torch.float32 or uniforms.numel() != N:
+            raise ValueError("uniforms must be float32 [num_rows]")
+    o = out if out is not None else {}
+    o.setdefault("tokens", torch.empty(N, dtype=torch.int32, device=logits.device))
+    if want_logp:
+        o.setdefault("logp", torch.empty(N, dtype=torch.float32, device=logits.device))
+    _check(_lib.otk_sample_tokens(ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits),
+                                  _ptr(uniforms) if not greedy else None, float(logit_scale), int(bool(greedy)),
+                                  _ptr(o["tokens"]), _ptr(o.get("logp")), _stream(stream)))
     return o
 
 

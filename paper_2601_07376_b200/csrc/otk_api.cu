@@ -318,6 +318,36 @@ otk_status otk_turn_returns(otk_ctx* ctx, const otk_traj_batch* batch, int32_t n
   return OTK_OK;
 }
 
+otk_status otk_sample_tokens(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld, otk_dtype dtype,
+                             const void* logits, const float* uniforms, float logit_scale, int32_t greedy,
+                             int32_t* tokens, float* logp, otk_stream_t stream) {
+  OTK_REQUIRE(ctx, OTK_ERR_INVALID_ARG, "ctx is NULL");
+  OTK_REQUIRE(dtype == OTK_BF16 || dtype == OTK_F32, OTK_ERR_DTYPE, "unknown dtype");
+  OTK_REQUIRE(num_rows >= 0 && vocab >= 1 && ld >= vocab && vocab < (int64_t(1) << 31), OTK_ERR_SHAPE,
+              "need num_rows >= 0, 1 <= vocab < 2^31, ld >= vocab");
+  OTK_REQUIRE(logits && tokens, OTK_ERR_INVALID_ARG, "logits / tokens is NULL");
+  OTK_REQUIRE(greedy == 0 || greedy == 1, OTK_ERR_INVALID_ARG, "greedy must be 0 or 1");
+  OTK_REQUIRE(greedy || uniforms, OTK_ERR_INVALID_ARG, "uniforms is NULL (required unless greedy)");
+  OTK_REQUIRE(aligned16(logits) && (ld * int64_t(dtype_size(dtype))) % 16 == 0, OTK_ERR_ALIGNMENT,
+              "logits base and row stride must be 16-byte aligned");
+  OTK_REQUIRE(logit_scale > 0 && std::isfinite(logit_scale), OTK_ERR_INVALID_ARG, "logit_scale must be > 0");
+  if (num_rows == 0) return OTK_OK;
+  otk::SampleParams p;
+  p.num_rows = num_rows;
+  p.vocab = vocab;
+  p.ld = ld;
+  p.logits = logits;
+  p.u = uniforms;
+  p.scale = logit_scale;
+  p.greedy = greedy;
+  p.tokens = tokens;
+  p.logp = logp;
+  p.err = ctx->d_err;
+  OTK_CUDA(otk::launch_sample(p, dtype, ctx->num_sms, reinterpret_cast<cudaStream_t>(stream)), "k_sample launch");
+  ctx->launches += 1;
+  return OTK_OK;
+}
+
 otk_status otk_logprob_entropy_fwd(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld, otk_dtype dtype,
                                    const void* logits, const int32_t* targets, const uint8_t* row_mask,
                                    float logit_scale, float* logp, float* entropy, float* lse, otk_stream_t stream) {

@@ -146,6 +146,19 @@ struct TurnParams {
 };
 cudaError_t launch_turn_returns(const TurnParams& p, cudaStream_t s);
 
+struct SampleParams {
+  int64_t num_rows, vocab, ld;
+  const void* logits;
+  const float* u;
+  float scale;
+  int greedy;
+  int csize;  // CTAs per row (thread-block cluster), set by the launcher
+  int32_t* tokens;
+  float* logp;
+  int* err;
+};
+cudaError_t launch_sample(const SampleParams& p, int dtype, int num_sms, cudaStream_t s);
+
 __device__ __forceinline__ void set_error(int* err, int code) { atomicCAS(err, 0, code); }
 
 }  // namespace otk

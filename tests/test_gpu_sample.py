@@ -1,0 +1,141 @@
+"""Rollout sampling kernel (R32) vs the oracle (-m gpu).
+
+Greedy tokens are bit-exact (argmax, ties to the lowest id). A sampled token is an integer decided by
+floating point: the kernel's fp32 cdf and the oracle's float64 cdf agree to ~1e-6, so the token must
+equal the oracle's whenever u lies farther than TOL = 2e-5 from the boundaries of the oracle token's
+cdf interval, and otherwise must be a token whose interval is within TOL of u (either neighbour of a
+boundary is a correct draw). logp of the returned token within the forward tolerance (2e-3 bf16).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle_ref as O
+from synth import make_logits
+from tests.gpu_common import LOGP_TOL
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-5
+
+
+@pytest.fixture(scope="module")
+def otk():
+    import paper_2601_07376_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(otk):
+    c = otk.Context(0)
+    yield c
+    c.close()
+
+
+def _cdf(x, s):
+    z = s * np.asarray(x, np.float64)
+    e = np.exp(z - z.max())
+    return np.cumsum(e / math.fsum(e))
+
+
+def _check_sampled(tok, lp, wide, u, s, dtype, rows):
+    exact = 0
+    for j in rows:
+        t = int(tok[j])
+        want, wlp = O.sample_token(wide[j], float(u[j]), s)
+        cdf = _cdf(wide[j], s)
+        lo = cdf[want - 1] if want > 0 else 0.0
+        if t == want:
+            exact += 1
+        else:
+            far = (u[j] - lo) > TOL and (cdf[want] - u[j]) > TOL
+            assert not far, (j, t, want, u[j], lo, cdf[want])
+            glo = cdf[t - 1] if t > 0 else 0.0
+            assert glo - TOL <= u[j] <= cdf[t] + TOL, (j, t, want)
+        z = s * wide[j]
+        zl = z.max() + math.log(math.fsum(np.exp(z - z.max())))
+        assert abs(float(lp[j]) - (z[t] - zl)) < LOGP_TOL[dtype], (j, float(lp[j]), z[t] - zl)
+    return exact
+
+
+@pytest.mark.parametrize("dtype,V,ld,n,scale", [("bf16", 151936, 151936, 384, 1.0), ("bf16", 151936, 151936, 300, 0.7),
+                                                ("f32", 1000, 1000, 300, 1.0), ("bf16", 4100, 4104, 200, 1.3),
+                                                ("bf16", 17, 24, 64, 1.0), ("f32", 50000, 50004, 64, 2.0)])
+def test_sample_tokens_vs_oracle(otk, ctx, dtype, V, ld, n, scale):
+    logits, _ = make_logits(n, V, ld=ld if ld != V else None, dtype=dtype, seed=V % 977 + n, device="cpu")
+    wide = logits.double().numpy()[:, :V]
+    rng = np.random.default_rng(V + n)
+    u = rng.random(n).astype(np.float32)
+    u[:4] = [0.0, np.float32(1.0 - 2 ** -24), 0.5, np.float32(1e-7)]      # edges of [0, 1)
+    out = otk.otk_sample_tokens(ctx, logits.cuda(), torch.from_numpy(u).cuda(), logit_scale=scale, vocab=V)
+    ctx.check()
+    tok = out["tokens"].cpu().numpy()
+    lp = out["logp"].cpu().numpy()
+    assert np.all((tok >= 0) & (tok < V))
+    rows = range(n) if V * n <= 4e7 else sorted(set(range(0, n, max(1, n // 64))) | {0, 1, 2, 3, n - 1})
+    exact = _check_sampled(tok, lp, wide, u.astype(np.float64), scale, dtype, rows)
+    assert exact >= 0.9 * len(rows)
+
+
+def test_greedy_bit_exact(otk, ctx):
+    n, V = 96, 151936
+    logits, _ = make_logits(n, V, dtype="bf16", seed=5, device="cpu")
+    x = logits.clone()
+    x[1, :] = 0.0                                   # SPEC.md:316 zero weights -> token 0
+    x[2, 77] = x[2, 150001] = x[2].max() + 1.0      # ties -> lowest id
+    x[3, :] = float("-inf")
+    x[3, 151935] = 1.0                              # the last column is the only finite one
+    x[4, :] = float("-inf")                         # degenerate row: token 0, logp -inf
+    x[5, 0:100] = float("-inf")
+    out = otk.otk_sample_tokens(ctx, x.cuda(), greedy=True)
+    ctx.check()
+    tok = out["tokens"].cpu().numpy()
+    wide = x.double().numpy()
+    for j in range(n):
+        if j == 4:
+            assert tok[j] == 0 and out["logp"][j].item() == float("-inf")
+            continue
+        assert tok[j] == int(np.argmax(wide[j])), j
+        assert abs(out["logp"][j].item() - O.sample_token(wide[j], 0.0, greedy=True)[1]) < LOGP_TOL["bf16"]
+    assert tok[1] == 0 and tok[2] == 77 and tok[3] == 151935
+
+
+def test_sample_masked_columns_never_drawn(otk, ctx):
+    """-inf logits carry no mass: a draw never lands on them (also at u ~ 1)."""
+    n, V = 256, 8192
+    logits, _ = make_logits(n, V, dtype="bf16", seed=9, device="cpu")
+    keep = torch.zeros(V, dtype=torch.bool)
+    keep[torch.randperm(V, generator=torch.Generator().manual_seed(1))[:40]] = True
+    logits[:, ~keep] = float("-inf")
+    u = torch.rand(n, generator=torch.Generator().manual_seed(2))
+    u[:3] = torch.tensor([0.0, 1.0 - 2 ** -24, 0.9999])
+    out = otk.otk_sample_tokens(ctx, logits.cuda(), u.float().cuda())
+    ctx.check()
+    assert bool(keep[out["tokens"].cpu().long()].all())
+
+
+def test_sample_empirical_distribution(otk, ctx):
+    """frequencies of 2^16 draws (seeded uniforms) within 4 sigma of softmax(s x)."""
+    V, n, s = 8, 1 << 16, 0.8
+    x = torch.tensor([1.0, 0.0, -1.0, 2.0, 0.5, -3.0, 1.5, 0.25], dtype=torch.float32)
+    logits = x.repeat(n, 1)
+    u = torch.rand(n, generator=torch.Generator().manual_seed(3)).float()
+    out = otk.otk_sample_tokens(ctx, logits.cuda(), u.cuda(), logit_scale=s)
+    ctx.check()
+    f = np.bincount(out["tokens"].cpu().numpy(), minlength=V) / n
+    p = np.exp(s * x.double().numpy())
+    p /= p.sum()
+    assert np.all(np.abs(f - p) < 4 * np.sqrt(p * (1 - p) / n))
+
+
+def test_sample_errors(otk, ctx):
+    logits = torch.zeros(4, 64, device="cuda")
+    with pytest.raises(ValueError):
+        otk.otk_sample_tokens(ctx, logits)                       # uniforms required unless greedy
+    with pytest.raises(otk.OtkError):
+        otk.otk_sample_tokens(ctx, logits, torch.zeros(4, device="cuda"), logit_scale=0.0)
+    otk.otk_sample_tokens(ctx, logits, torch.tensor([0.1, 1.5, 0.2, 0.3], device="cuda"))
+    with pytest.raises(otk.OtkError) as e:
+        ctx.check()
+    assert e.value.status == 1                                   # OTK_ERR_INVALID_ARG: u outside [0, 1)
