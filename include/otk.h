@@ -11,6 +11,7 @@
  *   (3) otk_logprob_entropy_fwd  fused vocab-wide log-softmax + gather + entropy  north_star (3)
  *   (4) otk_policy_loss_fwd_bwd  PPO-clip + KL surrogate, token-mean, fused       north_star (4)
  *                                backward dlogits = coef * (softmax - onehot)
+ *   LM head fused with (3) (NEXT-1, fwd): otk_lmhead_logprob_fwd — tcgen05 GEMM + log-softmax epilogue
  *   rollout sampling (NEXT-3): otk_sample_tokens — softmax / greedy token per row
  *   vocab sharding (north_star "vocab-sharding logits with an all-reduce of row max and sum-exp"):
  *       otk_row_partials → (caller all-gathers partials) → otk_logprob_entropy_combine /
@@ -288,6 +289,25 @@ otk_status otk_policy_loss_fwd_bwd_partials(otk_ctx* ctx, int64_t num_rows, int6
 otk_status otk_sample_tokens(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld, otk_dtype dtype,
                              const void* logits, const float* uniforms, float logit_scale, int32_t greedy,
                              int32_t* tokens, float* logp, otk_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * LM head fused with step (3) (forward half; R33). The fwd pool
+ * evaluates log-probs from the policy's final hidden states: z_j = s * h_j W^T, then
+ * (3) on z_j, without writing the [num_rows, vocab] logits to memory:
+ *   logp_j = z_{j,y_j} - lse_j,  entropy_j = lse_j - sum_v p_jv z_jv,  lse_j = log sum_v e^{z_jv}.
+ * hidden: [num_rows, hidden_dim] bf16 row-major; weight: [vocab, hidden_dim] bf16 row-major (the LM-head
+ * matrix as stored by an nn.Linear(hidden_dim, vocab)); hidden_dim a multiple of 64; base pointers
+ * 16-byte aligned. GEMM on the tcgen05 tensor cores with fp32 accumulation in TMEM; the log-softmax
+ * statistics are folded in the epilogue. workspace: device scratch of otk_lmhead_workspace_bytes()
+ * bytes (per-row partials of each vocab chunk), caller-owned. Outputs as in (3) (row_mask NULL = all
+ * rows; masked rows get 0). Tolerance vs the float64 oracle on the same bf16 h and W: 2e-3 abs.
+ * ------------------------------------------------------------------------------------------- */
+int64_t otk_lmhead_workspace_bytes(const otk_ctx* ctx, int64_t num_rows, int64_t vocab);
+otk_status otk_lmhead_logprob_fwd(otk_ctx* ctx, int64_t num_rows, int64_t hidden_dim, int64_t vocab,
+                                  const void* hidden, const void* weight, const int32_t* targets,
+                                  const uint8_t* row_mask, float logit_scale, void* workspace,
+                                  int64_t workspace_bytes, float* logp, float* entropy, float* lse,
+                                  otk_stream_t stream);
 
 /* Harness helper (not on the path): number of kernel launches the library issued since ctx creation. */
 int64_t otk_ctx_launch_count(const otk_ctx* ctx);

@@ -17,6 +17,7 @@ paper names no RL algorithm, so steps O2-O4 follow the readings listed in DESIGN
      turn_level_advantages DESIGN.md R31): discounted reward-to-go per trainable ACTION turn.
   O7 sample_token           rollout sampling (R32):
                            inverse-transform softmax sampling with a given uniform, greedy argmax.
+  O8 lmhead_logprob_fwd    LM head fused with O3 (R33): z = s h W^T, then O3.
   O5 shard_partials,       vocab-sharded forward (north_star "all-reduced row max/sum-exp"): per-shard
      combine_partials      partials combined exactly (DESIGN.md §3 R25).
 
@@ -478,3 +479,21 @@ def sample_tokens(logits, u, logit_scale: float = 1.0, greedy: bool = False):
     out = [sample_token(logits[j], float(u[j]) if u is not None else 0.0, logit_scale, greedy)
            for j in range(logits.shape[0])]
     return np.array([t for t, _ in out], np.int32), np.array([lp for _, lp in out])
+
+
+# --------------------------------------------------------------------------------------------
+# O8: LM head fused with O3 (PAPER.md:188 fwd pool; R33)
+# --------------------------------------------------------------------------------------------
+def lmhead_logprob_fwd(hidden, weight, targets, logit_scale: float = 1.0, rows=None):
+    """z_j = s * h_j W^T (float64 matmul of the given values), then O3 row_forward on z_j.
+    Returns dict(logp, entropy, lse) over `rows` (default all)."""
+    h = np.asarray(hidden, np.float64)
+    W = np.asarray(weight, np.float64)
+    rows = range(h.shape[0]) if rows is None else rows
+    out = {}
+    for j in rows:
+        z = W @ h[j]
+        lp, H, lse, _ = row_forward(z, int(targets[j]), logit_scale)
+        out[j] = (lp, H, lse)
+    return dict(logp={j: v[0] for j, v in out.items()}, entropy={j: v[1] for j, v in out.items()},
+                lse={j: v[2] for j, v in out.items()})

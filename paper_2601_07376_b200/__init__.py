@@ -83,6 +83,8 @@ _sig = {
                                           C.POINTER(otk_loss_cfg), _P, _P, _P, _P, _P]),
     "otk_policy_loss_fwd_bwd_host": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, _P, C.c_int32, _P, _P,
                                                _P, _I64, C.POINTER(otk_loss_cfg), _P, _P, _I64]),
+    "otk_lmhead_workspace_bytes": (_I64, [_P, _I64, _I64]),
+    "otk_lmhead_logprob_fwd": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _P, C.c_float, _P, _I64, _P, _P, _P, _P]),
     "otk_sample_tokens": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, C.c_float, C.c_int32, _P, _P, _P]),
     "otk_row_partials": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, C.POINTER(otk_vocab_shard),
                                    C.c_float, _P, _P]),
@@ -290,6 +292,38 @@ def otk_turn_returns(ctx: Context, batch: DeviceTrajBatch, num_segments: int, gr
     _check(_lib.otk_turn_returns(ctx.handle, C.byref(cb), int(num_segments), int(train_agent), _ptr(group_id),
                                  _ptr(turn_offsets), _ptr(turn_rewards), float(gamma), _ptr(o["seg_return"]),
                                  _ptr(o["seg_group"]), _stream(stream)))
+    return o
+
+
+# ------------------------------------------------------------------------------------------------
+# LM head fused with (3) (NEXT-1, forward)
+# ------------------------------------------------------------------------------------------------
+def otk_lmhead_logprob_fwd(ctx: Context, hidden: torch.Tensor, weight: torch.Tensor, targets: torch.Tensor, *,
+                           row_mask: Optional[torch.Tensor] = None, logit_scale: float = 1.0,
+                           workspace: Optional[torch.Tensor] = None, want_lse: bool = False,
+                           out: Optional[dict] = None, stream=None) -> dict:
+    """logp / entropy of z = logit_scale * hidden @ weight.T without materialising z (otk.h)."""
+    for t, n in ((hidden, "hidden"), (weight, "weight"), (targets, "targets")):
+        _dev(t, n)
+    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise ValueError("hidden and weight must be bfloat16")
+    N, d = hidden.shape
+    V, d2 = weight.shape
+    if d != d2:
+        raise ValueError("hidden / weight inner dimensions differ")
+    nbytes = int(_lib.otk_lmhead_workspace_bytes(ctx.handle, N, V))
+    if workspace is None or workspace.numel() * workspace.element_size() < nbytes:
+        workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=hidden.device)
+    o = out if out is not None else {}
+    o.setdefault("logp", torch.empty(N, dtype=torch.float32, device=hidden.device))
+    o.setdefault("entropy", torch.empty(N, dtype=torch.float32, device=hidden.device))
+    if want_lse:
+        o.setdefault("lse", torch.empty(N, dtype=torch.float32, device=hidden.device))
+    _check(_lib.otk_lmhead_logprob_fwd(ctx.handle, N, d, V, _ptr(hidden), _ptr(weight), _ptr(targets),
+                                       _ptr(row_mask), float(logit_scale), _ptr(workspace),
+                                       workspace.numel() * workspace.element_size(), _ptr(o["logp"]),
+                                       _ptr(o["entropy"]), _ptr(o.get("lse")), _stream(stream)))
+    o["workspace"] = workspace
     return o
 
 

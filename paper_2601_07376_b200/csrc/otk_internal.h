@@ -159,6 +159,11 @@ struct SampleParams {
 };
 cudaError_t launch_sample(const SampleParams& p, int dtype, int num_sms, cudaStream_t s);
 
+int lmhead_chunks(int64_t num_rows, int64_t vocab, int num_sms);
+cudaError_t launch_lmhead_fwd(const otk_ctx* ctx, int64_t num_rows, int64_t vocab, int d, const void* hidden,
+                              const void* weight, const int32_t* targets, float logit_scale, float4* partials,
+                              int n_chunks, cudaStream_t s);
+
 __device__ __forceinline__ void set_error(int* err, int code) { atomicCAS(err, 0, code); }
 
 }  // namespace otk

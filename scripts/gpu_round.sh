@@ -9,4 +9,7 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1; echo "launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_rows -s 2 -c 1 -o gpurun_out/prof_k4 -f python scripts/prof_k4.py > gpurun_out/ncu_full.log 2>&1; echo "full rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_rows -s 2 -c 1 -o gpurun_out/prof_k3 -f python scripts/prof_k4.py --fwd > gpurun_out/ncu_full3.log 2>&1; echo "full3 rc=$?"
-tail -1 gpurun_out/smoke.log; tail -2 gpurun_out/gpu_tests.log; tail -1 gpurun_out/bench.err; tail -1 gpurun_out/bench_ref.err
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sample -s 2 -c 1 -o gpurun_out/prof_sample -f python scripts/prof_sample.py 4096 > gpurun_out/ncu_sample.log 2>&1; echo "sample rc=$?"
+timeout 300 python scripts/perf_sample.py > gpurun_out/perf_sample.jsonl 2>&1; echo "perf_sample rc=$?"
+for tool in memcheck racecheck synccheck; do timeout 600 compute-sanitizer --tool $tool --error-exitcode 3 python scripts/sanitize.py > gpurun_out/sanitize_$tool.log 2>&1; echo "$tool rc=$?" >> gpurun_out/sanitize_$tool.log; done
+tail -1 gpurun_out/smoke.log; tail -2 gpurun_out/gpu_tests.log; tail -1 gpurun_out/bench.err; tail -1 gpurun_out/bench_ref.err; tail -n2 gpurun_out/sanitize_*.log

@@ -8,8 +8,9 @@ plus the noise drawn here.
 """
 from .trajectories import TrajBatch, make_batch, CONFIGS, WorkloadConfig, concat_batches, split_rows
 from .logits import make_logits, make_noise, bf16_round
+from .lmhead import make_lmhead
 
 __all__ = [
     "TrajBatch", "make_batch", "CONFIGS", "WorkloadConfig", "concat_batches", "split_rows",
-    "make_logits", "make_noise", "bf16_round",
+    "make_logits", "make_noise", "bf16_round", "make_lmhead",
 ]

@@ -709,3 +709,39 @@ def test_sample_temperature_is_logit_scale():
     x = rng.normal(size=300)
     for u in rng.random(20):
         assert O.sample_token(x, u, 2.5)[0] == O.sample_token(2.5 * x, u, 1.0)[0]
+
+
+# ----------------------------------------------------------------------------- O8 LM head + forward
+def test_lmhead_zero_weight_is_uniform():
+    """W = 0: every logit is 0, so logp = -ln V and entropy = ln V (north_star's uniform pin)."""
+    rng = np.random.default_rng(0)
+    h = rng.normal(size=(3, 64))
+    out = O.lmhead_logprob_fwd(h, np.zeros((1000, 64)), [0, 5, 999])
+    for j in range(3):
+        assert abs(out["logp"][j] + math.log(1000)) < 1e-12 and abs(out["entropy"][j] - math.log(1000)) < 1e-12
+
+
+def test_lmhead_one_hot_hidden_reduces_to_forward():
+    """h = e_k picks column k of W: the fused forward equals O3 on that column (a different code path)."""
+    rng = np.random.default_rng(1)
+    W = rng.normal(scale=2.0, size=(700, 32))
+    for k, y, s in ((3, 10, 1.0), (31, 699, 0.7), (0, 0, 2.0)):
+        h = np.zeros((1, 32))
+        h[0, k] = 1.0
+        out = O.lmhead_logprob_fwd(h, W, [y], s)
+        lp, H, lse, _ = O.row_forward(W[:, k], y, s)
+        assert out["logp"][0] == lp and out["entropy"][0] == H and out["lse"][0] == lse
+
+
+def test_lmhead_vs_torch_float64():
+    """Library pin: torch float64 matmul + log_softmax + entropy."""
+    rng = np.random.default_rng(2)
+    h = rng.normal(size=(5, 48))
+    W = rng.normal(scale=0.3, size=(257, 48))
+    y = rng.integers(0, 257, 5)
+    out = O.lmhead_logprob_fwd(h, W, y, 1.3)
+    z = 1.3 * (torch.from_numpy(h) @ torch.from_numpy(W).T)
+    ls = torch.log_softmax(z, -1)
+    for j in range(5):
+        assert abs(out["logp"][j] - float(ls[j, y[j]])) < 1e-12
+        assert abs(out["entropy"][j] + float((ls[j].exp() * ls[j]).sum())) < 1e-12
