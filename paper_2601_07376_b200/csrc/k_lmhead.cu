@@ -4,18 +4,19 @@
 // old / reference policy; with the LM head fused, its input is the final hidden state h [N, d] and the
 // head weight W [V, d] (logits z = s * h W^T).
 //
-// tcgen05 GEMM, one CTA per SM (persistent), warp-specialised:
-//   warp 0      TMA producer: 2-D tensor-map loads (128-byte swizzle) of a 256 x 64 tile of h and a
-//               256 x 64 tile of W per stage (3 stages x 64 KB);
-//   warp 1      MMA issuer: per 64-wide k-block four K=16 steps of two tcgen05.mma (M = 128 each, the two
-//               halves of the 256-row tile, N = 256) into TMEM (2 x 256 fp32 columns = all 512);
-//               tcgen05.commit frees the smem stage and, after the last k-block, signals the epilogue;
-//   warps 2-9   epilogue: warp w reads TMEM lane quadrant w % 4 of accumulator (w - 2) / 4 with
-//               tcgen05.ld.32x32b.x32 — one thread per row, 256 logits per vocab tile — and folds them into
-//               the row's online (reference m, sum 2^{y-m}, sum 2^{y-m}(y-m)) in the log2 domain
-//               (y = s log2(e) z) plus the target logit.
-// A work unit is (256-row tile, vocab chunk); each unit writes per-row partials (m, s, t, y_target - m or
-// -inf) of its chunk, and k_combine (the vocab-shard combine) turns the chunks into logp / entropy / lse.
+// tcgen05 GEMM on CTA pairs (cta_group::2, a 2-CTA cluster on the two SMs of a TPC), persistent:
+//   the pair computes a 256-row x 256-column tile per MMA (M = 256, N = 256, K = 16): each CTA stages its
+//   own 128 rows of h and half (128 columns) of the W tile per 64-wide k-block (6 stages x 32 KB), and
+//   holds its 128 rows x 256 fp32 accumulators in TMEM — twice (512 columns), so the epilogue of tile t
+//   overlaps the MMAs of tile t + 1.
+//   warp 0      TMA producer (both CTAs): 2-D tensor-map loads, 128-byte swizzle, completion counted on
+//               the leader CTA's stage barrier;
+//   warp 1      MMA issuer (leader CTA, one thread): tcgen05.mma.cta_group::2; tcgen05.commit multicast
+//               frees the stage in both CTAs and, after the last k-block, signals both epilogues;
+//   warps 2-5   epilogue (both CTAs): warp w reads TMEM lane quadrant w % 4 with tcgen05.ld.32x32b.x32 —
+//               one thread per row, 256 logits per vocab tile — and folds them into the row's online
+//               (reference m, sum 2^{y-m}, sum 2^{y-m}(y-m)) in the log2 domain (y = s log2(e) z) plus the
+//               target logit; then arrives on the leader's accumulator-empty barrier (DSMEM for the peer).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -29,22 +30,23 @@ namespace otk {
 
 using namespace ptx;
 
-constexpr int kLmRows = 256;   // rows per tile (two M = 128 MMAs)
-constexpr int kLmCols = 256;   // vocab columns per tile (MMA N)
+constexpr int kLmRows = 256;   // rows per pair tile (128 per CTA)
+constexpr int kLmCols = 256;   // vocab columns per tile (MMA N; 128 staged per CTA)
 constexpr int kLmK = 64;       // hidden elements per k-block (128 bytes of bf16: one swizzle atom row)
-constexpr int kLmStages = 3;
-constexpr int kLmABytes = kLmRows * kLmK * 2;  // 32 KB
-constexpr int kLmBBytes = kLmCols * kLmK * 2;  // 32 KB
+constexpr int kLmStages = 6;
+constexpr int kLmABytes = 128 * kLmK * 2;  // 16 KB: this CTA's rows
+constexpr int kLmBBytes = 128 * kLmK * 2;  // 16 KB: this CTA's half of the columns
 constexpr int kLmStageBytes = kLmABytes + kLmBBytes;
-constexpr int kLmEpiWarps = 8;
+constexpr int kLmEpiWarps = 4;
 constexpr int kLmThreads = 32 * (2 + kLmEpiWarps);
 constexpr int kLmSmemBytes = kLmStages * kLmStageBytes + 1024 /* 1 KB alignment slack */ + 256 /* barriers */;
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address of the same offset in CTA rank 0
 
 struct LmParams {
   int64_t num_rows, vocab;
   int d;                 // hidden size (multiple of 64)
   int n_rowtiles;        // ceil(num_rows / 256)
-  int n_chunks;          // vocab chunks per row tile
+  int n_chunks;          // vocab chunks
   int n_coltiles;        // ceil(vocab / 256)
   const int32_t* targets;
   float k2;              // logit_scale * log2(e)
@@ -52,11 +54,13 @@ struct LmParams {
 };
 
 // ---- PTX wrappers specific to the tensor-core path -------------------------------------------------
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+// 2-CTA TMA: lands in this CTA's smem, completes bytes on the leader CTA's barrier.
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_leader, int c0,
+                                                 int c1) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          dst),
-      "l"(map), "r"(bar), "r"(c0), "r"(c1)
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(dst),
+      "l"(map), "r"(bar_leader), "r"(c0), "r"(c1)
       : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
@@ -68,20 +72,36 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return uint64_t((saddr & 0x3FFFFu) >> 4) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
          (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
-// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, N = 256, M = 128.
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, N = 256, M = 256 (CTA pair).
 constexpr uint32_t kLmIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kLmCols >> 3) << 17) |
-                              (uint32_t(128 >> 4) << 24);
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+                              (uint32_t(kLmRows >> 4) << 24);
+__device__ __forceinline__ void umma_pair_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(kLmIdesc), "r"(accumulate)
       : "memory");
 }
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+// arrive (once) on the barrier at this smem offset in BOTH CTAs of the pair when the issued MMAs complete
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(uint16_t(0x3))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* smem_dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
+               "r"(ncols)
                : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
@@ -100,6 +120,22 @@ __device__ __forceinline__ int chunk_tile0(int c, int n_chunks, int n_coltiles) 
   return int((int64_t(c) * n_coltiles) / n_chunks);
 }
 
+// Work unit u -> (vocab chunk c, row tile rt), blocked: units run in row blocks of kLmRowBlock tiles; inside
+// a block, chunk-major. The ~74 pairs running at the same time then share kLmRowBlock tiles of h (~29 MB at d = 3584,
+// reused from L2 by every vocab tile of their units) and ~74 / kLmRowBlock chunks of W, so W is read from
+// HBM once per row block instead of once per row tile (and h never thrashes L2).
+#ifndef OTK_LM_ROWBLOCK
+#define OTK_LM_ROWBLOCK 16
+#endif
+constexpr int kLmRowBlock = OTK_LM_ROWBLOCK;  // measured: 16 ~ 32 > 8 > 64 > 4 (scripts/perf_lmhead.py)
+__device__ __forceinline__ void unit_coords(int u, int n_rowtiles, int n_chunks, int& c, int& rt) {
+  const int R = min(kLmRowBlock, n_rowtiles);
+  const int per_block = R * n_chunks;
+  const int rb = u / per_block, w = u - rb * per_block;
+  const int Rb = min(R, n_rowtiles - rb * R);  // the last block may hold fewer row tiles
+  c = w / Rb;
+  rt = rb * R + (w - c * Rb);
+}
 __global__ void __launch_bounds__(kLmThreads, 1)
     k_lmhead_fwd(const __grid_constant__ CUtensorMap tm_h, const __grid_constant__ CUtensorMap tm_w,
                  const LmParams p) {
@@ -107,11 +143,13 @@ __global__ void __launch_bounds__(kLmThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kLmStages * kLmStageBytes);
   uint64_t* empty = full + kLmStages;
-  uint64_t* tfull = empty + kLmStages;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* tfull = empty + kLmStages;  // [2] accumulator buffers
+  uint64_t* tempty = tfull + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = int(cluster_ctarank());
+  const int pair = int(cluster_id_x()), npairs = int(nclusters_x());
   const int n_units = p.n_rowtiles * p.n_chunks;
   const int kblocks = p.d / kLmK;
 
@@ -120,36 +158,37 @@ __global__ void __launch_bounds__(kLmThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, kLmEpiWarps);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 2 * kLmEpiWarps);
+    }
     fence_mbar_init();
     prefetch_tmap(&tm_h);
     prefetch_tmap(&tm_w);
   }
-  if (warp == 1) {
-    tmem_alloc(tmem_slot, 512);
-    tmem_relinquish();
-  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- TMA producer
+    // ---------------- TMA producer (both CTAs)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const int rt = u / p.n_chunks, c = u % p.n_chunks;
+      for (int u = pair; u < n_units; u += npairs) {
+        int c, rt;
+        unit_coords(u, p.n_rowtiles, p.n_chunks, c, rt);
         const int t0 = chunk_tile0(c, p.n_chunks, p.n_coltiles), t1 = chunk_tile0(c + 1, p.n_chunks, p.n_coltiles);
         for (int t = t0; t < t1; ++t) {
           for (int kb = 0; kb < kblocks; ++kb) {
             mbar_wait(&empty[s], ph ^ 1u);
             const uint32_t a = smem_u32(smem + s * kLmStageBytes);
-            mbar_arrive_expect_tx(&full[s], kLmStageBytes);
-            tma_load_2d(a, &tm_h, smem_u32(&full[s]), kb * kLmK, rt * kLmRows);
-            tma_load_2d(a + kLmABytes, &tm_w, smem_u32(&full[s]), kb * kLmK, t * kLmCols);
+            const uint32_t bar = smem_u32(&full[s]) & kPeerBitMask;
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * kLmStageBytes);
+            tma_load_2d_pair(a, &tm_h, bar, kb * kLmK, rt * kLmRows + rank * 128);
+            tma_load_2d_pair(a + kLmABytes, &tm_w, bar, kb * kLmK, t * kLmCols + rank * 128);
             if (++s == kLmStages) {
               s = 0;
               ph ^= 1u;
@@ -159,59 +198,61 @@ __global__ void __launch_bounds__(kLmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one thread)
-    if (lane == 0) {
+    // ---------------- MMA issuer (leader CTA, one thread)
+    if (rank == 0 && lane == 0) {
       int s = 0;
       uint32_t ph = 0;
       uint32_t it = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const int c = u % p.n_chunks;
+      for (int u = pair; u < n_units; u += npairs) {
+        int c, rt;
+        unit_coords(u, p.n_rowtiles, p.n_chunks, c, rt);
         const int t0 = chunk_tile0(c, p.n_chunks, p.n_coltiles), t1 = chunk_tile0(c + 1, p.n_chunks, p.n_coltiles);
         for (int t = t0; t < t1; ++t, ++it) {
-          mbar_wait(tempty, (it & 1u) ^ 1u);  // the epilogue has drained the accumulators
+          const uint32_t acc = it & 1u;
+          mbar_wait(&tempty[acc], ((it >> 1) & 1u) ^ 1u);  // both epilogues drained this buffer
           tc_fence_after();
+          const uint32_t d = tmem + acc * kLmCols;
           for (int kb = 0; kb < kblocks; ++kb) {
             mbar_wait(&full[s], ph);
             tc_fence_after();
             const uint32_t a = smem_u32(smem + s * kLmStageBytes);
             const uint32_t b = a + kLmABytes;
 #pragma unroll
-            for (int k = 0; k < kLmK / 16; ++k) {
-              const uint64_t bd = sw128_desc(b + k * 32);
-              umma_bf16(tmem, sw128_desc(a + k * 32), bd, (kb | k) != 0);
-              umma_bf16(tmem + kLmCols, sw128_desc(a + kLmABytes / 2 + k * 32), bd, (kb | k) != 0);
-            }
-            umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+            for (int k = 0; k < kLmK / 16; ++k)
+              umma_pair_bf16(d, sw128_desc(a + k * 32), sw128_desc(b + k * 32), (kb | k) != 0);
+            umma_commit_pair(&empty[s]);  // frees the stage in both CTAs once these MMAs have read it
             if (++s == kLmStages) {
               s = 0;
               ph ^= 1u;
             }
           }
-          umma_commit(tfull);  // accumulators complete
+          umma_commit_pair(&tfull[acc]);  // accumulators complete in both CTAs
         }
       }
     }
   } else {
-    // ---------------- epilogue: one thread per row
-    const int q = warp & 3;           // TMEM lane quadrant this warp may access
-    const int half = (warp - 2) >> 2;  // accumulator (row half of the tile)
-    const uint32_t tbase = tmem + (uint32_t(32 * q) << 16) + uint32_t(half * kLmCols);
+    // ---------------- epilogue (both CTAs): one thread per row
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const uint32_t tlane = tmem + (uint32_t(32 * q) << 16);
+    const uint32_t tempty_leader = smem_u32(&tempty[0]) & kPeerBitMask;
     const float k2 = p.k2;
     uint32_t it = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      const int rt = u / p.n_chunks, c = u % p.n_chunks;
+    for (int u = pair; u < n_units; u += npairs) {
+      int c, rt;
+      unit_coords(u, p.n_rowtiles, p.n_chunks, c, rt);
       const int t0 = chunk_tile0(c, p.n_chunks, p.n_coltiles), t1 = chunk_tile0(c + 1, p.n_chunks, p.n_coltiles);
-      const int64_t row = int64_t(rt) * kLmRows + half * 128 + q * 32 + lane;
+      const int64_t row = int64_t(rt) * kLmRows + rank * 128 + q * 32 + lane;
       const int ycol = row < p.num_rows ? p.targets[row] : -1;
       float m = -1e30f, s = 0.f, tt = 0.f, zy = -INFINITY;
       for (int t = t0; t < t1; ++t, ++it) {
-        mbar_wait(tfull, it & 1u);
+        const uint32_t acc = it & 1u;
+        mbar_wait(&tfull[acc], (it >> 1) & 1u);
         tc_fence_after();
         const int64_t col_t = int64_t(t) * kLmCols;
 #pragma unroll 1
         for (int cc = 0; cc < kLmCols / 32; ++cc) {
           float v[32];
-          tmem_ld32(tbase + uint32_t(cc * 32), v);
+          tmem_ld32(tlane + acc * kLmCols + uint32_t(cc * 32), v);
           const int64_t col0 = col_t + cc * 32;
           const int64_t rem = p.vocab - col0;
           const int nvalid = rem < 32 ? int(rem) : 32;
@@ -243,18 +284,18 @@ __global__ void __launch_bounds__(kLmThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty);
+        if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
       }
       if (row < p.num_rows)
         p.partials[int64_t(c) * p.num_rows + row] = make_float4(m, s, tt, zy == -INFINITY ? -INFINITY : zy - m);
     }
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // every MMA consumed and every remote arrive delivered before TMEM is released
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc_pair(tmem, 512);
   }
 }
 
@@ -286,17 +327,18 @@ bool make_map(CUtensorMap* map, const void* base, int64_t rows, int d, int box_r
 }  // namespace
 
 int lmhead_chunks(int64_t num_rows, int64_t vocab, int num_sms) {
-  // vocab chunks per row tile: enough units for whole waves of the persistent grid (ties: fewer chunks)
+  // vocab chunks: enough (row tile, chunk) units for whole waves of the persistent CTA pairs, chunks of
+  // nearly equal tile counts (ties: fewer chunks)
   const int64_t rt = (num_rows + kLmRows - 1) / kLmRows;
   const int64_t nt = (vocab + kLmCols - 1) / kLmCols;
+  const int64_t pairs = std::max(1, num_sms / 2);
   int best = 1;
   double best_eff = 0.0;
-  for (int c = 1; c <= std::min<int64_t>(nt, 64); ++c) {
+  for (int c = 1; c <= std::min<int64_t>(nt, 256); ++c) {
     const int64_t units = rt * c;
-    const int64_t waves = (units + num_sms - 1) / num_sms;
-    // the largest unit has ceil(nt / c) tiles: time ~ waves * ceil(nt/c); work = rt * nt tiles
-    const double t = double(waves) * double((nt + c - 1) / c);
-    const double eff = double(rt * nt) / (t * num_sms);
+    const int64_t waves = (units + pairs - 1) / pairs;
+    const double t = double(waves) * double((nt + c - 1) / c);  // the largest unit has ceil(nt / c) tiles
+    const double eff = double(rt * nt) / (t * pairs);
     if (eff > best_eff + 1e-6) {
       best_eff = eff;
       best = c;
@@ -309,7 +351,7 @@ cudaError_t launch_lmhead_fwd(const otk_ctx* ctx, int64_t num_rows, int64_t voca
                               const void* weight, const int32_t* targets, float logit_scale, float4* partials,
                               int n_chunks, cudaStream_t s) {
   CUtensorMap th, tw;
-  if (!make_map(&th, hidden, num_rows, d, kLmRows) || !make_map(&tw, weight, vocab, d, kLmCols))
+  if (!make_map(&th, hidden, num_rows, d, 128) || !make_map(&tw, weight, vocab, d, 128))
     return cudaErrorInvalidValue;
   LmParams p;
   p.num_rows = num_rows;
@@ -328,8 +370,21 @@ cudaError_t launch_lmhead_fwd(const otk_ctx* ctx, int64_t num_rows, int64_t voca
     attr = true;
   }
   const int units = p.n_rowtiles * p.n_chunks;
-  const int grid = std::min(units, ctx->num_sms);
-  k_lmhead_fwd<<<grid, kLmThreads, kLmSmemBytes, s>>>(th, tw, p);
+  const int pairs = std::max(1, std::min(units, ctx->num_sms / 2));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(2 * pairs), 1, 1);
+  cfg.blockDim = dim3(kLmThreads, 1, 1);
+  cfg.dynamicSmemBytes = kLmSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr2[1];
+  attr2[0].id = cudaLaunchAttributeClusterDimension;
+  attr2[0].val.clusterDim.x = 2;
+  attr2[0].val.clusterDim.y = 1;
+  attr2[0].val.clusterDim.z = 1;
+  cfg.attrs = attr2;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_lmhead_fwd, th, tw, p);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
