@@ -27,6 +27,9 @@ for V, dtype in ((151936, "bf16"), (1000, "f32")):
     otk.otk_sample_tokens(ctx, lg, u)
     otk.otk_sample_tokens(ctx, lg, greedy=True)
     otk.otk_sample_tokens(ctx, lg[:3].contiguous(), u[:3].contiguous())   # clustered rows
+from synth import make_lmhead
+h, w, y = make_lmhead(300, 1000, 128, seed=4, device="cuda")
+otk.otk_lmhead_logprob_fwd(ctx, h, w, y)
 torch.cuda.synchronize()
 ctx.check()
 print("sanitize ok")
