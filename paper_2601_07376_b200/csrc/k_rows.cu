@@ -667,9 +667,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
         if (p.ref_logp) ref_n = p.ref_logp[row];
       }
     }
+    // the target logit, read straight from HBM (one sector per row), one row ahead: issued once the next
+    // row's target has arrived (after this row's pass 1), consumed by the next row's finalize
+    auto xy_of = [&](int64_t r, int32_t yy) -> float {
+      const int64_t g = int64_t(yy) - p.vocab_start;
+      return (g >= 0 && g < p.vocab) ? VT::load1(p.logits, r * p.ld + g) : 0.f;
+    };
+    float xy_n = (row < p.num_rows && row_active(p, y_n, m_n)) ? xy_of(row, y_n) : 0.f;
     for (; row < p.num_rows; row += ngroups) {
       const int32_t y = y_n;
       const uint8_t m = m_n;
+      const float xy = xy_n;
       RowSide sd{0.0, old_n, ref_n, 0};
       const int32_t rt = rt_n;
       const int64_t nrow = row + ngroups;
@@ -684,6 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       }
       if (!row_active(p, y, m)) {
         inactive_row<T, MODE>(p, row, ct, crank, c0, segn, m != 0);
+        if (nrow < p.num_rows && row_active(p, y_n, m_n)) xy_n = xy_of(nrow, y_n);
         continue;
       }
       const int64_t ylc64 = int64_t(y) - p.vocab_start - c0;  // target column local to this CTA's segment
@@ -692,10 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
         sd.A = p.adv[p.adv_index ? p.adv_index[row] : rt];
         if (p.reduction != OTK_TOKEN_MEAN) sd.nb = p.traj_tokens[rt];
       }
-      // the target logit, read straight from HBM (one sector per row; in flight during pass 1)
       const int64_t yg = int64_t(y) - p.vocab_start;
-      const float xy = (yg >= 0 && yg < p.vocab)
-                           ? VT::load1(p.logits, row * p.ld + yg) : 0.f;
 
       // ---------------- pass 1: online max / sum 2^(y-m) / sum 2^(y-m)(y-m), one exponential per element
       const int owner_ct = ylc >= 0 ? ((ylc % CE) / EV) % kNCT : -1;  // thread that stores the target column
@@ -769,6 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       };
       for (int c = 0; c < nch - 1; ++c) chunk1(c, std::false_type{});
       if (nch > 0) chunk1(nch - 1, std::true_type{});
+      if (nrow < p.num_rows && row_active(p, y_n, m_n)) xy_n = xy_of(nrow, y_n);
       const Stat st{mref, f2_sum(rS), f2_sum(rT)};
       if (kBwd) tmem_wait_st();
 
