@@ -132,7 +132,8 @@ def test_advantage_closed_forms_and_errors(otk, ctx):
 # ------------------------------------------------------------------------------------------ (3) forward
 @pytest.mark.parametrize("V,ld,dtype,n", [(1024, 1024, "f32", 256), (1000, 1008, "bf16", 300), (4096, 4096, "bf16", 513),
                                           (151936, 151936, "bf16", 160), (33001, 33008, "bf16", 97),
-                                          (151936, 151936, "f32", 40), (2, 8, "bf16", 33), (3, 4, "f32", 17)])
+                                          (151936, 151936, "f32", 40), (2, 8, "bf16", 33), (3, 4, "f32", 17),
+                                          (262144, 262144, "bf16", 40), (300000, 300000, "f32", 12)])
 def test_logprob_entropy_fwd(otk, ctx, V, ld, dtype, n):
     d, h = row_problem(n, V, dtype=dtype, ld=ld, seed=V + n, uniform_rows=(3,))
     rm = d["mask"] if n % 2 else None
@@ -158,6 +159,8 @@ CASES = [
     (33001, 33008, "bf16", 120, 0.0, 3, 1.0, False),
     (151936, 151936, "bf16", 150, 0.04, 3, 1.0, True),
     (151936, 151936, "f32", 24, 0.04, 3, 1 / 0.7, True),
+    (262144, 262144, "bf16", 40, 0.04, 3, 1.0, True),     # 4-CTA clusters (Gemma-class vocabulary)
+    (300000, 300000, "f32", 10, 0.04, 3, 1.0, True),      # 8-CTA clusters
 ]
 
 

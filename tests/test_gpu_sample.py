@@ -61,7 +61,8 @@ def _check_sampled(tok, lp, wide, u, s, dtype, rows):
 
 @pytest.mark.parametrize("dtype,V,ld,n,scale", [("bf16", 151936, 151936, 384, 1.0), ("bf16", 151936, 151936, 300, 0.7),
                                                 ("f32", 1000, 1000, 300, 1.0), ("bf16", 4100, 4104, 200, 1.3),
-                                                ("bf16", 17, 24, 64, 1.0), ("f32", 50000, 50004, 64, 2.0)])
+                                                ("bf16", 17, 24, 64, 1.0), ("f32", 50000, 50004, 64, 2.0),
+                                                ("bf16", 262144, 262144, 64, 1.0)])
 def test_sample_tokens_vs_oracle(otk, ctx, dtype, V, ld, n, scale):
     logits, _ = make_logits(n, V, ld=ld if ld != V else None, dtype=dtype, seed=V % 977 + n, device="cpu")
     wide = logits.double().numpy()[:, :V]
