@@ -6,6 +6,7 @@ import numpy as np, torch
 import paper_2601_07376_b200 as otk
 from synth import make_batch, make_logits, make_noise
 ap = argparse.ArgumentParser(); ap.add_argument("--rows", type=int, default=65536); ap.add_argument("--iters", type=int, default=10); ap.add_argument("--mask", default="data", choices=["data", "ones", "zeros"])
+ap.add_argument("--variant", default="", help="NEXT-4 loss variant: ent | dual | seqmean | seqsum | sft | turn")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 ctx = otk.Context(0)
@@ -25,9 +26,19 @@ if a.mask == "ones": lm.fill_(1)
 if a.mask == "zeros": lm.fill_(0)
 ntr = int(lm.sum())
 alg = ntr * (4 * V + 21) + (n - ntr) * (2 * V + 1)
+kw = dict(ent=dict(ent_coef=0.01), dual=dict(dual_clip=3.0), seqmean=dict(reduction=1), seqsum=dict(reduction=2),
+          sft=dict(sft=True)).get(a.variant, {})
+cfg = otk.LossCfg(**kw, traj_loss_tokens=m["traj_loss_tokens"], n_active_traj=m["n_active_traj"])
+adv_use = adv
+if a.variant == "turn":   # turn-level credit: A read per row through the row's segment
+    mt = otk.otk_build_masks(ctx, db, row_seg=True)
+    tr = otk.otk_turn_returns(ctx, db, tb.num_segments, torch.from_numpy(tb.group_id).cuda(),
+                              torch.from_numpy(tb.turn_offsets).cuda(), torch.from_numpy(tb.turn_rewards).cuda(), 0.9)
+    adv_use = otk.otk_group_advantages(ctx, tr["seg_group"], 64, returns=tr["seg_return"], skip_ungrouped=True)["adv"]
+    cfg = otk.LossCfg(adv_index=mt["row_seg"][:n].clone())
 def run(k):
     lg, tg = bufs[k % 2]; o, r = olds[k % 2]
-    otk.otk_policy_loss_fwd_bwd(ctx, lg, tg, lm, rt, adv, o, r, m["n_loss"], otk.LossCfg(), dlogits=dl, want_logp=False)
+    otk.otk_policy_loss_fwd_bwd(ctx, lg, tg, lm, rt, adv_use, o, r, m["n_loss"], cfg, dlogits=dl, want_logp=False)
 def runf(k):
     lg, tg = bufs[k % 2]
     otk.otk_logprob_entropy_fwd(ctx, lg, tg)
@@ -42,4 +53,4 @@ for name, fn, by in (("bwd", run, alg), ("fwd", runf, n * (2 * V + 12))):
     ms = ev[0].elapsed_time(ev[1]) / a.iters
     res[name] = dict(ms=round(ms, 4), GBps=round(by / ms / 1e6, 1), frac=round(by / ms / 1e6 / 6532.2, 4))
 ctx.check()
-print(json.dumps(dict(lib=os.environ.get("OTK_LIB", "default"), mask=a.mask, ntr=ntr, **res)))
+print(json.dumps(dict(lib=os.environ.get("OTK_LIB", "default"), mask=a.mask, variant=a.variant or "default", ntr=ntr, **res)))
