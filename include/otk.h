@@ -300,7 +300,8 @@ otk_status otk_sample_tokens(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int6
  * 16-byte aligned. GEMM on the tcgen05 tensor cores with fp32 accumulation in TMEM; the log-softmax
  * statistics are folded in the epilogue. workspace: device scratch of otk_lmhead_workspace_bytes()
  * bytes (per-row partials of each vocab chunk), caller-owned. Outputs as in (3) (row_mask NULL = all
- * rows; masked rows get 0). Tolerance vs the float64 oracle on the same bf16 h and W: 2e-3 abs.
+ * rows; masked rows get 0). A target outside [0, vocab) on an unmasked row sets OTK_ERR_TARGET_RANGE
+ * (that row's logp is -inf). Tolerance vs the float64 oracle on the same bf16 h and W: 2e-3 abs.
  * ------------------------------------------------------------------------------------------- */
 int64_t otk_lmhead_workspace_bytes(const otk_ctx* ctx, int64_t num_rows, int64_t vocab);
 otk_status otk_lmhead_logprob_fwd(otk_ctx* ctx, int64_t num_rows, int64_t hidden_dim, int64_t vocab,

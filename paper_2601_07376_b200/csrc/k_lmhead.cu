@@ -49,8 +49,10 @@ struct LmParams {
   int n_chunks;          // vocab chunks
   int n_coltiles;        // ceil(vocab / 256)
   const int32_t* targets;
+  const uint8_t* row_mask;  // NULL = all rows
   float k2;              // logit_scale * log2(e)
   float4* partials;      // [n_chunks][num_rows]
+  int* err;
 };
 
 // ---- PTX wrappers specific to the tensor-core path -------------------------------------------------
@@ -243,6 +245,8 @@ __global__ void __launch_bounds__(kLmThreads, 1)
       const int t0 = chunk_tile0(c, p.n_chunks, p.n_coltiles), t1 = chunk_tile0(c + 1, p.n_chunks, p.n_coltiles);
       const int64_t row = int64_t(rt) * kLmRows + rank * 128 + q * 32 + lane;
       const int ycol = row < p.num_rows ? p.targets[row] : -1;
+      if (c == 0 && row < p.num_rows && (!p.row_mask || p.row_mask[row]) && (ycol < 0 || ycol >= p.vocab))
+        set_error(p.err, OTK_ERR_TARGET_RANGE);  // such a row's logp is -inf
       float m = -1e30f, s = 0.f, tt = 0.f, zy = -INFINITY;
       for (int t = t0; t < t1; ++t, ++it) {
         const uint32_t acc = it & 1u;
@@ -302,14 +306,15 @@ __global__ void __launch_bounds__(kLmThreads, 1)
 // ---- host side -----------------------------------------------------------------------------------------
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  // resolved once (thread-safe static initialisation) through the runtime, so libotk needs no -lcuda
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
     cudaDriverEntryPointQueryResult q;
     void* f = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    return nullptr;
+  }();
   return fn;
 }
 
@@ -348,8 +353,8 @@ int lmhead_chunks(int64_t num_rows, int64_t vocab, int num_sms) {
 }
 
 cudaError_t launch_lmhead_fwd(const otk_ctx* ctx, int64_t num_rows, int64_t vocab, int d, const void* hidden,
-                              const void* weight, const int32_t* targets, float logit_scale, float4* partials,
-                              int n_chunks, cudaStream_t s) {
+                              const void* weight, const int32_t* targets, const uint8_t* row_mask, float logit_scale,
+                              float4* partials, int n_chunks, cudaStream_t s) {
   CUtensorMap th, tw;
   if (!make_map(&th, hidden, num_rows, d, 128) || !make_map(&tw, weight, vocab, d, 128))
     return cudaErrorInvalidValue;
@@ -361,14 +366,13 @@ cudaError_t launch_lmhead_fwd(const otk_ctx* ctx, int64_t num_rows, int64_t voca
   p.n_chunks = n_chunks;
   p.n_coltiles = int((vocab + kLmCols - 1) / kLmCols);
   p.targets = targets;
+  p.row_mask = row_mask;
+  p.err = ctx->d_err;
   p.k2 = logit_scale * 1.4426950408889634f;
   p.partials = partials;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_lmhead_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kLmSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  // per launch (cheap, and correct for every device of the process)
+  cudaError_t ea = cudaFuncSetAttribute(k_lmhead_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kLmSmemBytes);
+  if (ea != cudaSuccess) return ea;
   const int units = p.n_rowtiles * p.n_chunks;
   const int pairs = std::max(1, std::min(units, ctx->num_sms / 2));
   cudaLaunchConfig_t cfg = {};

@@ -414,10 +414,9 @@ __global__ void __launch_bounds__(kSampleThreads, OTK_SAMPLE_MINB) k_sample(cons
   if (kCl) cluster_sync_all();  // no CTA exits while a peer may still read its s_cta
 }
 
-namespace {
-int sample_occupancy(int dtype) {
-  static int occ[2] = {0, 0};
-  int& o = occ[dtype == OTK_BF16 ? 0 : 1];
+// resident CTAs per SM of the clustered variant (the launch shape depends on it); cached in the ctx
+int sample_occupancy(otk_ctx* ctx, int dtype) {
+  int& o = ctx->sample_occ[dtype == OTK_BF16 ? 0 : 1];
   if (o == 0) {
     int a = 0;
     if (dtype == OTK_BF16)
@@ -428,11 +427,10 @@ int sample_occupancy(int dtype) {
   }
   return o;
 }
-}  // namespace
 
-cudaError_t launch_sample(const SampleParams& p0, int dtype, int num_sms, cudaStream_t s) {
+cudaError_t launch_sample(otk_ctx* ctx, const SampleParams& p0, int dtype, cudaStream_t s) {
   SampleParams p = p0;
-  const int64_t slots = int64_t(num_sms) * sample_occupancy(dtype);
+  const int64_t slots = int64_t(ctx->num_sms) * sample_occupancy(ctx, dtype);
   // cluster size: when rows are few, as many CTAs per row as fit in ONE wave of resident CTAs; one CTA
   // per row otherwise (a cluster barrier per row costs more than the last wave's imbalance)
   const int best_c = int(std::min<int64_t>(kSampleMaxCluster, std::max<int64_t>(1, slots / p.num_rows)));

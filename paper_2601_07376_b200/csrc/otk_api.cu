@@ -343,7 +343,7 @@ otk_status otk_sample_tokens(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int6
   p.tokens = tokens;
   p.logp = logp;
   p.err = ctx->d_err;
-  OTK_CUDA(otk::launch_sample(p, dtype, ctx->num_sms, reinterpret_cast<cudaStream_t>(stream)), "k_sample launch");
+  OTK_CUDA(otk::launch_sample(ctx, p, dtype, reinterpret_cast<cudaStream_t>(stream)), "k_sample launch");
   ctx->launches += 1;
   return OTK_OK;
 }
@@ -374,8 +374,8 @@ otk_status otk_lmhead_logprob_fwd(otk_ctx* ctx, int64_t num_rows, int64_t hidden
               "workspace smaller than otk_lmhead_workspace_bytes()");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   float4* part = reinterpret_cast<float4*>(workspace);
-  OTK_CUDA(otk::launch_lmhead_fwd(ctx, num_rows, vocab, int(hidden_dim), hidden, weight, targets, logit_scale, part,
-                                  n_chunks, s),
+  OTK_CUDA(otk::launch_lmhead_fwd(ctx, num_rows, vocab, int(hidden_dim), hidden, weight, targets, row_mask,
+                                  logit_scale, part, n_chunks, s),
            "k_lmhead_fwd launch");
   ctx->launches += 1;
   OTK_CUDA(otk::launch_combine(ctx, num_rows, n_chunks, part, row_mask, logp, entropy, lse, s), "k_combine launch");

@@ -23,6 +23,7 @@ struct otk_ctx {
   cudaStream_t exec_stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t launches = 0;
+  int sample_occ[2] = {0, 0};      // k_sample resident CTAs per SM (bf16, fp32), queried on first use
 };
 
 namespace otk {
@@ -157,12 +158,12 @@ struct SampleParams {
   float* logp;
   int* err;
 };
-cudaError_t launch_sample(const SampleParams& p, int dtype, int num_sms, cudaStream_t s);
+cudaError_t launch_sample(otk_ctx* ctx, const SampleParams& p, int dtype, cudaStream_t s);
 
 int lmhead_chunks(int64_t num_rows, int64_t vocab, int num_sms);
 cudaError_t launch_lmhead_fwd(const otk_ctx* ctx, int64_t num_rows, int64_t vocab, int d, const void* hidden,
-                              const void* weight, const int32_t* targets, float logit_scale, float4* partials,
-                              int n_chunks, cudaStream_t s);
+                              const void* weight, const int32_t* targets, const uint8_t* row_mask, float logit_scale,
+                              float4* partials, int n_chunks, cudaStream_t s);
 
 __device__ __forceinline__ void set_error(int* err, int code) { atomicCAS(err, 0, code); }
 

@@ -62,3 +62,13 @@ def test_lmhead_validation(otk, ctx):
     h, w, y = make_lmhead(8, 100, 96, seed=1)     # hidden_dim not a multiple of 64
     with pytest.raises(otk.OtkError):
         otk.otk_lmhead_logprob_fwd(ctx, h.cuda(), w.cuda(), y.cuda())
+    h, w, y = make_lmhead(8, 100, 64, seed=1)
+    y[3] = 100                                     # target out of range on an unmasked row
+    otk.otk_lmhead_logprob_fwd(ctx, h.cuda(), w.cuda(), y.cuda())
+    with pytest.raises(otk.OtkError) as e:
+        ctx.check()
+    assert e.value.status == 8                     # OTK_ERR_TARGET_RANGE
+    mask = torch.ones(8, dtype=torch.uint8)
+    mask[3] = 0                                    # ... but not when the row is masked
+    otk.otk_lmhead_logprob_fwd(ctx, h.cuda(), w.cuda(), y.cuda(), row_mask=mask.cuda())
+    ctx.check()
