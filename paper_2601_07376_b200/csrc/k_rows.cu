@@ -288,6 +288,10 @@ struct Smem {
   uint64_t xbar[2];
   float4 xrecv[2][8];                 // peer partials, double-buffered by active-row parity
   float4 wred[2][kConsumerWarps];     // warp partials, double-buffered by active-row parity
+  // FWD / PARTIAL: warp partials handed to the finalizer warp through a ring of kFinSlots rows
+  uint64_t ffull[4];                  // all consumer warps wrote slot k (count kConsumerWarps)
+  uint64_t fempty[4];                 // the finalizer has read slot k (count 1)
+  float4 fred[4][kConsumerWarps];
   float4 rowbc[2];                    // (stream kernel) row broadcast
   uint32_t tmem_base;
 };
@@ -520,6 +524,10 @@ __device__ __forceinline__ void row_kernel_setup(Smem& S, uint8_t* zero, int war
     }
     mbar_init(&S.xbar[0], 1);
     mbar_init(&S.xbar[1], 1);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&S.ffull[i], kConsumerWarps);
+      mbar_init(&S.fempty[i], 1);
+    }
     fence_mbar_init();
   }
   for (int i = threadIdx.x; i < kZeroBytes / 16; i += blockDim.x)
@@ -597,6 +605,96 @@ __device__ __forceinline__ void row_total(Smem& S, Stat st, int lane, int cw, in
   }
 }
 
+// FWD / PARTIAL finalizer (warp kConsumerWarps + 1, idle in these modes otherwise): takes each active row's 12
+// warp partials from the fred ring, reduces them exactly as row_total does (same order, same rounded ops, so
+// logp is bitwise equal to the BWD kernel's), exchanges with the cluster peers and writes the row's outputs.
+// The consumer warps therefore never wait for a row's reduction: they hand off their partial and stream on.
+template <typename T, int MODE>
+__device__ __forceinline__ void finalize_rows(const RowParams& p, Smem& S, int lane, int csize, uint32_t crank,
+                                              int64_t group, int64_t ngroups) {
+  using VT = Vec<T>;
+  const float s2 = __fmul_rn(p.scale, kLog2e);
+  uint32_t fs = 0, fph = 0, q = 0;
+  int64_t row = group;
+  int32_t y_n = 0;
+  uint8_t m_n = 0;
+  if (row < p.num_rows) {
+    y_n = p.targets[row];
+    m_n = p.mask ? p.mask[row] : 1;
+  }
+  auto xy_of = [&](int64_t r, int32_t yy) -> float {
+    const int64_t g = int64_t(yy) - p.vocab_start;
+    return (g >= 0 && g < p.vocab) ? VT::load1(p.logits, r * p.ld + g) : 0.f;
+  };
+  float xy_n = (row < p.num_rows && row_active(p, y_n, m_n)) ? xy_of(row, y_n) : 0.f;
+  for (; row < p.num_rows; row += ngroups) {
+    const int32_t y = y_n;
+    const uint8_t m = m_n;
+    const float xy = xy_n;
+    const int64_t nrow = row + ngroups;
+    if (nrow < p.num_rows) {
+      y_n = p.targets[nrow];
+      m_n = p.mask ? p.mask[nrow] : 1;
+    }
+    if (!row_active(p, y, m)) {  // the consumers wrote this row's zeros
+      if (nrow < p.num_rows && row_active(p, y_n, m_n)) xy_n = xy_of(nrow, y_n);
+      continue;
+    }
+    mbar_wait(&S.ffull[fs], fph);
+    Stat mine{-INFINITY, 0.f, 0.f};
+    if (lane < kConsumerWarps) {
+      const float4 w = S.fred[fs][lane];
+      mine = Stat{w.x, w.y, w.z};
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.fempty[fs]);
+    if (++fs == 4) {
+      fs = 0;
+      fph ^= 1u;
+    }
+    if (nrow < p.num_rows && row_active(p, y_n, m_n)) xy_n = xy_of(nrow, y_n);
+    const Stat r = warp_reduce(mine);
+    Stat tot;
+    const uint32_t par = q & 1u;
+    if (csize > 1) {
+      if (lane == 0) {
+        for (int dst = 0; dst < csize; ++dst) {
+          if (dst == int(crank)) continue;
+          st_async_f4(mapa(smem_u32(&S.xrecv[par][crank]), dst), r.m, r.s, r.t, 0.f, mapa(smem_u32(&S.xbar[par]), dst));
+        }
+        mbar_arrive_expect_tx(&S.xbar[par], 16u * uint32_t(csize - 1));
+      }
+      mbar_wait(&S.xbar[par], (q >> 1) & 1u);
+      if (csize == 2) {
+        const float4 P = S.xrecv[par][crank ^ 1u];
+        const Stat peer{P.x, P.y, P.z};
+        tot = crank == 0 ? combine(r, peer) : combine(peer, r);
+      } else {
+        tot = Stat{-INFINITY, 0.f, 0.f};
+        for (int k = 0; k < csize; ++k) {
+          const float4 P = (k == int(crank)) ? make_float4(r.m, r.s, r.t, 0.f) : S.xrecv[par][k];
+          tot = combine(tot, Stat{P.x, P.y, P.z});
+        }
+      }
+    } else {
+      tot = r;
+    }
+    const int64_t yg = int64_t(y) - p.vocab_start;
+    const float dy = (yg >= 0 && yg < p.vocab) ? __fmaf_rn(xy, s2, -tot.m) : -INFINITY;
+    if (lane == 0 && crank == 0) {
+      if (MODE == kModePartial) {
+        p.partials_out[row] = make_float4(tot.m, tot.s, tot.t, dy);
+      } else {
+        const RowStats rs = finalize(tot, dy);
+        p.logp[row] = rs.logp;
+        if (p.entropy) p.entropy[row] = rs.H;
+        if (p.lse) p.lse[row] = rs.lse;
+      }
+    }
+    ++q;
+  }
+}
+
 // =====================================================================================================
 // k_rows_tm: FWD / PARTIAL / BWD. Pass 1 streams each chunk from the ring exactly once (slot released
 // right away); for BWD the exponentials e = 2^(y - m_c) (bf16 for bf16 input, with m_c the thread's
@@ -634,7 +732,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
     if (lane == 0 && nch > 0) load_rows<T>(p, ring, S, group, ngroups, c0, seg_bytes, nch);
     __syncwarp();
   } else if (warp == kConsumerWarps + 1) {
-    if (kBwd && lane == 0) zero_rows<T>(p, zero, group, ngroups, c0, segn);
+    if (kBwd) {
+      if (lane == 0) zero_rows<T>(p, zero, group, ngroups, c0, segn);
+    } else {
+      finalize_rows<T, MODE>(p, S, lane, csize, crank, group, ngroups);
+    }
     __syncwarp();
   } else {
     const int ct = threadIdx.x - 32;
@@ -653,6 +755,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       if (p.reduction != OTK_TOKEN_MEAN) nact = *p.n_active;
     }
     uint32_t slot = 0, phase = 0, q = 0;
+    uint32_t fs = 0, fph = 0;  // FWD / PARTIAL: hand-off ring to the finalizer warp
 
     int64_t row = group;
     int32_t y_n = 0, rt_n = 0;
@@ -777,6 +880,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       if (nch > 0) chunk1(nch - 1, std::true_type{});
       if (nrow < p.num_rows && row_active(p, y_n, m_n)) xy_n = xy_of(nrow, y_n);
       const Stat st{mref, f2_sum(rS), f2_sum(rT)};
+      if (!kBwd) {  // hand the warp partial to the finalizer and stream on (no per-row barrier)
+        const Stat wst = warp_reduce(st);
+        if (lane == 0) {
+          mbar_wait(&S.fempty[fs], fph ^ 1u);
+          S.fred[fs][cw] = make_float4(wst.m, wst.s, wst.t, 0.f);
+          mbar_arrive(&S.ffull[fs]);
+        }
+        if (++fs == 4) {
+          fs = 0;
+          fph ^= 1u;
+        }
+        continue;
+      }
       if (kBwd) tmem_wait_st();
 
       Stat tot;
