@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-next", action="store_true",
+                    help="skip the side measurements of the forward (3) and the SURVEY.md §8(f) rows")
     ap.add_argument("--shard", default="batch", choices=["batch", "vocab"],
                     help="batch: each rank owns whole trajectories (weak scaling); vocab: each rank owns V/N "
                          "columns of every row (strong scaling, row partials all-gathered)")
@@ -311,6 +313,11 @@ def run_otk(args):
         res["e2e"] = e2e(args, W, world, step, cfg)
     if rank == 0 and not args.no_cpu_baseline and not vocab_mode:
         res["cpu_baseline"] = cpu_baseline(args, W, cfg)
+    if rank == 0 and world == 1 and not args.no_next and not vocab_mode:
+        try:
+            res["other_kernels"] = other_kernels(W)
+        except Exception as e:  # side measurements never invalidate the headline line
+            res["other_kernels"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         print(json.dumps(res), flush=True)
     if pg is not None:
@@ -320,6 +327,60 @@ def run_otk(args):
 
 
 # ------------------------------------------------------------------------------------------------
+def other_kernels(W):
+    """Side measurements (untimed for the headline, rank 0, N = 1): the forward (3) on one micro-batch, the
+    rollout sampler (NEXT-3) on a 4096-row decode batch and the fused LM-head forward (NEXT-1) at d = 3584 —
+    CUDA events on the launching stream, inputs HBM-resident, each against its own roofline."""
+    otk, ctx, V = W["otk"], W["ctx"], W["V"]
+    hbm, _ = peaks()
+    bf16_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 2250.0
+    bufs, tgts = W["bufs"], W["tgts"]
+
+    def timed(fn, iters):
+        for i in range(2):
+            fn(i)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(iters):
+            fn(i)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / iters
+
+    out = {}
+    M = bufs[0].shape[0]
+    ms = timed(lambda i: otk.otk_logprob_entropy_fwd(ctx, bufs[i % len(bufs)], tgts[i % len(tgts)]), 4)
+    gbs = M * (2 * V + 12) / ms / 1e6
+    out["logprob_entropy_fwd"] = {"rows": M, "ms": ms, "GBps": gbs, "frac_hbm": gbs / hbm,
+                                  "kernel": "k_rows_tm<bf16,FWD> (north_star (3))"}
+    n = 4096
+    u = torch.rand(n, device=bufs[0].device)
+    for mode in ("sample", "greedy"):
+        # row windows 4096 apart across the cycled buffers: no L2 reuse between iterations
+        ms = timed(lambda i: otk.otk_sample_tokens(
+            ctx, bufs[i % len(bufs)][(i * n) % (M - n):(i * n) % (M - n) + n], u, greedy=mode == "greedy"), 8)
+        gbs = n * (2 * V + 12) / ms / 1e6
+        out[f"sample_tokens_{mode}"] = {"rows": n, "us": ms * 1e3, "GBps": gbs, "frac_hbm": gbs / hbm,
+                                        "kernel": "k_sample (SURVEY.md §8(f) NEXT-3)"}
+    from synth import make_lmhead
+    rows, d = 8192, 3584
+    h, w, y = make_lmhead(rows, V, d, seed=1, device=bufs[0].device)
+    ws = [None]
+
+    def lm(i):
+        o = otk.otk_lmhead_logprob_fwd(ctx, h, w, y, workspace=ws[0])
+        ws[0] = o["workspace"]
+    ms = timed(lm, 3)
+    tf = 2.0 * rows * V * d / ms / 1e9
+    out["lmhead_logprob_fwd"] = {"rows": rows, "hidden_dim": d, "ms": ms, "TFLOPs": tf, "frac_bf16": tf / bf16_peak,
+                                 "kernel": "k_lmhead_fwd (tcgen05 cta_group::2; SURVEY.md §8(f) NEXT-1 fwd)"}
+    del h, w, y, ws
+    ctx.check()
+    return out
+
+
 def e2e(args, W, world, step, cfg):
     """Same metric through the C-ABI host-buffer entry point (otk_policy_loss_fwd_bwd_host): every
     micro-batch's logits + side arrays are copied H2D from pinned host memory inside the timed region
