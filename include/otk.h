@@ -303,7 +303,7 @@ otk_status otk_sample_tokens(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int6
  * rows; masked rows get 0). A target outside [0, vocab) on an unmasked row sets OTK_ERR_TARGET_RANGE
  * (that row's logp is -inf). Tolerance vs the float64 oracle on the same bf16 h and W: 2e-3 abs.
  * ------------------------------------------------------------------------------------------- */
-int64_t otk_lmhead_workspace_bytes(const otk_ctx* ctx, int64_t num_rows, int64_t vocab);
+int64_t otk_lmhead_workspace_bytes(const otk_ctx* ctx, int64_t num_rows, int64_t vocab); /* -1: bad args */
 otk_status otk_lmhead_logprob_fwd(otk_ctx* ctx, int64_t num_rows, int64_t hidden_dim, int64_t vocab,
                                   const void* hidden, const void* weight, const int32_t* targets,
                                   const uint8_t* row_mask, float logit_scale, void* workspace,

@@ -28,9 +28,15 @@ Pins (tests/test_oracle_pins.py, -m "not gpu"): SPEC.md's ARITH worked example f
 segment enumeration, closed-form binary-group advantages, constant-group zero, zero-sum
 antisymmetry, uniform / two-level / V=2 rows for O3, torch float64 log_softmax
 (library routine), old=new and clip closed forms, k3 values, central finite differences of the
-loss for the gradient, and the SFT case against torch float64 cross_entropy autograd.
+loss for the gradient, and the SFT case against torch float64 cross_entropy autograd; loss variants
+(dual-clip / sequence-mean closed forms, entropy bonus vs torch autograd, finite differences); O6:
+hand-worked reward-to-go, agent views, the Bellman recursion, reduction to trajectory-level GRPO,
+a hand-worked group and per-group mean 0 / std 1; O7: SPEC.md greedy examples, V=2 closed form,
+uniform row = floor(uV), exactly-rounded prefix brute force, empirical frequencies, temperature;
+O8: W = 0 (uniform), one-hot h (reduces to O3), torch float64 matmul + log_softmax.
 Parity unpinned: none of the functions; the CHOICE among readings R2, R14-R16 (std estimator,
-clip epsilon, ratio clamp, KL estimator) cannot be pinned to anything the paper prints.
+clip epsilon, ratio clamp, KL estimator), R31 (turn units and discounting) and R32 (inverse transform
+as the sampling scheme) cannot be pinned to anything the paper prints.
 """
 from __future__ import annotations
 
