@@ -28,6 +28,8 @@
  *    out of range) set the ctx's sticky device error word; the offending rows / trajectories are then
  *    treated as loss-masked so kernels stay memory-safe; otk_ctx_check reports the first such error.
  *  - Outputs never alias inputs. A ctx may be used from one stream at a time (its scratch is shared).
+ *  - num_rows == 0 is valid: per-row arrays may then be NULL and nothing is launched, except by
+ *    otk_policy_loss_fwd_bwd, which still writes its (zero) stats unless cfg->accumulate_stats.
  *  - Layout: logits / dlogits are row-major [num_rows, ld] with ld >= vocab and ld * sizeof(dtype) a
  *    multiple of 16 bytes, base pointer 16-byte aligned. Row j's logits score target j (the caller
  *    shifts; R7). Only columns [0, vocab) are read or written.

@@ -58,7 +58,7 @@ otk_status check_rows(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld,
   OTK_REQUIRE(ctx, OTK_ERR_INVALID_ARG, "ctx is NULL");
   OTK_REQUIRE(dtype == OTK_BF16 || dtype == OTK_F32, OTK_ERR_DTYPE, "unknown dtype");
   OTK_REQUIRE(num_rows >= 0 && vocab >= 1 && ld >= vocab, OTK_ERR_SHAPE, "need num_rows >= 0, vocab >= 1, ld >= vocab");
-  OTK_REQUIRE(logits && targets, OTK_ERR_INVALID_ARG, "logits / targets is NULL");
+  OTK_REQUIRE(num_rows == 0 || (logits && targets), OTK_ERR_INVALID_ARG, "logits / targets is NULL");
   OTK_REQUIRE(aligned16(logits) && (ld * int64_t(dtype_size(dtype))) % 16 == 0, OTK_ERR_ALIGNMENT,
               "logits base and row stride must be 16-byte aligned");
   *csize = choose_csize(vocab, dtype_size(dtype), seg_elems);
@@ -66,7 +66,7 @@ otk_status check_rows(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld,
   return OTK_OK;
 }
 
-otk_status check_cfg(const otk_loss_cfg* cfg, const float* ref_logp) {
+otk_status check_cfg(const otk_loss_cfg* cfg, const float* ref_logp, int64_t num_rows) {
   OTK_REQUIRE(cfg, OTK_ERR_INVALID_ARG, "cfg is NULL");
   OTK_REQUIRE(cfg->clip_low >= 0 && cfg->clip_low < 1 && cfg->clip_high >= 0, OTK_ERR_INVALID_ARG,
               "clip_low must be in [0,1), clip_high >= 0");
@@ -75,7 +75,8 @@ otk_status check_cfg(const otk_loss_cfg* cfg, const float* ref_logp) {
   OTK_REQUIRE(cfg->logit_scale > 0 && std::isfinite(cfg->logit_scale), OTK_ERR_INVALID_ARG, "logit_scale must be > 0");
   OTK_REQUIRE(cfg->kl_beta >= 0 && std::isfinite(cfg->kl_beta), OTK_ERR_INVALID_ARG, "kl_beta must be >= 0");
   OTK_REQUIRE(cfg->kl_type >= 1 && cfg->kl_type <= 3, OTK_ERR_INVALID_ARG, "kl_type must be 1, 2 or 3");
-  OTK_REQUIRE(cfg->kl_beta == 0 || ref_logp, OTK_ERR_INVALID_ARG, "ref_logp is required when kl_beta != 0");
+  OTK_REQUIRE(cfg->kl_beta == 0 || ref_logp || num_rows == 0, OTK_ERR_INVALID_ARG,
+              "ref_logp is required when kl_beta != 0");
   OTK_REQUIRE(std::isfinite(cfg->ent_coef), OTK_ERR_INVALID_ARG, "ent_coef must be finite");
   OTK_REQUIRE(cfg->dual_clip == 0 || (cfg->dual_clip > 1 && std::isfinite(cfg->dual_clip)), OTK_ERR_INVALID_ARG,
               "dual_clip must be 0 (off) or > 1");
@@ -325,13 +326,13 @@ otk_status otk_sample_tokens(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int6
   OTK_REQUIRE(dtype == OTK_BF16 || dtype == OTK_F32, OTK_ERR_DTYPE, "unknown dtype");
   OTK_REQUIRE(num_rows >= 0 && vocab >= 1 && ld >= vocab && vocab < (int64_t(1) << 31), OTK_ERR_SHAPE,
               "need num_rows >= 0, 1 <= vocab < 2^31, ld >= vocab");
-  OTK_REQUIRE(logits && tokens, OTK_ERR_INVALID_ARG, "logits / tokens is NULL");
   OTK_REQUIRE(greedy == 0 || greedy == 1, OTK_ERR_INVALID_ARG, "greedy must be 0 or 1");
+  OTK_REQUIRE(logit_scale > 0 && std::isfinite(logit_scale), OTK_ERR_INVALID_ARG, "logit_scale must be > 0");
+  if (num_rows == 0) return OTK_OK;
+  OTK_REQUIRE(logits && tokens, OTK_ERR_INVALID_ARG, "logits / tokens is NULL");
   OTK_REQUIRE(greedy || uniforms, OTK_ERR_INVALID_ARG, "uniforms is NULL (required unless greedy)");
   OTK_REQUIRE(aligned16(logits) && (ld * int64_t(dtype_size(dtype))) % 16 == 0, OTK_ERR_ALIGNMENT,
               "logits base and row stride must be 16-byte aligned");
-  OTK_REQUIRE(logit_scale > 0 && std::isfinite(logit_scale), OTK_ERR_INVALID_ARG, "logit_scale must be > 0");
-  if (num_rows == 0) return OTK_OK;
   otk::SampleParams p;
   p.num_rows = num_rows;
   p.vocab = vocab;
@@ -363,12 +364,12 @@ otk_status otk_lmhead_logprob_fwd(otk_ctx* ctx, int64_t num_rows, int64_t hidden
               OTK_ERR_SHAPE, "need 0 <= num_rows < 2^31, 1 <= vocab < 2^31");
   OTK_REQUIRE(hidden_dim >= 64 && hidden_dim % 64 == 0 && hidden_dim <= 65536, OTK_ERR_SHAPE,
               "hidden_dim must be a positive multiple of 64 (<= 65536)");
+  OTK_REQUIRE(logit_scale > 0 && std::isfinite(logit_scale), OTK_ERR_INVALID_ARG, "logit_scale must be > 0");
+  if (num_rows == 0) return OTK_OK;
   OTK_REQUIRE(hidden && weight && targets && logp && workspace, OTK_ERR_INVALID_ARG,
               "hidden / weight / targets / logp / workspace is NULL");
   OTK_REQUIRE(aligned16(hidden) && aligned16(weight) && aligned16(workspace), OTK_ERR_ALIGNMENT,
               "hidden, weight and workspace must be 16-byte aligned");
-  OTK_REQUIRE(logit_scale > 0 && std::isfinite(logit_scale), OTK_ERR_INVALID_ARG, "logit_scale must be > 0");
-  if (num_rows == 0) return OTK_OK;
   const int n_chunks = otk::lmhead_chunks(num_rows, vocab, ctx->num_sms);
   OTK_REQUIRE(workspace_bytes >= int64_t(n_chunks) * num_rows * 16, OTK_ERR_SHAPE,
               "workspace smaller than otk_lmhead_workspace_bytes()");
@@ -389,7 +390,7 @@ otk_status otk_logprob_entropy_fwd(otk_ctx* ctx, int64_t num_rows, int64_t vocab
   int csize = 0, seg = 0;
   otk_status st = check_rows(ctx, num_rows, vocab, ld, dtype, logits, targets, &csize, &seg);
   if (st != OTK_OK) return st;
-  OTK_REQUIRE(logp, OTK_ERR_INVALID_ARG, "logp is NULL");
+  OTK_REQUIRE(logp || num_rows == 0, OTK_ERR_INVALID_ARG, "logp is NULL");
   OTK_REQUIRE(logit_scale > 0 && std::isfinite(logit_scale), OTK_ERR_INVALID_ARG, "logit_scale must be > 0");
   if (num_rows == 0) return OTK_OK;
   otk::RowParams p = base_params(ctx, num_rows, vocab, ld, logits, targets, row_mask, logit_scale, csize, seg);
@@ -411,11 +412,12 @@ otk_status otk_policy_loss_fwd_bwd(otk_ctx* ctx, int64_t num_rows, int64_t vocab
   int csize = 0, seg = 0;
   otk_status st = check_rows(ctx, num_rows, vocab, ld, dtype, logits, targets, &csize, &seg);
   if (st != OTK_OK) return st;
-  st = check_cfg(cfg, ref_logp);
+  st = check_cfg(cfg, ref_logp, num_rows);
   if (st != OTK_OK) return st;
-  OTK_REQUIRE(loss_mask && row_traj && adv && old_logp && n_loss && dlogits && stats, OTK_ERR_INVALID_ARG,
-              "loss_mask, row_traj, adv, old_logp, n_loss, dlogits and stats are required");
-  OTK_REQUIRE(dlogits != logits, OTK_ERR_INVALID_ARG, "dlogits must not alias logits");
+  OTK_REQUIRE(n_loss && stats, OTK_ERR_INVALID_ARG, "n_loss and stats are required");
+  OTK_REQUIRE(num_rows == 0 || (loss_mask && row_traj && adv && old_logp && dlogits), OTK_ERR_INVALID_ARG,
+              "loss_mask, row_traj, adv, old_logp and dlogits are required (num_rows > 0)");
+  OTK_REQUIRE(dlogits != logits || num_rows == 0, OTK_ERR_INVALID_ARG, "dlogits must not alias logits");
   OTK_REQUIRE(aligned16(dlogits), OTK_ERR_ALIGNMENT, "dlogits must be 16-byte aligned");
   otk::RowParams p = base_params(ctx, num_rows, vocab, ld, logits, targets, loss_mask, float(cfg->logit_scale),
                                  csize, seg);
@@ -432,7 +434,7 @@ otk_status otk_row_partials(otk_ctx* ctx, int64_t num_rows, int64_t vocab_local,
   int csize = 0, seg = 0;
   otk_status st = check_rows(ctx, num_rows, vocab_local, ld, dtype, logits, targets, &csize, &seg);
   if (st != OTK_OK) return st;
-  OTK_REQUIRE(shard && partials, OTK_ERR_INVALID_ARG, "shard / partials is NULL");
+  OTK_REQUIRE(shard && (partials || num_rows == 0), OTK_ERR_INVALID_ARG, "shard / partials is NULL");
   OTK_REQUIRE(shard->vocab_start >= 0 && shard->vocab_start + vocab_local <= shard->vocab_total, OTK_ERR_SHAPE,
               "shard outside [0, vocab_total)");
   OTK_REQUIRE(aligned16(partials), OTK_ERR_ALIGNMENT, "partials must be 16-byte aligned");
@@ -451,7 +453,7 @@ otk_status otk_row_partials(otk_ctx* ctx, int64_t num_rows, int64_t vocab_local,
 otk_status otk_logprob_entropy_combine(otk_ctx* ctx, int64_t num_rows, int32_t nshards, const float* partials,
                                        const uint8_t* row_mask, float* logp, float* entropy, float* lse,
                                        otk_stream_t stream) {
-  OTK_REQUIRE(ctx && partials && logp, OTK_ERR_INVALID_ARG, "ctx / partials / logp is NULL");
+  OTK_REQUIRE(ctx && ((partials && logp) || num_rows == 0), OTK_ERR_INVALID_ARG, "ctx / partials / logp is NULL");
   OTK_REQUIRE(num_rows >= 0 && nshards >= 1, OTK_ERR_SHAPE, "num_rows >= 0 and nshards >= 1 required");
   OTK_REQUIRE(aligned16(partials), OTK_ERR_ALIGNMENT, "partials must be 16-byte aligned");
   if (num_rows == 0) return OTK_OK;
@@ -472,14 +474,14 @@ otk_status otk_policy_loss_fwd_bwd_partials(otk_ctx* ctx, int64_t num_rows, int6
   int csize = 0, seg = 0;
   otk_status st = check_rows(ctx, num_rows, vocab_local, ld, dtype, logits, targets, &csize, &seg);
   if (st != OTK_OK) return st;
-  st = check_cfg(cfg, ref_logp);
+  st = check_cfg(cfg, ref_logp, num_rows);
   if (st != OTK_OK) return st;
   OTK_REQUIRE(loss_mask && row_traj && adv && old_logp && n_loss && dlogits && stats && shard && partials,
               OTK_ERR_INVALID_ARG, "a required pointer is NULL");
   OTK_REQUIRE(nshards >= 1, OTK_ERR_SHAPE, "nshards >= 1 required");
   OTK_REQUIRE(shard->vocab_start >= 0 && shard->vocab_start + vocab_local <= shard->vocab_total, OTK_ERR_SHAPE,
               "shard outside [0, vocab_total)");
-  OTK_REQUIRE(dlogits != logits, OTK_ERR_INVALID_ARG, "dlogits must not alias logits");
+  OTK_REQUIRE(dlogits != logits || num_rows == 0, OTK_ERR_INVALID_ARG, "dlogits must not alias logits");
   OTK_REQUIRE(aligned16(dlogits) && aligned16(partials), OTK_ERR_ALIGNMENT, "dlogits / partials alignment");
   otk::RowParams p = base_params(ctx, num_rows, vocab_local, ld, logits, targets, loss_mask,
                                  float(cfg->logit_scale), csize, seg);
@@ -504,7 +506,7 @@ otk_status otk_policy_loss_fwd_bwd_host(otk_ctx* ctx, int64_t num_rows, int64_t 
   int csize = 0, seg = 0;
   otk_status st = check_rows(ctx, num_rows, vocab, ld, dtype, logits_host, targets_host, &csize, &seg);
   if (st != OTK_OK) return st;
-  st = check_cfg(cfg, ref_logp_host);
+  st = check_cfg(cfg, ref_logp_host, num_rows);
   if (st != OTK_OK) return st;
   OTK_REQUIRE(loss_mask_host && row_traj_host && adv_host && old_logp_host && stats_host && num_traj >= 1,
               OTK_ERR_INVALID_ARG, "a required host pointer is NULL");

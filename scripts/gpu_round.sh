@@ -6,10 +6,13 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
 timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?" >> gpurun_out/bench_ref.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1; echo "launches rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-next > gpurun_out/ncu_bench.log 2>&1; echo "launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_rows -s 2 -c 1 -o gpurun_out/prof_k4 -f python scripts/prof_k4.py > gpurun_out/ncu_full.log 2>&1; echo "full rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_rows -s 2 -c 1 -o gpurun_out/prof_k3 -f python scripts/prof_k4.py --fwd > gpurun_out/ncu_full3.log 2>&1; echo "full3 rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sample -s 2 -c 1 -o gpurun_out/prof_sample -f python scripts/prof_sample.py 4096 > gpurun_out/ncu_sample.log 2>&1; echo "sample rc=$?"
 timeout 300 python scripts/perf_sample.py > gpurun_out/perf_sample.jsonl 2>&1; echo "perf_sample rc=$?"
 for tool in memcheck racecheck synccheck; do timeout 600 compute-sanitizer --tool $tool --error-exitcode 3 python scripts/sanitize.py > gpurun_out/sanitize_$tool.log 2>&1; echo "$tool rc=$?" >> gpurun_out/sanitize_$tool.log; done
 tail -1 gpurun_out/smoke.log; tail -2 gpurun_out/gpu_tests.log; tail -1 gpurun_out/bench.err; tail -1 gpurun_out/bench_ref.err; tail -n2 gpurun_out/sanitize_*.log
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_lmhead -s 2 -c 1 -o gpurun_out/prof_lmhead -f python scripts/prof_lmhead.py 8192 > gpurun_out/ncu_lmhead.log 2>&1; echo "lmhead rc=$?"
+for n in 4096 8192 16384; do timeout 60 python scripts/perf_lmhead.py --rows $n --iters 5 2>&1 | tail -1; done > gpurun_out/perf_lmhead.jsonl
+for v in "" ent dual seqmean seqsum sft turn; do timeout 120 python scripts/perf_k4.py --variant "$v" 2>&1 | tail -1; done > gpurun_out/perf_variants.jsonl

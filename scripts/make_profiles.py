@@ -38,7 +38,8 @@ def launches(tag):
         for o in out:
             f.write(f'{o[0]},"{o[1]}","{o[2]}","{o[3]}",{o[4]:.0f}\n')
     # the timed otk step: masks, advantages and the loss launches (setup K3 / torch kernels excluded)
-    step_k = [o for o in out if o[1].startswith("otk::") and "k_rows_tm<__nv_bfloat16, 0>" not in o[1]]
+    step_names = ("otk::k_build_masks", "otk::k_group_advantages", "otk::k_rows_tm<__nv_bfloat16, 2>")
+    step_k = [o for o in out if o[1] in step_names]
     tot = {}
     for o in out:
         tot.setdefault(o[1], [0, 0.0])

@@ -1,0 +1,104 @@
+"""Degenerate and empty inputs through the C ABI (-m gpu): zero rows, every row masked (N_loss = 0), a
+one-token vocabulary, empty trajectories — each against the oracle or the closed form."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle_ref as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def otk():
+    import paper_2601_07376_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(otk):
+    c = otk.Context(0)
+    yield c
+    c.close()
+
+
+def test_zero_rows_every_entry_point(otk, ctx):
+    V = 4096
+    lg = torch.empty((0, V), dtype=torch.bfloat16, device="cuda")
+    tg = torch.empty(0, dtype=torch.int32, device="cuda")
+    assert otk.otk_logprob_entropy_fwd(ctx, lg, tg)["logp"].numel() == 0
+    assert otk.otk_sample_tokens(ctx, lg, torch.empty(0, device="cuda"))["tokens"].numel() == 0
+    assert otk.otk_row_partials(ctx, lg, tg, 0, V).numel() == 0
+    h = torch.empty((0, 64), dtype=torch.bfloat16, device="cuda")
+    w = torch.zeros((V, 64), dtype=torch.bfloat16, device="cuda")
+    assert otk.otk_lmhead_logprob_fwd(ctx, h, w, tg)["logp"].numel() == 0
+    # the loss over zero rows still writes the (zero) stats when not accumulating, and keeps them otherwise
+    stats = torch.full((5,), 3.0, dtype=torch.float64, device="cuda")
+    e = torch.empty(0, device="cuda")
+    args = (lg, tg, torch.empty(0, dtype=torch.uint8, device="cuda"), torch.empty(0, dtype=torch.int32, device="cuda"),
+            torch.zeros(1, dtype=torch.float64, device="cuda"), e, e, torch.zeros(1, dtype=torch.int64, device="cuda"))
+    otk.otk_policy_loss_fwd_bwd(ctx, *args, otk.LossCfg(), stats=stats, accumulate=True)
+    assert stats.tolist() == [3.0] * 5
+    otk.otk_policy_loss_fwd_bwd(ctx, *args, otk.LossCfg(), stats=stats, accumulate=False)
+    assert stats.tolist() == [0.0] * 5
+    ctx.check()
+
+
+def test_all_rows_masked(otk, ctx):
+    """N_loss = 0 (R17): loss 0, every dlogits row 0, no trainable tokens."""
+    from synth import make_logits
+    n, V = 64, 4096
+    lg, tg = make_logits(n, V, dtype="bf16", seed=2, device="cuda")
+    dl = torch.full_like(lg, 5.0)
+    out = otk.otk_policy_loss_fwd_bwd(ctx, lg, tg, torch.zeros(n, dtype=torch.uint8, device="cuda"),
+                                      torch.zeros(n, dtype=torch.int32, device="cuda"),
+                                      torch.ones(1, dtype=torch.float64, device="cuda"),
+                                      torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda"),
+                                      torch.zeros(1, dtype=torch.int64, device="cuda"), otk.LossCfg(), dlogits=dl)
+    ctx.check()
+    st = otk.stats_dict(out["stats"])
+    assert st["loss"] == 0.0 and st["n_tokens"] == 0.0
+    assert bool((dl == 0).all())
+
+
+def test_one_token_vocabulary(otk, ctx):
+    """V = 1: the only token has probability 1 — logp = 0 and entropy = 0 (to fp32 rounding of s*x), the sampler
+    returns it, and the gradient row is coef * (1 - 1) = 0."""
+    n = 16
+    lg = torch.randn((n, 8), device="cuda").to(torch.bfloat16)     # ld = 8 (16-byte rows), vocab = 1
+    tg = torch.zeros(n, dtype=torch.int32, device="cuda")
+    f = otk.otk_logprob_entropy_fwd(ctx, lg, tg, vocab=1)
+    assert float(f["logp"].abs().max()) < 1e-6 and float(f["entropy"].abs().max()) < 1e-6
+    s = otk.otk_sample_tokens(ctx, lg, torch.rand(n, device="cuda"), vocab=1)
+    assert int(s["tokens"].max()) == 0 and float(s["logp"].abs().max()) < 1e-6
+    dl = torch.full_like(lg, 9.0)
+    otk.otk_policy_loss_fwd_bwd(ctx, lg, tg, torch.ones(n, dtype=torch.uint8, device="cuda"),
+                                torch.zeros(n, dtype=torch.int32, device="cuda"),
+                                torch.ones(1, dtype=torch.float64, device="cuda"), torch.zeros(n, device="cuda"),
+                                torch.zeros(n, device="cuda"), torch.full((1,), n, dtype=torch.int64, device="cuda"),
+                                otk.LossCfg(), vocab=1, dlogits=dl)
+    ctx.check()
+    # coef * expm1(logp) with logp ~ 1e-8 of rounding: zero within the dlogits tolerance (1e-5 |coef|)
+    assert float(dl[:, 0].float().abs().max()) < 1e-6 and bool((dl[:, 1:] == 9.0).all())   # columns >= vocab untouched
+
+
+def test_empty_trajectories_in_batch(otk, ctx):
+    """Trajectories with no segments and no rows sit between normal ones: masks, counts, returns exact."""
+    from synth.trajectories import _pack
+    C, A, Ob = O.CONTEXT, O.ACTION, O.OBSERVATION
+    tb = _pack([[(C, -1, 3), (A, 0, 4)], [], [(C, -1, 2), (A, 0, 2), (Ob, -1, 1)], []],
+               [[1.0], [], [0.5], [2.0]], [0, 0, 1, 1], 2)
+    db = otk.traj_batch_to_device(tb)
+    m = otk.otk_build_masks(ctx, db, row_seg=True)
+    ctx.check()
+    om = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated)
+    for k in ("loss_mask", "row_traj", "row_seg", "traj_loss_tokens"):
+        assert np.array_equal(m[k].cpu().numpy(), om[k]), k
+    assert int(m["n_active_traj"].item()) == 2
+    a = otk.otk_group_advantages(ctx, torch.from_numpy(tb.group_id).cuda(), 2,
+                                 turn_offsets=torch.from_numpy(tb.turn_offsets).cuda(),
+                                 turn_rewards=torch.from_numpy(tb.turn_rewards).cuda())
+    want = O.group_advantages(tb.group_id, O.episode_returns(tb.turn_offsets, tb.turn_rewards), 2)["adv"]
+    assert np.max(np.abs(a["adv"].cpu().numpy() - want)) < 1e-6
