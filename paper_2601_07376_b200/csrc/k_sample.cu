@@ -276,6 +276,18 @@ __global__ void __launch_bounds__(kSampleThreads, OTK_SAMPLE_MINB) k_sample(cons
       }
     }
     const bool degenerate = !(M > kNoRef) || !(S > 0.f);  // no finite logit above -1e30
+#ifndef OTK_SAMPLE_NO_PREFETCH
+    // warm L2 with the start of this thread's slice of the next row while the search below (latency-bound)
+    // runs, so the next row's main pass starts from L2 rather than HBM
+    if (!greedy && row + ngroups < p.num_rows) {
+      const uint4* np = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(p.logits) + (row + ngroups) * p.ld);
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int v = w_v0 + lane + 32 * k;
+        if (v < w_v1) asm volatile("prefetch.global.L2 [%0];" ::"l"(np + v));
+      }
+    }
+#endif
 
     if (greedy || degenerate) {
       if (rank == 0 && tid == 0) {
