@@ -31,7 +31,67 @@ __global__ void k_mix12(const uint4* x, uint4* y, uint4* z, size_t n16) {
     asm volatile("st.global.cs.v4.b32 [%0], {%1, %1, %1, %1};" ::"l"(z + i), "r"(0) : "memory");
   }
 }
+// read-only: 8 independent 16-byte loads in flight per thread, XOR-folded, one word written per thread
+__global__ void k_read(const uint4* x, size_t n16, unsigned* out) {
+  unsigned acc = 0;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+  for (; i + 7 * stride < n16; i += 8 * stride) {
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldg(x + i + k * stride);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc ^= v[k].x ^ v[k].y ^ v[k].z ^ v[k].w;
+  }
+  for (; i < n16; i += stride) { uint4 v = __ldg(x + i); acc ^= v.x ^ v.y ^ v.z ^ v.w; }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+// read-only through 1-D bulk TMA into a shared-memory ring (the row kernels' load path)
+__global__ void k_read_bulk(const char* x, size_t nbytes, uint32_t chunk, unsigned* out) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) unsigned long long bar[8];
+  const int slots = 8;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < slots; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&bar[k])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    size_t n = 0;
+    for (size_t off = size_t(blockIdx.x) * chunk; off + chunk <= nbytes; off += size_t(gridDim.x) * chunk, ++n) {
+      const int s = int(n % slots);
+      const unsigned b = (unsigned)__cvta_generic_to_shared(&bar[s]);
+      if (n >= (size_t)slots) {  // wait for this slot's previous transfer (no consumer: pure read bandwidth)
+        unsigned ok = 0;
+        while (!ok) asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}" : "=r"(ok) : "r"(b), "r"(ph[s]) : "memory");
+        ph[s] ^= 1u;
+      }
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(chunk) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                   "r"((unsigned)__cvta_generic_to_shared(ring + size_t(s) * chunk)), "l"(x + off), "r"(chunk), "r"(b) : "memory");
+    }
+    for (int s = 0; s < slots; ++s) {
+      if (n > (size_t)s) {
+        const unsigned b = (unsigned)__cvta_generic_to_shared(&bar[s]);
+        unsigned ok = 0;
+        while (!ok) asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}" : "=r"(ok) : "r"(b), "r"(ph[s]) : "memory");
+      }
+    }
+    out[blockIdx.x] = ring[0];
+  }
+}
 extern "C" {
+int probe_read(const void* x, size_t nbytes, int grid, void* out, cudaStream_t s) {
+  k_read<<<grid, 512, 0, s>>>((const uint4*)x, nbytes / 16, (unsigned*)out);
+  return cudaGetLastError();
+}
+int probe_read_bulk(const void* x, size_t nbytes, int grid, unsigned chunk, void* out, cudaStream_t s) {
+  cudaFuncSetAttribute(k_read_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * chunk);
+  k_read_bulk<<<grid, 32, 8 * chunk, s>>>((const char*)x, nbytes, chunk, (unsigned*)out);
+  return cudaGetLastError();
+}
 int probe_write_stg(void* p, size_t nbytes, int grid, int plain, cudaStream_t s) {
   if (plain) k_write_stg_plain<<<grid, 512, 0, s>>>((uint4*)p, nbytes / 16);
   else k_write_stg<<<grid, 512, 0, s>>>((uint4*)p, nbytes / 16);

@@ -24,6 +24,12 @@ for g in (148 * 4, 148 * 8, 148 * 16):
 for ch in (4096, 16384, 65536):
     for g in (148, 296):
         res[f"bulk_w_chunk{ch}_grid{g}"] = t(lambda: L.probe_write_bulk(P(y), C.c_size_t(nb), g, ch, C.c_void_p(s)), nb)
+o = torch.empty(148 * 16 * 512, dtype=torch.int32, device="cuda")
+for g in (148 * 4, 148 * 8, 148 * 16):
+    res[f"ldg_read_grid{g}"] = t(lambda: L.probe_read(P(x), C.c_size_t(nb), g, P(o), C.c_void_p(s)), nb)
+for ch in (12288, 24576):
+    for g in (148, 296):
+        res[f"bulk_read_chunk{ch}_grid{g}"] = t(lambda: L.probe_read_bulk(P(x), C.c_size_t(nb), g, ch, P(o), C.c_void_p(s)), nb)
 res["memset_w"] = t(lambda: L.probe_memset(P(y), C.c_size_t(nb), C.c_void_p(s)), nb)
 res["mix_r1w2_grid1184"] = t(lambda: L.probe_mix12(P(x), P(y), P(z), C.c_size_t(nb), 1184, C.c_void_p(s)), 3 * nb)
 res["mix_r1w2_grid2368"] = t(lambda: L.probe_mix12(P(x), P(y), P(z), C.c_size_t(nb), 2368, C.c_void_p(s)), 3 * nb)
