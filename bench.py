@@ -383,7 +383,7 @@ def other_kernels(W):
 
 def e2e(args, W, world, step, cfg):
     """Same metric through the C-ABI host-buffer entry point (otk_policy_loss_fwd_bwd_host): every
-    micro-batch's logits + side arrays are copied H2D from pinned host memory inside the timed region
+    micro-batch's trainable logits rows + side arrays are copied H2D from pinned host memory inside the timed region
     (pipelined in 4096-row chunks on a copy stream), and the loss statistics come back D2H. The step's
     masks / advantages (device outputs of (1)-(2)) are inputs of this call and are staged once."""
     otk, ctx = W["otk"], W["ctx"]
@@ -419,11 +419,14 @@ def e2e(args, W, world, step, cfg):
     dt = (time.perf_counter() - t0) / args.e2e_steps
     row_bytes = W["bufs"][0].shape[1] * W["bufs"][0].element_size()
     side_b = 4 + 1 + 4 + 4 + (4 if mbs[0].ref_logp is not None else 0)
-    h2d = N * (row_bytes + side_b) + len(mbs) * (adv_h.numel() * 8 + 8)
+    # logits rows cross PCIe only when trainable (the C ABI copies the runs of loss_mask != 0 rows)
+    n_train = int(lm_h.sum().item())
+    h2d = n_train * row_bytes + N * side_b + len(mbs) * (adv_h.numel() * 8 + 8)
     return {"value": N * world / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": len(mbs) * 40, "steps": args.e2e_steps,
             "h2d_GBps": h2d / dt / 1e9,
-            "path": "otk_policy_loss_fwd_bwd_host (C ABI, pinned host buffers, 4096-row chunks double-buffered)",
+            "path": "otk_policy_loss_fwd_bwd_host (C ABI, pinned host buffers, 4096-row chunks double-buffered; "
+                    "logits of loss-masked rows are not copied)",
             "clock": "host wall clock around the blocking C-ABI calls" + ("; rank 0" if world > 1 else "")}
 
 

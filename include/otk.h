@@ -234,7 +234,8 @@ otk_status otk_policy_loss_fwd_bwd(otk_ctx* ctx, int64_t num_rows, int64_t vocab
 
 /* Same computation as otk_policy_loss_fwd_bwd but every array argument is a HOST pointer (pinned
  * memory recommended): rows are streamed through ctx-owned device staging buffers in chunks, with the
- * host->device copies of chunk k+1 overlapping the kernel on chunk k. dlogits_host may be NULL (the
+ * host->device copies of chunk k+1 overlapping the kernel on chunk k. Only the logits rows with
+ * loss_mask != 0 are copied (runs of consecutive rows, one copy each): a masked row is never read. dlogits_host may be NULL (the
  * gradient is then computed on the device and discarded); stats_host receives the result. Blocking:
  * returns after the stats have been copied back. Used to measure the end-to-end (e2e) metric. */
 otk_status otk_policy_loss_fwd_bwd_host(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld,

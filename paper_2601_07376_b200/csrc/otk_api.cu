@@ -557,8 +557,19 @@ otk_status otk_policy_loss_fwd_bwd_host(otk_ctx* ctx, int64_t num_rows, int64_t 
     char* sb = reinterpret_cast<char*>(ctx->stage[b]);
     if (k >= 2) OTK_CUDA(cudaStreamWaitEvent(cs, ctx->ev[2 + b], 0), "wait free");
     if (n > 0) {
-      OTK_CUDA(cudaMemcpyAsync(sb, reinterpret_cast<const char*>(logits_host) + size_t(r0) * row_bytes,
-                               size_t(n) * row_bytes, cudaMemcpyHostToDevice, cs), "H2D logits");
+      // logits: only the runs of trainable rows — the kernel never reads a loss-masked row (it only writes
+      // its zero gradient), so its bytes need not cross PCIe
+      for (int64_t a = 0; a < n;) {
+        while (a < n && !loss_mask_host[r0 + a]) ++a;
+        int64_t e = a;
+        while (e < n && loss_mask_host[r0 + e]) ++e;
+        if (e > a)
+          OTK_CUDA(cudaMemcpyAsync(sb + size_t(a) * row_bytes,
+                                   reinterpret_cast<const char*>(logits_host) + size_t(r0 + a) * row_bytes,
+                                   size_t(e - a) * row_bytes, cudaMemcpyHostToDevice, cs),
+                   "H2D logits");
+        a = e;
+      }
       OTK_CUDA(cudaMemcpyAsync(sb + off_tg, targets_host + r0, size_t(n) * 4, cudaMemcpyHostToDevice, cs), "H2D");
       OTK_CUDA(cudaMemcpyAsync(sb + off_m, loss_mask_host + r0, size_t(n), cudaMemcpyHostToDevice, cs), "H2D");
       OTK_CUDA(cudaMemcpyAsync(sb + off_rt, row_traj_host + r0, size_t(n) * 4, cudaMemcpyHostToDevice, cs), "H2D");
