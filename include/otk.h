@@ -313,6 +313,15 @@ otk_status otk_lmhead_logprob_fwd(otk_ctx* ctx, int64_t num_rows, int64_t hidden
                                   int64_t workspace_bytes, float* logp, float* entropy, float* lse,
                                   otk_stream_t stream);
 
+/* Vocab-sharded LM head (tensor-parallel head: this rank holds rows [vocab_start, vocab_start + vocab_local)
+ * of W, targets are global): writes this rank's per-row partials (m2, s, t2, w) — the otk_row_partials form —
+ * for the caller to all-gather into [nshards][num_rows][4] (rank order) and finish with
+ * otk_logprob_entropy_combine. workspace: otk_lmhead_workspace_bytes(ctx, num_rows, vocab_local) bytes. */
+otk_status otk_lmhead_row_partials(otk_ctx* ctx, int64_t num_rows, int64_t hidden_dim, int64_t vocab_local,
+                                   const void* hidden, const void* weight, const int32_t* targets,
+                                   const uint8_t* row_mask, const otk_vocab_shard* shard, float logit_scale,
+                                   void* workspace, int64_t workspace_bytes, float* partials, otk_stream_t stream);
+
 /* Harness helper (not on the path): number of kernel launches the library issued since ctx creation. */
 int64_t otk_ctx_launch_count(const otk_ctx* ctx);
 

@@ -85,6 +85,8 @@ _sig = {
                                                _P, _I64, C.POINTER(otk_loss_cfg), _P, _P, _I64]),
     "otk_lmhead_workspace_bytes": (_I64, [_P, _I64, _I64]),
     "otk_lmhead_logprob_fwd": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _P, C.c_float, _P, _I64, _P, _P, _P, _P]),
+    "otk_lmhead_row_partials": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _P, C.POINTER(otk_vocab_shard), C.c_float,
+                                          _P, _I64, _P, _P]),
     "otk_sample_tokens": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, C.c_float, C.c_int32, _P, _P, _P]),
     "otk_row_partials": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, C.POINTER(otk_vocab_shard),
                                    C.c_float, _P, _P]),
@@ -325,6 +327,29 @@ def otk_lmhead_logprob_fwd(ctx: Context, hidden: torch.Tensor, weight: torch.Ten
                                        _ptr(o["entropy"]), _ptr(o.get("lse")), _stream(stream)))
     o["workspace"] = workspace
     return o
+
+
+def otk_lmhead_row_partials(ctx: Context, hidden: torch.Tensor, weight_shard: torch.Tensor, targets: torch.Tensor,
+                            vocab_start: int, vocab_total: int, *, row_mask: Optional[torch.Tensor] = None,
+                            logit_scale: float = 1.0, workspace: Optional[torch.Tensor] = None,
+                            partials: Optional[torch.Tensor] = None, stream=None):
+    """This rank's [N, 4] partials of a vocab-sharded LM head (otk.h otk_lmhead_row_partials); returns
+    (partials, workspace)."""
+    for t, n in ((hidden, "hidden"), (weight_shard, "weight_shard"), (targets, "targets")):
+        _dev(t, n)
+    N, d = hidden.shape
+    Vl = weight_shard.shape[0]
+    nbytes = int(_lib.otk_lmhead_workspace_bytes(ctx.handle, N, Vl))
+    if workspace is None or workspace.numel() * workspace.element_size() < nbytes:
+        workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=hidden.device)
+    if partials is None:
+        partials = torch.empty((N, 4), dtype=torch.float32, device=hidden.device)
+    sh = otk_vocab_shard(int(vocab_start), int(vocab_total))
+    _check(_lib.otk_lmhead_row_partials(ctx.handle, N, d, Vl, _ptr(hidden), _ptr(weight_shard), _ptr(targets),
+                                        _ptr(row_mask), C.byref(sh), float(logit_scale), _ptr(workspace),
+                                        workspace.numel() * workspace.element_size(), _ptr(partials),
+                                        _stream(stream)))
+    return partials, workspace
 
 
 # ------------------------------------------------------------------------------------------------

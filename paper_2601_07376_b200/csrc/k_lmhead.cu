@@ -44,6 +44,7 @@ constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address of th
 
 struct LmParams {
   int64_t num_rows, vocab;
+  int64_t vocab_start, vocab_total;  // this rank's columns of a vocab-sharded head (0, vocab unsharded)
   int d;                 // hidden size (multiple of 64)
   int n_rowtiles;        // ceil(num_rows / 256)
   int n_chunks;          // vocab chunks
@@ -244,9 +245,12 @@ __global__ void __launch_bounds__(kLmThreads, 1)
       unit_coords(u, p.n_rowtiles, p.n_chunks, c, rt);
       const int t0 = chunk_tile0(c, p.n_chunks, p.n_coltiles), t1 = chunk_tile0(c + 1, p.n_chunks, p.n_coltiles);
       const int64_t row = int64_t(rt) * kLmRows + rank * 128 + q * 32 + lane;
-      const int ycol = row < p.num_rows ? p.targets[row] : -1;
-      if (c == 0 && row < p.num_rows && (!p.row_mask || p.row_mask[row]) && (ycol < 0 || ycol >= p.vocab))
-        set_error(p.err, OTK_ERR_TARGET_RANGE);  // such a row's logp is -inf
+      const int64_t yglob = row < p.num_rows ? int64_t(p.targets[row]) : -1;
+      if (c == 0 && p.vocab_start == 0 && row < p.num_rows && (!p.row_mask || p.row_mask[row]) &&
+          (yglob < 0 || yglob >= p.vocab_total))
+        set_error(p.err, OTK_ERR_TARGET_RANGE);  // such a row's logp is -inf (checked once, by shard 0)
+      const int64_t yl = yglob - p.vocab_start;  // target column local to this shard
+      const int ycol = (yl >= 0 && yl < p.vocab) ? int(yl) : -1;
       float m = -1e30f, s = 0.f, tt = 0.f, zy = -INFINITY;
       for (int t = t0; t < t1; ++t, ++it) {
         const uint32_t acc = it & 1u;
@@ -354,13 +358,16 @@ int lmhead_chunks(int64_t num_rows, int64_t vocab, int num_sms) {
 
 cudaError_t launch_lmhead_fwd(const otk_ctx* ctx, int64_t num_rows, int64_t vocab, int d, const void* hidden,
                               const void* weight, const int32_t* targets, const uint8_t* row_mask, float logit_scale,
-                              float4* partials, int n_chunks, cudaStream_t s) {
+                              float4* partials, int n_chunks, cudaStream_t s, int64_t vocab_start,
+                              int64_t vocab_total) {
   CUtensorMap th, tw;
   if (!make_map(&th, hidden, num_rows, d, 128) || !make_map(&tw, weight, vocab, d, 128))
     return cudaErrorInvalidValue;
   LmParams p;
   p.num_rows = num_rows;
   p.vocab = vocab;
+  p.vocab_start = vocab_start;
+  p.vocab_total = vocab_total > 0 ? vocab_total : vocab;
   p.d = d;
   p.n_rowtiles = int((num_rows + kLmRows - 1) / kLmRows);
   p.n_chunks = n_chunks;

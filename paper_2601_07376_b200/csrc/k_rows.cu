@@ -1187,6 +1187,31 @@ cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const
   return cudaErrorInvalidValue;
 }
 
+// several partials of one row (e.g. the vocab chunks of the fused LM head on one rank) -> one partial of the
+// same form, for a vocab-sharded caller to all-gather (same combine as above, rank order)
+__global__ void k_combine_to_partial(int64_t num_rows, int nparts, const float4* __restrict__ partials,
+                                     const uint8_t* __restrict__ row_mask, float4* out) {
+  for (int64_t row = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; row < num_rows;
+       row += int64_t(gridDim.x) * blockDim.x) {
+    if (row_mask && !row_mask[row]) {
+      out[row] = make_float4(-INFINITY, 0.f, 0.f, -INFINITY);
+      continue;
+    }
+    float dy;
+    const Stat tot = combine_partials(partials + row, num_rows, nparts, dy);
+    out[row] = make_float4(tot.m, tot.s, tot.t, dy);
+  }
+}
+
+cudaError_t launch_combine_to_partial(const otk_ctx* ctx, int64_t num_rows, int nparts, const float4* partials,
+                                      const uint8_t* row_mask, float4* out, cudaStream_t s) {
+  int64_t blocks = (num_rows + 255) / 256;
+  if (blocks > int64_t(ctx->num_sms) * 8) blocks = int64_t(ctx->num_sms) * 8;
+  if (blocks < 1) blocks = 1;
+  k_combine_to_partial<<<int(blocks), 256, 0, s>>>(num_rows, nparts, partials, row_mask, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_combine(const otk_ctx* ctx, int64_t num_rows, int nshards, const float4* partials,
                            const uint8_t* row_mask, float* logp, float* entropy, float* lse, cudaStream_t s) {
   int64_t blocks = (num_rows + 255) / 256;

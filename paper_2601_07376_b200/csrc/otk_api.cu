@@ -384,6 +384,40 @@ otk_status otk_lmhead_logprob_fwd(otk_ctx* ctx, int64_t num_rows, int64_t hidden
   return OTK_OK;
 }
 
+otk_status otk_lmhead_row_partials(otk_ctx* ctx, int64_t num_rows, int64_t hidden_dim, int64_t vocab_local,
+                                   const void* hidden, const void* weight, const int32_t* targets,
+                                   const uint8_t* row_mask, const otk_vocab_shard* shard, float logit_scale,
+                                   void* workspace, int64_t workspace_bytes, float* partials, otk_stream_t stream) {
+  OTK_REQUIRE(ctx && shard, OTK_ERR_INVALID_ARG, "ctx / shard is NULL");
+  OTK_REQUIRE(num_rows >= 0 && vocab_local >= 1 && vocab_local < (int64_t(1) << 31) && num_rows < (int64_t(1) << 31),
+              OTK_ERR_SHAPE, "need 0 <= num_rows < 2^31, 1 <= vocab_local < 2^31");
+  OTK_REQUIRE(shard->vocab_start >= 0 && shard->vocab_start + vocab_local <= shard->vocab_total &&
+                  shard->vocab_total < (int64_t(1) << 31),
+              OTK_ERR_SHAPE, "shard outside [0, vocab_total)");
+  OTK_REQUIRE(hidden_dim >= 64 && hidden_dim % 64 == 0 && hidden_dim <= 65536, OTK_ERR_SHAPE,
+              "hidden_dim must be a positive multiple of 64 (<= 65536)");
+  OTK_REQUIRE(logit_scale > 0 && std::isfinite(logit_scale), OTK_ERR_INVALID_ARG, "logit_scale must be > 0");
+  if (num_rows == 0) return OTK_OK;
+  OTK_REQUIRE(hidden && weight && targets && workspace && partials, OTK_ERR_INVALID_ARG,
+              "hidden / weight / targets / workspace / partials is NULL");
+  OTK_REQUIRE(aligned16(hidden) && aligned16(weight) && aligned16(workspace) && aligned16(partials),
+              OTK_ERR_ALIGNMENT, "hidden, weight, workspace and partials must be 16-byte aligned");
+  const int n_chunks = otk::lmhead_chunks(num_rows, vocab_local, ctx->num_sms);
+  OTK_REQUIRE(workspace_bytes >= int64_t(n_chunks) * num_rows * 16, OTK_ERR_SHAPE,
+              "workspace smaller than otk_lmhead_workspace_bytes()");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  float4* part = reinterpret_cast<float4*>(workspace);
+  OTK_CUDA(otk::launch_lmhead_fwd(ctx, num_rows, vocab_local, int(hidden_dim), hidden, weight, targets, row_mask,
+                                  logit_scale, part, n_chunks, s, shard->vocab_start, shard->vocab_total),
+           "k_lmhead_fwd launch");
+  ctx->launches += 1;
+  OTK_CUDA(otk::launch_combine_to_partial(ctx, num_rows, n_chunks, part, row_mask, reinterpret_cast<float4*>(partials),
+                                          s),
+           "k_combine_to_partial launch");
+  ctx->launches += 1;
+  return OTK_OK;
+}
+
 otk_status otk_logprob_entropy_fwd(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld, otk_dtype dtype,
                                    const void* logits, const int32_t* targets, const uint8_t* row_mask,
                                    float logit_scale, float* logp, float* entropy, float* lse, otk_stream_t stream) {

@@ -163,7 +163,10 @@ cudaError_t launch_sample(otk_ctx* ctx, const SampleParams& p, int dtype, cudaSt
 int lmhead_chunks(int64_t num_rows, int64_t vocab, int num_sms);
 cudaError_t launch_lmhead_fwd(const otk_ctx* ctx, int64_t num_rows, int64_t vocab, int d, const void* hidden,
                               const void* weight, const int32_t* targets, const uint8_t* row_mask, float logit_scale,
-                              float4* partials, int n_chunks, cudaStream_t s);
+                              float4* partials, int n_chunks, cudaStream_t s, int64_t vocab_start = 0,
+                              int64_t vocab_total = 0);
+cudaError_t launch_combine_to_partial(const otk_ctx* ctx, int64_t num_rows, int nparts, const float4* partials,
+                                      const uint8_t* row_mask, float4* out, cudaStream_t s);
 
 __device__ __forceinline__ void set_error(int* err, int code) { atomicCAS(err, 0, code); }
 

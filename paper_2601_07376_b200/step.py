@@ -30,7 +30,7 @@ import torch
 
 from . import (Context, DeviceTrajBatch, LossCfg, STATS_FIELDS, otk_build_masks, otk_group_advantages,
                otk_logprob_entropy_combine, otk_policy_loss_fwd_bwd, otk_policy_loss_fwd_bwd_partials,
-               otk_row_partials, otk_turn_returns)
+               otk_lmhead_row_partials, otk_row_partials, otk_turn_returns)
 
 
 @dataclass
@@ -72,6 +72,28 @@ class VocabShard:
                                                 ref_logp, n_loss, cfg, self.v0, self.vt, self._gather(part),
                                                 vocab_local=self.vl, dlogits=dlogits, stats=stats,
                                                 accumulate=accumulate)
+
+
+class LMHeadVocabShard:
+    """Tensor-parallel fused LM head (NEXT-1 forward): this rank holds rows [vocab_start, vocab_start +
+    vocab_local) of W; otk_lmhead_row_partials (16 B per row) -> all_gather in rank order -> exact combine.
+    Every rank ends with the same logp / entropy; the [N, V] logits exist nowhere."""
+
+    def __init__(self, ctx: Context, vocab_start: int, vocab_total: int, process_group=None):
+        self.ctx, self.v0, self.vt, self.pg = ctx, vocab_start, vocab_total, process_group
+        self.workspace = None
+
+    def forward(self, hidden: torch.Tensor, weight_shard: torch.Tensor, targets: torch.Tensor, row_mask=None,
+                logit_scale: float = 1.0):
+        part, self.workspace = otk_lmhead_row_partials(self.ctx, hidden, weight_shard, targets, self.v0, self.vt,
+                                                       row_mask=row_mask, logit_scale=logit_scale,
+                                                       workspace=self.workspace)
+        if self.pg is None:
+            gathered = part.unsqueeze(0)
+        else:
+            from .dist import all_gather_vocab_partials
+            gathered = all_gather_vocab_partials(part, self.pg)
+        return otk_logprob_entropy_combine(self.ctx, gathered, row_mask=row_mask)
 
 
 class PolicyLossStep:

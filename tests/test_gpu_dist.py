@@ -87,6 +87,16 @@ def _worker(rank, world, port, mode, q):
             res.update(adv=adv.cpu().numpy(), b0=b0, b1=b1, loss=otk.stats_dict(st.stats),
                        n_loss=int(st.masks["n_loss"].item()), n_loss_ref=int(st0.masks["n_loss"].item()),
                        dl_equal=bool(torch.equal(dl, dl0[r0:r1])))
+        elif mode == "lmhead_vocab":
+            from paper_2601_07376_b200.step import LMHeadVocabShard
+            from synth import make_lmhead
+            Vh = 20000
+            h, w, yy = make_lmhead(300, Vh, 128, seed=5, device=dev)
+            v0, v1 = vocab_shard_bounds(Vh, world)[rank]
+            out = LMHeadVocabShard(ctx, v0, Vh, dist.group.WORLD).forward(h, w[v0:v1].contiguous(), yy)
+            full = otk.otk_lmhead_logprob_fwd(ctx, h, w, yy)
+            res.update(loss=res["ref_loss"], lm_err=float((out["logp"] - full["logp"]).abs().max()),
+                       lm_logp=out["logp"].cpu().numpy())
         else:
             v0, v1 = vocab_shard_bounds(V, world)[rank]
             vs = VocabShard(ctx, v0, v1 - v0, V, dist.group.WORLD)
@@ -105,7 +115,7 @@ def _worker(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["batch", "vocab", "batch_turn"])
+@pytest.mark.parametrize("mode", ["batch", "vocab", "batch_turn", "lmhead_vocab"])
 def test_sharded_step_two_ranks_one_gpu(mode):
     world = 2
     ctx = mp.get_context("spawn")
@@ -128,6 +138,10 @@ def test_sharded_step_two_ranks_one_gpu(mode):
             assert np.array_equal(r["adv"], r["ref_adv"][r["b0"]:r["b1"]])     # global group statistics
             assert r["n_loss"] == r["n_loss_ref"]                               # global token count
             assert r["dl_equal"]                                                # same kernel, same rows
+    elif mode == "lmhead_vocab":
+        for r in res:
+            assert r["lm_err"] < 1e-5                                           # = the unsharded fused head
+        assert np.array_equal(res[0]["lm_logp"], res[1]["lm_logp"])             # identical on every rank
     else:
         assert res[0]["loss"]["loss"] == res[1]["loss"]["loss"]                 # identical on every rank
         for r in res:

@@ -72,3 +72,30 @@ def test_lmhead_validation(otk, ctx):
     mask[3] = 0                                    # ... but not when the row is masked
     otk.otk_lmhead_logprob_fwd(ctx, h.cuda(), w.cuda(), y.cuda(), row_mask=mask.cuda())
     ctx.check()
+
+
+@pytest.mark.parametrize("P,V", [(2, 151936), (3, 5000), (4, 1000)])
+def test_lmhead_vocab_sharded_equals_unsharded(otk, ctx, P, V):
+    """Tensor-parallel head: per-shard partials of W row blocks, combined in rank order, equal the unsharded
+    fused forward (1e-5) and the oracle (2e-3); targets fall in every shard."""
+    from paper_2601_07376_b200.dist import vocab_shard_bounds
+    from paper_2601_07376_b200.step import LMHeadVocabShard
+    N, d = 200, 128
+    h, w, y = make_lmhead(N, V, d, seed=P + V)
+    hc, wc, yc = h.cuda(), w.cuda(), y.cuda()
+    mask = (torch.arange(N) % 5 != 0).to(torch.uint8).cuda()
+    parts = []
+    for v0, v1 in vocab_shard_bounds(V, P):
+        sh = LMHeadVocabShard(ctx, v0, V)
+        part, _ = otk.otk_lmhead_row_partials(ctx, hc, wc[v0:v1].contiguous(), yc, v0, V, row_mask=mask)
+        parts.append(part)
+    comb = otk.otk_logprob_entropy_combine(ctx, torch.stack(parts), row_mask=mask)
+    ctx.check()
+    full = otk.otk_lmhead_logprob_fwd(ctx, hc, wc, yc, row_mask=mask)
+    assert float((comb["logp"] - full["logp"]).abs().max()) < 1e-5
+    assert float((comb["entropy"] - full["entropy"]).abs().max()) < 1e-5
+    rows = [j for j in range(0, N, 7) if mask[j]]
+    want = O.lmhead_logprob_fwd(h.double().numpy(), w.double().numpy(), y.numpy(), rows=rows)
+    lp = comb["logp"].cpu().numpy()
+    assert max(abs(lp[j] - want["logp"][j]) for j in rows) < TOL
+    assert bool((comb["logp"][~mask.bool()] == 0).all())
