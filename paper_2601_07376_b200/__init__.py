@@ -121,6 +121,42 @@ def _dev(t: torch.Tensor, name: str):
         raise ValueError(f"{name} must be contiguous")
 
 
+def _arr(t: Optional[torch.Tensor], name: str, dtype, numel: Optional[int], device, optional: bool = False,
+         at_least: bool = False):
+    """Marshalling check of a per-row / per-trajectory array: device, contiguity, dtype and size (the kernels
+    index these arrays by row, so a short array would be read out of bounds)."""
+    if t is None:
+        if optional:
+            return
+        raise ValueError(f"{name} is required")
+    _dev(t, name)
+    if t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if numel is not None and (t.numel() < numel if at_least else t.numel() != numel):
+        raise ValueError(f"{name} has {t.numel()} elements, expected {'>= ' if at_least else ''}{numel}")
+
+
+def _loss_args(logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss, cfg, dlogits, stats):
+    N = logits.shape[0]
+    dev = logits.device
+    _arr(targets, "targets", torch.int32, N, dev)
+    _arr(loss_mask, "loss_mask", torch.uint8, N, dev)
+    _arr(row_traj, "row_traj", torch.int32, N, dev)
+    _arr(adv, "adv", torch.float64, 1, dev, at_least=True)
+    _arr(old_logp, "old_logp", torch.float32, N, dev)
+    _arr(ref_logp, "ref_logp", torch.float32, N, dev, optional=True)   # required-ness: the C ABI checks it
+    _arr(n_loss, "n_loss", torch.int64, 1, dev)
+    _arr(stats, "stats", torch.float64, len(STATS_FIELDS), dev)
+    _arr(cfg.adv_index, "cfg.adv_index", torch.int32, N, dev, optional=True)
+    _arr(cfg.traj_loss_tokens, "cfg.traj_loss_tokens", torch.int64, None, dev, optional=True)
+    _arr(cfg.n_active_traj, "cfg.n_active_traj", torch.int64, 1, dev, optional=True)
+    _dev(dlogits, "dlogits")
+    if dlogits.shape != logits.shape or dlogits.dtype != logits.dtype:
+        raise ValueError("dlogits must have the logits' shape and dtype")
+
+
 def _stream(stream) -> Optional[int]:
     if stream is None:
         return torch.cuda.current_stream().cuda_stream
@@ -267,6 +303,10 @@ def otk_group_advantages(ctx: Context, group_id: torch.Tensor, num_groups: int, 
     _dev(group_id, "group_id")
     B = int(group_id.numel())
     dev = group_id.device
+    _arr(group_id, "group_id", torch.int32, B, dev)
+    _arr(returns, "returns", torch.float64, B, dev, optional=True)
+    _arr(turn_offsets, "turn_offsets", torch.int32, B + 1, dev, optional=True)
+    _arr(turn_rewards, "turn_rewards", torch.float64, None, dev, optional=True)
     o = out if out is not None else {}
     o.setdefault("adv", torch.empty(B, dtype=torch.float64, device=dev))
     o.setdefault("returns", torch.empty(B, dtype=torch.float64, device=dev))
@@ -287,6 +327,9 @@ def otk_turn_returns(ctx: Context, batch: DeviceTrajBatch, num_segments: int, gr
                      train_agent: int = OTK_ANY_AGENT, *, out: Optional[dict] = None, stream=None) -> dict:
     """(2') turn-level credit: per-segment reward-to-go of the trainable ACTION turns (otk.h otk_turn_returns)."""
     dev = batch.seg_offsets.device
+    _arr(group_id, "group_id", torch.int32, batch.num_traj, dev)
+    _arr(turn_offsets, "turn_offsets", torch.int32, batch.num_traj + 1, dev)
+    _arr(turn_rewards, "turn_rewards", torch.float64, None, dev)
     o = out if out is not None else {}
     o.setdefault("seg_return", torch.empty(num_segments, dtype=torch.float64, device=dev))
     o.setdefault("seg_group", torch.empty(num_segments, dtype=torch.int32, device=dev))
@@ -313,6 +356,8 @@ def otk_lmhead_logprob_fwd(ctx: Context, hidden: torch.Tensor, weight: torch.Ten
     V, d2 = weight.shape
     if d != d2:
         raise ValueError("hidden / weight inner dimensions differ")
+    _arr(targets, "targets", torch.int32, N, hidden.device)
+    _arr(row_mask, "row_mask", torch.uint8, N, hidden.device, optional=True)
     nbytes = int(_lib.otk_lmhead_workspace_bytes(ctx.handle, N, V))
     if workspace is None or workspace.numel() * workspace.element_size() < nbytes:
         workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=hidden.device)
@@ -339,6 +384,10 @@ def otk_lmhead_row_partials(ctx: Context, hidden: torch.Tensor, weight_shard: to
         _dev(t, n)
     N, d = hidden.shape
     Vl = weight_shard.shape[0]
+    if weight_shard.shape[1] != d or hidden.dtype != torch.bfloat16 or weight_shard.dtype != torch.bfloat16:
+        raise ValueError("hidden [N, d] and weight_shard [V_local, d] must be bfloat16 with the same d")
+    _arr(targets, "targets", torch.int32, N, hidden.device)
+    _arr(row_mask, "row_mask", torch.uint8, N, hidden.device, optional=True)
     nbytes = int(_lib.otk_lmhead_workspace_bytes(ctx.handle, N, Vl))
     if workspace is None or workspace.numel() * workspace.element_size() < nbytes:
         workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=hidden.device)
@@ -367,8 +416,7 @@ def otk_sample_tokens(ctx: Context, logits: torch.Tensor, uniforms: Optional[tor
         if uniforms is None:
             raise ValueError("uniforms are required unless greedy")
         _dev(uniforms, "uniforms")
-        if uniforms.dtype != torch.float32 or uniforms.numel() != N:
-            raise ValueError("uniforms must be float32 [num_rows]")
+        _arr(uniforms, "uniforms", torch.float32, N, logits.device)
     o = out if out is not None else {}
     o.setdefault("tokens", torch.empty(N, dtype=torch.int32, device=logits.device))
     if want_logp:
@@ -390,6 +438,8 @@ def otk_logprob_entropy_fwd(ctx: Context, logits: torch.Tensor, targets: torch.T
     N, ld = logits.shape
     V = ld if vocab is None else int(vocab)
     dev = logits.device
+    _arr(targets, "targets", torch.int32, N, dev)
+    _arr(row_mask, "row_mask", torch.uint8, N, dev, optional=True)
     o = out if out is not None else {}
     o.setdefault("logp", torch.empty(N, dtype=torch.float32, device=dev))
     o.setdefault("entropy", torch.empty(N, dtype=torch.float32, device=dev))
@@ -423,6 +473,7 @@ def otk_policy_loss_fwd_bwd(ctx: Context, logits: torch.Tensor, targets: torch.T
         entropy = torch.empty(N, dtype=torch.float32, device=dev)
     if stats is None:
         stats = torch.zeros(len(STATS_FIELDS), dtype=torch.float64, device=dev)
+    _loss_args(logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss, cfg, dlogits, stats)
     c = cfg.c(accumulate)
     _check(_lib.otk_policy_loss_fwd_bwd(ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits), _ptr(targets),
                                         _ptr(loss_mask), _ptr(row_traj), _ptr(adv), _ptr(old_logp),
@@ -462,8 +513,11 @@ def otk_row_partials(ctx: Context, logits: torch.Tensor, targets: torch.Tensor, 
     _dev(logits, "logits")
     N, ld = logits.shape
     V = ld if vocab_local is None else int(vocab_local)
+    _arr(targets, "targets", torch.int32, N, logits.device)
+    _arr(row_mask, "row_mask", torch.uint8, N, logits.device, optional=True)
     if partials is None:
         partials = torch.empty((N, 4), dtype=torch.float32, device=logits.device)
+    _arr(partials, "partials", torch.float32, 4 * N, logits.device)
     sh = otk_vocab_shard(int(vocab_start), int(vocab_total))
     _check(_lib.otk_row_partials(ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits), _ptr(targets),
                                  _ptr(row_mask), C.byref(sh), float(logit_scale), _ptr(partials), _stream(stream)))
@@ -474,8 +528,11 @@ def otk_logprob_entropy_combine(ctx: Context, partials: torch.Tensor, *, row_mas
                                 want_lse: bool = False, stream=None) -> dict:
     """partials: [nshards, N, 4] float32 (rank order)."""
     _dev(partials, "partials")
+    if partials.dim() != 3 or partials.shape[2] != 4 or partials.dtype != torch.float32:
+        raise ValueError("partials must be float32 [nshards, N, 4]")
     P, N, _ = partials.shape
     dev = partials.device
+    _arr(row_mask, "row_mask", torch.uint8, N, dev, optional=True)
     o = dict(logp=torch.empty(N, dtype=torch.float32, device=dev),
              entropy=torch.empty(N, dtype=torch.float32, device=dev))
     if want_lse:
@@ -502,6 +559,9 @@ def otk_policy_loss_fwd_bwd_partials(ctx: Context, logits: torch.Tensor, targets
         entropy = torch.empty(N, dtype=torch.float32, device=dev)
     if stats is None:
         stats = torch.zeros(len(STATS_FIELDS), dtype=torch.float64, device=dev)
+    _loss_args(logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss, cfg, dlogits, stats)
+    if partials.dim() != 3 or partials.shape[1:] != (N, 4) or partials.dtype != torch.float32:
+        raise ValueError("partials must be float32 [nshards, N, 4]")
     sh = otk_vocab_shard(int(vocab_start), int(vocab_total))
     c = cfg.c(accumulate)
     _check(_lib.otk_policy_loss_fwd_bwd_partials(

@@ -102,3 +102,24 @@ def test_empty_trajectories_in_batch(otk, ctx):
                                  turn_rewards=torch.from_numpy(tb.turn_rewards).cuda())
     want = O.group_advantages(tb.group_id, O.episode_returns(tb.turn_offsets, tb.turn_rewards), 2)["adv"]
     assert np.max(np.abs(a["adv"].cpu().numpy() - want)) < 1e-6
+
+
+def test_binding_rejects_malformed_arrays(otk, ctx):
+    """The binding checks dtype / size / device of every per-row array before the C call (a short array
+    would otherwise be read out of bounds by the kernels)."""
+    from synth import make_logits
+    n, V = 32, 1024
+    lg, tg = make_logits(n, V, dtype="bf16", seed=3, device="cuda")
+    with pytest.raises(ValueError):
+        otk.otk_logprob_entropy_fwd(ctx, lg, tg.long())                       # int64 targets
+    with pytest.raises(ValueError):
+        otk.otk_logprob_entropy_fwd(ctx, lg, tg[:-1].contiguous())            # short targets
+    args = dict(loss_mask=torch.ones(n, dtype=torch.uint8, device="cuda"),
+                row_traj=torch.zeros(n, dtype=torch.int32, device="cuda"),
+                adv=torch.ones(1, dtype=torch.float64, device="cuda"),
+                old_logp=torch.zeros(n - 1, device="cuda"), ref_logp=None,
+                n_loss=torch.full((1,), n, dtype=torch.int64, device="cuda"))
+    with pytest.raises(ValueError):
+        otk.otk_policy_loss_fwd_bwd(ctx, lg, tg, cfg=otk.LossCfg(kl_beta=0.0), **args)   # short old_logp
+    with pytest.raises(ValueError):
+        otk.otk_sample_tokens(ctx, lg, torch.rand(n, device="cuda", dtype=torch.float64))   # float64 uniforms
