@@ -406,9 +406,16 @@ def otk_lmhead_row_partials(ctx: Context, hidden: torch.Tensor, weight_shard: to
 # ------------------------------------------------------------------------------------------------
 def otk_sample_tokens(ctx: Context, logits: torch.Tensor, uniforms: Optional[torch.Tensor] = None, *,
                       logit_scale: float = 1.0, greedy: bool = False, vocab: Optional[int] = None,
-                      want_logp: bool = True, out: Optional[dict] = None, stream=None) -> dict:
+                      temperature: Optional[float] = None, want_logp: bool = True, out: Optional[dict] = None,
+                      stream=None) -> dict:
     """One token per row: inverse-transform draw from softmax(logit_scale * x) with the caller's uniforms,
-    or the greedy argmax (otk.h otk_sample_tokens)."""
+    or the greedy argmax (otk.h otk_sample_tokens). temperature (optional) sets logit_scale = 1/temperature;
+    below 1e-6 it means greedy."""
+    if temperature is not None:
+        if temperature < 1e-6:
+            greedy = True
+        else:
+            logit_scale = 1.0 / float(temperature)
     _dev(logits, "logits")
     N, ld = logits.shape
     V = ld if vocab is None else int(vocab)

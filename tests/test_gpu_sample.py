@@ -140,3 +140,15 @@ def test_sample_errors(otk, ctx):
     with pytest.raises(otk.OtkError) as e:
         ctx.check()
     assert e.value.status == 1                                   # OTK_ERR_INVALID_ARG: u outside [0, 1)
+
+
+def test_temperature_argument(otk, ctx):
+    """temperature = 1/logit_scale; temperature < 1e-6 is the greedy limit."""
+    from synth import make_logits
+    lg, _ = make_logits(64, 5000, dtype="bf16", seed=12, device="cuda")
+    u = torch.rand(64, device="cuda")
+    a = otk.otk_sample_tokens(ctx, lg, u, temperature=0.5)["tokens"]
+    b = otk.otk_sample_tokens(ctx, lg, u, logit_scale=2.0)["tokens"]
+    assert torch.equal(a, b)
+    g = otk.otk_sample_tokens(ctx, lg, u, temperature=1e-7)["tokens"]
+    assert torch.equal(g, otk.otk_sample_tokens(ctx, lg, greedy=True)["tokens"])
