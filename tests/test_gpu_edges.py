@@ -123,3 +123,41 @@ def test_binding_rejects_malformed_arrays(otk, ctx):
         otk.otk_policy_loss_fwd_bwd(ctx, lg, tg, cfg=otk.LossCfg(kl_beta=0.0), **args)   # short old_logp
     with pytest.raises(ValueError):
         otk.otk_sample_tokens(ctx, lg, torch.rand(n, device="cuda", dtype=torch.float64))   # float64 uniforms
+
+
+@pytest.mark.parametrize("dtype,V", [("bf16", 151936), ("f32", 151936), ("bf16", 262144), ("bf16", 33001)])
+def test_targets_on_segment_boundaries(otk, ctx, dtype, V):
+    """Targets on the first / last column of every CTA's column segment (row clusters split the vocabulary):
+    logp and the target column of dlogits (coef * (p_y - 1)) against the oracle."""
+    from synth import make_logits, make_noise
+    seg = None
+    for c in (1, 2, 4, 8):     # the row kernel's split (DESIGN.md §6): smallest power of two fitting 13 x 12 KB
+        s = ((V + c - 1) // c + 7) // 8 * 8
+        if s * (2 if dtype == "bf16" else 4) <= 13 * 12288:
+            seg = s
+            break
+    cols = sorted({0, V - 1} | {k * seg for k in range(1, (V + seg - 1) // seg)} |
+                  {k * seg - 1 for k in range(1, (V + seg - 1) // seg)} | {7, 8, V - 8})
+    n = len(cols)
+    ld = -(-V // 8) * 8                      # 16-byte rows
+    lg, _ = make_logits(n, V, ld=ld, dtype=dtype, seed=V % 1000 + 3, device="cpu")
+    tg = torch.tensor(cols, dtype=torch.int32)
+    wide = lg.double().numpy()[:, :V]
+    olp = np.array([O.row_forward(wide[j], cols[j])[0] for j in range(n)])
+    f = otk.otk_logprob_entropy_fwd(ctx, lg.cuda(), tg.cuda(), vocab=V)
+    ctx.check()
+    assert np.max(np.abs(f["logp"].cpu().numpy() - olp)) < (2e-3 if dtype == "bf16" else 1e-5)
+    old = (olp + make_noise(n, 0.05, 1).double().numpy()).astype(np.float32)
+    adv = torch.tensor([0.7], dtype=torch.float64)
+    out = otk.otk_policy_loss_fwd_bwd(ctx, lg.cuda(), tg.cuda(), torch.ones(n, dtype=torch.uint8).cuda(),
+                                      torch.zeros(n, dtype=torch.int32).cuda(), adv.cuda(),
+                                      torch.from_numpy(old).cuda(), None,
+                                      torch.tensor([n], dtype=torch.int64).cuda(), otk.LossCfg(kl_beta=0.0), vocab=V)
+    ctx.check()
+    want = O.policy_loss_fwd_bwd(wide, np.array(cols), np.ones(n, np.uint8), np.zeros(n, np.int32), adv.numpy(),
+                                 old.astype(np.float64), None, n, O.LossCfg(kl_beta=0.0))
+    g = out["dlogits"].double().cpu().numpy()
+    rel = 2.0 ** -7 if dtype == "bf16" else 1e-5
+    for j, y in enumerate(cols):
+        w = want["dlogits"][j][y]
+        assert abs(g[j, y] - w) <= rel * abs(w) + 1e-5 * abs(want["coef"][j]) + 1e-30, (j, y, g[j, y], w)
