@@ -695,6 +695,10 @@ __device__ __forceinline__ void finalize_rows(const RowParams& p, Smem& S, int l
   }
 }
 
+#ifdef OTK_PHASE_TIMING
+__device__ unsigned long long g_phase[8];  // experiments only: clock64 sums per phase (warp lane 0 of consumers)
+#endif
+
 // =====================================================================================================
 // k_rows_tm: FWD / PARTIAL / BWD. Pass 1 streams each chunk from the ring exactly once (slot released
 // right away); for BWD the exponentials e = 2^(y - m_c) (bf16 for bf16 input, with m_c the thread's
@@ -777,6 +781,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       return (g >= 0 && g < p.vocab) ? VT::load1(p.logits, r * p.ld + g) : 0.f;
     };
     float xy_n = (row < p.num_rows && row_active(p, y_n, m_n)) ? xy_of(row, y_n) : 0.f;
+#ifdef OTK_PHASE_TIMING
+    unsigned long long ph_a = 0, ph_b = 0, ph_c = 0, ph_d = 0, ph_in = 0;
+    long long t_prev = clock64();
+#endif
     for (; row < p.num_rows; row += ngroups) {
       const int32_t y = y_n;
       const uint8_t m = m_n;
@@ -796,6 +804,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       if (!row_active(p, y, m)) {
         inactive_row<T, MODE>(p, row, ct, crank, c0, segn, m != 0);
         if (nrow < p.num_rows && row_active(p, y_n, m_n)) xy_n = xy_of(nrow, y_n);
+#ifdef OTK_PHASE_TIMING
+        t_prev = clock64();
+#endif
         continue;
       }
       const int64_t ylc64 = int64_t(y) - p.vocab_start - c0;  // target column local to this CTA's segment
@@ -894,9 +905,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
         continue;
       }
       if (kBwd) tmem_wait_st();
+#ifdef OTK_PHASE_TIMING
+      const long long t_b = clock64();
+      ph_a += t_b - t_prev;
+#endif
 
       Stat tot;
       row_total(S, st, lane, cw, ct, csize, crank, q, tot);
+#ifdef OTK_PHASE_TIMING
+      const long long t_c = clock64();
+      ph_b += t_c - t_b;
+#endif
       const float dy = (yg >= 0 && yg < p.vocab) ? __fmaf_rn(xy, s2, -tot.m) : -INFINITY;
       if (MODE == kModePartial) {
         if (ct == 0 && crank == 0) p.partials_out[row] = make_float4(tot.m, tot.s, tot.t, dy);
@@ -981,10 +1000,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
             pass2(std::true_type{});
           // target column: coef * (p_y - 1), overwriting this thread's own vector store (program order)
           if (ct == owner_ct) VT::store1(drow, ylc, lo.gy);
+#ifdef OTK_PHASE_TIMING
+          ph_c += clock64() - t_c;
+#endif
         }
       }
       ++q;
+#ifdef OTK_PHASE_TIMING
+      t_prev = clock64();
+#endif
     }
+#ifdef OTK_PHASE_TIMING
+    if (kBwd && lane == 0) {
+      atomicAdd(&g_phase[0], ph_a);
+      atomicAdd(&g_phase[1], ph_b);
+      atomicAdd(&g_phase[2], ph_c);
+      atomicAdd(&g_phase[3], 1ull);
+    }
+#endif
     if (kBwd && ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl);
   }
   tc_fence_before();
@@ -1222,3 +1255,11 @@ cudaError_t launch_combine(const otk_ctx* ctx, int64_t num_rows, int nshards, co
 }
 
 }  // namespace otk
+
+#ifdef OTK_PHASE_TIMING
+extern "C" void otk_debug_phase(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, otk::g_phase, sizeof(unsigned long long) * 8);
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbol(otk::g_phase, z, sizeof(z));
+}
+#endif
