@@ -298,13 +298,14 @@ struct Smem {
 constexpr int kZeroBytes = 4096;  // zero block: source of the bulk stores that zero-fill masked rows
 constexpr size_t kRingBytes = size_t(kSlots) * kChunkBytes;
 constexpr size_t kSmemBytes = kRingBytes + kZeroBytes + sizeof(Smem);
+constexpr size_t smem_bytes_for(int ns) { return size_t(ns) * kChunkBytes + kZeroBytes + sizeof(Smem); }
 
 __device__ __forceinline__ bool row_active(const RowParams& p, int32_t y, uint8_t m) {
   return m && y >= 0 && int64_t(y) < p.vocab_total;
 }
 
 // ---- loader (warp 0, one thread): bulk-TMA every active row's column segment, chunk by chunk, into the ring
-template <typename T>
+template <typename T, int NS = kSlots>
 __device__ __forceinline__ void load_rows(const RowParams& p, uint8_t* ring, Smem& S, int64_t group, int64_t ngroups,
                                           int64_t c0, uint32_t seg_bytes, int nch) {
   const uint64_t pol = policy_evict_first();
@@ -331,7 +332,7 @@ __device__ __forceinline__ void load_rows(const RowParams& p, uint8_t* ring, Sme
       mbar_arrive_expect_tx(&S.full[slot], bytes);
       bulk_g2s(ring + size_t(slot) * kChunkBytes, src + off, bytes, &S.full[slot], pol);
       off += kChunkBytes;
-      if (++slot == kSlots) {
+      if (++slot == NS) {
         slot = 0;
         phase ^= 1u;
       }
@@ -708,13 +709,14 @@ __device__ unsigned long long g_phase[8];  // experiments only: clock64 sums per
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr bool kBwd = (MODE == kModeBwd);
+  constexpr int NS = kBwd ? kSlots : kSlotsFwd;  // ring slots (FWD / PARTIAL: two CTAs per SM)
   uint8_t* ring = smem;
-  uint8_t* zero = smem + kRingBytes;
-  Smem& S = *reinterpret_cast<Smem*>(smem + kRingBytes + kZeroBytes);
+  uint8_t* zero = smem + size_t(NS) * kChunkBytes;
+  Smem& S = *reinterpret_cast<Smem*>(smem + size_t(NS) * kChunkBytes + kZeroBytes);
   using VT = Vec<T>;
   constexpr int EV = VT::EV;
   constexpr int CE = kChunkBytes / int(sizeof(T));
-  constexpr bool kBwd = (MODE == kModeBwd);
   constexpr int kColM = 8 * kMaxChunks;  // per-thread TMEM columns: [0, 8*kMaxChunks) e, then m_c
   static_assert(kColM + kMaxChunks <= kTmemWindow, "TMEM window too small");
   static_assert(kConsumerWarps / 4 * kTmemWindow <= 512, "TMEM has 512 columns");
@@ -733,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
   row_kernel_setup<kBwd>(S, zero, warp, csize);
 
   if (warp == 0) {
-    if (lane == 0 && nch > 0) load_rows<T>(p, ring, S, group, ngroups, c0, seg_bytes, nch);
+    if (lane == 0 && nch > 0) load_rows<T, NS>(p, ring, S, group, ngroups, c0, seg_bytes, nch);
     __syncwarp();
   } else if (warp == kConsumerWarps + 1) {
     if (kBwd) {
@@ -838,7 +840,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty[slot]);
-        if (++slot == kSlots) {
+        if (++slot == NS) {
           slot = 0;
           phase ^= 1u;
         }
@@ -1175,10 +1177,10 @@ __global__ void k_combine(int64_t num_rows, int nshards, const float4* __restric
 // ---- launchers ---------------------------------------------------------------------------------------
 template <typename KernelT>
 static cudaError_t launch_row_kernel(KernelT kern, const otk_ctx* ctx, const RowParams& p, cudaStream_t s,
-                                     int* grid_out) {
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes));
+                                     int* grid_out, size_t smem_bytes = kSmemBytes, int ctas_per_sm = 1) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes));
   if (e != cudaSuccess) return e;
-  int64_t groups = ctx->num_sms / p.csize;
+  int64_t groups = int64_t(ctx->num_sms) * ctas_per_sm / p.csize;
   if (groups > p.num_rows) groups = p.num_rows;
   if (groups < 1) groups = 1;
   const int grid = int(groups * p.csize);
@@ -1186,7 +1188,7 @@ static cudaError_t launch_row_kernel(KernelT kern, const otk_ctx* ctx, const Row
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1201,18 +1203,19 @@ static cudaError_t launch_row_kernel(KernelT kern, const otk_ctx* ctx, const Row
 
 cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const RowParams& p, cudaStream_t s,
                         int* grid_out) {
+  constexpr size_t kFwdSmem = smem_bytes_for(kSlotsFwd);  // ~104 KB: two CTAs per SM
   if (dtype == OTK_BF16) {
     using B = __nv_bfloat16;
     switch (mode) {
-      case kModeFwd: return launch_row_kernel(k_rows_tm<B, kModeFwd>, ctx, p, s, grid_out);
-      case kModePartial: return launch_row_kernel(k_rows_tm<B, kModePartial>, ctx, p, s, grid_out);
+      case kModeFwd: return launch_row_kernel(k_rows_tm<B, kModeFwd>, ctx, p, s, grid_out, kFwdSmem, 2);
+      case kModePartial: return launch_row_kernel(k_rows_tm<B, kModePartial>, ctx, p, s, grid_out, kFwdSmem, 2);
       case kModeBwd: return launch_row_kernel(k_rows_tm<B, kModeBwd>, ctx, p, s, grid_out);
       case kModeBwdPartials: return launch_row_kernel(k_rows_stream<B>, ctx, p, s, grid_out);
     }
   } else {
     switch (mode) {
-      case kModeFwd: return launch_row_kernel(k_rows_tm<float, kModeFwd>, ctx, p, s, grid_out);
-      case kModePartial: return launch_row_kernel(k_rows_tm<float, kModePartial>, ctx, p, s, grid_out);
+      case kModeFwd: return launch_row_kernel(k_rows_tm<float, kModeFwd>, ctx, p, s, grid_out, kFwdSmem, 2);
+      case kModePartial: return launch_row_kernel(k_rows_tm<float, kModePartial>, ctx, p, s, grid_out, kFwdSmem, 2);
       case kModeBwd: return launch_row_kernel(k_rows_tm<float, kModeBwd>, ctx, p, s, grid_out);
       case kModeBwdPartials: return launch_row_kernel(k_rows_stream<float>, ctx, p, s, grid_out);
     }

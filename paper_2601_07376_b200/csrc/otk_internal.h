@@ -38,6 +38,7 @@ enum Ticket { kTicketMasks = 0, kTicketRows = 1 };
 // 2 x 16-byte vectors per consumer thread.
 constexpr int kChunkBytes = 12288;       // one bulk-TMA transfer / ring slot
 constexpr int kSlots = 18;               // ring depth: 216 KB of shared memory per CTA
+constexpr int kSlotsFwd = 8;             // FWD / PARTIAL: 96 KB ring, so two CTAs share an SM (twice the warps)
 constexpr int kConsumerWarps = 12;       // 384 compute threads
 constexpr int kThreads = 32 * (2 + kConsumerWarps);  // + loader warp 0 + zero-fill warp 13
 constexpr int kMaxChunks = 13;           // a CTA's row segment (<= 13 chunks, 156 KB) is kept in TMEM
