@@ -15,7 +15,8 @@
  *   rollout sampling (NEXT-3): otk_sample_tokens — softmax / greedy token per row
  *   vocab sharding (north_star "vocab-sharding logits with an all-reduce of row max and sum-exp"):
  *       otk_row_partials → (caller all-gathers partials) → otk_logprob_entropy_combine /
- *       otk_policy_loss_fwd_bwd_partials.
+ *       otk_policy_loss_fwd_bwd_partials; or, fused: otk_policy_loss_fwd_bwd_vpf (the exchange runs inside
+ *       the kernel over NVLink peer memory, one read of the shard).
  *
  * Conventions (all entry points):
  *  - Pointers are DEVICE pointers unless stated otherwise. All buffers are caller-owned; the library
@@ -59,7 +60,8 @@ typedef enum {
   OTK_ERR_BAD_TRAJECTORY = 7,/* segment lengths/sources inconsistent with the row count     */
   OTK_ERR_TARGET_RANGE = 8,  /* target outside [0, vocab_total)                             */
   OTK_ERR_CUDA = 9,          /* a CUDA runtime call failed (see otk_last_error)             */
-  OTK_ERR_GROUP_RANGE = 10   /* group_id outside [0, num_groups)                            */
+  OTK_ERR_GROUP_RANGE = 10,  /* group_id outside [0, num_groups)                            */
+  OTK_ERR_PEER_TIMEOUT = 11  /* K4-VPF: a peer rank's row partial did not arrive in time     */
 } otk_status;
 
 typedef enum { OTK_SRC_CONTEXT = 0, OTK_SRC_ACTION = 1, OTK_SRC_OBSERVATION = 2, OTK_SRC_PAD = 3 } otk_source;
@@ -275,6 +277,57 @@ otk_status otk_policy_loss_fwd_bwd_partials(otk_ctx* ctx, int64_t num_rows, int6
                                             const otk_loss_cfg* cfg, const otk_vocab_shard* shard,
                                             int32_t nshards, const float* partials, void* dlogits, float* logp,
                                             float* entropy, otk_loss_stats* stats, otk_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * (4) on a vocab shard with the exchange fused into the kernel (K4-VPF; SURVEY.md §8(e) VOCAB row,
+ * DESIGN.md §7). Same result as otk_row_partials -> all-gather -> otk_policy_loss_fwd_bwd_partials
+ * (logp / entropy / loss stats bitwise equal; dlogits within the bf16 tolerance of (4)), but in ONE launch
+ * per rank and ONE read of the shard: after pass 1 of a row, the CTA pushes the row's 16-byte partial
+ * (m2, s, t2, w — the otk_row_partials form) into every peer's exchange buffer over NVLink (P2P stores of
+ * four 64-bit words, each = value | call epoch << 32, so every word validates itself and no memory fence
+ * is needed), waits until the peers' words of the same row carry this call's epoch,
+ * combines them in rank order (identical on every rank) and runs pass 2 from the tensor-memory-resident
+ * exponentials. The all-reduce of row max / sum-exp the north_star names is this exchange.
+ *   xchg[q]   : device pointer, valid in THIS process, to rank q's exchange buffer (xchg[rank] = own
+ *               buffer; peers' buffers mapped with otk_ipc_open, or plain buffers of the same device when
+ *               several ranks share one GPU), each otk_vpf_xchg_bytes(rows_cap, nranks) bytes, 16-byte
+ *               aligned, ZEROED once before the first call and then owned by the library's calls.
+ *   epoch     : 1 for the first call on a buffer set, +1 per call (all ranks in lockstep).
+ *   max_ctas  : 0 = one CTA per SM; otherwise at most this many CTAs (lets several ranks share a GPU).
+ * Every rank must make the same sequence of calls with the same num_rows / masks / targets; a partial that
+ * does not arrive within ~20 s sets OTK_ERR_PEER_TIMEOUT (sticky; later waits give up at once) instead of
+ * hanging. Requires nranks <= OTK_VPF_MAX_RANKS and num_rows <= rows_cap.
+ * ------------------------------------------------------------------------------------------- */
+#define OTK_VPF_MAX_RANKS 8
+typedef struct {
+  int32_t rank;
+  int32_t nranks;
+  int64_t rows_cap;
+  void* xchg[OTK_VPF_MAX_RANKS];
+  uint32_t epoch;
+  int32_t max_ctas;
+} otk_vpf_peers;
+
+int64_t otk_vpf_xchg_bytes(int64_t rows_cap, int32_t nranks); /* -1: bad args */
+otk_status otk_policy_loss_fwd_bwd_vpf(otk_ctx* ctx, int64_t num_rows, int64_t vocab_local, int64_t ld,
+                                       otk_dtype dtype, const void* logits, const int32_t* targets,
+                                       const uint8_t* loss_mask, const int32_t* row_traj, const double* adv,
+                                       const float* old_logp, const float* ref_logp, const int64_t* n_loss,
+                                       const otk_loss_cfg* cfg, const otk_vocab_shard* shard,
+                                       const otk_vpf_peers* peers /* host struct */, void* dlogits, float* logp,
+                                       float* entropy, otk_loss_stats* stats, otk_stream_t stream);
+
+/* Exchange buffers and their CUDA IPC plumbing (setup, not the hot path). otk_xchg_alloc: a zeroed device
+ * buffer of `bytes` on the ctx's device (its own cudaMalloc allocation, so an IPC handle maps exactly it);
+ * free with otk_xchg_free. For ranks on different GPUs of one node: otk_ipc_get_handle (cudaIpcGetMemHandle)
+ * gives 64 opaque bytes the caller exchanges (e.g. an all-gather over torch.distributed); otk_ipc_open
+ * (cudaIpcOpenMemHandle, peer access enabled) maps a peer's buffer into this process; otk_ipc_close unmaps. */
+#define OTK_IPC_HANDLE_BYTES 64
+otk_status otk_xchg_alloc(otk_ctx* ctx, int64_t bytes, void** dev_ptr_out);
+otk_status otk_xchg_free(otk_ctx* ctx, void* dev_ptr);
+otk_status otk_ipc_get_handle(const void* dev_ptr /* from otk_xchg_alloc */, void* handle_out /* 64 B, host */);
+otk_status otk_ipc_open(const void* handle /* host */, void** dev_ptr_out);
+otk_status otk_ipc_close(void* dev_ptr);
 
 /* ---------------------------------------------------------------------------------------------
  * Rollout-side token sampling (R32). PAPER.md:170-171 GENERATING

@@ -3,7 +3,7 @@
 Thin ctypes binding over ``libotk.so`` (C ABI, ``include/otk.h``). Functions carry the C names and
 only marshal arguments: every step of the path runs in the library's sm_100a kernels. torch supplies
 device memory and streams. There is no CPU fallback: importing this package without the built
-library raises ImportError (build it with ``python -m paper_2601_07376_b200.build``).
+library raises ImportError (build it with ``python paper_2601_07376_b200/build.py``).
 """
 from __future__ import annotations
 
@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("OTK_LIB") or os.path.join(HERE, "libotk.so")  # OTK_LIB: experiment builds only
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2601_07376_b200.build` "
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2601_07376_b200/build.py` "
                       "(the otk hot path has no CPU fallback)")
 _lib = C.CDLL(LIB_PATH)
 
@@ -30,7 +30,8 @@ CONTEXT, ACTION, OBSERVATION, PAD = 0, 1, 2, 3
 
 STATUS = {0: "OTK_OK", 1: "OTK_ERR_INVALID_ARG", 2: "OTK_ERR_SHAPE", 3: "OTK_ERR_ALIGNMENT", 4: "OTK_ERR_DTYPE",
           5: "OTK_ERR_EMPTY_GROUP", 6: "OTK_ERR_UNTERMINATED", 7: "OTK_ERR_BAD_TRAJECTORY",
-          8: "OTK_ERR_TARGET_RANGE", 9: "OTK_ERR_CUDA", 10: "OTK_ERR_GROUP_RANGE"}
+          8: "OTK_ERR_TARGET_RANGE", 9: "OTK_ERR_CUDA", 10: "OTK_ERR_GROUP_RANGE",
+          11: "OTK_ERR_PEER_TIMEOUT"}
 
 
 class OtkError(RuntimeError):
@@ -59,6 +60,15 @@ OTK_TOKEN_MEAN, OTK_SEQ_MEAN_TOKEN_MEAN, OTK_SEQ_MEAN_TOKEN_SUM = 0, 1, 2
 
 class otk_vocab_shard(C.Structure):
     _fields_ = [("vocab_start", C.c_int64), ("vocab_total", C.c_int64)]
+
+
+OTK_VPF_MAX_RANKS = 8
+OTK_IPC_HANDLE_BYTES = 64
+
+
+class otk_vpf_peers(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("rows_cap", C.c_int64),
+                ("xchg", C.c_void_p * OTK_VPF_MAX_RANKS), ("epoch", C.c_uint32), ("max_ctas", C.c_int32)]
 
 
 STATS_FIELDS = ("loss", "n_clipped", "kl_sum", "entropy_sum", "n_tokens")   # otk_loss_stats (5 doubles)
@@ -94,6 +104,15 @@ _sig = {
     "otk_policy_loss_fwd_bwd_partials": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, _P, _P, _P, _P,
                                                    _P, C.POINTER(otk_loss_cfg), C.POINTER(otk_vocab_shard),
                                                    C.c_int32, _P, _P, _P, _P, _P, _P]),
+    "otk_vpf_xchg_bytes": (_I64, [_I64, C.c_int32]),
+    "otk_policy_loss_fwd_bwd_vpf": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, _P, _P, _P, _P, _P,
+                                              C.POINTER(otk_loss_cfg), C.POINTER(otk_vocab_shard),
+                                              C.POINTER(otk_vpf_peers), _P, _P, _P, _P, _P]),
+    "otk_xchg_alloc": (C.c_int, [_P, _I64, C.POINTER(C.c_void_p)]),
+    "otk_xchg_free": (C.c_int, [_P, _P]),
+    "otk_ipc_get_handle": (C.c_int, [_P, _P]),
+    "otk_ipc_open": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
+    "otk_ipc_close": (C.c_int, [_P]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -578,5 +597,137 @@ def otk_policy_loss_fwd_bwd_partials(ctx: Context, logits: torch.Tensor, targets
     return dict(dlogits=dlogits, logp=logp, entropy=entropy, stats=stats)
 
 
+# ---- K4-VPF: vocab-sharded (4) with the row-partial exchange inside the kernel (otk.h otk_policy_loss_fwd_bwd_vpf)
+def otk_vpf_xchg_bytes(rows_cap: int, nranks: int) -> int:
+    n = int(_lib.otk_vpf_xchg_bytes(int(rows_cap), int(nranks)))
+    if n < 0:
+        raise ValueError("otk_vpf_xchg_bytes: bad rows_cap / nranks")
+    return n
+
+
+def otk_xchg_alloc(ctx: "Context", nbytes: int) -> int:
+    out = C.c_void_p()
+    _check(_lib.otk_xchg_alloc(ctx.handle, int(nbytes), C.byref(out)))
+    return int(out.value)
+
+
+def otk_xchg_free(ctx: "Context", ptr: int):
+    _check(_lib.otk_xchg_free(ctx.handle, C.c_void_p(int(ptr))))
+
+
+def otk_ipc_get_handle(ptr: int) -> bytes:
+    h = C.create_string_buffer(OTK_IPC_HANDLE_BYTES)
+    _check(_lib.otk_ipc_get_handle(C.c_void_p(int(ptr)), h))
+    return h.raw
+
+
+def otk_ipc_open(handle: bytes) -> int:
+    if len(handle) != OTK_IPC_HANDLE_BYTES:
+        raise ValueError("IPC handle must be OTK_IPC_HANDLE_BYTES bytes")
+    out = C.c_void_p()
+    _check(_lib.otk_ipc_open(C.create_string_buffer(bytes(handle), OTK_IPC_HANDLE_BYTES), C.byref(out)))
+    return int(out.value)
+
+
+def otk_ipc_close(ptr: int):
+    _check(_lib.otk_ipc_close(C.c_void_p(int(ptr))))
+
+
+class VpfExchange:
+    """One rank's view of the K4-VPF exchange buffers: the device address of every rank's buffer as seen from
+    this process (ptrs[rank] = own buffer from otk_xchg_alloc; peers' mapped with otk_ipc_open, or — ranks sharing
+    one GPU — the peers' own buffers). Keeps the per-call epoch (1, 2, ...), which all ranks advance in lockstep.
+    close() unmaps the opened peers and frees the owned buffer."""
+
+    def __init__(self, rank: int, nranks: int, rows_cap: int, ptrs, *, max_ctas: int = 0, opened=(),
+                 owner: Optional["Context"] = None):
+        if not (0 <= rank < nranks <= OTK_VPF_MAX_RANKS) or len(ptrs) != nranks:
+            raise ValueError("need 0 <= rank < nranks <= OTK_VPF_MAX_RANKS and one pointer per rank")
+        self.rank, self.nranks, self.rows_cap = rank, nranks, int(rows_cap)
+        self.ptrs, self.max_ctas, self.epoch, self.opened = [int(x) for x in ptrs], int(max_ctas), 0, list(opened)
+        self.owner = owner
+
+    @staticmethod
+    def local_group(ctxs, rows_cap: int, max_ctas: int = 0):
+        """Exchanges of len(ctxs) ranks that share ONE process (e.g. ranks co-scheduled on one GPU, each with
+        its own ctx and stream): plain device buffers, no IPC."""
+        P = len(ctxs)
+        ptrs = [otk_xchg_alloc(c, otk_vpf_xchg_bytes(rows_cap, P)) for c in ctxs]
+        return [VpfExchange(r, P, rows_cap, ptrs, max_ctas=max_ctas, owner=ctxs[r]) for r in range(P)]
+
+    def next_peers(self) -> otk_vpf_peers:
+        self.epoch += 1
+        pp = otk_vpf_peers(self.rank, self.nranks, self.rows_cap)
+        for q, a in enumerate(self.ptrs):
+            pp.xchg[q] = a
+        pp.epoch = self.epoch
+        pp.max_ctas = self.max_ctas
+        return pp
+
+    def close(self):
+        for a in self.opened:
+            otk_ipc_close(a)
+        self.opened = []
+        if self.owner is not None:
+            otk_xchg_free(self.owner, self.ptrs[self.rank])
+            self.owner = None
+
+
+def _row_view(t: torch.Tensor, name: str):
+    """(rows, ld) of a 2-D row-major tensor whose rows may be a column slice of a wider buffer (stride(1) == 1)."""
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dim() != 2 or t.stride(1) != 1 or (t.shape[0] > 1 and t.stride(0) < t.shape[1]):
+        raise ValueError(f"{name} must be 2-D with unit column stride")
+    return t.shape[0], (t.stride(0) if t.shape[0] > 1 else t.shape[1])
+
+
+def otk_policy_loss_fwd_bwd_vpf(ctx: Context, logits: torch.Tensor, targets, loss_mask, row_traj, adv, old_logp,
+                                ref_logp, n_loss, cfg: LossCfg, vocab_start: int, vocab_total: int,
+                                xchg: VpfExchange, *, dlogits: Optional[torch.Tensor] = None, logp=None,
+                                entropy=None, stats=None, accumulate: Optional[bool] = None, stream=None) -> dict:
+    """logits: this rank's shard [N, vocab_local] (may be a column slice of a wider row buffer); dlogits the
+    same shape (default: a new contiguous tensor)."""
+    N, ld = _row_view(logits, "logits")
+    V = logits.shape[1]
+    dev = logits.device
+    if dlogits is None:   # same row stride as the logits (the C ABI takes one ld for both)
+        dlogits = torch.empty((N, max(ld, V)), dtype=logits.dtype, device=dev)[:, :V]
+    Nd, ldd = _row_view(dlogits, "dlogits")
+    if dlogits.shape != logits.shape or dlogits.dtype != logits.dtype or ldd != ld:
+        raise ValueError("dlogits must have the logits' shape, dtype and row stride")
+    if logp is None:
+        logp = torch.empty(N, dtype=torch.float32, device=dev)
+    if entropy is None:
+        entropy = torch.empty(N, dtype=torch.float32, device=dev)
+    if stats is None:
+        stats = torch.zeros(len(STATS_FIELDS), dtype=torch.float64, device=dev)
+    _arr(targets, "targets", torch.int32, N, dev)
+    _arr(loss_mask, "loss_mask", torch.uint8, N, dev)
+    _arr(row_traj, "row_traj", torch.int32, N, dev)
+    _arr(adv, "adv", torch.float64, 1, dev, at_least=True)
+    _arr(old_logp, "old_logp", torch.float32, N, dev)
+    _arr(ref_logp, "ref_logp", torch.float32, N, dev, optional=True)
+    _arr(n_loss, "n_loss", torch.int64, 1, dev)
+    _arr(stats, "stats", torch.float64, len(STATS_FIELDS), dev)
+    _arr(logp, "logp", torch.float32, N, dev)
+    _arr(entropy, "entropy", torch.float32, N, dev)
+    _arr(cfg.adv_index, "cfg.adv_index", torch.int32, N, dev, optional=True)
+    _arr(cfg.traj_loss_tokens, "cfg.traj_loss_tokens", torch.int64, None, dev, optional=True)
+    _arr(cfg.n_active_traj, "cfg.n_active_traj", torch.int64, 1, dev, optional=True)
+    sh = otk_vocab_shard(int(vocab_start), int(vocab_total))
+    c = cfg.c(accumulate)
+    peers = xchg.next_peers()
+    st = _lib.otk_policy_loss_fwd_bwd_vpf(
+        ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits), _ptr(targets), _ptr(loss_mask), _ptr(row_traj),
+        _ptr(adv), _ptr(old_logp), _ptr(ref_logp), _ptr(n_loss), C.byref(c), C.byref(sh), C.byref(peers),
+        _ptr(dlogits), _ptr(logp), _ptr(entropy), _ptr(stats), _stream(stream))
+    if st != 0:
+        xchg.epoch -= 1   # nothing was launched: the ranks' epochs must stay in lockstep
+        _check(st)
+    return dict(dlogits=dlogits, logp=logp, entropy=entropy, stats=stats)
+
+
 __all__ = [n for n in list(globals()) if n.startswith("otk_") or n in (
-    "Context", "LossCfg", "OtkError", "DeviceTrajBatch", "traj_batch_to_device", "stats_dict", "EXPORTED")]
+    "Context", "LossCfg", "OtkError", "DeviceTrajBatch", "traj_batch_to_device", "stats_dict", "EXPORTED",
+    "VpfExchange")]

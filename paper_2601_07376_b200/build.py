@@ -1,6 +1,6 @@
 """Build libotk.so (the C-ABI library) in-tree with nvcc for sm_100a.
 
-    python -m paper_2601_07376_b200.build [--force] [--verbose]
+    python paper_2601_07376_b200/build.py [--force] [--verbose]
 
 The .so is git-ignored but travels to the GPU box with the gpurun snapshot.
 """

@@ -97,6 +97,76 @@ __device__ __forceinline__ Stat combine_partials(const float4* P, int64_t stride
   return tot;
 }
 
+// ---- K4-VPF exchange buffer (one per rank, include/otk.h otk_vpf_peers): [2 parities][rows_cap][P] records of
+// 32 bytes = four 64-bit words (value bits | epoch << 32) for m2, s, t2, w. Record (par, row, q) of rank p's
+// buffer is written by rank q; a reader accepts it when all four words carry the call's epoch (each word is
+// single-copy atomic, so a record is never half old, half new). Parity = epoch & 1: a rank can run at most
+// one call ahead of a peer (it needs the peer's records of every row to finish a call), so the two record
+// sets never collide.
+__host__ __device__ __forceinline__ int64_t vpf_rec_index(int64_t cap, int nranks, uint32_t par, int64_t row, int q) {
+  return (int64_t(par) * cap + row) * nranks + q;
+}
+constexpr uint64_t kVpfTimeoutNs = 20ull * 1000000000ull;
+__device__ __forceinline__ uint64_t vpf_word(float v, uint32_t ep) {
+  return uint64_t(__float_as_uint(v)) | (uint64_t(ep) << 32);
+}
+
+// Called by one thread per CTA (ct == 0) after the CTA's (cluster's) row total: push this rank's partial
+// `mine` = (m2, s, t2, w) to every peer (cluster rank 0 only), collect the peers' records of the same row and
+// combine all P in rank order exactly as combine_partials does. Identical bits on every rank.
+__device__ __forceinline__ Stat vpf_exchange(const RowParams& p, int64_t row, uint32_t crank, float4 mine, float& dy) {
+  const int P = p.vpf_nranks, me = p.vpf_rank;
+  const uint32_t par = p.vpf_epoch & 1u, ep = p.vpf_epoch;
+  const int64_t cap = p.vpf_rows_cap;
+  if (crank == 0) {
+    const int64_t i = vpf_rec_index(cap, P, par, row, me) * 32;
+    const uint64_t w0 = vpf_word(mine.x, ep), w1 = vpf_word(mine.y, ep), w2 = vpf_word(mine.z, ep),
+                   w3 = vpf_word(mine.w, ep);
+    for (int q = 0; q < P; ++q) {
+      if (q == me) continue;
+      char* b = reinterpret_cast<char*>(p.vpf_xchg[q]) + i;
+      st_pair_sys(b, w0, w1);
+      st_pair_sys(b + 16, w2, w3);
+    }
+  }
+  const char* own = reinterpret_cast<const char*>(p.vpf_xchg[me]);
+  Stat tot{-INFINITY, 0.f, 0.f};
+  float4 rec[OTK_VPF_MAX_RANKS];
+  for (int q = 0; q < P; ++q) {
+    if (q == me) {
+      rec[q] = mine;
+    } else {
+      const char* r = own + vpf_rec_index(cap, P, par, row, q) * 32;
+      uint64_t a0, a1, a2, a3;
+      auto ready = [&]() {
+        ld_pair_sys(r, a0, a1);
+        ld_pair_sys(r + 16, a2, a3);
+        return uint32_t(a0 >> 32) == ep && uint32_t(a1 >> 32) == ep && uint32_t(a2 >> 32) == ep &&
+               uint32_t(a3 >> 32) == ep;
+      };
+      bool ok = ready();
+      if (!ok) {
+        const uint64_t t0 = globaltimer_ns();
+        while (!(ok = ready())) {
+          if (*reinterpret_cast<volatile int*>(p.err) != 0) break;  // an earlier timeout / error: give up at once
+          if (globaltimer_ns() - t0 > kVpfTimeoutNs) {
+            set_error(p.err, OTK_ERR_PEER_TIMEOUT);
+            break;
+          }
+        }
+      }
+      rec[q] = ok ? make_float4(__uint_as_float(uint32_t(a0)), __uint_as_float(uint32_t(a1)),
+                                __uint_as_float(uint32_t(a2)), __uint_as_float(uint32_t(a3)))
+                  : make_float4(-INFINITY, 0.f, 0.f, -INFINITY);
+    }
+    tot = combine(tot, Stat{rec[q].x, rec[q].y, rec[q].z});
+  }
+  dy = -INFINITY;
+  for (int q = 0; q < P; ++q)
+    if (rec[q].w != -INFINITY) dy = __fadd_rn(rec[q].w, __fsub_rn(rec[q].x, tot.m));
+  return tot;
+}
+
 // One element pair of pass 1: d = s2*x - m; e = 2^d; S += e; T += e*d (per-lane fp32 chains; kInit starts
 // the chains instead of adding to them).
 template <bool kInit>
@@ -293,6 +363,7 @@ struct Smem {
   uint64_t fempty[4];                 // the finalizer has read slot k (count 1)
   float4 fred[4][kConsumerWarps];
   float4 rowbc[2];                    // (stream kernel) row broadcast
+  float4 vbc[2];                      // (K4-VPF) the rank-order row total + dy, broadcast by thread 0
   uint32_t tmem_base;
 };
 constexpr int kZeroBytes = 4096;  // zero block: source of the bulk stores that zero-fill masked rows
@@ -373,7 +444,7 @@ __device__ __forceinline__ void inactive_row(const RowParams& p, int64_t row, in
                                              int segn, bool bad_target) {
   if (bad_target && ct == 0 && crank == 0) set_error(p.err, OTK_ERR_TARGET_RANGE);
   if (ct != 0) return;
-  if (MODE == kModeBwd || MODE == kModeBwdPartials) {
+  if (MODE == kModeBwd || MODE == kModeBwdPartials || MODE == kModeBwdVpf) {
     if (p.zero_masked) {
       char* base = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
       const int done = int(((uint32_t(segn) * uint32_t(sizeof(T))) & ~15u) / sizeof(T));
@@ -709,7 +780,8 @@ __device__ unsigned long long g_phase[8];  // experiments only: clock64 sums per
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr bool kBwd = (MODE == kModeBwd);
+  constexpr bool kVpf = (MODE == kModeBwdVpf);  // BWD with the vocab-shard exchange fused in
+  constexpr bool kBwd = (MODE == kModeBwd) || kVpf;
   constexpr int NS = kBwd ? kSlots : kSlotsFwd;  // ring slots (FWD / PARTIAL: two CTAs per SM)
   uint8_t* ring = smem;
   uint8_t* zero = smem + size_t(NS) * kChunkBytes;
@@ -918,7 +990,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       const long long t_c = clock64();
       ph_b += t_c - t_b;
 #endif
-      const float dy = (yg >= 0 && yg < p.vocab) ? __fmaf_rn(xy, s2, -tot.m) : -INFINITY;
+      float dy = (yg >= 0 && yg < p.vocab) ? __fmaf_rn(xy, s2, -tot.m) : -INFINITY;
+      if constexpr (kVpf) {  // this rank's partial -> peers; peers' partials -> rank-order total (global row)
+        if (ct == 0) {
+          float gdy;
+          const Stat g = vpf_exchange(p, row, crank, make_float4(tot.m, tot.s, tot.t, dy), gdy);
+          S.vbc[q & 1u] = make_float4(g.m, g.s, g.t, gdy);
+        }
+        named_bar_sync(2, kNCT);
+        const float4 b = S.vbc[q & 1u];
+        tot = Stat{b.x, b.y, b.z};
+        dy = b.w;
+      }
       if (MODE == kModePartial) {
         if (ct == 0 && crank == 0) p.partials_out[row] = make_float4(tot.m, tot.s, tot.t, dy);
       } else {
@@ -1027,7 +1110,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
     cluster_sync_all();
   else
     __syncthreads();
-  if (kBwd && warp == 1) {
+  if (kBwd && warp == 1) {  // (kBwd includes K4-VPF)
     tc_fence_after();
     tmem_dealloc(S.tmem_base, 512);
   }
@@ -1177,10 +1260,12 @@ __global__ void k_combine(int64_t num_rows, int nshards, const float4* __restric
 // ---- launchers ---------------------------------------------------------------------------------------
 template <typename KernelT>
 static cudaError_t launch_row_kernel(KernelT kern, const otk_ctx* ctx, const RowParams& p, cudaStream_t s,
-                                     int* grid_out, size_t smem_bytes = kSmemBytes, int ctas_per_sm = 1) {
+                                     int* grid_out, size_t smem_bytes = kSmemBytes, int ctas_per_sm = 1,
+                                     int max_ctas = 0) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes));
   if (e != cudaSuccess) return e;
   int64_t groups = int64_t(ctx->num_sms) * ctas_per_sm / p.csize;
+  if (max_ctas > 0 && groups > max_ctas / p.csize) groups = max_ctas / p.csize;  // ranks sharing a GPU
   if (groups > p.num_rows) groups = p.num_rows;
   if (groups < 1) groups = 1;
   const int grid = int(groups * p.csize);
@@ -1202,7 +1287,7 @@ static cudaError_t launch_row_kernel(KernelT kern, const otk_ctx* ctx, const Row
 }
 
 cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const RowParams& p, cudaStream_t s,
-                        int* grid_out) {
+                        int* grid_out, int max_ctas) {
   constexpr size_t kFwdSmem = smem_bytes_for(kSlotsFwd);  // ~104 KB: two CTAs per SM
   if (dtype == OTK_BF16) {
     using B = __nv_bfloat16;
@@ -1211,6 +1296,8 @@ cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const
       case kModePartial: return launch_row_kernel(k_rows_tm<B, kModePartial>, ctx, p, s, grid_out, kFwdSmem, 2);
       case kModeBwd: return launch_row_kernel(k_rows_tm<B, kModeBwd>, ctx, p, s, grid_out);
       case kModeBwdPartials: return launch_row_kernel(k_rows_stream<B>, ctx, p, s, grid_out);
+      case kModeBwdVpf:
+        return launch_row_kernel(k_rows_tm<B, kModeBwdVpf>, ctx, p, s, grid_out, kSmemBytes, 1, max_ctas);
     }
   } else {
     switch (mode) {
@@ -1218,6 +1305,8 @@ cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const
       case kModePartial: return launch_row_kernel(k_rows_tm<float, kModePartial>, ctx, p, s, grid_out, kFwdSmem, 2);
       case kModeBwd: return launch_row_kernel(k_rows_tm<float, kModeBwd>, ctx, p, s, grid_out);
       case kModeBwdPartials: return launch_row_kernel(k_rows_stream<float>, ctx, p, s, grid_out);
+      case kModeBwdVpf:
+        return launch_row_kernel(k_rows_tm<float, kModeBwdVpf>, ctx, p, s, grid_out, kSmemBytes, 1, max_ctas);
     }
   }
   return cudaErrorInvalidValue;

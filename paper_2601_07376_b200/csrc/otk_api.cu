@@ -159,6 +159,7 @@ const char* otk_status_string(otk_status s) {
     case OTK_ERR_TARGET_RANGE: return "OTK_ERR_TARGET_RANGE";
     case OTK_ERR_CUDA: return "OTK_ERR_CUDA";
     case OTK_ERR_GROUP_RANGE: return "OTK_ERR_GROUP_RANGE";
+    case OTK_ERR_PEER_TIMEOUT: return "OTK_ERR_PEER_TIMEOUT";
   }
   return "OTK_ERR_UNKNOWN";
 }
@@ -527,6 +528,103 @@ otk_status otk_policy_loss_fwd_bwd_partials(otk_ctx* ctx, int64_t num_rows, int6
   OTK_CUDA(otk::launch_rows(ctx, otk::kModeBwdPartials, dtype, p, reinterpret_cast<cudaStream_t>(stream), nullptr),
            "k_rows<bwd_partials> launch");
   ctx->launches += 1;
+  return OTK_OK;
+}
+
+// ---- K4-VPF: (4) on a vocab shard with the row-partial exchange fused into the kernel -------------------
+int64_t otk_vpf_xchg_bytes(int64_t rows_cap, int32_t nranks) {
+  if (rows_cap < 1 || nranks < 1 || nranks > OTK_VPF_MAX_RANKS) return -1;
+  return 2 * rows_cap * nranks * 32;  // [2][cap][P] records of four (value | epoch) 64-bit words
+}
+
+otk_status otk_policy_loss_fwd_bwd_vpf(otk_ctx* ctx, int64_t num_rows, int64_t vocab_local, int64_t ld,
+                                       otk_dtype dtype, const void* logits, const int32_t* targets,
+                                       const uint8_t* loss_mask, const int32_t* row_traj, const double* adv,
+                                       const float* old_logp, const float* ref_logp, const int64_t* n_loss,
+                                       const otk_loss_cfg* cfg, const otk_vocab_shard* shard,
+                                       const otk_vpf_peers* peers, void* dlogits, float* logp, float* entropy,
+                                       otk_loss_stats* stats, otk_stream_t stream) {
+  int csize = 0, seg = 0;
+  otk_status st = check_rows(ctx, num_rows, vocab_local, ld, dtype, logits, targets, &csize, &seg);
+  if (st != OTK_OK) return st;
+  st = check_cfg(cfg, ref_logp, num_rows);
+  if (st != OTK_OK) return st;
+  OTK_REQUIRE(n_loss && stats && shard && peers, OTK_ERR_INVALID_ARG, "n_loss, stats, shard and peers are required");
+  OTK_REQUIRE(num_rows == 0 || (loss_mask && row_traj && adv && old_logp && dlogits), OTK_ERR_INVALID_ARG,
+              "loss_mask, row_traj, adv, old_logp and dlogits are required (num_rows > 0)");
+  OTK_REQUIRE(shard->vocab_start >= 0 && shard->vocab_start + vocab_local <= shard->vocab_total, OTK_ERR_SHAPE,
+              "shard outside [0, vocab_total)");
+  OTK_REQUIRE(peers->nranks >= 1 && peers->nranks <= OTK_VPF_MAX_RANKS && peers->rank >= 0 &&
+                  peers->rank < peers->nranks, OTK_ERR_INVALID_ARG, "need 0 <= rank < nranks <= OTK_VPF_MAX_RANKS");
+  OTK_REQUIRE(peers->rows_cap >= num_rows && peers->rows_cap >= 1, OTK_ERR_SHAPE, "num_rows > rows_cap");
+  OTK_REQUIRE(peers->epoch != 0, OTK_ERR_INVALID_ARG, "epoch must be >= 1");
+  OTK_REQUIRE(peers->max_ctas >= 0, OTK_ERR_INVALID_ARG, "max_ctas must be >= 0");
+  for (int q = 0; q < peers->nranks; ++q)
+    OTK_REQUIRE(peers->xchg[q] && aligned16(peers->xchg[q]), OTK_ERR_ALIGNMENT,
+                "every xchg[q] must be a 16-byte aligned device pointer");
+  OTK_REQUIRE(dlogits != logits || num_rows == 0, OTK_ERR_INVALID_ARG, "dlogits must not alias logits");
+  OTK_REQUIRE(aligned16(dlogits), OTK_ERR_ALIGNMENT, "dlogits must be 16-byte aligned");
+  OTK_REQUIRE(peers->max_ctas == 0 || peers->max_ctas >= csize, OTK_ERR_INVALID_ARG, "max_ctas below the cluster size");
+  otk::RowParams p = base_params(ctx, num_rows, vocab_local, ld, logits, targets, loss_mask,
+                                 float(cfg->logit_scale), csize, seg);
+  p.vocab_start = shard->vocab_start;
+  p.vocab_total = shard->vocab_total;
+  set_loss(p, row_traj, adv, old_logp, ref_logp, n_loss, cfg, dlogits, logp, entropy, stats);
+  for (int q = 0; q < peers->nranks; ++q) p.vpf_xchg[q] = peers->xchg[q];
+  p.vpf_rank = peers->rank;
+  p.vpf_nranks = peers->nranks;
+  p.vpf_epoch = peers->epoch;
+  p.vpf_rows_cap = peers->rows_cap;
+  OTK_CUDA(otk::launch_rows(ctx, otk::kModeBwdVpf, dtype, p, reinterpret_cast<cudaStream_t>(stream), nullptr,
+                            peers->max_ctas),
+           "k_rows<bwd_vpf> launch");
+  ctx->launches += 1;
+  return OTK_OK;
+}
+
+static_assert(sizeof(cudaIpcMemHandle_t) == OTK_IPC_HANDLE_BYTES, "IPC handle size");
+
+otk_status otk_xchg_alloc(otk_ctx* ctx, int64_t bytes, void** dev_ptr_out) {
+  OTK_REQUIRE(ctx && dev_ptr_out && bytes > 0, OTK_ERR_INVALID_ARG, "need ctx, dev_ptr_out and bytes > 0");
+  OTK_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  void* p = nullptr;
+  OTK_CUDA(cudaMalloc(&p, size_t(bytes)), "exchange buffer cudaMalloc");
+  cudaError_t e = cudaMemset(p, 0, size_t(bytes));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();  // zeroed before any peer can map and write it
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return cuda_fail(e, "exchange buffer zeroing");
+  }
+  *dev_ptr_out = p;
+  return OTK_OK;
+}
+
+otk_status otk_xchg_free(otk_ctx* ctx, void* dev_ptr) {
+  OTK_REQUIRE(ctx && dev_ptr, OTK_ERR_INVALID_ARG, "NULL pointer");
+  OTK_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  OTK_CUDA(cudaFree(dev_ptr), "cudaFree");
+  return OTK_OK;
+}
+
+otk_status otk_ipc_get_handle(const void* dev_ptr, void* handle_out) {
+  OTK_REQUIRE(dev_ptr && handle_out, OTK_ERR_INVALID_ARG, "NULL pointer");
+  cudaIpcMemHandle_t h;
+  OTK_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)), "cudaIpcGetMemHandle");
+  std::memcpy(handle_out, &h, sizeof(h));
+  return OTK_OK;
+}
+
+otk_status otk_ipc_open(const void* handle, void** dev_ptr_out) {
+  OTK_REQUIRE(handle && dev_ptr_out, OTK_ERR_INVALID_ARG, "NULL pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  OTK_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  return OTK_OK;
+}
+
+otk_status otk_ipc_close(void* dev_ptr) {
+  OTK_REQUIRE(dev_ptr, OTK_ERR_INVALID_ARG, "NULL pointer");
+  OTK_CUDA(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
   return OTK_OK;
 }
 

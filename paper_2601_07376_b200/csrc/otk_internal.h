@@ -48,7 +48,8 @@ enum RowMode : int {
   kModeFwd = 0,       // (3): logp / entropy / lse
   kModePartial = 1,   // vocab shard pass 1: per-row (m2, s, t2, zy)
   kModeBwd = 2,       // (4): pass 1 + loss + pass 2 from the SMEM-resident row segment
-  kModeBwdPartials = 3  // (4) on a vocab shard: stats from gathered partials, streaming pass 2
+  kModeBwdPartials = 3,  // (4) on a vocab shard: stats from gathered partials, streaming pass 2
+  kModeBwdVpf = 4        // (4) on a vocab shard, exchange fused in-kernel over peer memory (K4-VPF)
 };
 
 struct RowParams {
@@ -88,6 +89,11 @@ struct RowParams {
   int accumulate;
   void* dlogits;
   otk_loss_stats* stats;
+  // K4-VPF: in-kernel exchange of the 16-byte row partials with the other ranks
+  void* vpf_xchg[OTK_VPF_MAX_RANKS];  // exchange buffer of every rank (peer-mapped), [vpf_rank] = own
+  int vpf_rank, vpf_nranks;
+  uint32_t vpf_epoch;
+  int64_t vpf_rows_cap;
   // ctx scratch
   double* cta_partials;
   unsigned int* ticket;
@@ -96,7 +102,7 @@ struct RowParams {
 
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const RowParams& p, cudaStream_t s,
-                        int* grid_out);
+                        int* grid_out, int max_ctas = 0);
 cudaError_t launch_combine(const otk_ctx* ctx, int64_t num_rows, int nshards, const float4* partials,
                            const uint8_t* row_mask, float* logp, float* entropy, float* lse, cudaStream_t s);
 

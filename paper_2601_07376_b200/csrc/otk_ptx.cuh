@@ -256,5 +256,20 @@ __device__ __forceinline__ void stg_cs_v4(void* p, uint4 v) {
                : "memory");
 }
 
+// ---- K4-VPF exchange words (peer GPUs over NVLink): every 64-bit word carries (float value, u32 epoch), so
+// each word is single-copy atomic and self-validating — no release/acquire fences (no MEMBAR.SYS behind the
+// thread's outstanding pass-2 stores) are needed to publish or read a record.
+__device__ __forceinline__ void st_pair_sys(void* p, uint64_t a, uint64_t b) {
+  asm volatile("st.relaxed.sys.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_pair_sys(const void* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.relaxed.sys.global.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 }  // namespace ptx
 }  // namespace otk

@@ -14,6 +14,8 @@ cross-shard group statistics"):
 Vocab sharding (north_star: "vocab-sharding logits with an all-reduce of row max and sum-exp"):
   * vocab_shard_bounds  column ranges, multiples of 8 columns (16-byte aligned rows)
   * all_gather_vocab_partials  16 bytes per row per rank: (max, sum-exp, sum-exp*d, z_y)
+  * open_vpf_exchange   K4-VPF setup: every rank's exchange buffer mapped into every rank (CUDA IPC handles
+                        all-gathered once); the per-row exchange itself then runs inside the loss kernel
 """
 from __future__ import annotations
 
@@ -114,3 +116,24 @@ def all_gather_vocab_partials(partials: torch.Tensor, group=None) -> torch.Tenso
     out = torch.empty((world,) + tuple(partials.shape), dtype=partials.dtype, device=partials.device)
     dist.all_gather_into_tensor(out.view(-1), partials.contiguous().view(-1), group=group)
     return out
+
+
+def open_vpf_exchange(ctx, rows_cap: int, group=None, max_ctas: int = 0):
+    """K4-VPF setup (once per process group, not per step): allocate this rank's zeroed exchange buffer
+    (otk_xchg_alloc), all-gather the 64-byte CUDA IPC handles and map every peer's buffer (otk_ipc_open).
+    Returns the VpfExchange this rank passes to otk_policy_loss_fwd_bwd_vpf."""
+    from . import VpfExchange, otk_ipc_get_handle, otk_ipc_open, otk_vpf_xchg_bytes, otk_xchg_alloc
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    own = otk_xchg_alloc(ctx, otk_vpf_xchg_bytes(rows_cap, world))
+    handles = [None] * world
+    dist.all_gather_object(handles, otk_ipc_get_handle(own), group=group)
+    ptrs, opened = [], []
+    for q, h in enumerate(handles):
+        if q == rank:
+            ptrs.append(own)
+        else:
+            a = otk_ipc_open(h)
+            ptrs.append(a)
+            opened.append(a)
+    dist.barrier(group)  # every mapping exists before any rank's kernel writes into a peer
+    return VpfExchange(rank, world, rows_cap, ptrs, max_ctas=max_ctas, opened=opened, owner=ctx)

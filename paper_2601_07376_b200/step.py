@@ -15,6 +15,8 @@ batch-sharded, otk_group_advantages(skip_ungrouped) over the segments; the loss 
 
 Vocab sharding (VocabShard): every rank holds all rows and a column range; per micro-batch
   otk_row_partials -> all_gather(16 B / row) -> otk_policy_loss_fwd_bwd_partials (identical stats on all ranks).
+Fused vocab sharding (VocabShardFused, K4-VPF): one otk_policy_loss_fwd_bwd_vpf per micro-batch; the 16-byte
+row partials travel between the ranks' kernels over peer memory (no collective call, one read of the shard).
 
 No host synchronisation inside a step (n_loss and the stats never leave the device), so a step can be
 captured in a CUDA graph. Everything arithmetic happens in libotk's kernels; this module only moves
@@ -30,7 +32,8 @@ import torch
 
 from . import (Context, DeviceTrajBatch, LossCfg, STATS_FIELDS, otk_build_masks, otk_group_advantages,
                otk_logprob_entropy_combine, otk_policy_loss_fwd_bwd, otk_policy_loss_fwd_bwd_partials,
-               otk_lmhead_row_partials, otk_row_partials, otk_turn_returns)
+               otk_lmhead_row_partials, otk_policy_loss_fwd_bwd_vpf, otk_row_partials, otk_turn_returns,
+               VpfExchange)
 
 
 @dataclass
@@ -72,6 +75,24 @@ class VocabShard:
                                                 ref_logp, n_loss, cfg, self.v0, self.vt, self._gather(part),
                                                 vocab_local=self.vl, dlogits=dlogits, stats=stats,
                                                 accumulate=accumulate)
+
+
+class VocabShardFused(VocabShard):
+    """VocabShard whose loss runs as K4-VPF (otk_policy_loss_fwd_bwd_vpf): the exchange of row partials is
+    inside the kernel, over the VpfExchange's peer-mapped buffers (dist.open_vpf_exchange across processes,
+    VpfExchange.local_group for ranks sharing one process). Same results as VocabShard (logp / entropy / stats
+    bitwise equal). forward() is inherited (its exchange is the all-gather)."""
+
+    def __init__(self, ctx: Context, vocab_start: int, vocab_local: int, vocab_total: int, xchg: VpfExchange,
+                 process_group=None):
+        super().__init__(ctx, vocab_start, vocab_local, vocab_total, process_group)
+        self.xchg = xchg
+
+    def loss(self, logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss, cfg: LossCfg, *,
+             dlogits=None, stats=None, accumulate=None, stream=None):
+        return otk_policy_loss_fwd_bwd_vpf(self.ctx, logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp,
+                                           n_loss, cfg, self.v0, self.vt, self.xchg, dlogits=dlogits, stats=stats,
+                                           accumulate=accumulate, stream=stream)
 
 
 class LMHeadVocabShard:

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-python -m paper_2601_07376_b200.build
+python paper_2601_07376_b200/build.py
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python -m pytest tests -q -m gpu -p no:cacheprovider -x > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
 tail -2 gpurun_out/smoke.log; tail -4 gpurun_out/gpu_tests.log

@@ -1,6 +1,6 @@
 # full round evidence: tests, bench (all legs), ncu launch list of the bench, ncu full capture of K4/K3
 mkdir -p gpurun_out
-python -m paper_2601_07376_b200.build
+python paper_2601_07376_b200/build.py
 python -c "import __graft_entry__ as g; g.build()"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log

@@ -99,7 +99,13 @@ def _worker(rank, world, port, mode, q):
                        lm_logp=out["logp"].cpu().numpy())
         else:
             v0, v1 = vocab_shard_bounds(V, world)[rank]
-            vs = VocabShard(ctx, v0, v1 - v0, V, dist.group.WORLD)
+            if mode == "vocab_fused":   # K4-VPF: peers' exchange buffers mapped through CUDA IPC handles
+                from paper_2601_07376_b200.dist import open_vpf_exchange
+                from paper_2601_07376_b200.step import VocabShardFused
+                xchg = open_vpf_exchange(ctx, N, dist.group.WORLD)
+                vs = VocabShardFused(ctx, v0, v1 - v0, V, xchg, dist.group.WORLD)
+            else:
+                vs = VocabShard(ctx, v0, v1 - v0, V, dist.group.WORLD)
             st, _ = step_for(tb, vshard=vs, cols=(v0, v1))
             shard = logits[:, v0:v1].contiguous()
             dl = torch.empty_like(shard)
@@ -115,7 +121,7 @@ def _worker(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["batch", "vocab", "batch_turn", "lmhead_vocab"])
+@pytest.mark.parametrize("mode", ["batch", "vocab", "batch_turn", "lmhead_vocab", "vocab_fused"])
 def test_sharded_step_two_ranks_one_gpu(mode):
     world = 2
     ctx = mp.get_context("spawn")

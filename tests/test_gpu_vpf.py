@@ -1,0 +1,164 @@
+"""K4-VPF (otk_policy_loss_fwd_bwd_vpf): the vocab-sharded fused loss with the row-partial exchange inside the
+kernel (-m gpu). P ranks are co-scheduled on the one GPU of the box — each rank its own ctx, stream, column
+shard (a column slice of one [N, V] buffer) and max_ctas = 148 // P CTAs, exchanging through plain device
+buffers instead of IPC-mapped peer buffers (the kernel code and the per-rank call are the multi-GPU ones).
+
+Checks: logp / entropy bitwise equal on every rank AND to the gathered path (otk_row_partials -> stack ->
+otk_policy_loss_fwd_bwd_partials: same partials, same rank-order combine); loss stats identical on every rank;
+everything within the north_star tolerances of the float64 oracle; repeated calls (epoch parity) reproduce the
+same bits; a missing peer ends in OTK_ERR_PEER_TIMEOUT, not a hang."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle_ref as O
+from tests.gpu_common import LOGP_TOL, check_dlogits_rows, dcoef_rows, oracle_cfg, row_problem
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def otk():
+    import paper_2601_07376_b200 as m
+    return m
+
+
+def _bounds(V, P):
+    return [V * k // P // 8 * 8 for k in range(P)] + [V]
+
+
+def _run_vpf(otk, ctxs, xchgs, streams, d, V, nl, cfg, dl, calls=1):
+    P = len(ctxs)
+    b = _bounds(V, P)
+    torch.cuda.synchronize()
+    outs = []
+    for _ in range(calls):
+        res = []
+        for k in range(P):
+            with torch.cuda.stream(streams[k]):
+                res.append(otk.otk_policy_loss_fwd_bwd_vpf(
+                    ctxs[k], d["logits"][:, b[k]:b[k + 1]], d["targets"], d["mask"], d["row_traj"], d["adv"],
+                    d["old"], d["ref"], nl, cfg, b[k], V, xchgs[k], dlogits=dl[:, b[k]:b[k + 1]],
+                    stream=streams[k]))
+        outs.append(res)
+        torch.cuda.synchronize()
+    for c in ctxs:
+        c.check()
+    return outs
+
+
+@pytest.mark.parametrize("P,V,dtype,n", [(2, 151936, "bf16", 160), (4, 151936, "bf16", 96), (8, 151936, "bf16", 64),
+                                         (2, 151936, "f32", 40), (3, 3000, "f32", 50)])
+def test_vpf_equals_gathered_path_and_oracle(otk, P, V, dtype, n):
+    d, h = row_problem(n, V, dtype=dtype, seed=P * 1000 + n)
+    ctxs = [otk.Context(0) for _ in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    xchgs = otk.VpfExchange.local_group(ctxs, n, max_ctas=148 // P)
+    N = int(h["mask"].sum())
+    nl = torch.tensor([N], dtype=torch.int64, device="cuda")
+    cfg = otk.LossCfg()
+    dl = torch.full_like(d["logits"], 7.0)
+    outs = _run_vpf(otk, ctxs, xchgs, streams, d, V, nl, cfg, dl, calls=3)
+    res = outs[-1]
+    # identical on every rank, and across the three calls (epochs 1, 2, 3: both buffer parities reused)
+    for k in range(1, P):
+        assert torch.equal(res[k]["logp"], res[0]["logp"]) and torch.equal(res[k]["entropy"], res[0]["entropy"])
+        assert torch.equal(res[k]["stats"], res[0]["stats"])
+    for c in range(2):
+        for k in range(P):
+            assert torch.equal(outs[c][k]["logp"], res[k]["logp"])
+            assert torch.equal(outs[c][k]["stats"], res[k]["stats"])
+    # gathered path: same partials, same combine -> bitwise-equal logp / entropy
+    b = _bounds(V, P)
+    parts = torch.stack([otk.otk_row_partials(ctxs[0], d["logits"][:, b[k]:b[k + 1]].contiguous(), d["targets"],
+                                              b[k], V, row_mask=d["mask"]) for k in range(P)]).contiguous()
+    g = otk.otk_policy_loss_fwd_bwd_partials(ctxs[0], d["logits"][:, b[0]:b[1]].contiguous(), d["targets"], d["mask"],
+                                             d["row_traj"], d["adv"], d["old"], d["ref"], nl, cfg, b[0], V, parts)
+    ctxs[0].check()
+    assert torch.equal(g["logp"], res[0]["logp"]) and torch.equal(g["entropy"], res[0]["entropy"])
+    sg, sv = otk.stats_dict(g["stats"]), otk.stats_dict(res[0]["stats"])
+    assert abs(sg["loss"] - sv["loss"]) <= 1e-12 * max(1.0, abs(sg["loss"]))   # fp64 sums, CTA grouping differs
+    assert sg["n_tokens"] == sv["n_tokens"] == N and sg["n_clipped"] == sv["n_clipped"]
+    # oracle
+    ocfg = oracle_cfg(cfg)
+    want = O.policy_loss_fwd_bwd(h["wide"], h["targets"], h["mask"], h["row_traj"], h["adv"], h["old"], h["ref"], N,
+                                 ocfg)
+    tol = LOGP_TOL[dtype]
+    m = h["mask"].astype(bool)
+    assert np.max(np.abs(res[0]["logp"].cpu().numpy()[m] - want["logp"][m])) < tol
+    assert np.max(np.abs(res[0]["entropy"].cpu().numpy()[m] - want["entropy"][m])) < tol
+    assert abs(sv["loss"] - want["loss"]) <= 1e-4 * max(abs(want["loss"]), 1e-3)
+    rows = [j for j in range(n) if h["mask"][j]]
+    dc = dcoef_rows(h, want["logp"], ocfg, N, True)
+    assert check_dlogits_rows(dl, want["dlogits"], want["coef"], rows, dtype, V, dc) <= 1.0
+    gd = dl.float()
+    masked = [j for j in range(n) if not h["mask"][j]]
+    assert all(bool((gd[j] == 0).all()) for j in masked)          # every rank zero-filled its columns
+    for x in xchgs:
+        x.close()
+    for c in ctxs:
+        c.close()
+
+
+def test_vpf_equals_unsharded_kernel_dlogits(otk):
+    """The fused shard path writes the same dlogits as the unsharded loss within bf16 rounding, with a real
+    KL term and a mix of clipped rows."""
+    n, V, P = 200, 151936, 2
+    d, h = row_problem(n, V, dtype="bf16", seed=77, force_clip=5)
+    ctxs = [otk.Context(0) for _ in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    xchgs = otk.VpfExchange.local_group(ctxs, 4096, max_ctas=74)      # rows_cap > num_rows is fine
+    N = int(h["mask"].sum())
+    nl = torch.tensor([N], dtype=torch.int64, device="cuda")
+    cfg = otk.LossCfg(kl_beta=0.04)
+    dl = torch.empty_like(d["logits"])
+    res = _run_vpf(otk, ctxs, xchgs, streams, d, V, nl, cfg, dl)[0]
+    full = otk.otk_policy_loss_fwd_bwd(ctxs[0], d["logits"], d["targets"], d["mask"], d["row_traj"], d["adv"],
+                                       d["old"], d["ref"], nl, cfg)
+    ctxs[0].check()
+    assert float((res[0]["logp"] - full["logp"]).abs().max()) < 1e-5
+    a, bb = dl.float(), full["dlogits"].float()
+    err = ((a - bb).abs() / (bb.abs() * 2 ** -6 + 1e-9)).max().item()
+    assert err <= 1.0
+    sv, sf = otk.stats_dict(res[0]["stats"]), otk.stats_dict(full["stats"])
+    assert abs(sv["loss"] - sf["loss"]) <= 1e-5 * max(abs(sf["loss"]), 1e-3)
+    assert sv["n_clipped"] == sf["n_clipped"] and sv["n_tokens"] == sf["n_tokens"]
+    for x in xchgs:
+        x.close()
+
+
+def test_vpf_host_validation(otk):
+    ctx = otk.Context(0)
+    d, h = row_problem(8, 1024, dtype="bf16", seed=1)
+    nl = torch.tensor([int(h["mask"].sum())], dtype=torch.int64, device="cuda")
+    x = otk.VpfExchange.local_group([ctx, ctx], 4)          # rows_cap 4 < 8 rows
+    with pytest.raises(otk.OtkError, match="OTK_ERR_SHAPE"):
+        otk.otk_policy_loss_fwd_bwd_vpf(ctx, d["logits"][:, :512], d["targets"], d["mask"], d["row_traj"], d["adv"],
+                                        d["old"], d["ref"], nl, otk.LossCfg(), 0, 1024, x[0])
+    assert x[0].epoch == 0                                   # nothing launched: epoch not advanced
+    with pytest.raises(ValueError):
+        otk.VpfExchange(0, 9, 4, [0] * 9)
+    x[0].close()
+    x[1].close()
+    ctx.close()
+
+
+def test_vpf_missing_peer_times_out(otk):
+    """Only rank 0 of 2 runs: its CTAs give up after the timeout with OTK_ERR_PEER_TIMEOUT (sticky: later rows
+    do not wait again), so a lost peer costs ~20 s, never a hang."""
+    import time
+    n, V = 16, 2048
+    d, h = row_problem(n, V, dtype="bf16", seed=3, mask_p=1.0)
+    ctxs = [otk.Context(0), otk.Context(0)]
+    x = otk.VpfExchange.local_group(ctxs, n, max_ctas=8)
+    nl = torch.tensor([n], dtype=torch.int64, device="cuda")
+    t0 = time.time()
+    otk.otk_policy_loss_fwd_bwd_vpf(ctxs[0], d["logits"][:, :1024], d["targets"], d["mask"], d["row_traj"],
+                                    d["adv"], d["old"], d["ref"], nl, otk.LossCfg(), 0, V, x[0])
+    torch.cuda.synchronize()
+    dt = time.time() - t0
+    with pytest.raises(otk.OtkError, match="OTK_ERR_PEER_TIMEOUT"):
+        ctxs[0].check()
+    assert 10 < dt < 60, dt
+    for e in x:
+        e.close()
