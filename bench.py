@@ -46,9 +46,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-next", action="store_true",
                     help="skip the side measurements of the forward (3) and the SURVEY.md §8(f) rows")
-    ap.add_argument("--shard", default="batch", choices=["batch", "vocab"],
+    ap.add_argument("--shard", default="batch", choices=["batch", "vocab", "vocab-fused"],
                     help="batch: each rank owns whole trajectories (weak scaling); vocab: each rank owns V/N "
-                         "columns of every row (strong scaling, row partials all-gathered)")
+                         "columns of every row (strong scaling, row partials all-gathered); vocab-fused: the "
+                         "same split with the exchange inside the loss kernel (K4-VPF, CUDA IPC peer buffers)")
     return ap.parse_args()
 
 
@@ -142,7 +143,7 @@ def build_workload(args, rank, world, device):
     from paper_2601_07376_b200.step import MicroBatch, VocabShard
     from synth import CONFIGS, make_batch, make_logits, make_noise
     cfgw = CONFIGS[args.config]
-    vocab_mode = args.shard == "vocab"
+    vocab_mode = args.shard in ("vocab", "vocab-fused")
     brank = 0 if vocab_mode else rank
     tb = make_batch(args.config, seed=cfgw.seed + 1000 * brank)
     tb.group_id = tb.group_id + np.int32(brank * cfgw.num_groups)   # this rank's groups (global ids)
@@ -172,6 +173,14 @@ def build_workload(args, rank, world, device):
     if vocab_mode and world > 1:
         import torch.distributed as dist
         vshard.pg = dist.group.WORLD
+    if args.shard == "vocab-fused":   # K4-VPF: exchange buffers mapped once (setup, untimed)
+        from paper_2601_07376_b200.step import VocabShardFused
+        if world > 1:
+            from paper_2601_07376_b200.dist import open_vpf_exchange
+            xchg = open_vpf_exchange(ctx, M, vshard.pg)
+        else:
+            xchg = otk.VpfExchange.local_group([ctx], M)[0]
+        vshard = VocabShardFused(ctx, v0, Vl, V, xchg, vshard.pg)
     # old/ref = the fwd pool's log-probs (otk_logprob_entropy_fwd, or its vocab-sharded form) + synth noise
     if vocab_mode:
         base_logp = [vshard.forward(b, t)["logp"] for b, t in zip(bufs, tgts)]
@@ -206,7 +215,7 @@ def run_otk(args):
     from paper_2601_07376_b200.step import PolicyLossStep
     cfgw = W["cfgw"]
     cfg = otk.LossCfg(kl_beta=cfgw.kl_beta)
-    vocab_mode = args.shard == "vocab"
+    vocab_mode = args.shard in ("vocab", "vocab-fused")
     bpg = pg if not vocab_mode else None
     step = PolicyLossStep(ctx, W["dbatch"], W["gid"], cfgw.num_groups, W["toff"], W["trew"], W["Vl"], cfg,
                           process_group=bpg, global_num_traj=[W["tb"].num_traj] * world if bpg else None,
@@ -258,7 +267,12 @@ def run_otk(args):
     lm = step.masks["loss_mask"]
     n_train = [int(lm[mb.r0:mb.r1].sum()) for mb in W["mbs"]]
     n_rows = [mb.r1 - mb.r0 for mb in W["mbs"]]
-    if vocab_mode:   # row partials (read 2V_l) + all-gather + streaming pass 2 (read 2V_l, write 2V_l)
+    if args.shard == "vocab-fused":   # one read + one write of the shard, 32 B per peer per trainable row
+        Vl = W["Vl"]
+        side = 4 + 1 + 4 + 4 + (4 if cfgw.kl_beta else 0) + 32 * (world - 1)
+        bytes_k4 = [t * (4 * Vl + side) + (r - t) * (2 * Vl + 1) for t, r in zip(n_train, n_rows)]
+        kname = "k_rows_tm<bf16,BWD_VPF> (otk_policy_loss_fwd_bwd_vpf, exchange in-kernel)"
+    elif vocab_mode:   # row partials (read 2V_l) + all-gather + streaming pass 2 (read 2V_l, write 2V_l)
         Vl = W["Vl"]
         side = 4 + 1 + 4 + 4 + (4 if cfgw.kl_beta else 0) + 16 * world
         bytes_k4 = [t * (6 * Vl + side) + (r - t) * (2 * Vl + 1) for t, r in zip(n_train, n_rows)]
@@ -276,7 +290,8 @@ def run_otk(args):
     if world == 1:
         par = "single GPU" + (" (vocab-shard path, 1 shard)" if vocab_mode else "")
     else:
-        par = f"vocab-shard tp{world}" if vocab_mode else f"batch-shard dp{world}"
+        par = (f"vocab-shard tp{world}" + (" (K4-VPF)" if args.shard == "vocab-fused" else "")) if vocab_mode \
+            else f"batch-shard dp{world}"
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,

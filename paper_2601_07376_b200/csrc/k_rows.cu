@@ -111,24 +111,27 @@ __device__ __forceinline__ uint64_t vpf_word(float v, uint32_t ep) {
   return uint64_t(__float_as_uint(v)) | (uint64_t(ep) << 32);
 }
 
-// Called by one thread per CTA (ct == 0) after the CTA's (cluster's) row total: push this rank's partial
-// `mine` = (m2, s, t2, w) to every peer (cluster rank 0 only), collect the peers' records of the same row and
-// combine all P in rank order exactly as combine_partials does. Identical bits on every rank.
-__device__ __forceinline__ Stat vpf_exchange(const RowParams& p, int64_t row, uint32_t crank, float4 mine, float& dy) {
+// Push this rank's row partial `mine` = (m2, s, t2, w) into every peer's exchange buffer (one thread).
+__device__ __forceinline__ void vpf_push(const RowParams& p, int64_t row, float4 mine) {
+  const int P = p.vpf_nranks, me = p.vpf_rank;
+  const uint32_t par = p.vpf_epoch & 1u, ep = p.vpf_epoch;
+  const int64_t i = vpf_rec_index(p.vpf_rows_cap, P, par, row, me) * 32;
+  const uint64_t w0 = vpf_word(mine.x, ep), w1 = vpf_word(mine.y, ep), w2 = vpf_word(mine.z, ep),
+                 w3 = vpf_word(mine.w, ep);
+  for (int q = 0; q < P; ++q) {
+    if (q == me) continue;
+    char* b = reinterpret_cast<char*>(p.vpf_xchg[q]) + i;
+    st_pair_sys(b, w0, w1);
+    st_pair_sys(b + 16, w2, w3);
+  }
+}
+
+// Collect the peers' records of `row` (waiting for this call's epoch) and combine all P partials in rank order
+// exactly as combine_partials does (own = `mine`). Identical bits on every rank.
+__device__ __forceinline__ Stat vpf_collect(const RowParams& p, int64_t row, float4 mine, float& dy) {
   const int P = p.vpf_nranks, me = p.vpf_rank;
   const uint32_t par = p.vpf_epoch & 1u, ep = p.vpf_epoch;
   const int64_t cap = p.vpf_rows_cap;
-  if (crank == 0) {
-    const int64_t i = vpf_rec_index(cap, P, par, row, me) * 32;
-    const uint64_t w0 = vpf_word(mine.x, ep), w1 = vpf_word(mine.y, ep), w2 = vpf_word(mine.z, ep),
-                   w3 = vpf_word(mine.w, ep);
-    for (int q = 0; q < P; ++q) {
-      if (q == me) continue;
-      char* b = reinterpret_cast<char*>(p.vpf_xchg[q]) + i;
-      st_pair_sys(b, w0, w1);
-      st_pair_sys(b + 16, w2, w3);
-    }
-  }
   const char* own = reinterpret_cast<const char*>(p.vpf_xchg[me]);
   Stat tot{-INFINITY, 0.f, 0.f};
   float4 rec[OTK_VPF_MAX_RANKS];
@@ -165,6 +168,13 @@ __device__ __forceinline__ Stat vpf_exchange(const RowParams& p, int64_t row, ui
   for (int q = 0; q < P; ++q)
     if (rec[q].w != -INFINITY) dy = __fadd_rn(rec[q].w, __fsub_rn(rec[q].x, tot.m));
   return tot;
+}
+
+// Called by one thread per CTA (ct == 0) after the CTA's (cluster's) row total: push (cluster rank 0 only),
+// then collect and combine.
+__device__ __forceinline__ Stat vpf_exchange(const RowParams& p, int64_t row, uint32_t crank, float4 mine, float& dy) {
+  if (crank == 0) vpf_push(p, row, mine);
+  return vpf_collect(p, row, mine, dy);
 }
 
 // One element pair of pass 1: d = s2*x - m; e = 2^d; S += e; T += e*d (per-lane fp32 chains; kInit starts
@@ -355,8 +365,8 @@ struct Vec<__nv_bfloat16> {
 struct Smem {
   uint64_t full[kSlots];
   uint64_t empty[kSlots];
-  uint64_t xbar[2];
-  float4 xrecv[2][8];                 // peer partials, double-buffered by active-row parity
+  uint64_t xbar[4];
+  float4 xrecv[4][8];                 // peer partials, by active-row parity (pipelined loop: row index mod 4)
   float4 wred[2][kConsumerWarps];     // warp partials, double-buffered by active-row parity
   // FWD / PARTIAL: warp partials handed to the finalizer warp through a ring of kFinSlots rows
   uint64_t ffull[4];                  // all consumer warps wrote slot k (count kConsumerWarps)
@@ -594,8 +604,7 @@ __device__ __forceinline__ void row_kernel_setup(Smem& S, uint8_t* zero, int war
       mbar_init(&S.full[i], 1);
       mbar_init(&S.empty[i], kConsumerWarps);
     }
-    mbar_init(&S.xbar[0], 1);
-    mbar_init(&S.xbar[1], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&S.xbar[i], 1);
     for (int i = 0; i < 4; ++i) {
       mbar_init(&S.ffull[i], kConsumerWarps);
       mbar_init(&S.fempty[i], 1);
@@ -772,12 +781,295 @@ __device__ unsigned long long g_phase[8];  // experiments only: clock64 sums per
 #endif
 
 // =====================================================================================================
+// Pipelined K4-VPF consumer (kPipe; segments of <= kPipeChunks chunks, so TWO rows fit a warp's TMEM window).
+// Stage A(r): pass 1 of row r into TMEM half (q & 1), CTA reduction, then the row partial is SENT (cluster
+// peers through DSMEM; K4-VPF csize 1: the peer ranks) but not awaited. Stage B(r-1): wait for the previous
+// row's partials, loss terms, pass 2 from the other TMEM half. Order A(r), B(r-1), A(r+1), B(r), ...: the
+// exchange latency of a row (and the skew between the CTAs / ranks sharing it) is hidden behind a whole
+// pass 1. Cluster mailboxes are indexed by active-row index mod 4: a peer can be at most 3 rows ahead of the
+// row being read (its A(r+4) needs our A(r+2), which follows our B(r)).
+// =====================================================================================================
+constexpr int kPipeHalf = 64;                   // TMEM columns per half: [0, 56) e, [56, 63) m_c
+
+struct PipeRow {
+  int64_t row;
+  RowSide sd;
+  Stat r;          // this CTA's partial (cluster rank order combine in stage B)
+  float xy;
+  int32_t y;
+  int ylc, owner;
+  uint32_t q;
+};
+
+template <typename T, int MODE>
+__device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8_t* ring, int warp, int lane,
+                                              int csize, uint32_t crank, int64_t group, int64_t ngroups, int64_t c0,
+                                              int segn, int nch) {
+  constexpr bool kVpf = (MODE == kModeBwdVpf);
+  using VT = Vec<T>;
+  constexpr int EV = VT::EV;
+  constexpr int CE = kChunkBytes / int(sizeof(T));
+  constexpr int kColM = 8 * kPipeChunks;
+  static_assert(2 * kPipeHalf <= kTmemWindow && kColM + kPipeChunks <= kPipeHalf, "TMEM halves");
+  const int ct = threadIdx.x - 32;
+  const int cw = warp - 1;
+  const uint32_t tm0 = S.tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(kTmemWindow * (cw >> 2));
+  const float s2 = __fmul_rn(p.scale, kLog2e);
+  const uint64_t s2x2 = f2(s2, s2);
+  double acc_L = 0.0, acc_clip = 0.0, acc_kl = 0.0, acc_H = 0.0, acc_n = 0.0;
+  const int64_t nl = *p.n_loss;
+  const float invN = nl > 0 ? float(1.0 / double(nl)) : 0.f;
+  const int64_t nact = p.reduction != OTK_TOKEN_MEAN ? *p.n_active : 0;
+  uint32_t slot = 0, phase = 0, q = 0;
+
+  // ---- stage B: the previous row's statistics, loss and pass 2 -----------------------------------------
+  auto stage_b = [&](const PipeRow& pr) {
+    const uint32_t k = pr.q & 3u;
+    Stat tot;
+    if (csize > 1) {
+      mbar_wait(&S.xbar[k], (pr.q >> 2) & 1u);
+      tot = Stat{-INFINITY, 0.f, 0.f};
+      for (int c = 0; c < csize; ++c) {
+        const float4 P = (c == int(crank)) ? make_float4(pr.r.m, pr.r.s, pr.r.t, 0.f) : S.xrecv[k][c];
+        tot = combine(tot, Stat{P.x, P.y, P.z});
+      }
+    } else {
+      tot = pr.r;
+    }
+    const int64_t yg = int64_t(pr.y) - p.vocab_start;
+    float dy = (yg >= 0 && yg < p.vocab) ? __fmaf_rn(pr.xy, s2, -tot.m) : -INFINITY;
+    if constexpr (kVpf) {  // csize 1 here: the push went out in stage A
+      if (ct == 0) {
+        float gdy;
+        const Stat g = vpf_collect(p, pr.row, make_float4(tot.m, tot.s, tot.t, dy), gdy);
+        S.vbc[pr.q & 1u] = make_float4(g.m, g.s, g.t, gdy);
+      }
+      named_bar_sync(2, kNCT);
+      const float4 b = S.vbc[pr.q & 1u];
+      tot = Stat{b.x, b.y, b.z};
+      dy = b.w;
+    }
+    const RowStats rs = finalize(tot, dy);
+    const LossOut lo = loss_terms(p, rs.logp, rs.H, pr.sd, row_weight(p, invN, pr.sd.nb, nact));
+    if (ct == 0 && crank == 0) {
+      acc_L += double(lo.w) * double(lo.L);
+      acc_clip += lo.clipped ? 1.0 : 0.0;
+      acc_kl += double(lo.kl);
+      acc_H += double(rs.H);
+      acc_n += 1.0;
+      if (p.logp) p.logp[pr.row] = rs.logp;
+      if (p.entropy) p.entropy[pr.row] = rs.H;
+    }
+    const uint32_t tm = tm0 + (pr.q & 1u) * kPipeHalf;
+    char* drow = reinterpret_cast<char*>(p.dlogits) + (pr.row * p.ld + c0) * int64_t(sizeof(T));
+    char* tp = drow + ct * 16;
+    auto chunk2 = [&](int c, const uint4& e0, const uint4& e1, uint32_t mw, auto entf) {
+      constexpr bool kEnt = decltype(entf)::value;
+      const float dm = __fsub_rn(__uint_as_float(mw), rs.L2);
+      const float qc = ex2(dm);
+      uint4 g0, g1;
+      if constexpr (!kEnt) {
+        const float kt = __fmul_rn(lo.coef, qc);
+        g0 = VT::pass2(e0, kt);
+        g1 = VT::pass2(e1, kt);
+      } else {
+        const float Ac = qc * fmaf(lo.wcs, fmaf(kLn2, dm, rs.H), lo.coef);
+        const float Bc = qc * lo.wcs * kLn2;
+        g0 = VT::pass2_ent(e0, Ac, Bc);
+        g1 = VT::pass2_ent(e1, Ac, Bc);
+      }
+      char* q0 = tp + size_t(c) * kChunkBytes;
+      if (c < nch - 1 || (c + 1) * CE <= segn) {
+        stg_cs_v4(q0, g0);
+        stg_cs_v4(q0 + kNCT * 16, g1);
+      } else {
+        const uint4 gg[2] = {g0, g1};
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int lc = c * CE + (ct + kk * kNCT) * EV;
+          if (lc + EV <= segn) {
+            stg_cs_v4(q0 + kk * kNCT * 16, gg[kk]);
+          } else if (lc < segn) {
+            float g[EV];
+            VT::unpack(gg[kk], g);
+            for (int i = 0; i < EV && lc + i < segn; ++i) VT::store1(drow, lc + i, g[i]);
+          }
+        }
+      }
+    };
+    auto pass2 = [&](auto entf) {
+      uint4 a0, a1, b0, b1;
+      uint32_t am, bm;
+      tmem_ld8_1_issue(tm, tm + uint32_t(kColM), a0, a1, am);
+      tmem_wait_ld_dep(a0, a1, am);
+      for (int c = 0;;) {
+        if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), b0, b1, bm);
+        chunk2(c, a0, a1, am, entf);
+        if (++c >= nch) break;
+        tmem_wait_ld_dep(b0, b1, bm);
+        if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), a0, a1, am);
+        chunk2(c, b0, b1, bm, entf);
+        if (++c >= nch) break;
+        tmem_wait_ld_dep(a0, a1, am);
+      }
+    };
+    if (lo.wcs == 0.f)
+      pass2(std::false_type{});
+    else
+      pass2(std::true_type{});
+    if (ct == pr.owner) VT::store1(drow, pr.ylc, lo.gy);
+  };
+
+  int64_t row = group;
+  int32_t y_n = 0, rt_n = 0;
+  uint8_t m_n = 1;
+  float old_n = 0.f, ref_n = 0.f;
+  if (row < p.num_rows) {
+    y_n = p.targets[row];
+    m_n = p.mask ? p.mask[row] : 1;
+    rt_n = p.row_traj[row];
+    old_n = p.old_logp[row];
+    if (p.ref_logp) ref_n = p.ref_logp[row];
+  }
+  auto xy_of = [&](int64_t r, int32_t yy) -> float {
+    const int64_t g = int64_t(yy) - p.vocab_start;
+    return (g >= 0 && g < p.vocab) ? VT::load1(p.logits, r * p.ld + g) : 0.f;
+  };
+  float xy_n = (row < p.num_rows && row_active(p, y_n, m_n)) ? xy_of(row, y_n) : 0.f;
+  PipeRow prev;
+  bool has_prev = false;
+  for (; row < p.num_rows; row += ngroups) {
+    const int32_t y = y_n;
+    const uint8_t m = m_n;
+    const float xy = xy_n;
+    RowSide sd{0.0, old_n, ref_n, 0};
+    const int32_t rt = rt_n;
+    const int64_t nrow = row + ngroups;
+    if (nrow < p.num_rows) {
+      y_n = p.targets[nrow];
+      m_n = p.mask ? p.mask[nrow] : 1;
+      rt_n = p.row_traj[nrow];
+      old_n = p.old_logp[nrow];
+      if (p.ref_logp) ref_n = p.ref_logp[nrow];
+    }
+    if (!row_active(p, y, m)) {
+      inactive_row<T, MODE>(p, row, ct, crank, c0, segn, m != 0);
+      if (nrow < p.num_rows && row_active(p, y_n, m_n)) xy_n = xy_of(nrow, y_n);
+      continue;
+    }
+    const int64_t ylc64 = int64_t(y) - p.vocab_start - c0;
+    const int ylc = (ylc64 >= 0 && ylc64 < segn) ? int(ylc64) : -1;
+    sd.A = p.adv[p.adv_index ? p.adv_index[row] : rt];
+    if (p.reduction != OTK_TOKEN_MEAN) sd.nb = p.traj_tokens[rt];
+    const uint32_t tm = tm0 + (q & 1u) * kPipeHalf;
+
+    // ---------------- stage A: pass 1 into TMEM half (q & 1) (same arithmetic as the unpipelined loop)
+    uint64_t rS = 0ull, rT = 0ull;
+    float mref = -INFINITY;
+    auto chunk1 = [&](int c, auto tail) {
+      constexpr bool kTail = decltype(tail)::value;
+      mbar_wait(&S.full[slot], phase);
+      const uint8_t* buf = ring + size_t(slot) * kChunkBytes;
+      uint4 v0 = *reinterpret_cast<const uint4*>(buf + ct * 16);
+      uint4 v1 = *reinterpret_cast<const uint4*>(buf + (ct + kNCT) * 16);
+      if constexpr (kTail) {
+        const int lc0 = c * CE + ct * EV, lc1 = lc0 + kNCT * EV;
+        if (lc0 + EV > segn) v0 = VT::mask_tail(v0, segn - lc0);
+        if (lc1 + EV > segn) v1 = VT::mask_tail(v1, segn - lc1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[slot]);
+      if (++slot == kSlots) {
+        slot = 0;
+        phase ^= 1u;
+      }
+      uint64_t cS[2], cT[2];
+      uint4 e0, e1;
+      bool ok = false;
+      if (mref != -INFINITY) {
+        const uint64_t negm2 = f2(-mref, -mref);
+        e0 = VT::template pass1<true, false, true>(v0, s2x2, negm2, cS, cT);
+        e1 = VT::template pass1<true, false, false>(v1, s2x2, negm2, cS, cT);
+        const uint64_t sS = fadd2(cS[0], cS[1]), sT = fadd2(cT[0], cT[1]);
+        float s0, s1, t0, t1;
+        f2_split(sS, s0, s1);
+        f2_split(sT, t0, t1);
+        ok = fmaxf(s0, s1) <= 0x1p64f && !isnan(t0 + t1);
+        cS[0] = sS;
+        cT[0] = sT;
+      }
+      if (!ok) {
+        const float mx = VT::max_final(VT::max_acc(VT::max_acc(VT::max_init(), v0), v1));
+        if (mx > -1e30f) {
+          const float mn = fmaxf(mref, __fmul_rn(mx, s2));
+          if (mn > mref) {
+            if (mref != -INFINITY) {
+              const float d = __fsub_rn(mref, mn), f = ex2(d);
+              const uint64_t f2x = f2(f, f);
+              rT = fmul2(f2x, ffma2(f2(d, d), rS, rT));
+              rS = fmul2(rS, f2x);
+            }
+            mref = mn;
+          }
+        }
+        const float mr = (mref == -INFINITY) ? 0.f : mref;
+        const uint64_t negm2 = f2(-mr, -mr);
+        e0 = VT::template pass1<true, true, true>(v0, s2x2, negm2, cS, cT);
+        e1 = VT::template pass1<true, true, false>(v1, s2x2, negm2, cS, cT);
+        cS[0] = fadd2(cS[0], cS[1]);
+        cT[0] = fadd2(cT[0], cT[1]);
+      }
+      rS = fadd2(rS, cS[0]);
+      rT = fadd2(rT, cT[0]);
+      tmem_st8(tm + uint32_t(8 * c), e0, e1);
+      tmem_st1(tm + uint32_t(kColM + c), __float_as_uint(mref == -INFINITY ? 0.f : mref));
+    };
+    for (int c = 0; c < nch - 1; ++c) chunk1(c, std::false_type{});
+    if (nch > 0) chunk1(nch - 1, std::true_type{});
+    if (nrow < p.num_rows && row_active(p, y_n, m_n)) xy_n = xy_of(nrow, y_n);
+    tmem_wait_st();
+    // CTA reduction (as row_total), then send without waiting
+    const uint32_t par = q & 1u, k = q & 3u;
+    const Stat wst = warp_reduce(Stat{mref, f2_sum(rS), f2_sum(rT)});
+    if (lane == 0) S.wred[par][cw] = make_float4(wst.m, wst.s, wst.t, 0.f);
+    named_bar_sync(1, kNCT);
+    Stat mine{-INFINITY, 0.f, 0.f};
+    if (lane < kConsumerWarps) {
+      const float4 w = S.wred[par][lane];
+      mine = Stat{w.x, w.y, w.z};
+    }
+    const Stat r = warp_reduce(mine);
+    if (ct == 0) {
+      if (csize > 1) {
+        for (int dst = 0; dst < csize; ++dst) {
+          if (dst == int(crank)) continue;
+          st_async_f4(mapa(smem_u32(&S.xrecv[k][crank]), dst), r.m, r.s, r.t, 0.f, mapa(smem_u32(&S.xbar[k]), dst));
+        }
+        mbar_arrive_expect_tx(&S.xbar[k], 16u * uint32_t(csize - 1));
+      }
+      if constexpr (kVpf) {  // csize 1: this CTA's partial is the rank's
+        const int64_t yg = int64_t(y) - p.vocab_start;
+        const float dyl = (yg >= 0 && yg < p.vocab) ? __fmaf_rn(xy, s2, -r.m) : -INFINITY;
+        vpf_push(p, row, make_float4(r.m, r.s, r.t, dyl));
+      }
+    }
+    // ---------------- stage B of the previous row (its partials have had a whole pass 1 to arrive)
+    if (has_prev) stage_b(prev);
+    prev = PipeRow{row, sd, r, xy, y, ylc, ylc >= 0 ? ((ylc % CE) / EV) % kNCT : -1, q};
+    has_prev = true;
+    ++q;
+  }
+  if (has_prev) stage_b(prev);
+  if (ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl);
+}
+
+// =====================================================================================================
 // k_rows_tm: FWD / PARTIAL / BWD. Pass 1 streams each chunk from the ring exactly once (slot released
 // right away); for BWD the exponentials e = 2^(y - m_c) (bf16 for bf16 input, with m_c the thread's
 // running max after chunk c) and m_c are parked in TENSOR MEMORY, so pass 2 needs no second read of the
 // logits and no second exponential: softmax = e * 2^(m_c - lse).
 // =====================================================================================================
-template <typename T, int MODE>
+template <typename T, int MODE, bool kPipe = false>
 __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr bool kVpf = (MODE == kModeBwdVpf);  // BWD with the vocab-shard exchange fused in
@@ -816,6 +1108,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       finalize_rows<T, MODE>(p, S, lane, csize, crank, group, ngroups);
     }
     __syncwarp();
+  } else if constexpr (kPipe) {
+    consumer_pipe<T, MODE>(p, S, ring, warp, lane, csize, crank, group, ngroups, c0, segn, nch);
   } else {
     const int ct = threadIdx.x - 32;
     const int cw = warp - 1;
@@ -1297,6 +1591,8 @@ cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const
       case kModeBwd: return launch_row_kernel(k_rows_tm<B, kModeBwd>, ctx, p, s, grid_out);
       case kModeBwdPartials: return launch_row_kernel(k_rows_stream<B>, ctx, p, s, grid_out);
       case kModeBwdVpf:
+        if (p.pipe)
+          return launch_row_kernel(k_rows_tm<B, kModeBwdVpf, true>, ctx, p, s, grid_out, kSmemBytes, 1, max_ctas);
         return launch_row_kernel(k_rows_tm<B, kModeBwdVpf>, ctx, p, s, grid_out, kSmemBytes, 1, max_ctas);
     }
   } else {
@@ -1306,6 +1602,8 @@ cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const
       case kModeBwd: return launch_row_kernel(k_rows_tm<float, kModeBwd>, ctx, p, s, grid_out);
       case kModeBwdPartials: return launch_row_kernel(k_rows_stream<float>, ctx, p, s, grid_out);
       case kModeBwdVpf:
+        if (p.pipe)
+          return launch_row_kernel(k_rows_tm<float, kModeBwdVpf, true>, ctx, p, s, grid_out, kSmemBytes, 1, max_ctas);
         return launch_row_kernel(k_rows_tm<float, kModeBwdVpf>, ctx, p, s, grid_out, kSmemBytes, 1, max_ctas);
     }
   }

@@ -575,6 +575,12 @@ otk_status otk_policy_loss_fwd_bwd_vpf(otk_ctx* ctx, int64_t num_rows, int64_t v
   p.vpf_nranks = peers->nranks;
   p.vpf_epoch = peers->epoch;
   p.vpf_rows_cap = peers->rows_cap;
+  // pipelined loop (exchange latency hidden behind the next row's pass 1) when a CTA holds the whole shard row
+  // and two rows fit its tensor memory
+  p.pipe = csize == 1 && int64_t(seg) * int64_t(dtype_size(dtype)) <= int64_t(otk::kPipeChunks) * otk::kChunkBytes;
+#ifdef OTK_VPF_NOPIPE  // experiment builds only: measure the unpipelined loop
+  p.pipe = 0;
+#endif
   OTK_CUDA(otk::launch_rows(ctx, otk::kModeBwdVpf, dtype, p, reinterpret_cast<cudaStream_t>(stream), nullptr,
                             peers->max_ctas),
            "k_rows<bwd_vpf> launch");

@@ -43,6 +43,7 @@ constexpr int kConsumerWarps = 12;       // 384 compute threads
 constexpr int kThreads = 32 * (2 + kConsumerWarps);  // + loader warp 0 + zero-fill warp 13
 constexpr int kMaxChunks = 13;           // a CTA's row segment (<= 13 chunks, 156 KB) is kept in TMEM
 constexpr int kTmemWindow = 128;         // TMEM columns per consumer warp (3 windows per lane quadrant)
+constexpr int kPipeChunks = 7;           // pipelined K4-VPF: <= 7 chunks (84 KB) per CTA, two rows per TMEM window
 
 enum RowMode : int {
   kModeFwd = 0,       // (3): logp / entropy / lse
@@ -64,6 +65,7 @@ struct RowParams {
   int64_t vocab_total;   // global vocabulary (target range check)
   int seg_elems;         // per-CTA column segment (multiple of 8) when the cluster splits a row
   int csize;             // CTAs per row (cluster size)
+  int pipe;              // BWD_VPF: pipelined consumer loop (csize 1, segment <= kPipeChunks chunks)
   // forward outputs
   float* logp;
   float* entropy;

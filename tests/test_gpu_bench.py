@@ -38,3 +38,13 @@ def test_bench_reference_arm():
     d = _run("--impl", "reference", "--config", "tiny", "--steps", "1", "--warmup", "1")
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+
+
+@pytest.mark.parametrize("shard", ["vocab", "vocab-fused"])
+def test_bench_vocab_shard_paths(shard):
+    """The vocab-sharded step (gathered and K4-VPF) runs through bench.py at N = 1 with its own roofline line."""
+    d = _run("--config", "game", "--shard", shard, "--steps", "1", "--warmup", "3", "--micro-rows", "16384",
+             "--no-e2e", "--no-cpu-baseline", "--no-next")
+    assert d["value"] > 0 and d["scaling"] == "strong" and d["gpu_launches"] > 0
+    assert 0 < d["roofline"]["frac"] < 1.05
+    assert ("BWD_VPF" in d["roofline"]["kernel"]) == (shard == "vocab-fused")
