@@ -23,6 +23,7 @@
 #include <cuda_fp16.h>
 
 #include <cfloat>
+#include <mutex>
 #include <type_traits>
 
 #include "otk_internal.h"
@@ -1552,6 +1553,36 @@ __global__ void k_combine(int64_t num_rows, int nshards, const float4* __restric
 }
 
 // ---- launchers ---------------------------------------------------------------------------------------
+// Clusters of csize CTAs must fit inside one GPC, so fewer than num_sms / csize of them can be resident at once
+// (GPCs whose SM count is not a multiple of csize leave SMs over). A persistent grid larger than that runs in
+// two waves — half the throughput (measured for 4-CTA rows) — so the grid is capped at the resident count
+// (cudaOccupancyMaxActiveClusters; cached per (kernel, device, cluster size, smem, CTAs per SM)).
+struct ClusterCap {
+  const void* kern;
+  int dev, csize, per_sm;
+  size_t smem;
+  int clusters;
+};
+static std::mutex g_cap_mu;
+static ClusterCap g_cap[64];
+static int g_ncap = 0;
+
+template <typename KernelT>
+static int max_resident_clusters(KernelT kern, int dev, int csize, size_t smem, int per_sm, cudaLaunchConfig_t cfg) {
+  std::lock_guard<std::mutex> lk(g_cap_mu);
+  for (int i = 0; i < g_ncap; ++i)
+    if (g_cap[i].kern == (const void*)kern && g_cap[i].dev == dev && g_cap[i].csize == csize &&
+        g_cap[i].smem == smem && g_cap[i].per_sm == per_sm)
+      return g_cap[i].clusters;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;  // unknown: no cap
+  }
+  if (g_ncap < 64) g_cap[g_ncap++] = ClusterCap{(const void*)kern, dev, csize, per_sm, smem, n};
+  return n;
+}
+
 template <typename KernelT>
 static cudaError_t launch_row_kernel(KernelT kern, const otk_ctx* ctx, const RowParams& p, cudaStream_t s,
                                      int* grid_out, size_t smem_bytes = kSmemBytes, int ctas_per_sm = 1,
@@ -1560,12 +1591,7 @@ static cudaError_t launch_row_kernel(KernelT kern, const otk_ctx* ctx, const Row
   if (e != cudaSuccess) return e;
   int64_t groups = int64_t(ctx->num_sms) * ctas_per_sm / p.csize;
   if (max_ctas > 0 && groups > max_ctas / p.csize) groups = max_ctas / p.csize;  // ranks sharing a GPU
-  if (groups > p.num_rows) groups = p.num_rows;
-  if (groups < 1) groups = 1;
-  const int grid = int(groups * p.csize);
-  if (grid > kMaxCtas) return cudaErrorInvalidConfiguration;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = s;
@@ -1576,6 +1602,16 @@ static cudaError_t launch_row_kernel(KernelT kern, const otk_ctx* ctx, const Row
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = p.csize > 1 ? 1 : 0;
+  if (p.csize > 1) {
+    cfg.gridDim = dim3(unsigned(groups * p.csize));
+    const int cap = max_resident_clusters(kern, ctx->device, p.csize, smem_bytes, ctas_per_sm, cfg);
+    if (cap > 0 && groups > cap) groups = cap;
+  }
+  if (groups > p.num_rows) groups = p.num_rows;
+  if (groups < 1) groups = 1;
+  const int grid = int(groups * p.csize);
+  if (grid > kMaxCtas) return cudaErrorInvalidConfiguration;
+  cfg.gridDim = dim3(grid);
   if (grid_out) *grid_out = grid;
   return cudaLaunchKernelEx(&cfg, kern, p);
 }

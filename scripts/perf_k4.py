@@ -6,6 +6,7 @@ import numpy as np, torch
 import paper_2601_07376_b200 as otk
 from synth import make_batch, make_logits, make_noise
 ap = argparse.ArgumentParser(); ap.add_argument("--rows", type=int, default=65536); ap.add_argument("--iters", type=int, default=10); ap.add_argument("--mask", default="data", choices=["data", "ones", "zeros"])
+ap.add_argument("--vocab", type=int, default=151936)
 ap.add_argument("--variant", default="", help="NEXT-4 loss variant: ent | dual | seqmean | seqsum | sft | turn")
 a = ap.parse_args()
 torch.cuda.set_device(0)
@@ -14,7 +15,8 @@ tb = make_batch("math"); db = otk.traj_batch_to_device(tb)
 m = otk.otk_build_masks(ctx, db)
 adv = otk.otk_group_advantages(ctx, torch.from_numpy(tb.group_id).cuda(), 64, turn_offsets=torch.from_numpy(tb.turn_offsets).cuda(),
                                turn_rewards=torch.from_numpy(tb.turn_rewards).cuda())["adv"]
-n, V = a.rows, 151936
+n, V = a.rows, a.vocab
+peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6532.2
 bufs = [make_logits(n, V, dtype="bf16", seed=5 + k, device="cuda", rows_per_chunk=4096) for k in range(2)]
 olds = []
 for lg, tg in bufs:
@@ -51,6 +53,6 @@ for name, fn, by in (("bwd", run, alg), ("fwd", runf, n * (2 * V + 12))):
     for k in range(a.iters): fn(k)
     ev[1].record(); torch.cuda.synchronize()
     ms = ev[0].elapsed_time(ev[1]) / a.iters
-    res[name] = dict(ms=round(ms, 4), GBps=round(by / ms / 1e6, 1), frac=round(by / ms / 1e6 / 6532.2, 4))
+    res[name] = dict(ms=round(ms, 4), GBps=round(by / ms / 1e6, 1), frac=round(by / ms / 1e6 / peak, 4))
 ctx.check()
-print(json.dumps(dict(lib=os.environ.get("OTK_LIB", "default"), mask=a.mask, variant=a.variant or "default", ntr=ntr, **res)))
+print(json.dumps(dict(lib=os.environ.get("OTK_LIB", "default"), vocab=V, mask=a.mask, variant=a.variant or "default", ntr=ntr, **res)))
