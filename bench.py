@@ -46,14 +46,31 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-next", action="store_true",
                     help="skip the side measurements of the forward (3) and the SURVEY.md §8(f) rows")
-    ap.add_argument("--shard", default="batch", choices=["batch", "vocab", "vocab-fused"],
+    ap.add_argument("--vocab-ways", type=int, default=2,
+                    help="--shard 2d / 2d-fused: vocab shards per row block (world = batch shards x vocab-ways)")
+    ap.add_argument("--shard", default="batch", choices=["batch", "vocab", "vocab-fused", "2d", "2d-fused"],
                     help="batch: each rank owns whole trajectories (weak scaling); vocab: each rank owns V/N "
                          "columns of every row (strong scaling, row partials all-gathered); vocab-fused: the "
-                         "same split with the exchange inside the loss kernel (K4-VPF, CUDA IPC peer buffers)")
+                         "same split with the exchange inside the loss kernel (K4-VPF, CUDA IPC peer buffers); "
+                         "2d / 2d-fused: world / vocab-ways trajectory shards x vocab-ways column shards")
     return ap.parse_args()
 
 
 # ------------------------------------------------------------------------------------------------
+def shard_layout(args, world, rank):
+    """(Pv vocab shards per row block, nb batch shards, b, v, batch group, vocab group) of this rank."""
+    import torch.distributed as dist
+    if args.shard in ("2d", "2d-fused"):
+        if world == 1:
+            return dict(Pv=1, nb=1, b=0, v=0, bg=None, vg=None)
+        from paper_2601_07376_b200.dist import make_2d_groups
+        b, v, bg, vg = make_2d_groups(args.vocab_ways)
+        return dict(Pv=args.vocab_ways, nb=world // args.vocab_ways, b=b, v=v, bg=bg, vg=vg)
+    if args.shard in ("vocab", "vocab-fused"):
+        return dict(Pv=world, nb=1, b=0, v=rank, bg=None, vg=dist.group.WORLD if world > 1 else None)
+    return dict(Pv=1, nb=world, b=rank, v=0, bg=dist.group.WORLD if world > 1 else None, vg=None)
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -143,12 +160,13 @@ def build_workload(args, rank, world, device):
     from paper_2601_07376_b200.step import MicroBatch, VocabShard
     from synth import CONFIGS, make_batch, make_logits, make_noise
     cfgw = CONFIGS[args.config]
-    vocab_mode = args.shard in ("vocab", "vocab-fused")
-    brank = 0 if vocab_mode else rank
+    L = shard_layout(args, world, rank)
+    vocab_mode = args.shard != "batch"
+    brank = L["b"]
     tb = make_batch(args.config, seed=cfgw.seed + 1000 * brank)
     tb.group_id = tb.group_id + np.int32(brank * cfgw.num_groups)   # this rank's groups (global ids)
     N, V = tb.num_rows, cfgw.V
-    v0, v1 = vocab_shard_bounds(V, world)[rank] if vocab_mode else (0, V)
+    v0, v1 = vocab_shard_bounds(V, L["Pv"])[L["v"]]
     Vl = v1 - v0
     M = min(args.micro_rows, N)
     ctx = otk.Context(torch.cuda.current_device())
@@ -161,21 +179,17 @@ def build_workload(args, rank, world, device):
     for k in range(nbuf):
         lg, tg = make_logits(M, Vl, dtype=cfgw.dtype, seed=cfgw.seed * 100 + 10 * rank + k, device=device,
                              rows_per_chunk=4096)
-        if vocab_mode:   # global targets, identical on every rank
+        if vocab_mode:   # global targets, identical on every rank of the row block's vocab group
             g = torch.Generator(device=device)
-            g.manual_seed(cfgw.seed * 100 + k)
+            g.manual_seed(cfgw.seed * 100 + k + 7919 * brank)
             tg = torch.randint(0, V, (M,), generator=g, device=device, dtype=torch.int32)
         bufs.append(lg)
         tgts.append(tg)
     dlogits = torch.empty_like(bufs[0])
-    vshard = VocabShard(ctx, v0, Vl, V, None) if vocab_mode else None
-    pg = None
-    if vocab_mode and world > 1:
-        import torch.distributed as dist
-        vshard.pg = dist.group.WORLD
-    if args.shard == "vocab-fused":   # K4-VPF: exchange buffers mapped once (setup, untimed)
+    vshard = VocabShard(ctx, v0, Vl, V, L["vg"]) if vocab_mode else None
+    if args.shard.endswith("-fused"):   # K4-VPF: exchange buffers mapped once (setup, untimed)
         from paper_2601_07376_b200.step import VocabShardFused
-        if world > 1:
+        if L["vg"] is not None:
             from paper_2601_07376_b200.dist import open_vpf_exchange
             xchg = open_vpf_exchange(ctx, M, vshard.pg)
         else:
@@ -197,7 +211,7 @@ def build_workload(args, rank, world, device):
                               None if ref is None else ref.contiguous(), dlogits[:n]))
     ctx.check()
     return dict(otk=otk, cfgw=cfgw, tb=tb, ctx=ctx, dbatch=dbatch, gid=gid, toff=toff, trew=trew, bufs=bufs,
-                tgts=tgts, mbs=mbs, N=N, V=V, Vl=Vl, v0=v0, M=M, dlogits=dlogits, vshard=vshard)
+                tgts=tgts, mbs=mbs, N=N, V=V, Vl=Vl, v0=v0, M=M, dlogits=dlogits, vshard=vshard, L=L)
 
 
 def algorithmic_bytes(V, n_train, n_masked, beta):
@@ -215,11 +229,12 @@ def run_otk(args):
     from paper_2601_07376_b200.step import PolicyLossStep
     cfgw = W["cfgw"]
     cfg = otk.LossCfg(kl_beta=cfgw.kl_beta)
-    vocab_mode = args.shard in ("vocab", "vocab-fused")
-    bpg = pg if not vocab_mode else None
+    vocab_mode = args.shard != "batch"
+    L = W["L"]
+    bpg, nb, Pv = L["bg"], L["nb"], L["Pv"]
     step = PolicyLossStep(ctx, W["dbatch"], W["gid"], cfgw.num_groups, W["toff"], W["trew"], W["Vl"], cfg,
-                          process_group=bpg, global_num_traj=[W["tb"].num_traj] * world if bpg else None,
-                          global_num_groups=cfgw.num_groups * world if bpg else None, vocab_shard=W["vshard"])
+                          process_group=bpg, global_num_traj=[W["tb"].num_traj] * nb if bpg else None,
+                          global_num_groups=cfgw.num_groups * nb if bpg else None, vocab_shard=W["vshard"])
     stream = torch.cuda.current_stream()
     nmb = len(W["mbs"])
     # CUDA events around every loss launch of every timed step, on the launching stream
@@ -267,14 +282,14 @@ def run_otk(args):
     lm = step.masks["loss_mask"]
     n_train = [int(lm[mb.r0:mb.r1].sum()) for mb in W["mbs"]]
     n_rows = [mb.r1 - mb.r0 for mb in W["mbs"]]
-    if args.shard == "vocab-fused":   # one read + one write of the shard, 32 B per peer per trainable row
+    if args.shard.endswith("-fused"):   # one read + one write of the shard, 32 B per peer per trainable row
         Vl = W["Vl"]
-        side = 4 + 1 + 4 + 4 + (4 if cfgw.kl_beta else 0) + 32 * (world - 1)
+        side = 4 + 1 + 4 + 4 + (4 if cfgw.kl_beta else 0) + 32 * (Pv - 1)
         bytes_k4 = [t * (4 * Vl + side) + (r - t) * (2 * Vl + 1) for t, r in zip(n_train, n_rows)]
         kname = "k_rows_tm<bf16,BWD_VPF> (otk_policy_loss_fwd_bwd_vpf, exchange in-kernel)"
     elif vocab_mode:   # row partials (read 2V_l) + all-gather + streaming pass 2 (read 2V_l, write 2V_l)
         Vl = W["Vl"]
-        side = 4 + 1 + 4 + 4 + (4 if cfgw.kl_beta else 0) + 16 * world
+        side = 4 + 1 + 4 + 4 + (4 if cfgw.kl_beta else 0) + 16 * Pv
         bytes_k4 = [t * (6 * Vl + side) + (r - t) * (2 * Vl + 1) for t, r in zip(n_train, n_rows)]
         kname = "k_rows_tm<bf16,PARTIAL> + all_gather + k_rows_stream<bf16> (vocab-sharded loss)"
     else:
@@ -284,27 +299,28 @@ def run_otk(args):
     avg_ms = sum(k4_ms) / nmb
     achieved = avg_bytes / (avg_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
-    total_rows = W["N"] * (1 if vocab_mode else world)
+    total_rows = W["N"] * nb
     value = total_rows / (ms_per_step * 1e-3)
     step_bytes = sum(bytes_k4)
     if world == 1:
-        par = "single GPU" + (" (vocab-shard path, 1 shard)" if vocab_mode else "")
+        par = "single GPU" + (f" ({args.shard} path, 1 shard)" if vocab_mode else "")
     else:
-        par = (f"vocab-shard tp{world}" + (" (K4-VPF)" if args.shard == "vocab-fused" else "")) if vocab_mode \
-            else f"batch-shard dp{world}"
+        fused = " (K4-VPF)" if args.shard.endswith("-fused") else ""
+        par = (f"batch-shard dp{nb} x vocab-shard tp{Pv}{fused}" if args.shard.startswith("2d")
+               else f"vocab-shard tp{world}{fused}" if vocab_mode else f"batch-shard dp{world}")
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if vocab_mode else "weak",
+        "scaling": "strong" if (nb == 1 and Pv > 1) or args.shard in ("vocab", "vocab-fused") else "weak",
         "vs_baseline": None, "dtype": cfgw.dtype, "data": "synthetic (seeded; SURVEY.md §8(d) recipe)",
         "config": {"workload": f"{args.config}: {cfgw.note}",
-                   "global_batch_traj": W["tb"].num_traj * (1 if vocab_mode else world),
+                   "global_batch_traj": W["tb"].num_traj * nb,
                    "rows_per_gpu": W["N"], "vocab": W["V"], "vocab_per_gpu": W["Vl"], "micro_batch_rows": W["M"],
                    "micro_batches": nmb, "parallelism": par,
                    "l2": f"inputs >> L2: {len(W['bufs'])} logits buffers of "
                          f"{W['bufs'][0].numel() * W['bufs'][0].element_size() / 1e9:.1f} GB cycled",
                    "kl_beta": cfgw.kl_beta, "clip": [0.2, 0.2], "kl": "k3"},
-        "trainable_rows_per_s": sum(n_train) * (1 if vocab_mode else world) / (ms_per_step * 1e-3),
+        "trainable_rows_per_s": sum(n_train) * nb / (ms_per_step * 1e-3),
         "step_algorithmic_GBps": step_bytes / (ms_per_step * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "kernel": kname,
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

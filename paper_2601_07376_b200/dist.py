@@ -14,6 +14,9 @@ cross-shard group statistics"):
 Vocab sharding (north_star: "vocab-sharding logits with an all-reduce of row max and sum-exp"):
   * vocab_shard_bounds  column ranges, multiples of 8 columns (16-byte aligned rows)
   * all_gather_vocab_partials  16 bytes per row per rank: (max, sum-exp, sum-exp*d, z_y)
+2-D (batch x vocab) sharding: world = Pb * Pv ranks, rank = b * Pv + v; rank (b, v) holds trajectory shard b
+and vocab columns v. make_2d_groups builds the two families of subgroups: the batch exchanges above run inside
+the vocab-column group (same v, all b), the per-row partial exchange inside the row group (same b, all v).
   * open_vpf_exchange   K4-VPF setup: every rank's exchange buffer mapped into every rank (CUDA IPC handles
                         all-gathered once); the per-row exchange itself then runs inside the loss kernel
 """
@@ -137,3 +140,25 @@ def open_vpf_exchange(ctx, rows_cap: int, group=None, max_ctas: int = 0):
             opened.append(a)
     dist.barrier(group)  # every mapping exists before any rank's kernel writes into a peer
     return VpfExchange(rank, world, rows_cap, ptrs, max_ctas=max_ctas, opened=opened, owner=ctx)
+
+
+def make_2d_groups(vocab_ways: int, backend: Optional[str] = None):
+    """2-D sharding over the WORLD: returns (b, v, batch_group, vocab_group) for this rank, with
+    rank = b * vocab_ways + v. batch_group = the ranks holding the same vocab columns (different trajectories):
+    the batch-sharding exchanges (n_loss, group returns, stats). vocab_group = the ranks holding the same rows
+    (different columns): the row-partial exchange. Every rank creates every group (torch.distributed rule)."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    if vocab_ways < 1 or world % vocab_ways:
+        raise ValueError(f"world size {world} is not a multiple of vocab_ways {vocab_ways}")
+    nb = world // vocab_ways
+    b, v = divmod(rank, vocab_ways)
+    batch_group = vocab_group = None
+    for vv in range(vocab_ways):
+        g = dist.new_group([bb * vocab_ways + vv for bb in range(nb)], backend=backend)
+        if vv == v:
+            batch_group = g
+    for bb in range(nb):
+        g = dist.new_group([bb * vocab_ways + vv for vv in range(vocab_ways)], backend=backend)
+        if bb == b:
+            vocab_group = g
+    return b, v, batch_group, vocab_group

@@ -126,13 +126,13 @@ class PolicyLossStep:
                  credit: str = "trajectory", gamma: float = 1.0,
                  global_num_segments: Optional[Sequence[int]] = None):
         """process_group: batch sharding (this rank's trajectories; exchanges below). vocab_shard: vocab
-        sharding (every rank holds all rows, a column range of the logits). Exclusive.
+        sharding (the rank holds a column range of the logits of its rows). Both: 2-D sharding — process_group
+        is then the rank's batch group (same columns, other trajectories) and vocab_shard's group its vocab
+        group (same rows, other columns); dist.make_2d_groups builds them.
         credit: "trajectory" (north_star (2): one A per trajectory) or "turn" (NEXT-2, R31: the
         discounted reward-to-go of each trainable ACTION turn, group-normalised over the group's turns,
         read per row through the row's segment). global_num_segments: per-rank segment counts (batch
         sharding with turn credit; default: every rank has this rank's count)."""
-        if process_group is not None and vocab_shard is not None:
-            raise ValueError("batch and vocab sharding are exclusive in this step (2-D sharding is future work)")
         self.vshard = vocab_shard
         self.ctx, self.batch, self.cfg, self.vocab = ctx, batch, cfg, vocab   # (cfg may gain count pointers)
         self.group_id, self.num_groups = group_id, num_groups

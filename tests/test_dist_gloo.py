@@ -155,3 +155,68 @@ def test_vocab_shard_bounds():
         assert all(x[1] == y[0] for x, y in zip(b, b[1:]))
         assert all(x[0] % 8 == 0 for x in b)
     assert vocab_shard_bounds(151936, 4)[1] == (37984, 75968)
+
+
+def _worker_2d(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle_ref as O
+        from paper_2601_07376_b200.dist import make_2d_groups
+        from synth import make_batch
+        b, v, bg, vg = make_2d_groups(2)
+        # group membership: sum of WORLD ranks inside each group
+        t = torch.tensor([float(rank)])
+        dist.all_reduce(t, group=bg)
+        u = torch.tensor([float(rank)])
+        dist.all_reduce(u, group=vg)
+        # batch exchanges inside the batch group: n_loss of this rank's trajectory shard
+        tb = make_batch("game")
+        plan = plan_batch_shards(traj_costs(tb, 151936), 2)
+        b0, b1 = plan[b]
+        loc = _sub_batch(tb, b0, b1)
+        m_loc = O.build_masks(loc.tok_offsets, loc.seg_offsets, loc.seg_source, loc.seg_agent, loc.seg_len,
+                              loc.terminated, traj_agent=loc.traj_agent)
+        n_loss = torch.tensor([m_loc["n_loss"]], dtype=torch.int64)
+        all_reduce_n_loss(n_loss, bg)
+        # row partials inside the vocab group: rows of batch shard b, columns of vocab shard v
+        rng = np.random.default_rng(50 + b)
+        X = rng.normal(scale=3.0, size=(4, 1003))
+        Y = rng.integers(0, 1003, 4)
+        v0, v1 = vocab_shard_bounds(1003, 2)[v]
+        part = torch.tensor([O.shard_partials(X[j, v0:v1], int(Y[j]), v0) for j in range(4)], dtype=torch.float64)
+        g = all_gather_vocab_partials(part, vg)
+        comb = [O.combine_partials([tuple(g[k, j].tolist()) for k in range(2)]) for j in range(4)]
+        q.put(dict(rank=rank, b=b, v=v, bsum=float(t.item()), vsum=float(u.item()), n_loss=int(n_loss.item()),
+                   comb=comb, X=X, Y=Y))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_2d_batch_vocab_groups_gloo():
+    """2-D sharding (world 4 = 2 batch x 2 vocab): group membership, the global token count over the batch
+    group, and the rank-order combine of row partials over the vocab group equal the unsharded values."""
+    from oracle import oracle_ref as O
+    from synth import make_batch
+    world = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_2d, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda d: d["rank"])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    tb = make_batch("game")
+    full = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated,
+                         traj_agent=tb.traj_agent)
+    for r in res:
+        assert (r["b"], r["v"]) == divmod(r["rank"], 2)
+        assert r["bsum"] == r["v"] + (2 + r["v"])          # batch group {v, 2 + v}
+        assert r["vsum"] == 2 * r["b"] + (2 * r["b"] + 1)  # vocab group {2b, 2b + 1}
+        assert r["n_loss"] == full["n_loss"]               # global count over the batch group
+        for j in range(4):
+            lp, H = O.row_forward(r["X"][j], int(r["Y"][j]))[:2]
+            assert abs(r["comb"][j][0] - lp) < 1e-12 and abs(r["comb"][j][1] - H) < 1e-12

@@ -38,6 +38,8 @@ def _sub(tb, b0, b1):
 def _worker(rank, world, port, mode, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    if mode == "2d":
+        return _worker_2d(rank, world, q)
     torch.cuda.set_device(0)
     try:
         import paper_2601_07376_b200 as otk
@@ -119,6 +121,77 @@ def _worker(rank, world, port, mode, q):
         q.put(res)
     finally:
         dist.destroy_process_group()
+
+
+def _worker_2d(rank, world, q):
+    """2-D sharding, world 4 = 2 trajectory shards x 2 vocab shards: PolicyLossStep with the batch group as its
+    process group and a VocabShard over the vocab group; compared with the unsharded step on the same data."""
+    torch.cuda.set_device(0)
+    try:
+        import paper_2601_07376_b200 as otk
+        from paper_2601_07376_b200.dist import make_2d_groups, plan_batch_shards, traj_costs, vocab_shard_bounds
+        from paper_2601_07376_b200.step import MicroBatch, PolicyLossStep, VocabShard
+        from synth import make_logits, make_noise
+        dev = "cuda"
+        ctx = otk.Context(0)
+        b, v, bg, vg = make_2d_groups(2)
+        tb = _batch()
+        V, N = 4096, tb.num_rows
+        logits, targets = make_logits(N, V, dtype="bf16", seed=3, device=dev)
+        lp = otk.otk_logprob_entropy_fwd(ctx, logits, targets)["logp"]
+        old = (lp + make_noise(N, 0.05, 1, device=dev)).contiguous()
+        ref = (lp + make_noise(N, 0.1, 2, device=dev)).contiguous()
+        cfg = otk.LossCfg()
+
+        def step_for(bb, pg=None, counts=None, vshard=None, Vl=V):
+            db = otk.traj_batch_to_device(bb, dev)
+            return PolicyLossStep(ctx, db, torch.from_numpy(bb.group_id).to(dev), 4,
+                                  torch.from_numpy(bb.turn_offsets).to(dev), torch.from_numpy(bb.turn_rewards).to(dev),
+                                  Vl, cfg, process_group=pg, global_num_traj=counts,
+                                  global_num_groups=4 if pg is not None else None, vocab_shard=vshard)
+
+        st0 = step_for(tb)
+        dl0 = torch.empty_like(logits)
+        st0.run([MicroBatch(0, N, logits, targets, old, ref, dl0)])
+        plan = plan_batch_shards(traj_costs(tb, V), 2)
+        b0, b1 = plan[b]
+        r0, r1 = int(tb.tok_offsets[b0]), int(tb.tok_offsets[b1])
+        v0, v1 = vocab_shard_bounds(V, 2)[v]
+        st = step_for(_sub(tb, b0, b1), pg=bg, counts=[e - s for s, e in plan],
+                      vshard=VocabShard(ctx, v0, v1 - v0, V, vg), Vl=v1 - v0)
+        blk = logits[r0:r1, v0:v1].contiguous()
+        dl = torch.empty_like(blk)
+        st.run([MicroBatch(0, r1 - r0, blk, targets[r0:r1].contiguous(), old[r0:r1].contiguous(),
+                           ref[r0:r1].contiguous(), dl)])
+        ctx.check()
+        ref_blk = dl0[r0:r1, v0:v1].float()
+        q.put(dict(rank=rank, loss=otk.stats_dict(st.stats), ref_loss=otk.stats_dict(st0.stats),
+                   adv=st.adv_g["adv"].cpu().numpy(), ref_adv=st0.adv_out["adv"].cpu().numpy(),
+                   n_loss=int(st.masks["n_loss"].item()), n_loss_ref=int(st0.masks["n_loss"].item()),
+                   dl_err=float(((dl.float() - ref_blk).abs() / (ref_blk.abs() * 2 ** -6 + 1e-6)).max())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_2d_sharded_step_four_ranks_one_gpu():
+    world = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, "2d", q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda d: d["rank"])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in res:
+        ref = r["ref_loss"]
+        assert abs(r["loss"]["loss"] - ref["loss"]) <= 1e-5 * max(abs(ref["loss"]), 1e-6)
+        assert r["loss"]["n_tokens"] == ref["n_tokens"] and r["n_loss"] == r["n_loss_ref"]
+        assert np.array_equal(r["adv"], r["ref_adv"])      # global group statistics on every rank
+        assert r["dl_err"] <= 1.0
+    assert res[0]["loss"]["loss"] == res[1]["loss"]["loss"]   # the two vocab ranks of a row block agree
 
 
 @pytest.mark.parametrize("mode", ["batch", "vocab", "batch_turn", "lmhead_vocab", "vocab_fused"])
