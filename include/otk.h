@@ -292,7 +292,9 @@ otk_status otk_policy_loss_fwd_bwd_partials(otk_ctx* ctx, int64_t num_rows, int6
  *               buffer; peers' buffers mapped with otk_ipc_open, or plain buffers of the same device when
  *               several ranks share one GPU), each otk_vpf_xchg_bytes(rows_cap, nranks) bytes, 16-byte
  *               aligned, ZEROED once before the first call and then owned by the library's calls.
- *   epoch     : 1 for the first call on a buffer set, +1 per call (all ranks in lockstep).
+ *   (epoch)   : the call's tag = 1 + the calls completed on this buffer set, kept in the own buffer's tail
+ *               by the kernel itself (its last CTA bumps it), so calls may be captured in a CUDA graph and
+ *               replayed; all ranks must issue the same sequence of calls (lockstep).
  *   max_ctas  : 0 = one CTA per SM; otherwise at most this many CTAs (lets several ranks share a GPU).
  * Every rank must make the same sequence of calls with the same num_rows / masks / targets; a partial that
  * does not arrive within ~20 s sets OTK_ERR_PEER_TIMEOUT (sticky; later waits give up at once) instead of
@@ -304,7 +306,6 @@ typedef struct {
   int32_t nranks;
   int64_t rows_cap;
   void* xchg[OTK_VPF_MAX_RANKS];
-  uint32_t epoch;
   int32_t max_ctas;
 } otk_vpf_peers;
 

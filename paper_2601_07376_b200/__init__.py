@@ -68,7 +68,7 @@ OTK_IPC_HANDLE_BYTES = 64
 
 class otk_vpf_peers(C.Structure):
     _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("rows_cap", C.c_int64),
-                ("xchg", C.c_void_p * OTK_VPF_MAX_RANKS), ("epoch", C.c_uint32), ("max_ctas", C.c_int32)]
+                ("xchg", C.c_void_p * OTK_VPF_MAX_RANKS), ("max_ctas", C.c_int32)]
 
 
 STATS_FIELDS = ("loss", "n_clipped", "kl_sum", "entropy_sum", "n_tokens")   # otk_loss_stats (5 doubles)
@@ -636,7 +636,8 @@ def otk_ipc_close(ptr: int):
 class VpfExchange:
     """One rank's view of the K4-VPF exchange buffers: the device address of every rank's buffer as seen from
     this process (ptrs[rank] = own buffer from otk_xchg_alloc; peers' mapped with otk_ipc_open, or — ranks sharing
-    one GPU — the peers' own buffers). Keeps the per-call epoch (1, 2, ...), which all ranks advance in lockstep.
+    one GPU — the peers' own buffers). The per-call epoch lives on the device (own buffer tail, bumped by the kernel),
+    so calls are CUDA-graph capturable; all ranks must make the same sequence of calls.
     close() unmaps the opened peers and frees the owned buffer."""
 
     def __init__(self, rank: int, nranks: int, rows_cap: int, ptrs, *, max_ctas: int = 0, opened=(),
@@ -644,7 +645,7 @@ class VpfExchange:
         if not (0 <= rank < nranks <= OTK_VPF_MAX_RANKS) or len(ptrs) != nranks:
             raise ValueError("need 0 <= rank < nranks <= OTK_VPF_MAX_RANKS and one pointer per rank")
         self.rank, self.nranks, self.rows_cap = rank, nranks, int(rows_cap)
-        self.ptrs, self.max_ctas, self.epoch, self.opened = [int(x) for x in ptrs], int(max_ctas), 0, list(opened)
+        self.ptrs, self.max_ctas, self.opened = [int(x) for x in ptrs], int(max_ctas), list(opened)
         self.owner = owner
 
     @staticmethod
@@ -655,12 +656,10 @@ class VpfExchange:
         ptrs = [otk_xchg_alloc(c, otk_vpf_xchg_bytes(rows_cap, P)) for c in ctxs]
         return [VpfExchange(r, P, rows_cap, ptrs, max_ctas=max_ctas, owner=ctxs[r]) for r in range(P)]
 
-    def next_peers(self) -> otk_vpf_peers:
-        self.epoch += 1
+    def peers(self) -> otk_vpf_peers:
         pp = otk_vpf_peers(self.rank, self.nranks, self.rows_cap)
         for q, a in enumerate(self.ptrs):
             pp.xchg[q] = a
-        pp.epoch = self.epoch
         pp.max_ctas = self.max_ctas
         return pp
 
@@ -717,14 +716,12 @@ def otk_policy_loss_fwd_bwd_vpf(ctx: Context, logits: torch.Tensor, targets, los
     _arr(cfg.n_active_traj, "cfg.n_active_traj", torch.int64, 1, dev, optional=True)
     sh = otk_vocab_shard(int(vocab_start), int(vocab_total))
     c = cfg.c(accumulate)
-    peers = xchg.next_peers()
+    peers = xchg.peers()
     st = _lib.otk_policy_loss_fwd_bwd_vpf(
         ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits), _ptr(targets), _ptr(loss_mask), _ptr(row_traj),
         _ptr(adv), _ptr(old_logp), _ptr(ref_logp), _ptr(n_loss), C.byref(c), C.byref(sh), C.byref(peers),
         _ptr(dlogits), _ptr(logp), _ptr(entropy), _ptr(stats), _stream(stream))
-    if st != 0:
-        xchg.epoch -= 1   # nothing was launched: the ranks' epochs must stay in lockstep
-        _check(st)
+    _check(st)
     return dict(dlogits=dlogits, logp=logp, entropy=entropy, stats=stats)
 
 

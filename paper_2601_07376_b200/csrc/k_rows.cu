@@ -112,10 +112,16 @@ __device__ __forceinline__ uint64_t vpf_word(float v, uint32_t ep) {
   return uint64_t(__float_as_uint(v)) | (uint64_t(ep) << 32);
 }
 
+// The call's epoch: 1 + the calls completed on this buffer set, read from the device counter in the own buffer
+// (the last CTA of the call bumps it), so a CUDA-graph replay gets a fresh epoch without host involvement.
+__device__ __forceinline__ uint32_t vpf_epoch(const RowParams& p) {
+  return *reinterpret_cast<volatile uint32_t*>(p.vpf_counter) + 1u;
+}
+
 // Push this rank's row partial `mine` = (m2, s, t2, w) into every peer's exchange buffer (one thread).
-__device__ __forceinline__ void vpf_push(const RowParams& p, int64_t row, float4 mine) {
+__device__ __forceinline__ void vpf_push(const RowParams& p, int64_t row, float4 mine, uint32_t ep) {
   const int P = p.vpf_nranks, me = p.vpf_rank;
-  const uint32_t par = p.vpf_epoch & 1u, ep = p.vpf_epoch;
+  const uint32_t par = ep & 1u;
   const int64_t i = vpf_rec_index(p.vpf_rows_cap, P, par, row, me) * 32;
   const uint64_t w0 = vpf_word(mine.x, ep), w1 = vpf_word(mine.y, ep), w2 = vpf_word(mine.z, ep),
                  w3 = vpf_word(mine.w, ep);
@@ -129,9 +135,9 @@ __device__ __forceinline__ void vpf_push(const RowParams& p, int64_t row, float4
 
 // Collect the peers' records of `row` (waiting for this call's epoch) and combine all P partials in rank order
 // exactly as combine_partials does (own = `mine`). Identical bits on every rank.
-__device__ __forceinline__ Stat vpf_collect(const RowParams& p, int64_t row, float4 mine, float& dy) {
+__device__ __forceinline__ Stat vpf_collect(const RowParams& p, int64_t row, float4 mine, float& dy, uint32_t ep) {
   const int P = p.vpf_nranks, me = p.vpf_rank;
-  const uint32_t par = p.vpf_epoch & 1u, ep = p.vpf_epoch;
+  const uint32_t par = ep & 1u;
   const int64_t cap = p.vpf_rows_cap;
   const char* own = reinterpret_cast<const char*>(p.vpf_xchg[me]);
   Stat tot{-INFINITY, 0.f, 0.f};
@@ -173,9 +179,10 @@ __device__ __forceinline__ Stat vpf_collect(const RowParams& p, int64_t row, flo
 
 // Called by one thread per CTA (ct == 0) after the CTA's (cluster's) row total: push (cluster rank 0 only),
 // then collect and combine.
-__device__ __forceinline__ Stat vpf_exchange(const RowParams& p, int64_t row, uint32_t crank, float4 mine, float& dy) {
-  if (crank == 0) vpf_push(p, row, mine);
-  return vpf_collect(p, row, mine, dy);
+__device__ __forceinline__ Stat vpf_exchange(const RowParams& p, int64_t row, uint32_t crank, float4 mine, float& dy,
+                                             uint32_t ep) {
+  if (crank == 0) vpf_push(p, row, mine, ep);
+  return vpf_collect(p, row, mine, dy, ep);
 }
 
 // One element pair of pass 1: d = s2*x - m; e = 2^d; S += e; T += e*d (per-lane fp32 chains; kInit starts
@@ -562,7 +569,7 @@ __device__ __forceinline__ LossOut loss_terms(const RowParams& p, float lp, floa
 }
 
 __device__ __forceinline__ void stats_epilogue(const RowParams& p, double acc_L, double acc_clip, double acc_kl,
-                                               double acc_H, double acc_n, int64_t nl) {
+                                               double acc_H, double acc_n, int64_t nl, uint32_t vpf_ep = 0) {
   double* part = p.cta_partials + size_t(blockIdx.x) * kStatSlots;
   part[0] = acc_L;
   part[1] = acc_clip;
@@ -593,6 +600,7 @@ __device__ __forceinline__ void stats_epilogue(const RowParams& p, double acc_L,
       o->entropy_sum = tot[3];
       o->n_tokens = tot[4];
     }
+    if (p.vpf_counter) *p.vpf_counter = vpf_ep;  // K4-VPF: this call is complete on this rank
     *p.ticket = 0u;
   }
 }
@@ -822,6 +830,7 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
   const float invN = nl > 0 ? float(1.0 / double(nl)) : 0.f;
   const int64_t nact = p.reduction != OTK_TOKEN_MEAN ? *p.n_active : 0;
   uint32_t slot = 0, phase = 0, q = 0;
+  const uint32_t vep = (kVpf && ct == 0) ? vpf_epoch(p) : 0u;  // read before this CTA takes its ticket
 
   // ---- stage B: the previous row's statistics, loss and pass 2 -----------------------------------------
   auto stage_b = [&](const PipeRow& pr) {
@@ -842,7 +851,7 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
     if constexpr (kVpf) {  // csize 1 here: the push went out in stage A
       if (ct == 0) {
         float gdy;
-        const Stat g = vpf_collect(p, pr.row, make_float4(tot.m, tot.s, tot.t, dy), gdy);
+        const Stat g = vpf_collect(p, pr.row, make_float4(tot.m, tot.s, tot.t, dy), gdy, vep);
         S.vbc[pr.q & 1u] = make_float4(g.m, g.s, g.t, gdy);
       }
       named_bar_sync(2, kNCT);
@@ -1051,7 +1060,7 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
       if constexpr (kVpf) {  // csize 1: this CTA's partial is the rank's
         const int64_t yg = int64_t(y) - p.vocab_start;
         const float dyl = (yg >= 0 && yg < p.vocab) ? __fmaf_rn(xy, s2, -r.m) : -INFINITY;
-        vpf_push(p, row, make_float4(r.m, r.s, r.t, dyl));
+        vpf_push(p, row, make_float4(r.m, r.s, r.t, dyl), vep);
       }
     }
     // ---------------- stage B of the previous row (its partials have had a whole pass 1 to arrive)
@@ -1061,7 +1070,7 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
     ++q;
   }
   if (has_prev) stage_b(prev);
-  if (ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl);
+  if (ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl, vep);
 }
 
 // =====================================================================================================
@@ -1129,6 +1138,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
     }
     uint32_t slot = 0, phase = 0, q = 0;
     uint32_t fs = 0, fph = 0;  // FWD / PARTIAL: hand-off ring to the finalizer warp
+    const uint32_t vep = (kVpf && ct == 0) ? vpf_epoch(p) : 0u;  // read before this CTA takes its ticket
 
     int64_t row = group;
     int32_t y_n = 0, rt_n = 0;
@@ -1289,7 +1299,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       if constexpr (kVpf) {  // this rank's partial -> peers; peers' partials -> rank-order total (global row)
         if (ct == 0) {
           float gdy;
-          const Stat g = vpf_exchange(p, row, crank, make_float4(tot.m, tot.s, tot.t, dy), gdy);
+          const Stat g = vpf_exchange(p, row, crank, make_float4(tot.m, tot.s, tot.t, dy), gdy, vep);
           S.vbc[q & 1u] = make_float4(g.m, g.s, g.t, gdy);
         }
         named_bar_sync(2, kNCT);
@@ -1398,7 +1408,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       atomicAdd(&g_phase[3], 1ull);
     }
 #endif
-    if (kBwd && ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl);
+    if (kBwd && ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl, vep);
   }
   tc_fence_before();
   if (csize > 1)

@@ -534,7 +534,7 @@ otk_status otk_policy_loss_fwd_bwd_partials(otk_ctx* ctx, int64_t num_rows, int6
 // ---- K4-VPF: (4) on a vocab shard with the row-partial exchange fused into the kernel -------------------
 int64_t otk_vpf_xchg_bytes(int64_t rows_cap, int32_t nranks) {
   if (rows_cap < 1 || nranks < 1 || nranks > OTK_VPF_MAX_RANKS) return -1;
-  return 2 * rows_cap * nranks * 32;  // [2][cap][P] records of four (value | epoch) 64-bit words
+  return 2 * rows_cap * nranks * 32 + 64;  // [2][cap][P] records of four (value | epoch) words + call counter
 }
 
 otk_status otk_policy_loss_fwd_bwd_vpf(otk_ctx* ctx, int64_t num_rows, int64_t vocab_local, int64_t ld,
@@ -557,7 +557,6 @@ otk_status otk_policy_loss_fwd_bwd_vpf(otk_ctx* ctx, int64_t num_rows, int64_t v
   OTK_REQUIRE(peers->nranks >= 1 && peers->nranks <= OTK_VPF_MAX_RANKS && peers->rank >= 0 &&
                   peers->rank < peers->nranks, OTK_ERR_INVALID_ARG, "need 0 <= rank < nranks <= OTK_VPF_MAX_RANKS");
   OTK_REQUIRE(peers->rows_cap >= num_rows && peers->rows_cap >= 1, OTK_ERR_SHAPE, "num_rows > rows_cap");
-  OTK_REQUIRE(peers->epoch != 0, OTK_ERR_INVALID_ARG, "epoch must be >= 1");
   OTK_REQUIRE(peers->max_ctas >= 0, OTK_ERR_INVALID_ARG, "max_ctas must be >= 0");
   for (int q = 0; q < peers->nranks; ++q)
     OTK_REQUIRE(peers->xchg[q] && aligned16(peers->xchg[q]), OTK_ERR_ALIGNMENT,
@@ -573,7 +572,8 @@ otk_status otk_policy_loss_fwd_bwd_vpf(otk_ctx* ctx, int64_t num_rows, int64_t v
   for (int q = 0; q < peers->nranks; ++q) p.vpf_xchg[q] = peers->xchg[q];
   p.vpf_rank = peers->rank;
   p.vpf_nranks = peers->nranks;
-  p.vpf_epoch = peers->epoch;
+  p.vpf_counter = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(peers->xchg[peers->rank]) +
+                                              2 * peers->rows_cap * peers->nranks * 32);
   p.vpf_rows_cap = peers->rows_cap;
   // pipelined loop (exchange latency hidden behind the next row's pass 1) when a CTA holds the whole shard row
   // and two rows fit its tensor memory

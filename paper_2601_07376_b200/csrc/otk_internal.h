@@ -94,7 +94,7 @@ struct RowParams {
   // K4-VPF: in-kernel exchange of the 16-byte row partials with the other ranks
   void* vpf_xchg[OTK_VPF_MAX_RANKS];  // exchange buffer of every rank (peer-mapped), [vpf_rank] = own
   int vpf_rank, vpf_nranks;
-  uint32_t vpf_epoch;
+  uint32_t* vpf_counter;  // calls completed on this buffer set (own buffer tail); epoch = counter + 1
   int64_t vpf_rows_cap;
   // ctx scratch
   double* cta_partials;

@@ -5,8 +5,9 @@ buffers instead of IPC-mapped peer buffers (the kernel code and the per-rank cal
 
 Checks: logp / entropy bitwise equal on every rank AND to the gathered path (otk_row_partials -> stack ->
 otk_policy_loss_fwd_bwd_partials: same partials, same rank-order combine); loss stats identical on every rank;
-everything within the north_star tolerances of the float64 oracle; repeated calls (epoch parity) reproduce the
-same bits; a missing peer ends in OTK_ERR_PEER_TIMEOUT, not a hang."""
+everything within the north_star tolerances of the float64 oracle; repeated calls (epoch parity) and CUDA-graph
+replays (the epoch lives on the device) reproduce the same bits; a missing peer ends in OTK_ERR_PEER_TIMEOUT,
+not a hang."""
 import numpy as np
 import pytest
 import torch
@@ -135,7 +136,6 @@ def test_vpf_host_validation(otk):
     with pytest.raises(otk.OtkError, match="OTK_ERR_SHAPE"):
         otk.otk_policy_loss_fwd_bwd_vpf(ctx, d["logits"][:, :512], d["targets"], d["mask"], d["row_traj"], d["adv"],
                                         d["old"], d["ref"], nl, otk.LossCfg(), 0, 1024, x[0])
-    assert x[0].epoch == 0                                   # nothing launched: epoch not advanced
     with pytest.raises(ValueError):
         otk.VpfExchange(0, 9, 4, [0] * 9)
     x[0].close()
@@ -162,3 +162,46 @@ def test_vpf_missing_peer_times_out(otk):
     assert 10 < dt < 60, dt
     for e in x:
         e.close()
+
+
+def test_vpf_cuda_graph_replay(otk):
+    """Each rank's call captured in its own CUDA graph and replayed three times (each replay on its rank's
+    stream): the device-resident epoch advances per replay, so every replay reproduces the eager bits."""
+    n, V, P = 96, 151936, 2
+    d, h = row_problem(n, V, dtype="bf16", seed=21)
+    ctxs = [otk.Context(0) for _ in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    xchgs = otk.VpfExchange.local_group(ctxs, n, max_ctas=74)
+    nl = torch.tensor([int(h["mask"].sum())], dtype=torch.int64, device="cuda")
+    cfg = otk.LossCfg(kl_beta=0.04)
+    dl = torch.empty_like(d["logits"])
+    eager = _run_vpf(otk, ctxs, xchgs, streams, d, V, nl, cfg, dl)[0]
+    eager = [{k: t.clone() for k, t in r.items() if k != "dlogits"} for r in eager]
+    dl_eager = dl.clone()
+    b = _bounds(V, P)
+    outs = [dict(logp=torch.empty(n, device="cuda"), entropy=torch.empty(n, device="cuda"),
+                 stats=torch.zeros(5, dtype=torch.float64, device="cuda")) for _ in range(P)]
+    graphs = [torch.cuda.CUDAGraph() for _ in range(P)]
+    torch.cuda.synchronize()
+    for k in range(P):
+        with torch.cuda.graph(graphs[k], stream=streams[k]):
+            otk.otk_policy_loss_fwd_bwd_vpf(ctxs[k], d["logits"][:, b[k]:b[k + 1]], d["targets"], d["mask"],
+                                            d["row_traj"], d["adv"], d["old"], d["ref"], nl, cfg, b[k], V, xchgs[k],
+                                            dlogits=dl[:, b[k]:b[k + 1]], **outs[k])
+    for _ in range(3):
+        dl.zero_()
+        for o in outs:
+            o["logp"].zero_()
+        torch.cuda.synchronize()
+        for k in range(P):
+            with torch.cuda.stream(streams[k]):
+                graphs[k].replay()
+        torch.cuda.synchronize()
+        for c in ctxs:
+            c.check()
+        for k in range(P):
+            assert torch.equal(outs[k]["logp"], eager[k]["logp"])
+            assert torch.equal(outs[k]["stats"], eager[k]["stats"])
+        assert torch.equal(dl, dl_eager)
+    for x in xchgs:
+        x.close()
