@@ -83,3 +83,20 @@ def test_graft_build_from_clean_tree(tmp_path):
             "assert 'paper_2601_07376_b200' not in sys.modules, 'package imported before the build'\n"
             "assert m.LIB.endswith('libotk.so') and callable(m.build)\n") % root
     subprocess.check_call([sys.executable, "-c", code])
+
+
+def test_vpf_host_side_without_gpu(lib):
+    """K4-VPF sizing and argument checks are host-only (no CUDA call): exchange-buffer bytes = two parities of
+    32-byte records per (row, rank) plus the 64-byte call-counter tail; NULL ctx / peers are rejected."""
+    L, _ = lib
+    L.otk_vpf_xchg_bytes.restype = C.c_int64
+    L.otk_vpf_xchg_bytes.argtypes = [C.c_int64, C.c_int32]
+    assert L.otk_vpf_xchg_bytes(1000, 4) == 2 * 1000 * 4 * 32 + 64
+    assert L.otk_vpf_xchg_bytes(0, 4) == -1 and L.otk_vpf_xchg_bytes(10, 9) == -1 and L.otk_vpf_xchg_bytes(10, 0) == -1
+    import paper_2601_07376_b200 as otk
+    assert otk.otk_vpf_xchg_bytes(65536, 8) == 2 * 65536 * 8 * 32 + 64
+    assert C.sizeof(otk.otk_vpf_peers) == 4 + 4 + 8 + 8 * otk.OTK_VPF_MAX_RANKS + 8   # matches include/otk.h
+    st = L.otk_policy_loss_fwd_bwd_vpf(None, C.c_int64(0), C.c_int64(1), C.c_int64(8), 1, *([None] * 15))
+    assert st == 1   # OTK_ERR_INVALID_ARG (ctx is NULL)
+    assert L.otk_ipc_get_handle(None, None) == 1 and L.otk_ipc_open(None, None) == 1
+    assert L.otk_xchg_alloc(None, C.c_int64(64), None) == 1
