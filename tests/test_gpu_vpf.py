@@ -205,3 +205,61 @@ def test_vpf_cuda_graph_replay(otk):
         assert torch.equal(dl, dl_eager)
     for x in xchgs:
         x.close()
+
+
+@pytest.mark.parametrize("case", ["zero_rows", "all_masked", "bad_target"])
+def test_vpf_edges(otk, case):
+    """Degenerate inputs keep every rank in lockstep: no rows, only loss-masked rows (zero-filled, no exchange),
+    and an out-of-range target on a trainable row (skipped by every rank, OTK_ERR_TARGET_RANGE). A normal call
+    on the same buffers afterwards still matches the gathered path (the call counters advanced together)."""
+    n, V, P = 40, 4096, 2
+    d, h = row_problem(n, V, dtype="bf16", seed=9, mask_p=0.0 if case == "all_masked" else 0.7)
+    ctxs = [otk.Context(0) for _ in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    xchgs = otk.VpfExchange.local_group(ctxs, n, max_ctas=16)
+    cfg = otk.LossCfg()
+    b = _bounds(V, P)
+    dl = torch.full_like(d["logits"], 7.0)
+    if case == "zero_rows":
+        e = {k: (t[:0] if isinstance(t, torch.Tensor) and t.dim() >= 1 and t.shape[0] == n else t)
+             for k, t in d.items()}
+        e["logits"] = d["logits"][:0]
+        nl = torch.zeros(1, dtype=torch.int64, device="cuda")
+        out = _run_vpf(otk, ctxs, xchgs, streams, e, V, nl, cfg, dl[:0])[0]
+        for r in out:
+            assert otk.stats_dict(r["stats"])["n_tokens"] == 0
+    elif case == "all_masked":
+        nl = torch.zeros(1, dtype=torch.int64, device="cuda")
+        out = _run_vpf(otk, ctxs, xchgs, streams, d, V, nl, cfg, dl)[0]
+        assert bool((dl == 0).all())
+        for r in out:
+            assert otk.stats_dict(r["stats"])["n_tokens"] == 0 and bool((r["logp"] == 0).all())
+    else:
+        j = int(np.flatnonzero(h["mask"])[0])
+        bad = d["targets"].clone()
+        bad[j] = V + 5
+        e = dict(d, targets=bad)
+        nl = torch.tensor([int(h["mask"].sum())], dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
+        for k in range(P):
+            otk.otk_policy_loss_fwd_bwd_vpf(ctxs[k], e["logits"][:, b[k]:b[k + 1]], e["targets"], e["mask"],
+                                            e["row_traj"], e["adv"], e["old"], e["ref"], nl, cfg, b[k], V, xchgs[k],
+                                            dlogits=dl[:, b[k]:b[k + 1]], stream=streams[k])
+        torch.cuda.synchronize()
+        for c in ctxs:
+            with pytest.raises(otk.OtkError, match="OTK_ERR_TARGET_RANGE"):
+                c.check()
+        assert bool((dl[j] == 0).all())
+        keep = ctxs   # they own the exchange buffers; fresh contexts for the next call (the error word is sticky)
+        ctxs = [otk.Context(0) for _ in range(P)]
+    # a normal call afterwards, same buffers: equal to the gathered path
+    nl = torch.tensor([int(h["mask"].sum())], dtype=torch.int64, device="cuda")
+    out = _run_vpf(otk, ctxs, xchgs, streams, d, V, nl, cfg, dl)[0]
+    parts = torch.stack([otk.otk_row_partials(ctxs[0], d["logits"][:, b[k]:b[k + 1]].contiguous(), d["targets"],
+                                              b[k], V, row_mask=d["mask"]) for k in range(P)]).contiguous()
+    g = otk.otk_policy_loss_fwd_bwd_partials(ctxs[0], d["logits"][:, b[0]:b[1]].contiguous(), d["targets"], d["mask"],
+                                             d["row_traj"], d["adv"], d["old"], d["ref"], nl, cfg, b[0], V, parts)
+    ctxs[0].check()
+    assert torch.equal(g["logp"], out[0]["logp"]) and torch.equal(out[1]["logp"], out[0]["logp"])
+    for x in xchgs:
+        x.close()
