@@ -346,7 +346,7 @@ def run_otk(args):
         res["cpu_baseline"] = cpu_baseline(args, W, cfg)
     if rank == 0 and world == 1 and not args.no_next and not vocab_mode:
         try:
-            res["other_kernels"] = other_kernels(W)
+            res["other_kernels"] = other_kernels(W, step, cfg)
         except Exception as e:  # side measurements never invalidate the headline line
             res["other_kernels"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
@@ -358,7 +358,7 @@ def run_otk(args):
 
 
 # ------------------------------------------------------------------------------------------------
-def other_kernels(W):
+def other_kernels(W, step, cfg):
     """Side measurements (untimed for the headline, rank 0, N = 1): the forward (3) on one micro-batch, the
     rollout sampler (NEXT-3) on a 4096-row decode batch and the fused LM-head forward (NEXT-1) at d = 3584 —
     CUDA events on the launching stream, inputs HBM-resident, each against its own roofline."""
@@ -408,6 +408,36 @@ def other_kernels(W):
     out["lmhead_logprob_fwd"] = {"rows": rows, "hidden_dim": d, "ms": ms, "TFLOPs": tf, "frac_bf16": tf / bf16_peak,
                                  "kernel": "k_lmhead_fwd (tcgen05 cta_group::2; SURVEY.md §8(f) NEXT-1 fwd)"}
     del h, w, y, ws
+    # K4-VPF (vocab-sharded loss, exchange in-kernel): P = 2 ranks co-scheduled on this GPU (own ctx, stream,
+    # column shard, 74 CTAs each) on micro-batch 0, against the unsharded loss on the same rows
+    mb = W["mbs"][0]
+    lm, rt = step.masks["loss_mask"][mb.r0:mb.r1], step.masks["row_traj"][mb.r0:mb.r1]
+    adv, nl = step.adv_out["adv"], step.masks["n_loss"]
+    ms_u = timed(lambda i: otk.otk_policy_loss_fwd_bwd(ctx, mb.logits, mb.targets, lm, rt, adv, mb.old_logp,
+                                                       mb.ref_logp, nl, cfg, dlogits=mb.dlogits, want_logp=False), 4)
+    P = 2
+    b = [V * k // P // 8 * 8 for k in range(P)] + [V]
+    ctxs = [otk.Context(ctx.device) for _ in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    xs = otk.VpfExchange.local_group(ctxs, M, max_ctas=148 // P)
+    main = torch.cuda.current_stream()
+
+    def vpf(i):
+        for s_ in streams:
+            s_.wait_stream(main)
+        for q in range(P):
+            otk.otk_policy_loss_fwd_bwd_vpf(ctxs[q], mb.logits[:, b[q]:b[q + 1]], mb.targets, lm, rt, adv,
+                                            mb.old_logp, mb.ref_logp, nl, cfg, b[q], V, xs[q],
+                                            dlogits=mb.dlogits[:, b[q]:b[q + 1]], stream=streams[q])
+        for s_ in streams:
+            main.wait_stream(s_)
+    ms_v = timed(vpf, 4)
+    for c in ctxs:
+        c.check()
+    for x in xs:
+        x.close()
+    out["vocab_shard_vpf_p2_one_gpu"] = {"rows": M, "ms": ms_v, "ms_unsharded": ms_u, "vs_unsharded": ms_u / ms_v,
+                                         "kernel": "k_rows_tm<bf16,BWD_VPF> x 2 ranks co-scheduled (DESIGN.md §7)"}
     ctx.check()
     return out
 
