@@ -105,3 +105,67 @@ def test_fullsize_microbatch(otk, name, rows):
     want_loss = math.fsum(L) / N
     assert abs(st["loss"] - want_loss) <= 1e-4 * max(abs(want_loss), np.abs(L).sum() / N)
     ctx.close()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_fullsize_vpf_microbatch(otk, P):
+    """K4-VPF at the bench's full size (one 65,536-row math micro-batch, V = 151936, P ranks co-scheduled on the
+    GPU in the perf_vpf.py launch configuration): sampled rows against the oracle, and every row against the
+    unsharded kernel (logp 1e-5, dlogits within bf16 rounding, identical loss stats up to fp64 summation)."""
+    cfgw = CONFIGS["math"]
+    V, M, dev = cfgw.V, 65536, "cuda"
+    tb = make_batch("math")
+    om = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated,
+                       traj_agent=tb.traj_agent)
+    logits, targets = make_logits(M, V, dtype="bf16", seed=cfgw.seed * 100 + 1, device=dev, rows_per_chunk=4096)
+    mask = om["loss_mask"][:M]
+    rt = om["row_traj"][:M]
+    oadv = O.group_advantages(tb.group_id, O.episode_returns(tb.turn_offsets, tb.turn_rewards), tb.num_groups)["adv"]
+    tr = np.flatnonzero(mask)
+    sample = sorted(set(tr[np.linspace(0, len(tr) - 1, 8).astype(int)].tolist()))
+    y = targets.cpu().numpy()
+    wide = {j: logits[j].double().cpu().numpy() for j in sample}
+    base = np.zeros(M)
+    for j in sample:
+        base[j] = O.row_forward(wide[j], int(y[j]))[0]
+    old = torch.from_numpy(base).float().to(dev) + make_noise(M, 0.05, 11, device=dev)
+    ref = torch.from_numpy(base).float().to(dev) + make_noise(M, 0.1, 12, device=dev)
+    d = dict(logits=logits, targets=targets, mask=torch.from_numpy(mask).to(dev),
+             row_traj=torch.from_numpy(rt).to(dev), adv=torch.from_numpy(oadv).to(dev), old=old.contiguous(),
+             ref=ref.contiguous())
+    N = int(mask.sum())
+    nl = torch.tensor([N], dtype=torch.int64, device=dev)
+    cfg = otk.LossCfg(kl_beta=cfgw.kl_beta)
+    ctxs = [otk.Context(0) for _ in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    xchgs = otk.VpfExchange.local_group(ctxs, M, max_ctas=148 // P)
+    b = [V * k // P // 8 * 8 for k in range(P)] + [V]
+    dl = torch.empty_like(logits)
+    torch.cuda.synchronize()
+    res = []
+    for k in range(P):
+        res.append(otk.otk_policy_loss_fwd_bwd_vpf(ctxs[k], logits[:, b[k]:b[k + 1]], targets, d["mask"],
+                                                   d["row_traj"], d["adv"], d["old"], d["ref"], nl, cfg, b[k], V,
+                                                   xchgs[k], dlogits=dl[:, b[k]:b[k + 1]], stream=streams[k]))
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check()
+    full = otk.otk_policy_loss_fwd_bwd(ctxs[0], logits, targets, d["mask"], d["row_traj"], d["adv"], d["old"],
+                                       d["ref"], nl, cfg)
+    ctxs[0].check()
+    for k in range(1, P):
+        assert torch.equal(res[k]["logp"], res[0]["logp"]) and torch.equal(res[k]["stats"], res[0]["stats"])
+    assert float((res[0]["logp"] - full["logp"]).abs().max()) < 1e-5
+    sv, sf = otk.stats_dict(res[0]["stats"]), otk.stats_dict(full["stats"])
+    assert abs(sv["loss"] - sf["loss"]) <= 1e-6 * max(abs(sf["loss"]), 1e-3) and sv["n_tokens"] == sf["n_tokens"] == N
+    for r0 in range(0, M, 8192):   # every row vs the unsharded kernel, in blocks (memory)
+        a = dl[r0:r0 + 8192].float()
+        f = full["dlogits"][r0:r0 + 8192].float()
+        assert float(((a - f).abs() / (f.abs() * 2 ** -6 + 1e-9)).max()) <= 1.0
+    ocfg = oracle_cfg(cfg)
+    for j in sample:
+        lp = O.row_forward(wide[j], int(y[j]))[0]
+        assert abs(float(res[0]["logp"][j]) - lp) < LOGP_TOL["bf16"]
+    del full
+    for x in xchgs:
+        x.close()
