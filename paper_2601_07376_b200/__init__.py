@@ -690,17 +690,21 @@ def otk_policy_loss_fwd_bwd_vpf(ctx: Context, logits: torch.Tensor, targets, los
     N, ld = _row_view(logits, "logits")
     V = logits.shape[1]
     dev = logits.device
-    if dlogits is None:   # same row stride as the logits (the C ABI takes one ld for both)
-        dlogits = torch.empty((N, max(ld, V)), dtype=logits.dtype, device=dev)[:, :V]
+    # default outputs are allocated (and zeroed) on the stream the call runs on: ranks run on their own streams
+    import contextlib
+    on = torch.cuda.stream(stream) if isinstance(stream, torch.cuda.Stream) else contextlib.nullcontext()
+    with on:
+        if dlogits is None:   # same row stride as the logits (the C ABI takes one ld for both)
+            dlogits = torch.empty((N, max(ld, V)), dtype=logits.dtype, device=dev)[:, :V]
+        if logp is None:
+            logp = torch.empty(N, dtype=torch.float32, device=dev)
+        if entropy is None:
+            entropy = torch.empty(N, dtype=torch.float32, device=dev)
+        if stats is None:
+            stats = torch.zeros(len(STATS_FIELDS), dtype=torch.float64, device=dev)
     Nd, ldd = _row_view(dlogits, "dlogits")
     if dlogits.shape != logits.shape or dlogits.dtype != logits.dtype or ldd != ld:
         raise ValueError("dlogits must have the logits' shape, dtype and row stride")
-    if logp is None:
-        logp = torch.empty(N, dtype=torch.float32, device=dev)
-    if entropy is None:
-        entropy = torch.empty(N, dtype=torch.float32, device=dev)
-    if stats is None:
-        stats = torch.zeros(len(STATS_FIELDS), dtype=torch.float64, device=dev)
     _arr(targets, "targets", torch.int32, N, dev)
     _arr(loss_mask, "loss_mask", torch.uint8, N, dev)
     _arr(row_traj, "row_traj", torch.int32, N, dev)
