@@ -521,10 +521,28 @@ def cpu_baseline(args, W, cfg, seconds=None):
         ntrain += int(lm.sum())
         r0 += block
         block = min(block * 2, 1024)
-    return {"value": done / t_used, "unit": UNIT, "cores": threads, "kind": "oracle",
+    # the same oracle on ONE thread, on the first 256 rows (libgomp's thread count, then back)
+    one = None
+    try:
+        import ctypes
+        gomp = ctypes.CDLL("libgomp.so.1")
+        n1 = min(256, mb.r1 - mb.r0)
+        lg = OC.bf16_bits(mb.logits[:n1]) if cfgw.dtype == "bf16" else mb.logits[:n1].cpu().numpy()
+        tg = mb.targets[:n1].cpu().numpy()
+        base = OC.logprob_entropy(lg, tg)["logp"]
+        old = (base + make_noise(n1, 0.05, 7000).double().numpy()).astype(np.float32)
+        ref = (base + make_noise(n1, 0.1, 9000).double().numpy()).astype(np.float32) if cfg.kl_beta else None
+        gomp.omp_set_num_threads(1)
+        t = time.perf_counter()
+        OC.policy_loss(lg, tg, m["loss_mask"][:n1], m["row_traj"][:n1], adv, old, ref, m["n_loss"], ocfg)
+        one = n1 / (time.perf_counter() - t)
+        gomp.omp_set_num_threads(threads)
+    except OSError:
+        pass
+    return {"value": done / t_used, "unit": UNIT, "cores": threads, "kind": "oracle", "value_1thread": one,
             "sample": f"first {done} rows of micro-batch 0 of the {args.config} workload ({ntrain} trainable): "
                       f"fused loss fwd+bwd with dlogits materialised, C float64 oracle (oracle/oracle_cpu.c, "
-                      f"OpenMP {threads} threads), {t_used:.1f} s"}
+                      f"OpenMP {threads} threads), {t_used:.1f} s; value_1thread: the first 256 rows on one thread"}
 
 
 # ------------------------------------------------------------------------------------------------
