@@ -789,6 +789,75 @@ __device__ __forceinline__ void finalize_rows(const RowParams& p, Smem& S, int l
 __device__ unsigned long long g_phase[8];  // experiments only: clock64 sums per phase (warp lane 0 of consumers)
 #endif
 
+// One chunk of pass 1, shared by the row loops: wait for the ring slot, read this thread's two 16-byte vectors,
+// release the slot at once, and add (sum e, sum e*d) of the chunk to the row accumulators (rS, rT) against the row
+// reference mref. mref is set by the row's first chunk (exact path) and raised only when a chunk's partial sums
+// overflow 2^64 or turn NaN (a -inf logit) — then the chunk is redone on the exact path (clamp, packed max,
+// rescale) — so the common chunk needs neither a max reduction nor a rescale. kTail: the segment's last chunk
+// (lanes past segn become -1e30). e0 / e1: the chunk's exponentials (kKeepE: for the tensor-memory copy).
+template <typename T, bool kKeepE, bool kTail, int NS>
+__device__ __forceinline__ void pass1_chunk(Smem& S, const uint8_t* ring, uint32_t& slot, uint32_t& phase, int ct,
+                                            int lane, int c, int segn, float s2, uint64_t s2x2, float& mref,
+                                            uint64_t& rS, uint64_t& rT, uint4& e0, uint4& e1) {
+  using VT = Vec<T>;
+  constexpr int EV = VT::EV;
+  constexpr int CE = kChunkBytes / int(sizeof(T));
+  mbar_wait(&S.full[slot], phase);
+  const uint8_t* buf = ring + size_t(slot) * kChunkBytes;
+  uint4 v0 = *reinterpret_cast<const uint4*>(buf + ct * 16);
+  uint4 v1 = *reinterpret_cast<const uint4*>(buf + (ct + kNCT) * 16);
+  if constexpr (kTail) {
+    const int lc0 = c * CE + ct * EV, lc1 = lc0 + kNCT * EV;
+    if (lc0 + EV > segn) v0 = VT::mask_tail(v0, segn - lc0);
+    if (lc1 + EV > segn) v1 = VT::mask_tail(v1, segn - lc1);
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&S.empty[slot]);
+  if (++slot == NS) {
+    slot = 0;
+    phase ^= 1u;
+  }
+  uint64_t cS[2], cT[2];
+  bool ok = false;
+  if (mref != -INFINITY) {  // fast path: fixed reference, no clamp
+    const uint64_t negm2 = f2(-mref, -mref);
+    e0 = VT::template pass1<kKeepE, false, true>(v0, s2x2, negm2, cS, cT);
+    e1 = VT::template pass1<kKeepE, false, false>(v1, s2x2, negm2, cS, cT);
+    const uint64_t sS = fadd2(cS[0], cS[1]), sT = fadd2(cT[0], cT[1]);
+    float s0, s1, t0, t1;
+    f2_split(sS, s0, s1);
+    f2_split(sT, t0, t1);
+    ok = fmaxf(s0, s1) <= 0x1p64f && !isnan(t0 + t1);  // also false for inf / NaN sums
+    cS[0] = sS;
+    cT[0] = sT;
+  }
+  if (!ok) {  // exact path: the row's first chunk, an overflow, or -inf logits
+    // lanes at or below -1e30 (masked tails, clamped -inf) never set the reference: with a reference that
+    // large, s2*x - m would be dominated by the rounding residual of the product
+    const float mx = VT::max_final(VT::max_acc(VT::max_acc(VT::max_init(), v0), v1));
+    if (mx > -1e30f) {
+      const float mn = fmaxf(mref, __fmul_rn(mx, s2));
+      if (mn > mref) {
+        if (mref != -INFINITY) {
+          const float d = __fsub_rn(mref, mn), f = ex2(d);
+          const uint64_t f2x = f2(f, f);
+          rT = fmul2(f2x, ffma2(f2(d, d), rS, rT));
+          rS = fmul2(rS, f2x);
+        }
+        mref = mn;
+      }
+    }
+    const float mr = (mref == -INFINITY) ? 0.f : mref;
+    const uint64_t negm2 = f2(-mr, -mr);
+    e0 = VT::template pass1<kKeepE, true, true>(v0, s2x2, negm2, cS, cT);
+    e1 = VT::template pass1<kKeepE, true, false>(v1, s2x2, negm2, cS, cT);
+    cS[0] = fadd2(cS[0], cS[1]);
+    cT[0] = fadd2(cT[0], cT[1]);
+  }
+  rS = fadd2(rS, cS[0]);
+  rT = fadd2(rT, cT[0]);
+}
+
 // =====================================================================================================
 // Pipelined K4-VPF consumer (kPipe; segments of <= kPipeChunks chunks, so TWO rows fit a warp's TMEM window).
 // Stage A(r): pass 1 of row r into TMEM half (q & 1), CTA reduction, then the row partial is SENT (cluster
@@ -977,60 +1046,9 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
     uint64_t rS = 0ull, rT = 0ull;
     float mref = -INFINITY;
     auto chunk1 = [&](int c, auto tail) {
-      constexpr bool kTail = decltype(tail)::value;
-      mbar_wait(&S.full[slot], phase);
-      const uint8_t* buf = ring + size_t(slot) * kChunkBytes;
-      uint4 v0 = *reinterpret_cast<const uint4*>(buf + ct * 16);
-      uint4 v1 = *reinterpret_cast<const uint4*>(buf + (ct + kNCT) * 16);
-      if constexpr (kTail) {
-        const int lc0 = c * CE + ct * EV, lc1 = lc0 + kNCT * EV;
-        if (lc0 + EV > segn) v0 = VT::mask_tail(v0, segn - lc0);
-        if (lc1 + EV > segn) v1 = VT::mask_tail(v1, segn - lc1);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[slot]);
-      if (++slot == kSlots) {
-        slot = 0;
-        phase ^= 1u;
-      }
-      uint64_t cS[2], cT[2];
       uint4 e0, e1;
-      bool ok = false;
-      if (mref != -INFINITY) {
-        const uint64_t negm2 = f2(-mref, -mref);
-        e0 = VT::template pass1<true, false, true>(v0, s2x2, negm2, cS, cT);
-        e1 = VT::template pass1<true, false, false>(v1, s2x2, negm2, cS, cT);
-        const uint64_t sS = fadd2(cS[0], cS[1]), sT = fadd2(cT[0], cT[1]);
-        float s0, s1, t0, t1;
-        f2_split(sS, s0, s1);
-        f2_split(sT, t0, t1);
-        ok = fmaxf(s0, s1) <= 0x1p64f && !isnan(t0 + t1);
-        cS[0] = sS;
-        cT[0] = sT;
-      }
-      if (!ok) {
-        const float mx = VT::max_final(VT::max_acc(VT::max_acc(VT::max_init(), v0), v1));
-        if (mx > -1e30f) {
-          const float mn = fmaxf(mref, __fmul_rn(mx, s2));
-          if (mn > mref) {
-            if (mref != -INFINITY) {
-              const float d = __fsub_rn(mref, mn), f = ex2(d);
-              const uint64_t f2x = f2(f, f);
-              rT = fmul2(f2x, ffma2(f2(d, d), rS, rT));
-              rS = fmul2(rS, f2x);
-            }
-            mref = mn;
-          }
-        }
-        const float mr = (mref == -INFINITY) ? 0.f : mref;
-        const uint64_t negm2 = f2(-mr, -mr);
-        e0 = VT::template pass1<true, true, true>(v0, s2x2, negm2, cS, cT);
-        e1 = VT::template pass1<true, true, false>(v1, s2x2, negm2, cS, cT);
-        cS[0] = fadd2(cS[0], cS[1]);
-        cT[0] = fadd2(cT[0], cT[1]);
-      }
-      rS = fadd2(rS, cS[0]);
-      rT = fadd2(rT, cT[0]);
+      pass1_chunk<T, true, decltype(tail)::value, kSlots>(S, ring, slot, phase, ct, lane, c, segn, s2, s2x2, mref, rS,
+                                                          rT, e0, e1);
       tmem_st8(tm + uint32_t(8 * c), e0, e1);
       tmem_st1(tm + uint32_t(kColM + c), __float_as_uint(mref == -INFINITY ? 0.f : mref));
     };
@@ -1205,62 +1223,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       float mref = -INFINITY;
       // one chunk of pass 1; kTail only for the segment's last chunk (lanes past segn become -1e30)
       auto chunk1 = [&](int c, auto tail) {
-        constexpr bool kTail = decltype(tail)::value;
-        mbar_wait(&S.full[slot], phase);
-        const uint8_t* buf = ring + size_t(slot) * kChunkBytes;
-        uint4 v0 = *reinterpret_cast<const uint4*>(buf + ct * 16);
-        uint4 v1 = *reinterpret_cast<const uint4*>(buf + (ct + kNCT) * 16);
-        if constexpr (kTail) {
-          const int lc0 = c * CE + ct * EV, lc1 = lc0 + kNCT * EV;
-          if (lc0 + EV > segn) v0 = VT::mask_tail(v0, segn - lc0);
-          if (lc1 + EV > segn) v1 = VT::mask_tail(v1, segn - lc1);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&S.empty[slot]);
-        if (++slot == NS) {
-          slot = 0;
-          phase ^= 1u;
-        }
-        uint64_t cS[2], cT[2];
         uint4 e0, e1;
-        bool ok = false;
-        if (mref != -INFINITY) {  // fast path: fixed reference, no clamp
-          const uint64_t negm2 = f2(-mref, -mref);
-          e0 = VT::template pass1<kBwd, false, true>(v0, s2x2, negm2, cS, cT);
-          e1 = VT::template pass1<kBwd, false, false>(v1, s2x2, negm2, cS, cT);
-          const uint64_t sS = fadd2(cS[0], cS[1]), sT = fadd2(cT[0], cT[1]);
-          float s0, s1, t0, t1;
-          f2_split(sS, s0, s1);
-          f2_split(sT, t0, t1);
-          ok = fmaxf(s0, s1) <= 0x1p64f && !isnan(t0 + t1);  // also false for inf / NaN sums
-          cS[0] = sS;
-          cT[0] = sT;
-        }
-        if (!ok) {  // exact path: the row's first chunk, an overflow, or -inf logits
-          // lanes at or below -1e30 (masked tails, clamped -inf) never set the reference: with a reference
-          // that large, s2*x - m would be dominated by the rounding residual of the product
-          const float mx = VT::max_final(VT::max_acc(VT::max_acc(VT::max_init(), v0), v1));
-          if (mx > -1e30f) {
-            const float mn = fmaxf(mref, __fmul_rn(mx, s2));
-            if (mn > mref) {
-              if (mref != -INFINITY) {
-                const float d = __fsub_rn(mref, mn), f = ex2(d);
-                const uint64_t f2x = f2(f, f);
-                rT = fmul2(f2x, ffma2(f2(d, d), rS, rT));
-                rS = fmul2(rS, f2x);
-              }
-              mref = mn;
-            }
-          }
-          const float mr = (mref == -INFINITY) ? 0.f : mref;
-          const uint64_t negm2 = f2(-mr, -mr);
-          e0 = VT::template pass1<kBwd, true, true>(v0, s2x2, negm2, cS, cT);
-          e1 = VT::template pass1<kBwd, true, false>(v1, s2x2, negm2, cS, cT);
-          cS[0] = fadd2(cS[0], cS[1]);
-          cT[0] = fadd2(cT[0], cT[1]);
-        }
-        rS = fadd2(rS, cS[0]);
-        rT = fadd2(rT, cT[0]);
+        pass1_chunk<T, kBwd, decltype(tail)::value, NS>(S, ring, slot, phase, ct, lane, c, segn, s2, s2x2, mref, rS,
+                                                        rT, e0, e1);
         if (kBwd) {
           tmem_st8(tm + uint32_t(8 * c), e0, e1);
           tmem_st1(tm + uint32_t(kColM + c), __float_as_uint(mref == -INFINITY ? 0.f : mref));
