@@ -789,6 +789,73 @@ __device__ __forceinline__ void finalize_rows(const RowParams& p, Smem& S, int l
 __device__ unsigned long long g_phase[8];  // experiments only: clock64 sums per phase (warp lane 0 of consumers)
 #endif
 
+// Pass 2 of one row segment, shared by the row loops: dlogits = e * (coef * 2^(m_c - lse)) from tensor memory (e of
+// chunk c at columns tm + 8c, its reference m_c at tm + kColM + c). The TMEM load of chunk c+1 is in flight while
+// chunk c is scaled and stored (two register sets, ping-pong, no copies). The entropy-bonus form (one extra MUFU,
+// log2 e, per element) is selected once per row. The caller then stores the target column.
+template <typename T, int kColM>
+__device__ __forceinline__ void pass2_row(char* drow, uint32_t tm, int ct, int nch, int segn, const RowStats& rs,
+                                          const LossOut& lo) {
+  using VT = Vec<T>;
+  constexpr int EV = VT::EV;
+  constexpr int CE = kChunkBytes / int(sizeof(T));
+  char* tp = drow + ct * 16;
+  auto chunk2 = [&](int c, const uint4& e0, const uint4& e1, uint32_t mw, auto entf) {
+    constexpr bool kEnt = decltype(entf)::value;
+    const float dm = __fsub_rn(__uint_as_float(mw), rs.L2);  // m_c - lse (log2 units)
+    const float qc = ex2(dm);
+    uint4 g0, g1;
+    if constexpr (!kEnt) {
+      const float kt = __fmul_rn(lo.coef, qc);
+      g0 = VT::pass2(e0, kt);
+      g1 = VT::pass2(e1, kt);
+    } else {  // g = e q (coef + wcs (ln2 (log2 e + m_c - lse) + H))
+      const float Ac = qc * fmaf(lo.wcs, fmaf(kLn2, dm, rs.H), lo.coef);
+      const float Bc = qc * lo.wcs * kLn2;
+      g0 = VT::pass2_ent(e0, Ac, Bc);
+      g1 = VT::pass2_ent(e1, Ac, Bc);
+    }
+    char* q0 = tp + size_t(c) * kChunkBytes;
+    if (c < nch - 1 || (c + 1) * CE <= segn) {
+      stg_cs_v4(q0, g0);
+      stg_cs_v4(q0 + kNCT * 16, g1);
+    } else {  // last, partial chunk
+      const uint4 gg[2] = {g0, g1};
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int lc = c * CE + (ct + k * kNCT) * EV;
+        if (lc + EV <= segn) {
+          stg_cs_v4(q0 + k * kNCT * 16, gg[k]);
+        } else if (lc < segn) {
+          float g[EV];
+          VT::unpack(gg[k], g);
+          for (int i = 0; i < EV && lc + i < segn; ++i) VT::store1(drow, lc + i, g[i]);
+        }
+      }
+    }
+  };
+  auto pass2 = [&](auto entf) {
+    uint4 a0, a1, b0, b1;
+    uint32_t am, bm;
+    tmem_ld8_1_issue(tm, tm + uint32_t(kColM), a0, a1, am);
+    tmem_wait_ld_dep(a0, a1, am);
+    for (int c = 0;;) {
+      if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), b0, b1, bm);
+      chunk2(c, a0, a1, am, entf);
+      if (++c >= nch) break;
+      tmem_wait_ld_dep(b0, b1, bm);
+      if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), a0, a1, am);
+      chunk2(c, b0, b1, bm, entf);
+      if (++c >= nch) break;
+      tmem_wait_ld_dep(a0, a1, am);
+    }
+  };
+  if (lo.wcs == 0.f)
+    pass2(std::false_type{});
+  else
+    pass2(std::true_type{});
+}
+
 // One chunk of pass 1, shared by the row loops: wait for the ring slot, read this thread's two 16-byte vectors,
 // release the slot at once, and add (sum e, sum e*d) of the chunk to the row accumulators (rS, rT) against the row
 // reference mref. mref is set by the row's first chunk (exact path) and raised only when a chunk's partial sums
@@ -941,61 +1008,7 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
     }
     const uint32_t tm = tm0 + (pr.q & 1u) * kPipeHalf;
     char* drow = reinterpret_cast<char*>(p.dlogits) + (pr.row * p.ld + c0) * int64_t(sizeof(T));
-    char* tp = drow + ct * 16;
-    auto chunk2 = [&](int c, const uint4& e0, const uint4& e1, uint32_t mw, auto entf) {
-      constexpr bool kEnt = decltype(entf)::value;
-      const float dm = __fsub_rn(__uint_as_float(mw), rs.L2);
-      const float qc = ex2(dm);
-      uint4 g0, g1;
-      if constexpr (!kEnt) {
-        const float kt = __fmul_rn(lo.coef, qc);
-        g0 = VT::pass2(e0, kt);
-        g1 = VT::pass2(e1, kt);
-      } else {
-        const float Ac = qc * fmaf(lo.wcs, fmaf(kLn2, dm, rs.H), lo.coef);
-        const float Bc = qc * lo.wcs * kLn2;
-        g0 = VT::pass2_ent(e0, Ac, Bc);
-        g1 = VT::pass2_ent(e1, Ac, Bc);
-      }
-      char* q0 = tp + size_t(c) * kChunkBytes;
-      if (c < nch - 1 || (c + 1) * CE <= segn) {
-        stg_cs_v4(q0, g0);
-        stg_cs_v4(q0 + kNCT * 16, g1);
-      } else {
-        const uint4 gg[2] = {g0, g1};
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-          const int lc = c * CE + (ct + kk * kNCT) * EV;
-          if (lc + EV <= segn) {
-            stg_cs_v4(q0 + kk * kNCT * 16, gg[kk]);
-          } else if (lc < segn) {
-            float g[EV];
-            VT::unpack(gg[kk], g);
-            for (int i = 0; i < EV && lc + i < segn; ++i) VT::store1(drow, lc + i, g[i]);
-          }
-        }
-      }
-    };
-    auto pass2 = [&](auto entf) {
-      uint4 a0, a1, b0, b1;
-      uint32_t am, bm;
-      tmem_ld8_1_issue(tm, tm + uint32_t(kColM), a0, a1, am);
-      tmem_wait_ld_dep(a0, a1, am);
-      for (int c = 0;;) {
-        if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), b0, b1, bm);
-        chunk2(c, a0, a1, am, entf);
-        if (++c >= nch) break;
-        tmem_wait_ld_dep(b0, b1, bm);
-        if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), a0, a1, am);
-        chunk2(c, b0, b1, bm, entf);
-        if (++c >= nch) break;
-        tmem_wait_ld_dep(a0, a1, am);
-      }
-    };
-    if (lo.wcs == 0.f)
-      pass2(std::false_type{});
-    else
-      pass2(std::true_type{});
+    pass2_row<T, kColM>(drow, tm, ct, nch, segn, rs, lo);
     if (ct == pr.owner) VT::store1(drow, pr.ylc, lo.gy);
   };
 
@@ -1296,63 +1309,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
           // ---------------- pass 2: dlogits = e * (coef * 2^(m_c - lse)) from TMEM; the TMEM load of chunk
           // c+1 is in flight while chunk c is scaled and stored (two register sets, ping-pong, no copies)
           char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
-          char* tp = drow + ct * 16;
-          // one chunk of pass 2; kEnt selects the entropy-bonus form (one extra MUFU, log2 e, per element)
-          auto chunk2 = [&](int c, const uint4& e0, const uint4& e1, uint32_t mw, auto entf) {
-            constexpr bool kEnt = decltype(entf)::value;
-            const float dm = __fsub_rn(__uint_as_float(mw), rs.L2);   // m_c - lse (log2 units)
-            const float qc = ex2(dm);
-            uint4 g0, g1;
-            if constexpr (!kEnt) {
-              const float kt = __fmul_rn(lo.coef, qc);
-              g0 = VT::pass2(e0, kt);
-              g1 = VT::pass2(e1, kt);
-            } else {  // g = e q (coef + wcs (ln2 (log2 e + m_c - lse) + H))
-              const float Ac = qc * fmaf(lo.wcs, fmaf(kLn2, dm, rs.H), lo.coef);
-              const float Bc = qc * lo.wcs * kLn2;
-              g0 = VT::pass2_ent(e0, Ac, Bc);
-              g1 = VT::pass2_ent(e1, Ac, Bc);
-            }
-            char* q0 = tp + size_t(c) * kChunkBytes;
-            if (c < nch - 1 || (c + 1) * CE <= segn) {
-              stg_cs_v4(q0, g0);
-              stg_cs_v4(q0 + kNCT * 16, g1);
-            } else {  // last, partial chunk
-              const uint4 gg[2] = {g0, g1};
-#pragma unroll
-              for (int k = 0; k < 2; ++k) {
-                const int lc = c * CE + (ct + k * kNCT) * EV;
-                if (lc + EV <= segn) {
-                  stg_cs_v4(q0 + k * kNCT * 16, gg[k]);
-                } else if (lc < segn) {
-                  float g[EV];
-                  VT::unpack(gg[k], g);
-                  for (int i = 0; i < EV && lc + i < segn; ++i) VT::store1(drow, lc + i, g[i]);
-                }
-              }
-            }
-          };
-          // TMEM load of chunk c+1 in flight while chunk c is scaled and stored (two register sets)
-          auto pass2 = [&](auto entf) {
-            uint4 a0, a1, b0, b1;
-            uint32_t am, bm;
-            tmem_ld8_1_issue(tm, tm + uint32_t(kColM), a0, a1, am);
-            tmem_wait_ld_dep(a0, a1, am);
-            for (int c = 0;;) {
-              if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), b0, b1, bm);
-              chunk2(c, a0, a1, am, entf);
-              if (++c >= nch) break;
-              tmem_wait_ld_dep(b0, b1, bm);
-              if (c + 1 < nch) tmem_ld8_1_issue(tm + uint32_t(8 * (c + 1)), tm + uint32_t(kColM + c + 1), a0, a1, am);
-              chunk2(c, b0, b1, bm, entf);
-              if (++c >= nch) break;
-              tmem_wait_ld_dep(a0, a1, am);
-            }
-          };
-          if (lo.wcs == 0.f)
-            pass2(std::false_type{});
-          else
-            pass2(std::true_type{});
+          pass2_row<T, kColM>(drow, tm, ct, nch, segn, rs, lo);
           // target column: coef * (p_y - 1), overwriting this thread's own vector store (program order)
           if (ct == owner_ct) VT::store1(drow, ylc, lo.gy);
 #ifdef OTK_PHASE_TIMING
