@@ -108,3 +108,62 @@ int probe_mix12(const void* x, void* y, void* z, size_t nbytes, int grid, cudaSt
   return cudaGetLastError();
 }
 }
+
+// ---- round-1 follow-up probes: the K4 traffic mix with more loads in flight --------------------------------
+// 1 read : 2 writes, 4 independent 16-byte loads in flight per thread before the 8 stores
+__global__ void k_mix12_u4(const uint4* x, uint4* y, uint4* z, size_t n16) {
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __ldg(x + i + k * stride);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(y + i + k * stride), "r"(v[k].x), "r"(v[k].y),
+                   "r"(v[k].z), "r"(v[k].w) : "memory");
+      asm volatile("st.global.cs.v4.b32 [%0], {%1, %1, %1, %1};" ::"l"(z + i + k * stride), "r"(0) : "memory");
+    }
+  }
+  for (; i < n16; i += stride) {
+    uint4 v = __ldg(x + i);
+    y[i] = v;
+    z[i] = make_uint4(0, 0, 0, 0);
+  }
+}
+// row-structured like the loss kernel: rows of `row16` vectors; even rows copied x -> y (read + write), odd rows
+// zero-filled in y (write only); one CTA per row at a time, 4 loads in flight per thread
+__global__ void k_mix_rows(const uint4* x, uint4* y, size_t nrows, size_t row16, int mode) {
+  for (size_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+    const uint4* xs = x + r * row16;
+    uint4* ys = y + r * row16;
+    const bool zero_row = mode == 0 ? (r & 1) : mode == 2;   // 0: alternate, 1: all copy, 2: all zero
+    if (zero_row) {
+      for (size_t i = threadIdx.x; i < row16; i += blockDim.x)
+        asm volatile("st.global.cs.v4.b32 [%0], {%1, %1, %1, %1};" ::"l"(ys + i), "r"(0) : "memory");
+    } else {
+      size_t i = threadIdx.x;
+      for (; i + 3 * blockDim.x < row16; i += 4 * blockDim.x) {
+        uint4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = __ldg(xs + i + k * blockDim.x);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(ys + i + k * blockDim.x), "r"(v[k].x),
+                       "r"(v[k].y), "r"(v[k].z), "r"(v[k].w) : "memory");
+      }
+      for (; i < row16; i += blockDim.x) ys[i] = __ldg(xs + i);
+    }
+  }
+}
+extern "C" {
+int probe_mix12_u4(const void* x, void* y, void* z, size_t nbytes, int grid, cudaStream_t s) {
+  k_mix12_u4<<<grid, 512, 0, s>>>((const uint4*)x, (uint4*)y, (uint4*)z, nbytes / 16);
+  return cudaGetLastError();
+}
+int probe_mix_rows(const void* x, void* y, size_t nbytes, size_t row_bytes, int grid, int threads, int mode,
+                   cudaStream_t s) {
+  k_mix_rows<<<grid, threads, 0, s>>>((const uint4*)x, (uint4*)y, nbytes / row_bytes, row_bytes / 16, mode);
+  return cudaGetLastError();
+}
+}
