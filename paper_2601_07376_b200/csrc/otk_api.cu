@@ -37,12 +37,13 @@ otk_status cuda_fail(cudaError_t e, const char* where) {
 size_t dtype_size(otk_dtype d) { return d == OTK_BF16 ? 2 : 4; }
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// Cluster size for the row kernels: the smallest power of two whose per-CTA column segment fits the
-// tensor-memory-resident budget (kMaxChunks chunks). Every mode uses the same rule so that the
+// Cluster size for the row kernels: the smallest number of CTAs (1..8, any size: a 3-CTA cluster keeps more SMs
+// busy than a 4-CTA one) whose per-CTA column segment fits the tensor-memory-resident budget
+// (kMaxChunks chunks). Every mode uses the same rule so that the
 // forward (3) and the fused loss (4) reduce in the same order (bitwise-equal logp: on-policy ratio = 1).
 int choose_csize(int64_t vocab, size_t es, int* seg_elems) {
   const int64_t budget = int64_t(otk::kMaxChunks) * otk::kChunkBytes;
-  for (int c = 1; c <= 8; c *= 2) {
+  for (int c = 1; c <= 8; ++c) {
     int64_t seg = (vocab + c - 1) / c;
     seg = (seg + 7) / 8 * 8;
     if (seg * int64_t(es) <= budget && int64_t(c - 1) * seg < vocab) {

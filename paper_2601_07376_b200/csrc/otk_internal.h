@@ -41,8 +41,8 @@ constexpr int kSlots = 18;               // ring depth: 216 KB of shared memory 
 constexpr int kSlotsFwd = 8;             // FWD / PARTIAL: 96 KB ring, so two CTAs share an SM (twice the warps)
 constexpr int kConsumerWarps = 12;       // 384 compute threads
 constexpr int kThreads = 32 * (2 + kConsumerWarps);  // + loader warp 0 + zero-fill warp 13
-constexpr int kMaxChunks = 13;           // a CTA's row segment (<= 13 chunks, 156 KB) is kept in TMEM
-constexpr int kTmemWindow = 128;         // TMEM columns per consumer warp (3 windows per lane quadrant)
+constexpr int kMaxChunks = 18;           // a CTA's row segment (<= 18 chunks, 216 KB) is kept in TMEM (162 columns)
+constexpr int kTmemWindow = 168;         // TMEM columns per consumer warp (3 windows per lane quadrant: 504 of 512)
 constexpr int kPipeChunks = 7;           // pipelined K4-VPF: <= 7 chunks (84 KB) per CTA, two rows per TMEM window
 
 enum RowMode : int {

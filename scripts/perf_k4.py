@@ -7,6 +7,7 @@ import paper_2601_07376_b200 as otk
 from synth import make_batch, make_logits, make_noise
 ap = argparse.ArgumentParser(); ap.add_argument("--rows", type=int, default=65536); ap.add_argument("--iters", type=int, default=10); ap.add_argument("--mask", default="data", choices=["data", "ones", "zeros"])
 ap.add_argument("--vocab", type=int, default=151936)
+ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
 ap.add_argument("--variant", default="", help="NEXT-4 loss variant: ent | dual | seqmean | seqsum | sft | turn")
 a = ap.parse_args()
 torch.cuda.set_device(0)
@@ -17,7 +18,8 @@ adv = otk.otk_group_advantages(ctx, torch.from_numpy(tb.group_id).cuda(), 64, tu
                                turn_rewards=torch.from_numpy(tb.turn_rewards).cuda())["adv"]
 n, V = a.rows, a.vocab
 peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6532.2
-bufs = [make_logits(n, V, dtype="bf16", seed=5 + k, device="cuda", rows_per_chunk=4096) for k in range(2)]
+bufs = [make_logits(n, V, dtype=a.dtype, seed=5 + k, device="cuda", rows_per_chunk=4096) for k in range(2)]
+es = 2 if a.dtype == "bf16" else 4
 olds = []
 for lg, tg in bufs:
     lp = otk.otk_logprob_entropy_fwd(ctx, lg, tg)["logp"]
@@ -27,7 +29,7 @@ lm, rt = m["loss_mask"][:n].clone(), m["row_traj"][:n]
 if a.mask == "ones": lm.fill_(1)
 if a.mask == "zeros": lm.fill_(0)
 ntr = int(lm.sum())
-alg = ntr * (4 * V + 21) + (n - ntr) * (2 * V + 1)
+alg = ntr * (2 * es * V + 21) + (n - ntr) * (es * V + 1)
 kw = dict(ent=dict(ent_coef=0.01), dual=dict(dual_clip=3.0), seqmean=dict(reduction=1), seqsum=dict(reduction=2),
           sft=dict(sft=True)).get(a.variant, {})
 cfg = otk.LossCfg(**kw, traj_loss_tokens=m["traj_loss_tokens"], n_active_traj=m["n_active_traj"])
@@ -45,7 +47,7 @@ def runf(k):
     lg, tg = bufs[k % 2]
     otk.otk_logprob_entropy_fwd(ctx, lg, tg)
 res = {}
-for name, fn, by in (("bwd", run, alg), ("fwd", runf, n * (2 * V + 12))):
+for name, fn, by in (("bwd", run, alg), ("fwd", runf, n * (es * V + 12))):
     for k in range(3): fn(k)
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -55,4 +57,4 @@ for name, fn, by in (("bwd", run, alg), ("fwd", runf, n * (2 * V + 12))):
     ms = ev[0].elapsed_time(ev[1]) / a.iters
     res[name] = dict(ms=round(ms, 4), GBps=round(by / ms / 1e6, 1), frac=round(by / ms / 1e6 / peak, 4))
 ctx.check()
-print(json.dumps(dict(lib=os.environ.get("OTK_LIB", "default"), vocab=V, mask=a.mask, variant=a.variant or "default", ntr=ntr, **res)))
+print(json.dumps(dict(lib=os.environ.get("OTK_LIB", "default"), vocab=V, dtype=a.dtype, mask=a.mask, variant=a.variant or "default", ntr=ntr, **res)))

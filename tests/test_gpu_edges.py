@@ -131,9 +131,9 @@ def test_targets_on_segment_boundaries(otk, ctx, dtype, V):
     logp and the target column of dlogits (coef * (p_y - 1)) against the oracle."""
     from synth import make_logits, make_noise
     seg = None
-    for c in (1, 2, 4, 8):     # the row kernel's split (DESIGN.md §6): smallest power of two fitting 13 x 12 KB
+    for c in range(1, 9):      # the row kernel's split (DESIGN.md §6): fewest CTAs whose segment fits 18 x 12 KB
         s = ((V + c - 1) // c + 7) // 8 * 8
-        if s * (2 if dtype == "bf16" else 4) <= 13 * 12288:
+        if s * (2 if dtype == "bf16" else 4) <= 18 * 12288 and (c - 1) * s < V:
             seg = s
             break
     cols = sorted({0, V - 1} | {k * seg for k in range(1, (V + seg - 1) // seg)} |

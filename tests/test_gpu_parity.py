@@ -159,8 +159,9 @@ CASES = [
     (33001, 33008, "bf16", 120, 0.0, 3, 1.0, False),
     (151936, 151936, "bf16", 150, 0.04, 3, 1.0, True),
     (151936, 151936, "f32", 24, 0.04, 3, 1 / 0.7, True),
-    (262144, 262144, "bf16", 40, 0.04, 3, 1.0, True),     # 4-CTA clusters (Gemma-class vocabulary)
-    (300000, 300000, "f32", 10, 0.04, 3, 1.0, True),      # 8-CTA clusters
+    (262144, 262144, "bf16", 40, 0.04, 3, 1.0, True),     # 3-CTA clusters (Gemma-class vocabulary)
+    (300000, 300000, "f32", 10, 0.04, 3, 1.0, True),      # 6-CTA clusters
+    (700003, 700008, "bf16", 8, 0.04, 3, 1.0, True),      # 7-CTA clusters (odd size, short last segment)
 ]
 
 
