@@ -220,3 +220,43 @@ def test_2d_batch_vocab_groups_gloo():
         for j in range(4):
             lp, H = O.row_forward(r["X"][j], int(r["Y"][j]))[:2]
             assert abs(r["comb"][j][0] - lp) < 1e-12 and abs(r["comb"][j][1] - H) < 1e-12
+
+
+def _worker_vpf_setup(rank, world, port, q):
+    """dist.open_vpf_exchange's host logic with the CUDA calls stubbed (CPU): every rank allocates its buffer,
+    the 64-byte handles are all-gathered in rank order, and each rank maps the OTHER ranks' handles."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2601_07376_b200 as otk
+        from paper_2601_07376_b200 import dist as D
+        base = 0x10000 * (rank + 1)
+        opened = []
+        otk.otk_xchg_alloc = lambda ctx, n: base
+        otk.otk_ipc_get_handle = lambda ptr: ptr.to_bytes(8, "little") * 8
+        otk.otk_ipc_open = lambda h: (opened.append(h), 0x7000000 + int.from_bytes(h[:8], "little"))[1]
+        x = D.open_vpf_exchange(object(), 1024)
+        q.put(dict(rank=rank, ptrs=x.ptrs, nranks=x.nranks, me=x.rank, opened=[int.from_bytes(h[:8], "little")
+                                                                               for h in opened]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_open_vpf_exchange_host_logic_gloo():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_vpf_setup, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda d: d["rank"])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in res:
+        k = r["rank"]
+        assert r["me"] == k and r["nranks"] == world
+        assert r["ptrs"][k] == 0x10000 * (k + 1)                                   # own buffer, unmapped
+        assert r["opened"] == [0x10000 * (j + 1) for j in range(world) if j != k]  # peers, rank order
+        assert all(r["ptrs"][j] == 0x7000000 + 0x10000 * (j + 1) for j in range(world) if j != k)
