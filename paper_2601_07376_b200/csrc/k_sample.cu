@@ -461,6 +461,11 @@ cudaError_t launch_sample(otk_ctx* ctx, const SampleParams& p0, int dtype, cudaS
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (best_c == 1) {
+#ifndef OTK_SAMPLE_V1
+    // sampled draws, one CTA per row: the ring-streamed kernel with an off-path search warp (k_sample_tm.cu);
+    // greedy stays here (its lane-strided pass measured faster: 225 vs 272 us at 4096 rows)
+    if (!p.greedy && sample_tm_fits(p.vocab, dtype)) return launch_sample_tm(ctx, p, dtype, s);
+#endif
     cfg.numAttrs = 0;
     return dtype == OTK_BF16 ? cudaLaunchKernelEx(&cfg, k_sample<__nv_bfloat16, false>, p)
                              : cudaLaunchKernelEx(&cfg, k_sample<float, false>, p);

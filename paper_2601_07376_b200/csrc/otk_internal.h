@@ -168,6 +168,9 @@ struct SampleParams {
   int* err;
 };
 cudaError_t launch_sample(otk_ctx* ctx, const SampleParams& p, int dtype, cudaStream_t s);
+constexpr int kSampleTmMaxChunks = 64;   // k_sample_tm: rows of <= 64 x 12 KB (bf16 V <= 393216, fp32 V <= 196608)
+bool sample_tm_fits(int64_t vocab, int dtype);
+cudaError_t launch_sample_tm(otk_ctx* ctx, const SampleParams& p, int dtype, cudaStream_t s);
 
 int lmhead_chunks(int64_t num_rows, int64_t vocab, int num_sms);
 cudaError_t launch_lmhead_fwd(const otk_ctx* ctx, int64_t num_rows, int64_t vocab, int d, const void* hidden,

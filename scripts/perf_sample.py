@@ -11,7 +11,7 @@ a = ap.parse_args()
 torch.cuda.set_device(0)
 ctx = otk.Context(0)
 V = 151936
-peak = 6532.2
+peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6532.2
 for n in [int(r) for r in a.rows.split(",")]:
     nb = max(2, -(-400_000_000 // (n * V * 2)))        # cycle >= 400 MB of logits (> L2)
     nb = min(nb, 8)
