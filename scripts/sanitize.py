@@ -27,6 +27,29 @@ for V, dtype in ((151936, "bf16"), (1000, "f32")):
     otk.otk_sample_tokens(ctx, lg, u)
     otk.otk_sample_tokens(ctx, lg, greedy=True)
     otk.otk_sample_tokens(ctx, lg[:3].contiguous(), u[:3].contiguous())   # clustered rows
+# large sampled batch: one CTA per row (k_sample_tm), bf16 and fp32, a ragged vocabulary
+for V, dtype in ((151936, "bf16"), (4100, "bf16"), (1003, "f32")):
+    lg, _ = make_logits(400, V, ld=-(-V // 8) * 8, dtype=dtype, seed=2, device="cuda")
+    otk.otk_sample_tokens(ctx, lg, torch.rand(400, device="cuda"), vocab=V)
+# K4-VPF: two ranks co-scheduled on the GPU
+lg, tg = make_logits(N, 4096, dtype="bf16", seed=3, device="cuda")
+ctxs = [otk.Context(0), otk.Context(0)]
+xs = otk.VpfExchange.local_group(ctxs, N, max_ctas=8)
+m = otk.otk_build_masks(ctx, db)
+a = otk.otk_group_advantages(ctx, torch.from_numpy(tb.group_id).cuda(), tb.num_groups,
+                             turn_offsets=torch.from_numpy(tb.turn_offsets).cuda(),
+                             turn_rewards=torch.from_numpy(tb.turn_rewards).cuda())
+o = torch.zeros(N, device="cuda")
+ss = [torch.cuda.Stream(), torch.cuda.Stream()]
+torch.cuda.synchronize()
+for k in range(2):
+    otk.otk_policy_loss_fwd_bwd_vpf(ctxs[k], lg[:, 2048 * k:2048 * (k + 1)], tg, m["loss_mask"], m["row_traj"], a["adv"],
+                                    o, o, m["n_loss"], otk.LossCfg(), 2048 * k, 4096, xs[k], stream=ss[k])
+torch.cuda.synchronize()
+for c in ctxs:
+    c.check()
+for x in xs:
+    x.close()
 from synth import make_lmhead
 h, w, y = make_lmhead(300, 1000, 128, seed=4, device="cuda")
 otk.otk_lmhead_logprob_fwd(ctx, h, w, y)
