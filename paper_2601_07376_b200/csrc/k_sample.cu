@@ -441,6 +441,14 @@ int sample_occupancy(otk_ctx* ctx, int dtype) {
 }
 
 cudaError_t launch_sample(otk_ctx* ctx, const SampleParams& p0, int dtype, cudaStream_t s) {
+#ifndef OTK_SAMPLE_V1
+  // sampled draws from one SM's worth of rows up: the ring-streamed kernel, one CTA per row, with an off-path
+  // search warp (k_sample_tm.cu; 256 rows 22.9 vs 25.1 us, 4096 rows 218 vs 262 us). Smaller batches keep the
+  // cluster-split kernel below (a cluster-split version of the ring kernel measured no faster at 16-128 rows);
+  // greedy stays here at every size (its lane-strided pass measured faster: 225 vs 272 us at 4096 rows).
+  if (!p0.greedy && p0.num_rows >= ctx->num_sms && sample_tm_fits(p0.vocab, dtype))
+    return launch_sample_tm(ctx, p0, dtype, s);
+#endif
   SampleParams p = p0;
   const int64_t slots = int64_t(ctx->num_sms) * sample_occupancy(ctx, dtype);
   // cluster size: when rows are few, as many CTAs per row as fit in ONE wave of resident CTAs; one CTA
@@ -461,11 +469,6 @@ cudaError_t launch_sample(otk_ctx* ctx, const SampleParams& p0, int dtype, cudaS
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (best_c == 1) {
-#ifndef OTK_SAMPLE_V1
-    // sampled draws, one CTA per row: the ring-streamed kernel with an off-path search warp (k_sample_tm.cu);
-    // greedy stays here (its lane-strided pass measured faster: 225 vs 272 us at 4096 rows)
-    if (!p.greedy && sample_tm_fits(p.vocab, dtype)) return launch_sample_tm(ctx, p, dtype, s);
-#endif
     cfg.numAttrs = 0;
     return dtype == OTK_BF16 ? cudaLaunchKernelEx(&cfg, k_sample<__nv_bfloat16, false>, p)
                              : cudaLaunchKernelEx(&cfg, k_sample<float, false>, p);
