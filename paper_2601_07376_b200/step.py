@@ -260,3 +260,45 @@ class PolicyLossStep:
     def run(self, micro_batches: Sequence[MicroBatch], on_launch=None):
         adv = self.masks_and_advantages()
         return self.loss(adv, micro_batches, on_launch)
+
+
+class LMHeadPolicyLoss:
+    """The policy loss and its gradients THROUGH the LM head (backward half, unfused
+    form): x = h Wᵀ (bf16 tensor-core GEMM, cuBLAS through torch — a plain library GEMM), then
+    (4) on x with cfg.logit_scale = s (otk_policy_loss_fwd_bwd: loss, stats and dx = dL/dx in one pass over x),
+    then dh = dx W and dW = dxᵀ h (cuBLAS). The fused alternative that never stores x needs x recomputed in the
+    backward — a fourth GEMM — which costs more than the traffic it saves at Qwen-class hidden sizes
+    (DESIGN.md §10); `timings=True` returns the measured split. x and dx buffers are reused across calls."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+        self._x = self._dx = None
+
+    def __call__(self, hidden: torch.Tensor, weight: torch.Tensor, targets, loss_mask, row_traj, adv, old_logp,
+                 ref_logp, n_loss, cfg: LossCfg, *, timings: bool = False) -> dict:
+        N, d = hidden.shape
+        V = weight.shape[0]
+        if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16 or weight.shape[1] != d:
+            raise ValueError("hidden [N, d] and weight [V, d] must be bfloat16")
+        if self._x is None or self._x.shape != (N, V):
+            self._x = torch.empty((N, V), dtype=torch.bfloat16, device=hidden.device)
+            self._dx = torch.empty_like(self._x)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timings else None
+        if ev:
+            ev[0].record()
+        torch.matmul(hidden, weight.t(), out=self._x)
+        if ev:
+            ev[1].record()
+        out = otk_policy_loss_fwd_bwd(self.ctx, self._x, targets, loss_mask, row_traj, adv, old_logp, ref_logp,
+                                      n_loss, cfg, dlogits=self._dx)
+        if ev:
+            ev[2].record()
+        dh = torch.matmul(self._dx, weight)
+        dW = torch.matmul(self._dx.t(), hidden)
+        out.update(dh=dh, dW=dW)
+        if ev:
+            ev[3].record()
+            torch.cuda.synchronize()
+            out["ms"] = dict(logits_gemm=ev[0].elapsed_time(ev[1]), loss_kernel=ev[1].elapsed_time(ev[2]),
+                             grad_gemms=ev[2].elapsed_time(ev[3]))
+        return out
