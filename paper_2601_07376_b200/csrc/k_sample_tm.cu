@@ -8,7 +8,8 @@
 //   warp 0 (one thread)  loader: 12 KB chunks of the row into an 8-slot ring (cp.async.bulk + mbarrier).
 //   warps 1-12           consumers: thread ct reads the ADJACENT 16-byte vectors 2ct, 2ct+1 of a chunk, so a warp
 //                        covers one contiguous 1 KB column segment per chunk. Per chunk and warp: a reference r
-//                        (raised, warp-uniformly, only when a value would pass 2^32 above it), the segment's sum of
+//                        (set by the first finite values, raised warp-uniformly only when a chunk sum overflows
+//                        2^64 — no max in the common chunk), the segment's sum of
 //                        e = 2^(x k2 - r) (one MUFU per element), reduced over the warp and stored with r.
 //                        No per-row barrier: the segment sums go to the
 //                        search warp through a 2-row mbarrier hand-off and the consumers stream on.
@@ -187,19 +188,30 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
         else if (v0 == nvec - 1 && tail_valid < EV) SV::mask_tail(q0, tail_valid);
         if (v0 + 1 >= nvec) q1 = ninf;
         else if (v0 + 1 == nvec - 1 && tail_valid < EV) SV::mask_tail(q1, tail_valid);
-        const float vm = fmaxf(SV::vmax(q0), SV::vmax(q1));
-        // raise the warp's reference (rare: the first finite values, or 2^32 above it)
-        if (__any_sync(0xffffffffu, vm * k2 > r + 32.f)) {
-          float wm = vm;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
-          if (wm * k2 > r) r = wm * k2;
-        }
+        // the warp's reference r: set from the warp maximum when there is none yet, and raised to the chunk's
+        // warp maximum only when a thread's chunk sum leaves [0, 2^64] (overflow; NaN from +inf) — detected from
+        // the sums, so the common chunk needs no max at all. Each chunk's sum is stored with its own r.
         float cs = 0.f;
-        if (r > kSNoRef) {
+        bool redo = !(r > kSNoRef);
+        if (!redo) {
           const float rk = -r;
           const uint64_t rk2 = f2(rk, rk);
           cs = __fadd_rn(SV::esum(q0, k2x2, rk2), SV::esum(q1, k2x2, rk2));
+          redo = __any_sync(0xffffffffu, !(cs <= 0x1p64f));
+        } else {
+          redo = true;
+        }
+        if (redo) {  // warp-uniform: the first chunk with a finite value, or an overflow
+          float wm = fmaxf(SV::vmax(q0), SV::vmax(q1));
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+          if (wm * k2 > r) r = wm * k2;
+          cs = 0.f;
+          if (r > kSNoRef) {
+            const float rk = -r;
+            const uint64_t rk2 = f2(rk, rk);
+            cs = __fadd_rn(SV::esum(q0, k2x2, rk2), SV::esum(q1, k2x2, rk2));
+          }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) cs = __fadd_rn(cs, __shfl_xor_sync(0xffffffffu, cs, o));
