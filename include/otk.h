@@ -339,6 +339,7 @@ otk_status otk_ipc_close(void* dev_ptr);
  *                OTK_ERR_INVALID_ARG in the error word and is clamped);
  *   greedy == 1: tokens[j] = argmax_v x_jv, ties to the lowest id (uniforms may be NULL).
  * logp[j] (NULL ok) = log p_j(tokens[j]). A row whose logits are all -inf gives token 0, logp -inf.
+ * Greedy with logp == NULL computes no exponentials (a pure max pass over the row).
  * logits: [num_rows, ld] bf16 / fp32, 16-byte aligned rows; tokens[num_rows] i32 (device).
  * One HBM read of each logit (the re-reads of pass 2/3 hit L2). Parity: greedy bit-exact; a sampled
  * token is exact unless u_j lies within 2e-5 of a cdf boundary, where either neighbour is accepted.

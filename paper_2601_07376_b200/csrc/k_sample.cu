@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(kSampleThreads, OTK_SAMPLE_MINB) k_sample(cons
   const float thr = 32.f / k2;  // raise the reference only when values would pass 2^32
   const uint64_t k2x2 = f2(k2, k2);
   const bool greedy = p.greedy != 0;
+  const bool need_sum = !(greedy && p.logp == nullptr);  // greedy without logp: the argmax needs no exponentials
 
   int parity = 0;
   for (int64_t row = group; row < p.num_rows; row += ngroups, parity ^= 1) {
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(kSampleThreads, OTK_SAMPLE_MINB) k_sample(cons
         const float mk = -vm * k2;
         mk2 = f2(mk, mk);
       }
-      a2 = SV::acc(q, k2x2, mk2, a2);
+      if (need_sum) a2 = SV::acc(q, k2x2, mk2, a2);
       if (greedy && vm > best) {
         best = vm;
         bv = vk;
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(kSampleThreads, OTK_SAMPLE_MINB) k_sample(cons
         S += sr * rescale(mr, M, k2);
       }
     }
-    const bool degenerate = !(M > kNoRef) || !(S > 0.f);  // no finite logit above -1e30
+    const bool degenerate = !(M > kNoRef) || (need_sum && !(S > 0.f));  // no finite logit above -1e30
 #ifndef OTK_SAMPLE_NO_PREFETCH
     // warm L2 with the start of this thread's slice of the next row while the search below (latency-bound)
     // runs, so the next row's main pass starts from L2 rather than HBM

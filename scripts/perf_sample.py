@@ -43,6 +43,25 @@ for n in [int(r) for r in a.rows.split(",")]:
         by = n * (2 * V + 12)
         res[mode] = dict(us=round(ms * 1e3, 1), GBps=round(by / ms / 1e6, 1), frac=round(by / ms / 1e6 / peak, 4),
                          rows_per_s=round(n / ms * 1e3))
+    # greedy without logp (no exponentials)
+    toks = torch.empty(n, dtype=torch.int32, device="cuda")
+    def fg(k):
+        otk.otk_sample_tokens(ctx, bufs[k % nb], greedy=True, want_logp=False, out=dict(tokens=toks))
+    for k in range(3): fg(k)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s_ = torch.cuda.Stream()
+    s_.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s_):
+        with torch.cuda.graph(g, stream=s_):
+            for k in range(a.iters): fg(k)
+    torch.cuda.synchronize()
+    g.replay(); torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record(); g.replay(); ev[1].record(); torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / a.iters
+    by = n * (2 * V + 4)
+    res["greedy_nologp"] = dict(us=round(ms * 1e3, 1), GBps=round(by / ms / 1e6, 1), frac=round(by / ms / 1e6 / peak, 4))
     print(json.dumps(dict(rows=n, bufs=nb, **res)), flush=True)
     del bufs
 ctx.check()

@@ -152,3 +152,21 @@ def test_temperature_argument(otk, ctx):
     assert torch.equal(a, b)
     g = otk.otk_sample_tokens(ctx, lg, u, temperature=1e-7)["tokens"]
     assert torch.equal(g, otk.otk_sample_tokens(ctx, lg, greedy=True)["tokens"])
+
+
+def test_greedy_without_logp_same_tokens(otk, ctx):
+    """Greedy with logp not requested skips the exponentials: the same tokens (ties, -inf rows, degenerate rows)."""
+    n, V = 700, 151936
+    logits, _ = make_logits(n, V, dtype="bf16", seed=8, device="cpu")
+    x = logits.clone()
+    x[2, 77] = x[2, 150001] = x[2].max() + 1.0
+    x[4, :] = float("-inf")
+    x[5, 0:100] = float("-inf")
+    xc = x.cuda()
+    a = otk.otk_sample_tokens(ctx, xc, greedy=True)
+    b = otk.otk_sample_tokens(ctx, xc, greedy=True, want_logp=False)
+    c = otk.otk_sample_tokens(ctx, xc[:40].contiguous(), greedy=True, want_logp=False)   # cluster-split rows
+    ctx.check()
+    assert "logp" not in b
+    assert torch.equal(a["tokens"], b["tokens"]) and torch.equal(a["tokens"][:40], c["tokens"])
+    assert int(b["tokens"][4]) == 0 and int(b["tokens"][2]) == 77
