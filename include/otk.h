@@ -281,13 +281,18 @@ otk_status otk_policy_loss_fwd_bwd_partials(otk_ctx* ctx, int64_t num_rows, int6
 /* ---------------------------------------------------------------------------------------------
  * (4) on a vocab shard with the exchange fused into the kernel (K4-VPF; SURVEY.md §8(e) VOCAB row,
  * DESIGN.md §7). Same result as otk_row_partials -> all-gather -> otk_policy_loss_fwd_bwd_partials
- * (logp / entropy / loss stats bitwise equal; dlogits within the bf16 tolerance of (4)), but in ONE launch
+ * (logp / entropy bitwise equal; loss stats up to fp64 summation order; dlogits within the bf16 tolerance of
+ * (4)), but in ONE launch
  * per rank and ONE read of the shard: after pass 1 of a row, the CTA pushes the row's 16-byte partial
  * (m2, s, t2, w — the otk_row_partials form) into every peer's exchange buffer over NVLink (P2P stores of
  * four 64-bit words, each = value | call epoch << 32, so every word validates itself and no memory fence
  * is needed), waits until the peers' words of the same row carry this call's epoch,
  * combines them in rank order (identical on every rank) and runs pass 2 from the tensor-memory-resident
  * exponentials. The all-reduce of row max / sum-exp the north_star names is this exchange.
+ * logits / dlogits: this rank's column shard [num_rows, vocab_local] with row stride ld (e.g. a column slice of
+ * a wider row buffer); every other argument as in otk_policy_loss_fwd_bwd_partials (targets global).
+ *   rank, nranks: this rank's index in rank order (= shard order) and the number of ranks (<= 8).
+ *   rows_cap  : the row capacity the exchange buffers were sized for (the same value on every call on them).
  *   xchg[q]   : device pointer, valid in THIS process, to rank q's exchange buffer (xchg[rank] = own
  *               buffer; peers' buffers mapped with otk_ipc_open, or plain buffers of the same device when
  *               several ranks share one GPU), each otk_vpf_xchg_bytes(rows_cap, nranks) bytes, 16-byte
@@ -298,7 +303,9 @@ otk_status otk_policy_loss_fwd_bwd_partials(otk_ctx* ctx, int64_t num_rows, int6
  *   max_ctas  : 0 = one CTA per SM; otherwise at most this many CTAs (lets several ranks share a GPU).
  * Every rank must make the same sequence of calls with the same num_rows / masks / targets; a partial that
  * does not arrive within ~20 s sets OTK_ERR_PEER_TIMEOUT (sticky; later waits give up at once) instead of
- * hanging. Requires nranks <= OTK_VPF_MAX_RANKS and num_rows <= rows_cap.
+ * hanging. Host-checked (nothing launched): ctx / shard / peers / required arrays NULL, rank / nranks out of range,
+ * num_rows > rows_cap, an xchg pointer NULL or not 16-byte aligned, max_ctas below the cluster size, dlogits
+ * aliasing logits (OTK_ERR_INVALID_ARG / OTK_ERR_SHAPE / OTK_ERR_ALIGNMENT).
  * ------------------------------------------------------------------------------------------- */
 #define OTK_VPF_MAX_RANKS 8
 typedef struct {
