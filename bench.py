@@ -394,22 +394,11 @@ def other_kernels(W, step, cfg):
             ctx, bufs[i % len(bufs)][(i * n) % (M - n):(i * n) % (M - n) + n], u, greedy=mode == "greedy"), 8)
         gbs = n * (2 * V + 12) / ms / 1e6
         out[f"sample_tokens_{mode}"] = {"rows": n, "us": ms * 1e3, "GBps": gbs, "frac_hbm": gbs / hbm,
-                                        "kernel": "k_sample (SURVEY.md §8(f) NEXT-3)"}
-    from synth import make_lmhead
-    rows, d = 8192, 3584
-    h, w, y = make_lmhead(rows, V, d, seed=1, device=bufs[0].device)
-    ws = [None]
-
-    def lm(i):
-        o = otk.otk_lmhead_logprob_fwd(ctx, h, w, y, workspace=ws[0])
-        ws[0] = o["workspace"]
-    ms = timed(lm, 3)
-    tf = 2.0 * rows * V * d / ms / 1e9
-    out["lmhead_logprob_fwd"] = {"rows": rows, "hidden_dim": d, "ms": ms, "TFLOPs": tf, "frac_bf16": tf / bf16_peak,
-                                 "kernel": "k_lmhead_fwd (tcgen05 cta_group::2; SURVEY.md §8(f) NEXT-1 fwd)"}
-    del h, w, y, ws
+                                        "kernel": ("k_sample" if mode == "greedy" else "k_sample_tm")
+                                        + " (SURVEY.md §8(f) NEXT-3)"}
     # K4-VPF (vocab-sharded loss, exchange in-kernel): P = 2 ranks co-scheduled on this GPU (own ctx, stream,
-    # column shard, 74 CTAs each) on micro-batch 0, against the unsharded loss on the same rows
+    # column shard, 74 CTAs each) on micro-batch 0, against the unsharded loss on the same rows (measured before
+    # the tensor-core benchmark below, whose power draw would slow whichever runs after it)
     mb = W["mbs"][0]
     lm, rt = step.masks["loss_mask"][mb.r0:mb.r1], step.masks["row_traj"][mb.r0:mb.r1]
     adv, nl = step.adv_out["adv"], step.masks["n_loss"]
@@ -438,6 +427,19 @@ def other_kernels(W, step, cfg):
         x.close()
     out["vocab_shard_vpf_p2_one_gpu"] = {"rows": M, "ms": ms_v, "ms_unsharded": ms_u, "vs_unsharded": ms_u / ms_v,
                                          "kernel": "k_rows_tm<bf16,BWD_VPF> x 2 ranks co-scheduled (DESIGN.md §7)"}
+    from synth import make_lmhead
+    rows, d = 8192, 3584
+    h, w, y = make_lmhead(rows, V, d, seed=1, device=bufs[0].device)
+    ws = [None]
+
+    def lm(i):
+        o = otk.otk_lmhead_logprob_fwd(ctx, h, w, y, workspace=ws[0])
+        ws[0] = o["workspace"]
+    ms = timed(lm, 3)
+    tf = 2.0 * rows * V * d / ms / 1e9
+    out["lmhead_logprob_fwd"] = {"rows": rows, "hidden_dim": d, "ms": ms, "TFLOPs": tf, "frac_bf16": tf / bf16_peak,
+                                 "kernel": "k_lmhead_fwd (tcgen05 cta_group::2; SURVEY.md §8(f) NEXT-1 fwd)"}
+    del h, w, y, ws
     ctx.check()
     return out
 
