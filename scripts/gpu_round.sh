@@ -16,3 +16,8 @@ tail -1 gpurun_out/smoke.log; tail -2 gpurun_out/gpu_tests.log; tail -1 gpurun_o
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_lmhead -s 2 -c 1 -o gpurun_out/prof_lmhead -f python scripts/prof_lmhead.py 8192 > gpurun_out/ncu_lmhead.log 2>&1; echo "lmhead rc=$?"
 for n in 4096 8192 16384; do timeout 60 python scripts/perf_lmhead.py --rows $n --iters 5 2>&1 | tail -1; done > gpurun_out/perf_lmhead.jsonl
 for v in "" ent dual seqmean seqsum sft turn; do timeout 120 python scripts/perf_k4.py --variant "$v" 2>&1 | tail -1; done > gpurun_out/perf_variants.jsonl
+# round-1 additions: K4-VPF (emulated ranks), the loss through the LM head, the traffic-structure probe
+timeout 300 python scripts/perf_vpf.py --ranks 2 4 8 > gpurun_out/perf_vpf.jsonl 2>&1; echo "perf_vpf rc=$?"
+timeout 300 python scripts/vpf_isolation.py > gpurun_out/vpf_isolation.jsonl 2>&1; echo "vpf_isolation rc=$?"
+for n in 4096 8192; do timeout 200 python scripts/perf_lmhead_loss.py --rows $n 2>&1 | tail -1; done > gpurun_out/perf_lmhead_loss.jsonl
+timeout 300 python scripts/hbm_probe3.py > gpurun_out/hbm_probe3.json 2>&1; echo "hbm_probe3 rc=$?"

@@ -95,6 +95,8 @@ if __name__ == "__main__":
     import shutil
     for src, dst in (("perf_sample.jsonl", "perf_sample.jsonl"), ("perf_lmhead.jsonl", "perf_lmhead.jsonl"),
                      ("perf_variants.jsonl", "perf_variants.jsonl"), ("perf_vpf.jsonl", "perf_vpf.jsonl"),
+                     ("vpf_isolation.jsonl", "vpf_isolation.jsonl"), ("perf_lmhead_loss.jsonl", "perf_lmhead_loss.jsonl"),
+                     ("hbm_probe3.json", "hbm_probe3.json"),
                      ("sanitize_memcheck.log", "sanitize_memcheck.txt"),
                      ("sanitize_racecheck.log", "sanitize_racecheck.txt"),
                      ("sanitize_synccheck.log", "sanitize_synccheck.txt")):
