@@ -1,19 +1,24 @@
 // k_rows.cu — the fused vocab-row kernels behind otk_logprob_entropy_fwd (north_star (3)),
 // otk_policy_loss_fwd_bwd (north_star (4)) and the vocab-sharded variants.
 //
-// k_rows_tm (modes FWD / PARTIAL / BWD): one persistent CTA per SM; a row is split over a
-// thread-block cluster of `csize` CTAs (csize = 2 for bf16 V = 151936: 148 KB per CTA).
-//   warp 0, lane 0 : producer — 1-D bulk TMA (cp.async.bulk) of 8 KB chunks into a 27-slot (216 KB)
-//                    shared-memory ring, L2 evict_first, paced by per-slot empty mbarriers.
-//   warps 1..8     : consumers — read each chunk from the ring once and release the slot at once, so
-//                    the ring streams the next row while this one is computed. Pass 1: online max
-//                    (packed bf16 max) and 2^(y - m) once per element (MUFU), sums in 4 independent
-//                    fp32 chains; for the loss (BWD) e = 2^(y - m_c) is parked in TENSOR MEMORY (f16 for
-//                    bf16 input; 152 of a warp's 256 TMEM columns), with the chunk's reference max m_c.
-//                    Warp shuffle + CTA combine + cluster exchange of 16-byte partials through DSMEM
-//                    (st.async + mbarrier). Loss terms in fp64 by one thread. Pass 2: softmax =
-//                    e * 2^(m_c - lse): one FMUL per element (no second read of the logits, no second
-//                    exponential), dlogits = coef * (softmax - onehot), 16-byte streaming stores.
+// k_rows_tm (modes FWD / PARTIAL / BWD / BWD_VPF): persistent CTAs (BWD: one per SM; FWD / PARTIAL: two per
+// SM); a row is split over a thread-block cluster of `csize` CTAs (any size 1-8, the fewest whose segment fits
+// kMaxChunks chunks; csize = 2 for bf16 V = 151936: 148 KB per CTA), the grid capped at the resident clusters.
+//   warp 0, lane 0 : loader — 1-D bulk TMA (cp.async.bulk) of 12 KB chunks of every active row's segment into
+//                    an 18-slot (216 KB; FWD / PARTIAL: 8-slot) shared-memory ring, L2 evict_first, paced by
+//                    per-slot empty mbarriers. Loss-masked rows are never read.
+//   warps 1..12    : consumers — read each chunk from the ring once (two 16-byte vectors per thread) and
+//                    release the slot at once. Pass 1 (pass1_chunk): 2^(y - m) once per element (MUFU) with
+//                    packed fp32x2 sums against a per-thread reference m set by the row's first chunk and
+//                    raised only when a chunk's sums overflow; for the loss (BWD) e (bf16) and the chunk's
+//                    reference m_c are parked in TENSOR MEMORY (9 columns per chunk in a 168-column window).
+//                    Row total: warp shuffles + lane-parallel CTA combine + cluster exchange of 16-byte
+//                    partials through DSMEM (st.async + mbarrier); K4-VPF adds the exchange with the other
+//                    ranks over peer memory (epoch-tagged words). Pass 2 (pass2_row): softmax = e * 2^(m_c -
+//                    lse) from tensor memory (no second read of the logits, no second exponential),
+//                    dlogits = coef * (softmax - onehot) as bf16x2 products, 16-byte streaming stores.
+//   warp 13        : BWD: zero-fills the dlogits of masked rows with bulk async stores; FWD / PARTIAL: the
+//                    finalizer (row reduction, exchange and outputs off the consumers' critical path).
 // k_rows_stream (mode BWD_PARTIALS, vocab shard): stats come from the all-gathered partials, so the
 //   row is streamed once through the ring and written (one exponential per element).
 // Rows with loss mask 0 are never read: their dlogits are zero-filled (write-only).
