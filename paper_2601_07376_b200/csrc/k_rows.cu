@@ -225,9 +225,6 @@ struct Vec<float> {
   __device__ static __forceinline__ uint4 pack(const float (&g)[4]) {
     return make_uint4(__float_as_uint(g[0]), __float_as_uint(g[1]), __float_as_uint(g[2]), __float_as_uint(g[3]));
   }
-  // e values are kept at full precision for fp32 inputs
-  __device__ static __forceinline__ uint4 pack_e(const float (&e)[4]) { return pack(e); }
-  __device__ static __forceinline__ void unpack_e(const uint4 v, float (&e)[4]) { unpack(v, e); }
   // lanes >= nvalid become -1e30 (finite: e = 0 and e*d = 0, no NaN in the fast path)
   __device__ static __forceinline__ uint4 mask_tail(uint4 v, int nvalid) {
     constexpr uint32_t kLow = 0xf149f2cau;  // -1.0e30f
@@ -287,26 +284,6 @@ struct Vec<__nv_bfloat16> {
   __device__ static __forceinline__ uint4 pack(const float (&g)[8]) {
     return make_uint4(pack_bf16x2(g[0], g[1]), pack_bf16x2(g[2], g[3]), pack_bf16x2(g[4], g[5]),
                       pack_bf16x2(g[6], g[7]));
-  }
-  // e = 2^(y - m) in [0, 1] is kept as f16 (11-bit significand; DESIGN.md §6 error budget)
-  __device__ static __forceinline__ uint32_t h2(float lo, float hi) {
-    uint32_t r;
-    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-    return r;
-  }
-  __device__ static __forceinline__ void h2f(uint32_t w, float& lo, float& hi) {
-    asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
-        : "=f"(lo), "=f"(hi)
-        : "r"(w));
-  }
-  __device__ static __forceinline__ uint4 pack_e(const float (&e)[8]) {
-    return make_uint4(h2(e[0], e[1]), h2(e[2], e[3]), h2(e[4], e[5]), h2(e[6], e[7]));
-  }
-  __device__ static __forceinline__ void unpack_e(const uint4 v, float (&e)[8]) {
-    h2f(v.x, e[0], e[1]);
-    h2f(v.y, e[2], e[3]);
-    h2f(v.z, e[4], e[5]);
-    h2f(v.w, e[6], e[7]);
   }
   // lanes >= nvalid become -1e30 (bf16 0xf14a: finite, so e = 0 and e*d = 0 without NaN)
   __device__ static __forceinline__ uint32_t mask_word(uint32_t w, int lane0, int nvalid) {
