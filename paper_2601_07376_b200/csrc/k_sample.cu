@@ -111,8 +111,8 @@ __device__ __forceinline__ float ld_cluster_f32(uint32_t addr) {
 
 constexpr float kNoRef = -1e30f;  // reference before the first finite logit (logits <= -1e30 carry no mass)
 
-template <typename T, bool kCl>
-__global__ void __launch_bounds__(kSampleThreads, OTK_SAMPLE_MINB) k_sample(const SampleParams p) {
+template <typename T, bool kCl, int kMinB = OTK_SAMPLE_MINB>
+__global__ void __launch_bounds__(kSampleThreads, kMinB) k_sample(const SampleParams p) {
   using SV = SVec<T>;
   constexpr int EV = SV::EV;
 #ifndef OTK_SAMPLE_U
@@ -427,31 +427,22 @@ __global__ void __launch_bounds__(kSampleThreads, OTK_SAMPLE_MINB) k_sample(cons
   if (kCl) cluster_sync_all();  // no CTA exits while a peer may still read its s_cta
 }
 
-// resident CTAs per SM of the clustered variant (the launch shape depends on it); cached in the ctx
-int sample_occupancy(otk_ctx* ctx, int dtype) {
-  int& o = ctx->sample_occ[dtype == OTK_BF16 ? 0 : 1];
+// resident CTAs per SM of the clustered variant (the launch shape depends on it); cached in the ctx per (dtype,
+// register budget)
+template <typename T, int kMinB>
+int sample_occupancy(otk_ctx* ctx, int slot) {
+  int& o = ctx->sample_occ[slot];
   if (o == 0) {
     int a = 0;
-    if (dtype == OTK_BF16)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_sample<__nv_bfloat16, true>, kSampleThreads, 0);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_sample<float, true>, kSampleThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_sample<T, true, kMinB>, kSampleThreads, 0);
     o = std::max(a, 1);
   }
   return o;
 }
 
-cudaError_t launch_sample(otk_ctx* ctx, const SampleParams& p0, int dtype, cudaStream_t s) {
-#ifndef OTK_SAMPLE_V1
-  // sampled draws from one SM's worth of rows up: the ring-streamed kernel, one CTA per row, with an off-path
-  // search warp (k_sample_tm.cu; 256 rows 22.9 vs 25.1 us, 4096 rows 218 vs 262 us). Smaller batches keep the
-  // cluster-split kernel below (a cluster-split version of the ring kernel measured no faster at 16-128 rows);
-  // greedy stays here at every size (its lane-strided pass measured faster: 225 vs 272 us at 4096 rows).
-  if (!p0.greedy && p0.num_rows >= ctx->num_sms && sample_tm_fits(p0.vocab, dtype))
-    return launch_sample_tm(ctx, p0, dtype, s);
-#endif
-  SampleParams p = p0;
-  const int64_t slots = int64_t(ctx->num_sms) * sample_occupancy(ctx, dtype);
+template <typename T, int kMinB>
+static cudaError_t launch_lane_strided(otk_ctx* ctx, SampleParams p, cudaStream_t s, int occ_slot) {
+  const int64_t slots = int64_t(ctx->num_sms) * sample_occupancy<T, kMinB>(ctx, occ_slot);
   // cluster size: when rows are few, as many CTAs per row as fit in ONE wave of resident CTAs; one CTA
   // per row otherwise (a cluster barrier per row costs more than the last wave's imbalance)
   const int best_c = int(std::min<int64_t>(kSampleMaxCluster, std::max<int64_t>(1, slots / p.num_rows)));
@@ -471,11 +462,27 @@ cudaError_t launch_sample(otk_ctx* ctx, const SampleParams& p0, int dtype, cudaS
   cfg.numAttrs = 1;
   if (best_c == 1) {
     cfg.numAttrs = 0;
-    return dtype == OTK_BF16 ? cudaLaunchKernelEx(&cfg, k_sample<__nv_bfloat16, false>, p)
-                             : cudaLaunchKernelEx(&cfg, k_sample<float, false>, p);
+    return cudaLaunchKernelEx(&cfg, k_sample<T, false, kMinB>, p);
   }
-  return dtype == OTK_BF16 ? cudaLaunchKernelEx(&cfg, k_sample<__nv_bfloat16, true>, p)
-                           : cudaLaunchKernelEx(&cfg, k_sample<float, true>, p);
+  return cudaLaunchKernelEx(&cfg, k_sample<T, true, kMinB>, p);
+}
+
+cudaError_t launch_sample(otk_ctx* ctx, const SampleParams& p0, int dtype, cudaStream_t s) {
+#ifndef OTK_SAMPLE_V1
+  // sampled draws from one SM's worth of rows up: the ring-streamed kernel, one CTA per row, with an off-path
+  // search warp (k_sample_tm.cu; 256 rows 22.9 vs 25.1 us, 4096 rows 218 vs 262 us). Smaller batches keep the
+  // cluster-split kernel below (a cluster-split version of the ring kernel measured no faster at 16-128 rows);
+  // greedy stays here at every size (its lane-strided pass measured faster: 225 vs 272 us at 4096 rows).
+  if (!p0.greedy && p0.num_rows >= ctx->num_sms && sample_tm_fits(p0.vocab, dtype))
+    return launch_sample_tm(ctx, p0, dtype, s);
+#endif
+  // lane-strided kernel; at <= 64 rows with twice the registers per thread (2 resident CTAs per SM: 16 rows
+  // 8.4 vs 9.5 us, 64 rows 12.2 vs 13.9 us; slower from 128 rows, profiles/r01_sample_tuning_sweep_graph.txt)
+  const bool bf = dtype == OTK_BF16;
+  if (p0.num_rows <= 64)
+    return bf ? launch_lane_strided<__nv_bfloat16, 2>(ctx, p0, s, 2) : launch_lane_strided<float, 2>(ctx, p0, s, 3);
+  return bf ? launch_lane_strided<__nv_bfloat16, OTK_SAMPLE_MINB>(ctx, p0, s, 0)
+            : launch_lane_strided<float, OTK_SAMPLE_MINB>(ctx, p0, s, 1);
 }
 
 }  // namespace otk

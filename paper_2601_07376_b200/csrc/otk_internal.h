@@ -23,7 +23,7 @@ struct otk_ctx {
   cudaStream_t exec_stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t launches = 0;
-  int sample_occ[2] = {0, 0};      // k_sample resident CTAs per SM (bf16, fp32), queried on first use
+  int sample_occ[4] = {0, 0, 0, 0};  // k_sample resident CTAs per SM (bf16, fp32; x2 register budgets), on first use
 };
 
 namespace otk {
