@@ -260,3 +260,47 @@ def test_open_vpf_exchange_host_logic_gloo():
         assert r["ptrs"][k] == 0x10000 * (k + 1)                                   # own buffer, unmapped
         assert r["opened"] == [0x10000 * (j + 1) for j in range(world) if j != k]  # peers, rank order
         assert all(r["ptrs"][j] == 0x7000000 + 0x10000 * (j + 1) for j in range(world) if j != k)
+
+
+def _worker_layout(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import argparse
+        import importlib.util
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+        bench = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(bench)
+        out = {}
+        for shard in ("batch", "vocab", "2d"):
+            L = bench.shard_layout(argparse.Namespace(shard=shard, vocab_ways=2), world, rank)
+            t = torch.tensor([float(rank)])
+            if L["vg"] is not None:
+                dist.all_reduce(t, group=L["vg"])
+            out[shard] = (L["Pv"], L["nb"], L["b"], L["v"], float(t.item()))
+        q.put(dict(rank=rank, out=out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_shard_layout_gloo():
+    """bench.py's rank layout for --shard batch / vocab / 2d (world 4, 2 vocab ways): shard counts, this rank's
+    (batch, vocab) index and the vocab group's membership."""
+    world = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_layout, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda d: d["rank"])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in res:
+        k = r["rank"]
+        assert r["out"]["batch"][:4] == (1, 4, k, 0)
+        assert r["out"]["vocab"][:4] == (4, 1, 0, k) and r["out"]["vocab"][4] == 0 + 1 + 2 + 3
+        b, v = divmod(k, 2)
+        assert r["out"]["2d"][:4] == (2, 2, b, v) and r["out"]["2d"][4] == 2 * b + (2 * b + 1)
