@@ -170,3 +170,39 @@ def test_greedy_without_logp_same_tokens(otk, ctx):
     assert "logp" not in b
     assert torch.equal(a["tokens"], b["tokens"]) and torch.equal(a["tokens"][:40], c["tokens"])
     assert int(b["tokens"][4]) == 0 and int(b["tokens"][2]) == 77
+
+
+@pytest.mark.parametrize("dtype,V", [("bf16", 151936), ("f32", 50000), ("bf16", 4100)])
+def test_sampled_degenerate_rows_ring_kernel(otk, ctx, dtype, V):
+    """>= 148 rows (the ring kernel): all -inf rows give token 0 / logp -inf; a single finite column is always
+    drawn (first, last, and a middle column, for u = 0 and u -> 1); rows with huge logit ranges (overflow path)."""
+    n = 200
+    ld = -(-V // 8) * 8                                  # 16-byte rows
+    logits, _ = make_logits(n, V, ld=ld if ld != V else None, dtype=dtype, seed=V % 101, device="cpu")
+    x = logits.clone()[:, :V]
+    x[0, :] = float("-inf")
+    for j, col in ((1, 0), (2, V - 1), (3, V // 2), (4, 0), (5, V - 1)):
+        x[j, :] = float("-inf")
+        x[j, col] = 3.0
+    x[6, : V // 2] = -80.0          # a large step inside the row: the warp reference is raised on overflow
+    x[6, V // 2:] = 60.0
+    x[7, :] = -200.0                 # all far below 0
+    x[7, V - 3] = 150.0
+    u = torch.rand(n, generator=torch.Generator().manual_seed(4)).float()
+    u[1:4] = 0.0
+    u[4:6] = 1.0 - 2 ** -24
+    xp = torch.full((n, ld), float("nan"), dtype=x.dtype)   # padding columns never read
+    xp[:, :V] = x
+    out = otk.otk_sample_tokens(ctx, xp.cuda(), u.cuda(), vocab=V)
+    ctx.check()
+    tok = out["tokens"].cpu().numpy()
+    lp = out["logp"].cpu().numpy()
+    assert tok[0] == 0 and lp[0] == float("-inf")
+    assert [int(t) for t in tok[1:6]] == [0, V - 1, V // 2, 0, V - 1]
+    assert np.allclose(lp[1:6], 0.0, atol=1e-6)
+    assert V // 2 <= tok[6] < V                   # all the mass sits in the upper half
+    assert tok[7] == V - 3
+    wide = x.double().numpy()
+    rows = list(range(8, n, 7))
+    exact = _check_sampled(tok, lp, wide, u.double().numpy(), 1.0, dtype, rows)
+    assert exact >= 0.9 * len(rows)
