@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-parity", action="store_true", help="skip the parity block (SURVEY.md §8(d)(v))")
     ap.add_argument("--no-next", action="store_true",
                     help="skip the side measurements of the forward (3) and the SURVEY.md §8(f) rows")
     ap.add_argument("--vocab-ways", type=int, default=2,
@@ -343,7 +344,9 @@ def run_otk(args):
     if not args.no_e2e and not vocab_mode:
         res["e2e"] = e2e(args, W, world, step, cfg)
     if rank == 0 and not args.no_cpu_baseline and not vocab_mode:
-        res["cpu_baseline"] = cpu_baseline(args, W, cfg)
+        res["cpu_baseline"], inp = cpu_baseline(args, W, cfg)
+        if not args.no_parity:
+            res["parity"] = parity_block(W, step, cfg, inp)
     if rank == 0 and world == 1 and not args.no_next and not vocab_mode:
         try:
             res["other_kernels"] = other_kernels(W, step, cfg)
@@ -446,13 +449,19 @@ def other_kernels(W, step, cfg):
 
 def e2e(args, W, world, step, cfg):
     """Same metric through the C-ABI host-buffer entry point (otk_policy_loss_fwd_bwd_host): every
-    micro-batch's trainable logits rows + side arrays are copied H2D from pinned host memory inside the timed region
-    (pipelined in 4096-row chunks on a copy stream), and the loss statistics come back D2H. The step's
-    masks / advantages (device outputs of (1)-(2)) are inputs of this call and are staged once."""
+    micro-batch's trainable logits rows + side arrays are copied H2D from pinned host memory inside the timed
+    region (pipelined in 4096-row chunks on a copy stream), and the step's result comes back D2H: the gradient
+    rows of every trainable token (cudaMemcpy2DAsync of [0, V) per run of trainable rows, on the execution
+    stream, overlapping the next chunk's H2D) plus the loss statistics. Masked rows' gradient is zero by
+    definition (loss_mask is on the host), so with zero_masked_rows = 0 it neither crosses PCIe nor is
+    zero-filled on the device. The step's masks / advantages (device outputs of (1)-(2)) are inputs of this
+    call and are staged once."""
+    import dataclasses
     otk, ctx = W["otk"], W["ctx"]
     mbs = W["mbs"]
     N = W["N"]
     host_bufs = [b.cpu().pin_memory() for b in W["bufs"]]
+    dl_host = torch.empty(W["bufs"][0].shape, dtype=W["bufs"][0].dtype).pin_memory()   # one micro-batch
     adv = step.masks_and_advantages()
     torch.cuda.synchronize()
     n_loss = int(step.masks["n_loss"].item())
@@ -462,14 +471,16 @@ def e2e(args, W, world, step, cfg):
     side = [(mb.targets.cpu().pin_memory(), mb.old_logp.cpu().pin_memory(),
              None if mb.ref_logp is None else mb.ref_logp.cpu().pin_memory()) for mb in mbs]
     nb = len(host_bufs)
+    hcfg = dataclasses.replace(cfg, zero_masked_rows=False)
 
     def one_step():
         tot = 0.0
         for i, mb in enumerate(mbs):
             tg, old, ref = side[i]
-            s = otk.otk_policy_loss_fwd_bwd_host(ctx, host_bufs[i % nb][:mb.r1 - mb.r0], tg, lm_h[mb.r0:mb.r1],
-                                                 rt_h[mb.r0:mb.r1], adv_h, old, ref, n_loss, cfg,
-                                                 rows_per_chunk=4096)
+            n = mb.r1 - mb.r0
+            s = otk.otk_policy_loss_fwd_bwd_host(ctx, host_bufs[i % nb][:n], tg, lm_h[mb.r0:mb.r1],
+                                                 rt_h[mb.r0:mb.r1], adv_h, old, ref, n_loss, hcfg,
+                                                 dlogits=dl_host[:n], rows_per_chunk=4096)
             tot += s["loss"]
         return tot
 
@@ -480,16 +491,32 @@ def e2e(args, W, world, step, cfg):
         one_step()
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / args.e2e_steps
+    # the returned gradient of the last micro-batch equals the device path's on a sampled trainable row
+    mb = mbs[-1]
+    n = mb.r1 - mb.r0
+    tr = torch.nonzero(lm_h[mb.r0:mb.r1]).flatten()
+    match = None
+    if tr.numel():
+        j = int(tr[tr.numel() // 2])
+        ref_dev = otk.otk_policy_loss_fwd_bwd(ctx, mb.logits, mb.targets, step.masks["loss_mask"][mb.r0:mb.r1],
+                                              step.masks["row_traj"][mb.r0:mb.r1], adv, mb.old_logp, mb.ref_logp,
+                                              step.masks["n_loss"], cfg, dlogits=mb.dlogits, want_logp=False)
+        torch.cuda.synchronize()
+        match = bool(torch.equal(ref_dev["dlogits"][j].cpu(), dl_host[j]))
     row_bytes = W["bufs"][0].shape[1] * W["bufs"][0].element_size()
     side_b = 4 + 1 + 4 + 4 + (4 if mbs[0].ref_logp is not None else 0)
-    # logits rows cross PCIe only when trainable (the C ABI copies the runs of loss_mask != 0 rows)
+    # logits rows cross PCIe only when trainable (the C ABI copies the runs of loss_mask != 0 rows), and so do
+    # their gradient rows on the way back
     n_train = int(lm_h.sum().item())
     h2d = n_train * row_bytes + N * side_b + len(mbs) * (adv_h.numel() * 8 + 8)
+    d2h = n_train * W["V"] * W["bufs"][0].element_size() + len(mbs) * 40
     return {"value": N * world / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": len(mbs) * 40, "steps": args.e2e_steps,
-            "h2d_GBps": h2d / dt / 1e9,
+            "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+            "h2d_GBps": h2d / dt / 1e9, "d2h_GBps": d2h / dt / 1e9,
+            "dlogits_returned_equal_device": match,
             "path": "otk_policy_loss_fwd_bwd_host (C ABI, pinned host buffers, 4096-row chunks double-buffered; "
-                    "logits of loss-masked rows are not copied)",
+                    "logits of loss-masked rows are not copied; the gradient rows of trainable tokens come back "
+                    "D2H into a pinned host buffer, masked rows' zero gradient is implied by loss_mask)",
             "clock": "host wall clock around the blocking C-ABI calls" + ("; rank 0" if world > 1 else "")}
 
 
@@ -503,12 +530,14 @@ def cpu_baseline(args, W, cfg, seconds=None):
     seconds = args.cpu_seconds if seconds is None else seconds
     tb, cfgw = W["tb"], W["cfgw"]
     mb = W["mbs"][0]
-    m = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated)
+    m = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated,
+                      traj_agent=tb.traj_agent)
     adv = O.group_advantages(tb.group_id - tb.group_id.min(), O.episode_returns(tb.turn_offsets, tb.turn_rewards),
                              cfgw.num_groups)["adv"]
     ocfg = O.LossCfg(kl_beta=cfg.kl_beta)
     threads = os.cpu_count()
     done, ntrain, t_used, r0, block = 0, 0, 0.0, 0, 64
+    olds, refs = [], []
     while t_used < seconds and r0 + block <= mb.r1 - mb.r0:
         lg = OC.bf16_bits(mb.logits[r0:r0 + block]) if cfgw.dtype == "bf16" else mb.logits[r0:r0 + block].cpu().numpy()
         tg = mb.targets[r0:r0 + block].cpu().numpy()
@@ -516,6 +545,8 @@ def cpu_baseline(args, W, cfg, seconds=None):
         old = (base + make_noise(block, 0.05, 7000 + r0).double().numpy()).astype(np.float32)
         ref = (base + make_noise(block, 0.1, 9000 + r0).double().numpy()).astype(np.float32) if cfg.kl_beta else None
         lm = m["loss_mask"][r0:r0 + block]
+        olds.append(old)
+        refs.append(ref)
         t = time.perf_counter()
         OC.policy_loss(lg, tg, lm, m["row_traj"][r0:r0 + block], adv, old, ref, m["n_loss"], ocfg)
         t_used += time.perf_counter() - t
@@ -541,10 +572,50 @@ def cpu_baseline(args, W, cfg, seconds=None):
         gomp.omp_set_num_threads(threads)
     except OSError:
         pass
-    return {"value": done / t_used, "unit": UNIT, "cores": threads, "kind": "oracle", "value_1thread": one,
-            "sample": f"first {done} rows of micro-batch 0 of the {args.config} workload ({ntrain} trainable): "
-                      f"fused loss fwd+bwd with dlogits materialised, C float64 oracle (oracle/oracle_cpu.c, "
-                      f"OpenMP {threads} threads), {t_used:.1f} s; value_1thread: the first 256 rows on one thread"}
+    res = {"value": done / t_used, "unit": UNIT, "cores": threads, "kind": "oracle", "value_1thread": one,
+           "sample": f"first {done} rows of micro-batch 0 of the {args.config} workload ({ntrain} trainable): "
+                     f"fused loss fwd+bwd with dlogits materialised, C float64 oracle (oracle/oracle_cpu.c, "
+                     f"OpenMP {threads} threads), {t_used:.1f} s; value_1thread: the first 256 rows on one thread"}
+    inputs = dict(rows=done, masks=m, adv=adv, old=np.concatenate(olds) if olds else None,
+                  ref=np.concatenate(refs) if refs and cfg.kl_beta else None, ocfg=ocfg)
+    return res, inputs
+
+
+def parity_block(W, step, cfg, inp):
+    """the CUDA path against the C float64 oracle on the cpu_baseline sample, every row
+    (oracle/parity.py; error / tolerance ratios <= 1 pass). Masks and advantages over this rank's whole batch;
+    the loss kernel (in the bench's launch configuration) re-run on the sampled rows of micro-batch 0 with the
+    oracle's masks, advantages and old / ref (= oracle logp + noise) as inputs. Untimed, after the timed region."""
+    from oracle import parity as P
+    otk, ctx, cfgw = W["otk"], W["ctx"], W["cfgw"]
+    m, n = inp["masks"], inp["rows"]
+    dev = W["bufs"][0].device
+    adv_gpu = step.adv_out["adv"].double().cpu().numpy()
+    out = {"masks_bit_exact": bool(np.array_equal(step.masks["loss_mask"].cpu().numpy(), m["loss_mask"])
+                                   and np.array_equal(step.masks["row_traj"].cpu().numpy(), m["row_traj"])
+                                   and int(step.masks["n_loss"].item()) == m["n_loss"]),
+           "adv_max_abs_err": float(np.max(np.abs(adv_gpu - inp["adv"]))),
+           "adv_tol": P.ADV_TOL}
+    out["adv_ratio"] = out["adv_max_abs_err"] / P.ADV_TOL
+    if n == 0:
+        return out
+    mb = W["mbs"][0]
+    lg, tg = mb.logits[:n], mb.targets[:n]
+    lm, rt = m["loss_mask"][:n], m["row_traj"][:n]
+    dl = W["dlogits"][:n]
+    r = otk.otk_policy_loss_fwd_bwd(ctx, lg, tg, torch.from_numpy(lm).to(dev), torch.from_numpy(rt).to(dev),
+                                    torch.from_numpy(inp["adv"]).to(dev), torch.from_numpy(inp["old"]).to(dev),
+                                    None if inp["ref"] is None else torch.from_numpy(inp["ref"]).to(dev),
+                                    torch.tensor([m["n_loss"]], dtype=torch.int64, device=dev), cfg, dlogits=dl)
+    ctx.check()
+    par = P.microbatch_parity(lg, tg, lm, rt, inp["adv"], inp["old"], inp["ref"], m["n_loss"], inp["ocfg"],
+                              cfgw.dtype, W["V"], r["logp"], r["entropy"], dl, otk.stats_dict(r["stats"]))
+    out.update(par)
+    out["tolerances"] = {"logp": P.LOGP_TOL[cfgw.dtype], "entropy": P.LOGP_TOL[cfgw.dtype],
+                         "dlogits_elem": f"{P.DL_REL[cfgw.dtype]:.4g}|ref| + dcoef|p-onehot| (+ target term)",
+                         "dlogits_l1": P.DL_L1_REL[cfgw.dtype], "loss_rel": P.LOSS_REL, "adv": P.ADV_TOL}
+    out["pass"] = bool(P.parity_ok(par) and out["masks_bit_exact"] and out["adv_ratio"] <= 1)
+    return out
 
 
 # ------------------------------------------------------------------------------------------------
@@ -562,7 +633,8 @@ def run_reference(args):
     tb = make_batch(args.config)
     V = cfgw.V
     rows = 256   # bounded per-step sample: the whole --steps/--warmup run stays within minutes
-    m = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated)
+    m = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated,
+                      traj_agent=tb.traj_agent)
     R = O.episode_returns(tb.turn_offsets, tb.turn_rewards)
     adv = O.group_advantages(tb.group_id, R, cfgw.num_groups)["adv"]
     lg, tg = make_logits(rows, V, dtype=cfgw.dtype, seed=cfgw.seed * 100, device="cpu")
@@ -573,7 +645,8 @@ def run_reference(args):
     ocfg = O.LossCfg(kl_beta=cfgw.kl_beta)
 
     def step():
-        mm = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated)
+        mm = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated,
+                           traj_agent=tb.traj_agent)
         aa = O.group_advantages(tb.group_id, O.episode_returns(tb.turn_offsets, tb.turn_rewards), cfgw.num_groups)
         OC.policy_loss(bits, tg.numpy(), mm["loss_mask"][:rows], mm["row_traj"][:rows], aa["adv"], old,
                        ref if cfgw.kl_beta else None, mm["n_loss"], ocfg)

@@ -237,9 +237,14 @@ otk_status otk_policy_loss_fwd_bwd(otk_ctx* ctx, int64_t num_rows, int64_t vocab
 /* Same computation as otk_policy_loss_fwd_bwd but every array argument is a HOST pointer (pinned
  * memory recommended): rows are streamed through ctx-owned device staging buffers in chunks, with the
  * host->device copies of chunk k+1 overlapping the kernel on chunk k. Only the logits rows with
- * loss_mask != 0 are copied (runs of consecutive rows, one copy each): a masked row is never read. dlogits_host may be NULL (the
- * gradient is then computed on the device and discarded); stats_host receives the result. Blocking:
- * returns after the stats have been copied back. Used to measure the end-to-end (e2e) metric. */
+ * loss_mask != 0 are copied (runs of consecutive rows, one copy each): a masked row is never read.
+ * dlogits_host ([num_rows, ld], same dtype) may be NULL (the gradient is then computed on the device and
+ * discarded). Otherwise columns [0, vocab) of its rows are written: every row when cfg->zero_masked_rows
+ * (masked rows get zeros), else only the trainable rows (masked rows stay untouched, and only the trainable
+ * rows' gradients cross PCIe — pre-zero the buffer once to hold the complete gradient). stats_host receives
+ * the result. Token-mean reduction only; cfg->adv_index must be NULL. Blocking: returns after the
+ * stats and dlogits have been copied back, with the first device-side data error of this call (as
+ * otk_ctx_check would report it; the sticky word is cleared). Used to measure the end-to-end (e2e) metric. */
 otk_status otk_policy_loss_fwd_bwd_host(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld,
                                         otk_dtype dtype, const void* logits_host, const int32_t* targets_host,
                                         const uint8_t* loss_mask_host, const int32_t* row_traj_host,

@@ -120,7 +120,7 @@ int orc_policy_loss(int64_t n_rows, int64_t V, int64_t ld, int32_t dtype, const 
                     const int32_t* targets, const uint8_t* loss_mask, const int32_t* row_traj,
                     const double* adv, const float* old_logp, const float* ref_logp, int64_t n_loss,
                     const orc_cfg* cfg, double* dlogits, double* logp, double* entropy,
-                    double* row_L, uint8_t* row_clipped, double* row_kl) {
+                    double* row_L, uint8_t* row_clipped, double* row_kl, double* row_lse, double* row_coef) {
   const double s = cfg->logit_scale;
   const double invN = n_loss > 0 ? 1.0 / (double)n_loss : 0.0;
   int bad = 0;
@@ -128,6 +128,8 @@ int orc_policy_loss(int64_t n_rows, int64_t V, int64_t ld, int32_t dtype, const 
   for (int64_t j = 0; j < n_rows; ++j) {
     double* dl = dlogits ? dlogits + j * V : 0;
     logp[j] = entropy[j] = row_L[j] = row_kl[j] = 0.0;
+    if (row_lse) row_lse[j] = 0.0;
+    if (row_coef) row_coef[j] = 0.0;
     row_clipped[j] = 0;
     if (!loss_mask[j]) {
       if (dl && cfg->zero_masked_rows) for (int64_t v = 0; v < V; ++v) dl[v] = 0.0;
@@ -144,8 +146,10 @@ int orc_policy_loss(int64_t n_rows, int64_t V, int64_t ld, int32_t dtype, const 
     row_L[j] = L;
     row_kl[j] = kl;
     row_clipped[j] = (uint8_t)clipped;
+    const double coef = -s * invN * G;
+    if (row_lse) row_lse[j] = lse;
+    if (row_coef) row_coef[j] = coef;
     if (dl) {
-      double coef = -s * invN * G;
       for (int64_t v = 0; v < V; ++v) {
         double p = exp(s * widen(logits, dtype, j * ld + v) - lse);
         dl[v] = coef * (p - (v == targets[j] ? 1.0 : 0.0));
@@ -185,5 +189,49 @@ int orc_build_masks(int32_t B, const int64_t* tok_offsets, const int32_t* seg_of
     total += cnt;
   }
   *n_loss = total;
+  return 0;
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * Comparison helper (test infrastructure; the tolerance policy is passed in by the caller, see
+ * oracle/parity.py). For each selected row j it re-forms the O4 gradient element by element in
+ * float64 from the row's own lse_j and coef_j (outputs of orc_policy_loss, or an alternative coef for
+ * a row on a clip / clamp kink):
+ *     p_v = exp(s x_v - lse_j),  q_v = p_v - [v == y_j],  want_v = coef_j q_v
+ * and compares it with the CUDA path's value got_v (fp32, or bf16 bits, row stride got_ld):
+ *     floor_v = dcoef_j |q_v| + [v == y_j] |coef_j| p_v logp_err
+ *     tol_v   = rel |want_v| + floor_v
+ * dcoef_j is the absolute error bound of coef_j, and the target column's extra term is the error
+ * p_y * dlogp of coef * expm1(logp). Outputs per row: max_v |got_v - want_v| / tol_v (0/0 = 0, x/0 = inf),
+ * sum |got - want|, sum |want|, sum floor. Rows with sel[j] == 0 are skipped (outputs untouched). */
+int orc_dlogits_compare(int64_t n_rows, int64_t V, int64_t ld, int32_t dtype, const void* logits,
+                        const int32_t* targets, const uint8_t* sel, double logit_scale, const double* lse,
+                        const double* coef, const double* dcoef, double logp_err, double rel,
+                        const void* got, int64_t got_ld, int32_t got_dtype,
+                        double* max_ratio, double* l1_err, double* l1_ref, double* l1_floor) {
+  const double s = logit_scale;
+#pragma omp parallel for schedule(static)
+  for (int64_t j = 0; j < n_rows; ++j) {
+    if (sel && !sel[j]) continue;
+    double worst = 0.0;
+    nsum E = {0, 0}, R = {0, 0}, F = {0, 0};
+    for (int64_t v = 0; v < V; ++v) {
+      double p = exp(s * widen(logits, dtype, j * ld + v) - lse[j]);
+      double q = p - (v == targets[j] ? 1.0 : 0.0);
+      double want = coef[j] * q;
+      double floor_v = dcoef[j] * fabs(q) + (v == targets[j] ? fabs(coef[j]) * p * logp_err : 0.0);
+      double tol = rel * fabs(want) + floor_v;
+      double d = fabs(widen(got, got_dtype, j * got_ld + v) - want);
+      double r = d == 0.0 ? 0.0 : (tol > 0.0 ? d / tol : INFINITY);
+      if (r > worst || r != r) worst = r != r ? INFINITY : r;
+      nadd(&E, d);
+      nadd(&R, fabs(want));
+      nadd(&F, floor_v);
+    }
+    max_ratio[j] = worst;
+    l1_err[j] = nget(&E);
+    l1_ref[j] = nget(&R);
+    l1_floor[j] = nget(&F);
+  }
   return 0;
 }

@@ -79,15 +79,38 @@ def policy_loss(logits: np.ndarray, targets, loss_mask, row_traj, adv, old_logp,
     old = np.ascontiguousarray(old_logp, np.float32)
     ref = None if ref_logp is None else np.ascontiguousarray(ref_logp, np.float32)
     dl = np.zeros((n, V)) if want_dlogits else None
-    logp, H, L, kl = (np.zeros(n) for _ in range(4))
+    logp, H, L, kl, lse, coef = (np.zeros(n) for _ in range(6))
     clipped = np.zeros(n, np.uint8)
     bad = lib().orc_policy_loss(C.c_int64(n), C.c_int64(V), C.c_int64(ld), C.c_int32(_dtype_code(logits)),
                                 _p(logits), _p(targets), _p(mask), _p(rt), _p(adv), _p(old), _p(ref),
                                 C.c_int64(int(n_loss)), C.byref(c), _p(dl), _p(logp), _p(H), _p(L),
-                                _p(clipped), _p(kl))
+                                _p(clipped), _p(kl), _p(lse), _p(coef))
     if bad:
         raise ValueError("target out of range")
-    return dict(dlogits=dl, logp=logp, entropy=H, row_L=L, row_clipped=clipped, row_kl=kl)
+    return dict(dlogits=dl, logp=logp, entropy=H, row_L=L, row_clipped=clipped, row_kl=kl, row_lse=lse,
+                row_coef=coef)
+
+
+def dlogits_compare(logits: np.ndarray, targets, sel, logit_scale, lse, coef, dcoef, logp_err, rel, got,
+                    V=None):
+    """Element-by-element comparison of a CUDA-path dlogits block (`got`: float32 or bf16 bits, [n, >= V])
+    with the O4 gradient re-formed in float64 from the oracle's per-row lse / coef (orc_dlogits_compare;
+    the tolerance terms come from oracle/parity.py)."""
+    logits = np.ascontiguousarray(logits)
+    got = np.ascontiguousarray(got)
+    n, ld = logits.shape
+    V = ld if V is None else V
+    targets = np.ascontiguousarray(targets, np.int32)
+    sel = None if sel is None else np.ascontiguousarray(sel, np.uint8)
+    lse = np.ascontiguousarray(lse, np.float64)
+    coef = np.ascontiguousarray(coef, np.float64)
+    dcoef = np.ascontiguousarray(dcoef, np.float64)
+    out = [np.zeros(n) for _ in range(4)]
+    lib().orc_dlogits_compare(C.c_int64(n), C.c_int64(V), C.c_int64(ld), C.c_int32(_dtype_code(logits)),
+                              _p(logits), _p(targets), _p(sel), C.c_double(logit_scale), _p(lse), _p(coef), _p(dcoef),
+                              C.c_double(logp_err), C.c_double(rel), _p(got), C.c_int64(got.shape[1]),
+                              C.c_int32(_dtype_code(got)), _p(out[0]), _p(out[1]), _p(out[2]), _p(out[3]))
+    return dict(max_ratio=out[0], l1_err=out[1], l1_ref=out[2], l1_floor=out[3])
 
 
 def build_masks(tb, train_agent=-1):

@@ -1,0 +1,228 @@
+"""Comparison of CUDA-path outputs with the float64 oracle — TEST INFRASTRUCTURE.
+
+Only tests/ and bench.py's cpu_baseline / parity leg use this module. It imports the oracle (oracle_ref,
+oracle_cpu) and nothing from the CUDA path: the CUDA path's outputs come in as plain tensors / arrays.
+
+Tolerances (BASELINE.json north_star; DESIGN.md §6 "Error budget"):
+  masks, row_traj, token counts, group sizes ........ bit-exact
+  advantages ........................................ 1e-6 abs
+  logp, entropy ..................................... 2e-3 abs for bf16 logits, 1e-5 for fp32
+  loss .............................................. 1e-4 x max(|loss|, sum_j w_j |L_j|)   (R22)
+  dlogits, per element (row j, column v; q_v = p_v - [v = y_j], the oracle's coef_j and p_v):
+      |got - want| <= rel |want| + dcoef_j |q_v| + [v = y_j] |coef_j| p_y LOGP_ERR
+      rel = 2^-7 (bf16 output: e and the product are each rounded once, <= 2^-8 each) or 1e-5 (fp32);
+      dcoef_j = COEF_REL |coef_j| + LOGP_ERR s w_j |dG/dlogp| is the absolute error coef_j inherits from the
+      fp32 logp (coef = -s w G(logp), and G's PPO / KL parts can cancel); the target column carries
+      coef * p_y * dlogp from expm1(logp). Both floors scale with the element's own |p_v - onehot|, so a
+      tiny-probability element is checked relative to itself, never against a row-wide floor.
+  dlogits, per row (L1): sum_v |got - want| <= L1_REL sum_v |want| + sum_v floor_v, L1_REL = 2^-8 (bf16; the
+      mean of two round-to-nearest errors is well below the per-element 2^-7 worst case) or 1e-5 (fp32).
+  Rows within KINK_EPS of a clip / ratio-clamp / KL-clamp / dual-clip boundary accept either branch's
+  coefficient (the fp32 and the float64 logp can fall on different sides); both are checked in full.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from oracle import oracle_ref as O
+
+LOGP_TOL = {"bf16": 2e-3, "f32": 1e-5}
+ADV_TOL = 1e-6
+LOSS_REL = 1e-4
+DL_REL = {"bf16": 2.0 ** -7, "f32": 1e-5}
+DL_L1_REL = {"bf16": 2.0 ** -8, "f32": 1e-5}
+COEF_REL = 1e-5
+LOGP_ERR = 1e-5
+KINK_EPS = 1e-4
+
+
+def _arr(x):
+    return np.asarray(x, np.float64)
+
+
+def g_sensitivity(logp, old, ref, A, cfg):
+    """|dG/dlogp| (vectorised): G = dL/dlogp = -A r (unclipped PPO part) + beta * Gk; dG/dlogp = -A r +
+    beta * (k3: e^d, k2: 1, k1: 0). Bounded from above on both branches (used for an error bound only)."""
+    logp, old, A = _arr(logp), _arr(old), _arr(A)
+    C = cfg.log_ratio_clamp
+    out = np.zeros_like(logp)
+    if not getattr(cfg, "sft", False):
+        out += np.abs(A) * np.exp(np.clip(logp - old, -C, C))
+    if cfg.kl_beta:
+        if cfg.kl_type == O.KL_K3:
+            out += cfg.kl_beta * np.exp(np.clip(_arr(ref) - logp, -C, C))
+        elif cfg.kl_type == O.KL_K2:
+            out += cfg.kl_beta
+    return out
+
+
+def coef_error(coef, logp, old, ref, A, w, cfg):
+    """Absolute error bound of coef_j = -s w_j G_j(logp_j) given a LOGP_ERR error in the fp32 logp."""
+    return COEF_REL * np.abs(_arr(coef)) + LOGP_ERR * abs(cfg.logit_scale) * np.abs(_arr(w)) * \
+        g_sensitivity(logp, old, ref, A, cfg)
+
+
+def near_kink(logp, old, ref, A, cfg, eps=KINK_EPS):
+    """Scalar: is the row's clip / clamp decision within eps of a boundary (either branch correct)?"""
+    C = cfg.log_ratio_clamp
+    r = math.exp(max(min(logp - old, C), -C))
+    k = (abs(abs(logp - old) - C) < eps
+         or (not getattr(cfg, "sft", False) and (abs(r - (1 + cfg.clip_high)) < eps or abs(r - (1 - cfg.clip_low)) < eps)))
+    if cfg.kl_beta and ref is not None and cfg.kl_type == O.KL_K3:
+        k = k or abs(abs(ref - logp) - C) < eps
+    dual = getattr(cfg, "dual_clip", 0.0)
+    if dual and A < 0:
+        rbar = min(max(r, 1 - cfg.clip_low), 1 + cfg.clip_high)
+        k = k or abs(max(-A * r, -A * rbar) + dual * A) < eps * abs(A)
+    return bool(k)
+
+
+def branch_coefs(logp, old, ref, A, w, cfg):
+    """Every coefficient a near-kink row may correctly carry: G_pg in {-A r, 0} x G_kl in {k3 slope, 0}."""
+    C = cfg.log_ratio_clamp
+    s = cfg.logit_scale
+    if getattr(cfg, "sft", False):
+        pgs = [-1.0]
+    else:
+        pgs = [-A * math.exp(max(min(logp - old, C), -C)), 0.0]
+    kls = [0.0]
+    if cfg.kl_beta:
+        if cfg.kl_type == O.KL_K3:
+            kls = [1.0 - math.exp(max(min(ref - logp, C), -C)), 0.0]
+        elif cfg.kl_type == O.KL_K1:
+            kls = [1.0]
+        else:
+            kls = [logp - ref]
+    return [-s * w * (gp + cfg.kl_beta * gk) for gp in pgs for gk in kls]
+
+
+def row_ratio(got, want, q, y, coef, dcoef, dtype, ent_mag=None):
+    """max(elementwise ratio, L1 ratio) of one row; `want` = coef q (+ entropy term), q = p - onehot."""
+    rel = DL_REL[dtype]
+    aq = np.abs(q)
+    floor = dcoef * aq
+    floor[y] += abs(coef) * (q[y] + 1.0) * LOGP_ERR
+    if ent_mag is not None:
+        floor = floor + rel * ent_mag
+    d = np.abs(_arr(got) - want)
+    tol = rel * np.abs(want) + floor
+    with np.errstate(divide="ignore", invalid="ignore"):
+        r = np.where(d == 0, 0.0, d / tol)
+    r = np.where(np.isnan(r), np.inf, r)
+    l1 = math.fsum(d) / (DL_L1_REL[dtype] * math.fsum(np.abs(want)) + math.fsum(floor) + 1e-300) \
+        if d.any() else 0.0
+    return max(float(np.max(r)) if r.size else 0.0, l1)
+
+
+# ------------------------------------------------------------------------------------------------
+# all-row comparison of a full micro-batch (C oracle, chunked host copies) — tests/test_gpu_fullsize.py,
+# bench.py parity block
+# ------------------------------------------------------------------------------------------------
+def _host_rows(t, r0, r1, dtype):
+    from oracle import oracle_cpu as OC
+    if dtype == "bf16":
+        return OC.bf16_bits(t[r0:r1])
+    return t[r0:r1].detach().cpu().contiguous().numpy()
+
+
+def oracle_logp(logits, targets, V, dtype, chunk=4096, logit_scale=1.0):
+    """Oracle O3 (C, float64) over every row of a device tensor, chunked through host memory."""
+    from oracle import oracle_cpu as OC
+    n = logits.shape[0]
+    out = {k: np.zeros(n) for k in ("logp", "entropy", "lse")}
+    for r0 in range(0, n, chunk):
+        r1 = min(n, r0 + chunk)
+        f = OC.logprob_entropy(_host_rows(logits, r0, r1, dtype), targets[r0:r1].cpu().numpy(), V=V,
+                               logit_scale=logit_scale)
+        for k in out:
+            out[k][r0:r1] = f[k]
+    return out
+
+
+def microbatch_parity(logits, targets, loss_mask, row_traj, adv, old, ref, n_loss, cfg, dtype, V,
+                      got_logp, got_entropy, got_dlogits, got_stats, chunk=4096):
+    """Every row of one micro-batch: the C oracle (O3 + O4, float64) against the CUDA path's outputs.
+
+    logits / targets / got_* may be device tensors; loss_mask, row_traj, adv, old, ref are host arrays (old and
+    ref float32, as the kernel read them). cfg: oracle_ref.LossCfg (token-mean). got_stats: dict with loss,
+    n_clipped, n_tokens. Returns the max error / tolerance ratios (<= 1 passes) and the raw maxima."""
+    from oracle import oracle_cpu as OC
+    n = logits.shape[0]
+    mask = np.asarray(loss_mask, np.uint8)
+    rt = np.asarray(row_traj)
+    adv = _arr(adv)
+    s = cfg.logit_scale
+    w_tok = 1.0 / n_loss if n_loss > 0 else 0.0
+    glp = got_logp.double().cpu().numpy() if hasattr(got_logp, "cpu") else _arr(got_logp)
+    gH = got_entropy.double().cpu().numpy() if hasattr(got_entropy, "cpu") else _arr(got_entropy)
+    row_L = np.zeros(n)
+    clipped = 0
+    n_kink = 0
+    worst_el, worst_l1, worst_lp, worst_H = 0.0, 0.0, 0.0, 0.0
+    masked_nonzero = 0
+    for r0 in range(0, n, chunk):
+        r1 = min(n, r0 + chunk)
+        bits = _host_rows(logits, r0, r1, dtype)
+        tg = targets[r0:r1].cpu().numpy()
+        m = mask[r0:r1]
+        o = OC.policy_loss(bits, tg, m, rt[r0:r1], adv, old[r0:r1], None if ref is None else ref[r0:r1], n_loss,
+                           cfg, V=V, want_dlogits=False)
+        row_L[r0:r1] = o["row_L"]
+        clipped += int(o["row_clipped"].sum())
+        tr = m != 0
+        if tr.any():
+            worst_lp = max(worst_lp, float(np.max(np.abs(glp[r0:r1][tr] - o["logp"][tr]))))
+            worst_H = max(worst_H, float(np.max(np.abs(gH[r0:r1][tr] - o["entropy"][tr]))))
+        A = adv[rt[r0:r1]]
+        refc = None if ref is None else ref[r0:r1]
+        dc = coef_error(o["row_coef"], o["logp"], old[r0:r1], refc if refc is not None else 0.0, A, w_tok, cfg)
+        got = _host_rows(got_dlogits, r0, r1, dtype)
+        cmp = OC.dlogits_compare(bits, tg, m, s, o["row_lse"], o["row_coef"], dc, LOGP_ERR, DL_REL[dtype], got,
+                                 V=V)
+        el = cmp["max_ratio"]
+        l1 = cmp["l1_err"] / (DL_L1_REL[dtype] * cmp["l1_ref"] + cmp["l1_floor"] + 1e-300)
+        l1[cmp["l1_err"] == 0] = 0.0
+        bad = np.flatnonzero(tr & ((el > 1.0) | (l1 > 1.0)))
+        for i in bad:   # a row on a clip / clamp boundary may carry the other branch's coefficient
+            j = r0 + i
+            refj = None if ref is None else float(ref[j])
+            if not near_kink(o["logp"][i], float(old[j]), refj, float(A[i]), cfg):
+                continue
+            n_kink += 1
+            best = (el[i], l1[i])
+            for c in branch_coefs(o["logp"][i], float(old[j]), refj, float(A[i]), w_tok, cfg):
+                one = np.zeros(r1 - r0, np.uint8)
+                one[i] = 1
+                cc = OC.dlogits_compare(bits, tg, one, s, o["row_lse"], np.full(r1 - r0, c),
+                                        np.full(r1 - r0, dc[i]), LOGP_ERR, DL_REL[dtype], got, V=V)
+                li = cc["l1_err"][i] / (DL_L1_REL[dtype] * cc["l1_ref"][i] + cc["l1_floor"][i] + 1e-300)
+                if max(cc["max_ratio"][i], li) < max(best):
+                    best = (cc["max_ratio"][i], li)
+            el[i], l1[i] = best
+        if tr.any():
+            worst_el = max(worst_el, float(np.max(el[tr])))
+            worst_l1 = max(worst_l1, float(np.max(l1[tr])))
+        if (~tr).any():
+            masked_nonzero += int(np.count_nonzero(got[~tr][:, :V]))
+    loss = math.fsum(row_L[mask != 0] * w_tok)
+    scale = max(abs(loss), math.fsum(np.abs(row_L[mask != 0])) * w_tok)
+    loss_err = abs(got_stats["loss"] - loss)
+    return {
+        "rows": int(n), "trainable": int(mask.sum()),
+        "logp_max_abs_err": worst_lp, "logp_ratio": worst_lp / LOGP_TOL[dtype],
+        "entropy_max_abs_err": worst_H, "entropy_ratio": worst_H / LOGP_TOL[dtype],
+        "dlogits_elem_ratio": worst_el, "dlogits_l1_ratio": worst_l1,
+        "masked_rows_nonzero": masked_nonzero,
+        "loss": got_stats["loss"], "loss_oracle": loss, "loss_abs_err": loss_err,
+        "loss_ratio": loss_err / (LOSS_REL * scale) if scale > 0 else (0.0 if loss_err == 0 else math.inf),
+        "n_clipped": int(got_stats["n_clipped"]), "n_clipped_oracle": clipped, "kink_rows": n_kink,
+        "n_tokens_exact": int(got_stats["n_tokens"]) == int(mask.sum()),
+    }
+
+
+def parity_ok(p):
+    return (p["logp_ratio"] <= 1 and p["entropy_ratio"] <= 1 and p["dlogits_elem_ratio"] <= 1
+            and p["dlogits_l1_ratio"] <= 1 and p["loss_ratio"] <= 1 and p["masked_rows_nonzero"] == 0
+            and p["n_tokens_exact"] and abs(p["n_clipped"] - p["n_clipped_oracle"]) <= p["kink_rows"])

@@ -140,6 +140,18 @@ def _dev(t: torch.Tensor, name: str):
         raise ValueError(f"{name} must be contiguous")
 
 
+def _host(t: torch.Tensor, name: str, dtype, numel: Optional[int]):
+    """Marshalling check of a HOST array of the host-buffer entry point (the C side reads numel elements)."""
+    if t.is_cuda:
+        raise ValueError(f"{name}: the host entry point takes CPU tensors")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {numel}")
+
+
 def _arr(t: Optional[torch.Tensor], name: str, dtype, numel: Optional[int], device, optional: bool = False,
          at_least: bool = False):
     """Marshalling check of a per-row / per-trajectory array: device, contiguity, dtype and size (the kernels
@@ -511,12 +523,25 @@ def otk_policy_loss_fwd_bwd(ctx: Context, logits: torch.Tensor, targets: torch.T
 def otk_policy_loss_fwd_bwd_host(ctx: Context, logits: torch.Tensor, targets, loss_mask, row_traj, adv, old_logp,
                                  ref_logp, n_loss: int, cfg: LossCfg = LossCfg(), *, vocab: Optional[int] = None,
                                  dlogits: Optional[torch.Tensor] = None, rows_per_chunk: int = 4096):
-    """Host-buffer entry point: every tensor is a CPU (ideally pinned) tensor; returns the stats dict."""
-    for t in (logits, targets, loss_mask, row_traj, adv, old_logp):
-        if t.is_cuda:
-            raise ValueError("host entry point takes CPU tensors")
+    """Host-buffer entry point: every tensor is a CPU (ideally pinned) tensor; returns the stats dict.
+    dlogits (CPU, same shape / dtype as logits) receives the gradient (trainable rows only when
+    cfg.zero_masked_rows is False)."""
     N, ld = logits.shape
     V = ld if vocab is None else int(vocab)
+    _host(logits, "logits", logits.dtype, N * ld)
+    if logits.dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("logits must be float32 or bfloat16")
+    _host(targets, "targets", torch.int32, N)
+    _host(loss_mask, "loss_mask", torch.uint8, N)
+    _host(row_traj, "row_traj", torch.int32, N)
+    _host(adv, "adv", torch.float64, None)
+    if adv.numel() < 1:
+        raise ValueError("adv must hold >= 1 trajectory")
+    _host(old_logp, "old_logp", torch.float32, N)
+    if ref_logp is not None:
+        _host(ref_logp, "ref_logp", torch.float32, N)
+    if dlogits is not None:
+        _host(dlogits, "dlogits", logits.dtype, N * ld)
     stats = (C.c_double * len(STATS_FIELDS))()
     c = cfg.c(False)
     _check(_lib.otk_policy_loss_fwd_bwd_host(ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits), _ptr(targets),

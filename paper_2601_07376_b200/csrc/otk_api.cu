@@ -728,15 +728,30 @@ otk_status otk_policy_loss_fwd_bwd_host(otk_ctx* ctx, int64_t num_rows, int64_t 
                                  has_ref ? reinterpret_cast<const float*>(sb + off_ref) : nullptr, d_nl, &c2,
                                  sb + off_dl, nullptr, nullptr, d_stats, reinterpret_cast<otk_stream_t>(xs));
     if (st != OTK_OK) return st;
-    if (dlogits_host && n > 0)
-      OTK_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(dlogits_host) + size_t(r0) * row_bytes, sb + off_dl,
-                               size_t(n) * row_bytes, cudaMemcpyDeviceToHost, xs), "D2H dlogits");
+    if (dlogits_host && n > 0) {
+      // columns [0, vocab) only (the padding of a host row is never written); with zero_masked_rows = 0 only the
+      // runs of trainable rows come back, so masked rows of the host buffer stay untouched (otk.h)
+      const size_t wb = size_t(vocab) * es;
+      for (int64_t a = 0; a < n;) {
+        if (!cfg->zero_masked_rows)
+          while (a < n && !loss_mask_host[r0 + a]) ++a;
+        int64_t e = a;
+        while (e < n && (cfg->zero_masked_rows || loss_mask_host[r0 + e])) ++e;
+        if (e > a)
+          OTK_CUDA(cudaMemcpy2DAsync(reinterpret_cast<char*>(dlogits_host) + size_t(r0 + a) * row_bytes, row_bytes,
+                                     sb + off_dl + size_t(a) * row_bytes, row_bytes, wb, size_t(e - a),
+                                     cudaMemcpyDeviceToHost, xs),
+                   "D2H dlogits");
+        a = e;
+      }
+    }
     OTK_CUDA(cudaEventRecord(ctx->ev[2 + b], xs), "record free");
     if (num_rows == 0) break;
   }
   OTK_CUDA(cudaMemcpyAsync(stats_host, d_stats, sizeof(otk_loss_stats), cudaMemcpyDeviceToHost, xs), "D2H stats");
   OTK_CUDA(cudaStreamSynchronize(xs), "sync exec");
-  return OTK_OK;
+  // the call is blocking, so it reports the device-side data errors of its own launches (sticky word) itself
+  return otk_ctx_check(ctx, reinterpret_cast<otk_stream_t>(xs));
 }
 
 }  // extern "C"

@@ -1,16 +1,14 @@
-"""Shared helpers for the -m gpu parity tests: problem setup and the tolerance checks of DESIGN.md §3/§6."""
+"""Shared helpers for the -m gpu parity tests: problem setup and the tolerance checks of DESIGN.md §6
+(the tolerance model itself lives in oracle/parity.py, shared with bench.py's parity block)."""
 import math
 
 import numpy as np
 import torch
 
 from oracle import oracle_ref as O
+from oracle import parity as P
+from oracle.parity import KINK_EPS, LOGP_TOL  # noqa: F401  (north_star: log-probs within 2e-3 abs, bf16 logits)
 from synth import make_logits, make_noise
-
-BF16_REL = 2.0 ** -7      # dlogits per-element relative tolerance (bf16 output)
-F32_REL = 1e-5            # dlogits per-element relative tolerance (fp32 output)
-COEF_ABS = 1e-5           # dlogits absolute floor, in units of |coef_j|
-LOGP_TOL = {"bf16": 2e-3, "f32": 1e-5}   # north_star: log-probs within 2e-3 abs (bf16 logits)
 
 
 def oracle_cfg(cfg):
@@ -44,45 +42,63 @@ def row_problem(n, V, *, dtype="bf16", ld=None, seed=0, mask_p=0.7, B=6, old_sd=
     return d, h
 
 
-def near_kink(logp, old, ref, A, cfg, eps=1e-4):
-    """Rows whose clip / clamp decision is within eps of a boundary: either branch is correct."""
-    r = math.exp(max(min(logp - old, cfg.log_ratio_clamp), -cfg.log_ratio_clamp))
-    return (abs(r - (1 + cfg.clip_high)) < eps or abs(r - (1 - cfg.clip_low)) < eps
-            or abs(abs(logp - old) - cfg.log_ratio_clamp) < eps
-            or (ref is not None and abs(abs(ref - logp) - cfg.log_ratio_clamp) < eps))
+def near_kink(logp, old, ref, A, cfg, eps=KINK_EPS):
+    """Rows whose clip / clamp decision is within eps of a boundary: either branch is correct (both are
+    checked, see check_dlogits_rows)."""
+    return P.near_kink(logp, old, ref, A, cfg, eps)
 
 
 def coef_sensitivity(logp, old, ref, A, N, cfg):
-    """|d coef_j / d logp_j| from oracle quantities: coef = -s (m/N) G(logp) with dG/dlogp = -A r
-    (unclipped) + beta * (k3: e^d, k1: 0, k2: 1). The kernel's fp32 logp carries ~1e-6 absolute error,
-    so coef inherits |dcoef/dlogp| * dlogp of ABSOLUTE error even when coef itself is tiny (G can cancel)."""
-    C = cfg.log_ratio_clamp
-    r = math.exp(max(min(logp - old, C), -C))
-    s = cfg.logit_scale
-    dg = abs(A) * r
-    if cfg.kl_beta:
-        if cfg.kl_type == 3:
-            dg += cfg.kl_beta * math.exp(max(min(ref - logp, C), -C))
-        elif cfg.kl_type == 2:
-            dg += cfg.kl_beta
-    return s * dg / max(N, 1)
+    """|d coef_j / d logp_j| per unit weight 1/N: coef = -s w G(logp) with dG/dlogp = -A r (unclipped) +
+    beta * (k3: e^d, k1: 0, k2: 1)."""
+    return abs(cfg.logit_scale) * float(P.g_sensitivity(logp, old, ref, A, cfg)) / max(N, 1)
 
 
-def check_dlogits_rows(got, want, coef, rows, dtype, V, dcoef=None, logp_err=1e-5):
-    """|d| <= rel*|ref| + 1e-5*|coef_j| + logp_err*|dcoef_j/dlogp_j| per element."""
-    rel = BF16_REL if dtype == "bf16" else F32_REL
+def dcoef_rows(h, want_logp, cfg, N, beta, W=None):
+    """Per trainable row: |d coef_j / d logp_j| (row weight W[j], default the token-mean 1/N)."""
+    out = {}
+    for j in range(len(h["mask"])):
+        if h["mask"][j]:
+            w = (1.0 / max(N, 1)) if W is None else float(W[j])
+            out[j] = abs(cfg.logit_scale) * w * float(P.g_sensitivity(want_logp[j], h["old"][j],
+                                                                       h["ref"][j] if beta else 0.0,
+                                                                       h["adv"][h["row_traj"][j]], cfg))
+    return out
+
+
+def check_dlogits_rows(got, want, coef, rows, dtype, V, dcoef=None, logp_err=P.LOGP_ERR, *, wide, targets,
+                       scale=1.0, h=None, cfg=None, W=None, ent=None):
+    """Worst max(elementwise, L1) error / tolerance ratio over `rows` (oracle/parity.py):
+    |d_v| <= rel |want_v| + (1e-5 |coef_j| + logp_err |dcoef_j/dlogp_j|) |p_v - [v=y_j]| + [v=y_j] |coef_j| p_y logp_err,
+    and sum_v |d_v| <= L1_REL sum_v |want_v| + sum_v floor_v. `wide[j]` (array or callable) is the row's
+    logits in float64, from which the oracle's p is formed. With h / cfg given, a row near a clip / clamp kink
+    passes if either branch's coefficient passes. ent = (c_H, H dict): entropy-bonus rows (want includes the
+    bonus term; its magnitude w c_H s p (|ln p| + H) gets the relative tolerance too)."""
     worst = 0.0
     for j in rows:
-        g = got[j, :V].double().cpu().numpy() if isinstance(got, torch.Tensor) else got[j]
-        w = want[j]
-        floor = COEF_ABS * abs(coef[j]) + (logp_err * dcoef[j] if dcoef is not None else 0.0)
-        tol = rel * np.abs(w) + floor + 1e-30
-        ratio = float(np.max(np.abs(g - w) / tol))
-        worst = max(worst, ratio)
+        g = got[j, :V].double().cpu().numpy() if isinstance(got, torch.Tensor) else np.asarray(got[j])
+        x = wide(j) if callable(wide) else wide[j]
+        y = int(targets[j])
+        lpj, H, _, p = O.row_forward(x[:V], y, scale)
+        q = p.copy()
+        q[y] -= 1.0
+        w = np.asarray(want[j], np.float64)
+        c = float(coef[j])
+        dslope = dcoef[j] if dcoef is not None else 0.0
+        ent_mag = None
+        if ent is not None:
+            c_h, wj = ent
+            with np.errstate(divide="ignore"):
+                lnp = np.where(p > 0, np.log(np.where(p > 0, p, 1.0)), 0.0)
+            ent_mag = abs(wj[j] * c_h * scale) * p * (np.abs(lnp) + H)
+        cands = [(c, w)]
+        if h is not None and cfg is not None:
+            A = h["adv"][h["row_traj"][j]]
+            refj = h["ref"][j] if cfg.kl_beta else None
+            if P.near_kink(lpj, h["old"][j], refj, A, cfg):
+                wj = (1.0 / max(int(h["mask"].sum()), 1)) if W is None else float(W[j])
+                cands += [(a, w + (a - c) * q) for a in P.branch_coefs(lpj, h["old"][j], refj, A, wj, cfg)]
+        best = min(P.row_ratio(g, wc, q, y, cc, P.COEF_REL * abs(cc) + logp_err * dslope, dtype, ent_mag)
+                   for cc, wc in cands)
+        worst = max(worst, best)
     return worst
-
-
-def dcoef_rows(h, want_logp, cfg, N, beta):
-    return {j: coef_sensitivity(want_logp[j], h["old"][j], h["ref"][j] if beta else 0.0,
-                                h["adv"][h["row_traj"][j]], N, cfg)
-            for j in range(len(h["mask"])) if h["mask"][j]}

@@ -156,8 +156,10 @@ def test_targets_on_segment_boundaries(otk, ctx, dtype, V):
     ctx.check()
     want = O.policy_loss_fwd_bwd(wide, np.array(cols), np.ones(n, np.uint8), np.zeros(n, np.int32), adv.numpy(),
                                  old.astype(np.float64), None, n, O.LossCfg(kl_beta=0.0))
-    g = out["dlogits"].double().cpu().numpy()
-    rel = 2.0 ** -7 if dtype == "bf16" else 1e-5
-    for j, y in enumerate(cols):
-        w = want["dlogits"][j][y]
-        assert abs(g[j, y] - w) <= rel * abs(w) + 1e-5 * abs(want["coef"][j]) + 1e-30, (j, y, g[j, y], w)
+    from tests.gpu_common import check_dlogits_rows, dcoef_rows
+    h = dict(old=old.astype(np.float64), ref=np.zeros(n), adv=adv.numpy(), row_traj=np.zeros(n, np.int32),
+             mask=np.ones(n, np.uint8))
+    ocfg = O.LossCfg(kl_beta=0.0)
+    dc = dcoef_rows(h, want["logp"], ocfg, n, 0.0)
+    assert check_dlogits_rows(out["dlogits"], want["dlogits"], want["coef"], list(range(n)), dtype, V, dc, wide=wide,
+                              targets=np.array(cols), h=h, cfg=ocfg) <= 1.0

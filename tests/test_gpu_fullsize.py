@@ -1,7 +1,6 @@
 """Full-size parity (-m gpu): BASELINE configs at V = 151936 in the launch configuration bench.py times
-(65,536-row micro-batches of the fused loss), checked on sampled rows the oracle computes one by one,
-plus properties over every row. Inputs of every sampled row come from the seeded generator and the
-oracle only (old/ref of sampled rows = oracle logp + noise)."""
+(65,536-row micro-batches of the fused loss), every row against the C float64 oracle (oracle/parity.py).
+Inputs come from the seeded generator and the oracle only (old / ref = oracle logp + noise)."""
 import math
 
 import numpy as np
@@ -10,7 +9,7 @@ import torch
 
 from oracle import oracle_ref as O
 from synth import CONFIGS, make_batch, make_logits, make_noise
-from tests.gpu_common import LOGP_TOL, check_dlogits_rows, dcoef_rows, oracle_cfg
+from tests.gpu_common import LOGP_TOL, oracle_cfg
 
 pytestmark = pytest.mark.gpu
 
@@ -21,15 +20,19 @@ def otk():
     return m
 
 
-@pytest.mark.parametrize("name,rows", [("math", 65536), ("game", 32768), ("marl", 32768)])
-def test_fullsize_microbatch(otk, name, rows):
-    from paper_2601_07376_b200.step import MicroBatch, PolicyLossStep
+@pytest.mark.parametrize("name", ["math", "game", "marl"])
+def test_fullsize_microbatch(otk, name):
+    """EVERY row of one 65,536-row micro-batch (the bench's launch configuration) against the C float64
+    oracle: (3) logp / entropy, then (4) with old / ref = oracle logp + noise (nothing derived from the CUDA
+    path): logp, entropy, each dlogits element and row L1 (oracle/parity.py tolerances), masked rows exactly 0,
+    the micro-batch loss and the clipped / token counts."""
+    from oracle import parity as P
+    from paper_2601_07376_b200.step import PolicyLossStep
     cfgw = CONFIGS[name]
-    V = cfgw.V
+    V, M, dev = cfgw.V, 65536, "cuda"
     ctx = otk.Context(0)
     tb = make_batch(name)
     db = otk.traj_batch_to_device(tb)
-    dev = "cuda"
     cfg = otk.LossCfg(kl_beta=cfgw.kl_beta)
     step = PolicyLossStep(ctx, db, torch.from_numpy(tb.group_id).to(dev), tb.num_groups,
                           torch.from_numpy(tb.turn_offsets).to(dev), torch.from_numpy(tb.turn_rewards).to(dev), V, cfg)
@@ -43,67 +46,31 @@ def test_fullsize_microbatch(otk, name, rows):
     oadv = O.group_advantages(tb.group_id, O.episode_returns(tb.turn_offsets, tb.turn_rewards), tb.num_groups)["adv"]
     assert np.max(np.abs(adv.cpu().numpy() - oadv)) < 1e-6
 
-    # one micro-batch of logits (the bench's generator), sampled rows, and their oracle inputs
-    M = rows
     logits, targets = make_logits(M, V, dtype="bf16", seed=cfgw.seed * 100, device=dev, rows_per_chunk=4096)
     mask = om["loss_mask"][:M]
-    tr = np.flatnonzero(mask)
-    ms = np.flatnonzero(mask == 0)
-    sample = sorted(set(tr[np.linspace(0, len(tr) - 1, 12).astype(int)].tolist()
-                        + ms[np.linspace(0, len(ms) - 1, 4).astype(int)].tolist() + [M - 1]))
-    y = targets.cpu().numpy()
-    wide = {j: logits[j].double().cpu().numpy() for j in sample}
-    olp = {j: O.row_forward(wide[j], int(y[j]))[0] for j in sample}
-    fwd = otk.otk_logprob_entropy_fwd(ctx, logits, targets)                            # (3) on every row
-    for j in sample:
-        lp, H, _, _ = O.row_forward(wide[j], int(y[j]))
-        assert abs(float(fwd["logp"][j]) - lp) < LOGP_TOL["bf16"] and abs(float(fwd["entropy"][j]) - H) < LOGP_TOL["bf16"]
-    n_old = make_noise(M, 0.05, 11, device=dev)
-    n_ref = make_noise(M, 0.1, 12, device=dev)
-    old = fwd["logp"] + n_old
-    ref = fwd["logp"] + n_ref
-    sidx = torch.tensor(sample, device=dev)
-    olp_t = torch.tensor([olp[j] for j in sample], dtype=torch.float64)
-    old[sidx] = (olp_t + n_old[sidx].double().cpu()).float().to(dev)
-    ref[sidx] = (olp_t + n_ref[sidx].double().cpu()).float().to(dev)
+    rt = om["row_traj"][:M]
+    # (3) on every row
+    fwd = otk.otk_logprob_entropy_fwd(ctx, logits, targets)
+    ctx.check()
+    of = P.oracle_logp(logits, targets, V, "bf16")
+    assert float(np.max(np.abs(fwd["logp"].double().cpu().numpy() - of["logp"]))) < LOGP_TOL["bf16"]
+    assert float(np.max(np.abs(fwd["entropy"].double().cpu().numpy() - of["entropy"]))) < LOGP_TOL["bf16"]
+    del fwd
+    # (4) on every row, old / ref from the oracle's logp
+    old = (of["logp"] + make_noise(M, 0.05, 11).double().numpy()).astype(np.float32)
+    ref = (of["logp"] + make_noise(M, 0.1, 12).double().numpy()).astype(np.float32)
     dl = torch.empty_like(logits)
     out = otk.otk_policy_loss_fwd_bwd(ctx, logits, targets, step.masks["loss_mask"][:M], step.masks["row_traj"][:M],
-                                      adv, old, ref if cfgw.kl_beta else None, step.masks["n_loss"], cfg,
-                                      dlogits=dl)
+                                      adv, torch.from_numpy(old).to(dev),
+                                      torch.from_numpy(ref).to(dev) if cfgw.kl_beta else None,
+                                      step.masks["n_loss"], cfg, dlogits=dl)
     ctx.check()
-    ocfg = oracle_cfg(cfg)
-    N = om["n_loss"]
-    old_h, ref_h = old.double().cpu().numpy(), ref.double().cpu().numpy()
-    want = O.policy_loss_fwd_bwd(lambda j: wide[j], y, om["loss_mask"], om["row_traj"], oadv, old_h,
-                                 ref_h if cfgw.kl_beta else None, N, ocfg, rows=sample)
-    h = dict(old=old_h, ref=ref_h, adv=oadv, row_traj=om["row_traj"], mask=np.zeros(M, np.uint8))
-    h["mask"][[j for j in sample if mask[j]]] = 1
-    dc = dcoef_rows(h, {j: want["logp"][j] for j in sample}, ocfg, N, cfgw.kl_beta)
-    trows = [j for j in sample if mask[j]]
-    assert check_dlogits_rows(dl, want["dlogits"], want["coef"], trows, "bf16", V, dc) <= 1.0
-    for j in sample:
-        assert abs(float(out["logp"][j]) - want["logp"][j]) < LOGP_TOL["bf16"]
-        if not mask[j]:
-            assert bool((dl[j] == 0).all())
-    # properties over every row of the micro-batch
-    m_t = step.masks["loss_mask"][:M].bool()
-    assert bool((dl[~m_t] == 0).all())                                   # mask soundness
     st = otk.stats_dict(out["stats"])
-    assert st["n_tokens"] == int(mask.sum())
-    # loss = sum_j m_j L_j / N restated in float64 from the kernel's own per-row logp (property at any size)
-    lp = out["logp"].double().cpu().numpy()[mask == 1]
-    A = oadv[om["row_traj"][:M][mask == 1]]
-    C = 20.0
-    d = np.clip(lp - old_h[mask == 1], -C, C)
-    r = np.exp(d)
-    pg = np.maximum(-A * r, -A * np.clip(r, 0.8, 1.2))
-    kl = 0.0
-    if cfgw.kl_beta:
-        dd = np.clip(ref_h[mask == 1] - lp, -C, C)
-        kl = np.expm1(dd) - dd
-    L = pg + cfgw.kl_beta * kl
-    want_loss = math.fsum(L) / N
-    assert abs(st["loss"] - want_loss) <= 1e-4 * max(abs(want_loss), np.abs(L).sum() / N)
+    par = P.microbatch_parity(logits, targets, mask, rt, oadv, old, ref if cfgw.kl_beta else None, om["n_loss"],
+                              oracle_cfg(cfg), "bf16", V, out["logp"], out["entropy"], dl, st)
+    print(name, par)
+    assert P.parity_ok(par), par
+    assert par["trainable"] == int(mask.sum()) and par["rows"] == M
     ctx.close()
 
 

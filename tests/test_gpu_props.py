@@ -51,13 +51,15 @@ def test_random_loss_vs_oracle(otk, ctx, V, n, dtype, scale, beta, kl, seed):
     assert np.all(f["logp"].cpu().numpy()[m] == got["logp"].cpu().numpy()[m])   # (3) and (4): bitwise equal logp
     kinks = {j for j in range(n) if m[j] and near_kink(want["logp"][j], h["old"][j], h["ref"][j] if beta else None,
                                                        h["adv"][h["row_traj"][j]], ocfg)}
-    rows = [j for j in range(n) if m[j] and j not in kinks]
+    rows = [j for j in range(n) if m[j]]
     dc = dcoef_rows(h, want["logp"], ocfg, N, beta)
-    assert check_dlogits_rows(got["dlogits"], want["dlogits"], want["coef"], rows, dtype, V, dc) <= 1.0
-    if N and not kinks:
+    assert check_dlogits_rows(got["dlogits"], want["dlogits"], want["coef"], rows, dtype, V, dc, wide=h["wide"],
+                              targets=h["targets"], scale=scale, h=h, cfg=ocfg) <= 1.0
+    if N:
         st_ = otk.stats_dict(got["stats"])
         scale_ = max(abs(want["loss"]), sum(abs(O.row_loss_terms(want["logp"][j], h["old"][j],
                                                                  h["ref"][j] if beta else None,
                                                                  h["adv"][h["row_traj"][j]], ocfg)[0])
                                             for j in range(n) if m[j]) / N)
-        assert abs(st_["loss"] - want["loss"]) <= 1e-4 * scale_
+        assert abs(st_["loss"] - want["loss"]) <= 1e-4 * scale_           # L is continuous across the kinks
+        assert abs(st_["n_clipped"] - want["stats"]["n_clipped"]) <= len(kinks)

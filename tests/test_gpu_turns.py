@@ -11,7 +11,7 @@ import torch
 from oracle import oracle_ref as O
 from synth import CONFIGS, make_batch, make_logits, make_noise
 from synth.trajectories import random_small_batch
-from tests.gpu_common import check_dlogits_rows, dcoef_rows, near_kink, oracle_cfg
+from tests.gpu_common import check_dlogits_rows, dcoef_rows, oracle_cfg
 
 pytestmark = pytest.mark.gpu
 
@@ -120,8 +120,8 @@ def test_turn_level_step(otk, ctx, dtype, V, gamma):
     # dlogits: the oracle's, with per-row advantage taken through row_seg
     h = dict(old=old.astype(np.float64), ref=ref.astype(np.float64), adv=adv_seg, row_traj=om["row_seg"],
              mask=om["loss_mask"])
-    rows = [j for j in range(N) if om["loss_mask"][j] and not near_kink(want["logp"][j], h["old"][j], h["ref"][j],
-                                                                         adv_seg[om["row_seg"][j]], ocfg)]
+    rows = [j for j in range(N) if om["loss_mask"][j]]
     dc = dcoef_rows(h, want["logp"], ocfg, n_loss, True)
-    assert check_dlogits_rows(dl, want["dlogits"], want["coef"], rows, dtype, V, dc) <= 1.0
+    assert check_dlogits_rows(dl, want["dlogits"], want["coef"], rows, dtype, V, dc, wide=wide, targets=y, h=h,
+                              cfg=ocfg) <= 1.0
     assert bool((dl[torch.from_numpy(om["loss_mask"] == 0).cuda()] == 0).all())

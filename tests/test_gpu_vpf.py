@@ -91,7 +91,8 @@ def test_vpf_equals_gathered_path_and_oracle(otk, P, V, dtype, n):
     assert abs(sv["loss"] - want["loss"]) <= 1e-4 * max(abs(want["loss"]), 1e-3)
     rows = [j for j in range(n) if h["mask"][j]]
     dc = dcoef_rows(h, want["logp"], ocfg, N, True)
-    assert check_dlogits_rows(dl, want["dlogits"], want["coef"], rows, dtype, V, dc) <= 1.0
+    assert check_dlogits_rows(dl, want["dlogits"], want["coef"], rows, dtype, V, dc, wide=h["wide"],
+                              targets=h["targets"], h=h, cfg=ocfg) <= 1.0
     gd = dl.float()
     masked = [j for j in range(n) if not h["mask"][j]]
     assert all(bool((gd[j] == 0).all()) for j in masked)          # every rank zero-filled its columns
