@@ -399,9 +399,9 @@ def other_kernels(W, step, cfg):
         out[f"sample_tokens_{mode}"] = {"rows": n, "us": ms * 1e3, "GBps": gbs, "frac_hbm": gbs / hbm,
                                         "kernel": ("k_sample" if mode == "greedy" else "k_sample_tm")
                                         + " (SURVEY.md §8(f) NEXT-3)"}
-    # K4-VPF (vocab-sharded loss, exchange in-kernel): P = 2 ranks co-scheduled on this GPU (own ctx, stream,
-    # column shard, 74 CTAs each) on micro-batch 0, against the unsharded loss on the same rows (measured before
-    # the tensor-core benchmark below, whose power draw would slow whichever runs after it)
+    # K4-VPF (vocab-sharded loss, exchange in-kernel): P = 2 ranks emulated on this GPU in ONE cooperative launch
+    # (own ctx, column shard, 74 CTAs each) on micro-batch 0, against the unsharded loss on the same rows (measured
+    # before the tensor-core benchmark below, whose power draw would slow whichever runs after it)
     mb = W["mbs"][0]
     lm, rt = step.masks["loss_mask"][mb.r0:mb.r1], step.masks["row_traj"][mb.r0:mb.r1]
     adv, nl = step.adv_out["adv"], step.masks["n_loss"]
@@ -410,26 +410,19 @@ def other_kernels(W, step, cfg):
     P = 2
     b = [V * k // P // 8 * 8 for k in range(P)] + [V]
     ctxs = [otk.Context(ctx.device) for _ in range(P)]
-    streams = [torch.cuda.Stream() for _ in range(P)]
-    xs = otk.VpfExchange.local_group(ctxs, M, max_ctas=148 // P)
-    main = torch.cuda.current_stream()
+    xs = otk.VpfExchange.local_group(ctxs, M)
 
     def vpf(i):
-        for s_ in streams:
-            s_.wait_stream(main)
-        for q in range(P):
-            otk.otk_policy_loss_fwd_bwd_vpf(ctxs[q], mb.logits[:, b[q]:b[q + 1]], mb.targets, lm, rt, adv,
-                                            mb.old_logp, mb.ref_logp, nl, cfg, b[q], V, xs[q],
-                                            dlogits=mb.dlogits[:, b[q]:b[q + 1]], stream=streams[q])
-        for s_ in streams:
-            main.wait_stream(s_)
+        otk.otk_policy_loss_fwd_bwd_vpf_group(ctxs, [mb.logits[:, b[q]:b[q + 1]] for q in range(P)], mb.targets, lm,
+                                              rt, adv, mb.old_logp, mb.ref_logp, nl, cfg, b[:P], V, xs,
+                                              dlogits=[mb.dlogits[:, b[q]:b[q + 1]] for q in range(P)])
     ms_v = timed(vpf, 4)
     for c in ctxs:
         c.check()
     for x in xs:
         x.close()
     out["vocab_shard_vpf_p2_one_gpu"] = {"rows": M, "ms": ms_v, "ms_unsharded": ms_u, "vs_unsharded": ms_u / ms_v,
-                                         "kernel": "k_rows_tm<bf16,BWD_VPF> x 2 ranks co-scheduled (DESIGN.md §7)"}
+                                         "kernel": "k_rows_vpf_group<bf16>: 2 ranks in one launch (DESIGN.md §7)"}
     from synth import make_lmhead
     rows, d = 8192, 3584
     h, w, y = make_lmhead(rows, V, d, seed=1, device=bufs[0].device)

@@ -217,6 +217,11 @@ typedef struct {
   const int64_t* n_active_traj;    /* device [1]: trajectories with >= 1 loss token, global (seq-mean) */
   const int32_t* adv_index;        /* device [num_rows] or NULL: A_j = adv[adv_index[j]] instead of
                                       adv[row_traj[j]] (turn-level credit: row_seg + segment advantages) */
+  int64_t num_adv;                 /* elements of adv (>= 1 when num_rows > 0): a row whose index into adv
+                                      (row_traj[j] or adv_index[j]) is outside [0, num_adv) sets
+                                      OTK_ERR_GROUP_RANGE and is treated as loss-masked (memory-safe)      */
+  int64_t num_traj;                /* elements of traj_loss_tokens (sequence-mean reductions; row_traj[j]
+                                      outside [0, num_traj) is a GROUP_RANGE data error as above)         */
 } otk_loss_cfg;
 
 typedef struct {
@@ -329,6 +334,31 @@ otk_status otk_policy_loss_fwd_bwd_vpf(otk_ctx* ctx, int64_t num_rows, int64_t v
                                        const otk_loss_cfg* cfg, const otk_vocab_shard* shard,
                                        const otk_vpf_peers* peers /* host struct */, void* dlogits, float* logp,
                                        float* entropy, otk_loss_stats* stats, otk_stream_t stream);
+
+/* K4-VPF ranks EMULATED on one GPU in ONE launch (single-GPU tests, smoke and bench only; a real multi-GPU job
+ * makes one otk_policy_loss_fwd_bwd_vpf call per rank). calls[k] is rank k's call: its own ctx (distinct per
+ * rank: scratch and ticket), column shard, exchange view (peers->rank == k, peers->nranks == nranks) and outputs;
+ * the row-side arrays are shared. The launch hosts every rank's CTAs (the SMs split evenly between the ranks,
+ * one CTA per SM) and is cooperative — all CTAs are resident at once, so the in-kernel exchange never waits on an
+ * unscheduled rank (separate launches on separate streams carry no such guarantee, and a profiler serialising
+ * them would time out). Returns OTK_ERR_CUDA if the grid cannot be co-resident. Same results, bit for bit, as
+ * the per-rank calls. Counts as one launch on calls[0].ctx. */
+typedef struct {
+  otk_ctx* ctx;
+  int64_t vocab_local;
+  const void* logits;             /* this rank's shard [num_rows, vocab_local], row stride ld */
+  otk_vocab_shard shard;
+  const otk_vpf_peers* peers;
+  void* dlogits;                  /* [num_rows, vocab_local], row stride ld */
+  float* logp;                    /* [num_rows] or NULL */
+  float* entropy;                 /* [num_rows] or NULL */
+  otk_loss_stats* stats;          /* device */
+} otk_vpf_rank_call;
+otk_status otk_policy_loss_fwd_bwd_vpf_group(int32_t nranks, const otk_vpf_rank_call* calls, int64_t num_rows,
+                                             int64_t ld, otk_dtype dtype, const int32_t* targets,
+                                             const uint8_t* loss_mask, const int32_t* row_traj, const double* adv,
+                                             const float* old_logp, const float* ref_logp, const int64_t* n_loss,
+                                             const otk_loss_cfg* cfg, otk_stream_t stream);
 
 /* Exchange buffers and their CUDA IPC plumbing (setup, not the hot path). otk_xchg_alloc: a zeroed device
  * buffer of `bytes` on the ctx's device (its own cudaMalloc allocation, so an IPC handle maps exactly it);

@@ -199,38 +199,43 @@ int orc_build_masks(int32_t B, const int64_t* tok_offsets, const int32_t* seg_of
  * a row on a clip / clamp kink):
  *     p_v = exp(s x_v - lse_j),  q_v = p_v - [v == y_j],  want_v = coef_j q_v
  * and compares it with the CUDA path's value got_v (fp32, or bf16 bits, row stride got_ld):
- *     floor_v = dcoef_j |q_v| + [v == y_j] |coef_j| p_v logp_err
+ *     floor_v = dcoef_j |q_v| + [v == y_j] |coef_j| p_v logp_err + abs_floor
  *     tol_v   = rel |want_v| + floor_v
- * dcoef_j is the absolute error bound of coef_j, and the target column's extra term is the error
- * p_y * dlogp of coef * expm1(logp). Outputs per row: max_v |got_v - want_v| / tol_v (0/0 = 0, x/0 = inf),
- * sum |got - want|, sum |want|, sum floor. Rows with sel[j] == 0 are skipped (outputs untouched). */
+ * dcoef_j is the absolute error bound of coef_j, the target column's extra term is the error p_y * dlogp of
+ * coef * expm1(logp), and abs_floor covers values below the output format's smallest normal (flushed to 0).
+ * Outputs per row: max_v |got_v - want_v| / tol_v (0/0 = 0, x/0 = inf), and over the non-target columns
+ * sum |got - want|, sum |want|, sum want^2, sum floor. Rows with sel[j] == 0 are skipped (outputs untouched). */
 int orc_dlogits_compare(int64_t n_rows, int64_t V, int64_t ld, int32_t dtype, const void* logits,
                         const int32_t* targets, const uint8_t* sel, double logit_scale, const double* lse,
-                        const double* coef, const double* dcoef, double logp_err, double rel,
+                        const double* coef, const double* dcoef, double logp_err, double rel, double abs_floor,
                         const void* got, int64_t got_ld, int32_t got_dtype,
-                        double* max_ratio, double* l1_err, double* l1_ref, double* l1_floor) {
+                        double* max_ratio, double* l1_err, double* l1_ref, double* l2_ref, double* l1_floor) {
   const double s = logit_scale;
 #pragma omp parallel for schedule(static)
   for (int64_t j = 0; j < n_rows; ++j) {
     if (sel && !sel[j]) continue;
     double worst = 0.0;
-    nsum E = {0, 0}, R = {0, 0}, F = {0, 0};
+    nsum E = {0, 0}, R = {0, 0}, R2 = {0, 0}, F = {0, 0};
     for (int64_t v = 0; v < V; ++v) {
       double p = exp(s * widen(logits, dtype, j * ld + v) - lse[j]);
       double q = p - (v == targets[j] ? 1.0 : 0.0);
       double want = coef[j] * q;
-      double floor_v = dcoef[j] * fabs(q) + (v == targets[j] ? fabs(coef[j]) * p * logp_err : 0.0);
+      double floor_v = dcoef[j] * fabs(q) + (v == targets[j] ? fabs(coef[j]) * p * logp_err : 0.0) + abs_floor;
       double tol = rel * fabs(want) + floor_v;
       double d = fabs(widen(got, got_dtype, j * got_ld + v) - want);
       double r = d == 0.0 ? 0.0 : (tol > 0.0 ? d / tol : INFINITY);
       if (r > worst || r != r) worst = r != r ? INFINITY : r;
-      nadd(&E, d);
-      nadd(&R, fabs(want));
-      nadd(&F, floor_v);
+      if (v != targets[j]) {  /* row sums over the non-target columns (the target column is one element) */
+        nadd(&E, d);
+        nadd(&R, fabs(want));
+        nadd(&R2, want * want);
+        nadd(&F, floor_v);
+      }
     }
     max_ratio[j] = worst;
     l1_err[j] = nget(&E);
     l1_ref[j] = nget(&R);
+    l2_ref[j] = nget(&R2);
     l1_floor[j] = nget(&F);
   }
   return 0;

@@ -91,7 +91,7 @@ def policy_loss(logits: np.ndarray, targets, loss_mask, row_traj, adv, old_logp,
                 row_coef=coef)
 
 
-def dlogits_compare(logits: np.ndarray, targets, sel, logit_scale, lse, coef, dcoef, logp_err, rel, got,
+def dlogits_compare(logits: np.ndarray, targets, sel, logit_scale, lse, coef, dcoef, logp_err, rel, abs_floor, got,
                     V=None):
     """Element-by-element comparison of a CUDA-path dlogits block (`got`: float32 or bf16 bits, [n, >= V])
     with the O4 gradient re-formed in float64 from the oracle's per-row lse / coef (orc_dlogits_compare;
@@ -105,12 +105,13 @@ def dlogits_compare(logits: np.ndarray, targets, sel, logit_scale, lse, coef, dc
     lse = np.ascontiguousarray(lse, np.float64)
     coef = np.ascontiguousarray(coef, np.float64)
     dcoef = np.ascontiguousarray(dcoef, np.float64)
-    out = [np.zeros(n) for _ in range(4)]
+    out = [np.zeros(n) for _ in range(5)]
     lib().orc_dlogits_compare(C.c_int64(n), C.c_int64(V), C.c_int64(ld), C.c_int32(_dtype_code(logits)),
                               _p(logits), _p(targets), _p(sel), C.c_double(logit_scale), _p(lse), _p(coef), _p(dcoef),
-                              C.c_double(logp_err), C.c_double(rel), _p(got), C.c_int64(got.shape[1]),
-                              C.c_int32(_dtype_code(got)), _p(out[0]), _p(out[1]), _p(out[2]), _p(out[3]))
-    return dict(max_ratio=out[0], l1_err=out[1], l1_ref=out[2], l1_floor=out[3])
+                              C.c_double(logp_err), C.c_double(rel), C.c_double(abs_floor), _p(got),
+                              C.c_int64(got.shape[1]), C.c_int32(_dtype_code(got)), _p(out[0]), _p(out[1]),
+                              _p(out[2]), _p(out[3]), _p(out[4]))
+    return dict(max_ratio=out[0], l1_err=out[1], l1_ref=out[2], l2_ref=out[3], l1_floor=out[4])
 
 
 def build_masks(tb, train_agent=-1):

@@ -9,14 +9,23 @@ Tolerances (BASELINE.json north_star; DESIGN.md §6 "Error budget"):
   logp, entropy ..................................... 2e-3 abs for bf16 logits, 1e-5 for fp32
   loss .............................................. 1e-4 x max(|loss|, sum_j w_j |L_j|)   (R22)
   dlogits, per element (row j, column v; q_v = p_v - [v = y_j], the oracle's coef_j and p_v):
-      |got - want| <= rel |want| + dcoef_j |q_v| + [v = y_j] |coef_j| p_y LOGP_ERR
-      rel = 2^-7 (bf16 output: e and the product are each rounded once, <= 2^-8 each) or 1e-5 (fp32);
+      |got - want| <= rel |want| + dcoef_j |q_v| + [v = y_j] |coef_j| p_y LOGP_ERR + ABS_FLOOR
+      rel = 2^-7 (1 + 2^-6) for bf16 output: e and the product are each rounded once to 8 significant bits
+      (<= 2^-8 relative each), plus the 16-bit split of the fp32 scale (3 x 2^-16); 1e-5 for fp32 output.
       dcoef_j = COEF_REL |coef_j| + LOGP_ERR s w_j |dG/dlogp| is the absolute error coef_j inherits from the
       fp32 logp (coef = -s w G(logp), and G's PPO / KL parts can cancel); the target column carries
       coef * p_y * dlogp from expm1(logp). Both floors scale with the element's own |p_v - onehot|, so a
-      tiny-probability element is checked relative to itself, never against a row-wide floor.
-  dlogits, per row (L1): sum_v |got - want| <= L1_REL sum_v |want| + sum_v floor_v, L1_REL = 2^-8 (bf16; the
-      mean of two round-to-nearest errors is well below the per-element 2^-7 worst case) or 1e-5 (fp32).
+      tiny-probability element is checked relative to itself, never against a row-wide floor. ABS_FLOOR =
+      2^-126 (the smallest normal of fp32 and bf16): values below it may flush to 0 (fp32 math is
+      flush-to-zero, and bf16 subnormals end at 2^-133) — e.g. p ~ e^-90 behind a dominant logit.
+  dlogits, per row (L1, over the non-target columns v != y_j; the target column is one element, formed
+      separately as coef expm1(logp), and carries half of the row's |want| mass, so it stays with the
+      per-element check): sum_v |got - want| <= L1_REL sum_v |want| + 3 rel sqrt(sum_v want_v^2) + sum_v floor_v.
+      The element errors are independent roundings with mean < L1_REL |want_v| (2^-8; two RNE roundings
+      average ~2^-9) and range <= rel |want_v|, so by Hoeffding the sum exceeds its mean by more than
+      3 rel sqrt(sum want^2) with probability < e^-18 per row. Where the mass is spread over many elements the
+      second term vanishes and the check is 2^-8, half the per-element bound; a row dominated by one or two
+      elements is left to the per-element check.
   Rows within KINK_EPS of a clip / ratio-clamp / KL-clamp / dual-clip boundary accept either branch's
   coefficient (the fp32 and the float64 logp can fall on different sides); both are checked in full.
 """
@@ -31,8 +40,10 @@ from oracle import oracle_ref as O
 LOGP_TOL = {"bf16": 2e-3, "f32": 1e-5}
 ADV_TOL = 1e-6
 LOSS_REL = 1e-4
-DL_REL = {"bf16": 2.0 ** -7, "f32": 1e-5}
+DL_REL = {"bf16": 2.0 ** -7 * (1 + 2.0 ** -6), "f32": 1e-5}
 DL_L1_REL = {"bf16": 2.0 ** -8, "f32": 1e-5}
+L1_DEV = 3.0          # Hoeffding deviation, in units of rel * sqrt(sum want^2)
+ABS_FLOOR = 2.0 ** -126
 COEF_REL = 1e-5
 LOGP_ERR = 1e-5
 KINK_EPS = 1e-4
@@ -98,11 +109,18 @@ def branch_coefs(logp, old, ref, A, w, cfg):
     return [-s * w * (gp + cfg.kl_beta * gk) for gp in pgs for gk in kls]
 
 
+def l1_ratio(err, ref, ref_sq, floor, dtype):
+    """Row L1 check (module docstring): sum|d| / (L1_REL sum|want| + L1_DEV rel sqrt(sum want^2) + sum floor)."""
+    err = _arr(err)
+    den = DL_L1_REL[dtype] * _arr(ref) + L1_DEV * DL_REL[dtype] * np.sqrt(_arr(ref_sq)) + _arr(floor) + 1e-300
+    return np.where(err == 0, 0.0, err / den)
+
+
 def row_ratio(got, want, q, y, coef, dcoef, dtype, ent_mag=None):
     """max(elementwise ratio, L1 ratio) of one row; `want` = coef q (+ entropy term), q = p - onehot."""
     rel = DL_REL[dtype]
     aq = np.abs(q)
-    floor = dcoef * aq
+    floor = dcoef * aq + ABS_FLOOR
     floor[y] += abs(coef) * (q[y] + 1.0) * LOGP_ERR
     if ent_mag is not None:
         floor = floor + rel * ent_mag
@@ -111,8 +129,10 @@ def row_ratio(got, want, q, y, coef, dcoef, dtype, ent_mag=None):
     with np.errstate(divide="ignore", invalid="ignore"):
         r = np.where(d == 0, 0.0, d / tol)
     r = np.where(np.isnan(r), np.inf, r)
-    l1 = math.fsum(d) / (DL_L1_REL[dtype] * math.fsum(np.abs(want)) + math.fsum(floor) + 1e-300) \
-        if d.any() else 0.0
+    nt = np.ones(len(d), bool)
+    nt[y] = False
+    l1 = float(l1_ratio(math.fsum(d[nt]), math.fsum(np.abs(want[nt])), math.fsum(want[nt] * want[nt]),
+                        math.fsum(floor[nt]), dtype))
     return max(float(np.max(r)) if r.size else 0.0, l1)
 
 
@@ -179,11 +199,10 @@ def microbatch_parity(logits, targets, loss_mask, row_traj, adv, old, ref, n_los
         refc = None if ref is None else ref[r0:r1]
         dc = coef_error(o["row_coef"], o["logp"], old[r0:r1], refc if refc is not None else 0.0, A, w_tok, cfg)
         got = _host_rows(got_dlogits, r0, r1, dtype)
-        cmp = OC.dlogits_compare(bits, tg, m, s, o["row_lse"], o["row_coef"], dc, LOGP_ERR, DL_REL[dtype], got,
-                                 V=V)
+        cmp = OC.dlogits_compare(bits, tg, m, s, o["row_lse"], o["row_coef"], dc, LOGP_ERR, DL_REL[dtype],
+                                 ABS_FLOOR, got, V=V)
         el = cmp["max_ratio"]
-        l1 = cmp["l1_err"] / (DL_L1_REL[dtype] * cmp["l1_ref"] + cmp["l1_floor"] + 1e-300)
-        l1[cmp["l1_err"] == 0] = 0.0
+        l1 = l1_ratio(cmp["l1_err"], cmp["l1_ref"], cmp["l2_ref"], cmp["l1_floor"], dtype)
         bad = np.flatnonzero(tr & ((el > 1.0) | (l1 > 1.0)))
         for i in bad:   # a row on a clip / clamp boundary may carry the other branch's coefficient
             j = r0 + i
@@ -196,8 +215,8 @@ def microbatch_parity(logits, targets, loss_mask, row_traj, adv, old, ref, n_los
                 one = np.zeros(r1 - r0, np.uint8)
                 one[i] = 1
                 cc = OC.dlogits_compare(bits, tg, one, s, o["row_lse"], np.full(r1 - r0, c),
-                                        np.full(r1 - r0, dc[i]), LOGP_ERR, DL_REL[dtype], got, V=V)
-                li = cc["l1_err"][i] / (DL_L1_REL[dtype] * cc["l1_ref"][i] + cc["l1_floor"][i] + 1e-300)
+                                        np.full(r1 - r0, dc[i]), LOGP_ERR, DL_REL[dtype], ABS_FLOOR, got, V=V)
+                li = float(l1_ratio(cc["l1_err"][i], cc["l1_ref"][i], cc["l2_ref"][i], cc["l1_floor"][i], dtype))
                 if max(cc["max_ratio"][i], li) < max(best):
                     best = (cc["max_ratio"][i], li)
             el[i], l1[i] = best

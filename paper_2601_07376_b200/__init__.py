@@ -52,7 +52,8 @@ class otk_loss_cfg(C.Structure):
                 ("log_ratio_clamp", C.c_double), ("logit_scale", C.c_double), ("kl_type", C.c_int32),
                 ("zero_masked_rows", C.c_int32), ("accumulate_stats", C.c_int32), ("reserved", C.c_int32),
                 ("ent_coef", C.c_double), ("dual_clip", C.c_double), ("reduction", C.c_int32), ("sft", C.c_int32),
-                ("traj_loss_tokens", C.c_void_p), ("n_active_traj", C.c_void_p), ("adv_index", C.c_void_p)]
+                ("traj_loss_tokens", C.c_void_p), ("n_active_traj", C.c_void_p), ("adv_index", C.c_void_p),
+                ("num_adv", C.c_int64), ("num_traj", C.c_int64)]
 
 
 OTK_TOKEN_MEAN, OTK_SEQ_MEAN_TOKEN_MEAN, OTK_SEQ_MEAN_TOKEN_SUM = 0, 1, 2
@@ -69,6 +70,12 @@ OTK_IPC_HANDLE_BYTES = 64
 class otk_vpf_peers(C.Structure):
     _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("rows_cap", C.c_int64),
                 ("xchg", C.c_void_p * OTK_VPF_MAX_RANKS), ("max_ctas", C.c_int32)]
+
+
+class otk_vpf_rank_call(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("vocab_local", C.c_int64), ("logits", C.c_void_p), ("shard", otk_vocab_shard),
+                ("peers", C.POINTER(otk_vpf_peers)), ("dlogits", C.c_void_p), ("logp", C.c_void_p),
+                ("entropy", C.c_void_p), ("stats", C.c_void_p)]
 
 
 STATS_FIELDS = ("loss", "n_clipped", "kl_sum", "entropy_sum", "n_tokens")   # otk_loss_stats (5 doubles)
@@ -108,6 +115,8 @@ _sig = {
     "otk_policy_loss_fwd_bwd_vpf": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, _P, _P, _P, _P, _P,
                                               C.POINTER(otk_loss_cfg), C.POINTER(otk_vocab_shard),
                                               C.POINTER(otk_vpf_peers), _P, _P, _P, _P, _P]),
+    "otk_policy_loss_fwd_bwd_vpf_group": (C.c_int, [C.c_int32, C.POINTER(otk_vpf_rank_call), _I64, _I64, C.c_int,
+                                                    _P, _P, _P, _P, _P, _P, _P, C.POINTER(otk_loss_cfg), _P]),
     "otk_xchg_alloc": (C.c_int, [_P, _I64, C.POINTER(C.c_void_p)]),
     "otk_xchg_free": (C.c_int, [_P, _P]),
     "otk_ipc_get_handle": (C.c_int, [_P, _P]),
@@ -220,12 +229,15 @@ class LossCfg:
     n_active_traj: Optional[torch.Tensor] = None      # device i64 [1] (sequence-mean reductions, global)
     adv_index: Optional[torch.Tensor] = None          # device i32 [num_rows]: A_j = adv[adv_index[j]] (turn level)
 
-    def c(self, accumulate: Optional[bool] = None) -> otk_loss_cfg:
+    def c(self, accumulate: Optional[bool] = None, adv: Optional[torch.Tensor] = None) -> otk_loss_cfg:
+        """The C struct; `adv` (the advantage array of the call) gives num_adv, the kernels' index bound."""
         acc = self.accumulate_stats if accumulate is None else accumulate
         return otk_loss_cfg(self.clip_low, self.clip_high, self.kl_beta, self.log_ratio_clamp, self.logit_scale,
                             int(self.kl_type), int(bool(self.zero_masked_rows)), int(bool(acc)), 0,
                             float(self.ent_coef), float(self.dual_clip), int(self.reduction), int(bool(self.sft)),
-                            _ptr(self.traj_loss_tokens), _ptr(self.n_active_traj), _ptr(self.adv_index))
+                            _ptr(self.traj_loss_tokens), _ptr(self.n_active_traj), _ptr(self.adv_index),
+                            int(adv.numel()) if adv is not None else 0,
+                            int(self.traj_loss_tokens.numel()) if self.traj_loss_tokens is not None else 0)
 
 
 class Context:
@@ -512,7 +524,7 @@ def otk_policy_loss_fwd_bwd(ctx: Context, logits: torch.Tensor, targets: torch.T
     if stats is None:
         stats = torch.zeros(len(STATS_FIELDS), dtype=torch.float64, device=dev)
     _loss_args(logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss, cfg, dlogits, stats)
-    c = cfg.c(accumulate)
+    c = cfg.c(accumulate, adv)
     _check(_lib.otk_policy_loss_fwd_bwd(ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits), _ptr(targets),
                                         _ptr(loss_mask), _ptr(row_traj), _ptr(adv), _ptr(old_logp),
                                         _ptr(ref_logp), _ptr(n_loss), C.byref(c), _ptr(dlogits), _ptr(logp),
@@ -543,7 +555,7 @@ def otk_policy_loss_fwd_bwd_host(ctx: Context, logits: torch.Tensor, targets, lo
     if dlogits is not None:
         _host(dlogits, "dlogits", logits.dtype, N * ld)
     stats = (C.c_double * len(STATS_FIELDS))()
-    c = cfg.c(False)
+    c = cfg.c(False, adv)
     _check(_lib.otk_policy_loss_fwd_bwd_host(ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits), _ptr(targets),
                                              _ptr(loss_mask), _ptr(row_traj), int(adv.numel()), _ptr(adv),
                                              _ptr(old_logp), _ptr(ref_logp), int(n_loss), C.byref(c),
@@ -614,7 +626,7 @@ def otk_policy_loss_fwd_bwd_partials(ctx: Context, logits: torch.Tensor, targets
     if partials.dim() != 3 or partials.shape[1:] != (N, 4) or partials.dtype != torch.float32:
         raise ValueError("partials must be float32 [nshards, N, 4]")
     sh = otk_vocab_shard(int(vocab_start), int(vocab_total))
-    c = cfg.c(accumulate)
+    c = cfg.c(accumulate, adv)
     _check(_lib.otk_policy_loss_fwd_bwd_partials(
         ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits), _ptr(targets), _ptr(loss_mask), _ptr(row_traj),
         _ptr(adv), _ptr(old_logp), _ptr(ref_logp), _ptr(n_loss), C.byref(c), C.byref(sh), int(partials.shape[0]),
@@ -744,7 +756,7 @@ def otk_policy_loss_fwd_bwd_vpf(ctx: Context, logits: torch.Tensor, targets, los
     _arr(cfg.traj_loss_tokens, "cfg.traj_loss_tokens", torch.int64, None, dev, optional=True)
     _arr(cfg.n_active_traj, "cfg.n_active_traj", torch.int64, 1, dev, optional=True)
     sh = otk_vocab_shard(int(vocab_start), int(vocab_total))
-    c = cfg.c(accumulate)
+    c = cfg.c(accumulate, adv)
     peers = xchg.peers()
     st = _lib.otk_policy_loss_fwd_bwd_vpf(
         ctx.handle, N, V, ld, _dtype_code(logits), _ptr(logits), _ptr(targets), _ptr(loss_mask), _ptr(row_traj),
@@ -752,6 +764,63 @@ def otk_policy_loss_fwd_bwd_vpf(ctx: Context, logits: torch.Tensor, targets, los
         _ptr(dlogits), _ptr(logp), _ptr(entropy), _ptr(stats), _stream(stream))
     _check(st)
     return dict(dlogits=dlogits, logp=logp, entropy=entropy, stats=stats)
+
+
+def otk_policy_loss_fwd_bwd_vpf_group(ctxs, logits_shards, targets, loss_mask, row_traj, adv, old_logp, ref_logp,
+                                      n_loss, cfg: LossCfg, vocab_starts, vocab_total: int, xchgs, *,
+                                      dlogits=None, outs=None, accumulate: Optional[bool] = None,
+                                      stream=None) -> list:
+    """K4-VPF with P ranks EMULATED on this GPU in ONE cooperative launch (otk.h otk_policy_loss_fwd_bwd_vpf_group):
+    rank k = (ctxs[k], logits_shards[k] = column slice [vocab_starts[k], +width) of the rows, xchgs[k]). Every
+    rank's CTAs are resident together, so nothing depends on separate launches being co-scheduled. Returns one
+    dict per rank (dlogits, logp, entropy, stats), bitwise the per-rank calls' results."""
+    P = len(ctxs)
+    if not (len(logits_shards) == len(vocab_starts) == len(xchgs) == P):
+        raise ValueError("one logits shard, vocab start and exchange per rank")
+    N, ld = _row_view(logits_shards[0], "logits")
+    dev = logits_shards[0].device
+    res = []
+    for k in range(P):
+        lg = logits_shards[k]
+        n_k, ld_k = _row_view(lg, "logits")
+        if n_k != N or ld_k != ld or lg.dtype != logits_shards[0].dtype:
+            raise ValueError("every shard needs the same rows, row stride and dtype")
+        dl = dlogits[k] if dlogits is not None else torch.empty((N, max(ld, lg.shape[1])), dtype=lg.dtype,
+                                                                 device=dev)[:, :lg.shape[1]]
+        Nd, ldd = _row_view(dl, "dlogits")
+        if dl.shape != lg.shape or dl.dtype != lg.dtype or ldd != ld:
+            raise ValueError("dlogits must have the logits' shape, dtype and row stride")
+        o = dict(outs[k]) if outs is not None else dict(
+            logp=torch.empty(N, dtype=torch.float32, device=dev),
+            entropy=torch.empty(N, dtype=torch.float32, device=dev),
+            stats=torch.zeros(len(STATS_FIELDS), dtype=torch.float64, device=dev))
+        _arr(o["logp"], "logp", torch.float32, N, dev)
+        _arr(o["entropy"], "entropy", torch.float32, N, dev)
+        _arr(o["stats"], "stats", torch.float64, len(STATS_FIELDS), dev)
+        o["dlogits"] = dl
+        res.append(o)
+    _arr(targets, "targets", torch.int32, N, dev)
+    _arr(loss_mask, "loss_mask", torch.uint8, N, dev)
+    _arr(row_traj, "row_traj", torch.int32, N, dev)
+    _arr(adv, "adv", torch.float64, 1, dev, at_least=True)
+    _arr(old_logp, "old_logp", torch.float32, N, dev)
+    _arr(ref_logp, "ref_logp", torch.float32, N, dev, optional=True)
+    _arr(n_loss, "n_loss", torch.int64, 1, dev)
+    _arr(cfg.adv_index, "cfg.adv_index", torch.int32, N, dev, optional=True)
+    _arr(cfg.traj_loss_tokens, "cfg.traj_loss_tokens", torch.int64, None, dev, optional=True)
+    _arr(cfg.n_active_traj, "cfg.n_active_traj", torch.int64, 1, dev, optional=True)
+    peers = [x.peers() for x in xchgs]
+    calls = (otk_vpf_rank_call * P)()
+    for k in range(P):
+        o = res[k]
+        calls[k] = otk_vpf_rank_call(ctxs[k].handle.value, logits_shards[k].shape[1], _ptr(logits_shards[k]),
+                                     otk_vocab_shard(int(vocab_starts[k]), int(vocab_total)), C.pointer(peers[k]),
+                                     _ptr(o["dlogits"]), _ptr(o["logp"]), _ptr(o["entropy"]), _ptr(o["stats"]))
+    c = cfg.c(accumulate, adv)
+    _check(_lib.otk_policy_loss_fwd_bwd_vpf_group(P, calls, N, ld, _dtype_code(logits_shards[0]), _ptr(targets),
+                                                  _ptr(loss_mask), _ptr(row_traj), _ptr(adv), _ptr(old_logp),
+                                                  _ptr(ref_logp), _ptr(n_loss), C.byref(c), _stream(stream)))
+    return res
 
 
 __all__ = [n for n in list(globals()) if n.startswith("otk_") or n in (

@@ -28,6 +28,7 @@
 #include <cuda_fp16.h>
 
 #include <cfloat>
+#include <cstring>
 #include <mutex>
 #include <type_traits>
 
@@ -163,9 +164,12 @@ __device__ __forceinline__ Stat vpf_collect(const RowParams& p, int64_t row, flo
       if (!ok) {
         const uint64_t t0 = globaltimer_ns();
         while (!(ok = ready())) {
-          if (*reinterpret_cast<volatile int*>(p.err) != 0) break;  // an earlier timeout / error: give up at once
+          // only a peer timeout of THIS call ends the wait early (a data error elsewhere never does: every
+          // valid row still gets its peers' partials)
+          if (*reinterpret_cast<volatile uint32_t*>(p.vpf_abort) == ep) break;
           if (globaltimer_ns() - t0 > kVpfTimeoutNs) {
             set_error(p.err, OTK_ERR_PEER_TIMEOUT);
+            *reinterpret_cast<volatile uint32_t*>(p.vpf_abort) = ep;
             break;
           }
         }
@@ -180,6 +184,30 @@ __device__ __forceinline__ Stat vpf_collect(const RowParams& p, int64_t row, flo
   for (int q = 0; q < P; ++q)
     if (rec[q].w != -INFINITY) dy = __fadd_rn(rec[q].w, __fsub_rn(rec[q].x, tot.m));
   return tot;
+}
+
+// Before its first push a call (epoch ep) waits until every peer has completed call ep - 2: the records of call
+// ep go to the parity buffer that call ep - 2 read. Normally the wait is immediate (finishing call ep - 1 needed
+// the peers' records of ep - 1, so they were past ep - 2); it matters when call ep - 1 exchanged nothing (no
+// active rows) and a fast rank would otherwise overwrite records a slow peer is still reading. One thread per CTA.
+__device__ __forceinline__ void vpf_window(const RowParams& p, uint32_t ep) {
+  if (ep <= 2u) return;
+  const int64_t tail = int64_t(2) * p.vpf_rows_cap * p.vpf_nranks * 32;
+  for (int q = 0; q < p.vpf_nranks; ++q) {
+    if (q == p.vpf_rank) continue;
+    const volatile uint32_t* c =
+        reinterpret_cast<const volatile uint32_t*>(reinterpret_cast<const char*>(p.vpf_xchg[q]) + tail);
+    if (*c + 2u >= ep) continue;
+    const uint64_t t0 = globaltimer_ns();
+    while (*c + 2u < ep) {
+      if (*reinterpret_cast<volatile uint32_t*>(p.vpf_abort) == ep) return;
+      if (globaltimer_ns() - t0 > kVpfTimeoutNs) {
+        set_error(p.err, OTK_ERR_PEER_TIMEOUT);
+        *reinterpret_cast<volatile uint32_t*>(p.vpf_abort) = ep;
+        return;
+      }
+    }
+  }
 }
 
 // Called by one thread per CTA (ct == 0) after the CTA's (cluster's) row total: push (cluster rank 0 only),
@@ -495,6 +523,24 @@ __device__ __forceinline__ float row_weight(const RowParams& p, float invN, int6
   return nb > 0 ? float(1.0 / (double(nb) * double(nact))) : 0.f;
 }
 
+// A_j and n_b of a trainable row. An index outside adv (row_traj[j] or adv_index[j] vs num_adv) or outside
+// traj_tokens (sequence-mean reductions) is a data error: OTK_ERR_GROUP_RANGE (reported by `reporter`), and the
+// row is treated as loss-masked (weight 0: zero gradient, no stats, logp / entropy 0) — never read out of bounds.
+__device__ __forceinline__ bool row_side(const RowParams& p, int64_t row, int32_t rt, RowSide& sd, bool reporter) {
+  const int64_t ai = p.adv_index ? int64_t(p.adv_index[row]) : int64_t(rt);
+  const bool seq = p.reduction != OTK_TOKEN_MEAN;
+  const bool ok = ai >= 0 && ai < p.num_adv && (!seq || (rt >= 0 && int64_t(rt) < p.num_traj));
+  if (!ok) {
+    if (reporter) set_error(p.err, OTK_ERR_GROUP_RANGE);
+    sd.A = 0.0;
+    sd.nb = 0;
+    return false;
+  }
+  sd.A = p.adv[ai];
+  if (seq) sd.nb = p.traj_tokens[rt];
+  return true;
+}
+
 __device__ __forceinline__ LossOut loss_terms(const RowParams& p, float lp, float H, const RowSide& sd, float w) {
   const float C = float(p.clamp);
   bool clipped = false;
@@ -550,9 +596,11 @@ __device__ __forceinline__ LossOut loss_terms(const RowParams& p, float lp, floa
   return o;
 }
 
+// vblock / vgrid: the CTA's index and count within this call (a grouped launch hosts several calls)
 __device__ __forceinline__ void stats_epilogue(const RowParams& p, double acc_L, double acc_clip, double acc_kl,
-                                               double acc_H, double acc_n, int64_t nl, uint32_t vpf_ep = 0) {
-  double* part = p.cta_partials + size_t(blockIdx.x) * kStatSlots;
+                                               double acc_H, double acc_n, int64_t nl, unsigned vblock, unsigned vgrid,
+                                               uint32_t vpf_ep = 0) {
+  double* part = p.cta_partials + size_t(vblock) * kStatSlots;
   part[0] = acc_L;
   part[1] = acc_clip;
   part[2] = acc_kl;
@@ -560,10 +608,10 @@ __device__ __forceinline__ void stats_epilogue(const RowParams& p, double acc_L,
   part[4] = acc_n;
   __threadfence();
   const unsigned int t = atomicAdd(p.ticket, 1u);
-  if (t == gridDim.x - 1) {
+  if (t == vgrid - 1) {
     __threadfence();
     double tot[5] = {0, 0, 0, 0, 0};
-    for (unsigned int b = 0; b < gridDim.x; ++b) {
+    for (unsigned int b = 0; b < vgrid; ++b) {
       const volatile double* q2 = p.cta_partials + size_t(b) * kStatSlots;
       for (int k = 0; k < 5; ++k) tot[k] += q2[k];
     }
@@ -926,12 +974,13 @@ struct PipeRow {
   int32_t y;
   int ylc, owner;
   uint32_t q;
+  bool side_ok;
 };
 
 template <typename T, int MODE>
 __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8_t* ring, int warp, int lane,
                                               int csize, uint32_t crank, int64_t group, int64_t ngroups, int64_t c0,
-                                              int segn, int nch) {
+                                              int segn, int nch, unsigned vblock, unsigned vgrid) {
   constexpr bool kVpf = (MODE == kModeBwdVpf);
   using VT = Vec<T>;
   constexpr int EV = VT::EV;
@@ -949,6 +998,7 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
   const int64_t nact = p.reduction != OTK_TOKEN_MEAN ? *p.n_active : 0;
   uint32_t slot = 0, phase = 0, q = 0;
   const uint32_t vep = (kVpf && ct == 0) ? vpf_epoch(p) : 0u;  // read before this CTA takes its ticket
+  if (kVpf && ct == 0) vpf_window(p, vep);
 
   // ---- stage B: the previous row's statistics, loss and pass 2 -----------------------------------------
   auto stage_b = [&](const PipeRow& pr) {
@@ -978,15 +1028,17 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
       dy = b.w;
     }
     const RowStats rs = finalize(tot, dy);
-    const LossOut lo = loss_terms(p, rs.logp, rs.H, pr.sd, row_weight(p, invN, pr.sd.nb, nact));
+    const LossOut lo = loss_terms(p, rs.logp, rs.H, pr.sd, pr.side_ok ? row_weight(p, invN, pr.sd.nb, nact) : 0.f);
     if (ct == 0 && crank == 0) {
-      acc_L += double(lo.w) * double(lo.L);
-      acc_clip += lo.clipped ? 1.0 : 0.0;
-      acc_kl += double(lo.kl);
-      acc_H += double(rs.H);
-      acc_n += 1.0;
-      if (p.logp) p.logp[pr.row] = rs.logp;
-      if (p.entropy) p.entropy[pr.row] = rs.H;
+      if (pr.side_ok) {
+        acc_L += double(lo.w) * double(lo.L);
+        acc_clip += lo.clipped ? 1.0 : 0.0;
+        acc_kl += double(lo.kl);
+        acc_H += double(rs.H);
+        acc_n += 1.0;
+      }
+      if (p.logp) p.logp[pr.row] = pr.side_ok ? rs.logp : 0.f;
+      if (p.entropy) p.entropy[pr.row] = pr.side_ok ? rs.H : 0.f;
     }
     const uint32_t tm = tm0 + (pr.q & 1u) * kPipeHalf;
     char* drow = reinterpret_cast<char*>(p.dlogits) + (pr.row * p.ld + c0) * int64_t(sizeof(T));
@@ -1033,8 +1085,7 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
     }
     const int64_t ylc64 = int64_t(y) - p.vocab_start - c0;
     const int ylc = (ylc64 >= 0 && ylc64 < segn) ? int(ylc64) : -1;
-    sd.A = p.adv[p.adv_index ? p.adv_index[row] : rt];
-    if (p.reduction != OTK_TOKEN_MEAN) sd.nb = p.traj_tokens[rt];
+    const bool side_ok = row_side(p, row, rt, sd, ct == 0 && crank == 0);
     const uint32_t tm = tm0 + (q & 1u) * kPipeHalf;
 
     // ---------------- stage A: pass 1 into TMEM half (q & 1) (same arithmetic as the unpipelined loop)
@@ -1078,12 +1129,12 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
     }
     // ---------------- stage B of the previous row (its partials have had a whole pass 1 to arrive)
     if (has_prev) stage_b(prev);
-    prev = PipeRow{row, sd, r, xy, y, ylc, ylc >= 0 ? ((ylc % CE) / EV) % kNCT : -1, q};
+    prev = PipeRow{row, sd, r, xy, y, ylc, ylc >= 0 ? ((ylc % CE) / EV) % kNCT : -1, q, side_ok};
     has_prev = true;
     ++q;
   }
   if (has_prev) stage_b(prev);
-  if (ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl, vep);
+  if (ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl, vblock, vgrid, vep);
 }
 
 // =====================================================================================================
@@ -1092,8 +1143,8 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
 // running max after chunk c) and m_c are parked in TENSOR MEMORY, so pass 2 needs no second read of the
 // logits and no second exponential: softmax = e * 2^(m_c - lse).
 // =====================================================================================================
-template <typename T, int MODE, bool kPipe = false>
-__global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
+template <typename T, int MODE, bool kPipe>
+__device__ __forceinline__ void rows_tm_body(const RowParams& p, unsigned vblock, unsigned vgrid) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr bool kVpf = (MODE == kModeBwdVpf);  // BWD with the vocab-shard exchange fused in
   constexpr bool kBwd = (MODE == kModeBwd) || kVpf;
@@ -1111,8 +1162,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int csize = p.csize;
   const uint32_t crank = csize > 1 ? cluster_ctarank() : 0u;
-  const int64_t group = blockIdx.x / csize;
-  const int64_t ngroups = gridDim.x / csize;
+  const int64_t group = vblock / csize;
+  const int64_t ngroups = vgrid / csize;
   const int64_t c0 = int64_t(crank) * p.seg_elems;
   const int64_t c1 = min(p.vocab, c0 + int64_t(p.seg_elems));
   const int segn = c1 > c0 ? int(c1 - c0) : 0;
@@ -1132,7 +1183,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
     }
     __syncwarp();
   } else if constexpr (kPipe) {
-    consumer_pipe<T, MODE>(p, S, ring, warp, lane, csize, crank, group, ngroups, c0, segn, nch);
+    consumer_pipe<T, MODE>(p, S, ring, warp, lane, csize, crank, group, ngroups, c0, segn, nch, vblock, vgrid);
   } else {
     const int ct = threadIdx.x - 32;
     const int cw = warp - 1;
@@ -1152,6 +1203,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
     uint32_t slot = 0, phase = 0, q = 0;
     uint32_t fs = 0, fph = 0;  // FWD / PARTIAL: hand-off ring to the finalizer warp
     const uint32_t vep = (kVpf && ct == 0) ? vpf_epoch(p) : 0u;  // read before this CTA takes its ticket
+    if (kVpf && ct == 0) vpf_window(p, vep);
 
     int64_t row = group;
     int32_t y_n = 0, rt_n = 0;
@@ -1203,10 +1255,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       }
       const int64_t ylc64 = int64_t(y) - p.vocab_start - c0;  // target column local to this CTA's segment
       const int ylc = (ylc64 >= 0 && ylc64 < segn) ? int(ylc64) : -1;
-      if (kBwd) {  // consumed after pass 1
-        sd.A = p.adv[p.adv_index ? p.adv_index[row] : rt];
-        if (p.reduction != OTK_TOKEN_MEAN) sd.nb = p.traj_tokens[rt];
-      }
+      bool side_ok = true;
+      if (kBwd) side_ok = row_side(p, row, rt, sd, ct == 0 && crank == 0);  // consumed after pass 1
       const int64_t yg = int64_t(y) - p.vocab_start;
 
       // ---------------- pass 1: online max / sum 2^(y-m) / sum 2^(y-m)(y-m), one exponential per element
@@ -1278,15 +1328,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
             if (p.lse) p.lse[row] = rs.lse;
           }
         } else {
-          const LossOut lo = loss_terms(p, rs.logp, rs.H, sd, row_weight(p, invN, sd.nb, nact));
+          const LossOut lo = loss_terms(p, rs.logp, rs.H, sd, side_ok ? row_weight(p, invN, sd.nb, nact) : 0.f);
           if (ct == 0 && crank == 0) {
-            acc_L += double(lo.w) * double(lo.L);
-            acc_clip += lo.clipped ? 1.0 : 0.0;
-            acc_kl += double(lo.kl);
-            acc_H += double(rs.H);
-            acc_n += 1.0;
-            if (p.logp) p.logp[row] = rs.logp;
-            if (p.entropy) p.entropy[row] = rs.H;
+            if (side_ok) {
+              acc_L += double(lo.w) * double(lo.L);
+              acc_clip += lo.clipped ? 1.0 : 0.0;
+              acc_kl += double(lo.kl);
+              acc_H += double(rs.H);
+              acc_n += 1.0;
+            }
+            if (p.logp) p.logp[row] = side_ok ? rs.logp : 0.f;
+            if (p.entropy) p.entropy[row] = side_ok ? rs.H : 0.f;
           }
           // ---------------- pass 2: dlogits = e * (coef * 2^(m_c - lse)) from TMEM; the TMEM load of chunk
           // c+1 is in flight while chunk c is scaled and stored (two register sets, ping-pong, no copies)
@@ -1312,7 +1364,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
       atomicAdd(&g_phase[3], 1ull);
     }
 #endif
-    if (kBwd && ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl, vep);
+    if (kBwd && ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl, vblock, vgrid, vep);
   }
   tc_fence_before();
   if (csize > 1)
@@ -1323,6 +1375,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
     tc_fence_after();
     tmem_dealloc(S.tmem_base, 512);
   }
+}
+
+template <typename T, int MODE, bool kPipe = false>
+__global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
+  rows_tm_body<T, MODE, kPipe>(p, blockIdx.x, gridDim.x);
+}
+
+// K4-VPF ranks emulated on ONE GPU in ONE launch (otk_policy_loss_fwd_bwd_vpf_group): CTA block b runs call
+// b / blocks_per_set as its CTA b % blocks_per_set. Every rank's CTAs are resident together by construction
+// (cooperative launch, or a checked resident-cluster count), so the in-kernel exchange never waits on a rank
+// the hardware has not scheduled — unlike separate launches on separate streams, which CUDA does not co-schedule.
+struct RowParamsSet {
+  RowParams p[OTK_VPF_MAX_RANKS];
+  int nsets;
+  int blocks_per_set;
+};
+template <typename T, bool kPipe>
+__global__ void __launch_bounds__(kThreads, 1) k_rows_vpf_group(const __grid_constant__ RowParamsSet ps) {
+  const unsigned set = blockIdx.x / unsigned(ps.blocks_per_set);
+  rows_tm_body<T, kModeBwdVpf, kPipe>(ps.p[set], blockIdx.x - set * unsigned(ps.blocks_per_set),
+                                       unsigned(ps.blocks_per_set));
 }
 
 // =====================================================================================================
@@ -1387,17 +1460,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) 
       const Stat tot = combine_partials(p.partials_in + row, p.num_rows, p.nshards, dy);
       const RowStats rs = finalize(tot, dy);
       const int32_t rt = p.row_traj[row];
-      RowSide sd{p.adv[p.adv_index ? p.adv_index[row] : rt], p.old_logp[row], p.ref_logp ? p.ref_logp[row] : 0.f,
-                 p.reduction != OTK_TOKEN_MEAN ? p.traj_tokens[rt] : 0};
-      const LossOut lo = loss_terms(p, rs.logp, rs.H, sd, row_weight(p, invN, sd.nb, nact));
+      RowSide sd{0.0, p.old_logp[row], p.ref_logp ? p.ref_logp[row] : 0.f, 0};
+      const bool side_ok = row_side(p, row, rt, sd, ct == 0 && crank == 0);
+      const LossOut lo = loss_terms(p, rs.logp, rs.H, sd, side_ok ? row_weight(p, invN, sd.nb, nact) : 0.f);
       if (ct == 0 && crank == 0) {
-        acc_L += double(lo.w) * double(lo.L);
-        acc_clip += lo.clipped ? 1.0 : 0.0;
-        acc_kl += double(lo.kl);
-        acc_H += double(rs.H);
-        acc_n += 1.0;
-        if (p.logp) p.logp[row] = rs.logp;
-        if (p.entropy) p.entropy[row] = rs.H;
+        if (side_ok) {
+          acc_L += double(lo.w) * double(lo.L);
+          acc_clip += lo.clipped ? 1.0 : 0.0;
+          acc_kl += double(lo.kl);
+          acc_H += double(rs.H);
+          acc_n += 1.0;
+        }
+        if (p.logp) p.logp[row] = side_ok ? rs.logp : 0.f;
+        if (p.entropy) p.entropy[row] = side_ok ? rs.H : 0.f;
       }
       const float L2 = rs.L2, coef = lo.coef;
       char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
@@ -1441,7 +1516,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) 
       }
       ++q;
     }
-    if (ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl);
+    if (ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl, blockIdx.x, gridDim.x);
   }
   if (csize > 1) cluster_sync_all();
 }
@@ -1558,6 +1633,58 @@ cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const
     }
   }
   return cudaErrorInvalidValue;
+}
+
+// K4-VPF ranks emulated in one launch: blocks_per_set = the SMs / nsets (one CTA per SM, a multiple of the cluster
+// size), so the whole grid is one resident wave; csize 1 launches cooperatively (the driver refuses a grid that
+// cannot be co-resident), csize > 1 checks the resident-cluster count.
+cudaError_t launch_rows_vpf_group(const otk_ctx* ctx, otk_dtype dtype, const RowParams* ps, int nsets, bool pipe,
+                                  cudaStream_t s, int* grid_out) {
+  RowParamsSet set;
+  std::memset(&set, 0, sizeof(set));
+  if (nsets < 1 || nsets > OTK_VPF_MAX_RANKS) return cudaErrorInvalidValue;
+  for (int k = 0; k < nsets; ++k) set.p[k] = ps[k];
+  const int csize = ps[0].csize;
+  int64_t groups = int64_t(ctx->num_sms) / nsets / csize;
+  if (groups > ps[0].num_rows) groups = ps[0].num_rows;
+  if (groups < 1) groups = 1;
+  set.nsets = nsets;
+  set.blocks_per_set = int(groups * csize);
+  const int grid = set.blocks_per_set * nsets;
+  if (grid > ctx->num_sms) return cudaErrorCooperativeLaunchTooLarge;
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes));
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    if (csize > 1) {
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = csize;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(grid);
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      const int cap = max_resident_clusters(kern, ctx->device, csize, kSmemBytes, 1, cfg);
+      if (cap > 0 && grid / csize > cap) return cudaErrorCooperativeLaunchTooLarge;
+    } else {
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+    }
+    cfg.gridDim = dim3(grid);
+    if (grid_out) *grid_out = grid;
+    return cudaLaunchKernelEx(&cfg, kern, set);
+  };
+  if (dtype == OTK_BF16) {
+    using B = __nv_bfloat16;
+    return pipe ? go(k_rows_vpf_group<B, true>) : go(k_rows_vpf_group<B, false>);
+  }
+  return pipe ? go(k_rows_vpf_group<float, true>) : go(k_rows_vpf_group<float, false>);
 }
 
 // several partials of one row (e.g. the vocab chunks of the fused LM head on one rank) -> one partial of the

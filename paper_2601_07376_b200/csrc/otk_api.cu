@@ -86,6 +86,9 @@ otk_status check_cfg(const otk_loss_cfg* cfg, const float* ref_logp, int64_t num
   OTK_REQUIRE(cfg->reduction == OTK_TOKEN_MEAN || (cfg->traj_loss_tokens && cfg->n_active_traj), OTK_ERR_INVALID_ARG,
               "sequence-mean reductions need traj_loss_tokens and n_active_traj");
   OTK_REQUIRE(cfg->sft == 0 || cfg->sft == 1, OTK_ERR_INVALID_ARG, "sft must be 0 or 1");
+  OTK_REQUIRE(num_rows == 0 || cfg->num_adv >= 1, OTK_ERR_INVALID_ARG, "cfg->num_adv (elements of adv) must be >= 1");
+  OTK_REQUIRE(cfg->reduction == OTK_TOKEN_MEAN || num_rows == 0 || cfg->num_traj >= 1, OTK_ERR_INVALID_ARG,
+              "sequence-mean reductions need cfg->num_traj (elements of traj_loss_tokens) >= 1");
   return OTK_OK;
 }
 
@@ -131,6 +134,8 @@ void set_loss(otk::RowParams& p, const int32_t* row_traj, const double* adv, con
   p.traj_tokens = cfg->traj_loss_tokens;
   p.n_active = cfg->n_active_traj;
   p.adv_index = cfg->adv_index;
+  p.num_adv = cfg->num_adv;
+  p.num_traj = cfg->num_traj;
   p.zero_masked = cfg->zero_masked_rows;
   p.accumulate = cfg->accumulate_stats;
   p.dlogits = dlogits;
@@ -535,16 +540,19 @@ otk_status otk_policy_loss_fwd_bwd_partials(otk_ctx* ctx, int64_t num_rows, int6
 // ---- K4-VPF: (4) on a vocab shard with the row-partial exchange fused into the kernel -------------------
 int64_t otk_vpf_xchg_bytes(int64_t rows_cap, int32_t nranks) {
   if (rows_cap < 1 || nranks < 1 || nranks > OTK_VPF_MAX_RANKS) return -1;
-  return 2 * rows_cap * nranks * 32 + 64;  // [2][cap][P] records of four (value | epoch) words + call counter
+  return 2 * rows_cap * nranks * 32 + 64;  // [2][cap][P] records of four (value | epoch) words + tail: call
+                                            // counter (u32), abort epoch (u32)
 }
 
-otk_status otk_policy_loss_fwd_bwd_vpf(otk_ctx* ctx, int64_t num_rows, int64_t vocab_local, int64_t ld,
-                                       otk_dtype dtype, const void* logits, const int32_t* targets,
-                                       const uint8_t* loss_mask, const int32_t* row_traj, const double* adv,
-                                       const float* old_logp, const float* ref_logp, const int64_t* n_loss,
-                                       const otk_loss_cfg* cfg, const otk_vocab_shard* shard,
-                                       const otk_vpf_peers* peers, void* dlogits, float* logp, float* entropy,
-                                       otk_loss_stats* stats, otk_stream_t stream) {
+}  // extern "C"
+
+// One rank's K4-VPF call: host checks + its RowParams (shared by the single-call and the grouped entry points).
+static otk_status vpf_params(otk_ctx* ctx, int64_t num_rows, int64_t vocab_local, int64_t ld, otk_dtype dtype,
+                             const void* logits, const int32_t* targets, const uint8_t* loss_mask,
+                             const int32_t* row_traj, const double* adv, const float* old_logp, const float* ref_logp,
+                             const int64_t* n_loss, const otk_loss_cfg* cfg, const otk_vocab_shard* shard,
+                             const otk_vpf_peers* peers, void* dlogits, float* logp, float* entropy,
+                             otk_loss_stats* stats, otk::RowParams* out) {
   int csize = 0, seg = 0;
   otk_status st = check_rows(ctx, num_rows, vocab_local, ld, dtype, logits, targets, &csize, &seg);
   if (st != OTK_OK) return st;
@@ -575,6 +583,7 @@ otk_status otk_policy_loss_fwd_bwd_vpf(otk_ctx* ctx, int64_t num_rows, int64_t v
   p.vpf_nranks = peers->nranks;
   p.vpf_counter = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(peers->xchg[peers->rank]) +
                                               2 * peers->rows_cap * peers->nranks * 32);
+  p.vpf_abort = p.vpf_counter + 1;
   p.vpf_rows_cap = peers->rows_cap;
   // pipelined loop (exchange latency hidden behind the next row's pass 1) when a CTA holds the whole shard row
   // and two rows fit its tensor memory
@@ -582,10 +591,57 @@ otk_status otk_policy_loss_fwd_bwd_vpf(otk_ctx* ctx, int64_t num_rows, int64_t v
 #ifdef OTK_VPF_NOPIPE  // experiment builds only: measure the unpipelined loop
   p.pipe = 0;
 #endif
+  *out = p;
+  return OTK_OK;
+}
+
+extern "C" {
+
+otk_status otk_policy_loss_fwd_bwd_vpf(otk_ctx* ctx, int64_t num_rows, int64_t vocab_local, int64_t ld,
+                                       otk_dtype dtype, const void* logits, const int32_t* targets,
+                                       const uint8_t* loss_mask, const int32_t* row_traj, const double* adv,
+                                       const float* old_logp, const float* ref_logp, const int64_t* n_loss,
+                                       const otk_loss_cfg* cfg, const otk_vocab_shard* shard,
+                                       const otk_vpf_peers* peers, void* dlogits, float* logp, float* entropy,
+                                       otk_loss_stats* stats, otk_stream_t stream) {
+  otk::RowParams p;
+  otk_status st = vpf_params(ctx, num_rows, vocab_local, ld, dtype, logits, targets, loss_mask, row_traj, adv,
+                             old_logp, ref_logp, n_loss, cfg, shard, peers, dlogits, logp, entropy, stats, &p);
+  if (st != OTK_OK) return st;
   OTK_CUDA(otk::launch_rows(ctx, otk::kModeBwdVpf, dtype, p, reinterpret_cast<cudaStream_t>(stream), nullptr,
                             peers->max_ctas),
            "k_rows<bwd_vpf> launch");
   ctx->launches += 1;
+  return OTK_OK;
+}
+
+otk_status otk_policy_loss_fwd_bwd_vpf_group(int32_t nranks, const otk_vpf_rank_call* calls, int64_t num_rows,
+                                             int64_t ld, otk_dtype dtype, const int32_t* targets,
+                                             const uint8_t* loss_mask, const int32_t* row_traj, const double* adv,
+                                             const float* old_logp, const float* ref_logp, const int64_t* n_loss,
+                                             const otk_loss_cfg* cfg, otk_stream_t stream) {
+  OTK_REQUIRE(calls && nranks >= 1 && nranks <= OTK_VPF_MAX_RANKS, OTK_ERR_INVALID_ARG,
+              "need 1 <= nranks <= OTK_VPF_MAX_RANKS calls");
+  otk::RowParams ps[OTK_VPF_MAX_RANKS];
+  for (int k = 0; k < nranks; ++k) {
+    const otk_vpf_rank_call& c = calls[k];
+    OTK_REQUIRE(c.ctx && c.peers, OTK_ERR_INVALID_ARG, "every call needs a ctx and peers");
+    OTK_REQUIRE(c.peers->rank == k && c.peers->nranks == nranks, OTK_ERR_INVALID_ARG,
+                "calls[k] must be rank k of an nranks-rank exchange");
+    for (int q = 0; q < k; ++q)
+      OTK_REQUIRE(calls[q].ctx != c.ctx, OTK_ERR_INVALID_ARG, "every rank needs its own ctx (scratch, ticket)");
+    OTK_REQUIRE(c.ctx->device == calls[0].ctx->device, OTK_ERR_INVALID_ARG, "all ctxs must be on one device");
+    otk_status st = vpf_params(c.ctx, num_rows, c.vocab_local, ld, dtype, c.logits, targets, loss_mask, row_traj, adv,
+                               old_logp, ref_logp, n_loss, cfg, &c.shard, c.peers, c.dlogits, c.logp, c.entropy,
+                               c.stats, &ps[k]);
+    if (st != OTK_OK) return st;
+    OTK_REQUIRE(ps[k].csize == ps[0].csize && ps[k].pipe == ps[0].pipe, OTK_ERR_SHAPE,
+                "every rank's shard must use the same cluster size and loop (near-equal shard widths)");
+  }
+  OTK_CUDA(otk::launch_rows_vpf_group(calls[0].ctx, dtype, ps, nranks, ps[0].pipe != 0,
+                                      reinterpret_cast<cudaStream_t>(stream), nullptr),
+           "k_rows_vpf_group launch (all ranks co-resident)");
+  calls[0].ctx->launches += 1;
   return OTK_OK;
 }
 
@@ -645,7 +701,9 @@ otk_status otk_policy_loss_fwd_bwd_host(otk_ctx* ctx, int64_t num_rows, int64_t 
   int csize = 0, seg = 0;
   otk_status st = check_rows(ctx, num_rows, vocab, ld, dtype, logits_host, targets_host, &csize, &seg);
   if (st != OTK_OK) return st;
-  st = check_cfg(cfg, ref_logp_host, num_rows);
+  otk_loss_cfg hc = *cfg;
+  hc.num_adv = num_traj;
+  st = check_cfg(&hc, ref_logp_host, num_rows);
   if (st != OTK_OK) return st;
   OTK_REQUIRE(loss_mask_host && row_traj_host && adv_host && old_logp_host && stats_host && num_traj >= 1,
               OTK_ERR_INVALID_ARG, "a required host pointer is NULL");
@@ -720,6 +778,7 @@ otk_status otk_policy_loss_fwd_bwd_host(otk_ctx* ctx, int64_t num_rows, int64_t 
     OTK_CUDA(cudaStreamWaitEvent(xs, ctx->ev[b], 0), "wait ready");
     otk_loss_cfg c2 = *cfg;
     c2.accumulate_stats = 1;
+    c2.num_adv = num_traj;  // adv_host holds num_traj advantages
     st = otk_policy_loss_fwd_bwd(ctx, std::max<int64_t>(n, 0), vocab, ld, dtype, sb,
                                  reinterpret_cast<const int32_t*>(sb + off_tg),
                                  reinterpret_cast<const uint8_t*>(sb + off_m),

@@ -86,6 +86,8 @@ struct RowParams {
   const int64_t* traj_tokens;
   const int64_t* n_active;
   const int32_t* adv_index;  // NULL: adv[row_traj[row]]
+  int64_t num_adv;           // elements of adv (index bound)
+  int64_t num_traj;          // elements of traj_tokens (index bound, sequence-mean reductions)
   int kl_type;
   int zero_masked;
   int accumulate;
@@ -95,6 +97,7 @@ struct RowParams {
   void* vpf_xchg[OTK_VPF_MAX_RANKS];  // exchange buffer of every rank (peer-mapped), [vpf_rank] = own
   int vpf_rank, vpf_nranks;
   uint32_t* vpf_counter;  // calls completed on this buffer set (own buffer tail); epoch = counter + 1
+  uint32_t* vpf_abort;    // epoch of a call that hit a peer timeout (own buffer tail + 4): its later waits end
   int64_t vpf_rows_cap;
   // ctx scratch
   double* cta_partials;
@@ -105,6 +108,8 @@ struct RowParams {
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const RowParams& p, cudaStream_t s,
                         int* grid_out, int max_ctas = 0);
+cudaError_t launch_rows_vpf_group(const otk_ctx* ctx, otk_dtype dtype, const RowParams* ps, int nsets, bool pipe,
+                                  cudaStream_t s, int* grid_out);
 cudaError_t launch_combine(const otk_ctx* ctx, int64_t num_rows, int nshards, const float4* partials,
                            const uint8_t* row_mask, float* logp, float* entropy, float* lse, cudaStream_t s);
 

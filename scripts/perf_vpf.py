@@ -1,8 +1,10 @@
-"""Vocab-sharded fused loss on one math micro-batch, P ranks co-scheduled on ONE GPU (each rank: own ctx, stream,
-column shard and 148 // P CTAs), three ways (CUDA events around all ranks' work, 2 cycled input buffers):
+"""Vocab-sharded fused loss on one math micro-batch, P ranks emulated on ONE GPU (each rank: own ctx, column shard),
+three ways (CUDA events around all ranks' work, 2 cycled input buffers):
   unsharded : otk_policy_loss_fwd_bwd on the whole GPU (the reference point)
-  gathered  : per rank otk_row_partials -> (stack = the all-gather) -> otk_policy_loss_fwd_bwd_partials
-  vpf       : per rank otk_policy_loss_fwd_bwd_vpf (K4-VPF: the exchange inside the kernel)
+  gathered  : per rank otk_row_partials -> (stack = the all-gather) -> otk_policy_loss_fwd_bwd_partials (per-rank
+              streams; each launch may use every SM)
+  vpf       : otk_policy_loss_fwd_bwd_vpf_group (K4-VPF, the exchange inside the kernel): all ranks in ONE
+              cooperative launch, 148 // P CTAs per rank
 Throughput = logit rows of the micro-batch / time; GB/s = the unsharded algorithmic bytes / time.
 Usage: python scripts/perf_vpf.py [--rows 65536] [--iters 10] [--ranks 2 4]"""
 import argparse
@@ -79,7 +81,7 @@ for P in a.ranks:
     b = [V * k // P // 8 * 8 for k in range(P)] + [V]
     ctxs = [otk.Context(0) for _ in range(P)]
     streams = [torch.cuda.Stream() for _ in range(P)]
-    xs = otk.VpfExchange.local_group(ctxs, n, max_ctas=148 // P)
+    xs = otk.VpfExchange.local_group(ctxs, n)
     # the gathered path needs contiguous shards (its binding takes [N, vocab_local] tensors)
     shards = [[bufs[j][0][:, b[k]:b[k + 1]].contiguous() for k in range(P)] for j in range(2)]
     dls = [torch.empty_like(shards[0][k]) for k in range(P)]
@@ -87,12 +89,12 @@ for P in a.ranks:
     outs = [dict(logp=torch.empty(n, device="cuda"), entropy=torch.empty(n, device="cuda"),
                  stats=torch.zeros(5, dtype=torch.float64, device="cuda")) for _ in range(P)]
 
-    def vpf(k):
+    def vpf(k):   # all P ranks in one cooperative launch (k_rows_vpf_group)
         lg, tg = bufs[k % 2]
         o, r = olds[k % 2]
-        for q in range(P):
-            otk.otk_policy_loss_fwd_bwd_vpf(ctxs[q], lg[:, b[q]:b[q + 1]], tg, lm, rt, adv, o, r, nl, cfg, b[q], V,
-                                            xs[q], dlogits=dl[:, b[q]:b[q + 1]], stream=streams[q], **outs[q])
+        otk.otk_policy_loss_fwd_bwd_vpf_group(ctxs, [lg[:, b[q]:b[q + 1]] for q in range(P)], tg, lm, rt, adv, o, r,
+                                              nl, cfg, b[:P], V, xs, dlogits=[dl[:, b[q]:b[q + 1]] for q in range(P)],
+                                              outs=outs)
 
     def gathered(k):
         tg = bufs[k % 2][1]
@@ -112,7 +114,7 @@ for P in a.ranks:
     ms_v = timed(vpf, streams)
     for c in ctxs:
         c.check()
-    report("vpf", P, ms_v, max_ctas_per_rank=148 // P)
+    report("vpf", P, ms_v, ctas_per_rank=148 // P, launch="one grouped launch")
     ms_g = timed(gathered, streams)
     for c in ctxs:
         c.check()

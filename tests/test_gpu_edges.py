@@ -163,3 +163,59 @@ def test_targets_on_segment_boundaries(otk, ctx, dtype, V):
     dc = dcoef_rows(h, want["logp"], ocfg, n, 0.0)
     assert check_dlogits_rows(out["dlogits"], want["dlogits"], want["coef"], list(range(n)), dtype, V, dc, wide=wide,
                               targets=np.array(cols), h=h, cfg=ocfg) <= 1.0
+
+
+def test_adv_index_out_of_range_is_a_data_error(otk, ctx):
+    """a row whose row_traj (or adv_index) points outside adv is OTK_ERR_GROUP_RANGE, that row is treated
+    as loss-masked (zero gradient, logp 0, not counted), and every other row equals a call with valid indices."""
+    from tests.gpu_common import row_problem
+    n, V = 64, 4096
+    d, h = row_problem(n, V, seed=12, mask_p=1.0, B=4)
+    nl = torch.tensor([n], dtype=torch.int64, device="cuda")
+    good = otk.otk_policy_loss_fwd_bwd(ctx, d["logits"], d["targets"], d["mask"], d["row_traj"], d["adv"], d["old"],
+                                       d["ref"], nl, otk.LossCfg())
+    ctx.check()
+    for field in ("row_traj", "adv_index"):
+        rt = d["row_traj"].clone()
+        cfg = otk.LossCfg()
+        if field == "row_traj":
+            rt[9] = 4                                   # adv has 4 entries
+        else:
+            ai = d["row_traj"].clone()
+            ai[9] = -1
+            cfg = otk.LossCfg(adv_index=ai)
+        bad = otk.otk_policy_loss_fwd_bwd(ctx, d["logits"], d["targets"], d["mask"], rt, d["adv"], d["old"], d["ref"],
+                                          nl, cfg)
+        with pytest.raises(otk.OtkError, match="OTK_ERR_GROUP_RANGE"):
+            ctx.check()
+        assert bool((bad["dlogits"][9] == 0).all()) and float(bad["logp"][9]) == 0.0
+        keep = torch.ones(n, dtype=torch.bool, device="cuda")
+        keep[9] = False
+        assert torch.equal(bad["dlogits"][keep], good["dlogits"][keep])
+        assert torch.equal(bad["logp"][keep], good["logp"][keep])
+        assert otk.stats_dict(bad["stats"])["n_tokens"] == n - 1
+
+
+def test_host_entry_point_writes_vocab_columns_and_trainable_rows_only(otk, ctx):
+    """the host-buffer entry point writes only columns [0, vocab) of dlogits_host, and with
+    zero_masked_rows = 0 only the trainable rows (masked rows keep the caller's bytes)."""
+    from tests.gpu_common import row_problem
+    n, V, ld = 300, 1000, 1008
+    d, h = row_problem(n, V, ld=ld, seed=14)
+    N = int(h["mask"].sum())
+    hostd = {k: v.cpu().pin_memory() for k, v in d.items()}
+    for zero in (True, False):
+        cfg = otk.LossCfg(zero_masked_rows=zero)
+        dl_host = torch.full(d["logits"].shape, 7.0, dtype=d["logits"].dtype).pin_memory()
+        st = otk.otk_policy_loss_fwd_bwd_host(ctx, hostd["logits"], hostd["targets"], hostd["mask"], hostd["row_traj"],
+                                              hostd["adv"], hostd["old"], hostd["ref"], N, cfg, vocab=V,
+                                              dlogits=dl_host, rows_per_chunk=64)
+        dev = otk.otk_policy_loss_fwd_bwd(ctx, d["logits"], d["targets"], d["mask"], d["row_traj"], d["adv"],
+                                          d["old"], d["ref"], torch.tensor([N], dtype=torch.int64, device="cuda"),
+                                          otk.LossCfg(), vocab=V)
+        ctx.check()
+        assert bool((dl_host[:, V:] == 7.0).all())
+        m = torch.from_numpy(h["mask"]).bool()
+        assert torch.equal(dl_host[m, :V], dev["dlogits"][:, :V].cpu()[m])
+        assert bool((dl_host[~m, :V] == (0.0 if zero else 7.0)).all())
+        assert st["n_tokens"] == N

@@ -76,8 +76,8 @@ def test_fullsize_microbatch(otk, name):
 
 @pytest.mark.parametrize("P", [2, 4])
 def test_fullsize_vpf_microbatch(otk, P):
-    """K4-VPF at the bench's full size (one 65,536-row math micro-batch, V = 151936, P ranks co-scheduled on the
-    GPU in the perf_vpf.py launch configuration): sampled rows against the oracle, and every row against the
+    """K4-VPF at the bench's full size (one 65,536-row math micro-batch, V = 151936, P ranks emulated in one
+    grouped launch, as perf_vpf.py times it): sampled rows against the oracle, and every row against the
     unsharded kernel (logp 1e-5, dlogits within bf16 rounding, identical loss stats up to fp64 summation)."""
     cfgw = CONFIGS["math"]
     V, M, dev = cfgw.V, 65536, "cuda"
@@ -104,16 +104,13 @@ def test_fullsize_vpf_microbatch(otk, P):
     nl = torch.tensor([N], dtype=torch.int64, device=dev)
     cfg = otk.LossCfg(kl_beta=cfgw.kl_beta)
     ctxs = [otk.Context(0) for _ in range(P)]
-    streams = [torch.cuda.Stream() for _ in range(P)]
-    xchgs = otk.VpfExchange.local_group(ctxs, M, max_ctas=148 // P)
+    xchgs = otk.VpfExchange.local_group(ctxs, M)
     b = [V * k // P // 8 * 8 for k in range(P)] + [V]
     dl = torch.empty_like(logits)
     torch.cuda.synchronize()
-    res = []
-    for k in range(P):
-        res.append(otk.otk_policy_loss_fwd_bwd_vpf(ctxs[k], logits[:, b[k]:b[k + 1]], targets, d["mask"],
-                                                   d["row_traj"], d["adv"], d["old"], d["ref"], nl, cfg, b[k], V,
-                                                   xchgs[k], dlogits=dl[:, b[k]:b[k + 1]], stream=streams[k]))
+    res = otk.otk_policy_loss_fwd_bwd_vpf_group(ctxs, [logits[:, b[k]:b[k + 1]] for k in range(P)], targets,
+                                                d["mask"], d["row_traj"], d["adv"], d["old"], d["ref"], nl, cfg,
+                                                b[:P], V, xchgs, dlogits=[dl[:, b[k]:b[k + 1]] for k in range(P)])
     torch.cuda.synchronize()
     for c in ctxs:
         c.check()

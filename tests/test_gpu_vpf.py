@@ -1,13 +1,15 @@
 """K4-VPF (otk_policy_loss_fwd_bwd_vpf): the vocab-sharded fused loss with the row-partial exchange inside the
-kernel (-m gpu). P ranks are co-scheduled on the one GPU of the box — each rank its own ctx, stream, column
-shard (a column slice of one [N, V] buffer) and max_ctas = 148 // P CTAs, exchanging through plain device
-buffers instead of IPC-mapped peer buffers (the kernel code and the per-rank call are the multi-GPU ones).
+kernel (-m gpu). P ranks are emulated on the one GPU of the box in ONE cooperative launch
+(otk_policy_loss_fwd_bwd_vpf_group): each rank its own ctx, column shard (a column slice of one [N, V] buffer)
+and 148 // P CTAs, exchanging through plain device buffers instead of IPC-mapped peer buffers (the kernel code
+and the per-rank parameters are the multi-GPU ones). Every rank's CTAs are resident together, so the test never
+depends on separate launches being co-scheduled (which CUDA does not promise, and a profiler breaks).
 
 Checks: logp / entropy bitwise equal on every rank AND to the gathered path (otk_row_partials -> stack ->
 otk_policy_loss_fwd_bwd_partials: same partials, same rank-order combine); loss stats identical on every rank;
 everything within the north_star tolerances of the float64 oracle; repeated calls (epoch parity) and CUDA-graph
-replays (the epoch lives on the device) reproduce the same bits; a missing peer ends in OTK_ERR_PEER_TIMEOUT,
-not a hang."""
+replays (the epoch lives on the device) reproduce the same bits; a data error on one row leaves every other row
+exact; a missing peer ends in OTK_ERR_PEER_TIMEOUT, not a hang."""
 import numpy as np
 import pytest
 import torch
@@ -29,19 +31,16 @@ def _bounds(V, P):
 
 
 def _run_vpf(otk, ctxs, xchgs, streams, d, V, nl, cfg, dl, calls=1):
+    """`calls` consecutive grouped launches (all P ranks in one launch each); `streams` is unused (kept for the
+    call sites' symmetry with the per-rank form)."""
     P = len(ctxs)
     b = _bounds(V, P)
     torch.cuda.synchronize()
     outs = []
     for _ in range(calls):
-        res = []
-        for k in range(P):
-            with torch.cuda.stream(streams[k]):
-                res.append(otk.otk_policy_loss_fwd_bwd_vpf(
-                    ctxs[k], d["logits"][:, b[k]:b[k + 1]], d["targets"], d["mask"], d["row_traj"], d["adv"],
-                    d["old"], d["ref"], nl, cfg, b[k], V, xchgs[k], dlogits=dl[:, b[k]:b[k + 1]],
-                    stream=streams[k]))
-        outs.append(res)
+        outs.append(otk.otk_policy_loss_fwd_bwd_vpf_group(
+            ctxs, [d["logits"][:, b[k]:b[k + 1]] for k in range(P)], d["targets"], d["mask"], d["row_traj"],
+            d["adv"], d["old"], d["ref"], nl, cfg, b[:P], V, xchgs, dlogits=[dl[:, b[k]:b[k + 1]] for k in range(P)]))
         torch.cuda.synchronize()
     for c in ctxs:
         c.check()
@@ -166,8 +165,8 @@ def test_vpf_missing_peer_times_out(otk):
 
 
 def test_vpf_cuda_graph_replay(otk):
-    """Each rank's call captured in its own CUDA graph and replayed three times (each replay on its rank's
-    stream): the device-resident epoch advances per replay, so every replay reproduces the eager bits."""
+    """The grouped call captured in a CUDA graph and replayed three times: the device-resident epoch of every
+    rank advances per replay, so every replay reproduces the eager bits."""
     n, V, P = 96, 151936, 2
     d, h = row_problem(n, V, dtype="bf16", seed=21)
     ctxs = [otk.Context(0) for _ in range(P)]
@@ -180,23 +179,18 @@ def test_vpf_cuda_graph_replay(otk):
     eager = [{k: t.clone() for k, t in r.items() if k != "dlogits"} for r in eager]
     dl_eager = dl.clone()
     b = _bounds(V, P)
-    outs = [dict(logp=torch.empty(n, device="cuda"), entropy=torch.empty(n, device="cuda"),
-                 stats=torch.zeros(5, dtype=torch.float64, device="cuda")) for _ in range(P)]
-    graphs = [torch.cuda.CUDAGraph() for _ in range(P)]
+    graph = torch.cuda.CUDAGraph()
     torch.cuda.synchronize()
-    for k in range(P):
-        with torch.cuda.graph(graphs[k], stream=streams[k]):
-            otk.otk_policy_loss_fwd_bwd_vpf(ctxs[k], d["logits"][:, b[k]:b[k + 1]], d["targets"], d["mask"],
-                                            d["row_traj"], d["adv"], d["old"], d["ref"], nl, cfg, b[k], V, xchgs[k],
-                                            dlogits=dl[:, b[k]:b[k + 1]], **outs[k])
+    with torch.cuda.graph(graph):
+        outs = otk.otk_policy_loss_fwd_bwd_vpf_group(
+            ctxs, [d["logits"][:, b[k]:b[k + 1]] for k in range(P)], d["targets"], d["mask"], d["row_traj"],
+            d["adv"], d["old"], d["ref"], nl, cfg, b[:P], V, xchgs, dlogits=[dl[:, b[k]:b[k + 1]] for k in range(P)])
     for _ in range(3):
         dl.zero_()
         for o in outs:
             o["logp"].zero_()
         torch.cuda.synchronize()
-        for k in range(P):
-            with torch.cuda.stream(streams[k]):
-                graphs[k].replay()
+        graph.replay()
         torch.cuda.synchronize()
         for c in ctxs:
             c.check()
@@ -242,15 +236,31 @@ def test_vpf_edges(otk, case):
         e = dict(d, targets=bad)
         nl = torch.tensor([int(h["mask"].sum())], dtype=torch.int64, device="cuda")
         torch.cuda.synchronize()
-        for k in range(P):
-            otk.otk_policy_loss_fwd_bwd_vpf(ctxs[k], e["logits"][:, b[k]:b[k + 1]], e["targets"], e["mask"],
-                                            e["row_traj"], e["adv"], e["old"], e["ref"], nl, cfg, b[k], V, xchgs[k],
-                                            dlogits=dl[:, b[k]:b[k + 1]], stream=streams[k])
+        out = otk.otk_policy_loss_fwd_bwd_vpf_group(
+            ctxs, [e["logits"][:, b[k]:b[k + 1]] for k in range(P)], e["targets"], e["mask"], e["row_traj"],
+            e["adv"], e["old"], e["ref"], nl, cfg, b[:P], V, xchgs, dlogits=[dl[:, b[k]:b[k + 1]] for k in range(P)])
         torch.cuda.synchronize()
         for c in ctxs:
             with pytest.raises(otk.OtkError, match="OTK_ERR_TARGET_RANGE"):
                 c.check()
         assert bool((dl[j] == 0).all())
+        # the data error must not end the other rows' waits — every other row equals the gathered path
+        # on the same inputs (which also skips row j)
+        gctx = otk.Context(0)
+        parts = torch.stack([otk.otk_row_partials(gctx, e["logits"][:, b[k]:b[k + 1]].contiguous(), e["targets"],
+                                                  b[k], V, row_mask=e["mask"]) for k in range(P)]).contiguous()
+        g = otk.otk_policy_loss_fwd_bwd_partials(gctx, e["logits"][:, b[0]:b[1]].contiguous(), e["targets"],
+                                                 e["mask"], e["row_traj"], e["adv"], e["old"], e["ref"], nl, cfg,
+                                                 b[0], V, parts)
+        torch.cuda.synchronize()
+        with pytest.raises(otk.OtkError, match="OTK_ERR_TARGET_RANGE"):
+            gctx.check()
+        for k in range(P):
+            assert torch.equal(out[k]["logp"], g["logp"]) and torch.equal(out[k]["entropy"], g["entropy"])
+        assert torch.equal(dl[:, b[0]:b[1]], g["dlogits"])
+        sv, sg = otk.stats_dict(out[0]["stats"]), otk.stats_dict(g["stats"])
+        assert sv["n_tokens"] == sg["n_tokens"] == int(h["mask"].sum()) - 1
+        gctx.close()
         keep = ctxs   # they own the exchange buffers; fresh contexts for the next call (the error word is sticky)
         ctxs = [otk.Context(0) for _ in range(P)]
     # a normal call afterwards, same buffers: equal to the gathered path

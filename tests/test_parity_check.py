@@ -57,7 +57,7 @@ def test_rounded_oracle_passes_and_c_agrees():
     assert np.max(np.abs(o["row_lse"][mask == 1] - O.logprob_entropy_fwd(wide, y)["lse"][mask == 1])) < 1e-12
     dc = P.coef_error(o["row_coef"], o["logp"], old, ref, adv[rt], 1.0 / N, cfg)
     c = OC.dlogits_compare(OC.bf16_bits(lg), y, mask, 1.0, o["row_lse"], o["row_coef"], dc, P.LOGP_ERR,
-                           P.DL_REL["bf16"], OC.bf16_bits(got))
+                           P.DL_REL["bf16"], P.ABS_FLOOR, OC.bf16_bits(got))
     assert np.max(c["max_ratio"][mask == 1]) <= 0.51
     # the C helper's per-row ratio equals the Python one (same formula, independent loops)
     for j in rows:
@@ -65,7 +65,7 @@ def test_rounded_oracle_passes_and_c_agrees():
         q = p.copy()
         q[y[j]] -= 1.0
         rp = P.row_ratio(got[j].double().numpy(), want["dlogits"][j], q, int(y[j]), want["coef"][j], dc[j], "bf16")
-        l1 = c["l1_err"][j] / (P.DL_L1_REL["bf16"] * c["l1_ref"][j] + c["l1_floor"][j])
+        l1 = float(P.l1_ratio(c["l1_err"][j], c["l1_ref"][j], c["l2_ref"][j], c["l1_floor"][j], "bf16"))
         assert abs(max(c["max_ratio"][j], l1) - rp) <= 1e-9 * max(1.0, rp)
 
 
@@ -91,8 +91,11 @@ def test_single_wrong_element_fails():
 
 
 def test_systematic_row_bias_fails_l1_only():
+    """A 0.6 % bias of a whole row passes every element (< 2^-7) but fails the row L1 check (> 2^-8), on a row
+    whose gradient mass is spread (the uniform row: the Hoeffding term of the L1 bound is small there)."""
     lg, tg, wide, y, mask, rt, adv, old, ref, N, cfg, want = _problem()
-    j = int(np.flatnonzero(mask)[4])
+    j = 1                                         # the uniform row (make_logits uniform_rows=(1,))
+    assert mask[j]
     bad = want["dlogits"].astype(np.float32).copy()
     bad[j] *= 1.0 + 2.0 ** -7.4                  # below the per-element 2^-7, above the L1 2^-8
     got = torch.from_numpy(bad)
@@ -101,7 +104,7 @@ def test_systematic_row_bias_fails_l1_only():
     q[y[j]] -= 1.0
     dc = float(P.coef_error(want["coef"][j], lp, old[j], ref[j], adv[rt[j]], 1.0 / N, cfg))
     d = np.abs(bad[j].astype(np.float64) - want["dlogits"][j])
-    assert np.max(d / (P.DL_REL["bf16"] * np.abs(want["dlogits"][j]) + dc * np.abs(q) + 1e-300)) <= 1.0
+    assert np.max(d / (P.DL_REL["bf16"] * np.abs(want["dlogits"][j]) + dc * np.abs(q) + P.ABS_FLOOR)) <= 1.0
     assert P.row_ratio(got[j].double().numpy(), want["dlogits"][j], q, int(y[j]), want["coef"][j], dc, "bf16") > 1.0
 
 
@@ -142,3 +145,22 @@ def test_microbatch_parity_flow_on_cpu():
     bad[3, 0] = 1e-20                             # a masked row not exactly zero
     par = P.microbatch_parity(lg, tg, mask, rt, adv, old, ref, N, cfg, "bf16", 2048, lp, H, bad, st, chunk=16)
     assert par["masked_rows_nonzero"] == 1 and not P.parity_ok(par)
+
+
+def test_underflow_below_smallest_normal_is_tolerated():
+    """A logit 90 above the rest: the other elements' gradient (~1e-45) is below fp32 / bf16 normals and may flush to
+    0 (oracle/parity.py ABS_FLOOR); an element above that range set to 0 still fails."""
+    V = 1024
+    x = np.zeros(V)
+    x[5] = 90.0
+    lp, H, lse, p = O.row_forward(x, 7)
+    coef = -1e-5
+    q = p.copy()
+    q[7] -= 1.0
+    want = coef * q
+    got = want.copy()
+    got[np.abs(want) < 2.0 ** -126] = 0.0
+    assert (got == 0).sum() > 1000
+    assert P.row_ratio(got, want, q, 7, coef, 1e-10, "f32") <= 1.0
+    got[5] = 0.0
+    assert P.row_ratio(got, want, q, 7, coef, 1e-10, "f32") > 1.0
