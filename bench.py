@@ -5,9 +5,12 @@
 
 A step = otk_build_masks + otk_group_advantages + otk_policy_loss_fwd_bwd over every micro-batch of
 the batch (A3 runs fused inside A4), on BASELINE.json configs[1] ("math": 512 trajectories x T=2048,
-V=151936 bf16 logits, N = 2^20 rows) per GPU. Under torchrun (N > 1) each rank holds its own 512
-trajectories (weak scaling) and the step adds the batch-sharding exchanges (all-reduce of the token
-count, all-gather of group returns, all-reduce of the loss statistics).
+V=151936 bf16 logits, N = 2^20 rows). Under torchrun (N > 1) the default layout is STRONG scaling of that one
+global batch: dist.plan_batch_shards splits it into contiguous trajectory ranges balanced by HBM bytes (groups
+straddle ranks: game / marl group ids are strided), and the step adds the batch-sharding exchanges (all-reduce
+of the token count, all-gather of group returns so every rank computes the global group statistics, all-reduce
+of the loss statistics). --layout weak gives every rank its own batch of the config instead. `--config game
+--gpus 8` is BASELINE configs[2] (128 game trajectories batch-sharded over 8 GPUs).
 Prints ONE JSON line on rank 0 (schema: the driver's bench contract).
 """
 from __future__ import annotations
@@ -49,6 +52,10 @@ def parse():
                     help="skip the side measurements of the forward (3) and the SURVEY.md §8(f) rows")
     ap.add_argument("--vocab-ways", type=int, default=2,
                     help="--shard 2d / 2d-fused: vocab shards per row block (world = batch shards x vocab-ways)")
+    ap.add_argument("--layout", default="strong", choices=["strong", "weak"],
+                    help="batch sharding (N > 1): strong = ONE global batch of the config split into contiguous "
+                         "trajectory ranges by dist.plan_batch_shards (groups straddle ranks; total work fixed); "
+                         "weak = every rank its own batch of the config (rank-local groups)")
     ap.add_argument("--shard", default="batch", choices=["batch", "vocab", "vocab-fused", "2d", "2d-fused"],
                     help="batch: each rank owns whole trajectories (weak scaling); vocab: each rank owns V/N "
                          "columns of every row (strong scaling, row partials all-gathered); vocab-fused: the "
@@ -164,8 +171,18 @@ def build_workload(args, rank, world, device):
     L = shard_layout(args, world, rank)
     vocab_mode = args.shard != "batch"
     brank = L["b"]
-    tb = make_batch(args.config, seed=cfgw.seed + 1000 * brank)
-    tb.group_id = tb.group_id + np.int32(brank * cfgw.num_groups)   # this rank's groups (global ids)
+    strong = args.layout == "strong" and not vocab_mode
+    tb_full, plan, b0 = None, None, 0
+    if strong:   # one global batch, contiguous trajectory ranges balanced by HBM cost
+        from paper_2601_07376_b200.dist import plan_batch_shards, traj_costs
+        from synth import slice_batch
+        tb_full = make_batch(args.config)
+        plan = plan_batch_shards(traj_costs(tb_full, cfgw.V), world) if world > 1 else [(0, tb_full.num_traj)]
+        b0, b1 = plan[rank]
+        tb = slice_batch(tb_full, b0, b1)
+    else:
+        tb = make_batch(args.config, seed=cfgw.seed + 1000 * brank)
+        tb.group_id = tb.group_id + np.int32(brank * cfgw.num_groups)   # this rank's groups (global ids)
     N, V = tb.num_rows, cfgw.V
     v0, v1 = vocab_shard_bounds(V, L["Pv"])[L["v"]]
     Vl = v1 - v0
@@ -212,7 +229,8 @@ def build_workload(args, rank, world, device):
                               None if ref is None else ref.contiguous(), dlogits[:n]))
     ctx.check()
     return dict(otk=otk, cfgw=cfgw, tb=tb, ctx=ctx, dbatch=dbatch, gid=gid, toff=toff, trew=trew, bufs=bufs,
-                tgts=tgts, mbs=mbs, N=N, V=V, Vl=Vl, v0=v0, M=M, dlogits=dlogits, vshard=vshard, L=L)
+                tgts=tgts, mbs=mbs, N=N, V=V, Vl=Vl, v0=v0, M=M, dlogits=dlogits, vshard=vshard, L=L,
+                strong=strong, tb_full=tb_full, plan=plan, b0=b0)
 
 
 def algorithmic_bytes(V, n_train, n_masked, beta):
@@ -233,9 +251,15 @@ def run_otk(args):
     vocab_mode = args.shard != "batch"
     L = W["L"]
     bpg, nb, Pv = L["bg"], L["nb"], L["Pv"]
+    if W["strong"]:
+        counts = [e - s_ for s_, e in W["plan"]]
+        g_groups = cfgw.num_groups
+    else:
+        counts = [W["tb"].num_traj] * nb
+        g_groups = cfgw.num_groups * nb
     step = PolicyLossStep(ctx, W["dbatch"], W["gid"], cfgw.num_groups, W["toff"], W["trew"], W["Vl"], cfg,
-                          process_group=bpg, global_num_traj=[W["tb"].num_traj] * nb if bpg else None,
-                          global_num_groups=cfgw.num_groups * nb if bpg else None, vocab_shard=W["vshard"])
+                          process_group=bpg, global_num_traj=counts if bpg else None,
+                          global_num_groups=g_groups if bpg else None, vocab_shard=W["vshard"])
     stream = torch.cuda.current_stream()
     nmb = len(W["mbs"])
     # CUDA events around every loss launch of every timed step, on the launching stream
@@ -300,11 +324,21 @@ def run_otk(args):
     avg_ms = sum(k4_ms) / nmb
     achieved = avg_bytes / (avg_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
-    total_rows = W["N"] * nb
+    total_rows = W["tb_full"].num_rows if W["strong"] else W["N"] * nb
     value = total_rows / (ms_per_step * 1e-3)
     step_bytes = sum(bytes_k4)
+    per_rank = {"rows": [W["N"]], "GB": [step_bytes / 1e9], "trainable": [sum(n_train)], "ms_k4": [sum(k4_ms)]}
+    if pg is not None:   # this step's per-rank work (load balance of the shard plan)
+        import torch.distributed as dist
+        t = torch.tensor([W["N"], step_bytes / 1e9, sum(n_train), sum(k4_ms)], dtype=torch.float64, device=device)
+        allt = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        per_rank = {k: [float(a[i]) for a in allt] for i, k in enumerate(("rows", "GB", "trainable", "ms_k4"))}
+    imbalance = max(per_rank["GB"]) / (sum(per_rank["GB"]) / len(per_rank["GB"]))
     if world == 1:
         par = "single GPU" + (f" ({args.shard} path, 1 shard)" if vocab_mode else "")
+    elif W["strong"]:
+        par = f"batch-shard dp{world}: one global batch, contiguous trajectory ranges (dist.plan_batch_shards)"
     else:
         fused = " (K4-VPF)" if args.shard.endswith("-fused") else ""
         par = (f"batch-shard dp{nb} x vocab-shard tp{Pv}{fused}" if args.shard.startswith("2d")
@@ -312,10 +346,14 @@ def run_otk(args):
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if (nb == 1 and Pv > 1) or args.shard in ("vocab", "vocab-fused") else "weak",
+        "scaling": "strong" if (W["strong"] or (nb == 1 and Pv > 1) or args.shard in ("vocab", "vocab-fused"))
+                   else "weak",
         "vs_baseline": None, "dtype": cfgw.dtype, "data": "synthetic (seeded; SURVEY.md §8(d) recipe)",
         "config": {"workload": f"{args.config}: {cfgw.note}",
-                   "global_batch_traj": W["tb"].num_traj * nb,
+                   "global_batch_traj": W["tb_full"].num_traj if W["strong"] else W["tb"].num_traj * nb,
+                   "layout": ("strong: one global batch split by dist.plan_batch_shards (HBM-cost balanced "
+                              "contiguous trajectory ranges; groups span ranks)") if W["strong"] else
+                             ("weak: every rank its own batch" if not vocab_mode else args.shard),
                    "rows_per_gpu": W["N"], "vocab": W["V"], "vocab_per_gpu": W["Vl"], "micro_batch_rows": W["M"],
                    "micro_batches": nmb, "parallelism": par,
                    "l2": f"inputs >> L2: {len(W['bufs'])} logits buffers of "
@@ -328,6 +366,7 @@ def run_otk(args):
                      "traffic": None, "peak_source": peak_src,
                      "bytes_per_launch": avg_bytes, "avg_launch_ms": avg_ms,
                      "share_of_step": sum(k4_ms) / ms_per_step},
+        "per_rank": per_rank, "imbalance_bytes_max_over_mean": imbalance,
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
         "loss": stats["loss"], "n_loss": stats["n_tokens"],
@@ -503,7 +542,8 @@ def e2e(args, W, world, step, cfg):
     n_train = int(lm_h.sum().item())
     h2d = n_train * row_bytes + N * side_b + len(mbs) * (adv_h.numel() * 8 + 8)
     d2h = n_train * W["V"] * W["bufs"][0].element_size() + len(mbs) * 40
-    return {"value": N * world / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
+    total = W["tb_full"].num_rows if W["strong"] else N * world
+    return {"value": total / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
             "h2d_GBps": h2d / dt / 1e9, "d2h_GBps": d2h / dt / 1e9,
             "dlogits_returned_equal_device": match,
@@ -525,8 +565,15 @@ def cpu_baseline(args, W, cfg, seconds=None):
     mb = W["mbs"][0]
     m = O.build_masks(tb.tok_offsets, tb.seg_offsets, tb.seg_source, tb.seg_agent, tb.seg_len, tb.terminated,
                       traj_agent=tb.traj_agent)
-    adv = O.group_advantages(tb.group_id - tb.group_id.min(), O.episode_returns(tb.turn_offsets, tb.turn_rewards),
-                             cfgw.num_groups)["adv"]
+    if W["strong"]:   # this rank's shard of one global batch: global token count, group statistics over all ranks
+        tf = W["tb_full"]
+        m["n_loss"] = O.build_masks(tf.tok_offsets, tf.seg_offsets, tf.seg_source, tf.seg_agent, tf.seg_len,
+                                    tf.terminated, traj_agent=tf.traj_agent)["n_loss"]
+        adv = O.group_advantages(tf.group_id, O.episode_returns(tf.turn_offsets, tf.turn_rewards),
+                                 cfgw.num_groups)["adv"][W["b0"]:W["b0"] + tb.num_traj]
+    else:
+        adv = O.group_advantages(tb.group_id - tb.group_id.min(), O.episode_returns(tb.turn_offsets, tb.turn_rewards),
+                                 cfgw.num_groups)["adv"]
     ocfg = O.LossCfg(kl_beta=cfg.kl_beta)
     threads = os.cpu_count()
     done, ntrain, t_used, r0, block = 0, 0, 0.0, 0, 64
@@ -583,7 +630,7 @@ def parity_block(W, step, cfg, inp):
     otk, ctx, cfgw = W["otk"], W["ctx"], W["cfgw"]
     m, n = inp["masks"], inp["rows"]
     dev = W["bufs"][0].device
-    adv_gpu = step.adv_out["adv"].double().cpu().numpy()
+    adv_gpu = step.adv_used.double().cpu().numpy()
     out = {"masks_bit_exact": bool(np.array_equal(step.masks["loss_mask"].cpu().numpy(), m["loss_mask"])
                                    and np.array_equal(step.masks["row_traj"].cpu().numpy(), m["row_traj"])
                                    and int(step.masks["n_loss"].item()) == m["n_loss"]),

@@ -116,8 +116,9 @@ def l1_ratio(err, ref, ref_sq, floor, dtype):
     return np.where(err == 0, 0.0, err / den)
 
 
-def row_ratio(got, want, q, y, coef, dcoef, dtype, ent_mag=None):
-    """max(elementwise ratio, L1 ratio) of one row; `want` = coef q (+ entropy term), q = p - onehot."""
+def row_ratio(got, want, q, y, coef, dcoef, dtype, ent_mag=None, detail=None):
+    """max(elementwise ratio, L1 ratio) of one row; `want` = coef q (+ entropy term), q = p - onehot.
+    detail (a dict) receives the worst element (index, got, want, tol) and the L1 ratio, for diagnostics."""
     rel = DL_REL[dtype]
     aq = np.abs(q)
     floor = dcoef * aq + ABS_FLOOR
@@ -133,6 +134,10 @@ def row_ratio(got, want, q, y, coef, dcoef, dtype, ent_mag=None):
     nt[y] = False
     l1 = float(l1_ratio(math.fsum(d[nt]), math.fsum(np.abs(want[nt])), math.fsum(want[nt] * want[nt]),
                         math.fsum(floor[nt]), dtype))
+    if detail is not None and r.size:
+        v = int(np.argmax(r))
+        detail.update(elem=v, got=float(_arr(got)[v]), want=float(want[v]), tol=float(tol[v]),
+                      elem_ratio=float(r[v]), l1_ratio=l1, target=int(y), coef=float(coef))
     return max(float(np.max(r)) if r.size else 0.0, l1)
 
 

@@ -393,6 +393,7 @@ struct Smem {
   float4 rowbc[2];                    // (stream kernel) row broadcast
   float4 vbc[2];                      // (K4-VPF) the rank-order row total + dy, broadcast by thread 0
   uint32_t tmem_base;
+  long long load_row;                 // the loader's current row (zero-fill pacing; INT64_MAX when done)
 };
 constexpr int kZeroBytes = 4096;  // zero block: source of the bulk stores that zero-fill masked rows
 constexpr size_t kRingBytes = size_t(kSlots) * kChunkBytes;
@@ -423,6 +424,9 @@ __device__ __forceinline__ void load_rows(const RowParams& p, uint8_t* ring, Sme
       m_n = p.mask ? p.mask[nrow] : 1;
     }
     if (!row_active(p, y, m)) continue;
+#ifndef OTK_NO_ZERO_PACING
+    *reinterpret_cast<volatile long long*>(&S.load_row) = row;  // masked rows before this one may be zero-filled
+#endif
     const char* src = base + row * row_bytes;
     uint32_t off = 0;
     for (int c = 0; c < nch; ++c) {
@@ -437,13 +441,14 @@ __device__ __forceinline__ void load_rows(const RowParams& p, uint8_t* ring, Sme
       }
     }
   }
+  *reinterpret_cast<volatile long long*>(&S.load_row) = 0x7fffffffffffffffll;
 }
 
 // ---- zero-filler (warp 13, one thread): the dlogits segment of every inactive row is written with bulk
 // async shared->global stores from a zeroed 4 KB block — never read, never touched by the consumers ----------
 template <typename T>
-__device__ __forceinline__ void zero_rows(const RowParams& p, const uint8_t* zero, int64_t group, int64_t ngroups,
-                                          int64_t c0, int segn) {
+__device__ __forceinline__ void zero_rows(const RowParams& p, const uint8_t* zero, Smem& S, int64_t group,
+                                          int64_t ngroups, int64_t c0, int segn) {
   if (!p.zero_masked) return;
   const uint32_t zero_bytes = (uint32_t(segn) * uint32_t(sizeof(T))) & ~15u;  // 16-byte multiple part
   if (!zero_bytes) return;
@@ -455,6 +460,11 @@ __device__ __forceinline__ void zero_rows(const RowParams& p, const uint8_t* zer
     const int32_t y = p.targets[row];
     const uint8_t m = p.mask ? p.mask[row] : 1;
     if (row_active(p, y, m)) continue;
+#ifndef OTK_NO_ZERO_PACING
+    // paced by the loader: a masked row is zero-filled only once the loader has reached the rows around it, so
+    // DRAM sees the write-only rows interleaved with the read+write rows instead of a write burst up front
+    while (*reinterpret_cast<volatile long long*>(&S.load_row) < row) __nanosleep(128);
+#endif
     char* dst = dbase + row * row_bytes;
     for (uint32_t off = 0; off < zero_bytes; off += kZeroBytes)
       bulk_s2g(dst + off, zero, min(uint32_t(kZeroBytes), zero_bytes - off), pol);
@@ -648,6 +658,7 @@ __device__ __forceinline__ void row_kernel_setup(Smem& S, uint8_t* zero, int war
       mbar_init(&S.ffull[i], kConsumerWarps);
       mbar_init(&S.fempty[i], 1);
     }
+    S.load_row = -1;
     fence_mbar_init();
   }
   for (int i = threadIdx.x; i < kZeroBytes / 16; i += blockDim.x)
@@ -1177,7 +1188,7 @@ __device__ __forceinline__ void rows_tm_body(const RowParams& p, unsigned vblock
     __syncwarp();
   } else if (warp == kConsumerWarps + 1) {
     if (kBwd) {
-      if (lane == 0) zero_rows<T>(p, zero, group, ngroups, c0, segn);
+      if (lane == 0) zero_rows<T>(p, zero, S, group, ngroups, c0, segn);
     } else {
       finalize_rows<T, MODE>(p, S, lane, csize, crank, group, ngroups);
     }
@@ -1428,7 +1439,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) 
     if (lane == 0 && nch > 0) load_rows<T>(p, ring, S, group, ngroups, c0, seg_bytes, nch);
     __syncwarp();
   } else if (warp == kConsumerWarps + 1) {
-    if (lane == 0) zero_rows<T>(p, zero, group, ngroups, c0, segn);
+    if (lane == 0) zero_rows<T>(p, zero, S, group, ngroups, c0, segn);
     __syncwarp();
   } else {
     const int ct = threadIdx.x - 32;

@@ -259,6 +259,7 @@ class PolicyLossStep:
 
     def run(self, micro_batches: Sequence[MicroBatch], on_launch=None):
         adv = self.masks_and_advantages()
+        self.adv_used = adv          # the advantages this step's loss read (this rank's part under sharding)
         return self.loss(adv, micro_batches, on_launch)
 
 

@@ -6,11 +6,11 @@ random numbers and lays out trajectories; it holds none of the method's arithmet
 inputs (old/ref log-probs) are built by the caller from an implementation's output
 plus the noise drawn here.
 """
-from .trajectories import TrajBatch, make_batch, CONFIGS, WorkloadConfig, concat_batches, split_rows
+from .trajectories import TrajBatch, make_batch, CONFIGS, WorkloadConfig, concat_batches, slice_batch, split_rows
 from .logits import make_logits, make_noise, bf16_round
 from .lmhead import make_lmhead
 
 __all__ = [
-    "TrajBatch", "make_batch", "CONFIGS", "WorkloadConfig", "concat_batches", "split_rows",
+    "TrajBatch", "make_batch", "CONFIGS", "WorkloadConfig", "concat_batches", "slice_batch", "split_rows",
     "make_logits", "make_noise", "bf16_round", "make_lmhead",
 ]

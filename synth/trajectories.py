@@ -249,6 +249,22 @@ def concat_batches(parts: List[TrajBatch]) -> TrajBatch:
                  traj_agent=tag if has_ag else None)
 
 
+def slice_batch(tb: TrajBatch, b0: int, b1: int) -> TrajBatch:
+    """Trajectories [b0, b1) of a batch as a batch of their own (offsets rebased; group ids stay global) — one
+    rank's shard of a global batch under batch sharding (paper_2601_07376_b200.dist.plan_batch_shards)."""
+    s0, s1 = int(tb.seg_offsets[b0]), int(tb.seg_offsets[b1])
+    t0, t1 = int(tb.turn_offsets[b0]), int(tb.turn_offsets[b1])
+    r0 = int(tb.tok_offsets[b0])
+    return TrajBatch(tok_offsets=(tb.tok_offsets[b0:b1 + 1] - r0).astype(np.int64),
+                     seg_offsets=(tb.seg_offsets[b0:b1 + 1] - s0).astype(np.int32),
+                     seg_source=tb.seg_source[s0:s1].copy(), seg_agent=tb.seg_agent[s0:s1].copy(),
+                     seg_len=tb.seg_len[s0:s1].copy(), terminated=tb.terminated[b0:b1].copy(),
+                     traj_agent=None if tb.traj_agent is None else tb.traj_agent[b0:b1].copy(),
+                     turn_offsets=(tb.turn_offsets[b0:b1 + 1] - t0).astype(np.int32),
+                     turn_rewards=tb.turn_rewards[t0:t1].copy(), group_id=tb.group_id[b0:b1].copy(),
+                     num_groups=tb.num_groups, meta=dict(tb.meta, shard=(b0, b1)))
+
+
 def split_rows(num_rows: int, rows_per_chunk: int):
     """Row ranges [r0, r1) of the micro-batches a step is streamed in."""
     return [(r, min(r + rows_per_chunk, num_rows)) for r in range(0, num_rows, rows_per_chunk)]

@@ -98,7 +98,11 @@ def check_dlogits_rows(got, want, coef, rows, dtype, V, dcoef=None, logp_err=P.L
             if P.near_kink(lpj, h["old"][j], refj, A, cfg):
                 wj = (1.0 / max(int(h["mask"].sum()), 1)) if W is None else float(W[j])
                 cands += [(a, w + (a - c) * q) for a in P.branch_coefs(lpj, h["old"][j], refj, A, wj, cfg)]
-        best = min(P.row_ratio(g, wc, q, y, cc, P.COEF_REL * abs(cc) + logp_err * dslope, dtype, ent_mag)
-                   for cc, wc in cands)
+        dets = [dict() for _ in cands]
+        rs = [P.row_ratio(g, wc, q, y, cc, P.COEF_REL * abs(cc) + logp_err * dslope, dtype, ent_mag, dets[i])
+              for i, (cc, wc) in enumerate(cands)]
+        best = min(rs)
+        if best > 1.0:   # diagnostics of a failing row (pytest shows captured stdout on failure)
+            print(f"dlogits row {j}: ratio {best:.4g}", dets[int(np.argmin(rs))])
         worst = max(worst, best)
     return worst

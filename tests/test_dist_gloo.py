@@ -28,16 +28,8 @@ def _free_port():
 
 
 def _sub_batch(tb, b0, b1):
-    from synth.trajectories import TrajBatch
-    s0, s1 = int(tb.seg_offsets[b0]), int(tb.seg_offsets[b1])
-    t0, t1 = int(tb.turn_offsets[b0]), int(tb.turn_offsets[b1])
-    r0 = int(tb.tok_offsets[b0])
-    return TrajBatch(tok_offsets=tb.tok_offsets[b0:b1 + 1] - r0, seg_offsets=(tb.seg_offsets[b0:b1 + 1] - s0).astype(np.int32),
-                     seg_source=tb.seg_source[s0:s1], seg_agent=tb.seg_agent[s0:s1], seg_len=tb.seg_len[s0:s1],
-                     terminated=tb.terminated[b0:b1],
-                     traj_agent=None if tb.traj_agent is None else tb.traj_agent[b0:b1],
-                     turn_offsets=(tb.turn_offsets[b0:b1 + 1] - t0).astype(np.int32),
-                     turn_rewards=tb.turn_rewards[t0:t1], group_id=tb.group_id[b0:b1], num_groups=tb.num_groups)
+    from synth import slice_batch
+    return slice_batch(tb, b0, b1)
 
 
 def _worker(rank, world, port, config, q):
@@ -89,7 +81,8 @@ def _worker(rank, world, port, config, q):
         gathered = all_gather_vocab_partials(part)
         comb = [O.combine_partials([tuple(gathered[k, j].tolist()) for k in range(world)]) for j in range(5)]
         q.put(dict(rank=rank, n_loss=int(n_loss.item()), gid=gid_g.numpy(), ret=ret_g.numpy(), adv=adv_g,
-                   plan=plan, stats=stats.numpy(), L=L, comb=comb, X=X, Y=Y, tadv=tadv_g))
+                   plan=plan, stats=stats.numpy(), L=L, comb=comb, X=X, Y=Y, tadv=tadv_g,
+                   loss_mask=m_loc["loss_mask"], row_traj=m_loc["row_traj"] + b0, adv_loc=adv_g[b0:b1]))
     finally:
         dist.destroy_process_group()
 
@@ -114,6 +107,17 @@ def test_batch_and_vocab_sharding_gloo(config):
                          traj_agent=tb.traj_agent)
     R = O.episode_returns(tb.turn_offsets, tb.turn_rewards)
     adv = O.group_advantages(tb.group_id, R, tb.num_groups)["adv"]
+    # the shards' per-row labels, concatenated in rank order, are the unsharded ones (bit-exact), and every
+    # rank's advantages of its own trajectories equal the unsharded oracle's (groups straddle the ranks: game
+    # ids are b mod 16, marl agent * 8 + episode group)
+    assert np.array_equal(np.concatenate([r["loss_mask"] for r in res]), full["loss_mask"])
+    assert np.array_equal(np.concatenate([r["row_traj"] for r in res]), full["row_traj"])
+    assert np.max(np.abs(np.concatenate([r["adv_loc"] for r in res]) - O.group_advantages(
+        tb.group_id, O.episode_returns(tb.turn_offsets, tb.turn_rewards), tb.num_groups)["adv"])) <= 1e-6
+    if config == "game":
+        for g in range(tb.num_groups):            # every group really spans both ranks
+            members = np.flatnonzero(tb.group_id == g)
+            assert members.min() < res[0]["plan"][0][1] <= members.max()
     for r in res:
         assert r["n_loss"] == full["n_loss"]                       # global token count, bit-exact
         assert np.array_equal(r["gid"], tb.group_id)               # gathered in rank order

@@ -42,6 +42,34 @@ def test_lmhead_fwd_vs_oracle(otk, ctx, N, V, d, scale):
     assert err < TOL, err
 
 
+def test_lmhead_fwd_timed_shapes(otk, ctx):
+    """The shapes the bench and scripts/perf_lmhead.py time (d = 3584, V = 151936): N = 4097 (one full row block of
+    16 tiles + a 1-row block), 8192 (two full blocks), 16401 (four blocks + a 17-row block, a ragged last tile).
+    h is one seeded [16401, 3584] matrix and the launches take its first N rows, so a row's oracle value is the same
+    for every N. >= 64 rows per N, spread over every row block (first / last row of each block and tile-boundary
+    rows included), against O8 at 2e-3."""
+    V, d, Nmax = 151936, 3584, 16384 + 17
+    h, w, y = make_lmhead(Nmax, V, d, seed=2024, device="cuda")
+    block = 16 * 256                                            # row tiles per row block x rows per tile
+    cand = set(np.linspace(0, Nmax - 1, 72).astype(int).tolist())
+    for b0 in range(0, Nmax, block):
+        cand |= {b0, b0 + 1, b0 + 255, b0 + 256, min(b0 + block - 1, Nmax - 1)}
+    cand |= {4095, 4096, 8191, 8192, 16383, 16384, Nmax - 1}
+    rows = sorted(j for j in cand if j < Nmax)
+    want = O.lmhead_logprob_fwd(h.cpu().double().numpy(), w.cpu().double().numpy(), y.cpu().numpy(), rows=rows)
+    ws = None
+    for N in (4097, 8192, Nmax):
+        out = otk.otk_lmhead_logprob_fwd(ctx, h[:N], w, y[:N], want_lse=True, workspace=ws)
+        ws = out["workspace"]
+        ctx.check()
+        rn = [j for j in rows if j < N]
+        assert len(rn) >= 64
+        lp, H, lse = (out[k].cpu().numpy() for k in ("logp", "entropy", "lse"))
+        err = max(max(abs(lp[j] - want["logp"][j]), abs(H[j] - want["entropy"][j]), abs(lse[j] - want["lse"][j]))
+                  for j in rn)
+        assert err < TOL, (N, err)
+
+
 def test_lmhead_row_mask_and_matches_materialised_path(otk, ctx):
     """Masked rows give 0; unmasked rows agree with cuBLAS-materialised fp32 logits + the row kernel."""
     N, V, d = 384, 6000, 256

@@ -1,7 +1,11 @@
 """Policy loss through the LM head (step.LMHeadPolicyLoss: cuBLAS GEMMs around otk_policy_loss_fwd_bwd) vs the
 float64 oracle on the same bf16 h and W (-m gpu): loss within 1e-3 relative (the logits are rounded to bf16 before
-the loss, as in any bf16 head), dh and dW within 2e-2 in relative Frobenius norm (bf16 logits, bf16 dx, fp32
-accumulation over V = 4096 / N = 512 terms)."""
+the loss, as in any bf16 head), and dh, dW ELEMENT-WISE:
+    |d - ref| <= 2^-8 |ref| + 6 * 2^-8 * sqrt(sum_v (dx_jv W_vi)^2)      (dW: the same with h)
+dx carries independent per-element rounding errors (<= 2^-7 relative, mean ~2^-9) and a bf16 logit
+may round to the neighbouring value (fp32 vs float64 accumulation), so the error of a sum over V terms has a spread
+of ~2^-9 sqrt(sum (dx W)^2); the output is rounded once more to bf16 (2^-8 |ref|). 6 x 2^-8 is ~12 of those
+spreads; a CPU emulation of the roundings reached 0.40 of this bound."""
 import numpy as np
 import pytest
 import torch
@@ -43,8 +47,15 @@ def test_lmhead_policy_loss_vs_oracle():
     ctx.check()
     loss = otk.stats_dict(out["stats"])["loss"]
     assert abs(loss - want["loss"]) <= 1e-3 * max(abs(want["loss"]), 1e-3), (loss, want["loss"])
-    for got, ref_ in ((out["dh"], dh_ref), (out["dW"], dW_ref)):
+    W, H = w.double().numpy(), h.double().numpy()
+    for got, ref_, spread in ((out["dh"], dh_ref, np.sqrt((dx ** 2) @ (W ** 2))),
+                              (out["dW"], dW_ref, np.sqrt((dx.T ** 2) @ (H ** 2)))):
         g = got.double().cpu().numpy()
-        assert np.linalg.norm(g - ref_) <= 2e-2 * np.linalg.norm(ref_)
+        d_ = np.abs(g - ref_)
+        tol = 2.0 ** -8 * np.abs(ref_) + 6 * 2.0 ** -8 * spread
+        ratio = np.where(d_ == 0, 0.0, d_ / np.maximum(tol, 1e-300))
+        assert float(ratio.max()) <= 1.0, float(ratio.max())
+    # rows with loss mask 0 contribute nothing: their dh rows are exactly 0
+    assert bool((out["dh"][torch.from_numpy(mask == 0).to(dev)] == 0).all())
     assert set(out["ms"]) == {"logits_gemm", "loss_kernel", "grad_gemms"}
     ctx.close()

@@ -257,7 +257,10 @@ def test_vpf_edges(otk, case):
             gctx.check()
         for k in range(P):
             assert torch.equal(out[k]["logp"], g["logp"]) and torch.equal(out[k]["entropy"], g["entropy"])
-        assert torch.equal(dl[:, b[0]:b[1]], g["dlogits"])
+        # pass 2 differs in form (bf16 e from tensor memory x scale vs one fp32 exponential per element): the two
+        # agree within bf16 rounding on every row, and row j is zero in both
+        a_, g_ = dl[:, b[0]:b[1]].float(), g["dlogits"].float()
+        assert float(((a_ - g_).abs() / (g_.abs() * 2 ** -6 + 1e-30)).max()) <= 1.0
         sv, sg = otk.stats_dict(out[0]["stats"]), otk.stats_dict(g["stats"])
         assert sv["n_tokens"] == sg["n_tokens"] == int(h["mask"].sum()) - 1
         gctx.close()
