@@ -12,6 +12,8 @@
  *   (4) otk_policy_loss_fwd_bwd  PPO-clip + KL surrogate, token-mean, fused       north_star (4)
  *                                backward dlogits = coef * (softmax - onehot)
  *   LM head fused with (3) (NEXT-1, fwd): otk_lmhead_logprob_fwd — tcgen05 GEMM + log-softmax epilogue
+ *   LM head fused with (4) (NEXT-1, fwd + bwd): otk_lmhead_policy_loss_fwd_bwd — loss, dh, dW; the
+ *                                dlogits exist only as SMEM tiles inside the backward tcgen05 GEMMs
  *   rollout sampling (NEXT-3): otk_sample_tokens — softmax / greedy token per row
  *   vocab sharding (north_star "vocab-sharding logits with an all-reduce of row max and sum-exp"):
  *       otk_row_partials → (caller all-gathers partials) → otk_logprob_entropy_combine /
@@ -418,6 +420,38 @@ otk_status otk_lmhead_row_partials(otk_ctx* ctx, int64_t num_rows, int64_t hidde
                                    const void* hidden, const void* weight, const int32_t* targets,
                                    const uint8_t* row_mask, const otk_vocab_shard* shard, float logit_scale,
                                    void* workspace, int64_t workspace_bytes, float* partials, otk_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Policy loss and its gradients THROUGH the LM head (both halves; PAPER.md:188,
+ * the "parameter updates" pool; DESIGN.md §6 "LM head, backward"). With x = h W^T (bf16 logits) and
+ * (4) on x with cfg->logit_scale = s:
+ *   loss / stats / logp / entropy  exactly as otk_policy_loss_fwd_bwd on the bf16-rounded x,
+ *   dhidden = dx W   [num_rows, hidden_dim] bf16,    dweight = dx^T h   [vocab, hidden_dim] bf16,
+ * where dx = dL/dx (the dlogits of (4)) is formed tile by tile inside the two backward tcgen05 GEMMs from
+ * x and four per-row constants — it is never written to memory. Three tensor-core GEMMs (x, dh, dW) and
+ * two small kernels (chunk-partial combine + loss terms; dh split-K reduction), in this stream order.
+ * hidden: [num_rows, hidden_dim] bf16, weight: [vocab, hidden_dim] bf16 (row-major, 16-byte aligned);
+ * hidden_dim a multiple of 64; vocab a multiple of 8 (16-byte rows of x). targets, loss_mask, row_traj,
+ * adv, old_logp, ref_logp, n_loss, cfg as in otk_policy_loss_fwd_bwd (token-mean or sequence-mean
+ * reductions, all A4 variants; targets global ids in [0, vocab)).
+ * workspace: otk_lmhead_loss_workspace_bytes() bytes, 16-byte aligned, caller-owned: x rounded to bf16 (RNE)
+ * in 64 x 64 tiles [rows_pad/64][cols_pad/64][64][64] (rows_pad, cols_pad = num_rows, vocab rounded up to 256;
+ * contiguous 8 KB tiles for the backward's TMA), then chunk partials, per-row constants, dh split-K partials. dhidden / dweight: outputs, bf16, must not alias any input. logp / entropy: NULL or
+ * [num_rows] f32 (loss-masked rows 0). stats: device otk_loss_stats (accumulated if cfg->accumulate_stats).
+ * Errors: host-checkable ones return at once; a target out of range sets OTK_ERR_TARGET_RANGE and an index
+ * out of range OTK_ERR_GROUP_RANGE (those rows are treated as loss-masked: zero gradient).
+ * Tolerance vs the float64 oracle on the same bf16 h and W (tests/test_gpu_lmhead_loss.py): loss 1e-3
+ * relative; dh, dW element-wise 2^-8 |ref| + 6 * 2^-8 * sqrt(sum_v (dx_jv W_vi)^2).
+ * ------------------------------------------------------------------------------------------- */
+int64_t otk_lmhead_loss_workspace_bytes(const otk_ctx* ctx, int64_t num_rows, int64_t hidden_dim,
+                                        int64_t vocab); /* -1: bad args */
+otk_status otk_lmhead_policy_loss_fwd_bwd(otk_ctx* ctx, int64_t num_rows, int64_t hidden_dim, int64_t vocab,
+                                          const void* hidden, const void* weight, const int32_t* targets,
+                                          const uint8_t* loss_mask, const int32_t* row_traj, const double* adv,
+                                          const float* old_logp, const float* ref_logp, const int64_t* n_loss,
+                                          const otk_loss_cfg* cfg, void* workspace, int64_t workspace_bytes,
+                                          void* dhidden, void* dweight, float* logp, float* entropy,
+                                          otk_loss_stats* stats, otk_stream_t stream);
 
 /* Harness helper (not on the path): number of kernel launches the library issued since ctx creation. */
 int64_t otk_ctx_launch_count(const otk_ctx* ctx);

@@ -250,3 +250,63 @@ def parity_ok(p):
     return (p["logp_ratio"] <= 1 and p["entropy_ratio"] <= 1 and p["dlogits_elem_ratio"] <= 1
             and p["dlogits_l1_ratio"] <= 1 and p["loss_ratio"] <= 1 and p["masked_rows_nonzero"] == 0
             and p["n_tokens_exact"] and abs(p["n_clipped"] - p["n_clipped_oracle"]) <= p["kink_rows"])
+
+
+# ------------------------------------------------------------------------------------------------
+# LM head (NEXT-1): dh / dW tolerance from ambiguous bf16 roundings of the logits (R38)
+# ------------------------------------------------------------------------------------------------
+def bf16_ulp(x):
+    """Spacing of bf16 numbers at |x| (8 significant bits): 2^(floor(log2|x|) - 7); the smallest normal's below."""
+    ax = np.maximum(np.abs(_arr(x)), 2.0 ** -126)
+    return np.exp2(np.floor(np.log2(ax)) - 7.0)
+
+
+def lmhead_flip_tolerance(h, W, x64, xb, y, coef, logp, old, ref, A, w_row, cfg, mask, acc_terms=None):
+    """Extra absolute tolerance of dh = dx W and dW = dx^T h where the device's bf16 logits may differ from the
+    oracle's by one bf16 rounding (R38).
+
+    The oracle rounds x64 = h W^T (float64) to bf16 (xb); the device rounds an fp32 accumulation of the same bf16
+    products, whose error is at most d 2^-24 sum_k |h_jk W_vk| (recursive fp32 summation, round to nearest). Where
+    x64 lies that close to a bf16 rounding midpoint either neighbour is a correct logit (as either branch of a clip
+    kink is a correct coefficient), and dx moves by first-order amounts that the rounding spread of the element-wise
+    check does not cover — one flipped element can dominate a column of dW. Bound, per ambiguous (j, v) with
+    Delta = the other neighbour - xb:
+      dx_jv itself:       |coef_j| p_jv |expm1(s Delta)|                    (delta_jv)
+      the row's lse:      |coef_j| p_jv' rho_j for every v',  rho_j = sum_v p_jv |expm1(s Delta_jv)|
+      the coefficient:    |dcoef_j / dlogp_j| s sum_v |Delta_jv| (p_jv + [v = y_j]) |p_jv' - [v' = y_j]|
+    each pushed through |W| (dh) or |h| (dW), the sum scaled by 1.5 for second-order terms. Returns
+    (tol_dh [N, d], tol_dW [V, d], number of ambiguous logits, the ambiguity mask). acc_terms overrides d in the
+    accumulation bound (tests widen it to exercise many flips)."""
+    h, W, x64, xb = _arr(h), _arr(W), _arr(x64), _arr(xb)
+    N, d = h.shape
+    s = cfg.logit_scale
+    eps = (d if acc_terms is None else acc_terms) * 2.0 ** -24 * (np.abs(h) @ np.abs(W).T)
+    u = bf16_ulp(xb)
+    side = np.where(x64 >= xb, 1.0, -1.0)
+    mid = xb + side * u / 2
+    amb = np.abs(x64 - mid) <= eps
+    delta = np.where(amb, side * u, 0.0)
+    z = s * xb
+    z = z - z.max(axis=1, keepdims=True)
+    P = np.exp(z)
+    P /= P.sum(axis=1, keepdims=True)
+    em = np.abs(np.expm1(s * delta))
+    ac = np.abs(_arr(coef))[:, None]
+    prim = ac * P * em
+    rho = (P * em).sum(axis=1)
+    onehot = np.zeros_like(P)
+    onehot[np.arange(N), np.asarray(y)] = 1.0
+    dlp = s * (np.abs(delta) * (P + onehot)).sum(axis=1)
+    sens = abs(s) * np.abs(_arr(w_row)) * g_sensitivity(logp, old, ref if cfg.kl_beta else 0.0, A, cfg)
+    dco = sens * dlp
+    ent = getattr(cfg, "ent_coef", 0.0)
+    if ent:   # the entropy-bonus part w c_H s p (ln p + H) of dx moves with p as well
+        with np.errstate(divide="ignore"):
+            lnP = np.where(P > 0, np.log(np.where(P > 0, P, 1.0)), 0.0)
+        Hrow = -(P * lnP).sum(axis=1, keepdims=True)
+        prim = prim + np.abs(_arr(w_row) * ent * s)[:, None] * P * (np.abs(lnP) + Hrow + 1.0) * em
+    m = (_arr(mask) != 0)[:, None]
+    E = m * (prim + (ac[:, 0] * rho)[:, None] * P + dco[:, None] * np.abs(P - onehot))
+    tol_dh = 1.5 * (E @ np.abs(W))
+    tol_dW = 1.5 * (E.T @ np.abs(h))
+    return tol_dh, tol_dW, int(amb.sum()), amb

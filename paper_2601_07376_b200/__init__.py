@@ -104,6 +104,9 @@ _sig = {
     "otk_lmhead_logprob_fwd": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _P, C.c_float, _P, _I64, _P, _P, _P, _P]),
     "otk_lmhead_row_partials": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _P, C.POINTER(otk_vocab_shard), C.c_float,
                                           _P, _I64, _P, _P]),
+    "otk_lmhead_loss_workspace_bytes": (_I64, [_P, _I64, _I64, _I64]),
+    "otk_lmhead_policy_loss_fwd_bwd": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                                 C.POINTER(otk_loss_cfg), _P, _I64, _P, _P, _P, _P, _P, _P]),
     "otk_sample_tokens": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, C.c_float, C.c_int32, _P, _P, _P]),
     "otk_row_partials": (C.c_int, [_P, _I64, _I64, _I64, C.c_int, _P, _P, _P, C.POINTER(otk_vocab_shard),
                                    C.c_float, _P, _P]),
@@ -179,8 +182,14 @@ def _arr(t: Optional[torch.Tensor], name: str, dtype, numel: Optional[int], devi
 
 
 def _loss_args(logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss, cfg, dlogits, stats):
-    N = logits.shape[0]
-    dev = logits.device
+    _side_args(logits.shape[0], logits.device, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss, cfg,
+               stats)
+    _dev(dlogits, "dlogits")
+    if dlogits.shape != logits.shape or dlogits.dtype != logits.dtype:
+        raise ValueError("dlogits must have the logits' shape and dtype")
+
+
+def _side_args(N, dev, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss, cfg, stats):
     _arr(targets, "targets", torch.int32, N, dev)
     _arr(loss_mask, "loss_mask", torch.uint8, N, dev)
     _arr(row_traj, "row_traj", torch.int32, N, dev)
@@ -192,9 +201,6 @@ def _loss_args(logits, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_
     _arr(cfg.adv_index, "cfg.adv_index", torch.int32, N, dev, optional=True)
     _arr(cfg.traj_loss_tokens, "cfg.traj_loss_tokens", torch.int64, None, dev, optional=True)
     _arr(cfg.n_active_traj, "cfg.n_active_traj", torch.int64, 1, dev, optional=True)
-    _dev(dlogits, "dlogits")
-    if dlogits.shape != logits.shape or dlogits.dtype != logits.dtype:
-        raise ValueError("dlogits must have the logits' shape and dtype")
 
 
 def _stream(stream) -> Optional[int]:
@@ -415,6 +421,62 @@ def otk_lmhead_logprob_fwd(ctx: Context, hidden: torch.Tensor, weight: torch.Ten
                                        _ptr(o["entropy"]), _ptr(o.get("lse")), _stream(stream)))
     o["workspace"] = workspace
     return o
+
+
+def otk_lmhead_policy_loss_fwd_bwd(ctx: Context, hidden: torch.Tensor, weight: torch.Tensor, targets: torch.Tensor,
+                                   loss_mask: torch.Tensor, row_traj: torch.Tensor, adv: torch.Tensor,
+                                   old_logp: torch.Tensor, ref_logp: Optional[torch.Tensor], n_loss: torch.Tensor,
+                                   cfg: LossCfg = LossCfg(), *, workspace: Optional[torch.Tensor] = None,
+                                   dhidden: Optional[torch.Tensor] = None, dweight: Optional[torch.Tensor] = None,
+                                   want_logp: bool = True, stats: Optional[torch.Tensor] = None,
+                                   accumulate: Optional[bool] = None, stream=None) -> dict:
+    """Loss, dh and dW through the LM head, x = hidden @ weight.T (otk.h NEXT-1 fwd + bwd). workspace / dhidden /
+    dweight are reused when passed; lmhead_x_from_workspace() reads the bf16 x the call left in the workspace."""
+    for t, n in ((hidden, "hidden"), (weight, "weight")):
+        _dev(t, n)
+    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise ValueError("hidden and weight must be bfloat16")
+    N, d = hidden.shape
+    V, d2 = weight.shape
+    if d != d2:
+        raise ValueError("hidden / weight inner dimensions differ")
+    dev = hidden.device
+    if dhidden is None:
+        dhidden = torch.empty_like(hidden)
+    if dweight is None:
+        dweight = torch.empty_like(weight)
+    for t, n, shp in ((dhidden, "dhidden", (N, d)), (dweight, "dweight", (V, d))):
+        _dev(t, n)
+        if tuple(t.shape) != shp or t.dtype != torch.bfloat16:
+            raise ValueError(f"{n} must be bfloat16 {shp}")
+    if stats is None:
+        stats = torch.zeros(len(STATS_FIELDS), dtype=torch.float64, device=dev)
+    logp = torch.empty(N, dtype=torch.float32, device=dev) if want_logp else None
+    entropy = torch.empty(N, dtype=torch.float32, device=dev) if want_logp else None
+    _side_args(N, dev, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss, cfg, stats)
+    nbytes = int(_lib.otk_lmhead_loss_workspace_bytes(ctx.handle, N, d, V))
+    if nbytes < 0:
+        raise ValueError("bad LM-head loss shapes")
+    if workspace is None or workspace.numel() * workspace.element_size() < nbytes:
+        workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+    c = cfg.c(accumulate, adv)
+    _check(_lib.otk_lmhead_policy_loss_fwd_bwd(ctx.handle, N, d, V, _ptr(hidden), _ptr(weight), _ptr(targets),
+                                               _ptr(loss_mask), _ptr(row_traj), _ptr(adv), _ptr(old_logp),
+                                               _ptr(ref_logp), _ptr(n_loss), C.byref(c), _ptr(workspace),
+                                               workspace.numel() * workspace.element_size(), _ptr(dhidden),
+                                               _ptr(dweight), _ptr(logp), _ptr(entropy), _ptr(stats),
+                                               _stream(stream)))
+    return dict(workspace=workspace, dh=dhidden, dW=dweight, logp=logp, entropy=entropy, stats=stats,
+                shape=(N, V))
+
+
+def lmhead_x_from_workspace(out: dict) -> torch.Tensor:
+    """The bf16 x = h W^T that otk_lmhead_policy_loss_fwd_bwd left at the start of its workspace, un-tiled to
+    [N, V] (a copy; otk.h: 64 x 64 tiles [rows_pad/64][cols_pad/64][64][64])."""
+    N, V = out["shape"]
+    rp, cp = (N + 255) // 256 * 256, (V + 255) // 256 * 256
+    t = out["workspace"][: rp * cp * 2].view(torch.bfloat16).view(rp // 64, cp // 64, 64, 64)
+    return t.permute(0, 2, 1, 3).reshape(rp, cp)[:N, :V].contiguous()
 
 
 def otk_lmhead_row_partials(ctx: Context, hidden: torch.Tensor, weight_shard: torch.Tensor, targets: torch.Tensor,

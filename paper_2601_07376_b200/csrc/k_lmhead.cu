@@ -25,10 +25,12 @@
 
 #include "otk_internal.h"
 #include "otk_ptx.cuh"
+#include "otk_umma.cuh"
 
 namespace otk {
 
 using namespace ptx;
+using namespace umma;
 
 constexpr int kLmRows = 256;   // rows per pair tile (128 per CTA)
 constexpr int kLmCols = 256;   // vocab columns per tile (MMA N; 128 staged per CTA)
@@ -40,7 +42,6 @@ constexpr int kLmStageBytes = kLmABytes + kLmBBytes;
 constexpr int kLmEpiWarps = 4;
 constexpr int kLmThreads = 32 * (2 + kLmEpiWarps);
 constexpr int kLmSmemBytes = kLmStages * kLmStageBytes + 1024 /* 1 KB alignment slack */ + 256 /* barriers */;
-constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address of the same offset in CTA rank 0
 
 struct LmParams {
   int64_t num_rows, vocab;
@@ -54,70 +55,16 @@ struct LmParams {
   float k2;              // logit_scale * log2(e)
   float4* partials;      // [n_chunks][num_rows]
   int* err;
+  // optional: the logits rounded to bf16 (the row statistics are then taken over the rounded values, so the
+  // backward's p = 2^(s log2(e) x - L2) from these logits sums to 1 — k_lmhead_bwd.cu), stored in 64 x 64 tiles:
+  // [rows_pad / 64][cols_pad / 64][64][64] with rows_pad / cols_pad the 256-padded sizes, every tile element
+  // written (rows >= num_rows and columns >= vocab hold 0: their h / W operands were zero-filled)
+  uint32_t* logits_out;
+  int64_t ld_out;        // tiles per tile row = cols_pad / 64
 };
 
-// ---- PTX wrappers specific to the tensor-core path -------------------------------------------------
-// 2-CTA TMA: lands in this CTA's smem, completes bytes on the leader CTA's barrier.
-__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_leader, int c0,
-                                                 int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-      "%4}], [%2];" ::"r"(dst),
-      "l"(map), "r"(bar_leader), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
-}
-// K-major operand, 128-byte swizzle: rows of 128 B, 8-row atoms 1024 B apart (SBO), LBO unused (1),
-// descriptor version 1 (sm_100), layout type 2 (SWIZZLE_128B).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return uint64_t((saddr & 0x3FFFFu) >> 4) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
-         (uint64_t(1) << 46) | (uint64_t(2) << 61);
-}
 // kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, N = 256, M = 256 (CTA pair).
-constexpr uint32_t kLmIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kLmCols >> 3) << 17) |
-                              (uint32_t(kLmRows >> 4) << 24);
-__device__ __forceinline__ void umma_pair_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(kLmIdesc), "r"(accumulate)
-      : "memory");
-}
-// arrive (once) on the barrier at this smem offset in BOTH CTAs of the pair when the issued MMAs complete
-__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"(uint16_t(0x3))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void tmem_alloc_pair(uint32_t* smem_dst, uint32_t ncols) {
-  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
-               "r"(ncols)
-               : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
-  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t* r = reinterpret_cast<uint32_t*>(v);
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
+constexpr uint32_t kLmIdesc = umma::idesc_bf16(kLmRows, kLmCols, false, false);
 
 __device__ __forceinline__ int chunk_tile0(int c, int n_chunks, int n_coltiles) {
   return int((int64_t(c) * n_coltiles) / n_chunks);
@@ -222,7 +169,7 @@ __global__ void __launch_bounds__(kLmThreads, 1)
             const uint32_t b = a + kLmABytes;
 #pragma unroll
             for (int k = 0; k < kLmK / 16; ++k)
-              umma_pair_bf16(d, sw128_desc(a + k * 32), sw128_desc(b + k * 32), (kb | k) != 0);
+              umma_pair_bf16<kLmIdesc>(d, sw128_kmajor_desc(a + k * 32), sw128_kmajor_desc(b + k * 32), (kb | k) != 0);
             umma_commit_pair(&empty[s]);  // frees the stage in both CTAs once these MMAs have read it
             if (++s == kLmStages) {
               s = 0;
@@ -264,6 +211,20 @@ __global__ void __launch_bounds__(kLmThreads, 1)
           const int64_t col0 = col_t + cc * 32;
           const int64_t rem = p.vocab - col0;
           const int nvalid = rem < 32 ? int(rem) : 32;
+          if (p.logits_out) {  // round to bf16 (RNE), store the row's 32 columns, and keep the rounded values
+            uint32_t w[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              w[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+              v[2 * j] = bf_lo(w[j]);
+              v[2 * j + 1] = bf_hi(w[j]);
+            }
+            // tile (row / 64, col0 / 64), element offset (row % 64) * 64 + col0 % 64: 64 contiguous bytes
+            uint4* dst = reinterpret_cast<uint4*>(p.logits_out) +
+                         (((row >> 6) * p.ld_out + (col0 >> 6)) * 4096 + (row & 63) * 64 + (col0 & 63)) / 8;
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) dst[q4] = make_uint4(w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2], w[4 * q4 + 3]);
+          }
           float cm = -INFINITY;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -308,33 +269,6 @@ __global__ void __launch_bounds__(kLmThreads, 1)
 }
 
 // ---- host side -----------------------------------------------------------------------------------------
-namespace {
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  // resolved once (thread-safe static initialisation) through the runtime, so libotk needs no -lcuda
-  static const PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
-    cudaDriverEntryPointQueryResult q;
-    void* f = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-    return nullptr;
-  }();
-  return fn;
-}
-
-bool make_map(CUtensorMap* map, const void* base, int64_t rows, int d, int box_rows) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {cuuint64_t(d), cuuint64_t(rows)};
-  cuuint64_t strides[1] = {cuuint64_t(d) * 2};
-  cuuint32_t box[2] = {cuuint32_t(kLmK), cuuint32_t(box_rows)};
-  cuuint32_t estr[2] = {1, 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-}  // namespace
-
 int lmhead_chunks(int64_t num_rows, int64_t vocab, int num_sms) {
   // vocab chunks: enough (row tile, chunk) units for whole waves of the persistent CTA pairs, chunks of
   // nearly equal tile counts (ties: fewer chunks)
@@ -359,9 +293,9 @@ int lmhead_chunks(int64_t num_rows, int64_t vocab, int num_sms) {
 cudaError_t launch_lmhead_fwd(const otk_ctx* ctx, int64_t num_rows, int64_t vocab, int d, const void* hidden,
                               const void* weight, const int32_t* targets, const uint8_t* row_mask, float logit_scale,
                               float4* partials, int n_chunks, cudaStream_t s, int64_t vocab_start,
-                              int64_t vocab_total) {
+                              int64_t vocab_total, void* logits_out, int64_t ld_out) {
   CUtensorMap th, tw;
-  if (!make_map(&th, hidden, num_rows, d, 128) || !make_map(&tw, weight, vocab, d, 128))
+  if (!make_map_2d(&th, hidden, num_rows, d, d, kLmK, 128) || !make_map_2d(&tw, weight, vocab, d, d, kLmK, 128))
     return cudaErrorInvalidValue;
   LmParams p;
   p.num_rows = num_rows;
@@ -377,6 +311,8 @@ cudaError_t launch_lmhead_fwd(const otk_ctx* ctx, int64_t num_rows, int64_t voca
   p.err = ctx->d_err;
   p.k2 = logit_scale * 1.4426950408889634f;
   p.partials = partials;
+  p.logits_out = reinterpret_cast<uint32_t*>(logits_out);
+  p.ld_out = ld_out;
   // per launch (cheap, and correct for every device of the process)
   cudaError_t ea = cudaFuncSetAttribute(k_lmhead_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kLmSmemBytes);
   if (ea != cudaSuccess) return ea;

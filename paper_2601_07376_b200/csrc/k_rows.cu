@@ -70,7 +70,9 @@ __device__ __forceinline__ Stat combine(const Stat a, const Stat b) {
 }
 
 struct RowStats {
-  float L2;    // log2(e) * lse
+  float L2;    // log2(e) * lse = m + lg2S (rounded: use m and lg2S separately where |m| is large)
+  float m;     // the row total's reference (log2 units)
+  float lg2S;  // log2 of the sum relative to m
   float logp;  // z_y - lse
   float H;     // entropy
   float lse;
@@ -81,6 +83,8 @@ struct RowStats {
 __device__ __forceinline__ RowStats finalize(const Stat t, const float dy) {
   RowStats r;
   const float lg2S = lg2(t.s);
+  r.m = t.m;
+  r.lg2S = lg2S;
   r.L2 = __fadd_rn(t.m, lg2S);
   r.lse = __fmul_rn(r.L2, kLn2);
   r.logp = __fmul_rn(kLn2, __fsub_rn(dy, lg2S));
@@ -283,6 +287,12 @@ struct Vec<float> {
     pass1_pair<kInit>(x[2], x[3], s2x2, negm2, aS[1], aT[1], e[2], e[3]);
     return kKeepE ? pack(e) : make_uint4(0, 0, 0, 0);
   }
+  // e * 2^-64, exact (the underflow-safe split of pass2_row)
+  __device__ static __forceinline__ uint4 scale_m64(const uint4 e) {
+    const float k = 5.42101086242752217e-20f;  // 2^-64
+    return make_uint4(__float_as_uint(__uint_as_float(e.x) * k), __float_as_uint(__uint_as_float(e.y) * k),
+                      __float_as_uint(__uint_as_float(e.z) * k), __float_as_uint(__uint_as_float(e.w) * k));
+  }
   // entropy-bonus variant: g = e (A + B log2 e)
   __device__ static __forceinline__ uint4 pass2_ent(const uint4 e, float A, float B) {
     float x[4], g[4];
@@ -359,6 +369,15 @@ struct Vec<__nv_bfloat16> {
     asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(t) : "r"(w), "r"(lo2));
     asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(hi2), "r"(t));
     return r;
+  }
+  // e * 2^-64, exact (bf16x2 multiply by a power of two; the underflow-safe split of pass2_row)
+  __device__ static __forceinline__ uint32_t scale_m64_word(uint32_t w) {
+    uint32_t r;
+    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(w), "r"(0x1F801F80u));  // bf16x2(2^-64)
+    return r;
+  }
+  __device__ static __forceinline__ uint4 scale_m64(const uint4 e) {
+    return make_uint4(scale_m64_word(e.x), scale_m64_word(e.y), scale_m64_word(e.z), scale_m64_word(e.w));
   }
   // entropy-bonus variant: g = e (A + B log2 e) in fp32, rounded once to bf16
   __device__ static __forceinline__ uint4 pass2_ent(const uint4 e, float A, float B) {
@@ -843,18 +862,26 @@ __device__ __forceinline__ void pass2_row(char* drow, uint32_t tm, int ct, int n
   char* tp = drow + ct * 16;
   auto chunk2 = [&](int c, const uint4& e0, const uint4& e1, uint32_t mw, auto entf) {
     constexpr bool kEnt = decltype(entf)::value;
-    const float dm = __fsub_rn(__uint_as_float(mw), rs.L2);  // m_c - lse (log2 units)
+    // m_c - lse (log2 units) as (m_c - m) - lg2S: the difference of the two references first (exact when they are
+    // close), so rows of large-magnitude logits (|m| ~ 1e4: fp32 ulp 2^-10) keep full relative accuracy in p
+    float dm = __fsub_rn(__fsub_rn(__uint_as_float(mw), rs.m), rs.lg2S);
+    uint4 e0s = e0, e1s = e1;
+    if (dm < -64.f) {  // 2^dm would flush to 0 while e (up to 2^64) times it need not: move 2^-64 into e (exact)
+      e0s = VT::scale_m64(e0);
+      e1s = VT::scale_m64(e1);
+      dm = __fadd_rn(dm, 64.f);
+    }
     const float qc = ex2(dm);
     uint4 g0, g1;
     if constexpr (!kEnt) {
       const float kt = __fmul_rn(lo.coef, qc);
-      g0 = VT::pass2(e0, kt);
-      g1 = VT::pass2(e1, kt);
+      g0 = VT::pass2(e0s, kt);
+      g1 = VT::pass2(e1s, kt);
     } else {  // g = e q (coef + wcs (ln2 (log2 e + m_c - lse) + H))
       const float Ac = qc * fmaf(lo.wcs, fmaf(kLn2, dm, rs.H), lo.coef);
       const float Bc = qc * lo.wcs * kLn2;
-      g0 = VT::pass2_ent(e0, Ac, Bc);
-      g1 = VT::pass2_ent(e1, Ac, Bc);
+      g0 = VT::pass2_ent(e0s, Ac, Bc);
+      g1 = VT::pass2_ent(e1s, Ac, Bc);
     }
     char* q0 = tp + size_t(c) * kChunkBytes;
     if (c < nch - 1 || (c + 1) * CE <= segn) {
@@ -1485,7 +1512,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) 
         if (p.logp) p.logp[row] = side_ok ? rs.logp : 0.f;
         if (p.entropy) p.entropy[row] = side_ok ? rs.H : 0.f;
       }
-      const float L2 = rs.L2, coef = lo.coef;
+      const float mr = rs.m, lg2S = rs.lg2S, coef = lo.coef;
       char* drow = reinterpret_cast<char*>(p.dlogits) + (row * p.ld + c0) * int64_t(sizeof(T));
       for (int c = 0; c < nch; ++c) {
         mbar_wait(&S.full[slot], phase);
@@ -1500,7 +1527,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_stream(const RowParams p) 
           VT::unpack(w, x);
 #pragma unroll
           for (int i = 0; i < EV; ++i) {
-            const float d = __fmaf_rn(x[i], s2, -L2);   // log2 p
+            const float d = __fsub_rn(__fmaf_rn(x[i], s2, -mr), lg2S);   // log2 p (reference first: see pass2_row)
             const float pv = ex2(d);
             // coef p + wcs p (ln p + H): the entropy-bonus term costs two FMAs, no extra exponential
             g[i] = lo.wcs == 0.f ? __fmul_rn(coef, pv) : pv * fmaf(lo.wcs, fmaf(kLn2, fmaxf(d, -1e30f), rs.H), coef);
@@ -1729,6 +1756,76 @@ cudaError_t launch_combine(const otk_ctx* ctx, int64_t num_rows, int nshards, co
   if (blocks > int64_t(ctx->num_sms) * 8) blocks = int64_t(ctx->num_sms) * 8;
   if (blocks < 1) blocks = 1;
   k_combine<<<int(blocks), 256, 0, s>>>(num_rows, nshards, partials, row_mask, logp, entropy, lse);
+  return cudaGetLastError();
+}
+
+
+// ---- NEXT-1 backward: per-row loss terms from the fused LM head's chunk partials ------------------------
+// One thread per row: combine the row's vocab-chunk partials (chunk order, as k_combine), finalize, evaluate the
+// loss terms of (4) (same loss_terms / row_side / row_weight as the row kernels), accumulate the stats, and write
+// the constants the backward GEMMs form dx from (k_lmhead_bwd.cu):
+//   dx_v = 2^d (alpha' + beta' d),  d = s log2(e) x_v - m,  alpha' = (coef + wcs H - wcs ln2 lg2S) 2^-lg2S,
+//   beta' = wcs ln2 2^-lg2S  (so dx_v = coef p_v + wcs p_v (ln p_v + H), the (4) gradient incl. the entropy bonus),
+// and gy = the target column's value (coef expm1(logp) + bonus). Inactive rows get m = 1e30 (2^d = 0), 0, 0, 0.
+// The loss partials are reduced per CTA in a fixed order and by the last CTA (ticket): deterministic.
+__global__ void __launch_bounds__(256) k_lmhead_loss_rows(const RowParams p, float4* __restrict__ rowc) {
+  __shared__ double red[8][5];
+  double acc[5] = {0, 0, 0, 0, 0};
+  const int64_t nl = *p.n_loss;
+  const float invN = nl > 0 ? float(1.0 / double(nl)) : 0.f;
+  const int64_t nact = p.reduction != OTK_TOKEN_MEAN ? *p.n_active : 0;
+  for (int64_t row = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; row < p.num_rows;
+       row += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t y = p.targets[row];
+    const uint8_t m = p.mask[row];
+    float4 rc = make_float4(1e30f, 0.f, 0.f, 0.f);
+    float lp_out = 0.f, H_out = 0.f;
+    if (row_active(p, y, m)) {
+      float dy;
+      const Stat tot = combine_partials(p.partials_in + row, p.num_rows, p.nshards, dy);
+      const RowStats rs = finalize(tot, dy);
+      RowSide sd{0.0, p.old_logp[row], p.ref_logp ? p.ref_logp[row] : 0.f, 0};
+      const bool side_ok = row_side(p, row, p.row_traj[row], sd, true);
+      const LossOut lo = loss_terms(p, rs.logp, rs.H, sd, side_ok ? row_weight(p, invN, sd.nb, nact) : 0.f);
+      if (side_ok) {
+        acc[0] += double(lo.w) * double(lo.L);
+        acc[1] += lo.clipped ? 1.0 : 0.0;
+        acc[2] += double(lo.kl);
+        acc[3] += double(rs.H);
+        acc[4] += 1.0;
+        lp_out = rs.logp;
+        H_out = rs.H;
+        const float sc = ex2(-rs.lg2S);
+        const float alpha = fmaf(lo.wcs, rs.H, lo.coef), beta = lo.wcs * kLn2;
+        rc = make_float4(rs.m, fmaf(-beta, rs.lg2S, alpha) * sc, beta * sc, lo.gy);
+      }
+    }
+    rowc[row] = rc;
+    if (p.logp) p.logp[row] = lp_out;
+    if (p.entropy) p.entropy[row] = H_out;
+  }
+  // CTA reduction in a fixed order: warp shuffles, then warp 0 over the warps
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    double v = acc[k];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[w][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t[5] = {0, 0, 0, 0, 0};
+    for (int i = 0; i < int(blockDim.x >> 5); ++i)
+      for (int k = 0; k < 5; ++k) t[k] += red[i][k];
+    stats_epilogue(p, t[0], t[1], t[2], t[3], t[4], nl, blockIdx.x, gridDim.x);
+  }
+}
+
+cudaError_t launch_lmhead_loss_rows(const otk_ctx* ctx, const RowParams& p, float4* rowc, cudaStream_t s) {
+  int64_t blocks = (p.num_rows + 255) / 256;
+  if (blocks > int64_t(ctx->num_sms) * 4) blocks = int64_t(ctx->num_sms) * 4;  // <= kMaxCtas stat slots
+  if (blocks < 1) blocks = 1;
+  k_lmhead_loss_rows<<<int(blocks), 256, 0, s>>>(p, rowc);
   return cudaGetLastError();
 }
 

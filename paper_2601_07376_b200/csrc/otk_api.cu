@@ -425,6 +425,88 @@ otk_status otk_lmhead_row_partials(otk_ctx* ctx, int64_t num_rows, int64_t hidde
   return OTK_OK;
 }
 
+namespace {
+struct LmLossWs {
+  int n_chunks, splits;
+  int64_t cols_pad, x_off, part_off, rowc_off, dh_off, bytes;
+};
+// workspace: x tiles [rows_pad/64][cols_pad/64][64][64] bf16 | chunk partials | row constants | dh split-K partials
+LmLossWs lm_loss_ws(const otk_ctx* ctx, int64_t num_rows, int64_t hidden_dim, int64_t vocab) {
+  LmLossWs w;
+  w.n_chunks = otk::lmhead_chunks(num_rows, vocab, ctx->num_sms);
+  w.splits = otk::lmhead_dh_splits(num_rows, vocab, int(hidden_dim), ctx->num_sms);
+  const int64_t rows_pad = (num_rows + 255) / 256 * 256;
+  w.cols_pad = (vocab + 255) / 256 * 256;
+  w.x_off = 0;
+  w.part_off = rows_pad * w.cols_pad * 2;
+  w.rowc_off = w.part_off + int64_t(w.n_chunks) * num_rows * 16;
+  w.dh_off = w.rowc_off + num_rows * 16;
+  w.bytes = w.dh_off + (w.splits > 1 ? int64_t(w.splits) * num_rows * hidden_dim * 4 : 0);
+  return w;
+}
+}  // namespace
+
+int64_t otk_lmhead_loss_workspace_bytes(const otk_ctx* ctx, int64_t num_rows, int64_t hidden_dim, int64_t vocab) {
+  if (!ctx || num_rows < 0 || vocab < 1 || hidden_dim < 64 || hidden_dim % 64 != 0) return -1;
+  return lm_loss_ws(ctx, num_rows, hidden_dim, vocab).bytes;
+}
+
+otk_status otk_lmhead_policy_loss_fwd_bwd(otk_ctx* ctx, int64_t num_rows, int64_t hidden_dim, int64_t vocab,
+                                          const void* hidden, const void* weight, const int32_t* targets,
+                                          const uint8_t* loss_mask, const int32_t* row_traj, const double* adv,
+                                          const float* old_logp, const float* ref_logp, const int64_t* n_loss,
+                                          const otk_loss_cfg* cfg, void* workspace, int64_t workspace_bytes,
+                                          void* dhidden, void* dweight, float* logp, float* entropy,
+                                          otk_loss_stats* stats, otk_stream_t stream) {
+  OTK_REQUIRE(ctx, OTK_ERR_INVALID_ARG, "ctx is NULL");
+  OTK_REQUIRE(num_rows >= 0 && vocab >= 8 && vocab % 8 == 0 && vocab < (int64_t(1) << 31) &&
+                  num_rows < (int64_t(1) << 31),
+              OTK_ERR_SHAPE, "need 0 <= num_rows < 2^31 and vocab a positive multiple of 8 (< 2^31)");
+  OTK_REQUIRE(hidden_dim >= 64 && hidden_dim % 64 == 0 && hidden_dim <= 65536, OTK_ERR_SHAPE,
+              "hidden_dim must be a positive multiple of 64 (<= 65536)");
+  otk_status st = check_cfg(cfg, ref_logp, num_rows);
+  if (st != OTK_OK) return st;
+  OTK_REQUIRE(stats, OTK_ERR_INVALID_ARG, "stats is NULL");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (num_rows == 0) return OTK_OK;
+  OTK_REQUIRE(hidden && weight && targets && loss_mask && row_traj && adv && old_logp && n_loss && workspace &&
+                  dhidden && dweight,
+              OTK_ERR_INVALID_ARG, "a required pointer is NULL");
+  OTK_REQUIRE(aligned16(hidden) && aligned16(weight) && aligned16(workspace) && aligned16(dhidden) &&
+                  aligned16(dweight),
+              OTK_ERR_ALIGNMENT, "hidden, weight, workspace, dhidden and dweight must be 16-byte aligned");
+  OTK_REQUIRE(dhidden != hidden && dhidden != weight && dweight != hidden && dweight != weight && dhidden != dweight,
+              OTK_ERR_INVALID_ARG, "outputs must not alias inputs");
+  const LmLossWs w = lm_loss_ws(ctx, num_rows, hidden_dim, vocab);
+  OTK_REQUIRE(workspace_bytes >= w.bytes, OTK_ERR_SHAPE, "workspace smaller than otk_lmhead_loss_workspace_bytes()");
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  void* logits = ws + w.x_off;
+  float4* part = reinterpret_cast<float4*>(ws + w.part_off);
+  float4* rowc = reinterpret_cast<float4*>(ws + w.rowc_off);
+  float* dh_part = reinterpret_cast<float*>(ws + w.dh_off);
+  const float scale = float(cfg->logit_scale);
+  // (a) x = h W^T on tcgen05: bf16 x tiles out + per-(row, vocab chunk) log-softmax partials of the rounded x
+  OTK_CUDA(otk::launch_lmhead_fwd(ctx, num_rows, vocab, int(hidden_dim), hidden, weight, targets, loss_mask, scale,
+                                  part, w.n_chunks, s, 0, vocab, logits, w.cols_pad / 64),
+           "k_lmhead_fwd launch");
+  ctx->launches += 1;
+  // (b) per row: combine, finalize, loss terms of (4), stats; the backward's per-row constants
+  int csize = 1, seg = 0;
+  otk::RowParams p = base_params(ctx, num_rows, vocab, vocab, logits, targets, loss_mask, scale, csize, seg);
+  p.partials_in = part;
+  p.nshards = w.n_chunks;
+  set_loss(p, row_traj, adv, old_logp, ref_logp, n_loss, cfg, nullptr, logp, entropy, stats);
+  OTK_CUDA(otk::launch_lmhead_loss_rows(ctx, p, rowc, s), "k_lmhead_loss_rows launch");
+  ctx->launches += 1;
+  // (c) dh = dx W and dW = dx^T h on tcgen05, dx formed in shared memory from x and the row constants
+  int nl = 0;
+  OTK_CUDA(otk::launch_lmhead_bwd(ctx, num_rows, vocab, int(hidden_dim), hidden, weight, logits, rowc, targets, 0,
+                                  scale, cfg->ent_coef != 0, dhidden, dweight, dh_part, w.splits, s, &nl),
+           "k_lmhead_bwd launch");
+  ctx->launches += nl;
+  return OTK_OK;
+}
+
 otk_status otk_logprob_entropy_fwd(otk_ctx* ctx, int64_t num_rows, int64_t vocab, int64_t ld, otk_dtype dtype,
                                    const void* logits, const int32_t* targets, const uint8_t* row_mask,
                                    float logit_scale, float* logp, float* entropy, float* lse, otk_stream_t stream) {

@@ -303,3 +303,36 @@ class LMHeadPolicyLoss:
             out["ms"] = dict(logits_gemm=ev[0].elapsed_time(ev[1]), loss_kernel=ev[1].elapsed_time(ev[2]),
                              grad_gemms=ev[2].elapsed_time(ev[3]))
         return out
+
+
+class LMHeadPolicyLossFused:
+    """The policy loss and its gradients THROUGH the LM head on this library's tcgen05 kernels (SURVEY.md §8(f)
+    NEXT-1, forward + backward; DESIGN.md §6 "LM head, backward"): one otk_lmhead_policy_loss_fwd_bwd call —
+    x = h Wᵀ with the log-softmax partials folded in its epilogue (x kept as bf16), the loss terms of (4) per row,
+    then dh = dx W and dW = dxᵀ h with dx formed tile by tile in shared memory from x (never written). Same
+    arguments and outputs as LMHeadPolicyLoss; x and the workspace are reused across calls."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+        self._bufs = {}
+
+    def __call__(self, hidden: torch.Tensor, weight: torch.Tensor, targets, loss_mask, row_traj, adv, old_logp,
+                 ref_logp, n_loss, cfg: LossCfg, *, timings: bool = False) -> dict:
+        from . import otk_lmhead_policy_loss_fwd_bwd
+        N, d = hidden.shape
+        V = weight.shape[0]
+        key = (N, V, d)
+        if key not in self._bufs:
+            self._bufs = {key: dict(workspace=None)}
+        b = self._bufs[key]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if timings else None
+        if ev:
+            ev[0].record()
+        out = otk_lmhead_policy_loss_fwd_bwd(self.ctx, hidden, weight, targets, loss_mask, row_traj, adv, old_logp,
+                                             ref_logp, n_loss, cfg, workspace=b["workspace"])
+        b["workspace"] = out["workspace"]
+        if ev:
+            ev[1].record()
+            torch.cuda.synchronize()
+            out["ms"] = dict(total=ev[0].elapsed_time(ev[1]))
+        return out

@@ -38,15 +38,16 @@ def launches(tag):
         for o in out:
             f.write(f'{o[0]},"{o[1]}","{o[2]}","{o[3]}",{o[4]:.0f}\n')
     # the timed otk step: masks, advantages and the loss launches (setup K3 / torch kernels excluded)
-    step_names = ("otk::k_build_masks", "otk::k_group_advantages", "otk::k_rows_tm<__nv_bfloat16, 2>")
-    step_k = [o for o in out if o[1] in step_names]
+    # K4 = k_rows_tm<bf16, BWD (=2), ...> whatever its trailing template arguments are
+    is_k4 = lambda name: name.startswith("otk::k_rows_tm<__nv_bfloat16, 2")
+    step_k = [o for o in out if o[1] in ("otk::k_build_masks", "otk::k_group_advantages") or is_k4(o[1])]
     tot = {}
     for o in out:
         tot.setdefault(o[1], [0, 0.0])
         tot[o[1]][0] += 1
         tot[o[1]][1] += o[4]
     s = sum(o[4] for o in step_k)
-    k4 = sum(o[4] for o in step_k if "k_rows_tm<__nv_bfloat16, 2>" in o[1])
+    k4 = sum(o[4] for o in step_k if is_k4(o[1]))
     lines = [f"ncu launch list of `bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline` ({len(out)} launches, "
              "cold-cache and serialised)", "", f"{'kernel':60s} {'n':>5s} {'total ms':>10s}"]
     for k, (n, t) in sorted(tot.items(), key=lambda kv: -kv[1][1]):

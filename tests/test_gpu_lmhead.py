@@ -51,7 +51,9 @@ def test_lmhead_fwd_timed_shapes(otk, ctx):
     V, d, Nmax = 151936, 3584, 16384 + 17
     h, w, y = make_lmhead(Nmax, V, d, seed=2024, device="cuda")
     block = 16 * 256                                            # row tiles per row block x rows per tile
-    cand = set(np.linspace(0, Nmax - 1, 72).astype(int).tolist())
+    cand = set()
+    for N in (4097, 8192, Nmax):                                # >= 64 spread rows below every N
+        cand |= set(np.linspace(0, N - 1, 64).astype(int).tolist())
     for b0 in range(0, Nmax, block):
         cand |= {b0, b0 + 1, b0 + 255, b0 + 256, min(b0 + block - 1, Nmax - 1)}
     cand |= {4095, 4096, 8191, 8192, 16383, 16384, Nmax - 1}

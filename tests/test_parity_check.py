@@ -164,3 +164,42 @@ def test_underflow_below_smallest_normal_is_tolerated():
     assert P.row_ratio(got, want, q, 7, coef, 1e-10, "f32") <= 1.0
     got[5] = 0.0
     assert P.row_ratio(got, want, q, 7, coef, 1e-10, "f32") > 1.0
+
+
+def test_lmhead_flip_tolerance_covers_flipped_roundings():
+    """The LM-head dh / dW flip allowance (oracle/parity.py lmhead_flip_tolerance, R38): flipping EVERY
+    ambiguous logit to its other bf16 neighbour moves the float64 oracle's dh and dW by no more than the allowance;
+    a flipped NON-ambiguous logit (a wrong rounding, not an accumulation-order effect) is not covered."""
+    from synth import make_lmhead
+    N, V, d = 96, 1024, 128
+    h, w, y = make_lmhead(N, V, d, seed=4)
+    H, Wm, yy = h.double().numpy(), w.double().numpy(), y.numpy()
+    x64 = H @ Wm.T
+    xb = torch.from_numpy(x64).to(torch.bfloat16).double().numpy()
+    rng = np.random.default_rng(1)
+    mask = (rng.random(N) < 0.8).astype(np.uint8)
+    rt = np.zeros(N, np.int32)
+    adv = np.array([0.9])
+    lp0 = np.array([O.row_forward(xb[j], int(yy[j]))[0] for j in range(N)])
+    old, ref = lp0 + 0.05, lp0 - 0.1
+    cfg = O.LossCfg(kl_beta=0.04)
+    n = int(mask.sum())
+    want = O.policy_loss_fwd_bwd(xb, yy, mask, rt, adv, old, ref, n, cfg)
+    args = (H, Wm, x64, xb, yy, want["coef"], want["logp"], old, ref, adv[rt], np.full(N, 1.0 / n), cfg, mask)
+    # a widened accumulation bound (as if d were 2^16) makes hundreds of logits ambiguous
+    tdh, tdW, n_amb, amb = P.lmhead_flip_tolerance(*args, acc_terms=2 ** 16)
+    assert n_amb > 100
+    u = P.bf16_ulp(xb)
+    side = np.where(x64 >= xb, 1.0, -1.0)
+    alt = O.policy_loss_fwd_bwd(np.where(amb, xb + side * u, xb), yy, mask, rt, adv, old, ref, n, cfg)
+    ddx = alt["dlogits"] - want["dlogits"]
+    assert np.all(np.abs(ddx @ Wm) <= tdh) and np.all(np.abs(ddx.T @ H) <= tdW)
+    assert np.max(np.abs(ddx @ Wm) / np.maximum(tdh, 1e-300)) > 0.05   # the allowance is not vacuous
+    # a flip outside the (real-d) ambiguous set is not covered: the largest trainable dx element, rounded the other way
+    t_dh, _, _, amb_d = P.lmhead_flip_tolerance(*args)
+    dx0 = want["dlogits"]
+    j, v = np.unravel_index(np.argmax(np.where(amb_d | (mask[:, None] == 0), 0, np.abs(dx0))), dx0.shape)
+    xw = xb.copy()
+    xw[j, v] += side[j, v] * u[j, v]
+    bad = O.policy_loss_fwd_bwd(xw, yy, mask, rt, adv, old, ref, n, cfg)["dlogits"]
+    assert np.max(np.abs((bad - dx0) @ Wm) - 2.0 ** -8 * np.abs(dx0 @ Wm) - t_dh) > 0
