@@ -430,7 +430,8 @@ otk_status otk_lmhead_row_partials(otk_ctx* ctx, int64_t num_rows, int64_t hidde
  * where dx = dL/dx (the dlogits of (4)) is formed tile by tile inside the two backward tcgen05 GEMMs from
  * x and four per-row constants — it is never written to memory. Three tensor-core GEMMs (x, dh, dW) and
  * two small kernels (chunk-partial combine + loss terms; dh split-K reduction), in this stream order.
- * hidden: [num_rows, hidden_dim] bf16, weight: [vocab, hidden_dim] bf16 (row-major, 16-byte aligned);
+ * hidden: [num_rows, hidden_dim] bf16, weight: [vocab, hidden_dim] bf16 (row-major, 16-byte aligned; dhidden,
+ * dweight and workspace 32-byte aligned: the epilogues write whole 32-byte sectors);
  * hidden_dim a multiple of 64; vocab a multiple of 8 (16-byte rows of x). targets, loss_mask, row_traj,
  * adv, old_logp, ref_logp, n_loss, cfg as in otk_policy_loss_fwd_bwd (token-mean or sequence-mean
  * reductions, all A4 variants; targets global ids in [0, vocab)).

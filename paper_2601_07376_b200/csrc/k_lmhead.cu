@@ -39,7 +39,7 @@ constexpr int kLmStages = 6;
 constexpr int kLmABytes = 128 * kLmK * 2;  // 16 KB: this CTA's rows
 constexpr int kLmBBytes = 128 * kLmK * 2;  // 16 KB: this CTA's half of the columns
 constexpr int kLmStageBytes = kLmABytes + kLmBBytes;
-constexpr int kLmEpiWarps = 4;
+constexpr int kLmEpiWarps = 4;  // one per TMEM lane quadrant (8, two per quadrant over half tiles: no faster)
 constexpr int kLmThreads = 32 * (2 + kLmEpiWarps);
 constexpr int kLmSmemBytes = kLmStages * kLmStageBytes + 1024 /* 1 KB alignment slack */ + 256 /* barriers */;
 
@@ -222,8 +222,8 @@ __global__ void __launch_bounds__(kLmThreads, 1)
             // tile (row / 64, col0 / 64), element offset (row % 64) * 64 + col0 % 64: 64 contiguous bytes
             uint4* dst = reinterpret_cast<uint4*>(p.logits_out) +
                          (((row >> 6) * p.ld_out + (col0 >> 6)) * 4096 + (row & 63) * 64 + (col0 & 63)) / 8;
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) dst[q4] = make_uint4(w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2], w[4 * q4 + 3]);
+            stg256(dst, make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]));
+            stg256(dst + 2, make_uint4(w[8], w[9], w[10], w[11]), make_uint4(w[12], w[13], w[14], w[15]));
           }
           float cm = -INFINITY;
 #pragma unroll

@@ -17,8 +17,11 @@
 // ready (both CTAs) + B (both CTAs' TMA on the leader's barrier) and issues 8 MMAs per stage. The transform
 // costs 2 MUFU ex2 per pair of elements = 8192 ex2 per CTA per stage against 1024 clocks of MMA (N = 512 keeps
 // it at half the SFU rate; N = 256 would saturate it).
-// After a unit's last stage the transform warps drain TMEM (tcgen05.ld 32x32b, one row per thread, 256 columns
+// After a unit's last stage the transform warps drain TMEM (tcgen05.ld 32x32b, one row per thread, 128 columns
 // per warp) into the output — bf16, or fp32 split-K partials for dh — and release the accumulators.
+// dh runs first; its units of hidden tile 0 also TMA-store each transformed A stage, so dx exists once in HBM as
+// 64 x 64 tiles (2 bytes per logit written, read once) and dW = dxᵀ h runs as a plain GEMM: dx is formed once
+// per element for dh's first hidden tile instead of once per hidden tile of each GEMM (2 x d/512 times).
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -39,10 +42,11 @@ constexpr int kBwK = 64;
 constexpr int kBwAStages = 6, kBwBStages = 4;
 constexpr int kBwABytes = 128 * kBwK * 2;  // 16 KB: this CTA's 128 M-rows x 64 k
 constexpr int kBwBBytes = 256 * kBwK * 2;  // 32 KB: this CTA's 2 x 128 N-columns x 64 k (4 TMA boxes of 64 x 64)
-constexpr int kBwXWarps = 16;  // transform + epilogue warps (2..17); warp 0 loads A, warp 18 loads B, warp 1 MMAs
-constexpr int kBwThreads = 32 * (3 + kBwXWarps);
+constexpr int kBwXWarps = 16;  // transform + epilogue warps (2..17); warp 0 loads A, warp 18 loads B, warp 1 MMAs,
+                               // warp 19 stores dx tiles (dh)
+constexpr int kBwThreads = 32 * (4 + kBwXWarps);
 constexpr int kBwBOff = kBwAStages * kBwABytes;
-constexpr int kBwSmemBytes = kBwBOff + kBwBStages * kBwBBytes + 1024 /* alignment slack */ + 256 /* barriers */;
+constexpr int kBwSmemBytes = kBwBOff + kBwBStages * kBwBBytes + 1024 /* alignment slack */ + 512 /* barriers */;
 static_assert(kBwSmemBytes <= 232448, "shared memory of one CTA");
 constexpr int kBwMtile = 256, kBwNtile = 512;
 
@@ -58,6 +62,8 @@ struct LmBwdParams {
   const int32_t* targets;
   int64_t vocab_start;   // global id of local vocab column 0
   float s2;              // logit_scale * log2(e)
+  int store_dx;          // dh: units of hidden tile 0 also store the transformed A (= dx tiles) through tm_dx
+  int xform;             // 0: A already holds dx (dW after dh stored it): no transform, the GEMM alone
   void* out;             // dh: fp32 [splits][num_rows][d] (splits > 1) or bf16 [num_rows][d]; dW: bf16 [vocab][d]
 };
 
@@ -195,7 +201,7 @@ __device__ unsigned long long g_bw_timing[2][8];
 template <int MODE, bool kEnt>
 __global__ void __launch_bounds__(kBwThreads, 1)
     k_lmhead_bwd(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                 const LmBwdParams p) {
+                 const __grid_constant__ CUtensorMap tm_dx, const LmBwdParams p) {
   constexpr bool kDh = MODE == 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -206,7 +212,8 @@ __global__ void __launch_bounds__(kBwThreads, 1)
   uint64_t* emptyB = fullB + kBwBStages;
   uint64_t* tfull = emptyB + kBwBStages;
   uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* xdone = tempty + 1;  // [kBwAStages] this CTA's transform of a stage is complete (dx store)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xdone + kBwAStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = int(cluster_ctarank());
@@ -221,7 +228,8 @@ __global__ void __launch_bounds__(kBwThreads, 1)
     for (int s = 0; s < kBwAStages; ++s) {
       mbar_init(&fullA[s], 1);
       mbar_init(&readyA[s], 2 * kBwXWarps);
-      mbar_init(&emptyA[s], 1);
+      mbar_init(&emptyA[s], p.store_dx ? 2 : 1);  // + the dx storer's release
+      mbar_init(&xdone[s], kBwXWarps);
     }
     for (int s = 0; s < kBwBStages; ++s) {
       mbar_init(&fullB[s], 1);
@@ -232,6 +240,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
     fence_mbar_init();
     prefetch_tmap(&tm_a);
     prefetch_tmap(&tm_b);
+    if (p.store_dx) prefetch_tmap(&tm_dx);
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
   tc_fence_before();
@@ -256,6 +265,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             tma_load_4d(a, &tm_a, &fullA[s], 0, 0, kb, m0 >> 6);
           else      // x tiles (row block kb, vocab blocks m0/64 .. +1): [2][64 rows][64 v], MN-major
             tma_load_4d(a, &tm_a, &fullA[s], 0, 0, m0 >> 6, kb);
+
           if (++s == kBwAStages) {
             s = 0;
             ph ^= 1u;
@@ -287,15 +297,43 @@ __global__ void __launch_bounds__(kBwThreads, 1)
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int q = 0; q < 2; ++q)
+            for (int q = 0; q < 2; ++q) {
               tma_load_2d_pair(b + h * 16384 + q * 8192, &tm_b, barB, nt * kBwNtile + h * 256 + rank * 128 + q * 64,
                                kb * kBwK);
+            }
           if (++s == kBwBStages) {
             s = 0;
             ph ^= 1u;
           }
         }
       }
+    }
+  } else if (warp == 3 + kBwXWarps) {
+    // ---------------- dx storer (dh, both CTAs): once the transform of a stage of a hidden-tile-0 unit is complete,
+    // TMA-store it (the dx tiles the dW GEMM reads), wait for the store to have read it, and release the stage
+    // (emptyA's second arrival; other units release at once)
+    if (lane == 0 && p.store_dx) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = pair; u < n_units; u += npairs) {
+        int mt, nt, kb0, kb1, sp;
+        bw_unit(p, u, mt, nt, kb0, kb1, sp);
+        const int m0 = mt * kBwMtile + rank * 128;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&xdone[s], ph);
+          if (nt == 0) {
+            tma_store_4d(&tm_dx, smem_u32(smem + s * kBwABytes), 0, 0, kb, m0 >> 6);
+            bulk_commit();
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+          mbar_arrive(&emptyA[s]);
+          if (++s == kBwAStages) {
+            s = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+      bulk_wait_all();
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader CTA, one thread)
@@ -396,7 +434,10 @@ __global__ void __launch_bounds__(kBwThreads, 1)
           }
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) mbar_arrive_remote(ready_leader + s * 8);
+          if (lane == 0) {
+            mbar_arrive_remote(ready_leader + s * 8);
+            if (p.store_dx) mbar_arrive(&xdone[s]);
+          }
           BW_ACC(5);
           if (++s == kBwAStages) {
             s = 0;
@@ -408,9 +449,22 @@ __global__ void __launch_bounds__(kBwThreads, 1)
         // values are loaded two stages ahead so the global-load latency never sits in front of a transform. A
         // quarter-warp is one k row: box 1 takes the chunks of the other parity (no bank conflict with box 0).
         const int jj = xt >> 3, b = (xt >> 2) & 1, qq = xt & 3;
-        RawK q0 = raw_consts(p, int64_t(kb0) * kBwK + jj);
-        RawK q1 = raw_consts(p, int64_t(kb0 + 1) * kBwK + jj);
+        RawK q0, q1;
+        if (p.xform) {
+          q0 = raw_consts(p, int64_t(kb0) * kBwK + jj);
+          q1 = raw_consts(p, int64_t(kb0 + 1) * kBwK + jj);
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
+          if (!p.xform) {  // A is dx already: relay the stage to the MMA
+            mbar_wait(&fullA[s], ph);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(ready_leader + s * 8);
+            if (++s == kBwAStages) {
+              s = 0;
+              ph ^= 1u;
+            }
+            continue;
+          }
           const RowK cur = cook<kEnt>(q0, p.vocab);
           q0 = q1;
           q1 = raw_consts(p, int64_t(kb + 2) * kBwK + jj);
@@ -429,7 +483,10 @@ __global__ void __launch_bounds__(kBwThreads, 1)
           }
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) mbar_arrive_remote(ready_leader + s * 8);
+          if (lane == 0) {
+            mbar_arrive_remote(ready_leader + s * 8);
+            if (p.store_dx) mbar_arrive(&xdone[s]);
+          }
           BW_ACC(5);
           if (++s == kBwAStages) {
             s = 0;
@@ -457,17 +514,22 @@ __global__ void __launch_bounds__(kBwThreads, 1)
         continue;
 #endif
         if (row < M && col < p.d) {
+          // 256-bit stores: every instruction writes whole 32-byte sectors (rows are 32-byte aligned: d % 64 == 0)
           if (f32out) {
-            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) +
-                                                    (int64_t(sp) * p.num_rows + row) * p.d + col);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) dst[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-          } else {
-            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.d + col);
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<float*>(p.out) +
+                                                  (int64_t(sp) * p.num_rows + row) * p.d + col);
+            const uint32_t* u = reinterpret_cast<const uint32_t*>(v);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              dst[k] = make_uint4(pack_bf16x2(v[8 * k], v[8 * k + 1]), pack_bf16x2(v[8 * k + 2], v[8 * k + 3]),
-                                  pack_bf16x2(v[8 * k + 4], v[8 * k + 5]), pack_bf16x2(v[8 * k + 6], v[8 * k + 7]));
+              stg256(dst + 2 * k, make_uint4(u[8 * k], u[8 * k + 1], u[8 * k + 2], u[8 * k + 3]),
+                     make_uint4(u[8 * k + 4], u[8 * k + 5], u[8 * k + 6], u[8 * k + 7]));
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.d + col);
+            uint32_t w[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) w[k] = pack_bf16x2(v[2 * k], v[2 * k + 1]);
+            stg256(dst, make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]));
+            stg256(dst + 2, make_uint4(w[8], w[9], w[10], w[11]), make_uint4(w[12], w[13], w[14], w[15]));
           }
         }
       }
@@ -508,16 +570,18 @@ __global__ void k_lmhead_dh_reduce(const float4* __restrict__ part, int splits, 
 // ---- host side -----------------------------------------------------------------------------------------
 // split-K of dh: (row tiles x hidden tiles) units are few (e.g. 32 x 7 at N = 8192, d = 3584) against 74 CTA
 // pairs; splitting the vocab (K) dimension fills whole waves. Cost model in stages: waves x (stages per unit +
-// an epilogue of ~8 stages), plus the partials' round trip through HBM; at most 4 splits.
+// an epilogue of ~8 stages), plus the partials' round trip through HBM; at most 16 splits.
 int lmhead_dh_splits(int64_t num_rows, int64_t vocab, int d, int num_sms) {
   const int64_t units = ((num_rows + kBwMtile - 1) / kBwMtile) * ((d + kBwNtile - 1) / kBwNtile);
   const int64_t kb = (vocab + kBwK - 1) / kBwK;
   const int64_t pairs = std::max(1, num_sms / 2);
   int best = 1;
   double best_t = 1e300;
-  for (int s = 1; s <= 4; ++s) {
+  // a split's fp32 partials cost 8 bytes per dh element (write + read) at ~5 TB/s, a stage ~0.55 us
+  const double part_stages = double(num_rows) * double(d) * 8.0 / 5e12 / 0.55e-6;
+  for (int s = 1; s <= 16; ++s) {
     const int64_t waves = (units * s + pairs - 1) / pairs;
-    const double t = double(waves) * double((kb + s - 1) / s + 8) + (s > 1 ? 2.0 * s * units * 8.0 / pairs : 0.0);
+    const double t = double(waves) * double((kb + s - 1) / s + 8) + (s > 1 ? s * part_stages : 0.0);
     if (t < best_t - 1e-9) {
       best_t = t;
       best = s;
@@ -527,7 +591,7 @@ int lmhead_dh_splits(int64_t num_rows, int64_t vocab, int d, int num_sms) {
 }
 
 static cudaError_t launch_bwd(const otk_ctx* ctx, int mode, bool ent, const CUtensorMap& ta, const CUtensorMap& tb,
-                              const LmBwdParams& p, cudaStream_t s) {
+                              const CUtensorMap& tdx, const LmBwdParams& p, cudaStream_t s) {
   auto kern = mode == 0 ? (ent ? k_lmhead_bwd<0, true> : k_lmhead_bwd<0, false>)
                         : (ent ? k_lmhead_bwd<1, true> : k_lmhead_bwd<1, false>);
   cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwSmemBytes);
@@ -546,15 +610,15 @@ static cudaError_t launch_bwd(const otk_ctx* ctx, int mode, bool ent, const CUte
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tdx, p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 cudaError_t launch_lmhead_bwd(const otk_ctx* ctx, int64_t num_rows, int64_t vocab, int d, const void* hidden,
-                              const void* weight, const void* logits, const float4* rowc, const int32_t* targets,
-                              int64_t vocab_start, float logit_scale, bool ent, void* dh, void* dw, float* dh_part,
-                              int dh_splits, cudaStream_t s, int* launches) {
+                              const void* weight, const void* logits, void* dx_tiles, const float4* rowc,
+                              const int32_t* targets, int64_t vocab_start, float logit_scale, bool ent, void* dh,
+                              void* dw, float* dh_part, int dh_splits, cudaStream_t s, int* launches) {
   LmBwdParams p;
   p.num_rows = num_rows;
   p.vocab = vocab;
@@ -568,15 +632,18 @@ cudaError_t launch_lmhead_bwd(const otk_ctx* ctx, int64_t num_rows, int64_t voca
   const int64_t rows_pad = (num_rows + 255) / 256 * 256, cols_pad = (vocab + 255) / 256 * 256;
   // dh: A = x [N, V] K-major (box 64 vocab x 128 rows), B = W [V, d] MN-major (box 64 hidden x 64 vocab)
   {
-    CUtensorMap ta, tb;
-    if (!make_map_tiles(&ta, logits, rows_pad, cols_pad, 1, 2) || !make_map_2d(&tb, weight, vocab, d, d, 64, kBwK))
+    CUtensorMap ta, tb, tdx;
+    if (!make_map_tiles(&ta, logits, rows_pad, cols_pad, 1, 2) || !make_map_2d(&tb, weight, vocab, d, d, 64, kBwK) ||
+        !make_map_tiles(&tdx, dx_tiles, rows_pad, cols_pad, 1, 2))
       return cudaErrorInvalidValue;
+    p.store_dx = 1;  // hidden-tile-0 units leave dx behind for the dW GEMM
+    p.xform = 1;
     p.n_mt = int((num_rows + kBwMtile - 1) / kBwMtile);
     p.kb_total = int((vocab + kBwK - 1) / kBwK);
     p.splits = dh_splits;
     p.kb_per_split = (p.kb_total + dh_splits - 1) / dh_splits;
     p.out = dh_splits > 1 ? static_cast<void*>(dh_part) : dh;
-    cudaError_t e = launch_bwd(ctx, 0, ent, ta, tb, p, s);
+    cudaError_t e = launch_bwd(ctx, 0, ent, ta, tb, tdx, p, s);
     if (e != cudaSuccess) return e;
     ++*launches;
     if (dh_splits > 1) {
@@ -589,17 +656,20 @@ cudaError_t launch_lmhead_bwd(const otk_ctx* ctx, int64_t num_rows, int64_t voca
       ++*launches;
     }
   }
-  // dW: A = xᵀ (x boxes of 64 vocab x 64 rows, MN-major), B = h [N, d] MN-major (box 64 hidden x 64 rows)
+  // dW = dxᵀ h: A = the dx tiles dh stored (boxes of 64 vocab x 64 rows, MN-major) — a plain GEMM, no transform;
+  // B = h [N, d] MN-major (box 64 hidden x 64 rows)
   {
     CUtensorMap ta, tb;
-    if (!make_map_tiles(&ta, logits, rows_pad, cols_pad, 2, 1) || !make_map_2d(&tb, hidden, num_rows, d, d, 64, kBwK))
+    if (!make_map_tiles(&ta, dx_tiles, rows_pad, cols_pad, 2, 1) || !make_map_2d(&tb, hidden, num_rows, d, d, 64, kBwK))
       return cudaErrorInvalidValue;
+    p.store_dx = 0;
+    p.xform = 0;
     p.n_mt = int((vocab + kBwMtile - 1) / kBwMtile);
     p.kb_total = int((num_rows + kBwK - 1) / kBwK);
     p.splits = 1;
     p.kb_per_split = p.kb_total;
     p.out = dw;
-    cudaError_t e = launch_bwd(ctx, 1, ent, ta, tb, p, s);
+    cudaError_t e = launch_bwd(ctx, 1, ent, ta, tb, ta, p, s);
     if (e != cudaSuccess) return e;
     ++*launches;
   }

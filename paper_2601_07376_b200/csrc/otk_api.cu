@@ -428,19 +428,22 @@ otk_status otk_lmhead_row_partials(otk_ctx* ctx, int64_t num_rows, int64_t hidde
 namespace {
 struct LmLossWs {
   int n_chunks, splits;
-  int64_t cols_pad, x_off, part_off, rowc_off, dh_off, bytes;
+  int64_t cols_pad, x_off, dx_off, part_off, rowc_off, dh_off, bytes;
 };
-// workspace: x tiles [rows_pad/64][cols_pad/64][64][64] bf16 | chunk partials | row constants | dh split-K partials
+// workspace: x tiles [rows_pad/64][cols_pad/64][64][64] bf16 | dx tiles (same layout) | chunk partials |
+// row constants | dh split-K partials
 LmLossWs lm_loss_ws(const otk_ctx* ctx, int64_t num_rows, int64_t hidden_dim, int64_t vocab) {
   LmLossWs w;
   w.n_chunks = otk::lmhead_chunks(num_rows, vocab, ctx->num_sms);
   w.splits = otk::lmhead_dh_splits(num_rows, vocab, int(hidden_dim), ctx->num_sms);
   const int64_t rows_pad = (num_rows + 255) / 256 * 256;
   w.cols_pad = (vocab + 255) / 256 * 256;
+  auto up = [](int64_t b) { return (b + 255) / 256 * 256; };  // every region 256-byte aligned (256-bit stores)
   w.x_off = 0;
-  w.part_off = rows_pad * w.cols_pad * 2;
-  w.rowc_off = w.part_off + int64_t(w.n_chunks) * num_rows * 16;
-  w.dh_off = w.rowc_off + num_rows * 16;
+  w.dx_off = up(rows_pad * w.cols_pad * 2);
+  w.part_off = up(w.dx_off + rows_pad * w.cols_pad * 2);
+  w.rowc_off = up(w.part_off + int64_t(w.n_chunks) * num_rows * 16);
+  w.dh_off = up(w.rowc_off + num_rows * 16);
   w.bytes = w.dh_off + (w.splits > 1 ? int64_t(w.splits) * num_rows * hidden_dim * 4 : 0);
   return w;
 }
@@ -472,15 +475,17 @@ otk_status otk_lmhead_policy_loss_fwd_bwd(otk_ctx* ctx, int64_t num_rows, int64_
   OTK_REQUIRE(hidden && weight && targets && loss_mask && row_traj && adv && old_logp && n_loss && workspace &&
                   dhidden && dweight,
               OTK_ERR_INVALID_ARG, "a required pointer is NULL");
-  OTK_REQUIRE(aligned16(hidden) && aligned16(weight) && aligned16(workspace) && aligned16(dhidden) &&
-                  aligned16(dweight),
-              OTK_ERR_ALIGNMENT, "hidden, weight, workspace, dhidden and dweight must be 16-byte aligned");
+  auto aligned32 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 31u) == 0; };
+  OTK_REQUIRE(aligned16(hidden) && aligned16(weight) && aligned32(workspace) && aligned32(dhidden) &&
+                  aligned32(dweight),
+              OTK_ERR_ALIGNMENT, "hidden / weight must be 16-byte, workspace / dhidden / dweight 32-byte aligned");
   OTK_REQUIRE(dhidden != hidden && dhidden != weight && dweight != hidden && dweight != weight && dhidden != dweight,
               OTK_ERR_INVALID_ARG, "outputs must not alias inputs");
   const LmLossWs w = lm_loss_ws(ctx, num_rows, hidden_dim, vocab);
   OTK_REQUIRE(workspace_bytes >= w.bytes, OTK_ERR_SHAPE, "workspace smaller than otk_lmhead_loss_workspace_bytes()");
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   void* logits = ws + w.x_off;
+  void* dx_tiles = ws + w.dx_off;
   float4* part = reinterpret_cast<float4*>(ws + w.part_off);
   float4* rowc = reinterpret_cast<float4*>(ws + w.rowc_off);
   float* dh_part = reinterpret_cast<float*>(ws + w.dh_off);
@@ -500,7 +505,8 @@ otk_status otk_lmhead_policy_loss_fwd_bwd(otk_ctx* ctx, int64_t num_rows, int64_
   ctx->launches += 1;
   // (c) dh = dx W and dW = dx^T h on tcgen05, dx formed in shared memory from x and the row constants
   int nl = 0;
-  OTK_CUDA(otk::launch_lmhead_bwd(ctx, num_rows, vocab, int(hidden_dim), hidden, weight, logits, rowc, targets, 0,
+  OTK_CUDA(otk::launch_lmhead_bwd(ctx, num_rows, vocab, int(hidden_dim), hidden, weight, logits, dx_tiles, rowc,
+                                  targets, 0,
                                   scale, cfg->ent_coef != 0, dhidden, dweight, dh_part, w.splits, s, &nl),
            "k_lmhead_bwd launch");
   ctx->launches += nl;

@@ -186,9 +186,9 @@ cudaError_t launch_lmhead_fwd(const otk_ctx* ctx, int64_t num_rows, int64_t voca
 cudaError_t launch_lmhead_loss_rows(const otk_ctx* ctx, const RowParams& p, float4* rowc, cudaStream_t s);
 int lmhead_dh_splits(int64_t num_rows, int64_t vocab, int d, int num_sms);
 cudaError_t launch_lmhead_bwd(const otk_ctx* ctx, int64_t num_rows, int64_t vocab, int d, const void* hidden,
-                              const void* weight, const void* logits, const float4* rowc, const int32_t* targets,
-                              int64_t vocab_start, float logit_scale, bool ent, void* dh, void* dw, float* dh_part,
-                              int dh_splits, cudaStream_t s, int* launches);
+                              const void* weight, const void* logits, void* dx_tiles, const float4* rowc,
+                              const int32_t* targets, int64_t vocab_start, float logit_scale, bool ent, void* dh,
+                              void* dw, float* dh_part, int dh_splits, cudaStream_t s, int* launches);
 cudaError_t launch_combine_to_partial(const otk_ctx* ctx, int64_t num_rows, int nparts, const float4* partials,
                                       const uint8_t* row_mask, float4* out, cudaStream_t s);
 

@@ -251,6 +251,12 @@ __device__ __forceinline__ float f2_sum(uint64_t v) {
 }
 
 // ---- global stores -----------------------------------------------------------------------------
+// 256-bit store (sm_100 STG.256): one full 32-byte sector per thread; p 32-byte aligned
+__device__ __forceinline__ void stg256(void* p, uint4 a, uint4 b) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
 __device__ __forceinline__ void stg_cs_v4(void* p, uint4 v) {
   asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");

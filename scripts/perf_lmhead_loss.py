@@ -11,7 +11,7 @@ import paper_2601_07376_b200 as otk
 from paper_2601_07376_b200.step import LMHeadPolicyLoss, LMHeadPolicyLossFused
 from synth import make_lmhead, make_noise
 ap = argparse.ArgumentParser(); ap.add_argument("--rows", type=int, default=8192); ap.add_argument("--d", type=int, default=3584)
-ap.add_argument("--vocab", type=int, default=151936); ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--vocab", type=int, default=151936); ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--impl", default="both")
 a = ap.parse_args()
 torch.cuda.set_device(0)
@@ -26,6 +26,21 @@ old = (lp + make_noise(N, 0.05, 1, device="cuda")).contiguous()
 ref = (lp + make_noise(N, 0.1, 2, device="cuda")).contiguous()
 nl = mask.sum().to(torch.int64).reshape(1)
 cfg = otk.LossCfg(kl_beta=0.04)
+
+
+def back_to_back(step):
+    """ms per call of `iters` calls enqueued back to back (no host sync in between, so host-side argument
+    marshalling overlaps the previous call's kernels — the device time, as bench.py measures a step)."""
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(a.iters):
+        step(h, w, y, mask, rt, adv, old, ref, nl, cfg)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / a.iters
+
+
 flops_gemm = 2.0 * N * V * d
 res = dict(rows=N, vocab=V, hidden_dim=d)
 if a.impl in ("both", "cublas"):
@@ -38,7 +53,7 @@ if a.impl in ("both", "cublas"):
         for k, v in o["ms"].items():
             acc[k] = acc.get(k, 0.0) + v / a.iters
     ctx.check()
-    tot = sum(acc.values())
+    tot = back_to_back(step)
     res["cublas"] = dict(ms={k: round(v, 4) for k, v in acc.items()}, total_ms=round(tot, 4),
                          loss_kernel_share=round(acc["loss_kernel"] / tot, 4),
                          gemm_TFLOPs=round(3 * flops_gemm / (acc["logits_gemm"] + acc["grad_gemms"]) / 1e9, 1),
@@ -49,10 +64,9 @@ if a.impl in ("both", "fused"):
     step = LMHeadPolicyLossFused(ctx)
     for _ in range(2):
         step(h, w, y, mask, rt, adv, old, ref, nl, cfg)
-    t = 0.0
-    for _ in range(a.iters):
-        o = step(h, w, y, mask, rt, adv, old, ref, nl, cfg, timings=True)
-        t += o["ms"]["total"] / a.iters
+    t = back_to_back(step)
+    o = step(h, w, y, mask, rt, adv, old, ref, nl, cfg)
+    torch.cuda.synchronize()
     ctx.check()
     res["fused"] = dict(total_ms=round(t, 4), step_TFLOPs=round(3 * flops_gemm / t / 1e9, 1))
     if a.impl == "both":
