@@ -144,49 +144,58 @@ __device__ __forceinline__ void vpf_push(const RowParams& p, int64_t row, float4
 }
 
 // Collect the peers' records of `row` (waiting for this call's epoch) and combine all P partials in rank order
-// exactly as combine_partials does (own = `mine`). Identical bits on every rank.
-__device__ __forceinline__ Stat vpf_collect(const RowParams& p, int64_t row, float4 mine, float& dy, uint32_t ep) {
+// exactly as combine_partials does (own = `mine`). Called by a whole warp: lane q waits for peer q's record, so
+// the P - 1 round trips to peer memory overlap (the wait is the slowest peer's, not the sum); then every lane
+// combines the P records in rank order (shuffles). Identical bits on every rank.
+__device__ __forceinline__ Stat vpf_collect(const RowParams& p, int64_t row, float4 mine, float& dy, uint32_t ep,
+                                            int lane) {
   const int P = p.vpf_nranks, me = p.vpf_rank;
   const uint32_t par = ep & 1u;
   const int64_t cap = p.vpf_rows_cap;
   const char* own = reinterpret_cast<const char*>(p.vpf_xchg[me]);
-  Stat tot{-INFINITY, 0.f, 0.f};
-  float4 rec[OTK_VPF_MAX_RANKS];
-  for (int q = 0; q < P; ++q) {
-    if (q == me) {
-      rec[q] = mine;
-    } else {
-      const char* r = own + vpf_rec_index(cap, P, par, row, q) * 32;
-      uint64_t a0, a1, a2, a3;
-      auto ready = [&]() {
-        ld_pair_sys(r, a0, a1);
-        ld_pair_sys(r + 16, a2, a3);
-        return uint32_t(a0 >> 32) == ep && uint32_t(a1 >> 32) == ep && uint32_t(a2 >> 32) == ep &&
-               uint32_t(a3 >> 32) == ep;
-      };
-      bool ok = ready();
-      if (!ok) {
-        const uint64_t t0 = globaltimer_ns();
-        while (!(ok = ready())) {
-          // only a peer timeout of THIS call ends the wait early (a data error elsewhere never does: every
-          // valid row still gets its peers' partials)
-          if (*reinterpret_cast<volatile uint32_t*>(p.vpf_abort) == ep) break;
-          if (globaltimer_ns() - t0 > kVpfTimeoutNs) {
-            set_error(p.err, OTK_ERR_PEER_TIMEOUT);
-            *reinterpret_cast<volatile uint32_t*>(p.vpf_abort) = ep;
-            break;
-          }
+  float4 rec = make_float4(-INFINITY, 0.f, 0.f, -INFINITY);
+  if (lane == me) {
+    rec = mine;
+  } else if (lane < P) {
+    const char* r = own + vpf_rec_index(cap, P, par, row, lane) * 32;
+    uint64_t a0, a1, a2, a3;
+    auto ready = [&]() {
+      ld_pair_sys(r, a0, a1);
+      ld_pair_sys(r + 16, a2, a3);
+      return uint32_t(a0 >> 32) == ep && uint32_t(a1 >> 32) == ep && uint32_t(a2 >> 32) == ep &&
+             uint32_t(a3 >> 32) == ep;
+    };
+    bool ok = ready();
+    if (!ok) {
+      const uint64_t t0 = globaltimer_ns();
+      while (!(ok = ready())) {
+        // only a peer timeout of THIS call ends the wait early (a data error elsewhere never does: every
+        // valid row still gets its peers' partials)
+        if (*reinterpret_cast<volatile uint32_t*>(p.vpf_abort) == ep) break;
+        if (globaltimer_ns() - t0 > kVpfTimeoutNs) {
+          set_error(p.err, OTK_ERR_PEER_TIMEOUT);
+          *reinterpret_cast<volatile uint32_t*>(p.vpf_abort) = ep;
+          break;
         }
       }
-      rec[q] = ok ? make_float4(__uint_as_float(uint32_t(a0)), __uint_as_float(uint32_t(a1)),
-                                __uint_as_float(uint32_t(a2)), __uint_as_float(uint32_t(a3)))
-                  : make_float4(-INFINITY, 0.f, 0.f, -INFINITY);
     }
-    tot = combine(tot, Stat{rec[q].x, rec[q].y, rec[q].z});
+    if (ok)
+      rec = make_float4(__uint_as_float(uint32_t(a0)), __uint_as_float(uint32_t(a1)), __uint_as_float(uint32_t(a2)),
+                        __uint_as_float(uint32_t(a3)));
   }
-  dy = -INFINITY;
-  for (int q = 0; q < P; ++q)
-    if (rec[q].w != -INFINITY) dy = __fadd_rn(rec[q].w, __fsub_rn(rec[q].x, tot.m));
+  __syncwarp();
+  Stat tot{-INFINITY, 0.f, 0.f};
+  float wsel = -INFINITY, xsel = 0.f;
+  for (int q = 0; q < P; ++q) {
+    const float rx = __shfl_sync(0xffffffffu, rec.x, q), ry = __shfl_sync(0xffffffffu, rec.y, q),
+                rz = __shfl_sync(0xffffffffu, rec.z, q), rw = __shfl_sync(0xffffffffu, rec.w, q);
+    tot = combine(tot, Stat{rx, ry, rz});
+    if (rw != -INFINITY) {  // the rank holding the target column (one)
+      wsel = rw;
+      xsel = rx;
+    }
+  }
+  dy = wsel == -INFINITY ? -INFINITY : __fadd_rn(wsel, __fsub_rn(xsel, tot.m));  // m_k - M exact (Sterbenz)
   return tot;
 }
 
@@ -214,12 +223,13 @@ __device__ __forceinline__ void vpf_window(const RowParams& p, uint32_t ep) {
   }
 }
 
-// Called by one thread per CTA (ct == 0) after the CTA's (cluster's) row total: push (cluster rank 0 only),
-// then collect and combine.
+// Called by one warp per CTA after the CTA's (cluster's) row total: push (lane 0 of cluster rank 0), then collect
+// and combine (the whole warp).
 __device__ __forceinline__ Stat vpf_exchange(const RowParams& p, int64_t row, uint32_t crank, float4 mine, float& dy,
-                                             uint32_t ep) {
-  if (crank == 0) vpf_push(p, row, mine, ep);
-  return vpf_collect(p, row, mine, dy, ep);
+                                             uint32_t ep, int lane) {
+  if (crank == 0 && lane == 0) vpf_push(p, row, mine, ep);
+  __syncwarp();
+  return vpf_collect(p, row, mine, dy, ep, lane);
 }
 
 // One element pair of pass 1: d = s2*x - m; e = 2^d; S += e; T += e*d (per-lane fp32 chains; kInit starts
@@ -411,6 +421,15 @@ struct Smem {
   float4 fred[4][kConsumerWarps];
   float4 rowbc[2];                    // (stream kernel) row broadcast
   float4 vbc[2];                      // (K4-VPF) the rank-order row total + dy, broadcast by thread 0
+  struct Pend {                       // (pipelined loop) a row whose stage B is pending, by active-row index mod 4
+    int64_t row, nb;                  // row < 0: end of this CTA's rows (K4-VPF collector)
+    double A;
+    float old_lp, ref_lp, rm, rs, rt, xy, dyl;
+    int32_t y, ylc, owner, side_ok;
+  } pend[4];
+  uint64_t pfull[4];                  // (pipelined K4-VPF) pend[k] written (thread 0 -> collector warp)
+  uint64_t cfull[4];                  // (pipelined K4-VPF) the rank-order total of row k is in ctot[k]
+  float4 ctot[4];
   uint32_t tmem_base;
   long long load_row;                 // the loader's current row (zero-fill pacing; INT64_MAX when done)
 };
@@ -676,6 +695,8 @@ __device__ __forceinline__ void row_kernel_setup(Smem& S, uint8_t* zero, int war
     for (int i = 0; i < 4; ++i) {
       mbar_init(&S.ffull[i], kConsumerWarps);
       mbar_init(&S.fempty[i], 1);
+      mbar_init(&S.pfull[i], 1);
+      mbar_init(&S.cfull[i], 1);
     }
     S.load_row = -1;
     fence_mbar_init();
@@ -1002,7 +1023,18 @@ __device__ __forceinline__ void pass1_chunk(Smem& S, const uint8_t* ring, uint32
 // pass 1. Cluster mailboxes are indexed by active-row index mod 4: a peer can be at most 3 rows ahead of the
 // row being read (its A(r+4) needs our A(r+2), which follows our B(r)).
 // =====================================================================================================
-constexpr int kPipeHalf = 64;                   // TMEM columns per half: [0, 56) e, [56, 63) m_c
+// Generalised to a lag of L rows (template kLag): L + 1 row slots in the warp's TMEM window, stage B(r - L) after
+// stage A(r), so L whole passes 1 hide a row's exchange and the skew between the ranks sharing it. Lag 1: slots
+// of 64 columns (segments <= 7 chunks: K4-VPF P = 4 at V = 151936); lag 3: four slots of 42 columns (<= 4 chunks:
+// P >= 8).
+template <int kLag>
+struct PipeCfg {
+  static constexpr int kSlotCols = kLag == 1 ? 64 : 42;          // TMEM columns per row slot
+  static constexpr int kMaxCh = kLag == 1 ? kPipeChunks : 4;      // chunks per row segment
+  static constexpr int kColM = 8 * kMaxCh;                        // [0, kColM) e, then one m_c column per chunk
+  static_assert((kLag + 1) * kSlotCols <= kTmemWindow && kColM + kMaxCh <= kSlotCols, "TMEM slots");
+  static_assert(kLag == 1 || kLag == 3, "lag 1 or 3 (slot index = q & kLag)");
+};
 
 struct PipeRow {
   int64_t row;
@@ -1015,7 +1047,7 @@ struct PipeRow {
   bool side_ok;
 };
 
-template <typename T, int MODE>
+template <typename T, int MODE, int kLag>
 __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8_t* ring, int warp, int lane,
                                               int csize, uint32_t crank, int64_t group, int64_t ngroups, int64_t c0,
                                               int segn, int nch, unsigned vblock, unsigned vgrid) {
@@ -1023,8 +1055,8 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
   using VT = Vec<T>;
   constexpr int EV = VT::EV;
   constexpr int CE = kChunkBytes / int(sizeof(T));
-  constexpr int kColM = 8 * kPipeChunks;
-  static_assert(2 * kPipeHalf <= kTmemWindow && kColM + kPipeChunks <= kPipeHalf, "TMEM halves");
+  constexpr int kColM = PipeCfg<kLag>::kColM;
+  constexpr int kSlotCols = PipeCfg<kLag>::kSlotCols;
   const int ct = threadIdx.x - 32;
   const int cw = warp - 1;
   const uint32_t tm0 = S.tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(kTmemWindow * (cw >> 2));
@@ -1035,11 +1067,24 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
   const float invN = nl > 0 ? float(1.0 / double(nl)) : 0.f;
   const int64_t nact = p.reduction != OTK_TOKEN_MEAN ? *p.n_active : 0;
   uint32_t slot = 0, phase = 0, q = 0;
-  const uint32_t vep = (kVpf && ct == 0) ? vpf_epoch(p) : 0u;  // read before this CTA takes its ticket
+  const uint32_t vep = (kVpf && ct < 32) ? vpf_epoch(p) : 0u;  // the collecting warp, before the ticket
   if (kVpf && ct == 0) vpf_window(p, vep);
 
-  // ---- stage B: the previous row's statistics, loss and pass 2 -----------------------------------------
-  auto stage_b = [&](const PipeRow& pr) {
+  // ---- stage B: a pending row's statistics, loss and pass 2 (its record in S.pend, written by thread 0 in its
+  // stage A, kLag rows ago — named barriers in between; the slot is rewritten only after every thread has passed
+  // the next stage A's barrier, i.e. left this stage B)
+  auto stage_b = [&](uint32_t qb) {
+    const Smem::Pend& pe = S.pend[qb & 3u];
+    PipeRow pr;
+    pr.row = pe.row;
+    pr.sd = RowSide{pe.A, pe.old_lp, pe.ref_lp, pe.nb};
+    pr.r = Stat{pe.rm, pe.rs, pe.rt};
+    pr.xy = pe.xy;
+    pr.y = pe.y;
+    pr.ylc = pe.ylc;
+    pr.owner = pe.owner;
+    pr.q = qb;
+    pr.side_ok = pe.side_ok != 0;
     const uint32_t k = pr.q & 3u;
     Stat tot;
     if (csize > 1) {
@@ -1054,14 +1099,9 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
     }
     const int64_t yg = int64_t(pr.y) - p.vocab_start;
     float dy = (yg >= 0 && yg < p.vocab) ? __fmaf_rn(pr.xy, s2, -tot.m) : -INFINITY;
-    if constexpr (kVpf) {  // csize 1 here: the push went out in stage A
-      if (ct == 0) {
-        float gdy;
-        const Stat g = vpf_collect(p, pr.row, make_float4(tot.m, tot.s, tot.t, dy), gdy, vep);
-        S.vbc[pr.q & 1u] = make_float4(g.m, g.s, g.t, gdy);
-      }
-      named_bar_sync(2, kNCT);
-      const float4 b = S.vbc[pr.q & 1u];
+    if constexpr (kVpf) {  // csize 1 here: pushed in stage A, collected by the collector warp meanwhile
+      mbar_wait(&S.cfull[k], (pr.q >> 2) & 1u);
+      const float4 b = S.ctot[k];
       tot = Stat{b.x, b.y, b.z};
       dy = b.w;
     }
@@ -1078,7 +1118,7 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
       if (p.logp) p.logp[pr.row] = pr.side_ok ? rs.logp : 0.f;
       if (p.entropy) p.entropy[pr.row] = pr.side_ok ? rs.H : 0.f;
     }
-    const uint32_t tm = tm0 + (pr.q & 1u) * kPipeHalf;
+    const uint32_t tm = tm0 + (pr.q & uint32_t(kLag)) * kSlotCols;
     char* drow = reinterpret_cast<char*>(p.dlogits) + (pr.row * p.ld + c0) * int64_t(sizeof(T));
     pass2_row<T, kColM>(drow, tm, ct, nch, segn, rs, lo);
     if (ct == pr.owner) VT::store1(drow, pr.ylc, lo.gy);
@@ -1100,8 +1140,7 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
     return (g >= 0 && g < p.vocab) ? VT::load1(p.logits, r * p.ld + g) : 0.f;
   };
   float xy_n = (row < p.num_rows && row_active(p, y_n, m_n)) ? xy_of(row, y_n) : 0.f;
-  PipeRow prev;
-  bool has_prev = false;
+  int npend = 0;  // rows whose stage B is pending: active-row indices q - npend .. q - 1
   for (; row < p.num_rows; row += ngroups) {
     const int32_t y = y_n;
     const uint8_t m = m_n;
@@ -1124,7 +1163,7 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
     const int64_t ylc64 = int64_t(y) - p.vocab_start - c0;
     const int ylc = (ylc64 >= 0 && ylc64 < segn) ? int(ylc64) : -1;
     const bool side_ok = row_side(p, row, rt, sd, ct == 0 && crank == 0);
-    const uint32_t tm = tm0 + (q & 1u) * kPipeHalf;
+    const uint32_t tm = tm0 + (q & uint32_t(kLag)) * kSlotCols;
 
     // ---------------- stage A: pass 1 into TMEM half (q & 1) (same arithmetic as the unpipelined loop)
     uint64_t rS = 0ull, rT = 0ull;
@@ -1163,15 +1202,43 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
         const int64_t yg = int64_t(y) - p.vocab_start;
         const float dyl = (yg >= 0 && yg < p.vocab) ? __fmaf_rn(xy, s2, -r.m) : -INFINITY;
         vpf_push(p, row, make_float4(r.m, r.s, r.t, dyl), vep);
+        S.pend[q & 3u].dyl = dyl;
       }
     }
-    // ---------------- stage B of the previous row (its partials have had a whole pass 1 to arrive)
-    if (has_prev) stage_b(prev);
-    prev = PipeRow{row, sd, r, xy, y, ylc, ylc >= 0 ? ((ylc % CE) / EV) % kNCT : -1, q, side_ok};
-    has_prev = true;
+    if (ct == 0) {
+      Smem::Pend& pe = S.pend[q & 3u];
+      pe.row = row;
+      pe.nb = sd.nb;
+      pe.A = sd.A;
+      pe.old_lp = sd.old_lp;
+      pe.ref_lp = sd.ref_lp;
+      pe.rm = r.m;
+      pe.rs = r.s;
+      pe.rt = r.t;
+      pe.xy = xy;
+      pe.y = y;
+      pe.ylc = ylc;
+      pe.owner = ylc >= 0 ? ((ylc % CE) / EV) % kNCT : -1;
+      pe.side_ok = side_ok ? 1 : 0;
+      if constexpr (kVpf) mbar_arrive(&S.pfull[q & 3u]);  // the collector may start on this row
+    }
+    // ---------------- stage B of the row kLag rows back (its partials have had kLag passes 1 to arrive)
+    if (npend == kLag) {
+      stage_b(q - uint32_t(kLag));
+      --npend;
+    }
+    ++npend;
     ++q;
   }
-  if (has_prev) stage_b(prev);
+  // thread 0 wrote the last pending record after the last stage A's barrier: one more barrier before reading it
+  named_bar_sync(1, kNCT);
+  if constexpr (kVpf) {
+    if (ct == 0) {  // end of rows for the collector (slot q & 3 was last read in stage B(q - 4), before the barrier)
+      S.pend[q & 3u].row = -1;
+      mbar_arrive(&S.pfull[q & 3u]);
+    }
+  }
+  for (; npend > 0; --npend) stage_b(q - uint32_t(npend));
   if (ct == 0) stats_epilogue(p, acc_L, acc_clip, acc_kl, acc_H, acc_n, nl, vblock, vgrid, vep);
 }
 
@@ -1181,7 +1248,28 @@ __device__ __forceinline__ void consumer_pipe(const RowParams& p, Smem& S, uint8
 // running max after chunk c) and m_c are parked in TENSOR MEMORY, so pass 2 needs no second read of the
 // logits and no second exponential: softmax = e * 2^(m_c - lse).
 // =====================================================================================================
-template <typename T, int MODE, bool kPipe>
+// Pipelined K4-VPF collector (warp kConsumerWarps + 2): for each active row in order, once thread 0 has pushed
+// the row's partial and recorded it in S.pend, wait for the P - 1 peer records (lane q: peer q), combine them in
+// rank order and hand the total to stage B through S.ctot / S.cfull — the round trips to peer memory run beside
+// the consumers' passes instead of in front of every stage B.
+__device__ __forceinline__ void vpf_collector(const RowParams& p, Smem& S, int lane) {
+  const uint32_t ep = vpf_epoch(p);  // before this CTA's ticket (taken by thread 0 of the consumers at the end)
+  for (uint32_t k = 0;; ++k) {
+    mbar_wait(&S.pfull[k & 3u], (k >> 2) & 1u);
+    const Smem::Pend& pe = S.pend[k & 3u];
+    const int64_t row = pe.row;
+    if (row < 0) break;
+    float gdy;
+    const Stat g = vpf_collect(p, row, make_float4(pe.rm, pe.rs, pe.rt, pe.dyl), gdy, ep, lane);
+    if (lane == 0) {
+      S.ctot[k & 3u] = make_float4(g.m, g.s, g.t, gdy);
+      mbar_arrive(&S.cfull[k & 3u]);
+    }
+    __syncwarp();
+  }
+}
+
+template <typename T, int MODE, int kPipe>
 __device__ __forceinline__ void rows_tm_body(const RowParams& p, unsigned vblock, unsigned vgrid) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr bool kVpf = (MODE == kModeBwdVpf);  // BWD with the vocab-shard exchange fused in
@@ -1220,8 +1308,10 @@ __device__ __forceinline__ void rows_tm_body(const RowParams& p, unsigned vblock
       finalize_rows<T, MODE>(p, S, lane, csize, crank, group, ngroups);
     }
     __syncwarp();
-  } else if constexpr (kPipe) {
-    consumer_pipe<T, MODE>(p, S, ring, warp, lane, csize, crank, group, ngroups, c0, segn, nch, vblock, vgrid);
+  } else if (warp == kConsumerWarps + 2) {
+    if constexpr (kVpf && kPipe > 0) vpf_collector(p, S, lane);  // the 15th warp exists for these kernels only
+  } else if constexpr (kPipe > 0) {
+    consumer_pipe<T, MODE, kPipe>(p, S, ring, warp, lane, csize, crank, group, ngroups, c0, segn, nch, vblock, vgrid);
   } else {
     const int ct = threadIdx.x - 32;
     const int cw = warp - 1;
@@ -1240,7 +1330,7 @@ __device__ __forceinline__ void rows_tm_body(const RowParams& p, unsigned vblock
     }
     uint32_t slot = 0, phase = 0, q = 0;
     uint32_t fs = 0, fph = 0;  // FWD / PARTIAL: hand-off ring to the finalizer warp
-    const uint32_t vep = (kVpf && ct == 0) ? vpf_epoch(p) : 0u;  // read before this CTA takes its ticket
+    const uint32_t vep = (kVpf && ct < 32) ? vpf_epoch(p) : 0u;  // the collecting warp, before the ticket
     if (kVpf && ct == 0) vpf_window(p, vep);
 
     int64_t row = group;
@@ -1345,10 +1435,10 @@ __device__ __forceinline__ void rows_tm_body(const RowParams& p, unsigned vblock
 #endif
       float dy = (yg >= 0 && yg < p.vocab) ? __fmaf_rn(xy, s2, -tot.m) : -INFINITY;
       if constexpr (kVpf) {  // this rank's partial -> peers; peers' partials -> rank-order total (global row)
-        if (ct == 0) {
+        if (ct < 32) {
           float gdy;
-          const Stat g = vpf_exchange(p, row, crank, make_float4(tot.m, tot.s, tot.t, dy), gdy, vep);
-          S.vbc[q & 1u] = make_float4(g.m, g.s, g.t, gdy);
+          const Stat g = vpf_exchange(p, row, crank, make_float4(tot.m, tot.s, tot.t, dy), gdy, vep, lane);
+          if (ct == 0) S.vbc[q & 1u] = make_float4(g.m, g.s, g.t, gdy);
         }
         named_bar_sync(2, kNCT);
         const float4 b = S.vbc[q & 1u];
@@ -1415,8 +1505,8 @@ __device__ __forceinline__ void rows_tm_body(const RowParams& p, unsigned vblock
   }
 }
 
-template <typename T, int MODE, bool kPipe = false>
-__global__ void __launch_bounds__(kThreads, 1) k_rows_tm(const RowParams p) {
+template <typename T, int MODE, int kPipe = 0>
+__global__ void __launch_bounds__(kThreads + (kPipe > 0 ? 32 : 0), 1) k_rows_tm(const RowParams p) {
   rows_tm_body<T, MODE, kPipe>(p, blockIdx.x, gridDim.x);
 }
 
@@ -1429,8 +1519,8 @@ struct RowParamsSet {
   int nsets;
   int blocks_per_set;
 };
-template <typename T, bool kPipe>
-__global__ void __launch_bounds__(kThreads, 1) k_rows_vpf_group(const __grid_constant__ RowParamsSet ps) {
+template <typename T, int kPipe>
+__global__ void __launch_bounds__(kThreads + (kPipe > 0 ? 32 : 0), 1) k_rows_vpf_group(const __grid_constant__ RowParamsSet ps) {
   const unsigned set = blockIdx.x / unsigned(ps.blocks_per_set);
   rows_tm_body<T, kModeBwdVpf, kPipe>(ps.p[set], blockIdx.x - set * unsigned(ps.blocks_per_set),
                                        unsigned(ps.blocks_per_set));
@@ -1613,13 +1703,13 @@ static int max_resident_clusters(KernelT kern, int dev, int csize, size_t smem, 
 template <typename KernelT>
 static cudaError_t launch_row_kernel(KernelT kern, const otk_ctx* ctx, const RowParams& p, cudaStream_t s,
                                      int* grid_out, size_t smem_bytes = kSmemBytes, int ctas_per_sm = 1,
-                                     int max_ctas = 0) {
+                                     int max_ctas = 0, int threads = kThreads) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes));
   if (e != cudaSuccess) return e;
   int64_t groups = int64_t(ctx->num_sms) * ctas_per_sm / p.csize;
   if (max_ctas > 0 && groups > max_ctas / p.csize) groups = max_ctas / p.csize;  // ranks sharing a GPU
   cudaLaunchConfig_t cfg{};
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -1654,8 +1744,12 @@ cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const
       case kModeBwd: return launch_row_kernel(k_rows_tm<B, kModeBwd>, ctx, p, s, grid_out);
       case kModeBwdPartials: return launch_row_kernel(k_rows_stream<B>, ctx, p, s, grid_out);
       case kModeBwdVpf:
+        if (p.pipe == 3)
+          return launch_row_kernel(k_rows_tm<B, kModeBwdVpf, 3>, ctx, p, s, grid_out, kSmemBytes, 1, max_ctas,
+                                   kThreads + 32);
         if (p.pipe)
-          return launch_row_kernel(k_rows_tm<B, kModeBwdVpf, true>, ctx, p, s, grid_out, kSmemBytes, 1, max_ctas);
+          return launch_row_kernel(k_rows_tm<B, kModeBwdVpf, 1>, ctx, p, s, grid_out, kSmemBytes, 1, max_ctas,
+                                   kThreads + 32);
         return launch_row_kernel(k_rows_tm<B, kModeBwdVpf>, ctx, p, s, grid_out, kSmemBytes, 1, max_ctas);
     }
   } else {
@@ -1665,8 +1759,12 @@ cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const
       case kModeBwd: return launch_row_kernel(k_rows_tm<float, kModeBwd>, ctx, p, s, grid_out);
       case kModeBwdPartials: return launch_row_kernel(k_rows_stream<float>, ctx, p, s, grid_out);
       case kModeBwdVpf:
+        if (p.pipe == 3)
+          return launch_row_kernel(k_rows_tm<float, kModeBwdVpf, 3>, ctx, p, s, grid_out, kSmemBytes, 1, max_ctas,
+                                   kThreads + 32);
         if (p.pipe)
-          return launch_row_kernel(k_rows_tm<float, kModeBwdVpf, true>, ctx, p, s, grid_out, kSmemBytes, 1, max_ctas);
+          return launch_row_kernel(k_rows_tm<float, kModeBwdVpf, 1>, ctx, p, s, grid_out, kSmemBytes, 1, max_ctas,
+                                   kThreads + 32);
         return launch_row_kernel(k_rows_tm<float, kModeBwdVpf>, ctx, p, s, grid_out, kSmemBytes, 1, max_ctas);
     }
   }
@@ -1676,7 +1774,7 @@ cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const
 // K4-VPF ranks emulated in one launch: blocks_per_set = the SMs / nsets (one CTA per SM, a multiple of the cluster
 // size), so the whole grid is one resident wave; csize 1 launches cooperatively (the driver refuses a grid that
 // cannot be co-resident), csize > 1 checks the resident-cluster count.
-cudaError_t launch_rows_vpf_group(const otk_ctx* ctx, otk_dtype dtype, const RowParams* ps, int nsets, bool pipe,
+cudaError_t launch_rows_vpf_group(const otk_ctx* ctx, otk_dtype dtype, const RowParams* ps, int nsets, int pipe,
                                   cudaStream_t s, int* grid_out) {
   RowParamsSet set;
   std::memset(&set, 0, sizeof(set));
@@ -1694,7 +1792,7 @@ cudaError_t launch_rows_vpf_group(const otk_ctx* ctx, otk_dtype dtype, const Row
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes));
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(kThreads + (pipe ? 32 : 0));  // + the collector warp of the pipelined loop
     cfg.dynamicSmemBytes = kSmemBytes;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -1720,9 +1818,10 @@ cudaError_t launch_rows_vpf_group(const otk_ctx* ctx, otk_dtype dtype, const Row
   };
   if (dtype == OTK_BF16) {
     using B = __nv_bfloat16;
-    return pipe ? go(k_rows_vpf_group<B, true>) : go(k_rows_vpf_group<B, false>);
+    return pipe == 3 ? go(k_rows_vpf_group<B, 3>) : pipe ? go(k_rows_vpf_group<B, 1>) : go(k_rows_vpf_group<B, 0>);
   }
-  return pipe ? go(k_rows_vpf_group<float, true>) : go(k_rows_vpf_group<float, false>);
+  return pipe == 3 ? go(k_rows_vpf_group<float, 3>) : pipe ? go(k_rows_vpf_group<float, 1>)
+                                                       : go(k_rows_vpf_group<float, 0>);
 }
 
 // several partials of one row (e.g. the vocab chunks of the fused LM head on one rank) -> one partial of the

@@ -675,7 +675,14 @@ static otk_status vpf_params(otk_ctx* ctx, int64_t num_rows, int64_t vocab_local
   p.vpf_rows_cap = peers->rows_cap;
   // pipelined loop (exchange latency hidden behind the next row's pass 1) when a CTA holds the whole shard row
   // and two rows fit its tensor memory
-  p.pipe = csize == 1 && int64_t(seg) * int64_t(dtype_size(dtype)) <= int64_t(otk::kPipeChunks) * otk::kChunkBytes;
+  {
+    const int64_t seg_bytes = int64_t(seg) * int64_t(dtype_size(dtype));
+    p.pipe = csize != 1 ? 0 : seg_bytes <= 4 * int64_t(otk::kChunkBytes) ? 3
+                               : seg_bytes <= int64_t(otk::kPipeChunks) * otk::kChunkBytes ? 1 : 0;
+  }
+#ifdef OTK_VPF_LAG1  // experiment builds only: the lag-1 pipeline for every segment that fits it
+  if (p.pipe == 3) p.pipe = 1;
+#endif
 #ifdef OTK_VPF_NOPIPE  // experiment builds only: measure the unpipelined loop
   p.pipe = 0;
 #endif
@@ -726,7 +733,7 @@ otk_status otk_policy_loss_fwd_bwd_vpf_group(int32_t nranks, const otk_vpf_rank_
     OTK_REQUIRE(ps[k].csize == ps[0].csize && ps[k].pipe == ps[0].pipe, OTK_ERR_SHAPE,
                 "every rank's shard must use the same cluster size and loop (near-equal shard widths)");
   }
-  OTK_CUDA(otk::launch_rows_vpf_group(calls[0].ctx, dtype, ps, nranks, ps[0].pipe != 0,
+  OTK_CUDA(otk::launch_rows_vpf_group(calls[0].ctx, dtype, ps, nranks, ps[0].pipe,
                                       reinterpret_cast<cudaStream_t>(stream), nullptr),
            "k_rows_vpf_group launch (all ranks co-resident)");
   calls[0].ctx->launches += 1;

@@ -65,7 +65,8 @@ struct RowParams {
   int64_t vocab_total;   // global vocabulary (target range check)
   int seg_elems;         // per-CTA column segment (multiple of 8) when the cluster splits a row
   int csize;             // CTAs per row (cluster size)
-  int pipe;              // BWD_VPF: pipelined consumer loop (csize 1, segment <= kPipeChunks chunks)
+  int pipe;              // BWD_VPF: pipelined consumer loop, lag in rows (csize 1): 3 for segments <= 4 chunks,
+                         // 1 for <= kPipeChunks, 0 = unpipelined
   // forward outputs
   float* logp;
   float* entropy;
@@ -108,7 +109,7 @@ struct RowParams {
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_rows(const otk_ctx* ctx, RowMode mode, otk_dtype dtype, const RowParams& p, cudaStream_t s,
                         int* grid_out, int max_ctas = 0);
-cudaError_t launch_rows_vpf_group(const otk_ctx* ctx, otk_dtype dtype, const RowParams* ps, int nsets, bool pipe,
+cudaError_t launch_rows_vpf_group(const otk_ctx* ctx, otk_dtype dtype, const RowParams* ps, int nsets, int pipe,
                                   cudaStream_t s, int* grid_out);
 cudaError_t launch_combine(const otk_ctx* ctx, int64_t num_rows, int nshards, const float4* partials,
                            const uint8_t* row_mask, float* logp, float* entropy, float* lse, cudaStream_t s);
