@@ -468,12 +468,24 @@ static cudaError_t launch_lane_strided(otk_ctx* ctx, SampleParams p, cudaStream_
 }
 
 cudaError_t launch_sample(otk_ctx* ctx, const SampleParams& p0, int dtype, cudaStream_t s) {
+#ifndef OTK_SAMPLE_NO_DEC
+  // decode batches (<= num_sms / 4 rows, the row range of each CTA held in shared memory): k_sample_dec
+  {
+    int csize = 0, nseg_c = 0;
+    if (sample_dec_shape(p0.num_rows, p0.vocab, dtype, ctx->num_sms, &csize, &nseg_c))
+      return launch_sample_dec(ctx, p0, dtype, csize, nseg_c, s);
+  }
+#endif
 #ifndef OTK_SAMPLE_V1
   // sampled draws from one SM's worth of rows up: the ring-streamed kernel, one CTA per row, with an off-path
   // search warp (k_sample_tm.cu; 256 rows 22.9 vs 25.1 us, 4096 rows 218 vs 262 us). Smaller batches keep the
   // cluster-split kernel below (a cluster-split version of the ring kernel measured no faster at 16-128 rows);
   // greedy stays here at every size (its lane-strided pass measured faster: 225 vs 272 us at 4096 rows).
-  if (!p0.greedy && p0.num_rows >= ctx->num_sms && sample_tm_fits(p0.vocab, dtype))
+#ifndef OTK_SAMPLE_TM_MIN_ROWS
+#define OTK_SAMPLE_TM_MIN_ROWS 96  // 96 rows: 17.0 vs 21.3 us lane-strided; 128 rows 17.2 vs 16.5 (even)
+#endif
+  if (!p0.greedy && p0.num_rows >= std::min<int64_t>(ctx->num_sms, OTK_SAMPLE_TM_MIN_ROWS) &&
+      sample_tm_fits(p0.vocab, dtype))
     return launch_sample_tm(ctx, p0, dtype, s);
 #endif
   // lane-strided kernel; at <= 64 rows with twice the registers per thread (2 resident CTAs per SM: 16 rows

@@ -176,6 +176,8 @@ struct SampleParams {
 cudaError_t launch_sample(otk_ctx* ctx, const SampleParams& p, int dtype, cudaStream_t s);
 constexpr int kSampleTmMaxChunks = 64;   // k_sample_tm: rows of <= 64 x 12 KB (bf16 V <= 393216, fp32 V <= 196608)
 bool sample_tm_fits(int64_t vocab, int dtype);
+bool sample_dec_shape(int64_t num_rows, int64_t vocab, int dtype, int num_sms, int* csize, int* nseg_c);
+cudaError_t launch_sample_dec(otk_ctx* ctx, SampleParams p, int dtype, int csize, int nseg_c, cudaStream_t s);
 cudaError_t launch_sample_tm(otk_ctx* ctx, const SampleParams& p, int dtype, cudaStream_t s);
 
 int lmhead_chunks(int64_t num_rows, int64_t vocab, int num_sms);

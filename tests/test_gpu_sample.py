@@ -206,3 +206,58 @@ def test_sampled_degenerate_rows_ring_kernel(otk, ctx, dtype, V):
     rows = list(range(8, n, 7))
     exact = _check_sampled(tok, lp, wide, u.double().numpy(), 1.0, dtype, rows)
     assert exact >= 0.9 * len(rows)
+
+
+@pytest.mark.parametrize("dtype,V,n", [("bf16", 151936, 16), ("bf16", 151936, 37), ("bf16", 151936, 1),
+                                       ("f32", 50000, 30), ("bf16", 4100, 9), ("bf16", 17, 5),
+                                       ("bf16", 151936, 100)])   # 100 rows: the ring kernel
+def test_decode_batches(otk, ctx, dtype, V, n):
+    """Decode-sized batches (<= 37 rows: k_sample_dec, one row per cluster, each CTA's column range held in shared memory;
+    96-147 rows: the ring kernel):
+    sampled draws vs the oracle, greedy bit-exact, degenerate rows, and single finite columns at the first / last
+    column and at the boundaries between the cluster's CTA ranges (u = 0 and u -> 1)."""
+    ld = -(-V // 8) * 8
+    logits, _ = make_logits(n, V, ld=ld if ld != V else None, dtype=dtype, seed=V % 89 + n, device="cpu")
+    x = logits.clone()[:, :V]
+    C = min(8, 148 // n)
+    es = 2 if dtype == "bf16" else 4
+    per = -(-(-(-(V * es) // 16) // 64) // C) * 64 * 16 // es     # columns per CTA range (whole 1 KB segments)
+    special = {}
+    if n >= 5:
+        x[0, :] = float("-inf")
+        special[0] = None
+        for j, col in ((1, 0), (2, V - 1), (3, min(per, V - 1)), (4, max(min(per, V - 1) - 1, 0))):
+            x[j, :] = float("-inf")
+            x[j, col] = 3.0
+            special[j] = col
+    if n >= 7:
+        x[5, : V // 2] = -80.0
+        x[5, V // 2:] = 60.0
+        x[6, :] = -200.0
+        x[6, V - 3] = 150.0
+        special[6] = V - 3
+    u = torch.rand(n, generator=torch.Generator().manual_seed(n)).float()
+    if n >= 5:
+        u[1:3] = 0.0
+        u[3:5] = 1.0 - 2 ** -24
+    xp = torch.full((n, ld), float("nan"), dtype=x.dtype)        # padding columns never read
+    xp[:, :V] = x
+    out = otk.otk_sample_tokens(ctx, xp.cuda(), u.cuda(), vocab=V)
+    g = otk.otk_sample_tokens(ctx, xp.cuda(), greedy=True, vocab=V)
+    ctx.check()
+    tok, lp = out["tokens"].cpu().numpy(), out["logp"].cpu().numpy()
+    gt, glp = g["tokens"].cpu().numpy(), g["logp"].cpu().numpy()
+    wide = x.double().numpy()
+    for j, col in special.items():
+        if col is None:
+            assert tok[j] == 0 and lp[j] == float("-inf") and gt[j] == 0 and glp[j] == float("-inf")
+        else:
+            assert tok[j] == col and gt[j] == col, (j, tok[j], gt[j], col)
+    if n >= 7:
+        assert V // 2 <= tok[5] < V
+    rows = [j for j in range(n) if j not in special and j != 5]
+    exact = _check_sampled(tok, lp, wide, u.double().numpy(), 1.0, dtype, rows)
+    assert exact >= 0.9 * len(rows)
+    for j in rows:
+        assert gt[j] == int(np.argmax(wide[j])), j
+        assert abs(float(glp[j]) - O.sample_token(wide[j], 0.0, greedy=True)[1]) < LOGP_TOL[dtype]
