@@ -402,8 +402,9 @@ def run_otk(args):
 # ------------------------------------------------------------------------------------------------
 def other_kernels(W, step, cfg):
     """Side measurements (untimed for the headline, rank 0, N = 1): the forward (3) on one micro-batch, the
-    rollout sampler (NEXT-3) on a 4096-row decode batch and the fused LM-head forward (NEXT-1) at d = 3584 —
-    CUDA events on the launching stream, inputs HBM-resident, each against its own roofline."""
+    rollout sampler (NEXT-3) on 4096- and 16-row decode batches, K4-VPF with P = 2, 4, 8 ranks emulated on this GPU,
+    the fused LM-head forward (NEXT-1) at d = 3584 and the policy loss through the LM head (NEXT-1 fwd + bwd) at
+    d = 1024 / 3584 against cuBLAS + (4) — CUDA events on the launching stream, inputs HBM-resident."""
     otk, ctx, V = W["otk"], W["ctx"], W["V"]
     hbm, _ = peaks()
     bf16_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]) \
@@ -446,22 +447,30 @@ def other_kernels(W, step, cfg):
     adv, nl = step.adv_out["adv"], step.masks["n_loss"]
     ms_u = timed(lambda i: otk.otk_policy_loss_fwd_bwd(ctx, mb.logits, mb.targets, lm, rt, adv, mb.old_logp,
                                                        mb.ref_logp, nl, cfg, dlogits=mb.dlogits, want_logp=False), 4)
-    P = 2
-    b = [V * k // P // 8 * 8 for k in range(P)] + [V]
-    ctxs = [otk.Context(ctx.device) for _ in range(P)]
-    xs = otk.VpfExchange.local_group(ctxs, M)
+    for P in (2, 4, 8):
+        b = [V * k // P // 8 * 8 for k in range(P)] + [V]
+        ctxs = [otk.Context(ctx.device) for _ in range(P)]
+        xs = otk.VpfExchange.local_group(ctxs, M)
 
-    def vpf(i):
-        otk.otk_policy_loss_fwd_bwd_vpf_group(ctxs, [mb.logits[:, b[q]:b[q + 1]] for q in range(P)], mb.targets, lm,
-                                              rt, adv, mb.old_logp, mb.ref_logp, nl, cfg, b[:P], V, xs,
-                                              dlogits=[mb.dlogits[:, b[q]:b[q + 1]] for q in range(P)])
-    ms_v = timed(vpf, 4)
-    for c in ctxs:
-        c.check()
-    for x in xs:
-        x.close()
-    out["vocab_shard_vpf_p2_one_gpu"] = {"rows": M, "ms": ms_v, "ms_unsharded": ms_u, "vs_unsharded": ms_u / ms_v,
-                                         "kernel": "k_rows_vpf_group<bf16>: 2 ranks in one launch (DESIGN.md §7)"}
+        def vpf(i):
+            otk.otk_policy_loss_fwd_bwd_vpf_group(ctxs, [mb.logits[:, b[q]:b[q + 1]] for q in range(P)], mb.targets,
+                                                  lm, rt, adv, mb.old_logp, mb.ref_logp, nl, cfg, b[:P], V, xs,
+                                                  dlogits=[mb.dlogits[:, b[q]:b[q + 1]] for q in range(P)])
+        ms_v = timed(vpf, 4)
+        for c in ctxs:
+            c.check()
+        for x in xs:
+            x.close()
+        out[f"vocab_shard_vpf_p{P}_one_gpu"] = {
+            "rows": M, "ms": ms_v, "ms_unsharded": ms_u, "vs_unsharded": ms_u / ms_v,
+            "kernel": f"k_rows_vpf_group<bf16>: {P} ranks in one launch, {148 // P} CTAs each (DESIGN.md §7)"}
+    # decode-sized sampling (k_sample_dec): 16 rows, windows cycled over the buffers (no L2 reuse)
+    n16 = 16
+    u16 = torch.rand(n16, device=bufs[0].device)
+    ms = timed(lambda i: otk.otk_sample_tokens(ctx, bufs[i % len(bufs)][(i * 4096) % (M - n16):
+                                                                      (i * 4096) % (M - n16) + n16], u16), 16)
+    out["sample_tokens_decode16"] = {"rows": n16, "us": ms * 1e3, "GBps": n16 * (2 * V + 12) / ms / 1e6,
+                                     "kernel": "k_sample_dec (one row per 8-CTA cluster; launch latency included)"}
     from synth import make_lmhead
     rows, d = 8192, 3584
     h, w, y = make_lmhead(rows, V, d, seed=1, device=bufs[0].device)
@@ -475,6 +484,30 @@ def other_kernels(W, step, cfg):
     out["lmhead_logprob_fwd"] = {"rows": rows, "hidden_dim": d, "ms": ms, "TFLOPs": tf, "frac_bf16": tf / bf16_peak,
                                  "kernel": "k_lmhead_fwd (tcgen05 cta_group::2; SURVEY.md §8(f) NEXT-1 fwd)"}
     del h, w, y, ws
+    # NEXT-1 fwd + bwd: the policy loss and dh / dW through the LM head, on this library's tcgen05 kernels
+    # (otk_lmhead_policy_loss_fwd_bwd) vs cuBLAS GEMMs around the loss kernel (4); same inputs, back to back
+    from paper_2601_07376_b200.step import LMHeadPolicyLoss, LMHeadPolicyLossFused
+    from synth import make_noise
+    for d in (1024, 3584):
+        h, w, y = make_lmhead(rows, V, d, seed=2, device=bufs[0].device)
+        msk = (torch.arange(rows, device=h.device) % 2).to(torch.uint8)
+        rtj = (torch.arange(rows, device=h.device, dtype=torch.int32) // 512)
+        advl = torch.linspace(-1, 1, rows // 512 + 1, device=h.device, dtype=torch.float64)
+        lp = otk.otk_lmhead_logprob_fwd(ctx, h, w, y)["logp"]
+        old = (lp + make_noise(rows, 0.05, 1, device=h.device)).contiguous()
+        ref = (lp + make_noise(rows, 0.1, 2, device=h.device)).contiguous()
+        nlr = msk.sum().to(torch.int64).reshape(1)
+        res = {}
+        for name, cls in (("cublas_gemms_plus_k4", LMHeadPolicyLoss), ("fused_tcgen05", LMHeadPolicyLossFused)):
+            st = cls(ctx)
+            res[name] = timed(lambda i: st(h, w, y, msk, rtj, advl, old, ref, nlr, cfg), 3)
+            del st
+        tf = 3 * 2.0 * rows * V * d / res["fused_tcgen05"] / 1e9
+        out[f"lmhead_policy_loss_d{d}"] = {
+            "rows": rows, "hidden_dim": d, "ms": res, "speedup_fused": res["cublas_gemms_plus_k4"] / res["fused_tcgen05"],
+            "fused_TFLOPs": tf, "fused_frac_bf16": tf / bf16_peak,
+            "kernel": "k_lmhead_fwd (x tiles) + k_lmhead_loss_rows + k_lmhead_bwd<dh, dW> (SURVEY.md §8(f) NEXT-1)"}
+        del h, w, y
     ctx.check()
     return out
 

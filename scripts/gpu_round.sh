@@ -1,4 +1,5 @@
-# full round evidence: tests, bench (all legs), ncu launch list of the bench, ncu full capture of K4/K3
+# full round evidence: tests, bench (all legs), ncu launch list of the bench, ncu full capture of K4/K3 and of the
+# round-2 kernels (LM-head backward, decode sampler), sanitizers + the racecheck reproducer, the side measurements
 mkdir -p gpurun_out
 python paper_2601_07376_b200/build.py
 python -c "import __graft_entry__ as g; g.build()"
@@ -21,3 +22,12 @@ timeout 300 python scripts/perf_vpf.py --ranks 2 4 8 > gpurun_out/perf_vpf.jsonl
 timeout 300 python scripts/vpf_isolation.py > gpurun_out/vpf_isolation.jsonl 2>&1; echo "vpf_isolation rc=$?"
 for n in 4096 8192; do timeout 200 python scripts/perf_lmhead_loss.py --rows $n 2>&1 | tail -1; done > gpurun_out/perf_lmhead_loss.jsonl
 timeout 300 python scripts/hbm_probe3.py > gpurun_out/hbm_probe3.json 2>&1; echo "hbm_probe3 rc=$?"
+# round-2 additions: the LM-head backward (fused vs cuBLAS at d = 1024 / 3584, ncu of both GEMMs), the decode sampler,
+# the racecheck reproducer of the TMA ring protocol
+for d in 1024 2048 3584; do timeout 200 python scripts/perf_lmhead_loss.py --rows 8192 --d $d 2>&1 | tail -1; done > gpurun_out/perf_lmhead_loss.jsonl
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_lmhead_bwd -c 2 -o gpurun_out/prof_lmbwd -f python scripts/prof_lmhead_loss.py 8192 3584 1 > gpurun_out/ncu_lmbwd.log 2>&1; echo "lmbwd rc=$?"
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/lmbwd_launches.csv python scripts/prof_lmhead_loss.py 8192 3584 1 > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_sample_dec -s 4 -c 1 -o gpurun_out/prof_sdec -f python scripts/prof_sample_dec.py 16 > gpurun_out/ncu_sdec.log 2>&1; echo "sdec rc=$?"
+timeout 300 python scripts/perf_sample.py --rows 1,16,32,64,96,128,256,1024,4096 > gpurun_out/perf_sample.jsonl 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -I paper_2601_07376_b200/csrc -o /tmp/rr scripts/repro/racecheck_tma_ring.cu && \
+  (timeout 300 compute-sanitizer --tool racecheck /tmp/rr > gpurun_out/racecheck_repro.log 2>&1; echo "repro rc=$?" >> gpurun_out/racecheck_repro.log)

@@ -89,10 +89,15 @@ if __name__ == "__main__":
     launches(tag)
     ncu_summary(os.path.join(OUT, "prof_k4.ncu-rep"), os.path.join(PROF, f"{tag}_k4_ncu.txt"))
     ncu_summary(os.path.join(OUT, "prof_k3.ncu-rep"), os.path.join(PROF, f"{tag}_k3_ncu.txt"))
-    for name in ("sample", "lmhead"):   # optional captures of the NEXT-3 / NEXT-1 kernels
+    for name in ("sample", "lmhead", "lmbwd", "sdec"):   # optional captures of the NEXT-3 / NEXT-1 kernels
         rep = os.path.join(OUT, f"prof_{name}.ncu-rep")
         if os.path.exists(rep):
-            ncu_summary(rep, os.path.join(PROF, f"{tag}_{name}_ncu.txt"))
+            if name == "lmbwd":   # two kernels (dh, dW): per-kernel metrics and stalls
+                txt = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_kernels.py"), rep],
+                                     capture_output=True, text=True).stdout
+                open(os.path.join(PROF, f"{tag}_{name}_ncu.txt"), "w").write(txt)
+            else:
+                ncu_summary(rep, os.path.join(PROF, f"{tag}_{name}_ncu.txt"))
     import shutil
     for src, dst in (("perf_sample.jsonl", "perf_sample.jsonl"), ("perf_lmhead.jsonl", "perf_lmhead.jsonl"),
                      ("perf_variants.jsonl", "perf_variants.jsonl"), ("perf_vpf.jsonl", "perf_vpf.jsonl"),
@@ -100,7 +105,8 @@ if __name__ == "__main__":
                      ("hbm_probe3.json", "hbm_probe3.json"),
                      ("sanitize_memcheck.log", "sanitize_memcheck.txt"),
                      ("sanitize_racecheck.log", "sanitize_racecheck.txt"),
-                     ("sanitize_synccheck.log", "sanitize_synccheck.txt")):
+                     ("sanitize_synccheck.log", "sanitize_synccheck.txt"),
+                     ("racecheck_repro.log", "racecheck_repro.txt"), ("lmbwd_launches.csv", "lmbwd_launches.csv")):
         if os.path.exists(os.path.join(OUT, src)):
             shutil.copy(os.path.join(OUT, src), os.path.join(PROF, f"{tag}_{dst}"))
     traffic(os.path.join(OUT, "prof_k4.ncu-rep"), tag)

@@ -53,6 +53,32 @@ for x in xs:
 from synth import make_lmhead
 h, w, y = make_lmhead(300, 1000, 128, seed=4, device="cuda")
 otk.otk_lmhead_logprob_fwd(ctx, h, w, y)
+# the policy loss through the LM head (NEXT-1 fwd + bwd: x tiles, loss rows, dh split-K + reduce, dW), ragged shapes
+h, w, y = make_lmhead(300, 1032, 192, seed=5, device="cuda")
+mk = (torch.arange(300, device="cuda") % 3 != 0).to(torch.uint8)
+rtj = torch.arange(300, device="cuda", dtype=torch.int32) // 100
+lp = otk.otk_lmhead_logprob_fwd(ctx, h, w, y)["logp"]
+nl = mk.sum().to(torch.int64).reshape(1)
+for cfg in (otk.LossCfg(), otk.LossCfg(ent_coef=0.02)):
+    otk.otk_lmhead_policy_loss_fwd_bwd(ctx, h, w, y, mk, rtj, torch.tensor([0.5, -0.3, 1.0], device="cuda",
+                                       dtype=torch.float64), lp.contiguous(), lp.contiguous(), nl, cfg)
+# decode-batch sampler (one row per cluster, ranges resident in shared memory) and the 100-row ring path
+for n in (1, 5, 37):
+    lg, _ = make_logits(n, 151936, dtype="bf16", seed=6, device="cuda")
+    otk.otk_sample_tokens(ctx, lg, torch.rand(n, device="cuda"))
+    otk.otk_sample_tokens(ctx, lg, greedy=True)
+# K4-VPF, grouped launch, lag-3 pipeline + collector warp (P = 8: <= 4-chunk shard rows)
+lg8, tg8 = make_logits(N, 8 * 1024, dtype="bf16", seed=7, device="cuda")
+ctx8 = [otk.Context(0) for _ in range(8)]
+xs8 = otk.VpfExchange.local_group(ctx8, N)
+b8 = [1024 * k for k in range(8)]
+otk.otk_policy_loss_fwd_bwd_vpf_group(ctx8, [lg8[:, 1024 * k:1024 * (k + 1)] for k in range(8)], tg8, m["loss_mask"],
+                                      m["row_traj"], a["adv"], o, o, m["n_loss"], otk.LossCfg(), b8, 8192, xs8)
+torch.cuda.synchronize()
+for c in ctx8:
+    c.check()
+for x in xs8:
+    x.close()
 torch.cuda.synchronize()
 ctx.check()
 print("sanitize ok")
