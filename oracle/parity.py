@@ -253,7 +253,7 @@ def parity_ok(p):
 
 
 # ------------------------------------------------------------------------------------------------
-# LM head (NEXT-1): dh / dW tolerance from ambiguous bf16 roundings of the logits (R38)
+# LM head (NEXT-1): dh / dW tolerance from ambiguous bf16 roundings of the logits (R34)
 # ------------------------------------------------------------------------------------------------
 def bf16_ulp(x):
     """Spacing of bf16 numbers at |x| (8 significant bits): 2^(floor(log2|x|) - 7); the smallest normal's below."""
@@ -263,7 +263,7 @@ def bf16_ulp(x):
 
 def lmhead_flip_tolerance(h, W, x64, xb, y, coef, logp, old, ref, A, w_row, cfg, mask, acc_terms=None):
     """Extra absolute tolerance of dh = dx W and dW = dx^T h where the device's bf16 logits may differ from the
-    oracle's by one bf16 rounding (R38).
+    oracle's by one bf16 rounding (R34).
 
     The oracle rounds x64 = h W^T (float64) to bf16 (xb); the device rounds an fp32 accumulation of the same bf16
     products, whose error is at most d 2^-24 sum_k |h_jk W_vk| (recursive fp32 summation, round to nearest). Where

@@ -167,7 +167,7 @@ def test_underflow_below_smallest_normal_is_tolerated():
 
 
 def test_lmhead_flip_tolerance_covers_flipped_roundings():
-    """The LM-head dh / dW flip allowance (oracle/parity.py lmhead_flip_tolerance, R38): flipping EVERY
+    """The LM-head dh / dW flip allowance (oracle/parity.py lmhead_flip_tolerance, R34): flipping EVERY
     ambiguous logit to its other bf16 neighbour moves the float64 oracle's dh and dW by no more than the allowance;
     a flipped NON-ambiguous logit (a wrong rounding, not an accumulation-order effect) is not covered."""
     from synth import make_lmhead
