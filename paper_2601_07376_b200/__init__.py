@@ -454,9 +454,7 @@ def otk_lmhead_policy_loss_fwd_bwd(ctx: Context, hidden: torch.Tensor, weight: t
     logp = torch.empty(N, dtype=torch.float32, device=dev) if want_logp else None
     entropy = torch.empty(N, dtype=torch.float32, device=dev) if want_logp else None
     _side_args(N, dev, targets, loss_mask, row_traj, adv, old_logp, ref_logp, n_loss, cfg, stats)
-    nbytes = int(_lib.otk_lmhead_loss_workspace_bytes(ctx.handle, N, d, V))
-    if nbytes < 0:
-        raise ValueError("bad LM-head loss shapes")
+    nbytes = max(int(_lib.otk_lmhead_loss_workspace_bytes(ctx.handle, N, d, V)), 16)  # -1: the call reports why
     if workspace is None or workspace.numel() * workspace.element_size() < nbytes:
         workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
     c = cfg.c(accumulate, adv)

@@ -106,3 +106,32 @@ def test_lmhead_fused_timed_vocab_and_hidden():
     """The timed shape's vocabulary and hidden size (V = 151936: 2374 vocab stages split across dh units; d = 3584: 7
     hidden tiles, the dx store of tile 0 read back by dW) on a ragged 257-row batch (one full 256-row tile + 1)."""
     _run_case("fused", 257, 151936, 3584, seed=17)
+
+
+def test_lmhead_fused_errors_and_empty():
+    """Host-checked errors of otk_lmhead_policy_loss_fwd_bwd return before any launch (otk.h): vocab not a multiple
+    of 8, hidden_dim not a multiple of 64, a 16- but not 32-byte-aligned gradient buffer; 0 rows is a no-op."""
+    import paper_2601_07376_b200 as otk
+    ctx = otk.Context(0)
+    dev = "cuda"
+
+    def args(N, V, d):
+        h, w, y = make_lmhead(N, V, d, seed=1, device=dev)
+        return (h, w, y, torch.ones(N, dtype=torch.uint8, device=dev), torch.zeros(N, dtype=torch.int32, device=dev),
+                torch.ones(1, dtype=torch.float64, device=dev), torch.zeros(N, device=dev), torch.zeros(N, device=dev),
+                torch.tensor([max(N, 1)], dtype=torch.int64, device=dev))
+    with pytest.raises(otk.OtkError) as e:
+        otk.otk_lmhead_policy_loss_fwd_bwd(ctx, *args(64, 1028, 128))
+    assert e.value.status == 2                                    # OTK_ERR_SHAPE
+    with pytest.raises(otk.OtkError) as e:
+        otk.otk_lmhead_policy_loss_fwd_bwd(ctx, *args(64, 1024, 96))
+    assert e.value.status == 2
+    a = args(64, 1024, 128)
+    buf = torch.empty(64 * 128 + 8, dtype=torch.bfloat16, device=dev)
+    with pytest.raises(otk.OtkError) as e:                        # dhidden at a 16-byte (not 32) offset
+        otk.otk_lmhead_policy_loss_fwd_bwd(ctx, *a, dhidden=buf[8:].view(64, 128))
+    assert e.value.status == 3                                    # OTK_ERR_ALIGNMENT
+    out = otk.otk_lmhead_policy_loss_fwd_bwd(ctx, *args(0, 1024, 128))
+    ctx.check()
+    assert out["dh"].shape == (0, 128)
+    ctx.close()
