@@ -439,6 +439,7 @@ otk_status otk_lmhead_row_partials(otk_ctx* ctx, int64_t num_rows, int64_t hidde
  * in 64 x 64 tiles [rows_pad/64][cols_pad/64][64][64] (rows_pad, cols_pad = num_rows, vocab rounded up to 256;
  * contiguous 8 KB tiles for the backward's TMA), then chunk partials, per-row constants, dh split-K partials. dhidden / dweight: outputs, bf16, must not alias any input. logp / entropy: NULL or
  * [num_rows] f32 (loss-masked rows 0). stats: device otk_loss_stats (accumulated if cfg->accumulate_stats).
+ * num_rows == 0: dweight is zeroed and the stats written as zeros (unless accumulate_stats); nothing else runs.
  * Errors: host-checkable ones return at once; a target out of range sets OTK_ERR_TARGET_RANGE and an index
  * out of range OTK_ERR_GROUP_RANGE (those rows are treated as loss-masked: zero gradient).
  * Tolerance vs the float64 oracle on the same bf16 h and W (tests/test_gpu_lmhead_loss.py): loss 1e-3

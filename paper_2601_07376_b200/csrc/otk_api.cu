@@ -471,7 +471,12 @@ otk_status otk_lmhead_policy_loss_fwd_bwd(otk_ctx* ctx, int64_t num_rows, int64_
   if (st != OTK_OK) return st;
   OTK_REQUIRE(stats, OTK_ERR_INVALID_ARG, "stats is NULL");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (num_rows == 0) return OTK_OK;
+  if (num_rows == 0) {  // no rows: dW = 0 and (unless accumulating) zero stats, as otk_policy_loss_fwd_bwd
+    OTK_REQUIRE(dweight, OTK_ERR_INVALID_ARG, "dweight is NULL");
+    OTK_CUDA(cudaMemsetAsync(dweight, 0, size_t(vocab) * size_t(hidden_dim) * 2, s), "zero dweight");
+    if (!cfg->accumulate_stats) OTK_CUDA(cudaMemsetAsync(stats, 0, sizeof(otk_loss_stats), s), "zero stats");
+    return OTK_OK;
+  }
   OTK_REQUIRE(hidden && weight && targets && loss_mask && row_traj && adv && old_logp && n_loss && workspace &&
                   dhidden && dweight,
               OTK_ERR_INVALID_ARG, "a required pointer is NULL");

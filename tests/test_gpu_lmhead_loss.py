@@ -131,7 +131,9 @@ def test_lmhead_fused_errors_and_empty():
     with pytest.raises(otk.OtkError) as e:                        # dhidden at a 16-byte (not 32) offset
         otk.otk_lmhead_policy_loss_fwd_bwd(ctx, *a, dhidden=buf[8:].view(64, 128))
     assert e.value.status == 3                                    # OTK_ERR_ALIGNMENT
-    out = otk.otk_lmhead_policy_loss_fwd_bwd(ctx, *args(0, 1024, 128))
+    out = otk.otk_lmhead_policy_loss_fwd_bwd(ctx, *args(0, 1024, 128),
+                                             stats=torch.full((5,), 7.0, dtype=torch.float64, device=dev))
     ctx.check()
     assert out["dh"].shape == (0, 128)
+    assert bool((out["dW"] == 0).all()) and bool((out["stats"] == 0).all())   # empty batch: no gradient, zero stats
     ctx.close()
