@@ -376,11 +376,15 @@ constexpr int kDecWarps = 16;
 constexpr int kDecThreads = 32 * kDecWarps;
 constexpr int kDecSeg = 1024;                        // bytes per segment (64 vectors: 2 per lane)
 constexpr int kDecMaxSegs = 200;                     // 200 KB of row per CTA
-constexpr size_t kDecSmemBase = 2048 + 64 * 4;       // part[] (float2 x kDecMaxSegs) + barriers, ahead of the data
+#ifndef OTK_SDEC_PARTS
+#define OTK_SDEC_PARTS 4
+#endif
+constexpr int kDecParts = OTK_SDEC_PARTS;            // bulk copies (and barriers) the range is loaded in
+constexpr size_t kDecSmemBase = 2048 + 512;          // part[] (float2 x kDecMaxSegs) + barriers, ahead of the data
 
 struct DecSmem {
   float2 part[kDecMaxSegs];                          // (sum of e at r, r) per segment
-  uint64_t full[4];
+  uint64_t full[16];
   float4 cta;                                        // (R_c, S_c, greedy max, greedy first index) — read over DSMEM
   float wb[kDecWarps];
   int wi[kDecWarps];
@@ -419,15 +423,15 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_sample_dec(const SampleParam
                                     : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
   const T* rbase = reinterpret_cast<const T*>(p.logits) + row * p.ld;
   // quarters of the range: part q covers segments [q0(q), q0(q+1))
-  auto q0 = [&](int q) { return (nseg * q + 3) / 4; };
+  auto q0 = [&](int q) { return (nseg * q + kDecParts - 1) / kDecParts; };
   SDEC_T(0);
 
   if (threadIdx.x == 0) {
-    for (int q = 0; q < 4; ++q) mbar_init(&S.full[q], 1);
+    for (int q = 0; q < kDecParts; ++q) mbar_init(&S.full[q], 1);
     fence_mbar_init();
     const uint64_t pol = policy_evict_first();
     const char* src = reinterpret_cast<const char*>(rbase) + int64_t(v_begin) * 16;
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kDecParts; ++q) {
       const int s0 = q0(q), s1 = q0(q + 1);
       const uint32_t b0 = uint32_t(s0) * kDecSeg, b1 = uint32_t(min(s1 * VPS, nv_c)) * 16u;
       if (b1 > b0) {
@@ -447,7 +451,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_sample_dec(const SampleParam
   int bidx = INT_MAX;
   int qw = 0;
   for (int sg = warp; sg < nseg; sg += kDecWarps) {
-    while (qw < 4 && q0(qw + 1) <= sg) ++qw;
+    while (qw < kDecParts && q0(qw + 1) <= sg) ++qw;
     mbar_wait(&S.full[qw], 0);
     const int v0 = v_begin + sg * VPS + 2 * lane;    // row vector index of q[0]
     uint4 q[2];
@@ -735,8 +739,11 @@ bool sample_dec_shape(int64_t num_rows, int64_t vocab, int dtype, int num_sms, i
   if (num_rows < 1 || num_rows > num_sms) return false;
   // at least 4 CTAs per row (<= 37 rows on 148 SMs): measured faster than the lane-strided kernel there (16 rows
   // 7.8 vs 8.4 us), slower with 2 (64 rows 13.0 vs 12.3 us: a 152 KB range per CTA is one SM's bandwidth share)
+#ifndef OTK_SDEC_MINC
+#define OTK_SDEC_MINC 4
+#endif
   const int64_t c = std::min<int64_t>(8, num_sms / num_rows);
-  if (c < 4) return false;
+  if (c < OTK_SDEC_MINC) return false;
   const int64_t per = (nsegs + c - 1) / c;
   if (per > kDecMaxSegs) return false;
   *csize = int(c);
