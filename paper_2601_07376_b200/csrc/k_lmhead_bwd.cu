@@ -190,7 +190,7 @@ __device__ __forceinline__ void bw_chunk(uint32_t addr, int yoff, bool zero, uin
 }
 
 #ifdef OTK_BW_TIMING  // experiments only: clock64 sums (MMA thread of each pair; transform warp 2 lane 0 of each CTA)
-__device__ unsigned long long g_bw_timing[2][8];
+__device__ unsigned long long g_bw_timing[2][2][8];  // [dh, dW][MMA thread, transform warp][slot]
 #define BW_T0() const long long _t0 = clock64()
 #define BW_ACC(slot) tacc[slot] += clock64() - _t0
 #else
@@ -260,11 +260,16 @@ __global__ void __launch_bounds__(kBwThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&emptyA[s], ph ^ 1u);
           const uint32_t a = smem_u32(smem + s * kBwABytes);
-          mbar_arrive_expect_tx(&fullA[s], kBwABytes);
-          if (kDh)  // x tiles (row block m0/64 .. +1, vocab block kb): [2][64 rows][64 v], K-major rows
-            tma_load_4d(a, &tm_a, &fullA[s], 0, 0, kb, m0 >> 6);
-          else      // x tiles (row block kb, vocab blocks m0/64 .. +1): [2][64 rows][64 v], MN-major
-            tma_load_4d(a, &tm_a, &fullA[s], 0, 0, m0 >> 6, kb);
+          if (!p.xform) {  // A is the operand as loaded: both CTAs' bytes counted on the leader's barrier, no relay
+            if (rank == 0) mbar_arrive_expect_tx(&fullA[s], 2 * kBwABytes);
+            tma_load_4d_pair(a, &tm_a, smem_u32(&fullA[s]) & kPeerBitMask, 0, 0, m0 >> 6, kb);
+          } else {
+            mbar_arrive_expect_tx(&fullA[s], kBwABytes);
+            if (kDh)  // x tiles (row block m0/64 .. +1, vocab block kb): [2][64 rows][64 v], K-major rows
+              tma_load_4d(a, &tm_a, &fullA[s], 0, 0, kb, m0 >> 6);
+            else      // x tiles (row block kb, vocab blocks m0/64 .. +1): [2][64 rows][64 v], MN-major
+              tma_load_4d(a, &tm_a, &fullA[s], 0, 0, m0 >> 6, kb);
+          }
 
           if (++s == kBwAStages) {
             s = 0;
@@ -357,7 +362,10 @@ __global__ void __launch_bounds__(kBwThreads, 1)
           }
           {
             BW_T0();
-            mbar_wait_cluster(&readyA[sa], pha);
+            if (p.xform)
+              mbar_wait_cluster(&readyA[sa], pha);
+            else
+              mbar_wait(&fullA[sa], pha);
             BW_ACC(1);
           }
 #ifdef OTK_BW_TIMING
@@ -397,7 +405,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
       }
 #ifdef OTK_BW_TIMING
       tacc[3] = clock64() - t_start;
-      for (int k = 0; k < 8; ++k) atomicAdd(&g_bw_timing[0][k], (unsigned long long)tacc[k]);
+      for (int k = 0; k < 8; ++k) atomicAdd(&g_bw_timing[kDh ? 0 : 1][0][k], (unsigned long long)tacc[k]);
 #endif
     }
   } else {
@@ -454,17 +462,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
           q0 = raw_consts(p, int64_t(kb0) * kBwK + jj);
           q1 = raw_consts(p, int64_t(kb0 + 1) * kBwK + jj);
         }
-        for (int kb = kb0; kb < kb1; ++kb) {
-          if (!p.xform) {  // A is dx already: relay the stage to the MMA
-            mbar_wait(&fullA[s], ph);
-            __syncwarp();
-            if (lane == 0) mbar_arrive_remote(ready_leader + s * 8);
-            if (++s == kBwAStages) {
-              s = 0;
-              ph ^= 1u;
-            }
-            continue;
-          }
+        for (int kb = kb0; kb < kb1 && p.xform; ++kb) {  // (A as loaded: nothing to transform, no relay)
           const RowK cur = cook<kEnt>(q0, p.vocab);
           q0 = q1;
           q1 = raw_consts(p, int64_t(kb + 2) * kBwK + jj);
@@ -540,7 +538,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
     }
 #ifdef OTK_BW_TIMING
     if (xt == 0)
-      for (int k = 4; k < 7; ++k) atomicAdd(&g_bw_timing[1][k], (unsigned long long)tacc[k]);
+      for (int k = 4; k < 7; ++k) atomicAdd(&g_bw_timing[kDh ? 0 : 1][1][k], (unsigned long long)tacc[k]);
 #endif
   }
   tc_fence_before();
@@ -664,6 +662,7 @@ cudaError_t launch_lmhead_bwd(const otk_ctx* ctx, int64_t num_rows, int64_t voca
       return cudaErrorInvalidValue;
     p.store_dx = 0;
     p.xform = 0;
+
     p.n_mt = int((vocab + kBwMtile - 1) / kBwMtile);
     p.kb_total = int((num_rows + kBwK - 1) / kBwK);
     p.splits = 1;
@@ -680,8 +679,8 @@ cudaError_t launch_lmhead_bwd(const otk_ctx* ctx, int64_t num_rows, int64_t voca
 
 #ifdef OTK_BW_TIMING
 extern "C" void otk_debug_bw(unsigned long long* out) {
-  cudaMemcpyFromSymbol(out, otk::g_bw_timing, sizeof(unsigned long long) * 16);
-  unsigned long long z[16] = {0};
+  cudaMemcpyFromSymbol(out, otk::g_bw_timing, sizeof(unsigned long long) * 32);
+  unsigned long long z[32] = {0};
   cudaMemcpyToSymbol(otk::g_bw_timing, z, sizeof(z));
 }
 #endif

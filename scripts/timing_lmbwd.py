@@ -19,7 +19,7 @@ ref = (lp + make_noise(n, 0.1, 2, device="cuda")).contiguous()
 nl = mask.sum().to(torch.int64).reshape(1)
 step = LMHeadPolicyLossFused(ctx)
 fn = otk._lib.otk_debug_bw
-buf = (ctypes.c_ulonglong * 16)()
+buf = (ctypes.c_ulonglong * 32)()
 step(h, w, y, mask, rt, adv, old, ref, nl, otk.LossCfg(kl_beta=0.04))
 torch.cuda.synchronize()
 fn(buf)   # reset
@@ -28,7 +28,10 @@ step(h, w, y, mask, rt, adv, old, ref, nl, otk.LossCfg(kl_beta=0.04))
 torch.cuda.synchronize()
 fn(buf)
 pairs, ctas = 74, 148
-m = [buf[k] / pairs for k in range(8)]
-t = [buf[8 + k] / ctas for k in range(8)]
-print(json.dumps(dict(rows=n, d=d, mma=dict(wait_B=m[0], wait_readyA=m[1], wait_tempty=m[2], total=m[3], stages=m[7]),
-                      xform=dict(wait_A=t[4], transform=t[5], epilogue=t[6]))))
+res = dict(rows=n, d=d)
+for kname, base in (("dh", 0), ("dW", 16)):
+    m = [buf[base + k] / pairs for k in range(8)]
+    t = [buf[base + 8 + k] / ctas for k in range(8)]
+    res[kname] = dict(mma=dict(wait_B=m[0], wait_readyA=m[1], wait_tempty=m[2], total=m[3], stages=m[7]),
+                      xform=dict(wait_A=t[4], transform=t[5], epilogue=t[6]))
+print(json.dumps(res))
