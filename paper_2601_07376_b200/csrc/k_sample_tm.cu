@@ -589,7 +589,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_sample_dec(const SampleParam
       const float4 v = part_of(rr);
       if (v.y > 0.f) Sw = __fadd_rn(Sw, __fmul_rn(v.y, ex2(v.x - R)));
     }
-    const bool degenerate = greedy ? !(B > -INFINITY) || (need_sum && !(Sw > 0.f))
+    // as the other samplers (R32): logits <= -1e30 carry no mass, a row without any larger one is degenerate
+    const bool degenerate = greedy ? !(B > -1e30f) || (need_sum && !(Sw > 0.f))
                                    : (!(R > kSNoRef) || !(Sw > 0.f));
     if (greedy || degenerate) {
       if (rank == 0 && lane == 0) {
