@@ -261,3 +261,18 @@ def test_decode_batches(otk, ctx, dtype, V, n):
     for j in rows:
         assert gt[j] == int(np.argmax(wide[j])), j
         assert abs(float(glp[j]) - O.sample_token(wide[j], 0.0, greedy=True)[1]) < LOGP_TOL[dtype]
+
+
+@pytest.mark.parametrize("n", [3, 200])
+def test_greedy_rows_below_no_mass_threshold(otk, ctx, n):
+    """R32: logits <= -1e30 carry no mass — a row of finite -1e31 logits is degenerate (token 0, logp -inf) in the
+    decode kernel (3 rows) and the lane-strided kernel (200 rows) alike, for greedy and sampled draws."""
+    x = torch.randn(n, 4096).to(torch.bfloat16)
+    x[0, :] = -1e31
+    xc = x.cuda()
+    g = otk.otk_sample_tokens(ctx, xc, greedy=True)
+    s = otk.otk_sample_tokens(ctx, xc, torch.full((n,), 0.5, device="cuda"))
+    ctx.check()
+    for o in (g, s):
+        assert int(o["tokens"][0]) == 0 and float(o["logp"][0]) == float("-inf")
+    assert int(g["tokens"][1]) == int(torch.argmax(x[1].float()))
