@@ -1,3 +1,5 @@
+# LM-head backward iteration: its tests, fused timing (default + optional DEFINES_B / DEFINES_C experiment builds
+# through gpu_lmbwd_ab.sh), per-kernel launch times
 # LM-head backward iteration: tests, timing (default + optional experiment builds), per-kernel launch times
 mkdir -p gpurun_out .variants
 python paper_2601_07376_b200/build.py

@@ -1,3 +1,5 @@
+# LM-head backward experiment: clock64 breakdown of the dh / dW kernels (MMA waits, transform, epilogue) from a
+# -DOTK_BW_TIMING build (scripts/timing_lmbwd.py)
 mkdir -p gpurun_out .variants
 python paper_2601_07376_b200/build.py
 python -c "
