@@ -39,7 +39,11 @@ using namespace umma;
 constexpr int kBwK = 64;
 // A and B have rings of their own: A needs TMA + the transform before the MMA may read it, B only TMA, so A
 // runs deeper (6 stages = 6 k-blocks ahead) than B (4) in the 227 KB of shared memory.
-constexpr int kBwAStages = 6, kBwBStages = 4;
+#ifndef OTK_BW_ASTAGES
+#define OTK_BW_ASTAGES 6
+#define OTK_BW_BSTAGES 4
+#endif
+constexpr int kBwAStages = OTK_BW_ASTAGES, kBwBStages = OTK_BW_BSTAGES;
 constexpr int kBwABytes = 128 * kBwK * 2;  // 16 KB: this CTA's 128 M-rows x 64 k
 constexpr int kBwBBytes = 256 * kBwK * 2;  // 32 KB: this CTA's 2 x 128 N-columns x 64 k (4 TMA boxes of 64 x 64)
 constexpr int kBwXWarps = 16;  // transform + epilogue warps (2..17); warp 0 loads A, warp 18 loads B, warp 1 MMAs,
