@@ -1,0 +1,36 @@
+"""The C ABI without Python: examples/c_api_step.c (masks -> advantages -> log-probs -> fused loss + dlogits on a
+batch with a closed-form loss) compiles as plain C against include/otk.h and libotk.so (CPU), and runs on the GPU
+(-m gpu) with the closed-form loss, advantages, token count and zero-sum gradient rows."""
+import os
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+
+
+def _build(tmp_path):
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    lib = os.path.join(ROOT, "paper_2601_07376_b200")
+    if not os.path.exists(os.path.join(lib, "libotk.so")):
+        pytest.skip("libotk.so not built")
+    exe = str(tmp_path / "c_api_step")
+    cmd = ["gcc", "-std=c11", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), "-I",
+           os.path.join(CUDA, "include"), os.path.join(ROOT, "examples", "c_api_step.c"), "-o", exe, "-L", lib,
+           "-lotk", "-L", os.path.join(CUDA, "lib64"), "-lcudart", "-lm", f"-Wl,-rpath,{lib}"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_c_example_compiles_as_plain_c(tmp_path):
+    assert os.path.exists(_build(tmp_path))
+
+
+@pytest.mark.gpu
+def test_c_example_runs(tmp_path):
+    r = subprocess.run([_build(tmp_path)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "-> ok" in r.stdout
