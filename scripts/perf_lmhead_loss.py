@@ -28,16 +28,24 @@ nl = mask.sum().to(torch.int64).reshape(1)
 cfg = otk.LossCfg(kl_beta=0.04)
 
 
-def back_to_back(step):
+CLOCKS = {}
+
+
+def back_to_back(step, name=None):
     """ms per call of `iters` calls enqueued back to back (no host sync in between, so host-side argument
-    marshalling overlaps the previous call's kernels — the device time, as bench.py measures a step)."""
+    marshalling overlaps the previous call's kernels — the device time, as bench.py measures a step); the SM clock
+    is sampled meanwhile (bench.py's NVML sampler) into CLOCKS[name]."""
+    from bench import ClockSampler
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    e0.record()
-    for _ in range(a.iters):
-        step(h, w, y, mask, rt, adv, old, ref, nl, cfg)
-    e1.record()
-    torch.cuda.synchronize()
+    with ClockSampler(0) as cs:
+        e0.record()
+        for _ in range(a.iters):
+            step(h, w, y, mask, rt, adv, old, ref, nl, cfg)
+        e1.record()
+        torch.cuda.synchronize()
+    if name:
+        CLOCKS[name] = cs.summary()
     return e0.elapsed_time(e1) / a.iters
 
 
@@ -53,7 +61,7 @@ if a.impl in ("both", "cublas"):
         for k, v in o["ms"].items():
             acc[k] = acc.get(k, 0.0) + v / a.iters
     ctx.check()
-    tot = back_to_back(step)
+    tot = back_to_back(step, "cublas")
     res["cublas"] = dict(ms={k: round(v, 4) for k, v in acc.items()}, total_ms=round(tot, 4),
                          loss_kernel_share=round(acc["loss_kernel"] / tot, 4),
                          gemm_TFLOPs=round(3 * flops_gemm / (acc["logits_gemm"] + acc["grad_gemms"]) / 1e9, 1),
@@ -64,7 +72,7 @@ if a.impl in ("both", "fused"):
     step = LMHeadPolicyLossFused(ctx)
     for _ in range(2):
         step(h, w, y, mask, rt, adv, old, ref, nl, cfg)
-    t = back_to_back(step)
+    t = back_to_back(step, "fused")
     o = step(h, w, y, mask, rt, adv, old, ref, nl, cfg)
     torch.cuda.synchronize()
     ctx.check()
@@ -77,4 +85,5 @@ if a.impl in ("both", "fused"):
                             dh_rel_fro=float((o["dh"].float() - ref_out["dh"].float()).norm() / ref_out["dh"].float().norm()),
                             dW_rel_fro=float((o["dW"].float() - ref_out["dW"].float()).norm() / ref_out["dW"].float().norm()))
         res["speedup_fused_vs_cublas"] = round(res["cublas"]["total_ms"] / t, 4)
+res["clocks"] = CLOCKS
 print(json.dumps(res))
