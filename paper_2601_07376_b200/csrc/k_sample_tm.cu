@@ -362,403 +362,403 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
 }
 
 // =====================================================================================================
-// k_sample_dec — decode-sized batches (a few to ~70 rows): ONE row per thread-block cluster of C CTAs, each CTA
-// holding its whole column range in shared memory (bulk TMA, 4 barriers: compute starts on the first quarter),
-// so the row is read from HBM once, in one round of latency, and the search never re-reads it from L2. Per CTA:
-// 16 warps over 1 KB segments (lane l: vectors 2l, 2l+1), a warp-uniform reference per warp (k_sample_tm's
-// scheme), one (sum of e, reference) per segment and a running per-warp total; per CTA (R_c, S_c) and the greedy
-// (max, first index); ONE cluster barrier, then a split arrive / wait so that only the crossing CTA's search is left
-// on the critical path; every CTA combines the C partials in rank order (lane r reads CTA r over DSMEM); the
-// crossing CTA's warp 0 finds the crossing segment (ballot scan), then from shared memory the crossing lane and,
-// one element per lane, the crossing column. Same contract and rounding fallback as the other samplers.
+// k_sample_dec — decode-sized batches (a few to ~37 rows): ONE row per thread-block cluster of C CTAs. Each CTA's
+// column range is loaded straight into registers (LDG.128, every load issued before any is used: the row is read
+// once, in one round of memory latency, and never re-read), and the pass has no __syncthreads and no cluster
+// barrier on its critical path:
+//   warp w of a CTA owns K = ceil(segments / 16) CONTIGUOUS 1 KB segments (lane l: vectors 2l, 2l+1 of each); per
+//     segment the sum of e = 2^(x k2 - r) at a warp-uniform reference r (k_sample_tm's scheme) and a running warp
+//     total (R_w, S_w) in column order, plus the greedy (max, first column);
+//   every warp PUSHES its partial to every CTA of the cluster (st.async + mbarrier complete_tx) and waits for the
+//     16 C partials of the row: a CTA never reads a peer's shared memory and leaves only after every push to it has
+//     landed, so there is no exit barrier;
+//   every warp combines the 16 C partials in column order (rank-major, warp-minor; lane l takes 16 C / 32 of them):
+//     max, scale, inclusive scan -> S, T = u S and the crossing warp of the row; that warp alone finds the
+//     crossing segment (its K segment sums, sequentially), lane (warp scan) and column (one element per lane) from
+//     its registers.
+// The mbarrier's initialisation is published by a split cluster arrive (kernel start) / wait (after the segment
+// pass, long complete). Same contract and rounding fallback as the other samplers (R32).
 // =====================================================================================================
 constexpr int kDecWarps = 16;
 constexpr int kDecThreads = 32 * kDecWarps;
 constexpr int kDecSeg = 1024;                        // bytes per segment (64 vectors: 2 per lane)
-constexpr int kDecMaxSegs = 200;                     // 200 KB of row per CTA
-#ifndef OTK_SDEC_PARTS
-#define OTK_SDEC_PARTS 4
-#endif
-constexpr int kDecParts = OTK_SDEC_PARTS;            // bulk copies (and barriers) the range is loaded in
-constexpr size_t kDecSmemBase = 2048 + 512;          // part[] (float2 x kDecMaxSegs) + barriers, ahead of the data
+constexpr int kDecMaxK = 8;                          // segments per warp held in registers (64 registers of data)
+constexpr int kDecMaxSegs = kDecWarps * kDecMaxK;    // 128 KB of row per CTA
+constexpr int kDecMaxC = 8;
 
 struct DecSmem {
-  float2 part[kDecMaxSegs];                          // (sum of e at r, r) per segment
-  uint64_t full[16];
-  float4 cta;                                        // (R_c, S_c, greedy max, greedy first index) — read over DSMEM
-  float wb[kDecWarps];
-  int wi[kDecWarps];
-  float2 wr[kDecWarps];                              // per warp (reference, sum of its segments at it)
+  float4 peer[kDecMaxC * kDecWarps];                 // pushed warp partials (R_w, S_w, greedy max, first column),
+  uint64_t xbar;                                     //   by rank * 16 + warp (column order)
 };
-static_assert(sizeof(DecSmem) <= kDecSmemBase, "decode sampler header");
 
-#ifdef OTK_SDEC_TIMING  // experiments only: globaltimer stamps of CTA 0 (ns)
-__device__ unsigned long long g_sdec_t[8];
-#define SDEC_T(i) if (blockIdx.x == 0 && threadIdx.x == 0) g_sdec_t[i] = globaltimer_ns()
+#ifdef OTK_SDEC_TIMING  // experiments only, thread 0 of every CTA (<= 256 CTAs): [0] globaltimer (ns) at the start,
+// [1 + i] clock64 at stamp i (SM cycles; reading the global timer costs far more than a clock read)
+__device__ unsigned long long g_sdec_t[256 * 8];
+#define SDEC_T(i)                                                                     \
+  if (threadIdx.x == 0 && blockIdx.x < 256) {                                         \
+    if ((i) == 0) g_sdec_t[blockIdx.x * 8] = globaltimer_ns();                        \
+    g_sdec_t[blockIdx.x * 8 + 1 + (i)] = clock64();                                   \
+  }
 #else
 #define SDEC_T(i)
 #endif
-template <typename T, bool kCl>
-__global__ void __launch_bounds__(kDecThreads, 1) k_sample_dec(const SampleParams p, int nseg_c) {
+
+__device__ __forceinline__ float redux_max_f32(float v) {   // warp max (sm_100a: one CREDUX)
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ int redux_min_s32(int v) {
+  int r;
+  asm volatile("redux.sync.min.s32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+#ifndef OTK_SDEC_MINB
+#define OTK_SDEC_MINB 1   // resident CTAs per SM asked of the 4-segment variant
+#endif
+template <typename T, int KMAX>
+__global__ void __launch_bounds__(kDecThreads, KMAX <= 4 ? OTK_SDEC_MINB : 1) k_sample_dec(const SampleParams p, int nseg_c) {
   using SV = SV2<T>;
   constexpr int EV = SV::EV;
   constexpr int VPS = kDecSeg / 16;                  // vectors per segment (64)
-  extern __shared__ __align__(1024) uint8_t smem[];
-  DecSmem& S = *reinterpret_cast<DecSmem*>(smem);
-  uint8_t* data = smem + kDecSmemBase;
+  __shared__ DecSmem S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int C = kCl ? p.csize : 1;
-  const int rank = kCl ? int(cluster_ctarank()) : 0;
-  const int64_t row = kCl ? int64_t(cluster_id_x()) : int64_t(blockIdx.x);
+  const int C = p.csize;
+  const int rank = int(cluster_ctarank());
+  const int64_t row = int64_t(cluster_id_x());
   const int nvec = int((p.vocab + EV - 1) / EV);
   const int tail_valid = int(p.vocab - int64_t(nvec - 1) * EV);
-  const int v_begin = rank * nseg_c * VPS;           // first vector of this CTA's range
-  const int nv_c = max(0, min(nseg_c * VPS, nvec - v_begin));
-  const int nseg = (nv_c + VPS - 1) / VPS;           // segments with data
+  const int K = (nseg_c + kDecWarps - 1) / kDecWarps;          // segments per warp (<= KMAX)
+  const int sg0 = rank * nseg_c + warp * K;                    // this warp's first segment in the row
+  const int sg1 = min(rank * nseg_c + min((warp + 1) * K, nseg_c), (nvec + VPS - 1) / VPS);
   const float k2 = p.scale * 1.4426950408889634f;
   const uint64_t k2x2 = f2(k2, k2);
   const bool greedy = p.greedy != 0;
   const bool need_sum = !(greedy && p.logp == nullptr);
   const uint4 ninf = sizeof(T) == 2 ? make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u)
                                     : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
-  const T* rbase = reinterpret_cast<const T*>(p.logits) + row * p.ld;
-  // quarters of the range: part q covers segments [q0(q), q0(q+1))
-  auto q0 = [&](int q) { return (nseg * q + kDecParts - 1) / kDecParts; };
+  const uint8_t* rbase = reinterpret_cast<const uint8_t*>(p.logits) + row * p.ld * int64_t(sizeof(T));
   SDEC_T(0);
 
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < kDecParts; ++q) mbar_init(&S.full[q], 1);
-    fence_mbar_init();
-    const uint64_t pol = policy_evict_first();
-    const char* src = reinterpret_cast<const char*>(rbase) + int64_t(v_begin) * 16;
-    for (int q = 0; q < kDecParts; ++q) {
-      const int s0 = q0(q), s1 = q0(q + 1);
-      const uint32_t b0 = uint32_t(s0) * kDecSeg, b1 = uint32_t(min(s1 * VPS, nv_c)) * 16u;
-      if (b1 > b0) {
-        mbar_arrive_expect_tx(&S.full[q], b1 - b0);
-        bulk_g2s(data + b0, src + b0, b1 - b0, &S.full[q], pol);
-      } else {
-        mbar_arrive(&S.full[q]);
-      }
+  // ---------------- the warp's segments into registers: every load issued before any is used
+  uint4 q[KMAX][2];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int v = (sg0 + k) * VPS + 2 * lane + j;
+      q[k][j] = (sg0 + k < sg1 && v < nvec) ? ldg_nc_v4(rbase + size_t(v) * 16) : ninf;
     }
+  const float u_in = greedy ? 0.f : p.u[row];
+  if (threadIdx.x == 0) {
+    mbar_init(&S.xbar, 1);
+    fence_mbar_init();
   }
-  __syncthreads();
+  asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");   // publishes xbar's init (waited below)
 
-  // ---------------- segments: warp w takes segments w, w + 8, ... (in order: waits the quarters in order)
-  float r = kSNoRef;                                 // warp-uniform reference (k2 units)
-  float racc = kSNoRef, sacc = 0.f;                  // this warp's running total of its segments, at racc
+  // ---------------- segments (column order): the warp's maximum is the reference of all its segments, so no sum
+  // can overflow (e <= 1, <= 512 per segment) and the segments' warp sums are independent of one another
+  float lm = -INFINITY;                              // the lane's maximum (raw logits)
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int v = (sg0 + k) * VPS + 2 * lane + j;
+      if (v == nvec - 1 && tail_valid < EV) SV::mask_tail(q[k][j], tail_valid);
+      lm = fmaxf(lm, SV::vmax(q[k][j]));            // ninf outside the range
+    }
+  const float wmax = redux_max_f32(lm);
+  const float r = wmax * k2;                         // warp-uniform reference (k2 units); <= kSNoRef: no mass
+  const bool has_mass = need_sum && r > kSNoRef;
+  float cs_l[KMAX], cs_k[KMAX];                      // per segment: the lane's / the warp's sum of e at r
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    cs_l[k] = 0.f;
+    if (has_mass && sg0 + k < sg1) {
+      const float rk = -r;
+      const uint64_t rk2 = f2(rk, rk);
+      cs_l[k] = __fadd_rn(SV::esum(q[k][0], k2x2, rk2), SV::esum(q[k][1], k2x2, rk2));
+    }
+    cs_k[k] = cs_l[k];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) cs_k[k] = __fadd_rn(cs_k[k], __shfl_xor_sync(0xffffffffu, cs_k[k], o));
+  float sacc = 0.f;                                  // the warp's total at r (column order)
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) sacc = __fadd_rn(sacc, cs_k[k]);
+  const float racc = has_mass ? r : kSNoRef;
   float best = -INFINITY;
   int bidx = INT_MAX;
-  int qw = 0;
-  for (int sg = warp; sg < nseg; sg += kDecWarps) {
-    while (qw < kDecParts && q0(qw + 1) <= sg) ++qw;
-    mbar_wait(&S.full[qw], 0);
-    const int v0 = v_begin + sg * VPS + 2 * lane;    // row vector index of q[0]
-    uint4 q[2];
+  if (greedy) {  // the first column holding the warp's maximum
+    int li = INT_MAX;
+    if (lm == wmax && wmax > -INFINITY) {
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int v = v0 + k;
-      q[k] = v < nvec ? *reinterpret_cast<const uint4*>(data + size_t(v - v_begin) * 16) : ninf;
-      if (v == nvec - 1 && tail_valid < EV) SV::mask_tail(q[k], tail_valid);
+      for (int k = KMAX - 1; k >= 0; --k)
+#pragma unroll
+        for (int j = 1; j >= 0; --j)
+#pragma unroll
+          for (int i = EV - 1; i >= 0; --i)
+            if (SV::elem(q[k][j], i) == lm) li = ((sg0 + k) * VPS + 2 * lane + j) * EV + i;
     }
-    if (greedy) {  // the lane's first maximum (column order: vector 0 before vector 1, element order inside)
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-#pragma unroll
-        for (int i = 0; i < EV; ++i) {
-          const float x = SV::elem(q[k], i);
-          if (x > best) {
-            best = x;
-            bidx = (v0 + k) * EV + i;
-          }
-        }
-    }
-    if (need_sum) {
-      float cs = 0.f;
-      bool redo = !(r > kSNoRef);
-      if (!redo) {
-        const float rk = -r;
-        const uint64_t rk2 = f2(rk, rk);
-        cs = __fadd_rn(SV::esum(q[0], k2x2, rk2), SV::esum(q[1], k2x2, rk2));
-        redo = __any_sync(0xffffffffu, !(cs <= 0x1p64f));
-      }
-      if (redo) {
-        float wm = fmaxf(SV::vmax(q[0]), SV::vmax(q[1]));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
-        if (wm * k2 > r) r = wm * k2;
-        cs = 0.f;
-        if (r > kSNoRef) {
-          const float rk = -r;
-          const uint64_t rk2 = f2(rk, rk);
-          cs = __fadd_rn(SV::esum(q[0], k2x2, rk2), SV::esum(q[1], k2x2, rk2));
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) cs = __fadd_rn(cs, __shfl_xor_sync(0xffffffffu, cs, o));
-      if (lane == 0) S.part[sg] = make_float2(cs, r);
-      if (r > racc) {  // the reference was raised: move the running total to it
-        sacc = racc > kSNoRef ? __fmul_rn(sacc, ex2(racc - r)) : 0.f;
-        racc = r;
-      }
-      sacc = __fadd_rn(sacc, cs);
-    }
+    best = wmax;
+    bidx = redux_min_s32(li);
   }
-  if (lane == 0) S.wr[warp] = make_float2(racc, sacc);
   SDEC_T(1);
-  if (greedy) {  // warp: max, then the first column holding it
-    float bw = best;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bw = fmaxf(bw, __shfl_xor_sync(0xffffffffu, bw, o));
-    int iw = best == bw ? bidx : INT_MAX;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) iw = min(iw, __shfl_xor_sync(0xffffffffu, iw, o));
-    if (lane == 0) {
-      S.wb[warp] = bw;
-      S.wi[warp] = iw;
-    }
-  }
-  __syncthreads();
-  // ---------------- CTA partial (warp 0; fixed order: lane-strided over segments, then butterfly)
-  if (warp == 0) {  // CTA partial from the warp totals (lane w: warp w; butterfly order)
-    float R = kSNoRef, Sl = 0.f;
-    if (need_sum) {
-      const float2 wv = lane < kDecWarps ? S.wr[lane] : make_float2(kSNoRef, 0.f);
-      R = wv.x;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) R = fmaxf(R, __shfl_xor_sync(0xffffffffu, R, o));
-      Sl = wv.y > 0.f ? __fmul_rn(wv.y, ex2(wv.x - R)) : 0.f;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) Sl = __fadd_rn(Sl, __shfl_xor_sync(0xffffffffu, Sl, o));
-    }
-    if (lane == 0) {
-      float B = -INFINITY;
-      int I = INT_MAX;
-      if (greedy)
-        for (int w = 0; w < kDecWarps; ++w) {
-          if (S.wb[w] > B) {
-            B = S.wb[w];
-            I = S.wi[w];
-          } else if (S.wb[w] == B) {
-            I = min(I, S.wi[w]);
-          }
-        }
-      S.cta = make_float4(R, Sl, B, __int_as_float(I));
-    }
-  }
+  // ---------------- push the warp partial to every CTA of the cluster (lane rr -> rank rr)
+  asm volatile("barrier.cluster.wait.acquire;" ::: "memory");   // every CTA's xbar is initialised
+  if (lane < C)
+    st_async_f4(mapa(smem_u32(&S.peer[rank * kDecWarps + warp]), uint32_t(lane)), racc, sacc, best,
+                __int_as_float(bidx), mapa(smem_u32(&S.xbar), uint32_t(lane)));
+  if (threadIdx.x == 0) mbar_arrive_expect_tx(&S.xbar, 16u * kDecWarps * uint32_t(C));
+  mbar_wait_cluster(&S.xbar, 0);
   SDEC_T(2);
-  if (kCl) cluster_sync_all(); else __syncthreads();
+
+  // ---------------- the 16 C warp partials in column order, identical in every warp of every CTA:
+  // lane l holds partials [l NP, (l + 1) NP)
+  const int NP = (kDecWarps * C + 31) / 32;          // <= 4
+  float4 pv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int idx = lane * NP + i;
+    pv[i] = (i < NP && idx < kDecWarps * C) ? S.peer[idx]
+                                            : make_float4(kSNoRef, 0.f, -INFINITY, __int_as_float(INT_MAX));
+  }
+  const float R = redux_max_f32(fmaxf(fmaxf(pv[0].x, pv[1].x), fmaxf(pv[2].x, pv[3].x)));
   SDEC_T(3);
-  // every CTA's partial is final: the exit barrier's arrive now (warp 0 after its DSMEM reads, below), its wait at
-  // the end — a CTA never exits while a peer may still read its partial, and only the search stays on the path
-  if (kCl && warp != 0) asm volatile("barrier.cluster.arrive.release;" ::: "memory");
-  // ---------------- row combine (rank order, identical in every CTA) and the crossing CTA
-  if (warp == 0) {
-    // lane rr reads CTA rr's partial (the C DSMEM round trips overlap); the rank-order loops below take them by
-    // shuffles
-    float4 mine4 = S.cta;
-    if (kCl && lane < C && lane != rank) {
-      const uint32_t ra = mapa(smem_u32(&S.cta), uint32_t(lane));
-      asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-                   : "=f"(mine4.x), "=f"(mine4.y), "=f"(mine4.z), "=f"(mine4.w)
-                   : "r"(ra)
-                   : "memory");
+  float B = -INFINITY;
+  int I = INT_MAX;
+  if (greedy) {
+    B = redux_max_f32(fmaxf(fmaxf(pv[0].z, pv[1].z), fmaxf(pv[2].z, pv[3].z)));
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (pv[i].z == B) I = min(I, __float_as_int(pv[i].w));
+    I = redux_min_s32(I);
+  }
+  float c[4], lt = 0.f;                              // masses at R, the lane's total
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    c[i] = pv[i].y > 0.f ? __fmul_rn(pv[i].y, ex2(pv[i].x - R)) : 0.f;
+    lt = __fadd_rn(lt, c[i]);
+  }
+  float incl = lt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = __fadd_rn(incl, y);
+  }
+  const float Sw = __shfl_sync(0xffffffffu, incl, 31);
+  SDEC_T(4);
+  // as the other samplers (R32): logits <= -1e30 carry no mass, a row without any larger one is degenerate
+  const bool degenerate = greedy ? !(B > -1e30f) || (need_sum && !(Sw > 0.f)) : (!(R > kSNoRef) || !(Sw > 0.f));
+  if (greedy || degenerate) {
+    if (rank == 0 && threadIdx.x == 0) {
+      p.tokens[row] = degenerate ? 0 : I;
+      if (p.logp) p.logp[row] = degenerate ? -INFINITY : (B * k2 - R - log2f(Sw)) * 0.6931471805599453f;
     }
-    if (kCl) asm volatile("barrier.cluster.arrive.release;" ::: "memory");
-    auto part_of = [&](int rr) -> float4 {
-      return make_float4(__shfl_sync(0xffffffffu, mine4.x, rr), __shfl_sync(0xffffffffu, mine4.y, rr),
-                         __shfl_sync(0xffffffffu, mine4.z, rr), __shfl_sync(0xffffffffu, mine4.w, rr));
-    };
-    float R = kSNoRef, B = -INFINITY;
-    int I = INT_MAX;
-    for (int rr = 0; rr < C; ++rr) {
-      const float4 v = part_of(rr);
-      R = fmaxf(R, v.x);
-      if (greedy) {
-        const int ir = __float_as_int(v.w);
-        if (v.z > B) {
-          B = v.z;
-          I = ir;
-        } else if (v.z == B) {
-          I = min(I, ir);
+  } else {
+    float u = u_in;
+    if (!(u >= 0.f && u < 1.f)) {
+      if (threadIdx.x == 0 && rank == 0) set_error(p.err, OTK_ERR_INVALID_ARG);
+      u = fminf(fmaxf(u, 0.f), 0.99999994f);
+    }
+    float Tt = u * Sw;
+    if (!(Tt < Sw)) Tt = Sw * 0.99999976f;
+    // crossing lane, then its crossing partial (column order); fallback: the last partial with mass
+    const unsigned cl = __ballot_sync(0xffffffffu, incl > Tt);
+    const unsigned nzl = __ballot_sync(0xffffffffu, lt > 0.f);
+    const int L = cl ? __ffs(cl) - 1 : 31 - __clz(nzl);
+    float P = __shfl_sync(0xffffffffu, __fadd_rn(incl, -lt), L);   // mass before lane L's partials
+    int X = -1, Xl = -1;
+    float Px = 0.f, Pl = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float ci = __shfl_sync(0xffffffffu, c[i], L);
+      if (i < NP) {
+        const float Pn = __fadd_rn(P, ci);
+        if (ci > 0.f) {
+          Xl = L * NP + i;
+          Pl = P;
         }
-      }
-    }
-    float Sw = 0.f;
-    for (int rr = 0; rr < C; ++rr) {
-      const float4 v = part_of(rr);
-      if (v.y > 0.f) Sw = __fadd_rn(Sw, __fmul_rn(v.y, ex2(v.x - R)));
-    }
-    // as the other samplers (R32): logits <= -1e30 carry no mass, a row without any larger one is degenerate
-    const bool degenerate = greedy ? !(B > -1e30f) || (need_sum && !(Sw > 0.f))
-                                   : (!(R > kSNoRef) || !(Sw > 0.f));
-    if (greedy || degenerate) {
-      if (rank == 0 && lane == 0) {
-        p.tokens[row] = degenerate ? 0 : I;
-        if (p.logp) p.logp[row] = degenerate ? -INFINITY : (B * k2 - R - log2f(Sw)) * 0.6931471805599453f;
-      }
-    } else {
-      float u = p.u[row];
-      if (!(u >= 0.f && u < 1.f)) {
-        if (lane == 0 && rank == 0) set_error(p.err, OTK_ERR_INVALID_ARG);
-        u = fminf(fmaxf(u, 0.f), 0.99999994f);
-      }
-      float Tt = u * Sw;
-      if (!(Tt < Sw)) Tt = Sw * 0.99999976f;
-      // crossing CTA (rank order), fallback: the last CTA with mass
-      int rs = -1, rlast = 0;
-      float P = 0.f, Pc = 0.f, Plast = 0.f;
-      for (int rr = 0; rr < C; ++rr) {
-        const float4 v = part_of(rr);
-        const float c = v.y > 0.f ? __fmul_rn(v.y, ex2(v.x - R)) : 0.f;
-        if (c > 0.f) {
-          rlast = rr;
-          Plast = P;
-        }
-        const float Pn = __fadd_rn(P, c);
-        if (Pn > Tt) {
-          rs = rr;
-          Pc = P;
-          break;
+        if (X < 0 && Pn > Tt) {
+          X = L * NP + i;
+          Px = P;
         }
         P = Pn;
       }
-      if (rs < 0) {
-        rs = rlast;
-        Pc = Plast;
+    }
+    if (X < 0) {
+      X = Xl;
+      Px = Pl;
+    }
+    SDEC_T(5);
+    if (X == rank * kDecWarps + warp) {
+      // this warp holds the crossing: segment (sequential over its K), lane (warp scan), column (one per lane);
+      // every segment of the warp is at its reference racc
+      const float fseg = ex2(racc - R);
+      int ks = -1, kl = 0;
+      float Pseg = Px, Plast = Px, Pk = Px;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (sg0 + k < sg1) {
+          const float ck = __fmul_rn(cs_k[k], fseg);
+          const float Pn = __fadd_rn(Pk, ck);
+          if (ck > 0.f) {
+            kl = k;
+            Plast = Pk;
+          }
+          if (ks < 0 && Pn > Tt) {
+            ks = k;
+            Pseg = Pk;
+          }
+          Pk = Pn;
+        }
       }
-      if (rank == rs) {
-        // crossing segment (column order), 32 per step: lane prefix sums, ballot of the first crossing
-        int seg = -1, seglast = -1;
-        float Pseg = 0.f, Pl = 0.f, fseg = 0.f, flast = 0.f;
-        P = Pc;
-        for (int base = 0; base < nseg && seg < 0; base += 32) {
-          const int i = base + lane;
-          float c = 0.f, f = 0.f;
-          if (i < nseg) {
-            const float2 v = S.part[i];
-            f = ex2(v.y - R);
-            c = v.x > 0.f ? __fmul_rn(v.x, f) : 0.f;
-          }
-          float incl = c;
+      if (ks < 0) {
+        ks = kl;
+        Pseg = Plast;
+      }
+      uint4 qa = ninf, qb = ninf;
+      float ls = 0.f;                                // the lane's sum of the segment (the pass's value, bit for bit)
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const float y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl = __fadd_rn(incl, y);
-          }
-          const unsigned cross = __ballot_sync(0xffffffffu, i < nseg && __fadd_rn(P, incl) > Tt);
-          const unsigned nz = __ballot_sync(0xffffffffu, c > 0.f);
-          if (nz) {
-            const int l = 31 - __clz(nz);
-            seglast = base + l;
-            Pl = __fadd_rn(P, __shfl_sync(0xffffffffu, incl - c, l));
-            flast = __shfl_sync(0xffffffffu, f, l);
-          }
-          if (cross) {
-            const int l = __ffs(cross) - 1;
-            seg = base + l;
-            Pseg = __fadd_rn(P, __shfl_sync(0xffffffffu, incl - c, l));
-            fseg = __shfl_sync(0xffffffffu, f, l);
-          }
-          P = __fadd_rn(P, __shfl_sync(0xffffffffu, incl, 31));
+      for (int k = 0; k < KMAX; ++k)
+        if (k == ks) {
+          qa = q[k][0];
+          qb = q[k][1];
+          ls = cs_l[k];
         }
-        if (seg < 0) {
-          seg = max(seglast, 0);
-          Pseg = Pl;
-          fseg = flast;
-        }
-        // the segment from SHARED memory: lane l's vectors 2l, 2l+1 (the e values of the segment pass, bit for bit)
-        const float rseg = S.part[seg].y;
-        const int v0 = v_begin + seg * VPS + 2 * lane;
-        uint4 q[2];
+      const int v0 = (sg0 + ks) * VPS + 2 * lane;
+      const float rk = -racc;
+      float li = ls;
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const int v = v0 + k;
-          q[k] = v < nvec ? *reinterpret_cast<const uint4*>(data + size_t(v - v_begin) * 16) : ninf;
-          if (v == nvec - 1 && tail_valid < EV) SV::mask_tail(q[k], tail_valid);
-        }
-        const float rk = -rseg;
-        const uint64_t rk2 = f2(rk, rk);
-        const float ls = __fadd_rn(SV::esum(q[0], k2x2, rk2), SV::esum(q[1], k2x2, rk2));
-        float incl = ls;
+      for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, li, o);
+        if (lane >= o) li = __fadd_rn(li, y);
+      }
+      const unsigned cross = __ballot_sync(0xffffffffu, __fadd_rn(Pseg, __fmul_rn(li, fseg)) > Tt);
+      const unsigned nz = __ballot_sync(0xffffffffu, ls > 0.f);
+      const int lw = cross ? __ffs(cross) - 1 : (nz ? 31 - __clz(nz) : 0);
+      // lane lw's 2 EV elements, one per lane (column order), scanned across the warp
+      const float base = __shfl_sync(0xffffffffu, __fadd_rn(Pseg, __fmul_rn(li - ls, fseg)), lw);
+      uint4 qq[2];
+      qq[0].x = __shfl_sync(0xffffffffu, qa.x, lw);
+      qq[0].y = __shfl_sync(0xffffffffu, qa.y, lw);
+      qq[0].z = __shfl_sync(0xffffffffu, qa.z, lw);
+      qq[0].w = __shfl_sync(0xffffffffu, qa.w, lw);
+      qq[1].x = __shfl_sync(0xffffffffu, qb.x, lw);
+      qq[1].y = __shfl_sync(0xffffffffu, qb.y, lw);
+      qq[1].z = __shfl_sync(0xffffffffu, qb.z, lw);
+      qq[1].w = __shfl_sync(0xffffffffu, qb.w, lw);
+      const int vl = __shfl_sync(0xffffffffu, v0, lw);
+      const int ke = lane / EV, ie = lane % EV;   // this lane's element (lanes >= 2 EV: none)
+      float x = -INFINITY, e = 0.f;
+      if (lane < 2 * EV) {
+        const uint4 qk = ke == 0 ? qq[0] : qq[1];
+        x = SV::elem(qk, ie);
+        e = __fmul_rn(e_elem<T>(qk, ie, k2, rk), fseg);
+      }
+      float acc = e;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const float y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl = __fadd_rn(incl, y);
-        }
-        const unsigned cross = __ballot_sync(0xffffffffu, __fadd_rn(Pseg, __fmul_rn(incl, fseg)) > Tt);
-        const unsigned nz = __ballot_sync(0xffffffffu, ls > 0.f);
-        const int lw = cross ? __ffs(cross) - 1 : (nz ? 31 - __clz(nz) : 0);
-        // lane lw's 2 EV elements, one per lane (column order), scanned across the warp
-        const float base = __shfl_sync(0xffffffffu, __fadd_rn(Pseg, __fmul_rn(incl - ls, fseg)), lw);
-        uint4 qq[2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          qq[k].x = __shfl_sync(0xffffffffu, q[k].x, lw);
-          qq[k].y = __shfl_sync(0xffffffffu, q[k].y, lw);
-          qq[k].z = __shfl_sync(0xffffffffu, q[k].z, lw);
-          qq[k].w = __shfl_sync(0xffffffffu, q[k].w, lw);
-        }
-        const int vl = __shfl_sync(0xffffffffu, v0, lw);
-        const int ke = lane / EV, ie = lane % EV;   // this lane's element (lanes >= 2 EV: none)
-        float x = -INFINITY, e = 0.f;
-        if (lane < 2 * EV) {
-          const uint4 qk = ke == 0 ? qq[0] : qq[1];
-          x = SV::elem(qk, ie);
-          e = __fmul_rn(e_elem<T>(qk, ie, k2, rk), fseg);
-        }
-        float acc = e;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const float y = __shfl_up_sync(0xffffffffu, acc, o);
-          if (lane >= o) acc = __fadd_rn(acc, y);
-        }
-        const unsigned hit = __ballot_sync(0xffffffffu, lane < 2 * EV && __fadd_rn(base, acc) > Tt);
-        const unsigned enz = __ballot_sync(0xffffffffu, e > 0.f);
-        const int li = hit ? __ffs(hit) - 1 : (enz ? 31 - __clz(enz) : 0);  // fallback: the last column with mass
-        const float xt = __shfl_sync(0xffffffffu, x, li);
-        if (lane == 0) {
-          p.tokens[row] = vl * EV + li;
-          if (p.logp) p.logp[row] = (xt * k2 - R - log2f(Sw)) * 0.6931471805599453f;
-        }
+      for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, acc, o);
+        if (lane >= o) acc = __fadd_rn(acc, y);
+      }
+      const unsigned hit = __ballot_sync(0xffffffffu, lane < 2 * EV && __fadd_rn(base, acc) > Tt);
+      const unsigned enz = __ballot_sync(0xffffffffu, e > 0.f);
+      const int le = hit ? __ffs(hit) - 1 : (enz ? 31 - __clz(enz) : 0);  // fallback: the last column with mass
+      const float xt = __shfl_sync(0xffffffffu, x, le);
+      if (lane == 0) {
+        p.tokens[row] = vl * EV + le;
+        if (p.logp) p.logp[row] = (xt * k2 - R - log2f(Sw)) * 0.6931471805599453f;
       }
     }
   }
-  SDEC_T(4);
-  if (kCl) asm volatile("barrier.cluster.wait.acquire;" ::: "memory");  // no CTA exits while a peer reads its partial
-  SDEC_T(5);
+  SDEC_T(6);
 }
 #ifdef OTK_SDEC_TIMING
-extern "C" void otk_debug_sdec(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_sdec_t, sizeof(g_sdec_t)); }
+extern "C" void otk_debug_sdec(unsigned long long* out) {  // out: [256][8]
+  cudaMemcpyFromSymbol(out, g_sdec_t, sizeof(g_sdec_t));
+}
 #endif
 
-// the decode kernel's shape for this batch, or false: C >= 4 CTAs per row with C * rows <= SMs and a range of at
-// most kDecMaxSegs segments per CTA
+namespace {
+template <int KMAX>
+const void* dec_kernel(int dtype) {
+  return dtype == OTK_BF16 ? reinterpret_cast<const void*>(k_sample_dec<__nv_bfloat16, KMAX>)
+                           : reinterpret_cast<const void*>(k_sample_dec<float, KMAX>);
+}
+const void* dec_kernel(int dtype, int nseg_c) {
+  return nseg_c <= kDecWarps * 4 ? dec_kernel<4>(dtype) : dec_kernel<8>(dtype);
+}
+// clusters of c CTAs of this kernel that can be resident at once (cached; the same for every B200)
+int dec_max_clusters(int dtype, int nseg_c, int c) {
+  static int cache[2][2][kDecMaxC + 1];
+  static bool init = false;
+  if (!init) {
+    for (auto& a : cache)
+      for (auto& b : a)
+        for (int& v : b) v = -1;
+    init = true;
+  }
+  int& slot = cache[dtype == OTK_BF16][nseg_c > kDecWarps * 4][c];
+  if (slot < 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(c), 1, 1);
+    cfg.blockDim = dim3(kDecThreads, 1, 1);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(c);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, dec_kernel(dtype, nseg_c), &cfg) != cudaSuccess) {
+      (void)cudaGetLastError();
+      n = 0;
+    }
+    slot = n;
+  }
+  return slot;
+}
+}  // namespace
+
+// the decode kernel's shape for this batch, or false: the largest C <= 8 CTAs per row (>= 4) whose clusters are
+// all resident at once (one wave), with at most kDecMaxSegs segments per CTA
 bool sample_dec_shape(int64_t num_rows, int64_t vocab, int dtype, int num_sms, int* csize, int* nseg_c) {
   const int64_t nvec = (vocab * (dtype == OTK_BF16 ? 2 : 4) + 15) / 16;
   const int64_t nsegs = (nvec + 63) / 64;
   if (num_rows < 1 || num_rows > num_sms) return false;
-  // at least 4 CTAs per row (<= 37 rows on 148 SMs): measured faster than the lane-strided kernel there (16 rows
-  // 7.8 vs 8.4 us), slower with 2 (64 rows 13.0 vs 12.3 us: a 152 KB range per CTA is one SM's bandwidth share)
+  // at least 3 CTAs per row (<= 49 rows on 148 SMs), the whole range in registers
 #ifndef OTK_SDEC_MINC
-#define OTK_SDEC_MINC 4
+#define OTK_SDEC_MINC 3
 #endif
-  const int64_t c = std::min<int64_t>(8, num_sms / num_rows);
-  if (c < OTK_SDEC_MINC) return false;
-  const int64_t per = (nsegs + c - 1) / c;
-  if (per > kDecMaxSegs) return false;
-  *csize = int(c);
-  *nseg_c = int(per);
-  return true;
+  for (int64_t c = std::min<int64_t>(kDecMaxC, num_sms / num_rows); c >= OTK_SDEC_MINC; --c) {
+    const int64_t per = (nsegs + c - 1) / c;
+    if (per > kDecMaxSegs) return false;
+    if (dec_max_clusters(dtype, int(per), int(c)) < num_rows) continue;
+    *csize = int(c);
+    *nseg_c = int(per);
+    return true;
+  }
+  return false;
 }
 
 cudaError_t launch_sample_dec(otk_ctx* ctx, SampleParams p, int dtype, int csize, int nseg_c, cudaStream_t s) {
   p.csize = csize;
-  const size_t smem = kDecSmemBase + size_t(nseg_c) * kDecSeg;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(p.num_rows * csize), 1, 1);
   cfg.blockDim = dim3(kDecThreads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -766,16 +766,14 @@ cudaError_t launch_sample_dec(otk_ctx* ctx, SampleParams p, int dtype, int csize
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = csize > 1 ? 1 : 0;
+  cfg.numAttrs = 1;
   auto go = [&](auto kern) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    e = cudaLaunchKernelEx(&cfg, kern, p, nseg_c);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p, nseg_c);
     return e != cudaSuccess ? e : cudaGetLastError();
   };
-  if (dtype == OTK_BF16)
-    return csize > 1 ? go(k_sample_dec<__nv_bfloat16, true>) : go(k_sample_dec<__nv_bfloat16, false>);
-  return csize > 1 ? go(k_sample_dec<float, true>) : go(k_sample_dec<float, false>);
+  const bool small = nseg_c <= kDecWarps * 4;   // <= 4 segments per warp: half the registers of data
+  if (dtype == OTK_BF16) return small ? go(k_sample_dec<__nv_bfloat16, 4>) : go(k_sample_dec<__nv_bfloat16, 8>);
+  return small ? go(k_sample_dec<float, 4>) : go(k_sample_dec<float, 8>);
 }
 
 bool sample_tm_fits(int64_t vocab, int dtype) {

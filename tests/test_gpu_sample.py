@@ -210,9 +210,10 @@ def test_sampled_degenerate_rows_ring_kernel(otk, ctx, dtype, V):
 
 @pytest.mark.parametrize("dtype,V,n", [("bf16", 151936, 16), ("bf16", 151936, 37), ("bf16", 151936, 1),
                                        ("f32", 50000, 30), ("bf16", 4100, 9), ("bf16", 17, 5),
+                                       ("bf16", 151936, 33), ("f32", 151936, 16),
                                        ("bf16", 151936, 100)])   # 100 rows: the ring kernel
 def test_decode_batches(otk, ctx, dtype, V, n):
-    """Decode-sized batches (<= 37 rows: k_sample_dec, one row per cluster, each CTA's column range held in shared memory;
+    """Decode-sized batches (<= 49 rows: k_sample_dec, one row per cluster, each CTA's column range held in registers;
     96-147 rows: the ring kernel):
     sampled draws vs the oracle, greedy bit-exact, degenerate rows, and single finite columns at the first / last
     column and at the boundaries between the cluster's CTA ranges (u = 0 and u -> 1)."""
@@ -236,6 +237,12 @@ def test_decode_batches(otk, ctx, dtype, V, n):
         x[6, :] = -200.0
         x[6, V - 3] = 150.0
         special[6] = V - 3
+    if n >= 16:   # the first column of CTA rank 1 for every cluster size the kernel may pick (3-8, by occupancy)
+        for j, c in zip(range(8, 14), range(3, 9)):
+            col = min(-(-(-(-(V * es) // 16) // 64) // c) * 64 * 16 // es, V - 1)
+            x[j, :] = float("-inf")
+            x[j, col] = 1.0
+            special[j] = col
     u = torch.rand(n, generator=torch.Generator().manual_seed(n)).float()
     if n >= 5:
         u[1:3] = 0.0
