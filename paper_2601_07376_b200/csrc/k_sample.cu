@@ -440,14 +440,57 @@ int sample_occupancy(otk_ctx* ctx, int slot) {
   return o;
 }
 
+// resident clusters of c CTAs of k_sample<T, true, kMinB> (cached per process; the same on every B200)
+template <typename T, int kMinB>
+int sample_max_clusters(int c) {
+  static int cache[kSampleMaxCluster + 1] = {};
+  int& slot = cache[c];
+  if (slot == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(c), 1, 1);
+    cfg.blockDim = dim3(kSampleThreads, 1, 1);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(c);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_sample<T, true, kMinB>, &cfg) != cudaSuccess) {
+      (void)cudaGetLastError();
+      n = 0;
+    }
+    slot = n > 0 ? n : -1;
+  }
+  return slot;
+}
+
 template <typename T, int kMinB>
 static cudaError_t launch_lane_strided(otk_ctx* ctx, SampleParams p, cudaStream_t s, int occ_slot) {
   const int64_t slots = int64_t(ctx->num_sms) * sample_occupancy<T, kMinB>(ctx, occ_slot);
   // cluster size: when rows are few, as many CTAs per row as fit in ONE wave of resident CTAs; one CTA
   // per row otherwise (a cluster barrier per row costs more than the last wave's imbalance)
-  const int best_c = int(std::min<int64_t>(kSampleMaxCluster, std::max<int64_t>(1, slots / p.num_rows)));
+  // per-row time ~ (rows per cluster) / (CTAs per row); clusters of c are placed by GPC, so fewer than slots / c of
+  // them may be resident at once (cudaOccupancyMaxActiveClusters): a cluster size whose clusters do not all fit
+  // would run a second wave (48 rows in 6-CTA clusters: 18.4 us)
+  int best_c = 1;
+  int64_t groups = std::min<int64_t>(p.num_rows, slots);
+  {
+    double best_t = 1e30;
+    for (int c = int(std::min<int64_t>(kSampleMaxCluster, std::max<int64_t>(1, slots / p.num_rows))); c >= 1; --c) {
+      const int64_t fit = c == 1 ? slots : std::min<int64_t>(slots / c, sample_max_clusters<T, kMinB>(c));
+      if (fit < 1) continue;
+      const int64_t g = std::min<int64_t>(p.num_rows, fit);
+      const double t = double((p.num_rows + g - 1) / g) / c;
+      if (t < best_t) {
+        best_t = t;
+        best_c = c;
+        groups = g;
+      }
+    }
+  }
   p.csize = best_c;
-  const int64_t groups = std::min<int64_t>(p.num_rows, slots / best_c);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(groups * best_c), 1, 1);
   cfg.blockDim = dim3(kSampleThreads, 1, 1);

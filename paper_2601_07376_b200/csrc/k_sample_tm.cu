@@ -104,6 +104,16 @@ struct SV2<float> {
   }
 };
 
+__device__ __forceinline__ float redux_max_f32(float v) {   // warp max (sm_100a: one CREDUX)
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ int redux_min_s32(int v) {
+  int r;
+  asm volatile("redux.sync.min.s32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+  return r;
+}
 // element i of a vector: its e at reference rk (same formula as esum, element by element)
 template <typename T>
 __device__ __forceinline__ float e_elem(const uint4& q, int i, float k2, float rk) {
@@ -111,6 +121,18 @@ __device__ __forceinline__ float e_elem(const uint4& q, int i, float k2, float r
 }
 }  // namespace
 
+#ifdef OTK_STM_TIMING  // experiments only: [cta][0] globaltimer at the start (ns), [cta][1..] clock64 stamps of the
+// first row: 1 start, 2 consumer warp 1 has chunk 0, 3 it has finished the row, 4 search warp has the row, 5 done
+__device__ unsigned long long g_stm_t[256 * 8];
+#define STM_T(i, who)                                                                 \
+  if ((who) && blockIdx.x < 256 && row == blockIdx.x) {                               \
+    if ((i) == 1) g_stm_t[blockIdx.x * 8] = globaltimer_ns();                         \
+    g_stm_t[blockIdx.x * 8 + (i)] = clock64();                                        \
+  }
+extern "C" void otk_debug_stm(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_stm_t, sizeof(g_stm_t)); }
+#else
+#define STM_T(i, who)
+#endif
 template <typename T>
 __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p) {
   using SV = SV2<T>;
@@ -130,6 +152,12 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
   const uint4 ninf = sizeof(T) == 2 ? make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u)
                                     : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
 
+#ifdef OTK_STM_TIMING
+  {
+    const int64_t row = blockIdx.x;
+    STM_T(1, threadIdx.x == 0);
+  }
+#endif
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSSlots; ++i) {
       mbar_init(&S.full[i], 1);
@@ -173,6 +201,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
       float r = kSNoRef;                      // warp-uniform reference (k2 units)
       for (int c = 0; c < nch; ++c) {
         mbar_wait(&S.full[slot], phase);
+        STM_T(2, c == 0 && ct == 0);
         const uint8_t* buf = ring + size_t(slot) * kSChunk + ct * 32;
         uint4 q0 = *reinterpret_cast<const uint4*>(buf);
         uint4 q1 = *reinterpret_cast<const uint4*>(buf + 16);
@@ -218,6 +247,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
         if (lane == 0) S.part[par][c][cw] = make_float2(cs, r);
       }
       __syncwarp();
+      STM_T(3, ct == 0);
       if (lane == 0) mbar_arrive(&S.hfull[par]);
       par ^= 1u;
       if (par == 0) hph ^= 1u;
@@ -227,20 +257,28 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
     uint32_t par = 0, hph = 0;
     for (int64_t row = blockIdx.x; row < p.num_rows; row += gridDim.x) {
       mbar_wait(&S.hfull[par], hph);
-      // row reference R and total S (fixed order: chunk-major, warp-minor, lane-strided then butterfly)
+      STM_T(4, lane == 0);
+      // row reference R and total S: lane l takes the B contiguous segments [l B, (l + 1) B) (column order:
+      // chunk-major, warp-minor), then one 32-lane scan of the lane totals
       const int nseg = nch * kSWarps;
-      float R = kSNoRef;
-      for (int i = lane; i < nseg; i += 32) R = fmaxf(R, S.part[par][i / kSWarps][i % kSWarps].y);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) R = fmaxf(R, __shfl_xor_sync(0xffffffffu, R, o));
-      float Sl = 0.f;
-      for (int i = lane; i < nseg; i += 32) {
-        const float2 v = S.part[par][i / kSWarps][i % kSWarps];
-        if (v.x > 0.f) Sl = __fadd_rn(Sl, __fmul_rn(v.x, ex2(v.y - R)));
+      const int B = (nseg + 31) / 32;
+      const int i0 = min(lane * B, nseg), i1 = min(i0 + B, nseg);
+      auto part_at = [&](int i) { return S.part[par][i / kSWarps][i % kSWarps]; };
+      float rl = kSNoRef;
+      for (int i = i0; i < i1; ++i) rl = fmaxf(rl, part_at(i).y);
+      const float R = redux_max_f32(rl);
+      float lt = 0.f;
+      for (int i = i0; i < i1; ++i) {
+        const float2 v = part_at(i);
+        if (v.x > 0.f) lt = __fadd_rn(lt, __fmul_rn(v.x, ex2(v.y - R)));
       }
-      float Sw = Sl;
+      float incl = lt;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) Sw = __fadd_rn(Sw, __shfl_xor_sync(0xffffffffu, Sw, o));
+      for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl = __fadd_rn(incl, y);
+      }
+      const float Sw = __shfl_sync(0xffffffffu, incl, 31);
       const bool degenerate = !(R > kSNoRef) || !(Sw > 0.f);
       const T* rbase = reinterpret_cast<const T*>(p.logits) + row * p.ld;
       if (degenerate) {  // no finite logit: token 0, logp -inf (as k_sample.cu)
@@ -258,44 +296,32 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
         }
         float Tt = u * Sw;
         if (!(Tt < Sw)) Tt = Sw * 0.99999976f;
-        // crossing segment, in column order; 32 segments per step: lane prefix sums, ballot of the first crossing
-        int seg = -1, seglast = -1;
-        float P = 0.f, Pseg = 0.f, Plast = 0.f, fseg = 0.f, flast = 0.f;
-        for (int base = 0; base < nseg && seg < 0; base += 32) {
-          const int i = base + lane;
-          float c = 0.f, f = 0.f;
-          if (i < nseg) {
-            const float2 v = S.part[par][i / kSWarps][i % kSWarps];
-            f = ex2(v.y - R);
-            c = v.x > 0.f ? __fmul_rn(v.x, f) : 0.f;
-          }
-          float incl = c;
+        // the crossing lane's range (fallback: the last lane with mass), then its segments one per lane, scanned
+        const unsigned cl = __ballot_sync(0xffffffffu, incl > Tt);
+        const unsigned nzl = __ballot_sync(0xffffffffu, lt > 0.f);
+        const int L = cl ? __ffs(cl) - 1 : 31 - __clz(nzl);
+        const float excl = __shfl_up_sync(0xffffffffu, incl, 1);
+        const float Pb = L == 0 ? 0.f : __shfl_sync(0xffffffffu, excl, L);
+        const int j0 = min(L * B, nseg), j1 = min(j0 + B, nseg);
+        const int i = j0 + lane;
+        float c = 0.f, f = 0.f;
+        if (i < j1) {
+          const float2 v = part_at(i);
+          f = ex2(v.y - R);
+          c = v.x > 0.f ? __fmul_rn(v.x, f) : 0.f;
+        }
+        float ic = c;
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const float y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl = __fadd_rn(incl, y);
-          }
-          const unsigned cross = __ballot_sync(0xffffffffu, i < nseg && __fadd_rn(P, incl) > Tt);
-          const unsigned nz = __ballot_sync(0xffffffffu, c > 0.f);
-          if (nz) {  // last segment with mass so far (fallback)
-            const int l = 31 - __clz(nz);
-            seglast = base + l;
-            Plast = __fadd_rn(P, __shfl_sync(0xffffffffu, incl - c, l));
-            flast = __shfl_sync(0xffffffffu, f, l);
-          }
-          if (cross) {
-            const int l = __ffs(cross) - 1;
-            seg = base + l;
-            Pseg = __fadd_rn(P, __shfl_sync(0xffffffffu, incl - c, l));
-            fseg = __shfl_sync(0xffffffffu, f, l);
-          }
-          P = __fadd_rn(P, __shfl_sync(0xffffffffu, incl, 31));
+        for (int o = 1; o < 32; o <<= 1) {
+          const float y = __shfl_up_sync(0xffffffffu, ic, o);
+          if (lane >= o) ic = __fadd_rn(ic, y);
         }
-        if (seg < 0) {
-          seg = seglast;
-          Pseg = Plast;
-          fseg = flast;
-        }
+        const unsigned crs = __ballot_sync(0xffffffffu, i < j1 && __fadd_rn(Pb, ic) > Tt);
+        const unsigned nzs = __ballot_sync(0xffffffffu, c > 0.f);
+        const int l = crs ? __ffs(crs) - 1 : (nzs ? 31 - __clz(nzs) : 0);   // fallback: the last with mass
+        const int seg = j0 + l;
+        const float Pseg = __fadd_rn(Pb, __shfl_sync(0xffffffffu, ic - c, l));
+        const float fseg = __shfl_sync(0xffffffffu, f, l);
         const int cstar = seg / kSWarps, wstar = seg % kSWarps;
         const float rseg = S.part[par][cstar][wstar].y;
         __syncwarp();
@@ -355,6 +381,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
           if (p.logp) p.logp[row] = (xt * k2 - R - log2f(Sw)) * 0.6931471805599453f;
         }
       }
+      STM_T(5, lane == 0);
       par ^= 1u;
       if (par == 0) hph ^= 1u;
     }
@@ -403,16 +430,6 @@ __device__ unsigned long long g_sdec_t[256 * 8];
 #define SDEC_T(i)
 #endif
 
-__device__ __forceinline__ float redux_max_f32(float v) {   // warp max (sm_100a: one CREDUX)
-  float r;
-  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
-  return r;
-}
-__device__ __forceinline__ int redux_min_s32(int v) {
-  int r;
-  asm volatile("redux.sync.min.s32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
-  return r;
-}
 __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
   uint4 v;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
