@@ -15,6 +15,8 @@
  *   LM head fused with (4) (NEXT-1, fwd + bwd): otk_lmhead_policy_loss_fwd_bwd — loss, dh, dW; the
  *                                dlogits exist only as SMEM tiles inside the backward tcgen05 GEMMs
  *   rollout sampling (NEXT-3): otk_sample_tokens — softmax / greedy token per row
+ *   batch sharding over NCCL: otk_comm_* and otk_batch_* — the three exchanges of a
+ *       batch-sharded step (global token count, group statistics, loss statistics).
  *   vocab sharding (north_star "vocab-sharding logits with an all-reduce of row max and sum-exp"):
  *       otk_row_partials → (caller all-gathers partials) → otk_logprob_entropy_combine /
  *       otk_policy_loss_fwd_bwd_partials; or, fused: otk_policy_loss_fwd_bwd_vpf (the exchange runs inside
@@ -63,7 +65,9 @@ typedef enum {
   OTK_ERR_TARGET_RANGE = 8,  /* target outside [0, vocab_total)                             */
   OTK_ERR_CUDA = 9,          /* a CUDA runtime call failed (see otk_last_error)             */
   OTK_ERR_GROUP_RANGE = 10,  /* group_id outside [0, num_groups)                            */
-  OTK_ERR_PEER_TIMEOUT = 11  /* K4-VPF: a peer rank's row partial did not arrive in time     */
+  OTK_ERR_PEER_TIMEOUT = 11, /* K4-VPF: a peer rank's row partial did not arrive in time     */
+  OTK_ERR_NCCL = 12,         /* NCCL could not be loaded or a collective failed (otk_last_error) */
+  OTK_ERR_NO_COMM = 13       /* a batch-sharded call on a ctx without otk_comm_init            */
 } otk_status;
 
 typedef enum { OTK_SRC_CONTEXT = 0, OTK_SRC_ACTION = 1, OTK_SRC_OBSERVATION = 2, OTK_SRC_PAD = 3 } otk_source;
@@ -454,6 +458,41 @@ otk_status otk_lmhead_policy_loss_fwd_bwd(otk_ctx* ctx, int64_t num_rows, int64_
                                           const otk_loss_cfg* cfg, void* workspace, int64_t workspace_bytes,
                                           void* dhidden, void* dweight, float* logp, float* entropy,
                                           otk_loss_stats* stats, otk_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Batch sharding over NCCL (SURVEY.md §8(b), §8(e) BATCH; PAPER.md:64 and :84 — one job's update spread over
+ * the GPUs of the shared cluster): rank r holds a contiguous range of the global batch's trajectories (groups
+ * may straddle ranks) and runs (1), (2), (4) on it; three exchanges make the result identical to one GPU's:
+ *   otk_build_masks (local)                    -> otk_batch_allreduce_i64(n_loss [, n_active_traj])
+ *   returns of the local trajectories          -> otk_batch_group_advantages (all-gather in rank order + (2) on
+ *                                                 the whole batch: every rank gets identical group statistics)
+ *   otk_policy_loss_fwd_bwd per micro-batch    -> otk_batch_allreduce_f64(stats, 5)
+ * The communicator belongs to the ctx (one ctx per rank / GPU). NCCL is bound at the first otk_comm_* call
+ * (dlopen of libnccl.so.2, or $OTK_NCCL_LIB; in a PyTorch process the copy torch already loaded), so the
+ * library has no link-time NCCL dependency; without NCCL these calls return OTK_ERR_NCCL. Collectives are
+ * stream-ordered on `stream`, capturable in a CUDA graph, and must be issued in the same order on every rank.
+ * ------------------------------------------------------------------------------------------- */
+#define OTK_COMM_ID_BYTES 128
+/* Host: a fresh NCCL unique id (on one rank; the caller hands the 128 bytes to every rank). */
+otk_status otk_comm_unique_id(unsigned char id[OTK_COMM_ID_BYTES]);
+/* Collective over the nranks processes (blocking until all have joined): ctx's device, rank in [0, nranks). */
+otk_status otk_comm_init(otk_ctx* ctx, const unsigned char id[OTK_COMM_ID_BYTES], int32_t nranks, int32_t rank);
+otk_status otk_comm_destroy(otk_ctx* ctx); /* also done by otk_ctx_destroy; no-op without a communicator */
+otk_status otk_comm_size(const otk_ctx* ctx, int32_t* nranks, int32_t* rank); /* OTK_ERR_NO_COMM if none */
+/* In place: buf[0, n) = sum over ranks (device int64 / float64). n >= 0. */
+otk_status otk_batch_allreduce_i64(otk_ctx* ctx, int64_t* buf, int64_t n, otk_stream_t stream);
+otk_status otk_batch_allreduce_f64(otk_ctx* ctx, double* buf, int64_t n, otk_stream_t stream);
+/* Step (2) over the global batch. group_id / returns: this rank's [num_traj_local] (device); counts: HOST
+ * [nranks] trajectories per rank (counts[rank] == num_traj_local; the shard plan knows them, so no size exchange);
+ * gid_all / ret_all: device [B = sum counts], filled with every rank's (group_id, return) in rank order;
+ * adv_all [B] and group_mean / group_std [num_groups] f64, group_size [num_groups] i32 (NULL ok): as
+ * otk_group_advantages on the whole batch, identical on every rank. This rank's advantages are
+ * adv_all + sum(counts[0 .. rank)). */
+otk_status otk_batch_group_advantages(otk_ctx* ctx, int32_t num_traj_local, const int32_t* group_id,
+                                      const double* returns, const int32_t* counts, int32_t num_groups,
+                                      uint32_t flags, double std_floor, int32_t* gid_all, double* ret_all,
+                                      double* adv_all, double* group_mean, double* group_std, int32_t* group_size,
+                                      otk_stream_t stream);
 
 /* Harness helper (not on the path): number of kernel launches the library issued since ctx creation. */
 int64_t otk_ctx_launch_count(const otk_ctx* ctx);

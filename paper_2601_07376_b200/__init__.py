@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 from dataclasses import dataclass
-from typing import Optional
+from typing import Optional, Sequence, Tuple
 
 import torch
 
@@ -31,7 +31,7 @@ CONTEXT, ACTION, OBSERVATION, PAD = 0, 1, 2, 3
 STATUS = {0: "OTK_OK", 1: "OTK_ERR_INVALID_ARG", 2: "OTK_ERR_SHAPE", 3: "OTK_ERR_ALIGNMENT", 4: "OTK_ERR_DTYPE",
           5: "OTK_ERR_EMPTY_GROUP", 6: "OTK_ERR_UNTERMINATED", 7: "OTK_ERR_BAD_TRAJECTORY",
           8: "OTK_ERR_TARGET_RANGE", 9: "OTK_ERR_CUDA", 10: "OTK_ERR_GROUP_RANGE",
-          11: "OTK_ERR_PEER_TIMEOUT"}
+          11: "OTK_ERR_PEER_TIMEOUT", 12: "OTK_ERR_NCCL", 13: "OTK_ERR_NO_COMM"}
 
 
 class OtkError(RuntimeError):
@@ -125,6 +125,14 @@ _sig = {
     "otk_ipc_get_handle": (C.c_int, [_P, _P]),
     "otk_ipc_open": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
     "otk_ipc_close": (C.c_int, [_P]),
+    "otk_comm_unique_id": (C.c_int, [_P]),
+    "otk_comm_init": (C.c_int, [_P, _P, C.c_int32, C.c_int32]),
+    "otk_comm_destroy": (C.c_int, [_P]),
+    "otk_comm_size": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "otk_batch_allreduce_i64": (C.c_int, [_P, _P, _I64, _P]),
+    "otk_batch_allreduce_f64": (C.c_int, [_P, _P, _I64, _P]),
+    "otk_batch_group_advantages": (C.c_int, [_P, C.c_int32, _P, _P, _P, C.c_int32, C.c_uint32, C.c_double,
+                                             _P, _P, _P, _P, _P, _P, _P]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -368,6 +376,80 @@ def otk_group_advantages(ctx: Context, group_id: torch.Tensor, num_groups: int, 
                                      _ptr(turn_offsets), _ptr(turn_rewards), flags, float(std_floor),
                                      _ptr(o["adv"]), _ptr(o["returns"]), _ptr(o["group_mean"]),
                                      _ptr(o["group_std"]), _ptr(o["group_size"]), _stream(stream)))
+    return o
+
+
+# ------------------------------------------------------------------------------------------------
+# batch sharding over NCCL (otk.h "Batch sharding"; SURVEY.md §8(e) BATCH)
+# ------------------------------------------------------------------------------------------------
+def otk_comm_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) on one rank; the caller hands it to every rank."""
+    buf = (C.c_ubyte * 128)()
+    _check(_lib.otk_comm_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+def otk_comm_init(ctx: Context, uid: bytes, nranks: int, rank: int) -> None:
+    if len(uid) != 128:
+        raise ValueError("uid must be the 128 bytes of otk_comm_unique_id")
+    buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+    _check(_lib.otk_comm_init(ctx.handle, C.cast(buf, C.c_void_p), int(nranks), int(rank)))
+
+
+def otk_comm_destroy(ctx: Context) -> None:
+    _check(_lib.otk_comm_destroy(ctx.handle))
+
+
+def otk_comm_size(ctx: Context) -> Tuple[int, int]:
+    n, r = C.c_int32(), C.c_int32()
+    _check(_lib.otk_comm_size(ctx.handle, C.byref(n), C.byref(r)))
+    return n.value, r.value
+
+
+def otk_batch_allreduce_i64(ctx: Context, buf: torch.Tensor, stream=None) -> torch.Tensor:
+    _arr(buf, "buf", torch.int64, None, buf.device)
+    _check(_lib.otk_batch_allreduce_i64(ctx.handle, _ptr(buf), int(buf.numel()), _stream(stream)))
+    return buf
+
+
+def otk_batch_allreduce_f64(ctx: Context, buf: torch.Tensor, stream=None) -> torch.Tensor:
+    _arr(buf, "buf", torch.float64, None, buf.device)
+    _check(_lib.otk_batch_allreduce_f64(ctx.handle, _ptr(buf), int(buf.numel()), _stream(stream)))
+    return buf
+
+
+def otk_batch_group_advantages(ctx: Context, group_id: torch.Tensor, returns: torch.Tensor, counts: Sequence[int],
+                               num_groups: int, *, std_norm: bool = True, unbiased: bool = False,
+                               std_floor: float = 1e-8, skip_ungrouped: bool = False, out: Optional[dict] = None,
+                               stream=None) -> dict:
+    """Step (2) over the global batch of a batch-sharded step: every rank's (group_id, return) gathered in rank
+    order over NCCL, then the group statistics on the whole batch (identical on every rank). `counts` = host list
+    of trajectories per rank. Returns gid_all, ret_all, adv_all (global), adv (this rank's slice) and the stats."""
+    dev = group_id.device
+    B = int(group_id.numel())
+    counts = [int(c) for c in counts]
+    total = sum(counts)
+    _arr(group_id, "group_id", torch.int32, B, dev)
+    _arr(returns, "returns", torch.float64, B, dev)
+    o = out if out is not None else {}
+    o.setdefault("gid_all", torch.empty(total, dtype=torch.int32, device=dev))
+    o.setdefault("ret_all", torch.empty(total, dtype=torch.float64, device=dev))
+    o.setdefault("adv_all", torch.empty(total, dtype=torch.float64, device=dev))
+    o.setdefault("group_mean", torch.empty(num_groups, dtype=torch.float64, device=dev))
+    o.setdefault("group_std", torch.empty(num_groups, dtype=torch.float64, device=dev))
+    o.setdefault("group_size", torch.empty(num_groups, dtype=torch.int32, device=dev))
+    for k in ("gid_all", "ret_all", "adv_all"):
+        _arr(o[k], k, o[k].dtype, total, dev)
+    flags = ((OTK_ADV_STD_NORM if std_norm else 0) | (OTK_ADV_UNBIASED if unbiased else 0)
+             | (OTK_ADV_SKIP_UNGROUPED if skip_ungrouped else 0))
+    cnt = (C.c_int32 * len(counts))(*counts)
+    _check(_lib.otk_batch_group_advantages(ctx.handle, B, _ptr(group_id), _ptr(returns), C.cast(cnt, C.c_void_p),
+                                           int(num_groups), flags, float(std_floor), _ptr(o["gid_all"]),
+                                           _ptr(o["ret_all"]), _ptr(o["adv_all"]), _ptr(o["group_mean"]),
+                                           _ptr(o["group_std"]), _ptr(o["group_size"]), _stream(stream)))
+    _, rank = otk_comm_size(ctx)
+    b0 = sum(counts[:rank])
+    o["adv"] = o["adv_all"][b0:b0 + B]
     return o
 
 

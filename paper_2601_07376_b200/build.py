@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2",
-    "--expt-relaxed-constexpr", "-cudart", "static",
+    "--expt-relaxed-constexpr", "-cudart", "static", "-ldl",
 ]
 
 

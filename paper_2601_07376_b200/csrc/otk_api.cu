@@ -146,6 +146,8 @@ void set_loss(otk::RowParams& p, const int32_t* row_traj, const double* adv, con
 
 }  // namespace
 
+otk_status otk::host_fail(otk_status s, const char* msg) { return fail(s, msg); }
+
 extern "C" {
 
 int otk_version(void) { return OTK_VERSION; }
@@ -166,6 +168,8 @@ const char* otk_status_string(otk_status s) {
     case OTK_ERR_CUDA: return "OTK_ERR_CUDA";
     case OTK_ERR_GROUP_RANGE: return "OTK_ERR_GROUP_RANGE";
     case OTK_ERR_PEER_TIMEOUT: return "OTK_ERR_PEER_TIMEOUT";
+    case OTK_ERR_NCCL: return "OTK_ERR_NCCL";
+    case OTK_ERR_NO_COMM: return "OTK_ERR_NO_COMM";
   }
   return "OTK_ERR_UNKNOWN";
 }
@@ -204,6 +208,7 @@ otk_status otk_ctx_create(int cuda_device, otk_ctx** out) {
 
 otk_status otk_ctx_destroy(otk_ctx* c) {
   if (!c) return OTK_OK;
+  otk::comm_release(c);
   cudaFree(c->d_err);
   cudaFree(c->d_tickets);
   cudaFree(c->d_partials);

@@ -24,9 +24,14 @@ struct otk_ctx {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t launches = 0;
   int sample_occ[4] = {0, 0, 0, 0};  // k_sample resident CTAs per SM (bf16, fp32; x2 register budgets), on first use
+  void* comm = nullptr;            // ncclComm_t of the batch-sharded step (otk_comm_init), or none
+  int comm_nranks = 0, comm_rank = 0;
 };
 
 namespace otk {
+
+otk_status host_fail(otk_status s, const char* msg);   // records otk_last_error's message (otk_api.cu)
+void comm_release(otk_ctx* ctx);                        // otk_comm.cu
 
 constexpr int kMaxCtas = 1024;
 constexpr int kStatSlots = 8;

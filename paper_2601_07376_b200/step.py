@@ -31,6 +31,7 @@ from typing import Callable, List, Optional, Sequence, Tuple
 import torch
 
 from . import (Context, DeviceTrajBatch, LossCfg, STATS_FIELDS, otk_build_masks, otk_group_advantages,
+               otk_batch_allreduce_f64, otk_batch_allreduce_i64, otk_batch_group_advantages, otk_comm_size,
                otk_logprob_entropy_combine, otk_policy_loss_fwd_bwd, otk_policy_loss_fwd_bwd_partials,
                otk_lmhead_row_partials, otk_policy_loss_fwd_bwd_vpf, otk_row_partials, otk_turn_returns,
                VpfExchange)
@@ -124,7 +125,7 @@ class PolicyLossStep:
                  process_group=None, global_num_traj: Optional[Sequence[int]] = None,
                  global_num_groups: Optional[int] = None, vocab_shard: Optional[VocabShard] = None,
                  credit: str = "trajectory", gamma: float = 1.0,
-                 global_num_segments: Optional[Sequence[int]] = None):
+                 global_num_segments: Optional[Sequence[int]] = None, collectives: str = "torch"):
         """process_group: batch sharding (this rank's trajectories; exchanges below). vocab_shard: vocab
         sharding (the rank holds a column range of the logits of its rows). Both: 2-D sharding — process_group
         is then the rank's batch group (same columns, other trajectories) and vocab_shard's group its vocab
@@ -132,13 +133,20 @@ class PolicyLossStep:
         credit: "trajectory" (north_star (2): one A per trajectory) or "turn" (NEXT-2, R31: the
         discounted reward-to-go of each trainable ACTION turn, group-normalised over the group's turns,
         read per row through the row's segment). global_num_segments: per-rank segment counts (batch
-        sharding with turn credit; default: every rank has this rank's count)."""
+        sharding with turn credit; default: every rank has this rank's count).
+        collectives: who runs batch sharding's three exchanges — "torch" (torch.distributed on process_group) or
+        "otk" (the library's own NCCL communicator on ctx, otk_comm_init: the C-ABI path a non-Python caller
+        uses; process_group is then not needed)."""
         self.vshard = vocab_shard
         self.ctx, self.batch, self.cfg, self.vocab = ctx, batch, cfg, vocab   # (cfg may gain count pointers)
         self.group_id, self.num_groups = group_id, num_groups
         self.turn_offsets, self.turn_rewards = turn_offsets, turn_rewards
         self.train_agent, self.std_norm, self.unbiased = train_agent, std_norm, unbiased
         self.pg = process_group
+        if collectives not in ("torch", "otk"):
+            raise ValueError(f"collectives must be 'torch' or 'otk', not {collectives!r}")
+        self.coll = collectives
+        self.sharded = process_group is not None or collectives == "otk"
         if credit not in ("trajectory", "turn"):
             raise ValueError(f"credit must be 'trajectory' or 'turn', not {credit!r}")
         self.credit, self.gamma = credit, float(gamma)
@@ -160,17 +168,20 @@ class PolicyLossStep:
         if cfg.reduction != 0:   # sequence-mean reductions read the per-trajectory token counts (R29)
             self.cfg = dataclasses.replace(cfg, traj_loss_tokens=self.masks["traj_loss_tokens"],
                                            n_active_traj=self.masks["n_active_traj"])
-        G_loc = global_num_groups if (process_group is not None and global_num_groups) else num_groups
+        G_loc = global_num_groups if (self.sharded and global_num_groups) else num_groups
         self.adv_out = dict(adv=torch.empty(E, dtype=torch.float64, device=dev),
                             returns=torch.empty(E, dtype=torch.float64, device=dev),
                             group_mean=torch.empty(G_loc, dtype=torch.float64, device=dev),
                             group_std=torch.empty(G_loc, dtype=torch.float64, device=dev),
                             group_size=torch.empty(G_loc, dtype=torch.int32, device=dev))
         self.stats = torch.zeros(len(STATS_FIELDS), dtype=torch.float64, device=dev)
-        if self.pg is not None:
-            import torch.distributed as dist
-            self.world = dist.get_world_size(self.pg)
-            self.rank = dist.get_rank(self.pg)
+        if self.sharded:
+            if self.coll == "otk":
+                self.world, self.rank = otk_comm_size(ctx)
+            else:
+                import torch.distributed as dist
+                self.world = dist.get_world_size(self.pg)
+                self.rank = dist.get_rank(self.pg)
             counts = list(global_num_traj) if global_num_traj is not None else [B] * self.world
             if credit == "turn":
                 counts = list(global_num_segments) if global_num_segments is not None else [S] * self.world
@@ -196,11 +207,16 @@ class PolicyLossStep:
                         row_seg=self.credit == "turn", out=self.masks)
         if self.credit == "turn":
             return self._turn_advantages()
-        if self.pg is None:
+        if not self.sharded:
             otk_group_advantages(self.ctx, self.group_id, self.num_groups, turn_offsets=self.turn_offsets,
                                  turn_rewards=self.turn_rewards, std_norm=self.std_norm, unbiased=self.unbiased,
                                  out=self.adv_out)
             return self.adv_out["adv"]
+        if self.coll == "otk":
+            self._otk_counts()
+            otk_group_advantages(self.ctx, self.group_id, self.G_global, turn_offsets=self.turn_offsets,
+                                 turn_rewards=self.turn_rewards, out=self.adv_out)
+            return self._otk_group_advantages(self.group_id, self.adv_out["returns"], False)
         from .dist import all_gather_group_returns, all_reduce_n_loss
         all_reduce_n_loss(self.masks["n_loss"], self.pg)
         if self.cfg.reduction != 0:
@@ -218,10 +234,13 @@ class PolicyLossStep:
         otk_turn_returns(self.ctx, self.batch, self.S, self.group_id, self.turn_offsets, self.turn_rewards,
                          self.gamma, self.train_agent, out=self.turn_out)
         seg_group, seg_return = self.turn_out["seg_group"], self.turn_out["seg_return"]
-        if self.pg is None:
+        if not self.sharded:
             otk_group_advantages(self.ctx, seg_group, self.num_groups, returns=seg_return, std_norm=self.std_norm,
                                  unbiased=self.unbiased, skip_ungrouped=True, out=self.adv_out)
             return self.adv_out["adv"]
+        if self.coll == "otk":
+            self._otk_counts()
+            return self._otk_group_advantages(seg_group, seg_return, True)
         from .dist import all_gather_group_returns, all_reduce_n_loss
         all_reduce_n_loss(self.masks["n_loss"], self.pg)
         if self.cfg.reduction != 0:
@@ -230,6 +249,20 @@ class PolicyLossStep:
         otk_group_advantages(self.ctx, self.gid_g, self.G_global, returns=self.ret_g, std_norm=self.std_norm,
                              unbiased=self.unbiased, skip_ungrouped=True, out=self.adv_g)
         return self.adv_g["adv"][self.b0:self.b0 + self.E]
+
+    def _otk_counts(self):   # exchange (1): global token / trajectory counts over the ctx's NCCL communicator
+        otk_batch_allreduce_i64(self.ctx, self.masks["n_loss"])
+        if self.cfg.reduction != 0:
+            otk_batch_allreduce_i64(self.ctx, self.masks["n_active_traj"])
+
+    def _otk_group_advantages(self, gid, ret, skip_ungrouped):   # exchange (2) + step (2) on the whole batch
+        o = otk_batch_group_advantages(self.ctx, gid, ret, self.counts, self.G_global, std_norm=self.std_norm,
+                                       unbiased=self.unbiased, skip_ungrouped=skip_ungrouped,
+                                       out=dict(gid_all=self.gid_g, ret_all=self.ret_g, adv_all=self.adv_g["adv"],
+                                                group_mean=self.adv_g["group_mean"],
+                                                group_std=self.adv_g["group_std"],
+                                                group_size=self.adv_g["group_size"]))
+        return o["adv"]
 
     # -- (3) + (4) --------------------------------------------------------------------------------
     def loss(self, adv: torch.Tensor, micro_batches: Sequence[MicroBatch],
@@ -252,7 +285,9 @@ class PolicyLossStep:
                                         stats=self.stats, accumulate=k > 0, want_logp=False)
             if on_launch:
                 on_launch(k, "end")
-        if self.pg is not None:
+        if self.sharded and self.coll == "otk":
+            otk_batch_allreduce_f64(self.ctx, self.stats)   # exchange (3)
+        elif self.sharded:
             from .dist import all_reduce_stats
             all_reduce_stats(self.stats, self.pg)
         return self.stats

@@ -57,6 +57,18 @@ def test_host_side_validation_without_gpu(lib):
     assert L.otk_ctx_destroy(None) == 0
     assert L.otk_build_masks(None, None, 0, None, None, None, None, None, None, None, None, None) == 1
     assert L.otk_turn_returns(None, None, 0, 0, None, None, None, C.c_double(1.0), None, None, None) == 1
+    # batch sharding over NCCL: argument errors before NCCL is touched
+    assert L.otk_comm_unique_id(None) == 1
+    assert L.otk_comm_init(None, None, 1, 0) == 1
+    assert L.otk_comm_destroy(None) == 1
+    n, r = C.c_int32(), C.c_int32()
+    assert L.otk_comm_size(None, C.byref(n), C.byref(r)) == 1
+    assert L.otk_batch_allreduce_i64(None, None, C.c_int64(1), None) == 1
+    assert L.otk_batch_allreduce_f64(None, None, C.c_int64(1), None) == 1
+    assert L.otk_batch_group_advantages(None, 0, None, None, None, 1, 0, C.c_double(1e-8), None, None, None, None,
+                                        None, None, None) == 1
+    L.otk_status_string.restype = C.c_char_p
+    assert L.otk_status_string(12) == b"OTK_ERR_NCCL" and L.otk_status_string(13) == b"OTK_ERR_NO_COMM"
     h = C.c_void_p()
     st = L.otk_ctx_create(0, C.byref(h))
     import torch
