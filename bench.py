@@ -56,6 +56,9 @@ def parse():
                     help="batch sharding (N > 1): strong = ONE global batch of the config split into contiguous "
                          "trajectory ranges by dist.plan_batch_shards (groups straddle ranks; total work fixed); "
                          "weak = every rank its own batch of the config (rank-local groups)")
+    ap.add_argument("--collectives", default="torch", choices=["torch", "otk"],
+                    help="batch sharding's exchanges: torch.distributed (default) or the library's own NCCL "
+                         "communicator (otk_comm_init + otk_batch_*, the C-ABI path)")
     ap.add_argument("--shard", default="batch", choices=["batch", "vocab", "vocab-fused", "2d", "2d-fused"],
                     help="batch: each rank owns whole trajectories (weak scaling); vocab: each rank owns V/N "
                          "columns of every row (strong scaling, row partials all-gathered); vocab-fused: the "
@@ -257,9 +260,16 @@ def run_otk(args):
     else:
         counts = [W["tb"].num_traj] * nb
         g_groups = cfgw.num_groups * nb
+    coll = "torch"
+    if args.collectives == "otk" and bpg is not None and not vocab_mode:
+        import torch.distributed as dist
+        uid = [otk.otk_comm_unique_id() if dist.get_rank(bpg) == 0 else None]
+        dist.broadcast_object_list(uid, src=dist.get_global_rank(bpg, 0), group=bpg)
+        otk.otk_comm_init(ctx, uid[0], dist.get_world_size(bpg), dist.get_rank(bpg))
+        coll = "otk"
     step = PolicyLossStep(ctx, W["dbatch"], W["gid"], cfgw.num_groups, W["toff"], W["trew"], W["Vl"], cfg,
                           process_group=bpg, global_num_traj=counts if bpg else None,
-                          global_num_groups=g_groups if bpg else None, vocab_shard=W["vshard"])
+                          global_num_groups=g_groups if bpg else None, vocab_shard=W["vshard"], collectives=coll)
     stream = torch.cuda.current_stream()
     nmb = len(W["mbs"])
     # CUDA events around every loss launch of every timed step, on the launching stream
@@ -356,6 +366,8 @@ def run_otk(args):
                              ("weak: every rank its own batch" if not vocab_mode else args.shard),
                    "rows_per_gpu": W["N"], "vocab": W["V"], "vocab_per_gpu": W["Vl"], "micro_batch_rows": W["M"],
                    "micro_batches": nmb, "parallelism": par,
+                   "collectives": {"torch": "torch.distributed (NCCL)", "otk": "otk_comm_* / otk_batch_* (NCCL)"}[coll]
+                   if world > 1 else None,
                    "l2": f"inputs >> L2: {len(W['bufs'])} logits buffers of "
                          f"{W['bufs'][0].numel() * W['bufs'][0].element_size() / 1e9:.1f} GB cycled",
                    "kl_beta": cfgw.kl_beta, "clip": [0.2, 0.2], "kl": "k3"},
