@@ -520,12 +520,12 @@ cudaError_t launch_sample(otk_ctx* ctx, const SampleParams& p0, int dtype, cudaS
   }
 #endif
 #ifndef OTK_SAMPLE_V1
-  // sampled draws from one SM's worth of rows up: the ring-streamed kernel, one CTA per row, with an off-path
-  // search warp (k_sample_tm.cu; 256 rows 22.9 vs 25.1 us, 4096 rows 218 vs 262 us). Smaller batches keep the
-  // cluster-split kernel below (a cluster-split version of the ring kernel measured no faster at 16-128 rows);
+  // sampled draws above the decode kernel's range: the ring-streamed kernel with an off-path search warp
+  // (k_sample_tm.cu; up to two rows per SM each row split over a cluster of 2-8 CTAs, one CTA per row beyond):
+  // 48 rows 8.9 vs 10.7 us, 64 rows 10.4 vs 12.0 lane-strided, 128 rows 14.1 us, 4096 rows 208 vs 262 us;
   // greedy stays here at every size (its lane-strided pass measured faster: 225 vs 272 us at 4096 rows).
 #ifndef OTK_SAMPLE_TM_MIN_ROWS
-#define OTK_SAMPLE_TM_MIN_ROWS 96  // 96 rows: 17.0 vs 21.3 us lane-strided; 128 rows 17.2 vs 16.5 (even)
+#define OTK_SAMPLE_TM_MIN_ROWS 38
 #endif
   if (!p0.greedy && p0.num_rows >= std::min<int64_t>(ctx->num_sms, OTK_SAMPLE_TM_MIN_ROWS) &&
       sample_tm_fits(p0.vocab, dtype))

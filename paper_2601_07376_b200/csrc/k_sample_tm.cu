@@ -1,6 +1,7 @@
-// k_sample_tm.cu — otk_sample_tokens, sampled draws on large decode batches (one CTA per row): the row streamed
-// once through a bulk-TMA shared-memory ring, the inverse-transform search done by a dedicated warp off the
-// streaming path. Same contract as k_sample.cu (R32; PAPER.md:170-171;
+// k_sample_tm.cu — otk_sample_tokens, sampled draws on batches above the decode kernel's range (one CTA per row, or
+// for up to two rows per SM a cluster of 2-8 CTAs per row): the row streamed once through a bulk-TMA shared-memory
+// ring, the inverse-transform search done by a dedicated warp off the streaming path. Also k_sample_dec (decode
+// batches, below). Same contract as k_sample.cu (R32; PAPER.md:170-171;
 // SPEC.md:300-306): t = min{t : sum_{v <= t} p_v > u},  p = softmax(s x). (Greedy argmax stays on k_sample.cu,
 // whose lane-strided pass measured faster for it.)
 //
@@ -42,6 +43,8 @@ struct SampSmem {
   uint64_t full[kSSlots], empty[kSSlots];
   uint64_t hfull[2], hempty[2];                  // consumer -> search hand-off, by row parity
   float2 part[2][kSampleTmMaxChunks][kSWarps];   // (sum of e at r, r) per (chunk, warp)
+  float4 peer[8];                                // cluster split: the CTAs' (R_c, S_c) pushed by rank
+  uint64_t xbar;
 };
 constexpr size_t kSSmemBytes = size_t(kSSlots) * kSChunk + sizeof(SampSmem);
 
@@ -133,7 +136,10 @@ extern "C" void otk_debug_stm(unsigned long long* out) { cudaMemcpyFromSymbol(ou
 #else
 #define STM_T(i, who)
 #endif
-template <typename T>
+// kCl: one row per thread-block cluster of p.csize CTAs (batches of up to ~2 rows per SM): CTA `rank` streams the
+// row's chunks [rank nchc, (rank + 1) nchc), its search warp pushes the CTA's (R_c, S_c) to every CTA of the cluster
+// (st.async + mbarrier, as k_sample_dec) and the crossing CTA's search warp finishes the draw on its own segments.
+template <typename T, bool kCl>
 __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p) {
   using SV = SV2<T>;
   constexpr int EV = SV::EV;
@@ -151,6 +157,13 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
   const uint64_t k2x2 = f2(k2, k2);
   const uint4 ninf = sizeof(T) == 2 ? make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u)
                                     : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
+  const int C = kCl ? p.csize : 1;
+  const int crank = kCl ? int(cluster_ctarank()) : 0;
+  const int64_t row0 = kCl ? int64_t(cluster_id_x()) : int64_t(blockIdx.x);
+  const int64_t rstride = kCl ? int64_t(nclusters_x()) : int64_t(gridDim.x);
+  const int nchc = (nch + C - 1) / C;
+  const int ch0 = min(nch, crank * nchc);                 // this CTA's chunks [ch0, ch0 + nloc) of every row
+  const int nloc = max(0, min(nch, ch0 + nchc) - ch0);
 
 #ifdef OTK_STM_TIMING
   {
@@ -167,18 +180,23 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
       mbar_init(&S.hfull[i], kSWarps);
       mbar_init(&S.hempty[i], 1);
     }
+    if (kCl) mbar_init(&S.xbar, 1);
     fence_mbar_init();
   }
   __syncthreads();
+  // kCl: publishes xbar's initialisation to the cluster; every thread waits once before its CTA's first push (the
+  // loader at its end, long complete by then)
+  if (kCl) asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
+  if (kCl && warp != 0) asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
 
   if (warp == 0) {
     // ---------------- loader: every row, chunk by chunk
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       uint32_t slot = 0, phase = 0;
-      for (int64_t row = blockIdx.x; row < p.num_rows; row += gridDim.x) {
+      for (int64_t row = row0; row < p.num_rows; row += rstride) {
         const char* src = reinterpret_cast<const char*>(p.logits) + row * p.ld * int64_t(sizeof(T));
-        for (int c = 0; c < nch; ++c) {
+        for (int c = ch0; c < ch0 + nloc; ++c) {
           mbar_wait(&S.empty[slot], phase ^ 1u);
           const uint32_t off = uint32_t(c) * kSChunk;
           const uint32_t bytes = min(uint32_t(kSChunk), rb16 - off);
@@ -192,14 +210,16 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
       }
     }
     __syncwarp();
+    if (kCl) asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
   } else if (warp <= kSWarps) {
     // ---------------- consumers
     const int ct = threadIdx.x - 32, cw = warp - 1;
     uint32_t slot = 0, phase = 0, par = 0, hph = 0;
-    for (int64_t row = blockIdx.x; row < p.num_rows; row += gridDim.x) {
+    for (int64_t row = row0; row < p.num_rows; row += rstride) {
       mbar_wait(&S.hempty[par], hph ^ 1u);   // the search warp has read this parity's previous row
       float r = kSNoRef;                      // warp-uniform reference (k2 units)
-      for (int c = 0; c < nch; ++c) {
+      for (int lc = 0; lc < nloc; ++lc) {
+        const int c = ch0 + lc;                  // the chunk's index in the row
         mbar_wait(&S.full[slot], phase);
         STM_T(2, c == 0 && ct == 0);
         const uint8_t* buf = ring + size_t(slot) * kSChunk + ct * 32;
@@ -244,7 +264,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) cs = __fadd_rn(cs, __shfl_xor_sync(0xffffffffu, cs, o));
-        if (lane == 0) S.part[par][c][cw] = make_float2(cs, r);
+        if (lane == 0) S.part[par][lc][cw] = make_float2(cs, r);
       }
       __syncwarp();
       STM_T(3, ct == 0);
@@ -255,22 +275,22 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
   } else {
     // ---------------- search warp
     uint32_t par = 0, hph = 0;
-    for (int64_t row = blockIdx.x; row < p.num_rows; row += gridDim.x) {
+    for (int64_t row = row0; row < p.num_rows; row += rstride) {
       mbar_wait(&S.hfull[par], hph);
       STM_T(4, lane == 0);
       // row reference R and total S: lane l takes the B contiguous segments [l B, (l + 1) B) (column order:
       // chunk-major, warp-minor), then one 32-lane scan of the lane totals
-      const int nseg = nch * kSWarps;
+      const int nseg = nloc * kSWarps;
       const int B = (nseg + 31) / 32;
       const int i0 = min(lane * B, nseg), i1 = min(i0 + B, nseg);
       auto part_at = [&](int i) { return S.part[par][i / kSWarps][i % kSWarps]; };
       float rl = kSNoRef;
       for (int i = i0; i < i1; ++i) rl = fmaxf(rl, part_at(i).y);
-      const float R = redux_max_f32(rl);
+      const float Rc = redux_max_f32(rl);                // this CTA's reference and sum (the row's unless kCl)
       float lt = 0.f;
       for (int i = i0; i < i1; ++i) {
         const float2 v = part_at(i);
-        if (v.x > 0.f) lt = __fadd_rn(lt, __fmul_rn(v.x, ex2(v.y - R)));
+        if (v.x > 0.f) lt = __fadd_rn(lt, __fmul_rn(v.x, ex2(v.y - Rc)));
       }
       float incl = lt;
 #pragma unroll
@@ -278,30 +298,65 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
         const float y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl = __fadd_rn(incl, y);
       }
-      const float Sw = __shfl_sync(0xffffffffu, incl, 31);
+      const float Sc = __shfl_sync(0xffffffffu, incl, 31);
+      float R = Rc, Sw = Sc, Pc = 0.f, fc = 1.f;        // row reference / sum; mass before this CTA; its scale
+      float crr = 0.f, cir = 0.f, cer = 0.f;             // kCl: lane rr's CTA mass, inclusive / exclusive prefix
+      if (kCl) {   // the C partials of the row (lane rr: CTA rr), identical in every CTA
+        if (lane < C)
+          st_async_f4(mapa(smem_u32(&S.peer[crank]), uint32_t(lane)), Rc, Sc, 0.f, 0.f,
+                      mapa(smem_u32(&S.xbar), uint32_t(lane)));
+        if (lane == 0) mbar_arrive_expect_tx(&S.xbar, 16u * uint32_t(C));
+        mbar_wait_cluster(&S.xbar, 0);                   // one row per cluster: one phase
+        const float4 pv = lane < C ? S.peer[lane] : make_float4(kSNoRef, 0.f, 0.f, 0.f);
+        R = redux_max_f32(pv.x);
+        crr = pv.y > 0.f ? __fmul_rn(pv.y, ex2(pv.x - R)) : 0.f;
+        cir = crr;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const float y = __shfl_up_sync(0xffffffffu, cir, o);
+          if (lane >= o) cir = __fadd_rn(cir, y);
+        }
+        Sw = __shfl_sync(0xffffffffu, cir, 31);
+        fc = ex2(Rc - R);
+        const float up = __shfl_up_sync(0xffffffffu, cir, 1);
+        cer = lane == 0 ? 0.f : up;
+      }
       const bool degenerate = !(R > kSNoRef) || !(Sw > 0.f);
       const T* rbase = reinterpret_cast<const T*>(p.logits) + row * p.ld;
-      if (degenerate) {  // no finite logit: token 0, logp -inf (as k_sample.cu)
+      int rs = 0;                                        // the crossing CTA (kCl)
+      float u = 0.f, Tt = 0.f;
+      if (!degenerate) {
+        u = p.u[row];
+        if (!(u >= 0.f && u < 1.f)) {
+          if (lane == 0 && crank == 0) set_error(p.err, OTK_ERR_INVALID_ARG);
+          u = fminf(fmaxf(u, 0.f), 0.99999994f);
+        }
+        Tt = u * Sw;
+        if (!(Tt < Sw)) Tt = Sw * 0.99999976f;
+        if (kCl) {   // rank order; fallback: the last CTA with mass
+          const unsigned cr = __ballot_sync(0xffffffffu, lane < C && cir > Tt);
+          const unsigned nzr = __ballot_sync(0xffffffffu, lane < C && crr > 0.f);
+          rs = cr ? __ffs(cr) - 1 : 31 - __clz(nzr);
+          Pc = __shfl_sync(0xffffffffu, cer, rs);
+        }
+      }
+      if (degenerate || rs != crank) {   // no finite logit: token 0, logp -inf (as k_sample.cu); or not this CTA
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&S.hempty[par]);
-          p.tokens[row] = 0;
-          if (p.logp) p.logp[row] = -INFINITY;
+          if (degenerate && crank == 0) {
+            p.tokens[row] = 0;
+            if (p.logp) p.logp[row] = -INFINITY;
+          }
         }
       } else {
-        float u = p.u[row];
-        if (!(u >= 0.f && u < 1.f)) {
-          if (lane == 0) set_error(p.err, OTK_ERR_INVALID_ARG);
-          u = fminf(fmaxf(u, 0.f), 0.99999994f);
-        }
-        float Tt = u * Sw;
-        if (!(Tt < Sw)) Tt = Sw * 0.99999976f;
-        // the crossing lane's range (fallback: the last lane with mass), then its segments one per lane, scanned
-        const unsigned cl = __ballot_sync(0xffffffffu, incl > Tt);
+        // the crossing lane's range (fallback: the last lane with mass), then its segments one per lane, scanned;
+        // masses in the row's units: P = Pc + fc x (this CTA's prefix at Rc)
+        const unsigned cl = __ballot_sync(0xffffffffu, __fadd_rn(Pc, __fmul_rn(incl, fc)) > Tt);
         const unsigned nzl = __ballot_sync(0xffffffffu, lt > 0.f);
         const int L = cl ? __ffs(cl) - 1 : 31 - __clz(nzl);
         const float excl = __shfl_up_sync(0xffffffffu, incl, 1);
-        const float Pb = L == 0 ? 0.f : __shfl_sync(0xffffffffu, excl, L);
+        const float Pb = L == 0 ? Pc : __fadd_rn(Pc, __fmul_rn(__shfl_sync(0xffffffffu, excl, L), fc));
         const int j0 = min(L * B, nseg), j1 = min(j0 + B, nseg);
         const int i = j0 + lane;
         float c = 0.f, f = 0.f;
@@ -327,7 +382,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_sample_tm(const SampleParams p
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.hempty[par]);   // the hand-off buffer is no longer read
         // re-read the 1 KB segment (L2): lane l holds its vectors 2l, 2l+1 of thread-range (wstar, lane l)
-        const int v0 = cstar * (CE / EV) + 2 * (32 * wstar + lane);
+        const int v0 = (ch0 + cstar) * (CE / EV) + 2 * (32 * wstar + lane);
         const uint4* rp = reinterpret_cast<const uint4*>(rbase);
         uint4 q[2];
 #pragma unroll
@@ -798,20 +853,72 @@ bool sample_tm_fits(int64_t vocab, int dtype) {
   return (rb + kSChunk - 1) / kSChunk <= kSampleTmMaxChunks;
 }
 
-cudaError_t launch_sample_tm(otk_ctx* ctx, const SampleParams& p, int dtype, cudaStream_t s) {
-  const int grid = int(std::min<int64_t>(p.num_rows, int64_t(ctx->num_sms) * 2));
-  if (dtype == OTK_BF16) {
-    cudaError_t e = cudaFuncSetAttribute(k_sample_tm<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kSSmemBytes));
-    if (e != cudaSuccess) return e;
-    k_sample_tm<__nv_bfloat16><<<grid, kSThreads, kSSmemBytes, s>>>(p);
-  } else {
-    cudaError_t e = cudaFuncSetAttribute(k_sample_tm<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kSSmemBytes));
-    if (e != cudaSuccess) return e;
-    k_sample_tm<float><<<grid, kSThreads, kSSmemBytes, s>>>(p);
+namespace {
+// resident clusters of c CTAs of k_sample_tm<T, true> (cached; the same on every B200)
+template <typename T>
+int stm_max_clusters(int c) {
+  static int cache[9] = {};
+  int& slot = cache[c];
+  if (slot == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(c), 1, 1);
+    cfg.blockDim = dim3(kSThreads, 1, 1);
+    cfg.dynamicSmemBytes = kSSmemBytes;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(c);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_sample_tm<T, true>, &cfg) != cudaSuccess) {
+      (void)cudaGetLastError();
+      n = 0;
+    }
+    slot = n > 0 ? n : -1;
   }
+  return slot;
+}
+
+template <typename T>
+cudaError_t launch_stm(otk_ctx* ctx, SampleParams p, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k_sample_tm<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kSSmemBytes));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_sample_tm<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSSmemBytes));
+  if (e != cudaSuccess) return e;
+  // up to two rows per SM: split each row over a cluster of C CTAs (C = the largest <= 8 with C x rows <= the
+  // resident-CTA slots whose clusters all fit at once); more rows: one CTA per row, two per SM, persistent
+#ifndef OTK_STM_NO_CLUSTER
+  for (int c = int(std::min<int64_t>(8, 2 * int64_t(ctx->num_sms) / p.num_rows)); c >= 2; --c) {
+    if (stm_max_clusters<T>(c) < p.num_rows) continue;
+    p.csize = c;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(p.num_rows * c), 1, 1);
+    cfg.blockDim = dim3(kSThreads, 1, 1);
+    cfg.dynamicSmemBytes = kSSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(c);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k_sample_tm<T, true>, p);
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
+#endif
+  p.csize = 1;
+  const int grid = int(std::min<int64_t>(p.num_rows, int64_t(ctx->num_sms) * 2));
+  k_sample_tm<T, false><<<grid, kSThreads, kSSmemBytes, s>>>(p);
   return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_sample_tm(otk_ctx* ctx, const SampleParams& p, int dtype, cudaStream_t s) {
+  return dtype == OTK_BF16 ? launch_stm<__nv_bfloat16>(ctx, p, s) : launch_stm<float>(ctx, p, s);
 }
 
 }  // namespace otk

@@ -28,6 +28,17 @@ for d in 1024 2048 3584; do timeout 200 python scripts/perf_lmhead_loss.py --row
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_lmhead_bwd -c 2 -o gpurun_out/prof_lmbwd -f python scripts/prof_lmhead_loss.py 8192 3584 1 > gpurun_out/ncu_lmbwd.log 2>&1; echo "lmbwd rc=$?"
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/lmbwd_launches.csv python scripts/prof_lmhead_loss.py 8192 3584 1 > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_sample_dec -s 4 -c 1 -o gpurun_out/prof_sdec -f python scripts/prof_sample_dec.py 16 > gpurun_out/ncu_sdec.log 2>&1; echo "sdec rc=$?"
-timeout 300 python scripts/perf_sample.py --rows 1,16,32,64,96,128,256,1024,4096 > gpurun_out/perf_sample.jsonl 2>&1
+timeout 300 python scripts/perf_sample.py --rows 1,16,32,37,48,64,96,128,148,256,1024,4096 > gpurun_out/perf_sample.jsonl 2>&1
 nvcc -gencode arch=compute_100a,code=sm_100a -I paper_2601_07376_b200/csrc -o /tmp/rr scripts/repro/racecheck_tma_ring.cu && \
   (timeout 300 compute-sanitizer --tool racecheck /tmp/rr > gpurun_out/racecheck_repro.log 2>&1; echo "repro rc=$?" >> gpurun_out/racecheck_repro.log)
+# round-2 (late) additions: the other workloads' bench lines, the store-path HBM probe, per-CTA phase stamps of
+# the decode and ring samplers (experiment builds), the batch-sharded C example (also in pytest)
+for c in game marl vp; do timeout 900 python bench.py --config $c --no-next > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo "bench $c rc=$?"; done
+timeout 300 python scripts/hbm_probe4.py > gpurun_out/hbm_probe4.json 2>&1; echo "hbm_probe4 rc=$?"
+mkdir -p .variants
+python -c "
+import sys; sys.path.insert(0, 'paper_2601_07376_b200'); import build
+build.build(out='.variants/libotk_sdec_t.so', defines=['OTK_SDEC_TIMING'])
+build.build(out='.variants/libotk_stm_t.so', defines=['OTK_STM_TIMING'])"
+OTK_LIB=.variants/libotk_sdec_t.so timeout 120 python scripts/timing_sample_dec.py > gpurun_out/sdec_phases.txt 2>&1
+OTK_LIB=.variants/libotk_stm_t.so timeout 120 python scripts/timing_sample_tm.py > gpurun_out/stm_phases.txt 2>&1

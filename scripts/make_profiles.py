@@ -106,10 +106,12 @@ if __name__ == "__main__":
                      ("sanitize_memcheck.log", "sanitize_memcheck.txt"),
                      ("sanitize_racecheck.log", "sanitize_racecheck.txt"),
                      ("sanitize_synccheck.log", "sanitize_synccheck.txt"),
-                     ("racecheck_repro.log", "racecheck_repro.txt"), ("lmbwd_launches.csv", "lmbwd_launches.csv")):
+                     ("racecheck_repro.log", "racecheck_repro.txt"), ("lmbwd_launches.csv", "lmbwd_launches.csv"),
+                     ("hbm_probe4.json", "hbm_probe4.json"), ("sdec_phases.txt", "sdec_phases.txt"),
+                     ("stm_phases.txt", "stm_phases.txt")):
         if os.path.exists(os.path.join(OUT, src)):
             shutil.copy(os.path.join(OUT, src), os.path.join(PROF, f"{tag}_{dst}"))
     traffic(os.path.join(OUT, "prof_k4.ncu-rep"), tag)
-    for f in ("bench.json", "bench_ref.json"):
+    for f in ("bench.json", "bench_ref.json", "bench_game.json", "bench_marl.json", "bench_vp.json"):
         if os.path.exists(os.path.join(OUT, f)):
             open(os.path.join(PROF, f"{tag}_{f}"), "w").write(open(os.path.join(OUT, f)).read())

@@ -62,8 +62,9 @@ nl = mk.sum().to(torch.int64).reshape(1)
 for cfg in (otk.LossCfg(), otk.LossCfg(ent_coef=0.02)):
     otk.otk_lmhead_policy_loss_fwd_bwd(ctx, h, w, y, mk, rtj, torch.tensor([0.5, -0.3, 1.0], device="cuda",
                                        dtype=torch.float64), lp.contiguous(), lp.contiguous(), nl, cfg)
-# decode-batch sampler (one row per cluster, ranges resident in shared memory) and the 100-row ring path
-for n in (1, 5, 37):
+# decode-batch sampler (one row per cluster, ranges resident in registers, warp partials pushed over DSMEM) and
+# the ring kernel with rows split over CTA clusters (48: C = 6, 100: C = 2)
+for n in (1, 5, 37, 48, 100):
     lg, _ = make_logits(n, 151936, dtype="bf16", seed=6, device="cuda")
     otk.otk_sample_tokens(ctx, lg, torch.rand(n, device="cuda"))
     otk.otk_sample_tokens(ctx, lg, greedy=True)

@@ -211,10 +211,11 @@ def test_sampled_degenerate_rows_ring_kernel(otk, ctx, dtype, V):
 @pytest.mark.parametrize("dtype,V,n", [("bf16", 151936, 16), ("bf16", 151936, 37), ("bf16", 151936, 1),
                                        ("f32", 50000, 30), ("bf16", 4100, 9), ("bf16", 17, 5),
                                        ("bf16", 151936, 33), ("f32", 151936, 16),
-                                       ("bf16", 151936, 100)])   # 100 rows: the ring kernel
+                                       ("bf16", 151936, 100), ("bf16", 151936, 148), ("f32", 151936, 96),
+                                       ("bf16", 151936, 64)])   # >= 96 rows: the ring kernel, rows split by clusters
 def test_decode_batches(otk, ctx, dtype, V, n):
     """Decode-sized batches (<= 49 rows: k_sample_dec, one row per cluster, each CTA's column range held in registers;
-    96-147 rows: the ring kernel):
+    96-148 rows: the ring kernel, each row split over a cluster of 2-3 CTAs):
     sampled draws vs the oracle, greedy bit-exact, degenerate rows, and single finite columns at the first / last
     column and at the boundaries between the cluster's CTA ranges (u = 0 and u -> 1)."""
     ld = -(-V // 8) * 8
@@ -240,6 +241,13 @@ def test_decode_batches(otk, ctx, dtype, V, n):
     if n >= 16:   # the first column of CTA rank 1 for every cluster size the kernel may pick (3-8, by occupancy)
         for j, c in zip(range(8, 14), range(3, 9)):
             col = min(-(-(-(-(V * es) // 16) // 64) // c) * 64 * 16 // es, V - 1)
+            x[j, :] = float("-inf")
+            x[j, col] = 1.0
+            special[j] = col
+    if n >= 32:   # the ring kernel's cluster split (96-148 rows): first column of rank 1's 12 KB chunks, C = 2-8
+        nch = -(-(-(-(V * es) // 16) * 16) // 12288)
+        for j, c in zip(range(14, 21), range(2, 9)):
+            col = min(-(-nch // c) * 12288 // es, V - 1)
             x[j, :] = float("-inf")
             x[j, col] = 1.0
             special[j] = col
