@@ -110,6 +110,8 @@ if __name__ == "__main__":
                      ("hbm_probe4.json", "hbm_probe4.json"), ("sdec_phases.txt", "sdec_phases.txt"),
                      ("stm_phases.txt", "stm_phases.txt")):
         if os.path.exists(os.path.join(OUT, src)):
+            if "compute-sanitizer is closed" in open(os.path.join(OUT, src), errors="replace").read():
+                continue   # the pool refused the sanitizer run: keep the last real log
             shutil.copy(os.path.join(OUT, src), os.path.join(PROF, f"{tag}_{dst}"))
     traffic(os.path.join(OUT, "prof_k4.ncu-rep"), tag)
     for f in ("bench.json", "bench_ref.json", "bench_game.json", "bench_marl.json", "bench_vp.json"):
