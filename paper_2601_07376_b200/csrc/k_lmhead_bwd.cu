@@ -60,15 +60,18 @@ constexpr uint32_t kIdescDw = idesc_bf16(256, 256, true, true);   // A MN-major,
 struct LmBwdParams {
   int64_t num_rows, vocab;
   int d;
-  int n_mt, n_nt;        // M tiles (rows for dh, vocab for dW), N tiles of 512 hidden columns
+  int n_mt, n_nt;        // M tiles (rows for dh, vocab for dW), N tiles of 512 hidden columns (of this launch)
+  int nt0;               // first hidden tile of this launch
   int kb_total, kb_per_split, splits;
   const float4* rowc;    // [num_rows] {m, alpha', beta', gy}
   const int32_t* targets;
   int64_t vocab_start;   // global id of local vocab column 0
   float s2;              // logit_scale * log2(e)
   int store_dx;          // dh: units of hidden tile 0 also store the transformed A (= dx tiles) through tm_dx
-  int xform;             // 0: A already holds dx (dW after dh stored it): no transform, the GEMM alone
-  void* out;             // dh: fp32 [splits][num_rows][d] (splits > 1) or bf16 [num_rows][d]; dW: bf16 [vocab][d]
+  int xform;             // 0: A already holds dx (dW, and dh's hidden tiles >= 1, after dh's tile 0 stored it):
+                         //    no transform, the GEMM alone
+  int f32out;            // dh: fp32 split-K partials [split][num_rows][d] (reduced afterwards) instead of bf16
+  void* out;             // dh: fp32 partials (f32out) or bf16 [num_rows][d]; dW: bf16 [vocab][d]
 };
 
 __device__ __forceinline__ void bw_unit(const LmBwdParams& p, int u, int& mt, int& nt, int& kb0, int& kb1, int& sp) {
@@ -76,7 +79,7 @@ __device__ __forceinline__ void bw_unit(const LmBwdParams& p, int u, int& mt, in
   sp = u / per;
   const int r = u - sp * per;
   mt = r / p.n_nt;
-  nt = r - mt * p.n_nt;
+  nt = p.nt0 + (r - mt * p.n_nt);
   kb0 = sp * p.kb_per_split;
   kb1 = min(p.kb_total, kb0 + p.kb_per_split);
 }
@@ -266,7 +269,10 @@ __global__ void __launch_bounds__(kBwThreads, 1)
           const uint32_t a = smem_u32(smem + s * kBwABytes);
           if (!p.xform) {  // A is the operand as loaded: both CTAs' bytes counted on the leader's barrier, no relay
             if (rank == 0) mbar_arrive_expect_tx(&fullA[s], 2 * kBwABytes);
-            tma_load_4d_pair(a, &tm_a, smem_u32(&fullA[s]) & kPeerBitMask, 0, 0, m0 >> 6, kb);
+            if (kDh)  // dx tiles (row block m0/64 .. +1, vocab block kb), K-major rows
+              tma_load_4d_pair(a, &tm_a, smem_u32(&fullA[s]) & kPeerBitMask, 0, 0, kb, m0 >> 6);
+            else      // dx tiles (row block kb, vocab blocks m0/64 .. +1), MN-major
+              tma_load_4d_pair(a, &tm_a, smem_u32(&fullA[s]) & kPeerBitMask, 0, 0, m0 >> 6, kb);
           } else {
             mbar_arrive_expect_tx(&fullA[s], kBwABytes);
             if (kDh)  // x tiles (row block m0/64 .. +1, vocab block kb): [2][64 rows][64 v], K-major rows
@@ -429,7 +435,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
         // for the unit. A quarter-warp covers 2 rows x 4 quarters: chunk sets of opposite parity, no conflict.
         const int r = xt >> 2, qq = xt & 3;
         const RowK rk = cook<kEnt>(raw_consts(p, m0 + r), p.vocab);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1 && p.xform; ++kb) {  // (A as loaded: nothing to transform, no relay)
           {
             BW_T0();
             mbar_wait(&fullA[s], ph);
@@ -505,7 +511,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
       const int64_t M = kDh ? p.num_rows : p.vocab;
       const uint32_t tl = tmem + (uint32_t(q * 32) << 16) + uint32_t(ch * 128);
       const int col0 = nt * kBwNtile + ch * 128;
-      const bool f32out = kDh && p.splits > 1;
+      const bool f32out = kDh && p.f32out;
 #pragma unroll 1
       for (int cc = 0; cc < 4; ++cc) {
         float v[32];
@@ -554,9 +560,12 @@ __global__ void __launch_bounds__(kBwThreads, 1)
   }
 }
 
-// dh = sum over splits of the fp32 partials (fixed order: deterministic), rounded once to bf16
-__global__ void k_lmhead_dh_reduce(const float4* __restrict__ part, int splits, int64_t n4, uint2* __restrict__ dh) {
+// dh = sum over splits of the fp32 partials (fixed order: deterministic), rounded once to bf16; hidden columns
+// [0, 512) (tile 0, its own launch) have splits0 partials, the others splits1
+__global__ void k_lmhead_dh_reduce(const float4* __restrict__ part, int splits0, int splits1, int d, int64_t n4,
+                                   uint2* __restrict__ dh) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+    const int splits = int((i * 4) % d) < kBwNtile ? splits0 : splits1;
     float4 a = part[i];
     for (int s = 1; s < splits; ++s) {
       const float4 b = part[int64_t(s) * n4 + i];
@@ -573,14 +582,14 @@ __global__ void k_lmhead_dh_reduce(const float4* __restrict__ part, int splits, 
 // split-K of dh: (row tiles x hidden tiles) units are few (e.g. 32 x 7 at N = 8192, d = 3584) against 74 CTA
 // pairs; splitting the vocab (K) dimension fills whole waves. Cost model in stages: waves x (stages per unit +
 // an epilogue of ~8 stages), plus the partials' round trip through HBM; at most 16 splits.
-int lmhead_dh_splits(int64_t num_rows, int64_t vocab, int d, int num_sms) {
-  const int64_t units = ((num_rows + kBwMtile - 1) / kBwMtile) * ((d + kBwNtile - 1) / kBwNtile);
+static int dh_splits_for(int64_t num_rows, int64_t vocab, int n_nt, int num_sms) {
+  const int64_t units = ((num_rows + kBwMtile - 1) / kBwMtile) * n_nt;
   const int64_t kb = (vocab + kBwK - 1) / kBwK;
   const int64_t pairs = std::max(1, num_sms / 2);
   int best = 1;
   double best_t = 1e300;
   // a split's fp32 partials cost 8 bytes per dh element (write + read) at ~5 TB/s, a stage ~0.55 us
-  const double part_stages = double(num_rows) * double(d) * 8.0 / 5e12 / 0.55e-6;
+  const double part_stages = double(num_rows) * double(n_nt) * kBwNtile * 8.0 / 5e12 / 0.55e-6;
   for (int s = 1; s <= 16; ++s) {
     const int64_t waves = (units * s + pairs - 1) / pairs;
     const double t = double(waves) * double((kb + s - 1) / s + 8) + (s > 1 ? s * part_stages : 0.0);
@@ -590,6 +599,23 @@ int lmhead_dh_splits(int64_t num_rows, int64_t vocab, int d, int num_sms) {
     }
   }
   return best;
+}
+// dh runs as two launches when d > 512: hidden tile 0 with the transform (storing the dx tiles), then tiles
+// 1 .. n-1 as a plain GEMM over those tiles — each with its own split-K
+static void dh_plan(int64_t num_rows, int64_t vocab, int d, int num_sms, int* s0, int* s1) {
+  const int n_nt = (d + kBwNtile - 1) / kBwNtile;
+#ifdef OTK_BW_ONE_DH  // experiment: one dh launch, the transform in every hidden tile
+  *s0 = *s1 = dh_splits_for(num_rows, vocab, n_nt, num_sms);
+  return;
+#endif
+  *s0 = dh_splits_for(num_rows, vocab, 1, num_sms);
+  *s1 = n_nt > 1 ? dh_splits_for(num_rows, vocab, n_nt - 1, num_sms) : 1;
+}
+// slices of the fp32 dh partial buffer [slices][num_rows][d] (1: no partials, dh written as bf16 directly)
+int lmhead_dh_splits(int64_t num_rows, int64_t vocab, int d, int num_sms) {
+  int s0, s1;
+  dh_plan(num_rows, vocab, d, num_sms, &s0, &s1);
+  return std::max(s0, s1);
 }
 
 static cudaError_t launch_bwd(const otk_ctx* ctx, int mode, bool ent, const CUtensorMap& ta, const CUtensorMap& tb,
@@ -638,21 +664,48 @@ cudaError_t launch_lmhead_bwd(const otk_ctx* ctx, int64_t num_rows, int64_t voca
     if (!make_map_tiles(&ta, logits, rows_pad, cols_pad, 1, 2) || !make_map_2d(&tb, weight, vocab, d, d, 64, kBwK) ||
         !make_map_tiles(&tdx, dx_tiles, rows_pad, cols_pad, 1, 2))
       return cudaErrorInvalidValue;
-    p.store_dx = 1;  // hidden-tile-0 units leave dx behind for the dW GEMM
-    p.xform = 1;
+    int s0, s1;
+    dh_plan(num_rows, vocab, d, ctx->num_sms, &s0, &s1);
     p.n_mt = int((num_rows + kBwMtile - 1) / kBwMtile);
     p.kb_total = int((vocab + kBwK - 1) / kBwK);
-    p.splits = dh_splits;
-    p.kb_per_split = (p.kb_total + dh_splits - 1) / dh_splits;
-    p.out = dh_splits > 1 ? static_cast<void*>(dh_part) : dh;
+    p.f32out = std::max(s0, s1) > 1 ? 1 : 0;
+    p.out = p.f32out ? static_cast<void*>(dh_part) : dh;
+    const int n_nt = p.n_nt;
+#ifdef OTK_BW_ONE_DH
+    const bool one = true;
+#else
+    const bool one = n_nt == 1;
+#endif
+    // (a) hidden tile 0 (every tile when `one`): the transform, and the dx tiles stored for the other GEMMs
+    p.store_dx = 1;
+    p.xform = 1;
+    p.nt0 = 0;
+    p.n_nt = one ? n_nt : 1;
+    p.splits = s0;
+    p.kb_per_split = (p.kb_total + s0 - 1) / s0;
     cudaError_t e = launch_bwd(ctx, 0, ent, ta, tb, tdx, p, s);
     if (e != cudaSuccess) return e;
     ++*launches;
-    if (dh_splits > 1) {
+    // (b) hidden tiles 1 .. n-1: a plain GEMM over the stored dx tiles (A K-major, the same tile layout as x)
+    if (!one) {
+      CUtensorMap tdxa;
+      if (!make_map_tiles(&tdxa, dx_tiles, rows_pad, cols_pad, 1, 2)) return cudaErrorInvalidValue;
+      p.store_dx = 0;
+      p.xform = 0;
+      p.nt0 = 1;
+      p.n_nt = n_nt - 1;
+      p.splits = s1;
+      p.kb_per_split = (p.kb_total + s1 - 1) / s1;
+      e = launch_bwd(ctx, 0, ent, tdxa, tb, tdxa, p, s);
+      if (e != cudaSuccess) return e;
+      ++*launches;
+    }
+    p.n_nt = n_nt;
+    if (p.f32out) {
       const int64_t n4 = num_rows * d / 4;
       int64_t blocks = std::min<int64_t>((n4 + 255) / 256, int64_t(ctx->num_sms) * 8);
-      k_lmhead_dh_reduce<<<int(blocks), 256, 0, s>>>(reinterpret_cast<const float4*>(dh_part), dh_splits, n4,
-                                                       reinterpret_cast<uint2*>(dh));
+      k_lmhead_dh_reduce<<<int(blocks), 256, 0, s>>>(reinterpret_cast<const float4*>(dh_part), s0, one ? s0 : s1, d,
+                                                       n4, reinterpret_cast<uint2*>(dh));
       e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       ++*launches;
@@ -666,7 +719,8 @@ cudaError_t launch_lmhead_bwd(const otk_ctx* ctx, int64_t num_rows, int64_t voca
       return cudaErrorInvalidValue;
     p.store_dx = 0;
     p.xform = 0;
-
+    p.nt0 = 0;
+    p.f32out = 0;
     p.n_mt = int((vocab + kBwMtile - 1) / kBwMtile);
     p.kb_total = int((num_rows + kBwK - 1) / kBwK);
     p.splits = 1;
