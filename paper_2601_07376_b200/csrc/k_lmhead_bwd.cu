@@ -19,9 +19,10 @@
 // it at half the SFU rate; N = 256 would saturate it).
 // After a unit's last stage the transform warps drain TMEM (tcgen05.ld 32x32b, one row per thread, 128 columns
 // per warp) into the output — bf16, or fp32 split-K partials for dh — and release the accumulators.
-// dh runs first; its units of hidden tile 0 also TMA-store each transformed A stage, so dx exists once in HBM as
-// 64 x 64 tiles (2 bytes per logit written, read once) and dW = dxᵀ h runs as a plain GEMM: dx is formed once
-// per element for dh's first hidden tile instead of once per hidden tile of each GEMM (2 x d/512 times).
+// dh's hidden tile 0 runs first (its own launch); its units also TMA-store each transformed A stage, so dx exists
+// once in HBM as 64 x 64 tiles (2 bytes per logit written). dh's hidden tiles 1 .. d/512 - 1 (a second launch) and
+// dW = dxᵀ h then run as plain GEMMs over those tiles: dx is formed once per element instead of once per hidden tile
+// of each GEMM (2 x d/512 times).
 #include <cuda_bf16.h>
 
 #include <algorithm>
