@@ -512,7 +512,7 @@ static cudaError_t launch_lane_strided(otk_ctx* ctx, SampleParams p, cudaStream_
 
 cudaError_t launch_sample(otk_ctx* ctx, const SampleParams& p0, int dtype, cudaStream_t s) {
 #ifndef OTK_SAMPLE_NO_DEC
-  // decode batches (<= num_sms / 4 rows, the row range of each CTA held in shared memory): k_sample_dec
+  // decode batches (<= num_sms / 3 rows where the clusters fit; each CTA's range held in registers): k_sample_dec
   {
     int csize = 0, nseg_c = 0;
     if (sample_dec_shape(p0.num_rows, p0.vocab, dtype, ctx->num_sms, &csize, &nseg_c))
