@@ -1029,8 +1029,8 @@ __device__ __forceinline__ void pass1_chunk(Smem& S, const uint8_t* ring, uint32
 // P >= 8).
 template <int kLag>
 struct PipeCfg {
-  static constexpr int kSlotCols = kLag == 1 ? 64 : 42;          // TMEM columns per row slot
-  static constexpr int kMaxCh = kLag == 1 ? kPipeChunks : 4;      // chunks per row segment
+  static constexpr int kSlotCols = kLag == 1 ? 64 : kTmemWindow / 4;   // TMEM columns per row slot
+  static constexpr int kMaxCh = kLag == 1 ? kPipeChunks : kLag3Chunks;  // chunks per row segment
   static constexpr int kColM = 8 * kMaxCh;                        // [0, kColM) e, then one m_c column per chunk
   static_assert((kLag + 1) * kSlotCols <= kTmemWindow && kColM + kMaxCh <= kSlotCols, "TMEM slots");
   static_assert(kLag == 1 || kLag == 3, "lag 1 or 3 (slot index = q & kLag)");

@@ -687,7 +687,7 @@ static otk_status vpf_params(otk_ctx* ctx, int64_t num_rows, int64_t vocab_local
   // and two rows fit its tensor memory
   {
     const int64_t seg_bytes = int64_t(seg) * int64_t(dtype_size(dtype));
-    p.pipe = csize != 1 ? 0 : seg_bytes <= 4 * int64_t(otk::kChunkBytes) ? 3
+    p.pipe = csize != 1 ? 0 : seg_bytes <= otk::kLag3Chunks * int64_t(otk::kChunkBytes) ? 3
                                : seg_bytes <= int64_t(otk::kPipeChunks) * otk::kChunkBytes ? 1 : 0;
   }
 #ifdef OTK_VPF_LAG1  // experiment builds only: the lag-1 pipeline for every segment that fits it

@@ -41,14 +41,26 @@ enum Ticket { kTicketMasks = 0, kTicketRows = 1 };
 // Warp 0 loads (bulk TMA), warps 1..12 compute (3 per SM sub-partition / TMEM lane quadrant; <= 128
 // registers per thread), warp 13 zero-fills masked rows (bulk async stores). A 12 KB chunk is exactly
 // 2 x 16-byte vectors per consumer thread.
+#ifndef OTK_K4_CW16
 constexpr int kChunkBytes = 12288;       // one bulk-TMA transfer / ring slot
 constexpr int kSlots = 18;               // ring depth: 216 KB of shared memory per CTA
 constexpr int kSlotsFwd = 8;             // FWD / PARTIAL: 96 KB ring, so two CTAs share an SM (twice the warps)
 constexpr int kConsumerWarps = 12;       // 384 compute threads
-constexpr int kThreads = 32 * (2 + kConsumerWarps);  // + loader warp 0 + zero-fill warp 13
 constexpr int kMaxChunks = 18;           // a CTA's row segment (<= 18 chunks, 216 KB) is kept in TMEM (162 columns)
 constexpr int kTmemWindow = 168;         // TMEM columns per consumer warp (3 windows per lane quadrant: 504 of 512)
 constexpr int kPipeChunks = 7;           // pipelined K4-VPF: <= 7 chunks (84 KB) per CTA, two rows per TMEM window
+constexpr int kLag3Chunks = 4;           // pipelined K4-VPF, lag 3: <= 4 chunks, four rows per TMEM window
+#else  // experiment: 16 consumer warps (4 per TMEM lane quadrant), 16 KB chunks
+constexpr int kChunkBytes = 16384;
+constexpr int kSlots = 13;               // 208 KB
+constexpr int kSlotsFwd = 6;             // 96 KB
+constexpr int kConsumerWarps = 16;
+constexpr int kMaxChunks = 14;           // 224 KB segments; 8 x 14 + 14 = 126 of a 128-column window
+constexpr int kTmemWindow = 128;
+constexpr int kPipeChunks = 7;           // 2 x 64-column slots
+constexpr int kLag3Chunks = 3;           // 4 x 32-column slots
+#endif
+constexpr int kThreads = 32 * (2 + kConsumerWarps);  // + loader warp 0 + zero-fill warp (last)
 
 enum RowMode : int {
   kModeFwd = 0,       // (3): logp / entropy / lse
