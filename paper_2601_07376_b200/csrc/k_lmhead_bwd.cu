@@ -611,6 +611,9 @@ static void dh_plan(int64_t num_rows, int64_t vocab, int d, int num_sms, int* s0
 #endif
   *s0 = dh_splits_for(num_rows, vocab, 1, num_sms);
   *s1 = n_nt > 1 ? dh_splits_for(num_rows, vocab, n_nt - 1, num_sms) : 1;
+#ifdef OTK_BW_S1  // experiment: the plain dh launch's split count
+  if (n_nt > 1) *s1 = OTK_BW_S1;
+#endif
 }
 // slices of the fp32 dh partial buffer [slices][num_rows][d] (1: no partials, dh written as bf16 directly)
 int lmhead_dh_splits(int64_t num_rows, int64_t vocab, int d, int num_sms) {
