@@ -257,6 +257,12 @@ __device__ __forceinline__ void stg256(void* p, uint4 a, uint4 b) {
                "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
                : "memory");
 }
+// 256-bit store with an L2 eviction-policy hint (createpolicy), e.g. evict_first for data not re-read soon
+__device__ __forceinline__ void stg256_hint(void* p, uint4 a, uint4 b, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p), "r"(a.x),
+               "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void stg_cs_v4(void* p, uint4 v) {
   asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
