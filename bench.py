@@ -556,8 +556,15 @@ def e2e(args, W, world, step, cfg):
     otk, ctx = W["otk"], W["ctx"]
     mbs = W["mbs"]
     N = W["N"]
-    host_bufs = [b.cpu().pin_memory() for b in W["bufs"]]
-    dl_host = torch.empty(W["bufs"][0].shape, dtype=W["bufs"][0].dtype).pin_memory()   # one micro-batch
+    # pinned host buffers allocated directly (no pageable staging copy); with several ranks on one node, one host
+    # logits buffer per rank (each rank's pinned footprint: 2 micro-batches = 40 GB at the math config)
+    nbh = len(W["bufs"]) if world == 1 else 1
+    host_bufs = []
+    for b in W["bufs"][:nbh]:
+        hb = torch.empty(b.shape, dtype=b.dtype, pin_memory=True)
+        hb.copy_(b)
+        host_bufs.append(hb)
+    dl_host = torch.empty(W["bufs"][0].shape, dtype=W["bufs"][0].dtype, pin_memory=True)   # one micro-batch
     adv = step.masks_and_advantages()
     torch.cuda.synchronize()
     n_loss = int(step.masks["n_loss"].item())
