@@ -113,3 +113,60 @@ def test_batch_sharded_step_over_the_library_comm(tmp_path, P, credit):
         assert x["stats"]["n_tokens"] == ref["n_tokens"]    # exchange 3
         for f in ("loss", "kl_sum", "entropy_sum", "n_clipped"):
             assert abs(x["stats"][f] - ref[f]) <= 1e-12 * max(1.0, abs(ref[f])), (f, x["stats"][f], ref[f])
+
+
+SCRIPT_EMPTY = r'''
+import json, sys, threading
+sys.path.insert(0, ROOT)
+import numpy as np, torch
+import paper_2601_07376_b200 as otk
+torch.cuda.set_device(0)
+gid = np.array([0, 1, 0, 2, 1], dtype=np.int32)
+ret = np.array([1.0, 0.0, -1.0, 2.0, 0.5])
+counts = [3, 0, 2]                       # rank 1 holds no trajectory
+ctx0 = otk.Context(0)
+ref = otk.otk_group_advantages(ctx0, torch.from_numpy(gid).cuda(), 3, returns=torch.from_numpy(ret).cuda())
+ref = {k: ref[k].cpu().numpy().tolist() for k in ("adv", "group_mean", "group_std", "group_size")}
+uid = otk.otk_comm_unique_id()
+res = [None] * 3
+def worker(r):
+    try:
+        torch.cuda.set_device(0)
+        with torch.cuda.stream(torch.cuda.Stream()):
+            ctx = otk.Context(0)
+            otk.otk_comm_init(ctx, uid, 3, r)
+            b0 = sum(counts[:r])
+            g = torch.from_numpy(gid[b0:b0 + counts[r]].copy()).cuda()
+            x = torch.from_numpy(ret[b0:b0 + counts[r]].copy()).cuda()
+            o = otk.otk_batch_group_advantages(ctx, g, x, counts, 3)
+            torch.cuda.current_stream().synchronize()
+            ctx.check()
+            res[r] = {k: o[k].cpu().numpy().tolist() for k in ("adv_all", "adv", "group_mean", "group_std", "group_size")}
+            otk.otk_comm_destroy(ctx)
+    except Exception as e:
+        res[r] = dict(error=repr(e))
+th = [threading.Thread(target=worker, args=(r,)) for r in range(3)]
+for t in th: t.start()
+for t in th: t.join(120)
+print(json.dumps(dict(ref=ref, ranks=res)))
+'''
+
+
+def test_group_advantages_with_an_empty_rank(tmp_path):
+    """otk_batch_group_advantages at 3 ranks with counts [3, 0, 2] (a rank without trajectories: its broadcasts are
+    skipped, its slice is empty): every rank gets the single-GPU statistics of the whole batch, bit for bit."""
+    so = _fake(tmp_path)
+    script = tmp_path / "run_empty.py"
+    script.write_text(SCRIPT_EMPTY.replace("ROOT", repr(ROOT), 1))
+    env = dict(os.environ, OTK_NCCL_LIB=so, PYTHONPATH=ROOT)
+    r = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    ref, ranks = out["ref"], out["ranks"]
+    b0 = [0, 3, 3]
+    for k, x in enumerate(ranks):
+        assert x is not None and "error" not in x, x
+        assert x["adv_all"] == ref["adv"]
+        assert x["adv"] == ref["adv"][b0[k]:b0[k] + [3, 0, 2][k]]
+        for f in ("group_mean", "group_std", "group_size"):
+            assert x[f] == ref[f], f
