@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-chunk", type=int, default=4096, help="rows per host-entry-point chunk (copy / compute overlap)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-parity", action="store_true", help="skip the parity block (SURVEY.md §8(d)(v))")
     ap.add_argument("--no-next", action="store_true",
@@ -583,7 +584,7 @@ def e2e(args, W, world, step, cfg):
             n = mb.r1 - mb.r0
             s = otk.otk_policy_loss_fwd_bwd_host(ctx, host_bufs[i % nb][:n], tg, lm_h[mb.r0:mb.r1],
                                                  rt_h[mb.r0:mb.r1], adv_h, old, ref, n_loss, hcfg,
-                                                 dlogits=dl_host[:n], rows_per_chunk=4096)
+                                                 dlogits=dl_host[:n], rows_per_chunk=args.e2e_chunk)
             tot += s["loss"]
         return tot
 
